@@ -1,0 +1,110 @@
+/* dbk.h — thin internal host→CUDA C-ABI of the dynbatch B200 library.
+ *
+ * Raw device pointers, sizes and a cudaStream_t (passed as void*); every
+ * launcher returns 0 or a cudaError_t value and never synchronizes. Device
+ * scalars (d_max, group counts, error flags) stay in device memory so one
+ * forward needs a single tiny device→host read (the step count).
+ *
+ * Node numbering: "global" node g = prog_off[e] + local id (CSR order =
+ * (example, node) order, which is the reference's member order).
+ */
+#ifndef DYNBATCH_DBK_H
+#define DYNBATCH_DBK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- scheduler
+ * Replaces max_root_distance_labels + schedule_improved/make_step
+ * (src/program.cpp:239-272, src/schedule.cpp:66-79,135-164). */
+
+/* labels[g] = longest root→g distance (Kahn per program, one thread per
+ * program); dev_scalars[0] = d_max (atomicMax), dev_scalars[1] |= 1 on a
+ * cycle / unreachable node. scratch: 2·N int32. child*: global ids or -1. */
+int dbk_sched_labels(int64_t b, int64_t N, const int32_t* prog_off, const int32_t* child_off,
+                     const int32_t* child_list, const int32_t* root_g, int32_t* labels,
+                     int32_t* scratch, int32_t* dev_scalars, void* stream);
+
+/* Stable counting sort of all N nodes by key = (d_max - label)·p + fid
+ * over CSR order; writes member_g[N] (sorted global ids), and the group
+ * tables: group_fid[G], group_begin[G+1], step_group_begin[S+1] with
+ * dev_scalars[2] = G. seg_hist must hold max_keys · n_segments ints with
+ * max_keys ≥ (d_max+1)·p; n_segments = ceil(N / 256). */
+int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, const int32_t* fid,
+                          const int32_t* labels, int32_t* dev_scalars, int32_t* seg_hist,
+                          int32_t* member_g, int32_t* group_fid, int32_t* group_begin,
+                          int32_t* step_group_begin, void* stream);
+
+/* Generic stable counting sort by an explicit key in [0, n_keys): order[]
+ * receives item indices sorted by key, stable in index order; offsets[n_keys+1]
+ * the bucket starts. Used for the MoE expert dispatch (group_by_function). */
+int dbk_stable_bucket_sort(int64_t n_items, int32_t n_keys, const int32_t* keys,
+                           int32_t* seg_hist, int32_t* order, int32_t* offsets, void* stream);
+
+/* ------------------------------------------------------ dense (Tier A) step
+ * One step of execute() (src/executor.cpp:117-166) with apply_module
+ * (src/modules.cpp:52-108): for every expensive member of step s,
+ * out = relu(bias + Σ_k Σ_i x_k[i]·W[(kW+i)W + j]) in fp64 with the
+ * reference's ascending fused multiply-add order. Leaves alias inputs. */
+int dbk_dense_step(int32_t step, int32_t width, const int32_t* step_group_begin,
+                   const int32_t* group_fid, const int32_t* group_begin, const int32_t* member_g,
+                   const int32_t* arity_of, const int32_t* child_off, const int32_t* child_list,
+                   const int32_t* example, const double* inputs, double* values,
+                   int32_t* present, const double* const* weights,
+                   const double* const* biases, int32_t* err, int32_t max_arity,
+                   int32_t blocks, void* stream);
+
+/* root rows → out[b × width] (fp64). */
+int dbk_dense_gather_roots(int64_t b, int32_t width, const int32_t* root_g,
+                           const int32_t* present, const double* values, double* out,
+                           int32_t* err, void* stream);
+
+/* ------------------------------------------------------- resblock (Tier B)
+ * Maps are C=128 × 14 × 14. Node values / inputs are fp32 "plane" maps
+ * [16 planes][196 px][8 ch]; per-step staging is bf16 planes over a packed,
+ * zero-padded 15×15 position grid. */
+int dbk_rb_plan(int32_t n_steps, int32_t p, const int32_t* step_group_begin,
+                const int32_t* group_key, const int32_t* group_begin, int32_t* seg_start,
+                int32_t* tiles, int32_t* step_tile_begin, int32_t* bin_tiles,
+                int32_t* step_bintile_begin, int32_t* step_positions, int32_t tile_m,
+                void* stream);
+int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream);
+int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int32_t* fid,
+                          const int32_t* example, const float* inputs, const float* values,
+                          float* chw, void* stream);
+int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_key,
+                  const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
+                  int32_t p, const int32_t* fid, const int32_t* child0g, const int32_t* child1g,
+                  const int32_t* example, const float* inputs, const float* values,
+                  void* stage_x, void* stage_cat, int64_t stage_stride, void* stream);
+/* conv kernels (tcgen05): kind 0 = conv1x1 over [x;y] → z (fp32 + bf16),
+ * 1 = conv3x3 #1 → mid (bf16), 2 = conv3x3 #2 + residual → node values. */
+int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
+                const int32_t* tiles, const int32_t* group_key, const int32_t* group_begin,
+                const int32_t* seg_start, const int32_t* member_g, int32_t p,
+                const int32_t* fid, const int32_t* child0g, const int32_t* example,
+                const void* stage_in, void* stage_out, float* zbuf, const float* inputs,
+                float* values, const void* const* wpack, const float* const* bias,
+                int64_t stage_stride, int32_t num_sms, void* stream);
+
+/* --------------------------------------------------------------------- MoE */
+/* top_k_gate (src/moe.cpp:36-69), one warp per token, fp64. */
+int dbk_moe_topk(int64_t T, int32_t n, int32_t k, const double* scores, int32_t* ids,
+                 double* weights, int32_t* err, void* stream);
+/* fp64 expert apply + staging (src/moe.cpp:98-145, 244-251), reference order. */
+int dbk_moe_expert_fp64(int64_t T, int32_t n, int32_t k, int32_t d, int32_t h,
+                        const int32_t* order, const int32_t* offsets, const double* x,
+                        const double* const* w1, const double* const* w2, double* hidden,
+                        double* staged, int32_t* tile_scratch /* n+1 */, void* stream);
+/* combine (src/moe.cpp:254-264): out[t] = Σ_slot w·y in slot order. */
+int dbk_moe_combine_fp64(int64_t T, int32_t k, int32_t d, const double* weights,
+                         const double* staged, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DYNBATCH_DBK_H */

@@ -1,0 +1,123 @@
+/* dynbatch_device.h — device extensions of the drop-in C ABI.
+ *
+ * Added beside (never instead of) the reference's 27 entry points, as
+ * SURVEY.md §8(b) recommends. Sessions keep a batch, its module weights and
+ * all scratch resident in HBM so that the forward pass — device scheduler
+ * (labels → stable (level, function) bucket sort → group/tile tables) plus
+ * the per-step gather / module / scatter kernels — can be timed alone, with
+ * host↔device traffic accounted separately (…_forward_host does both).
+ *
+ * Module kinds:
+ *   DB_MODULE_DENSE    — the reference module body (src/modules.cpp:52-108):
+ *                        relu(W·concat(operands) + b), fp64, same fused
+ *                        multiply-add order ⇒ bit-identical to the reference.
+ *   DB_MODULE_RESBLOCK — the north-star IEP residual block on C×H×W maps
+ *                        (C = 128, 14×14): unary y = relu(x + conv3(relu(conv3(x)))),
+ *                        binary z = relu(conv1x1([x;y])) then the unary block;
+ *                        tcgen05/TMEM implicit-GEMM kernels, bf16 operands,
+ *                        fp32 accumulation and fp32 node values.
+ * MoE precisions:
+ *   DB_MOE_FP64 — reference arithmetic order (src/moe.cpp:98-145, 254-264).
+ *   DB_MOE_BF16 — tcgen05 grouped GEMMs, bf16 operands, fp32 accumulation.
+ */
+#ifndef DYNBATCH_DYNBATCH_DEVICE_H
+#define DYNBATCH_DYNBATCH_DEVICE_H
+
+#include "dynbatch/dynbatch.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { DB_MODULE_DENSE = 0, DB_MODULE_RESBLOCK = 1 } db_module_kind;
+typedef enum { DB_MOE_FP64 = 0, DB_MOE_BF16 = 1 } db_moe_precision;
+
+typedef struct {
+  int32_t module_kind; /* db_module_kind */
+  int32_t channels;    /* RESBLOCK: C (must be 128) */
+  int32_t height;      /* RESBLOCK: H (must be 14)  */
+  int32_t width_px;    /* RESBLOCK: W (must be 14)  */
+} db_module_opts;
+
+/* Session statistics (db_iep_session_stats / db_moe_session_stats). */
+typedef struct {
+  int64_t steps;
+  int64_t groups;
+  int64_t expensive_calls;
+  int64_t peak_group_rows;
+  int64_t members;
+  int64_t kernel_launches; /* kernels enqueued by the last forward */
+  int64_t h2d_bytes;       /* per …_forward_host call */
+  int64_t d2h_bytes;
+  double algorithmic_flops; /* module FLOPs of one forward (2·MAC) */
+  double algorithmic_bytes; /* minimum HBM bytes of one forward */
+} db_session_stats_t;
+
+DYNBATCH_API int32_t db_device_count(void);
+/* Binds the calling thread to `device` and checks it is sm_100. */
+DYNBATCH_API db_status db_device_open(int32_t device);
+
+/* ---- IEP sessions ---- */
+typedef struct db_iep_session db_iep_session;
+
+/* Uploads programs [first, last) of `batch` (the whole batch when
+ * last <= first), their inputs and the module set ModuleSet(vocab, seed). */
+DYNBATCH_API db_status db_iep_session_create(const db_batch* batch, int64_t first, int64_t last,
+                                             uint64_t module_seed, const db_module_opts* opts,
+                                             db_iep_session** out);
+/* Executes a host-built schedule (any strategy) instead of the device
+ * scheduler; NULL restores the device improved scheduler. */
+DYNBATCH_API db_status db_iep_session_set_schedule(db_iep_session* s, const db_schedule* schedule);
+/* Enqueues one forward on the session stream (schedule + execute). */
+DYNBATCH_API db_status db_iep_session_forward(db_iep_session* s);
+/* End-to-end: pinned-host fp32 inputs (rows × width, reference row layout,
+ * CHW for RESBLOCK) → H2D → forward → D2H of the root outputs (fp32). */
+DYNBATCH_API db_status db_iep_session_forward_host(db_iep_session* s, const float* inputs,
+                                                   float* outputs);
+DYNBATCH_API db_status db_iep_session_synchronize(db_iep_session* s);
+DYNBATCH_API void* db_iep_session_stream(db_iep_session* s);
+DYNBATCH_API db_status db_iep_session_stats(db_iep_session* s, db_session_stats_t* out);
+/* Copies the device schedule of the last forward into a host handle. */
+DYNBATCH_API db_status db_iep_session_schedule(db_iep_session* s, db_schedule** out);
+/* Root outputs (as double, reference row layout) + integer trace. */
+DYNBATCH_API db_status db_iep_session_run(db_iep_session* s, db_run** out);
+/* Device level labels of the last forward (total_nodes int32, CSR order). */
+DYNBATCH_API db_status db_iep_session_labels(db_iep_session* s, int32_t* labels, int64_t n);
+DYNBATCH_API void db_iep_session_free(db_iep_session* s);
+
+/* db_execute with a module kind; schedule NULL = device improved scheduler. */
+DYNBATCH_API db_status db_execute_device(const db_batch* batch, const db_schedule* schedule,
+                                         uint64_t module_seed, const db_module_opts* opts,
+                                         db_run** out);
+
+/* ---- MoE sessions ---- */
+typedef struct db_moe_session db_moe_session;
+
+/* Generates inputs/scores (gen_moe_inputs) and experts (ExpertSet with
+ * mix_seed(seed, 0xe4be27)) exactly as db_moe_run does and uploads them.
+ * Tokens [first, last) are kept (all when last <= first). */
+DYNBATCH_API db_status db_moe_session_create(const db_moe_opts* opts, int32_t precision,
+                                             int64_t first, int64_t last, db_moe_session** out);
+DYNBATCH_API db_status db_moe_session_forward(db_moe_session* s);
+/* End-to-end: host fp32 inputs [T×d] and fp64 scores [T×n] → outputs fp32. */
+DYNBATCH_API db_status db_moe_session_forward_host(db_moe_session* s, const float* inputs,
+                                                   const double* scores, float* outputs);
+DYNBATCH_API db_status db_moe_session_synchronize(db_moe_session* s);
+DYNBATCH_API void* db_moe_session_stream(db_moe_session* s);
+DYNBATCH_API db_status db_moe_session_stats(db_moe_session* s, db_session_stats_t* out);
+/* Routing of the last forward: ids[T×k], weights[T×k], expert_offsets[n+1],
+ * sorted items[T×k] (token·k + slot in per-expert (token, slot) order). */
+DYNBATCH_API db_status db_moe_session_routing(db_moe_session* s, int32_t* ids, double* weights,
+                                              int32_t* expert_offsets, int32_t* items);
+DYNBATCH_API db_status db_moe_session_run(db_moe_session* s, db_run** out);
+DYNBATCH_API void db_moe_session_free(db_moe_session* s);
+
+/* db_moe_run with a precision (batched only). */
+DYNBATCH_API db_status db_moe_run_device(const db_moe_opts* opts, int32_t precision,
+                                         db_run** out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DYNBATCH_DYNBATCH_DEVICE_H */

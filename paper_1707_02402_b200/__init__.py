@@ -1,0 +1,419 @@
+"""dynbatch-b200 — Python host mirror of the drop-in C ABI.
+
+The product is ``libdynbatch.so`` (built in-tree from ``csrc/``): the
+reference's 27 ``db_*`` entry points (include/dynbatch/dynbatch.h) plus device
+sessions (include/dynbatch/dynbatch_device.h). This module only binds them
+with ctypes, mirroring the reference's C API names, argument meaning and
+error behaviour (every failing call raises :class:`DynbatchError` carrying
+the ``db_status`` and ``db_last_error()`` text). There is no Python or CPU
+compute path: if the shared library is missing this import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdynbatch.so")
+
+DB_OK = 0
+STATUS = {0: "DB_OK", 1: "DB_ERR_INVALID_ARG", 2: "DB_ERR_UNKNOWN_FUNCTION",
+          3: "DB_ERR_UNDERFULL_SEQUENCE", 4: "DB_ERR_OVERFULL_SEQUENCE",
+          5: "DB_ERR_INVALID_PROGRAM", 6: "DB_ERR_DEPENDENCY_VIOLATION",
+          7: "DB_ERR_MISSING_OPERAND", 8: "DB_ERR_SHAPE_MISMATCH", 9: "DB_ERR_NON_FINITE",
+          10: "DB_ERR_PARSE", 11: "DB_ERR_VERIFICATION_FAILED", 12: "DB_ERR_INTERNAL"}
+STRATEGY = {"naive": 0, "standard": 1, "improved": 2, "online": 3}
+WORKLOAD = {"balanced": 0, "balanced-tree": 0, "chain": 1, "chain-heavy": 1, "dag": 2,
+            "random-dag": 2}
+MODULE_DENSE, MODULE_RESBLOCK = 0, 1
+MOE_FP64, MOE_BF16 = 0, 1
+
+
+class DynbatchError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+class WorkloadOpts(C.Structure):
+    _fields_ = [("kind", C.c_int), ("batch", C.c_int64), ("vocab", C.c_int32),
+                ("width", C.c_int32), ("depth", C.c_int32), ("length", C.c_int32),
+                ("branch_prob", C.c_double), ("seed", C.c_uint64)]
+
+
+class BatchStats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("batch", "vocab", "width", "s_max", "d_max",
+                                         "total_nodes", "expensive_nodes")]
+
+
+class MoeOpts(C.Structure):
+    _fields_ = [("experts", C.c_int64), ("active_per_example", C.c_int64), ("batch", C.c_int64),
+                ("data_dim", C.c_int64), ("hidden", C.c_int64), ("seed", C.c_uint64)]
+
+
+class MemoryModel(C.Structure):
+    _fields_ = [("param_count", C.c_int64), ("activation_count", C.c_double),
+                ("memory_ratio", C.c_double)]
+
+
+class VerifyOpts(C.Structure):
+    _fields_ = [("seeds", C.c_int32), ("batch", C.c_int64), ("vocab", C.c_int32),
+                ("length", C.c_int32), ("width", C.c_int32), ("seed", C.c_uint64),
+                ("parallel", C.c_int32)]
+
+
+class ModuleOpts(C.Structure):
+    _fields_ = [("module_kind", C.c_int32), ("channels", C.c_int32), ("height", C.c_int32),
+                ("width_px", C.c_int32)]
+
+
+class SessionStats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("steps", "groups", "expensive_calls", "peak_group_rows",
+                                         "members", "kernel_launches", "h2d_bytes", "d2h_bytes")] + \
+               [("algorithmic_flops", C.c_double), ("algorithmic_bytes", C.c_double)]
+
+
+LOG_FN = C.CFUNCTYPE(None, C.c_char_p, C.c_void_p)
+VP = C.c_void_p
+PVP = C.POINTER(C.c_void_p)
+
+# name -> (restype, argtypes); the 27 reference entry points first.
+SIGNATURES = {
+    "db_version": (C.c_char_p, []),
+    "db_last_error": (C.c_char_p, []),
+    "db_string_free": (None, [VP]),
+    "db_batch_generate": (C.c_int32, [C.POINTER(WorkloadOpts), PVP]),
+    "db_batch_load_json": (C.c_int32, [C.c_char_p, C.c_int32, C.c_uint64, PVP]),
+    "db_batch_to_json": (C.c_int32, [VP, PVP]),
+    "db_batch_stats": (C.c_int32, [VP, C.POINTER(BatchStats)]),
+    "db_batch_free": (None, [VP]),
+    "db_schedule_build": (C.c_int32, [VP, C.c_int, PVP]),
+    "db_schedule_verify": (C.c_int32, [VP, VP]),
+    "db_schedule_step_count": (C.c_int64, [VP]),
+    "db_schedule_expensive_calls": (C.c_int32, [VP, VP, C.POINTER(C.c_int64)]),
+    "db_schedule_to_json": (C.c_int32, [VP, PVP]),
+    "db_schedule_inject_fault": (C.c_int32, [VP, C.c_char_p]),
+    "db_schedule_free": (None, [VP]),
+    "db_execute": (C.c_int32, [VP, VP, C.c_uint64, PVP]),
+    "db_run_outputs": (C.c_int32, [VP, C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int64)]),
+    "db_run_expensive_calls": (C.c_int64, [VP]),
+    "db_run_peak_group_rows": (C.c_int64, [VP]),
+    "db_run_module_seconds": (C.c_double, [VP]),
+    "db_run_stacking_seconds": (C.c_double, [VP]),
+    "db_run_total_seconds": (C.c_double, [VP]),
+    "db_run_trace_json": (C.c_int32, [VP, PVP]),
+    "db_run_free": (None, [VP]),
+    "db_moe_run": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, PVP]),
+    "db_moe_memory_model": (C.c_int32, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                                        C.POINTER(MemoryModel)]),
+    "db_verify_run": (C.c_int32, [C.POINTER(VerifyOpts), LOG_FN, VP]),
+    # device extensions (dynbatch_device.h)
+    "db_device_count": (C.c_int32, []),
+    "db_device_open": (C.c_int32, [C.c_int32]),
+    "db_iep_session_create": (C.c_int32, [VP, C.c_int64, C.c_int64, C.c_uint64,
+                                          C.POINTER(ModuleOpts), PVP]),
+    "db_iep_session_set_schedule": (C.c_int32, [VP, VP]),
+    "db_iep_session_forward": (C.c_int32, [VP]),
+    "db_iep_session_forward_host": (C.c_int32, [VP, VP, VP]),
+    "db_iep_session_synchronize": (C.c_int32, [VP]),
+    "db_iep_session_stream": (VP, [VP]),
+    "db_iep_session_stats": (C.c_int32, [VP, C.POINTER(SessionStats)]),
+    "db_iep_session_schedule": (C.c_int32, [VP, PVP]),
+    "db_iep_session_run": (C.c_int32, [VP, PVP]),
+    "db_iep_session_labels": (C.c_int32, [VP, VP, C.c_int64]),
+    "db_iep_session_free": (None, [VP]),
+    "db_execute_device": (C.c_int32, [VP, VP, C.c_uint64, C.POINTER(ModuleOpts), PVP]),
+    "db_moe_session_create": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, C.c_int64, C.c_int64,
+                                          PVP]),
+    "db_moe_session_forward": (C.c_int32, [VP]),
+    "db_moe_session_forward_host": (C.c_int32, [VP, VP, VP, VP]),
+    "db_moe_session_synchronize": (C.c_int32, [VP]),
+    "db_moe_session_stream": (VP, [VP]),
+    "db_moe_session_stats": (C.c_int32, [VP, C.POINTER(SessionStats)]),
+    "db_moe_session_routing": (C.c_int32, [VP, VP, VP, VP, VP]),
+    "db_moe_session_run": (C.c_int32, [VP, PVP]),
+    "db_moe_session_free": (None, [VP]),
+    "db_moe_run_device": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, PVP]),
+}
+
+_lib = None
+
+
+def lib():
+    """Loads libdynbatch.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python __graft_entry__.py build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().db_last_error().decode()
+
+
+def check(status: int):
+    if status != DB_OK:
+        raise DynbatchError(status, last_error())
+
+
+def _take_string(p: C.c_void_p) -> str:
+    s = C.cast(p, C.c_char_p).value.decode()
+    lib().db_string_free(p)
+    return s
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class _Handle:
+    _free = None
+
+    def __init__(self, h):
+        self.h = h
+
+    def close(self):
+        if self.h:
+            getattr(lib(), self._free)(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Batch(_Handle):
+    """db_batch: vocabulary + programs + seeded input rows."""
+    _free = "db_batch_free"
+
+    @classmethod
+    def generate(cls, kind="chain", batch=8, vocab=40, width=128, depth=4, length=16,
+                 branch_prob=0.1, seed=0):
+        o = WorkloadOpts(WORKLOAD[kind] if isinstance(kind, str) else kind, batch, vocab, width,
+                         depth, length, branch_prob, seed)
+        h = C.c_void_p()
+        check(lib().db_batch_generate(C.byref(o), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_json(cls, text: str, width: int, input_seed: int):
+        h = C.c_void_p()
+        check(lib().db_batch_load_json(text.encode(), width, input_seed, C.byref(h)))
+        return cls(h)
+
+    def to_json(self) -> str:
+        p = C.c_void_p()
+        check(lib().db_batch_to_json(self.h, C.byref(p)))
+        return _take_string(p)
+
+    def stats(self) -> BatchStats:
+        s = BatchStats()
+        check(lib().db_batch_stats(self.h, C.byref(s)))
+        return s
+
+    def schedule(self, strategy="improved") -> "Schedule":
+        h = C.c_void_p()
+        check(lib().db_schedule_build(self.h, STRATEGY[strategy], C.byref(h)))
+        return Schedule(h)
+
+    def execute(self, schedule: "Schedule", module_seed: int) -> "Run":
+        h = C.c_void_p()
+        check(lib().db_execute(self.h, schedule.h, module_seed, C.byref(h)))
+        return Run(h)
+
+    def execute_device(self, module_seed: int, module_kind=MODULE_DENSE, schedule=None) -> "Run":
+        h = C.c_void_p()
+        opts = ModuleOpts(module_kind, 128, 14, 14)
+        check(lib().db_execute_device(self.h, schedule.h if schedule else None, module_seed,
+                                      C.byref(opts), C.byref(h)))
+        return Run(h)
+
+
+class Schedule(_Handle):
+    _free = "db_schedule_free"
+
+    def verify(self, batch: Batch):
+        check(lib().db_schedule_verify(self.h, batch.h))
+
+    def step_count(self) -> int:
+        return lib().db_schedule_step_count(self.h)
+
+    def expensive_calls(self, batch: Batch) -> int:
+        v = C.c_int64()
+        check(lib().db_schedule_expensive_calls(self.h, batch.h, C.byref(v)))
+        return v.value
+
+    def to_json(self) -> str:
+        p = C.c_void_p()
+        check(lib().db_schedule_to_json(self.h, C.byref(p)))
+        return _take_string(p)
+
+    def inject_fault(self, kind: str):
+        check(lib().db_schedule_inject_fault(self.h, kind.encode()))
+
+
+class Run(_Handle):
+    _free = "db_run_free"
+
+    def outputs(self) -> np.ndarray:
+        d = C.POINTER(C.c_double)()
+        r, w = C.c_int64(), C.c_int64()
+        check(lib().db_run_outputs(self.h, C.byref(d), C.byref(r), C.byref(w)))
+        if r.value * w.value == 0:
+            return np.zeros((r.value, w.value))
+        return np.ctypeslib.as_array(d, shape=(r.value, w.value)).copy()
+
+    @property
+    def expensive_calls(self):
+        return lib().db_run_expensive_calls(self.h)
+
+    @property
+    def peak_group_rows(self):
+        return lib().db_run_peak_group_rows(self.h)
+
+    def trace_json(self) -> str:
+        p = C.c_void_p()
+        check(lib().db_run_trace_json(self.h, C.byref(p)))
+        return _take_string(p)
+
+
+def moe_run(experts, k, batch, data_dim, hidden, seed=0, batched=True) -> Run:
+    o = MoeOpts(experts, k, batch, data_dim, hidden, seed)
+    h = C.c_void_p()
+    check(lib().db_moe_run(C.byref(o), 1 if batched else 0, C.byref(h)))
+    return Run(h)
+
+
+def moe_memory_model(experts, k, hidden, data_dim, m) -> MemoryModel:
+    out = MemoryModel()
+    check(lib().db_moe_memory_model(experts, k, hidden, data_dim, m, C.byref(out)))
+    return out
+
+
+def verify_run(seeds=6, batch=6, vocab=9, length=10, width=8, seed=0, parallel=False, log=None):
+    lines = []
+
+    def _cb(line, _user):
+        lines.append(line.decode())
+        if log:
+            log(line.decode())
+
+    cb = LOG_FN(_cb)
+    o = VerifyOpts(seeds, batch, vocab, length, width, seed, 1 if parallel else 0)
+    st = lib().db_verify_run(C.byref(o), cb, None)
+    return st, lines
+
+
+class IepSession(_Handle):
+    """Device-resident IEP batch: forward = device scheduler + step kernels."""
+    _free = "db_iep_session_free"
+
+    def __init__(self, batch: Batch, module_seed: int, module_kind=MODULE_DENSE, first=0, last=0):
+        h = C.c_void_p()
+        opts = ModuleOpts(module_kind, 128, 14, 14)
+        check(lib().db_iep_session_create(batch.h, first, last, module_seed, C.byref(opts),
+                                          C.byref(h)))
+        super().__init__(h)
+
+    def set_schedule(self, schedule):
+        check(lib().db_iep_session_set_schedule(self.h, schedule.h if schedule else None))
+
+    def forward(self):
+        check(lib().db_iep_session_forward(self.h))
+
+    def forward_host(self, inputs: np.ndarray, outputs: np.ndarray):
+        check(lib().db_iep_session_forward_host(self.h, _ptr(inputs), _ptr(outputs)))
+
+    def synchronize(self):
+        check(lib().db_iep_session_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        return lib().db_iep_session_stream(self.h) or 0
+
+    def stats(self) -> SessionStats:
+        s = SessionStats()
+        check(lib().db_iep_session_stats(self.h, C.byref(s)))
+        return s
+
+    def schedule(self) -> Schedule:
+        h = C.c_void_p()
+        check(lib().db_iep_session_schedule(self.h, C.byref(h)))
+        return Schedule(h)
+
+    def run(self) -> Run:
+        h = C.c_void_p()
+        check(lib().db_iep_session_run(self.h, C.byref(h)))
+        return Run(h)
+
+    def labels(self, n_nodes: int) -> np.ndarray:
+        out = np.zeros(n_nodes, np.int32)
+        check(lib().db_iep_session_labels(self.h, _ptr(out), n_nodes))
+        return out
+
+
+class MoeSession(_Handle):
+    _free = "db_moe_session_free"
+
+    def __init__(self, experts, k, batch, data_dim, hidden, seed=0, precision=MOE_BF16, first=0,
+                 last=0):
+        o = MoeOpts(experts, k, batch, data_dim, hidden, seed)
+        h = C.c_void_p()
+        check(lib().db_moe_session_create(C.byref(o), precision, first, last, C.byref(h)))
+        super().__init__(h)
+        self.n, self.k, self.d = experts, k, data_dim
+        self.T = (last - first) if last > first else batch
+
+    def forward(self):
+        check(lib().db_moe_session_forward(self.h))
+
+    def forward_host(self, inputs, scores, outputs):
+        check(lib().db_moe_session_forward_host(self.h, _ptr(inputs), _ptr(scores), _ptr(outputs)))
+
+    def synchronize(self):
+        check(lib().db_moe_session_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        return lib().db_moe_session_stream(self.h) or 0
+
+    def stats(self) -> SessionStats:
+        s = SessionStats()
+        check(lib().db_moe_session_stats(self.h, C.byref(s)))
+        return s
+
+    def routing(self):
+        ids = np.zeros((self.T, self.k), np.int32)
+        w = np.zeros((self.T, self.k), np.float64)
+        off = np.zeros(self.n + 1, np.int32)
+        items = np.zeros(self.T * self.k, np.int32)
+        check(lib().db_moe_session_routing(self.h, _ptr(ids), _ptr(w), _ptr(off), _ptr(items)))
+        return ids, w, off, items
+
+    def run(self) -> Run:
+        h = C.c_void_p()
+        check(lib().db_moe_session_run(self.h, C.byref(h)))
+        return Run(h)
+
+
+def device_count() -> int:
+    return lib().db_device_count()
+
+
+def device_open(device: int):
+    check(lib().db_device_open(device))

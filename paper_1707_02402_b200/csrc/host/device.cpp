@@ -1,0 +1,378 @@
+// device.cpp — device context, batch upload, device scheduler and the IEP
+// session (forward = device scheduler + per-step module kernels).
+#include "device.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "dynbatch/dbk.h"
+#include "iep_rb.hpp"
+
+namespace dynbatch::dev {
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+
+namespace {
+thread_local int t_checked_device = -1;
+int g_sm_count = 0;
+}  // namespace
+
+void require_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  int count = 0;
+  if (e == cudaSuccess) e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw std::runtime_error(
+        "no CUDA device available: the dynbatch B200 library has no CPU fallback");
+  }
+  if (t_checked_device == dev) return;
+  cudaDeviceProp prop{};
+  check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+  if (prop.major != 10) {
+    throw std::runtime_error("device " + std::to_string(dev) + " (" + prop.name +
+                             ") is not sm_100; this library is built for sm_100a only");
+  }
+  g_sm_count = prop.multiProcessorCount;
+  t_checked_device = dev;
+}
+
+int sm_count() {
+  require_device();
+  return g_sm_count;
+}
+
+HostCSR make_csr(std::span<const Program> programs, const FunctionVocab& vocab) {
+  HostCSR c;
+  c.b = static_cast<std::int64_t>(programs.size());
+  c.p = vocab.size();
+  c.arity_of.resize(static_cast<size_t>(c.p));
+  c.expensive_of.resize(static_cast<size_t>(c.p));
+  for (const ModuleSpec& s : vocab.specs()) {
+    c.arity_of[static_cast<size_t>(s.function_id)] = s.arity;
+    c.expensive_of[static_cast<size_t>(s.function_id)] = s.is_expensive() ? 1 : 0;
+    c.max_arity = std::max(c.max_arity, s.arity);
+  }
+  std::int64_t N = 0;
+  for (const Program& p : programs) N += p.size();
+  if (N >= (1LL << 31)) throw_error(Errc::invalid_argument, "batch too large for int32 node ids");
+  c.N = N;
+  c.prog_off.reserve(static_cast<size_t>(c.b) + 1);
+  c.fid.reserve(static_cast<size_t>(N));
+  c.child_off.reserve(static_cast<size_t>(N) + 1);
+  c.example.reserve(static_cast<size_t>(N));
+  std::int32_t off = 0;
+  for (std::int64_t e = 0; e < c.b; ++e) {
+    const Program& prog = programs[static_cast<size_t>(e)];
+    c.prog_off.push_back(off);
+    c.root_g.push_back(off + prog.root);
+    c.s_max = std::max(c.s_max, prog.size());
+    for (const ProgramNode& node : prog.nodes) {
+      c.fid.push_back(node.function_id);
+      c.example.push_back(static_cast<std::int32_t>(e));
+      c.child_off.push_back(static_cast<std::int32_t>(c.child_list.size()));
+      for (int ch : node.children) c.child_list.push_back(off + ch);
+      c.child0.push_back(node.children.size() > 0 ? off + node.children[0] : -1);
+      c.child1.push_back(node.children.size() > 1 ? off + node.children[1] : -1);
+    }
+    off += prog.size();
+  }
+  c.prog_off.push_back(off);
+  c.child_off.push_back(static_cast<std::int32_t>(c.child_list.size()));
+  return c;
+}
+
+// ------------------------------------------------------ DeviceProgramBatch
+DeviceProgramBatch::DeviceProgramBatch(const HostCSR& csr, cudaStream_t s) : csr_(csr) {
+  prog_off.upload(csr.prog_off, s);
+  fid.upload(csr.fid, s);
+  child_off.upload(csr.child_off, s);
+  child_list.upload(csr.child_list, s);
+  child0.upload(csr.child0, s);
+  child1.upload(csr.child1, s);
+  example.upload(csr.example, s);
+  root_g.upload(csr.root_g, s);
+  arity_of.upload(csr.arity_of, s);
+  const size_t N = static_cast<size_t>(std::max<std::int64_t>(csr.N, 1));
+  labels.alloc(N);
+  scratch.alloc(2 * N);
+  scalars.alloc(8);
+  member_g.alloc(N);
+  // d_max + 1 <= s_max, so at most s_max * p (step, fid) keys / groups.
+  max_keys_ = std::max(1, csr.s_max) * csr.p;
+  const size_t nseg = (N + 255) / 256;
+  seg_hist.alloc(static_cast<size_t>(max_keys_) * nseg);
+  group_fid.alloc(static_cast<size_t>(max_keys_) + 1);
+  group_begin.alloc(static_cast<size_t>(max_keys_) + 2);
+  step_group_begin.alloc(static_cast<size_t>(std::max(1, csr.s_max)) + 2);
+}
+
+int DeviceProgramBatch::run_scheduler(cudaStream_t s) {
+  if (csr_.b == 0) {
+    steps = 0;
+    groups = 0;
+    return 0;
+  }
+  check(cudaMemsetAsync(scalars.get(), 0, sizeof(std::int32_t) * 8, s), "memset");
+  check(dbk_sched_labels(csr_.b, csr_.N, prog_off.get(), child_off.get(), child_list.get(),
+                         root_g.get(), labels.get(), scratch.get(), scalars.get(), s),
+        "dbk_sched_labels");
+  check(dbk_sched_bucket_sort(csr_.N, csr_.p, max_keys_, fid.get(), labels.get(), scalars.get(),
+                              seg_hist.get(), member_g.get(), group_fid.get(), group_begin.get(),
+                              step_group_begin.get(), s),
+        "dbk_sched_bucket_sort");
+  std::int32_t host_scal[3];
+  check(cudaMemcpyAsync(host_scal, scalars.get(), sizeof(host_scal), cudaMemcpyDeviceToHost, s),
+        "D2H scalars");
+  check(cudaStreamSynchronize(s), "scheduler sync");
+  if (host_scal[1]) throw_error(Errc::invalid_program, "cycle or unreachable node");
+  steps = host_scal[0] + 1;
+  groups = host_scal[2];
+  return steps;
+}
+
+int DeviceProgramBatch::load_schedule(const Schedule& schedule, cudaStream_t s) {
+  std::vector<std::int32_t> mg, gf, gb, sgb;
+  sgb.reserve(schedule.steps.size() + 1);
+  for (const Step& step : schedule.steps) {
+    sgb.push_back(static_cast<std::int32_t>(gf.size()));
+    for (const CallGroup& g : step) {
+      if (g.function_id < 0 || g.function_id >= csr_.p) {
+        throw_error(Errc::unknown_function, "function id " + std::to_string(g.function_id));
+      }
+      gf.push_back(g.function_id);
+      gb.push_back(static_cast<std::int32_t>(mg.size()));
+      for (const NodeRef& r : g.members) {
+        if (r.example < 0 || r.example >= csr_.b || r.node < 0 ||
+            r.node >= csr_.prog_off[static_cast<size_t>(r.example) + 1] -
+                          csr_.prog_off[static_cast<size_t>(r.example)]) {
+          throw_error(Errc::invalid_argument, "node ref out of range (" +
+                                                  std::to_string(r.example) + ", " +
+                                                  std::to_string(r.node) + ")");
+        }
+        mg.push_back(csr_.prog_off[static_cast<size_t>(r.example)] + r.node);
+      }
+    }
+  }
+  sgb.push_back(static_cast<std::int32_t>(gf.size()));
+  gb.push_back(static_cast<std::int32_t>(mg.size()));
+  member_g.upload(mg, s);
+  group_fid.upload(gf, s);
+  group_begin.upload(gb, s);
+  step_group_begin.upload(sgb, s);
+  steps = static_cast<int>(schedule.steps.size());
+  groups = static_cast<std::int64_t>(gf.size());
+  return steps;
+}
+
+Schedule DeviceProgramBatch::download_schedule(Strategy strategy, cudaStream_t s) const {
+  Schedule out{strategy, {}};
+  if (steps == 0) return out;
+  const auto sgb = step_group_begin.download(static_cast<size_t>(steps) + 1, s);
+  const auto gf = group_fid.download(static_cast<size_t>(groups), s);
+  const auto gb = group_begin.download(static_cast<size_t>(groups) + 1, s);
+  const auto mg = member_g.download(static_cast<size_t>(gb.back()), s);
+  out.steps.resize(static_cast<size_t>(steps));
+  for (int st = 0; st < steps; ++st) {
+    for (std::int32_t g = sgb[static_cast<size_t>(st)]; g < sgb[static_cast<size_t>(st) + 1]; ++g) {
+      CallGroup cg;
+      cg.function_id = gf[static_cast<size_t>(g)];
+      for (std::int32_t m = gb[static_cast<size_t>(g)]; m < gb[static_cast<size_t>(g) + 1]; ++m) {
+        const std::int32_t node = mg[static_cast<size_t>(m)];
+        const std::int32_t e = csr_.example[static_cast<size_t>(node)];
+        cg.members.push_back({e, node - csr_.prog_off[static_cast<size_t>(e)]});
+      }
+      out.steps[static_cast<size_t>(st)].push_back(std::move(cg));
+    }
+  }
+  return out;
+}
+
+ExecutionTrace DeviceProgramBatch::trace_counts(cudaStream_t s) const {
+  ExecutionTrace t;
+  t.per_function_calls.assign(static_cast<size_t>(csr_.p), 0);
+  if (steps == 0) return t;
+  const auto gf = group_fid.download(static_cast<size_t>(groups), s);
+  const auto gb = group_begin.download(static_cast<size_t>(groups) + 1, s);
+  for (std::int64_t g = 0; g < groups; ++g) {
+    const std::int32_t f = gf[static_cast<size_t>(g)];
+    ++t.per_function_calls[static_cast<size_t>(f)];
+    if (csr_.expensive_of[static_cast<size_t>(f)]) ++t.expensive_calls;
+    t.peak_group_rows = std::max<std::int64_t>(t.peak_group_rows,
+                                                gb[static_cast<size_t>(g) + 1] - gb[static_cast<size_t>(g)]);
+  }
+  return t;
+}
+
+// ------------------------------------------------------------- IepSession
+IepSession::IepSession(const FunctionVocab& vocab, std::span<const Program> programs,
+                       const TensorBatch& inputs, std::uint64_t module_seed, ModuleKind kind)
+    : kind_(kind), width_(vocab.width()) {
+  require_device();
+  require_valid_batch(programs, vocab);
+  if (inputs.rows() != static_cast<std::int64_t>(programs.size())) {
+    throw_error(Errc::row_count_mismatch, "inputs have " + std::to_string(inputs.rows()) +
+                                              " rows for batch of " + std::to_string(programs.size()));
+  }
+  if (!programs.empty() && inputs.width() != width_) {
+    throw_error(Errc::width_mismatch, "inputs width " + std::to_string(inputs.width()));
+  }
+  if (!inputs.all_finite()) throw_error(Errc::non_finite_value, "non-finite input");
+  check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  const HostCSR csr = make_csr(programs, vocab);
+  batch_ = std::make_unique<DeviceProgramBatch>(csr, stream_);
+  err_.alloc(4);
+  present_.alloc(static_cast<size_t>(std::max<std::int64_t>(csr.N, 1)));
+  if (kind_ == ModuleKind::dense) {
+    in64_.upload(inputs.data().data(), inputs.data().size(), stream_);
+    values64_.alloc(static_cast<size_t>(std::max<std::int64_t>(csr.N, 1)) * static_cast<size_t>(width_));
+    out64_.alloc(static_cast<size_t>(std::max<std::int64_t>(csr.b, 1)) * static_cast<size_t>(width_));
+    ModuleSet modules(vocab, module_seed);
+    std::vector<const double*> wt(static_cast<size_t>(vocab.size()), nullptr), bt = wt;
+    w64_.resize(static_cast<size_t>(vocab.size()));
+    for (int f = 0; f < vocab.size(); ++f) {
+      const ModuleImpl& m = modules.impl(f);
+      if (m.spec.arity == 0) continue;
+      std::vector<double> blob(m.weights);
+      blob.insert(blob.end(), m.bias.begin(), m.bias.end());
+      w64_[static_cast<size_t>(f)].upload(blob, stream_);
+      wt[static_cast<size_t>(f)] = w64_[static_cast<size_t>(f)].get();
+      bt[static_cast<size_t>(f)] = w64_[static_cast<size_t>(f)].get() + m.weights.size();
+    }
+    wtab_.upload(wt, stream_);
+    btab_.upload(bt, stream_);
+  } else {
+    init_resblock(inputs, module_seed);
+  }
+  check(cudaStreamSynchronize(stream_), "session upload");
+}
+
+
+void IepSession::set_schedule(const Schedule* schedule) {
+  if (schedule) {
+    batch_->load_schedule(*schedule, stream_);
+    host_schedule_ = true;
+    strategy_ = schedule->strategy;
+  } else {
+    host_schedule_ = false;
+    strategy_ = Strategy::improved;
+  }
+}
+
+void IepSession::forward() {
+  launches_ = 0;
+  check(cudaMemsetAsync(err_.get(), 0, sizeof(std::int32_t) * 4, stream_), "memset err");
+  check(cudaMemsetAsync(present_.get(), 0, present_.size() * sizeof(std::int32_t), stream_), "memset present");
+  if (!host_schedule_) {
+    batch_->run_scheduler(stream_);
+    launches_ += 4;  // labels, histogram, scan, scatter
+  }
+  if (kind_ == ModuleKind::dense) forward_dense(); else forward_resblock();
+}
+
+void IepSession::forward_dense() {
+  const HostCSR& c = batch_->csr();
+  const int blocks = std::min<std::int64_t>(std::max<std::int64_t>(1, (c.N + 7) / 8), sm_count() * 16);
+  for (int st = 0; st < batch_->steps; ++st) {
+    check(dbk_dense_step(st, width_, batch_->step_group_begin.get(), batch_->group_fid.get(),
+                         batch_->group_begin.get(), batch_->member_g.get(), batch_->arity_of.get(),
+                         batch_->child_off.get(), batch_->child_list.get(), batch_->example.get(),
+                         in64_.get(), values64_.get(), present_.get(), wtab_.get(), btab_.get(),
+                         err_.get(), std::max(1, c.max_arity), blocks, stream_),
+          "dbk_dense_step");
+    ++launches_;
+  }
+  check(dbk_dense_gather_roots(c.b, width_, batch_->root_g.get(), present_.get(),
+                               values64_.get(), out64_.get(), err_.get(), stream_),
+        "dbk_dense_gather_roots");
+  ++launches_;
+}
+
+void IepSession::check_errors() {
+  std::int32_t e = 0;
+  check(cudaMemcpyAsync(&e, err_.get(), sizeof(e), cudaMemcpyDeviceToHost, stream_), "D2H err");
+  check(cudaStreamSynchronize(stream_), "sync");
+  switch (e) {
+    case 0: return;
+    case 7: throw_error(Errc::missing_operand, "a call group read a node that was not yet computed");
+    case 9: throw_error(Errc::non_finite_value, "a module produced non-finite rows");
+    case 14: throw_error(Errc::single_assignment_violation, "a node was written twice");
+    default: throw std::runtime_error("device executor error " + std::to_string(e));
+  }
+}
+
+void IepSession::synchronize() {
+  check(cudaStreamSynchronize(stream_), "sync");
+  check_errors();
+}
+
+Schedule IepSession::download_schedule() {
+  return batch_->download_schedule(strategy_, stream_);
+}
+
+std::vector<std::int32_t> IepSession::download_labels() { return batch_->download_labels(stream_); }
+
+TensorBatch IepSession::download_outputs() {
+  synchronize();
+  const HostCSR& c = batch_->csr();
+  TensorBatch out(c.b, width_);
+  if (c.b == 0) return out;
+  if (kind_ == ModuleKind::dense) {
+    check(cudaMemcpyAsync(out.data().data(), out64_.get(), sizeof(double) * out.data().size(),
+                          cudaMemcpyDeviceToHost, stream_), "D2H outputs");
+    check(cudaStreamSynchronize(stream_), "sync");
+  } else {
+    std::vector<float> tmp(out.data().size());
+    download_resblock_outputs(tmp.data());
+    for (size_t i = 0; i < tmp.size(); ++i) out.data()[i] = tmp[i];
+  }
+  return out;
+}
+
+ExecutionTrace IepSession::trace() {
+  ExecutionTrace t = batch_->trace_counts(stream_);
+  t.per_step_seconds.assign(static_cast<size_t>(batch_->steps), 0.0);
+  return t;
+}
+
+double IepSession::algorithmic_flops() const {
+  const HostCSR& c = batch_->csr();
+  double f = 0.0;
+  for (std::int64_t g = 0; g < c.N; ++g) {
+    const int fid = c.fid[static_cast<size_t>(g)];
+    const int a = c.arity_of[static_cast<size_t>(fid)];
+    if (a == 0) continue;
+    if (kind_ == ModuleKind::dense) {
+      f += 2.0 * a * width_ * static_cast<double>(width_);
+    } else {
+      // 2·MAC of the convolutions only: conv3x3 ×2 on
+      // 128×14×14 = 115,605,504; binary adds conv1x1 256→128 = 12,845,056.
+      f += a == 2 ? 128450560.0 : 115605504.0;
+    }
+  }
+  return f;
+}
+
+double IepSession::algorithmic_bytes() const {
+  const HostCSR& c = batch_->csr();
+  const double row = (kind_ == ModuleKind::dense ? 8.0 : 4.0) * width_;
+  double bytes = 0.0;
+  for (std::int64_t g = 0; g < c.N; ++g) {
+    const int a = c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])];
+    if (a > 0) bytes += (a + 1) * row;  // read operands, write result
+  }
+  return bytes;
+}
+
+std::int64_t IepSession::h2d_bytes() const { return batch_->csr().b * width_ * 4; }
+std::int64_t IepSession::d2h_bytes() const { return batch_->csr().b * width_ * 4; }
+
+}  // namespace dynbatch::dev

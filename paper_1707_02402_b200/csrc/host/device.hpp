@@ -1,0 +1,190 @@
+// device.hpp — host-side orchestration of the device path (internal).
+//
+// Owns device memory, the session stream and the per-forward launch
+// sequence. Everything crosses into CUDA through the dbk_* C-ABI
+// (include/dynbatch/dbk.h); no CUDA types leak into the public headers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <vector>
+
+#include "dynbatch.hpp"
+
+namespace dynbatch::dev {
+
+// Throws std::runtime_error (→ DB_ERR_INTERNAL) with the CUDA error text.
+void check(cudaError_t e, const char* what);
+inline void check(int e, const char* what) { check(static_cast<cudaError_t>(e), what); }
+// Verifies a CUDA device is present and is an sm_100 part; there is no CPU
+// fallback, so every compute entry point calls this first.
+void require_device();
+int sm_count();
+
+template <class T>
+class Buf {
+ public:
+  Buf() = default;
+  explicit Buf(size_t n) { alloc(n); }
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  Buf(Buf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  Buf& operator=(Buf&& o) noexcept {
+    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    return *this;
+  }
+  ~Buf() { release(); }
+  void alloc(size_t n) {
+    release();
+    if (n == 0) n = 1;
+    check(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)), "cudaMalloc");
+    n_ = n;
+  }
+  void ensure(size_t n) { if (n > n_ || !p_) alloc(n); }
+  void upload(const T* src, size_t n, cudaStream_t s) {
+    ensure(n);
+    if (n) check(cudaMemcpyAsync(p_, src, n * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+  void zero(cudaStream_t s) { if (p_) check(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s), "memset"); }
+  std::vector<T> download(size_t n, cudaStream_t s) const {
+    std::vector<T> out(n);
+    if (n) check(cudaMemcpyAsync(out.data(), p_, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaStreamSynchronize(s), "sync");
+    return out;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+
+ private:
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+// Batch in CSR form (global node g = prog_off[e] + local id).
+struct HostCSR {
+  std::int64_t b = 0, N = 0;
+  int p = 0, max_arity = 0, s_max = 0;
+  std::vector<std::int32_t> prog_off, fid, child_off, child_list, child0, child1, example, root_g;
+  std::vector<std::int32_t> arity_of, expensive_of;
+};
+HostCSR make_csr(std::span<const Program> programs, const FunctionVocab& vocab);
+
+// Device copy of the CSR plus the device scheduler (labels + stable bucket
+// sort) and the schedule tables it writes (or that a host schedule fills).
+class DeviceProgramBatch {
+ public:
+  DeviceProgramBatch(const HostCSR& csr, cudaStream_t s);
+  const HostCSR& csr() const { return csr_; }
+
+  // Device improved scheduler; returns the step count (one small D2H).
+  int run_scheduler(cudaStream_t s);
+  // Installs a host-built schedule in the same table format.
+  int load_schedule(const Schedule& schedule, cudaStream_t s);
+  Schedule download_schedule(Strategy strategy, cudaStream_t s) const;
+  std::vector<std::int32_t> download_labels(cudaStream_t s) const { return labels.download(csr_.N, s); }
+  ExecutionTrace trace_counts(cudaStream_t s) const;
+
+  int steps = 0;
+  std::int64_t groups = 0;
+  Buf<std::int32_t> prog_off, fid, child_off, child_list, child0, child1, example, root_g;
+  Buf<std::int32_t> arity_of, labels, scratch, scalars, seg_hist;
+  Buf<std::int32_t> member_g, group_fid, group_begin, step_group_begin;
+
+ private:
+  HostCSR csr_;
+  int max_keys_ = 0;
+};
+
+enum class ModuleKind { dense = 0, resblock = 1 };
+
+class IepSession {
+ public:
+  IepSession(const FunctionVocab& vocab, std::span<const Program> programs,
+             const TensorBatch& inputs, std::uint64_t module_seed, ModuleKind kind);
+  ~IepSession();
+
+  void set_schedule(const Schedule* schedule);
+  void forward();
+  void forward_host(const float* inputs, float* outputs);
+  void synchronize();
+  cudaStream_t stream() const { return stream_; }
+
+  Schedule download_schedule();
+  std::vector<std::int32_t> download_labels();
+  TensorBatch download_outputs();
+  ExecutionTrace trace();
+  std::int64_t launches() const { return launches_; }
+  double algorithmic_flops() const;
+  double algorithmic_bytes() const;
+  const HostCSR& csr() const { return batch_->csr(); }
+  int width() const { return width_; }
+  ModuleKind kind() const { return kind_; }
+  std::int64_t h2d_bytes() const;
+  std::int64_t d2h_bytes() const;
+
+ private:
+  void forward_dense();
+  void forward_resblock();
+  void check_errors();
+  void init_resblock(const TensorBatch& inputs, std::uint64_t module_seed);
+  void upload_resblock_inputs(const float* chw_rows);
+  void download_resblock_outputs(float* chw_rows);
+
+  ModuleKind kind_;
+  int width_ = 0;
+  cudaStream_t stream_ = nullptr;
+  std::unique_ptr<DeviceProgramBatch> batch_;
+  bool host_schedule_ = false;
+  Strategy strategy_ = Strategy::improved;
+  std::int64_t launches_ = 0;
+  Buf<std::int32_t> err_;
+  Buf<std::int32_t> present_;
+  // dense
+  Buf<double> in64_, values64_, out64_;
+  std::vector<Buf<double>> w64_;
+  Buf<const double*> wtab_, btab_;
+  // resblock
+  struct RB;
+  std::unique_ptr<RB> rb_;
+  std::vector<cudaEvent_t> step_events_;
+  float total_ms_ = 0.f;
+};
+
+// MoE session (fp64 reference order or bf16 tensor-core grouped GEMMs).
+class MoeSession {
+ public:
+  MoeSession(const MoeConfig& cfg, std::uint64_t seed, int precision, std::int64_t first,
+             std::int64_t last);
+  ~MoeSession();
+  void forward();
+  void forward_host(const float* inputs, const double* scores, float* outputs);
+  void synchronize();
+  cudaStream_t stream() const { return stream_; }
+  void routing(std::int32_t* ids, double* weights, std::int32_t* offsets, std::int32_t* items);
+  TensorBatch download_outputs();
+  ExecutionTrace trace();
+  std::int64_t launches() const { return launches_; }
+  double algorithmic_flops() const;
+  double algorithmic_bytes() const;
+  std::int64_t tokens() const { return T_; }
+  std::int64_t h2d_bytes() const;
+  std::int64_t d2h_bytes() const;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+  cudaStream_t stream_ = nullptr;
+  std::int64_t T_ = 0;
+  std::int64_t launches_ = 0;
+};
+
+}  // namespace dynbatch::dev

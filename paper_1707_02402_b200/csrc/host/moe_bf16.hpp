@@ -1,0 +1,28 @@
+// moe_bf16.hpp — bf16 tensor-core MoE expert path (grouped tcgen05 GEMMs).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+
+#include "dynbatch.hpp"
+
+namespace dynbatch::dev {
+
+class MoeBf16 {
+ public:
+  MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed, cudaStream_t s);
+  ~MoeBf16();
+  void upload_inputs(const float* x, cudaStream_t s);
+  // Dispatch → GEMM1+ReLU → GEMM2 → combine; returns kernels launched.
+  int forward(const std::int32_t* ids, const double* wts, const std::int32_t* order,
+              const std::int32_t* offsets, cudaStream_t s);
+  void download_outputs(float* out, cudaStream_t s);
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace dynbatch::dev

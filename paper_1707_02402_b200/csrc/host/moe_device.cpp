@@ -1,0 +1,388 @@
+// moe_device.cpp — MoE layer on the device (host orchestration).
+//
+// Forward = top-k gate (dbk_moe_topk) → stable expert sort of the k·T
+// assignments in (token, slot) order (dbk_stable_bucket_sort; the reference
+// group_by_function, src/schedule.cpp:166-169 via src/moe.cpp:214-224) →
+// grouped expert application → slot-order combine.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "device.hpp"
+#include "dynbatch/dbk.h"
+#include "moe_bf16.hpp"
+
+namespace dynbatch {
+namespace dev {
+
+struct MoeDev {
+  std::int64_t T = 0;
+  int n = 0, k = 0, d = 0, h = 0;
+  Buf<double> x, scores, wts, hidden, staged, out;
+  Buf<std::int32_t> ids, order, offsets, seg_hist, tiles, err;
+  std::vector<Buf<double>> w;  // per expert: w1 | w2
+  Buf<const double*> w1tab, w2tab;
+
+  void alloc(std::int64_t T_, int n_, int k_, int d_, int h_) {
+    T = T_; n = n_; k = k_; d = d_; h = h_;
+    const size_t items = static_cast<size_t>(T) * static_cast<size_t>(k);
+    scores.alloc(static_cast<size_t>(T) * n);
+    wts.alloc(items);
+    ids.alloc(items);
+    order.alloc(items);
+    offsets.alloc(static_cast<size_t>(n) + 1);
+    seg_hist.alloc(static_cast<size_t>(n) * ((items + 255) / 256 + 1));
+    tiles.alloc(static_cast<size_t>(n) + 1);
+    err.alloc(4);
+  }
+  void alloc_fp64_work() {
+    const size_t items = static_cast<size_t>(T) * static_cast<size_t>(k);
+    x.alloc(static_cast<size_t>(T) * d);
+    hidden.alloc(items * static_cast<size_t>(h));
+    staged.alloc(items * static_cast<size_t>(d));
+    out.alloc(static_cast<size_t>(T) * d);
+  }
+  void upload_experts(const ExpertSet& experts, cudaStream_t s) {
+    w.resize(static_cast<size_t>(n));
+    std::vector<const double*> t1(static_cast<size_t>(n)), t2(static_cast<size_t>(n));
+    for (int e = 0; e < n; ++e) {
+      const Expert& ex = experts.expert(e);
+      Buf<double>& b = w[static_cast<size_t>(e)];
+      b.alloc(ex.w1.size() + ex.w2.size());
+      check(cudaMemcpyAsync(b.get(), ex.w1.data(), ex.w1.size() * 8, cudaMemcpyHostToDevice, s), "H2D w1");
+      check(cudaMemcpyAsync(b.get() + ex.w1.size(), ex.w2.data(), ex.w2.size() * 8, cudaMemcpyHostToDevice, s), "H2D w2");
+      t1[static_cast<size_t>(e)] = b.get();
+      t2[static_cast<size_t>(e)] = b.get() + ex.w1.size();
+    }
+    w1tab.upload(t1, s);
+    w2tab.upload(t2, s);
+  }
+  void gate(cudaStream_t s) {
+    check(cudaMemsetAsync(err.get(), 0, 16, s), "memset");
+    check(dbk_moe_topk(T, n, k, scores.get(), ids.get(), wts.get(), err.get(), s), "dbk_moe_topk");
+  }
+  void sort(cudaStream_t s) {
+    check(dbk_stable_bucket_sort(T * k, n, ids.get(), seg_hist.get(), order.get(), offsets.get(), s),
+          "dbk_stable_bucket_sort");
+  }
+  void experts_fp64(cudaStream_t s) {
+    check(dbk_moe_expert_fp64(T, n, k, d, h, order.get(), offsets.get(), x.get(), w1tab.get(),
+                              w2tab.get(), hidden.get(), staged.get(), tiles.get(), s),
+          "dbk_moe_expert_fp64");
+  }
+  void combine_fp64(cudaStream_t s) {
+    check(dbk_moe_combine_fp64(T, k, d, wts.get(), staged.get(), out.get(), s), "dbk_moe_combine_fp64");
+  }
+  void check_err(cudaStream_t s) {
+    std::int32_t e = 0;
+    check(cudaMemcpyAsync(&e, err.get(), 4, cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaStreamSynchronize(s), "sync");
+    if (e == 9) throw_error(Errc::non_finite_value, "non-finite gate score");
+    if (e) throw std::runtime_error("device MoE error " + std::to_string(e));
+  }
+  ExecutionTrace trace(cudaStream_t s) {
+    ExecutionTrace t;
+    t.per_function_calls.assign(static_cast<size_t>(n), 0);
+    const auto off = offsets.download(static_cast<size_t>(n) + 1, s);
+    for (int e = 0; e < n; ++e) {
+      const std::int64_t rows = off[static_cast<size_t>(e) + 1] - off[static_cast<size_t>(e)];
+      if (rows == 0) continue;
+      ++t.expensive_calls;
+      ++t.per_function_calls[static_cast<size_t>(e)];
+      t.peak_group_rows = std::max(t.peak_group_rows, rows);
+    }
+    t.per_step_seconds.assign(1, 0.0);
+    return t;
+  }
+};
+
+namespace {
+cudaStream_t make_stream() {
+  cudaStream_t s = nullptr;
+  check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  return s;
+}
+struct StreamGuard {
+  cudaStream_t s;
+  ~StreamGuard() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
+};
+}  // namespace
+
+// ------------------------------------------------------------ MoeSession
+struct MoeSession::Impl {
+  MoeConfig cfg;
+  int precision = 0;
+  MoeDev dev;
+  std::unique_ptr<MoeBf16> bf16;
+  std::vector<float> host_in;  // for e2e tests
+};
+
+MoeSession::MoeSession(const MoeConfig& cfg_in, std::uint64_t seed, int precision,
+                       std::int64_t first, std::int64_t last)
+    : impl_(std::make_unique<Impl>()) {
+  require_device();
+  cfg_in.check();
+  MoeConfig cfg = cfg_in;
+  if (last <= first) { first = 0; last = cfg.batch; }
+  if (first < 0 || last > cfg.batch) throw_error(Errc::invalid_argument, "token range out of bounds");
+  T_ = last - first;
+  impl_->cfg = cfg;
+  impl_->precision = precision;
+  stream_ = make_stream();
+  MoeDev& D = impl_->dev;
+  D.alloc(T_, static_cast<int>(cfg.experts), static_cast<int>(cfg.active_per_example),
+          static_cast<int>(cfg.data_dim), static_cast<int>(cfg.hidden));
+  // Fixture generation exactly as db_moe_run (src/c_api.cpp:270-290); the
+  // token slice keeps rows [first, last) of the full-batch generators.
+  const TensorBatch inputs = random_batch(cfg.batch, cfg.data_dim, mix_seed(seed, 0x10ULL));
+  const TensorBatch scores = random_batch(cfg.batch, cfg.experts, mix_seed(seed, 0x11ULL));
+  check(cudaMemcpyAsync(D.scores.get(), scores.data().data() + first * cfg.experts,
+                        sizeof(double) * static_cast<size_t>(T_ * cfg.experts), cudaMemcpyHostToDevice, stream_),
+        "H2D scores");
+  const std::uint64_t expert_seed = mix_seed(seed, 0xe4be27ULL);
+  if (precision == 0) {
+    D.alloc_fp64_work();
+    check(cudaMemcpyAsync(D.x.get(), inputs.data().data() + first * cfg.data_dim,
+                          sizeof(double) * static_cast<size_t>(T_ * cfg.data_dim), cudaMemcpyHostToDevice, stream_),
+          "H2D inputs");
+    const ExpertSet experts(cfg.experts, cfg.data_dim, cfg.hidden, expert_seed);
+    D.upload_experts(experts, stream_);
+  } else {
+    impl_->bf16 = std::make_unique<MoeBf16>(cfg, T_, expert_seed, stream_);
+    std::vector<float> xin(static_cast<size_t>(T_ * cfg.data_dim));
+    for (size_t i = 0; i < xin.size(); ++i) xin[i] = static_cast<float>(inputs.data()[static_cast<size_t>(first * cfg.data_dim) + i]);
+    impl_->bf16->upload_inputs(xin.data(), stream_);
+  }
+  check(cudaStreamSynchronize(stream_), "upload");
+}
+
+MoeSession::~MoeSession() {
+  impl_.reset();
+  if (stream_) {
+    cudaStreamSynchronize(stream_);
+    cudaStreamDestroy(stream_);
+  }
+}
+
+void MoeSession::forward() {
+  MoeDev& D = impl_->dev;
+  launches_ = 0;
+  D.gate(stream_);
+  D.sort(stream_);
+  launches_ += 1 + 3;
+  if (impl_->precision == 0) {
+    D.experts_fp64(stream_);
+    D.combine_fp64(stream_);
+    launches_ += 3 + 1;
+  } else {
+    launches_ += impl_->bf16->forward(D.ids.get(), D.wts.get(), D.order.get(), D.offsets.get(), stream_);
+  }
+}
+
+void MoeSession::forward_host(const float* inputs, const double* scores, float* outputs) {
+  MoeDev& D = impl_->dev;
+  check(cudaMemcpyAsync(D.scores.get(), scores, sizeof(double) * static_cast<size_t>(T_) * D.n,
+                        cudaMemcpyHostToDevice, stream_), "H2D scores");
+  if (impl_->precision == 0) throw_error(Errc::invalid_argument, "forward_host needs the bf16 session");
+  impl_->bf16->upload_inputs(inputs, stream_);
+  forward();
+  impl_->bf16->download_outputs(outputs, stream_);
+}
+
+void MoeSession::synchronize() {
+  check(cudaStreamSynchronize(stream_), "sync");
+  impl_->dev.check_err(stream_);
+}
+
+void MoeSession::routing(std::int32_t* ids, double* weights, std::int32_t* offsets, std::int32_t* items) {
+  synchronize();
+  MoeDev& D = impl_->dev;
+  const size_t nk = static_cast<size_t>(T_) * D.k;
+  if (ids) check(cudaMemcpyAsync(ids, D.ids.get(), nk * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+  if (weights) check(cudaMemcpyAsync(weights, D.wts.get(), nk * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+  if (offsets) check(cudaMemcpyAsync(offsets, D.offsets.get(), (static_cast<size_t>(D.n) + 1) * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+  if (items) check(cudaMemcpyAsync(items, D.order.get(), nk * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+  check(cudaStreamSynchronize(stream_), "sync");
+}
+
+TensorBatch MoeSession::download_outputs() {
+  synchronize();
+  MoeDev& D = impl_->dev;
+  TensorBatch out(T_, D.d);
+  if (impl_->precision == 0) {
+    check(cudaMemcpyAsync(out.data().data(), D.out.get(), sizeof(double) * out.data().size(),
+                          cudaMemcpyDeviceToHost, stream_), "D2H");
+    check(cudaStreamSynchronize(stream_), "sync");
+  } else {
+    std::vector<float> tmp(out.data().size());
+    impl_->bf16->download_outputs(tmp.data(), stream_);
+    check(cudaStreamSynchronize(stream_), "sync");
+    for (size_t i = 0; i < tmp.size(); ++i) out.data()[i] = tmp[i];
+  }
+  if (!out.all_finite()) throw_error(Errc::non_finite_value, "non-finite output");
+  return out;
+}
+
+ExecutionTrace MoeSession::trace() { return impl_->dev.trace(stream_); }
+
+double MoeSession::algorithmic_flops() const {
+  const MoeConfig& c = impl_->cfg;
+  return 4.0 * static_cast<double>(T_) * c.active_per_example * c.data_dim * static_cast<double>(c.hidden);
+}
+
+double MoeSession::algorithmic_bytes() const {
+  const MoeConfig& c = impl_->cfg;
+  const double es = impl_->precision == 0 ? 8.0 : 2.0;
+  // scores read, inputs read, weights read once, outputs written (fp32/fp64)
+  return static_cast<double>(T_) * c.experts * 8.0 + static_cast<double>(T_) * c.data_dim * es +
+         2.0 * c.experts * c.data_dim * static_cast<double>(c.hidden) * es +
+         static_cast<double>(T_) * c.data_dim * (impl_->precision == 0 ? 8.0 : 4.0);
+}
+
+std::int64_t MoeSession::h2d_bytes() const {
+  return T_ * impl_->cfg.data_dim * 4 + T_ * impl_->cfg.experts * 8;
+}
+std::int64_t MoeSession::d2h_bytes() const { return T_ * impl_->cfg.data_dim * 4; }
+
+}  // namespace dev
+
+// ------------------------------------------------------- C++ operator API
+GateAssignment top_k_gate(const TensorBatch& scores, std::int64_t k) {
+  const std::int64_t n = scores.width();
+  if (k < 1 || k > n) throw_error(Errc::k_too_large, "k=" + std::to_string(k) + " with n=" + std::to_string(n));
+  if (!scores.all_finite()) throw_error(Errc::non_finite_value, "non-finite gate score");
+  GateAssignment g;
+  g.per_example.resize(static_cast<size_t>(scores.rows()));
+  if (scores.rows() == 0) return g;
+  dev::require_device();
+  dev::StreamGuard sg{dev::make_stream()};
+  dev::MoeDev D;
+  D.alloc(scores.rows(), static_cast<int>(n), static_cast<int>(k), 1, 1);
+  D.scores.upload(scores.data().data(), scores.data().size(), sg.s);
+  D.gate(sg.s);
+  D.check_err(sg.s);
+  const auto ids = D.ids.download(static_cast<size_t>(scores.rows() * k), sg.s);
+  const auto w = D.wts.download(static_cast<size_t>(scores.rows() * k), sg.s);
+  for (std::int64_t t = 0; t < scores.rows(); ++t) {
+    auto& e = g.per_example[static_cast<size_t>(t)];
+    for (std::int64_t s = 0; s < k; ++s) {
+      e.push_back({ids[static_cast<size_t>(t * k + s)], w[static_cast<size_t>(t * k + s)]});
+    }
+  }
+  return g;
+}
+
+namespace {
+void check_moe_args(const TensorBatch& inputs, const ExpertSet& experts, const GateAssignment& gates) {
+  if (inputs.width() != experts.data_dim()) throw_error(Errc::width_mismatch, "inputs width " + std::to_string(inputs.width()));
+  if (gates.per_example.size() != static_cast<size_t>(inputs.rows())) {
+    throw_error(Errc::row_count_mismatch, "gate assignment rows do not match inputs");
+  }
+  if (!inputs.all_finite()) throw_error(Errc::non_finite_value, "non-finite input");
+}
+
+MoeResult moe_forward(const TensorBatch& inputs, const ExpertSet& experts, const GateAssignment& gates,
+                      bool batched) {
+  check_moe_args(inputs, experts, gates);
+  const std::int64_t T = inputs.rows();
+  const std::int64_t d = experts.data_dim();
+  MoeResult r;
+  r.outputs = TensorBatch(T, d);
+  r.trace.per_function_calls.assign(static_cast<size_t>(experts.size()), 0);
+  std::int64_t k = 0;
+  for (const auto& e : gates.per_example) k = std::max<std::int64_t>(k, static_cast<std::int64_t>(e.size()));
+  if (T == 0 || k == 0) return r;
+  // Ragged gate lists are padded with zero-weight slots on expert 0; the
+  // padding rows are excluded from the trace below.
+  std::vector<std::int32_t> ids(static_cast<size_t>(T * k), 0);
+  std::vector<double> w(static_cast<size_t>(T * k), 0.0);
+  std::vector<unsigned char> real(static_cast<size_t>(T * k), 0);
+  for (std::int64_t t = 0; t < T; ++t) {
+    const auto& es = gates.per_example[static_cast<size_t>(t)];
+    for (size_t s = 0; s < es.size(); ++s) {
+      if (es[s].expert < 0 || es[s].expert >= experts.size()) {
+        throw_error(Errc::invalid_argument, "expert id " + std::to_string(es[s].expert));
+      }
+      ids[static_cast<size_t>(t * k) + s] = es[s].expert;
+      w[static_cast<size_t>(t * k) + s] = es[s].weight;
+      real[static_cast<size_t>(t * k) + s] = 1;
+    }
+  }
+  dev::require_device();
+  dev::StreamGuard sg{dev::make_stream()};
+  dev::MoeDev D;
+  D.alloc(T, static_cast<int>(experts.size()), static_cast<int>(k), static_cast<int>(d), static_cast<int>(experts.hidden()));
+  D.alloc_fp64_work();
+  D.x.upload(inputs.data().data(), inputs.data().size(), sg.s);
+  D.ids.upload(ids, sg.s);
+  D.wts.upload(w, sg.s);
+  D.upload_experts(experts, sg.s);
+  const auto t0 = std::chrono::steady_clock::now();
+  if (batched) {
+    D.sort(sg.s);
+    D.experts_fp64(sg.s);
+  } else {
+    // One single-row expert call per (token, slot) in token-major order.
+    const std::int64_t items = T * k;
+    std::vector<std::int32_t> off(static_cast<size_t>(items) * static_cast<size_t>(experts.size() + 1));
+    std::vector<std::int32_t> order(static_cast<size_t>(items));
+    for (std::int64_t i = 0; i < items; ++i) {
+      order[static_cast<size_t>(i)] = static_cast<std::int32_t>(i);
+      for (std::int64_t e = 0; e <= experts.size(); ++e)
+        off[static_cast<size_t>(i * (experts.size() + 1) + e)] = e <= ids[static_cast<size_t>(i)] ? 0 : 1;
+    }
+    dev::Buf<std::int32_t> doff, dord;
+    doff.upload(off, sg.s);
+    dord.upload(order, sg.s);
+    for (std::int64_t i = 0; i < items; ++i) {
+      if (!real[static_cast<size_t>(i)]) continue;
+      // order[0] = item i → input row i / k, staged row i.
+      dev::check(dbk_moe_expert_fp64(1, static_cast<std::int32_t>(experts.size()), static_cast<std::int32_t>(k),
+                                     static_cast<std::int32_t>(d), static_cast<std::int32_t>(experts.hidden()),
+                                     dord.get() + i, doff.get() + i * (experts.size() + 1), D.x.get(),
+                                     D.w1tab.get(), D.w2tab.get(), D.hidden.get(), D.staged.get(),
+                                     D.tiles.get(), sg.s),
+                 "naive expert call");
+    }
+  }
+  D.combine_fp64(sg.s);
+  dev::check(cudaStreamSynchronize(sg.s), "sync");
+  const auto t1 = std::chrono::steady_clock::now();
+  dev::check(cudaMemcpy(r.outputs.data().data(), D.out.get(), sizeof(double) * r.outputs.data().size(),
+                        cudaMemcpyDeviceToHost), "D2H");
+  const double secs = std::chrono::duration<double>(t1 - t0).count();
+  r.trace.module_seconds = secs;
+  r.trace.total_seconds = secs;
+  r.trace.per_step_seconds.push_back(secs);
+  if (batched) {
+    std::vector<std::int64_t> rows(static_cast<size_t>(experts.size()), 0);
+    for (size_t i = 0; i < ids.size(); ++i) if (real[i]) ++rows[static_cast<size_t>(ids[i])];
+    for (std::int64_t e = 0; e < experts.size(); ++e) {
+      if (!rows[static_cast<size_t>(e)]) continue;
+      ++r.trace.expensive_calls;
+      ++r.trace.per_function_calls[static_cast<size_t>(e)];
+      r.trace.peak_group_rows = std::max(r.trace.peak_group_rows, rows[static_cast<size_t>(e)]);
+    }
+  } else {
+    for (size_t i = 0; i < ids.size(); ++i) {
+      if (!real[i]) continue;
+      ++r.trace.expensive_calls;
+      ++r.trace.per_function_calls[static_cast<size_t>(ids[i])];
+      r.trace.peak_group_rows = 1;
+    }
+  }
+  if (!r.outputs.all_finite()) throw_error(Errc::non_finite_value, "non-finite output");
+  return r;
+}
+}  // namespace
+
+MoeResult moe_forward_naive(const TensorBatch& inputs, const ExpertSet& experts, const GateAssignment& gates) {
+  return moe_forward(inputs, experts, gates, false);
+}
+
+MoeResult moe_forward_batched(const TensorBatch& inputs, const ExpertSet& experts, const GateAssignment& gates) {
+  return moe_forward(inputs, experts, gates, true);
+}
+
+}  // namespace dynbatch

@@ -1,0 +1,259 @@
+// sched.cu — device scheduler: level labels + stable (level, function) bucket
+// sort → device-side call-group index lists.
+//
+// Replaces, bit-for-bit, max_root_distance_labels (src/program.cpp:239-272)
+// and schedule_improved + make_step (src/schedule.cpp:66-79, 135-164): the
+// reference pools nodes by label, emits pools deepest first, and within a
+// pool sorts by (function id, example, node). Nodes are numbered in CSR order
+// (example-major, node-minor), so a STABLE sort by
+//     key = (d_max - label) * p + fid
+// reproduces that order exactly. Stability comes from scan-based ranks, not
+// atomics: every warp owns a 256-node segment, per-(key, segment) counts are
+// exclusive-scanned key-major, and each warp then walks its segment in order
+// assigning ranks with __match_any_sync.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dynbatch/dbk.h"
+
+namespace {
+
+constexpr int kSeg = 256;        // nodes per warp segment
+constexpr int kWarpsPerBlock = 8;
+
+// One thread per program: Kahn's algorithm from the root with the queue and
+// in-degree counters in the program's own slice of `scratch`.
+__global__ void k_labels(int64_t b, const int32_t* __restrict__ prog_off,
+                         const int32_t* __restrict__ child_off,
+                         const int32_t* __restrict__ child_list,
+                         const int32_t* __restrict__ root_g, int32_t* __restrict__ labels,
+                         int32_t* __restrict__ indeg, int32_t* __restrict__ queue,
+                         int32_t* __restrict__ scal) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int local_max = 0;
+  if (e < b) {
+    const int32_t base = prog_off[e], end = prog_off[e + 1];
+    for (int32_t g = base; g < end; ++g) {
+      indeg[g] = 0;
+      labels[g] = 0;
+    }
+    for (int32_t g = base; g < end; ++g)
+      for (int32_t c = child_off[g]; c < child_off[g + 1]; ++c) ++indeg[child_list[c]];
+    int32_t head = base, tail = base;
+    queue[tail++] = root_g[e];
+    while (head < tail) {
+      const int32_t v = queue[head++];
+      const int32_t next = labels[v] + 1;
+      for (int32_t c = child_off[v]; c < child_off[v + 1]; ++c) {
+        const int32_t u = child_list[c];
+        if (labels[u] < next) labels[u] = next;
+        if (--indeg[u] == 0) queue[tail++] = u;
+      }
+    }
+    if (head != end) atomicOr(&scal[1], 1);
+    for (int32_t g = base; g < end; ++g) local_max = max(local_max, labels[g]);
+  }
+  for (int o = 16; o > 0; o >>= 1) local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  if ((threadIdx.x & 31) == 0 && local_max > 0) atomicMax(&scal[0], local_max);
+}
+
+struct LevelKey {
+  const int32_t* fid;
+  const int32_t* labels;
+  const int32_t* scal;
+  int32_t p;
+  __device__ __forceinline__ int32_t operator()(int64_t i) const {
+    return (scal[0] - labels[i]) * p + fid[i];
+  }
+};
+
+struct ExplicitKey {
+  const int32_t* keys;
+  __device__ __forceinline__ int32_t operator()(int64_t i) const { return keys[i]; }
+};
+
+// Per-(key, segment) counts into hist[key * nseg + seg] (pre-zeroed).
+template <class Key>
+__global__ void k_seg_hist(int64_t n, int32_t nseg, Key key, int32_t* __restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  const int32_t seg = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (seg >= nseg) return;
+  const int64_t begin = static_cast<int64_t>(seg) * kSeg;
+  for (int it = 0; it < kSeg / 32; ++it) {
+    const int64_t i = begin + it * 32 + lane;
+    const int32_t k = i < n ? key(i) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    if (k >= 0 && lane == __ffs(peers) - 1) hist[static_cast<int64_t>(k) * nseg + seg] += __popc(peers);
+  }
+}
+
+// Single-block exclusive scan over hist[0 .. n_keys*nseg) (key-major), then
+// the group table: one group per non-empty key, in key order.
+__global__ void k_scan_groups(int64_t n, int32_t nseg, int32_t p, int32_t* __restrict__ hist,
+                              int32_t* __restrict__ scal, int32_t fixed_keys,
+                              int32_t* __restrict__ group_fid, int32_t* __restrict__ group_begin,
+                              int32_t* __restrict__ step_group_begin,
+                              int32_t* __restrict__ offsets) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t carry_s;
+  const int32_t n_keys = fixed_keys > 0 ? fixed_keys : (scal[0] + 1) * p;
+  const int64_t total = static_cast<int64_t>(n_keys) * nseg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthreads = blockDim.x;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  // Pass 1: exclusive scan in tiles of blockDim elements.
+  for (int64_t base = 0; base < total; base += nthreads) {
+    const int64_t i = base + tid;
+    const int32_t v = i < total ? hist[i] : 0;
+    int32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = lane < (nthreads >> 5) ? warp_tot[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_tot[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    const int32_t carry = carry_s;
+    const int32_t excl = carry + (warp > 0 ? warp_tot[warp - 1] : 0) + x - v;
+    if (i < total) hist[i] = excl;
+    __syncthreads();
+    if (tid == nthreads - 1) carry_s = excl + v;
+    __syncthreads();
+  }
+  // Pass 2: key k's bucket is [hist[k*nseg], hist[(k+1)*nseg]) (n at the end).
+  if (offsets) {  // generic sort: bucket starts only
+    for (int32_t k = tid; k <= n_keys; k += nthreads)
+      offsets[k] = k < n_keys ? hist[static_cast<int64_t>(k) * nseg] : static_cast<int32_t>(n);
+    return;
+  }
+  // Group numbering: exclusive scan of (bucket non-empty) over keys.
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  for (int32_t base = 0; base < n_keys; base += nthreads) {
+    const int32_t k = base + tid;
+    int32_t start = 0, end = 0, flag = 0;
+    if (k < n_keys) {
+      start = hist[static_cast<int64_t>(k) * nseg];
+      end = k + 1 < n_keys ? hist[static_cast<int64_t>(k + 1) * nseg] : static_cast<int32_t>(n);
+      flag = end > start;
+    }
+    int32_t x = flag;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = lane < (nthreads >> 5) ? warp_tot[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const int32_t gidx = carry_s + (warp > 0 ? warp_tot[warp - 1] : 0) + x - flag;
+    if (k < n_keys) {
+      if (flag) {
+        group_fid[gidx] = k % p;
+        group_begin[gidx] = start;
+      }
+      if (k % p == 0) step_group_begin[k / p] = gidx;
+    }
+    __syncthreads();
+    if (tid == nthreads - 1) carry_s = gidx + flag;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const int32_t G = carry_s;
+    group_begin[G] = static_cast<int32_t>(n);
+    step_group_begin[n_keys / p] = G;
+    scal[2] = G;
+  }
+}
+
+// Stable scatter: each warp walks its segment in order; the lowest lane of
+// each equal-key peer set claims popc(peers) slots from the (key, segment)
+// cursor, which no other warp touches.
+template <class Key>
+__global__ void k_seg_scatter(int64_t n, int32_t nseg, Key key, int32_t* __restrict__ hist,
+                              int32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int32_t seg = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (seg >= nseg) return;
+  const int64_t begin = static_cast<int64_t>(seg) * kSeg;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int it = 0; it < kSeg / 32; ++it) {
+    const int64_t i = begin + it * 32 + lane;
+    const int32_t k = i < n ? key(i) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    const int leader = __ffs(peers) - 1;
+    int32_t base = 0;
+    if (k >= 0 && lane == leader) {
+      int32_t* cur = hist + static_cast<int64_t>(k) * nseg + seg;
+      base = *cur;
+      *cur = base + __popc(peers);
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (k >= 0) out[base + __popc(peers & lt)] = static_cast<int32_t>(i);
+  }
+}
+
+inline int32_t n_segments(int64_t n) { return static_cast<int32_t>((n + kSeg - 1) / kSeg); }
+
+}  // namespace
+
+extern "C" int dbk_sched_labels(int64_t b, int64_t N, const int32_t* prog_off,
+                                const int32_t* child_off, const int32_t* child_list,
+                                const int32_t* root_g, int32_t* labels, int32_t* scratch,
+                                int32_t* dev_scalars, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (b <= 0) return 0;
+  const int threads = 128;
+  const int blocks = static_cast<int>((b + threads - 1) / threads);
+  // scratch = indeg[N] | queue[N]
+  k_labels<<<blocks, threads, 0, s>>>(b, prog_off, child_off, child_list, root_g, labels, scratch,
+                                      scratch + N, dev_scalars);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, const int32_t* fid,
+                                     const int32_t* labels, int32_t* dev_scalars,
+                                     int32_t* seg_hist, int32_t* member_g, int32_t* group_fid,
+                                     int32_t* group_begin, int32_t* step_group_begin,
+                                     void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int32_t nseg = n_segments(N);
+  cudaMemsetAsync(seg_hist, 0, sizeof(int32_t) * static_cast<size_t>(max_keys) * (nseg > 0 ? nseg : 1), s);
+  LevelKey key{fid, labels, dev_scalars, p};
+  const int blocks = (nseg + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (nseg > 0) k_seg_hist<<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist);
+  k_scan_groups<<<1, 1024, 0, s>>>(N, nseg > 0 ? nseg : 1, p, seg_hist, dev_scalars, 0, group_fid,
+                                   group_begin, step_group_begin, nullptr);
+  if (nseg > 0) k_seg_scatter<<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist, member_g);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_stable_bucket_sort(int64_t n_items, int32_t n_keys, const int32_t* keys,
+                                      int32_t* seg_hist, int32_t* order, int32_t* offsets,
+                                      void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int32_t nseg = n_segments(n_items) > 0 ? n_segments(n_items) : 1;
+  cudaMemsetAsync(seg_hist, 0, sizeof(int32_t) * static_cast<size_t>(n_keys) * nseg, s);
+  ExplicitKey key{keys};
+  const int blocks = (nseg + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  k_seg_hist<<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist);
+  k_scan_groups<<<1, 1024, 0, s>>>(n_items, nseg, 1, seg_hist, nullptr, n_keys, nullptr, nullptr,
+                                   nullptr, offsets);
+  k_seg_scatter<<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist, order);
+  return static_cast<int>(cudaGetLastError());
+}
