@@ -63,32 +63,40 @@ int dbk_dense_gather_roots(int64_t b, int32_t width, const int32_t* root_g,
                            int32_t* err, void* stream);
 
 /* ------------------------------------------------------- resblock (Tier B)
- * Maps are C=128 × 14 × 14. Node values / inputs are fp32 "plane" maps
+ * Maps are C=128 × 14 × 14. Node values / inputs are fp32 "plane maps"
  * [16 planes][196 px][8 ch]; per-step staging is bf16 planes over a packed,
- * zero-padded 15×15 position grid. */
-int dbk_rb_plan(int32_t n_steps, int32_t p, const int32_t* step_group_begin,
-                const int32_t* group_key, const int32_t* group_begin, int32_t* seg_start,
-                int32_t* tiles, int32_t* step_tile_begin, int32_t* bin_tiles,
-                int32_t* step_bintile_begin, int32_t* step_positions, int32_t tile_m,
+ * zero-padded 15×15 position grid (rb_conv.cu header). */
+
+/* Per step: segment starts (seg_start[g], -1 for leaf groups), tile lists
+ * (all expensive groups; binary groups only) and their per-step offsets. */
+int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
+                const int32_t* group_begin, const int32_t* arity_of, int32_t* seg_start,
+                int32_t* group_tile0, int32_t* group_bintile0, int32_t* step_tile_begin,
+                int32_t* step_bintile_begin, int32_t* step_positions, int32_t* tile_group,
+                int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, void* stream);
+/* Gather (+ fused channel concat for binary groups) of step `step` into the
+ * bf16 staging planes; plane_stride in positions. */
+int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_fid,
+                  const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
+                  const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
+                  const int32_t* child1, const int32_t* example, const float* inputs,
+                  const float* values, void* stage_x, void* stage_cat, int64_t plane_stride,
+                  int32_t blocks, void* stream);
+/* tcgen05 implicit-GEMM convolutions: kind 0 = conv1x1 over [x; y] → z
+ * (bf16 staging + fp32 parked in the node slot), 1 = conv3x3 #1 → mid
+ * (bf16), 2 = conv3x3 #2 + residual + ReLU → fp32 node values. */
+int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
+                const int32_t* tile_group, const int32_t* tile_q0, const int32_t* group_fid,
+                const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
+                const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
+                const int32_t* example, const void* stage_in, void* stage_out,
+                int64_t plane_stride, const float* inputs, float* values,
+                const void* const* wpack, const float* const* bias, int32_t num_sms,
                 void* stream);
 int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream);
 int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int32_t* fid,
-                          const int32_t* example, const float* inputs, const float* values,
-                          float* chw, void* stream);
-int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_key,
-                  const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
-                  int32_t p, const int32_t* fid, const int32_t* child0g, const int32_t* child1g,
-                  const int32_t* example, const float* inputs, const float* values,
-                  void* stage_x, void* stage_cat, int64_t stage_stride, void* stream);
-/* conv kernels (tcgen05): kind 0 = conv1x1 over [x;y] → z (fp32 + bf16),
- * 1 = conv3x3 #1 → mid (bf16), 2 = conv3x3 #2 + residual → node values. */
-int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
-                const int32_t* tiles, const int32_t* group_key, const int32_t* group_begin,
-                const int32_t* seg_start, const int32_t* member_g, int32_t p,
-                const int32_t* fid, const int32_t* child0g, const int32_t* example,
-                const void* stage_in, void* stage_out, float* zbuf, const float* inputs,
-                float* values, const void* const* wpack, const float* const* bias,
-                int64_t stage_stride, int32_t num_sms, void* stream);
+                          const int32_t* arity_of, const int32_t* example, const float* inputs,
+                          const float* values, float* chw, void* stream);
 
 /* --------------------------------------------------------------------- MoE */
 /* top_k_gate (src/moe.cpp:36-69), one warp per token, fp64. */

@@ -1,12 +1,29 @@
 // iep_rb.hpp — device state of the Tier-B residual-block IEP path.
 #pragma once
 
+#include <cstdint>
+#include <vector>
+
 #include "device.hpp"
 
 namespace dynbatch::dev {
 
 struct IepSession::RB {
-  // filled in iep_resblock.cpp
+  static constexpr int kFmap = 25088;  // floats per 128×14×14 plane map
+  static constexpr int kTileM = 256;
+  static constexpr int kGuard = 32;
+  std::int64_t plane_stride = 0;  // staging positions per plane
+  Buf<float> inputs;              // [b][kFmap] plane maps
+  Buf<float> values;              // [N][kFmap] node values (and parked z)
+  Buf<float> chw_in, chw_out;     // reference-layout rows for host I/O
+  Buf<std::uint16_t> stage_x, stage_cat, stage_mid;  // bf16 staging
+  std::vector<Buf<std::uint16_t>> wbuf;              // packed bf16 weights
+  std::vector<Buf<float>> bbuf;
+  Buf<const void*> w0tab, w1tab, w2tab;
+  Buf<const float*> b0tab, b1tab, b2tab;
+  Buf<std::int32_t> seg_start, group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
+      step_positions, tile_group, tile_q0, bin_group, bin_q0;
+  std::int64_t n_expensive = 0;
 };
 
 }  // namespace dynbatch::dev

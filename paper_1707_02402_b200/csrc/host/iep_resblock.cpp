@@ -1,9 +1,14 @@
-// iep_resblock.cpp — Tier-B residual conv module path of the IEP session.
+// iep_resblock.cpp — Tier-B residual conv module path of the IEP session:
+// weight packing for the tcgen05 kernels, buffer sizing and the per-step
+// launch sequence  plan → [gather → conv1x1 → conv3x3#1 → conv3x3#2]×steps.
+#include <algorithm>
+#include <cstring>
+
 #include "device.hpp"
+#include "dynbatch/dbk.h"
 #include "iep_rb.hpp"
 
 namespace dynbatch::dev {
-
 
 IepSession::~IepSession() {
   for (cudaEvent_t e : step_events_) cudaEventDestroy(e);
@@ -13,18 +18,187 @@ IepSession::~IepSession() {
   }
 }
 
+namespace {
 
-void IepSession::init_resblock(const TensorBatch&, std::uint64_t) {
-  throw std::runtime_error("resblock path not built yet");
+std::uint16_t to_bf16(double v) {
+  // round-to-nearest-even of the fp32 value, as __float2bfloat16_rn does
+  float f = static_cast<float>(v);
+  std::uint32_t u;
+  std::memcpy(&u, &f, 4);
+  const std::uint32_t lsb = (u >> 16) & 1u;
+  u += 0x7FFFu + lsb;
+  return static_cast<std::uint16_t>(u >> 16);
 }
-void IepSession::forward_resblock() {}
-void IepSession::upload_resblock_inputs(const float*) {}
-void IepSession::download_resblock_outputs(float*) {}
+
+// One 32 KB B stage per (tap | K-half): element (n = co, k = ci) of the
+// N=128 × K=128 block at ((k/8)·128 + n)·8 + k%8 (K-major, no swizzle).
+std::vector<std::uint16_t> pack_conv3(const std::vector<double>& w, int C) {
+  std::vector<std::uint16_t> out(static_cast<size_t>(9) * C * C);
+  for (int tap = 0; tap < 9; ++tap)
+    for (int ci = 0; ci < C; ++ci)
+      for (int co = 0; co < C; ++co)
+        out[static_cast<size_t>(tap) * C * C + (static_cast<size_t>(ci / 8) * C + co) * 8 + ci % 8] =
+            to_bf16(w[(static_cast<size_t>(tap) * C + ci) * C + co]);
+  return out;
+}
+
+std::vector<std::uint16_t> pack_conv1(const std::vector<double>& w, int C) {
+  std::vector<std::uint16_t> out(static_cast<size_t>(2) * C * C);
+  for (int ci = 0; ci < 2 * C; ++ci) {
+    const int kb = ci / C, k = ci % C;
+    for (int co = 0; co < C; ++co)
+      out[static_cast<size_t>(kb) * C * C + (static_cast<size_t>(k / 8) * C + co) * 8 + k % 8] =
+          to_bf16(w[static_cast<size_t>(ci) * C + co]);
+  }
+  return out;
+}
+
+}  // namespace
+
+void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_seed) {
+  constexpr int C = 128;
+  if (width_ != RB::kFmap) throw_error(Errc::width_mismatch, "resblock modules need width 25088 (128x14x14)");
+  const HostCSR& c = batch_->csr();
+  if (c.max_arity > 2) throw_error(Errc::arity_mismatch, "resblock modules support arity <= 2");
+  rb_ = std::make_unique<RB>();
+  RB& R = *rb_;
+  for (std::int64_t g = 0; g < c.N; ++g)
+    if (c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0) ++R.n_expensive;
+  const size_t b = static_cast<size_t>(std::max<std::int64_t>(c.b, 1));
+  const size_t N = static_cast<size_t>(std::max<std::int64_t>(c.N, 1));
+  R.inputs.alloc(b * RB::kFmap);
+  R.values.alloc(N * RB::kFmap);
+  R.chw_in.alloc(b * RB::kFmap);
+  R.chw_out.alloc(b * RB::kFmap);
+  // inputs: reference rows (CHW) → fp32 → plane maps
+  std::vector<float> tmp(inputs.data().size());
+  for (size_t i = 0; i < tmp.size(); ++i) tmp[i] = static_cast<float>(inputs.data()[i]);
+  check(cudaMemcpyAsync(R.chw_in.get(), tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+  check(dbk_rb_inputs_from_chw(c.b, R.chw_in.get(), R.inputs.get(), stream_), "inputs layout");
+  // staging: worst case every expensive node in one step, ≤ p groups per step
+  R.plane_stride = RB::kGuard + R.n_expensive * 225 + static_cast<std::int64_t>(c.p + 2) * RB::kTileM + 64;
+  const size_t ps = static_cast<size_t>(R.plane_stride);
+  R.stage_x.alloc(ps * 16 * 8);
+  R.stage_cat.alloc(ps * 32 * 8);
+  R.stage_mid.alloc(ps * 16 * 8);
+  R.stage_x.zero(stream_);
+  R.stage_cat.zero(stream_);
+  R.stage_mid.zero(stream_);
+  // schedule-derived tables (G ≤ max keys; tiles ≤ N_exp·225/256 + G)
+  const size_t G = static_cast<size_t>(std::max(1, c.s_max)) * c.p + 2;
+  const size_t S = static_cast<size_t>(std::max<std::int64_t>(c.N, 1)) + 2;  // naive: S = N
+  const size_t T = static_cast<size_t>(R.n_expensive) * 225 / RB::kTileM + G + 2;
+  R.seg_start.alloc(std::max(G, N + 2));
+  R.group_tile0.alloc(std::max(G, N + 2));
+  R.group_bintile0.alloc(std::max(G, N + 2));
+  R.step_tile_begin.alloc(S);
+  R.step_bintile_begin.alloc(S);
+  R.step_positions.alloc(S);
+  R.tile_group.alloc(T + N);
+  R.tile_q0.alloc(T + N);
+  R.bin_group.alloc(T + N);
+  R.bin_q0.alloc(T + N);
+  // weights
+  std::vector<const void*> w0(static_cast<size_t>(c.p), nullptr), w1 = w0, w2 = w0;
+  std::vector<const float*> b0(static_cast<size_t>(c.p), nullptr), b1 = b0, b2 = b0;
+  for (int f = 0; f < c.p; ++f) {
+    const int a = c.arity_of[static_cast<size_t>(f)];
+    if (a == 0) continue;
+    const ResBlockImpl m = make_resblock_impl(a, C, module_seed, f);
+    auto put_w = [&](const std::vector<std::uint16_t>& v) {
+      R.wbuf.emplace_back();
+      R.wbuf.back().upload(v, stream_);
+      return static_cast<const void*>(R.wbuf.back().get());
+    };
+    auto put_b = [&](const std::vector<double>& v) {
+      std::vector<float> fv(v.begin(), v.end());
+      R.bbuf.emplace_back();
+      R.bbuf.back().upload(fv, stream_);
+      return static_cast<const float*>(R.bbuf.back().get());
+    };
+    if (a == 2) {
+      w0[static_cast<size_t>(f)] = put_w(pack_conv1(m.w0, C));
+      b0[static_cast<size_t>(f)] = put_b(m.b0);
+    }
+    w1[static_cast<size_t>(f)] = put_w(pack_conv3(m.w1, C));
+    b1[static_cast<size_t>(f)] = put_b(m.b1);
+    w2[static_cast<size_t>(f)] = put_w(pack_conv3(m.w2, C));
+    b2[static_cast<size_t>(f)] = put_b(m.b2);
+  }
+  R.w0tab.upload(w0, stream_);
+  R.w1tab.upload(w1, stream_);
+  R.w2tab.upload(w2, stream_);
+  R.b0tab.upload(b0, stream_);
+  R.b1tab.upload(b1, stream_);
+  R.b2tab.upload(b2, stream_);
+}
+
+void IepSession::forward_resblock() {
+  RB& R = *rb_;
+  DeviceProgramBatch& B = *batch_;
+  const int S = B.steps;
+  if (S == 0) return;
+  const int sms = sm_count();
+  check(dbk_rb_plan(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
+                    R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(), R.step_tile_begin.get(),
+                    R.step_bintile_begin.get(), R.step_positions.get(), R.tile_group.get(), R.tile_q0.get(),
+                    R.bin_group.get(), R.bin_q0.get(), stream_),
+        "dbk_rb_plan");
+  launches_ += 2;
+  const int gather_blocks = static_cast<int>(std::min<std::int64_t>(std::max<std::int64_t>(R.n_expensive, 1), sms * 8));
+  for (int s = 0; s < S; ++s) {
+    check(dbk_rb_gather(s, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), R.seg_start.get(),
+                        B.member_g.get(), B.arity_of.get(), B.fid.get(), B.child0.get(), B.child1.get(),
+                        B.example.get(), R.inputs.get(), R.values.get(), R.stage_x.get(), R.stage_cat.get(),
+                        R.plane_stride, gather_blocks, stream_),
+          "dbk_rb_gather");
+    // conv1x1 over the binary groups' [x; y] → z (stage_x + parked fp32)
+    check(dbk_rb_conv(0, s, R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
+                      B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
+                      B.child0.get(), B.example.get(), R.stage_cat.get(), R.stage_x.get(), R.plane_stride,
+                      R.inputs.get(), R.values.get(), R.w0tab.get(), R.b0tab.get(), sms, stream_),
+          "conv1x1");
+    check(dbk_rb_conv(1, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
+                      B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
+                      B.child0.get(), B.example.get(), R.stage_x.get(), R.stage_mid.get(), R.plane_stride,
+                      R.inputs.get(), R.values.get(), R.w1tab.get(), R.b1tab.get(), sms, stream_),
+          "conv3x3 #1");
+    check(dbk_rb_conv(2, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
+                      B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
+                      B.child0.get(), B.example.get(), R.stage_mid.get(), nullptr, R.plane_stride,
+                      R.inputs.get(), R.values.get(), R.w2tab.get(), R.b2tab.get(), sms, stream_),
+          "conv3x3 #2");
+    launches_ += 4;
+  }
+  const HostCSR& c = B.csr();
+  check(dbk_rb_outputs_to_chw(c.b, B.root_g.get(), B.fid.get(), B.arity_of.get(), B.example.get(), R.inputs.get(),
+                              R.values.get(), R.chw_out.get(), stream_),
+        "outputs layout");
+  launches_ += 1;
+}
+
+void IepSession::upload_resblock_inputs(const float* chw_rows) {
+  RB& R = *rb_;
+  const std::int64_t b = batch_->csr().b;
+  check(cudaMemcpyAsync(R.chw_in.get(), chw_rows, sizeof(float) * static_cast<size_t>(b) * RB::kFmap,
+                        cudaMemcpyHostToDevice, stream_), "H2D inputs");
+  check(dbk_rb_inputs_from_chw(b, R.chw_in.get(), R.inputs.get(), stream_), "inputs layout");
+}
+
+void IepSession::download_resblock_outputs(float* chw_rows) {
+  RB& R = *rb_;
+  const std::int64_t b = batch_->csr().b;
+  check(cudaMemcpyAsync(chw_rows, R.chw_out.get(), sizeof(float) * static_cast<size_t>(b) * RB::kFmap,
+                        cudaMemcpyDeviceToHost, stream_), "D2H outputs");
+  check(cudaStreamSynchronize(stream_), "sync");
+}
+
 void IepSession::forward_host(const float* inputs, float* outputs) {
   if (kind_ != ModuleKind::resblock) throw_error(Errc::invalid_argument, "forward_host needs a resblock session");
   upload_resblock_inputs(inputs);
   forward();
   download_resblock_outputs(outputs);
+  check_errors();
 }
 
 }  // namespace dynbatch::dev

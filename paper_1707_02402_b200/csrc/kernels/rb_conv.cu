@@ -1,0 +1,529 @@
+// rb_conv.cu — Tier-B IEP module bodies: residual conv blocks on 128×14×14
+// feature maps as tcgen05/TMEM implicit-GEMM kernels (sm_100a).
+//
+// Module (north star; no reference implementation — SPEC.md:268-269):
+//   unary  y = relu(x + conv3x3_2(relu(conv3x3_1(x) + b1)) + b2)
+//   binary z = relu(conv1x1([x; y]) + b0), then the unary block on z.
+// Executor semantics around it follow src/executor.cpp:117-166 (gather child
+// k as operand k, apply, scatter to the member's slot); leaves alias the
+// example's input map instead of being copied.
+//
+// Data layout:
+//   * node values / inputs: fp32 "plane maps" [16 planes][196 px][8 ch]
+//     (plane j = channels 8j..8j+7) — 100,352 B per node;
+//   * per-step staging: bf16 planes over a packed position axis. Each image
+//     occupies a 15×15 grid (225 positions; row 14 and column 14 are zero
+//     pads shared with the next image / row), so a 3×3 tap (dh, dw) is the
+//     row shift dh·15 + dw of the same array. Images of one call group are
+//     contiguous; each group's segment starts on a TILE_M boundary so a CTA
+//     tile never mixes weights. Plane j of position q lives at
+//     ((j·PS) + GUARD + q) · 16 bytes.
+//   * tensor-core operands use the K-major SWIZZLE_NONE canonical layout
+//     (tc_common.cuh): the shared-memory A window [plane][position][8] is a
+//     valid operand starting at ANY position, so all nine taps read the same
+//     window at different row offsets — the im2col never materialises.
+//
+// Kernel (one CTA per SM, persistent over the step's tile list):
+//   warp 0 — producer: bulk async copies (TMA engine) of the A window
+//            (TILE_M + 32 positions × all input planes) and a ring of 32 KB
+//            weight stages (one 3×3 tap, or one 128-channel half of the 1×1);
+//   warp 1 — TMEM allocator + single-thread tcgen05.mma issuer
+//            (M = 128 per accumulator, N = 128, K = 16 per instruction);
+//   warps 2-5 — epilogue: tcgen05.ld of the fp32 accumulators, bias, ReLU,
+//            residual, pad masking, bf16 staging / fp32 node-value stores.
+// Accumulators are double-buffered in TMEM (2 × 256 columns) so the epilogue
+// of tile i overlaps the MMAs of tile i+1.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dynbatch/dbk.h"
+#include "tc_common.cuh"
+
+namespace {
+
+using namespace dbk;
+
+constexpr int kC = 128;              // channels
+constexpr int kPlanes = kC / 8;      // 16
+constexpr int kImg = 225;            // 15 × 15 packed grid per image
+constexpr int kPx = 196;             // 14 × 14
+constexpr int kFmap = kPlanes * kPx * 8;  // 25,088 floats per node map
+constexpr int kGuard = 32;           // zero positions before position 0
+constexpr int kTileM = 256;          // positions per CTA tile (2 accumulators)
+constexpr int kBStage = 128 * 128 * 2;  // 32 KB: N=128 × K=128 bf16
+constexpr int kThreads = 192;
+
+template <int KIND>
+struct Cfg;
+template <>
+struct Cfg<0> {  // conv1x1 over [x; y] (256 → 128)
+  static constexpr int kInPlanes = 32, kHalo = 0, kKB = 2, kStages = 2;
+};
+template <>
+struct Cfg<1> {  // conv3x3 #1 (128 → 128)
+  static constexpr int kInPlanes = 16, kHalo = 16, kKB = 9, kStages = 4;
+};
+template <>
+struct Cfg<2> : Cfg<1> {};  // conv3x3 #2 + residual
+
+template <int KIND>
+constexpr int win() { return kTileM + 2 * Cfg<KIND>::kHalo; }
+template <int KIND>
+constexpr int a_bytes() { return Cfg<KIND>::kInPlanes * win<KIND>() * 16; }
+template <int KIND>
+constexpr int smem_bytes() {
+  return a_bytes<KIND>() + Cfg<KIND>::kStages * kBStage + 256;
+}
+
+struct ConvParams {
+  int32_t step;
+  const int32_t* step_tile_begin;
+  const int32_t* tile_group;
+  const int32_t* tile_q0;
+  const int32_t* group_fid;
+  const int32_t* group_begin;
+  const int32_t* seg_start;
+  const int32_t* member_g;
+  const int32_t* arity_of;
+  const int32_t* fid;
+  const int32_t* child0;
+  const int32_t* example;
+  const __nv_bfloat16* stage_in;
+  __nv_bfloat16* stage_out;
+  int64_t ps;  // plane stride in positions
+  const float* inputs;
+  float* values;
+  const __nv_bfloat16* const* wpack;
+  const float* const* bias;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__ ConvParams P) {
+  using K = Cfg<KIND>;
+  constexpr int WIN = win<KIND>();
+  constexpr uint32_t IDESC = idesc_bf16_f32(128, 128);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + a_bytes<KIND>();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + K::kStages * kBStage);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = bars + 1;
+  uint64_t* b_full = bars + 2;
+  uint64_t* b_empty = b_full + K::kStages;
+  uint64_t* acc_full = b_empty + K::kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int s = 0; s < K::kStages; ++s) {
+      mbar_init(b_full + s, 1);
+      mbar_init(b_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int32_t t_begin = P.step_tile_begin[P.step];
+  const int32_t n_tiles = P.step_tile_begin[P.step + 1] - t_begin;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------ producer
+      uint32_t kbi = 0;
+      int it = 0;
+      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+        const int32_t g = P.tile_group[t_begin + t];
+        const int32_t q0 = P.tile_q0[t_begin + t];
+        const uint8_t* w = reinterpret_cast<const uint8_t*>(P.wpack[P.group_fid[g]]);
+        mbar_wait(a_empty, (it & 1) ^ 1);
+        mbar_expect_tx(a_full, a_bytes<KIND>());
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.stage_in) +
+                             static_cast<int64_t>(kGuard + q0 - K::kHalo) * 16;
+        for (int j = 0; j < K::kInPlanes; ++j) {
+          bulk_g2s(sA + j * WIN * 16, src + static_cast<int64_t>(j) * P.ps * 16, WIN * 16, a_full);
+        }
+        for (int kb = 0; kb < K::kKB; ++kb, ++kbi) {
+          const uint32_t s = kbi % K::kStages, ph = (kbi / K::kStages) & 1;
+          mbar_wait(b_empty + s, ph ^ 1);
+          mbar_expect_tx(b_full + s, kBStage);
+          bulk_g2s(sB + s * kBStage, w + static_cast<int64_t>(kb) * kBStage, kBStage, b_full + s);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------------------------------- MMA issuer
+      uint32_t kbi = 0;
+      int it = 0;
+      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+        const int abuf = it & 1;
+        mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
+        mbar_wait(a_full, it & 1);
+        tc_fence_after();
+        for (int kb = 0; kb < K::kKB; ++kb, ++kbi) {
+          const uint32_t s = kbi % K::kStages, ph = (kbi / K::kStages) & 1;
+          mbar_wait(b_full + s, ph);
+          tc_fence_after();
+          int shift = 0, plane0 = 0;
+          if (K::kKB == 9) {
+            shift = (kb / 3 - 1) * 15 + (kb % 3 - 1);
+          } else {
+            plane0 = kb * 16;
+          }
+#pragma unroll
+          for (int a = 0; a < kTileM / 128; ++a) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint32_t arow = static_cast<uint32_t>(K::kHalo + shift + a * 128);
+              const uint64_t ad = smem_desc(a_base + ((plane0 + 2 * kk) * WIN + arow) * 16, WIN * 16, 128);
+              const uint64_t bd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
+              mma_bf16(tmem_base + abuf * 256 + a * 128, ad, bd, IDESC, (kb | kk) != 0);
+            }
+          }
+          mma_commit(b_empty + s);
+        }
+        mma_commit(a_empty);
+        mma_commit(acc_full + abuf);
+      }
+    }
+  } else {  // ------------------------------------------------------ epilogue
+    const int quarter = warp & 3;
+    int it = 0;
+    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const int abuf = it & 1;
+      const int32_t g = P.tile_group[t_begin + t];
+      const int32_t q0 = P.tile_q0[t_begin + t];
+      const int32_t f = P.group_fid[g];
+      const int32_t gb0 = P.group_begin[g];
+      const int32_t rows = P.group_begin[g + 1] - gb0;
+      const int32_t seg = P.seg_start[g];
+      const float* __restrict__ bias = P.bias[f];
+      const bool binary = P.arity_of[f] == 2;
+      mbar_wait(acc_full + abuf, (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int a = 0; a < kTileM / 128; ++a) {
+        const int row = a * 128 + quarter * 32 + lane;
+        const int32_t q = q0 + row;
+        const int32_t local = q - seg;
+        const int32_t img = local / kImg, rem = local - img * kImg;
+        const int32_t r = rem / 15, c = rem - r * 15;
+        const bool valid = img < rows && r < 14 && c < 14;
+        const int32_t px = r * 14 + c;
+        int32_t node = 0;
+        const float* res = nullptr;
+        float* dst32 = nullptr;
+        if (valid && KIND != 1) {
+          node = P.member_g[gb0 + img];
+          dst32 = P.values + static_cast<int64_t>(node) * kFmap;
+          if (KIND == 2) {
+            if (binary) {
+              res = dst32;  // z was parked in the node's own slot by conv1x1
+            } else {
+              const int32_t ch = P.child0[node];
+              res = P.arity_of[P.fid[ch]] == 0 ? P.inputs + static_cast<int64_t>(P.example[ch]) * kFmap
+                                               : P.values + static_cast<int64_t>(ch) * kFmap;
+            }
+          }
+        }
+        uint8_t* out16 = reinterpret_cast<uint8_t*>(P.stage_out) + static_cast<int64_t>(kGuard + q) * 16;
+#pragma unroll 1
+        for (int cb = 0; cb < 4; ++cb) {
+          float v[32];
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * 256 + a * 128 + cb * 32, v);
+#pragma unroll
+          for (int pp = 0; pp < 4; ++pp) {
+            const int plane = cb * 4 + pp;
+            const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias + plane * 8));
+            const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias + plane * 8 + 4));
+            float o[8] = {v[pp * 8 + 0] + b_lo.x, v[pp * 8 + 1] + b_lo.y, v[pp * 8 + 2] + b_lo.z,
+                          v[pp * 8 + 3] + b_lo.w, v[pp * 8 + 4] + b_hi.x, v[pp * 8 + 5] + b_hi.y,
+                          v[pp * 8 + 6] + b_hi.z, v[pp * 8 + 7] + b_hi.w};
+            if (KIND == 2) {
+              if (valid) {
+                const float* rp = res + (plane * kPx + px) * 8;
+                const float4 r0 = *reinterpret_cast<const float4*>(rp);
+                const float4 r1 = *reinterpret_cast<const float4*>(rp + 4);
+                o[0] += r0.x; o[1] += r0.y; o[2] += r0.z; o[3] += r0.w;
+                o[4] += r1.x; o[5] += r1.y; o[6] += r1.z; o[7] += r1.w;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] = fmaxf(o[i], 0.0f);
+                float* dp = dst32 + (plane * kPx + px) * 8;
+                *reinterpret_cast<float4*>(dp) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4*>(dp + 4) = make_float4(o[4], o[5], o[6], o[7]);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) o[i] = valid ? fmaxf(o[i], 0.0f) : 0.0f;
+              uint4 pk;
+              pk.x = pack_bf16x2(o[0], o[1]);
+              pk.y = pack_bf16x2(o[2], o[3]);
+              pk.z = pack_bf16x2(o[4], o[5]);
+              pk.w = pack_bf16x2(o[6], o[7]);
+              *reinterpret_cast<uint4*>(out16 + static_cast<int64_t>(plane) * P.ps * 16) = pk;
+              if (KIND == 0 && valid) {  // fp32 z for the residual of the block
+                float* dp = dst32 + (plane * kPx + px) * 8;
+                *reinterpret_cast<float4*>(dp) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4*>(dp + 4) = make_float4(o[4], o[5], o[6], o[7]);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty + abuf);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ----------------------------------------------------------------- plan
+// Segment layout and tile lists for every step, from the group tables.
+// seg_start[g] is relative to the step's position origin; tiles of step s
+// occupy [step_tile_begin[s], step_tile_begin[s+1]).
+__global__ void k_rb_plan(int32_t n_steps, const int32_t* __restrict__ sgb,
+                          const int32_t* __restrict__ group_fid, const int32_t* __restrict__ group_begin,
+                          const int32_t* __restrict__ arity_of, int32_t* __restrict__ seg_start,
+                          int32_t* __restrict__ group_tile0, int32_t* __restrict__ group_bintile0,
+                          int32_t* __restrict__ step_tile_begin, int32_t* __restrict__ step_bintile_begin,
+                          int32_t* __restrict__ step_positions) {
+  // One thread per step computes its segment starts; tile prefixes over
+  // steps are then accumulated serially (steps are few for improved schedules).
+  for (int32_t s = threadIdx.x; s < n_steps; s += blockDim.x) {
+    int32_t cursor = 0, tiles = 0, bintiles = 0;
+    for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
+      const int32_t rows = group_begin[g + 1] - group_begin[g];
+      if (arity_of[group_fid[g]] == 0 || rows == 0) {
+        seg_start[g] = -1;
+        continue;
+      }
+      const int32_t nt = (rows * kImg + kTileM - 1) / kTileM;
+      seg_start[g] = cursor;
+      group_tile0[g] = tiles;
+      group_bintile0[g] = arity_of[group_fid[g]] == 2 ? bintiles : -1;
+      cursor += nt * kTileM;
+      tiles += nt;
+      if (arity_of[group_fid[g]] == 2) bintiles += nt;
+    }
+    step_positions[s] = cursor;
+    step_tile_begin[s + 1] = tiles;
+    step_bintile_begin[s + 1] = bintiles;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    step_tile_begin[0] = 0;
+    step_bintile_begin[0] = 0;
+    for (int32_t s = 0; s < n_steps; ++s) {
+      step_tile_begin[s + 1] += step_tile_begin[s];
+      step_bintile_begin[s + 1] += step_bintile_begin[s];
+    }
+  }
+}
+
+__global__ void k_rb_tiles(int32_t n_steps, const int32_t* __restrict__ sgb,
+                           const int32_t* __restrict__ group_fid, const int32_t* __restrict__ group_begin,
+                           const int32_t* __restrict__ arity_of, const int32_t* __restrict__ seg_start,
+                           const int32_t* __restrict__ group_tile0, const int32_t* __restrict__ group_bintile0,
+                           const int32_t* __restrict__ step_tile_begin,
+                           const int32_t* __restrict__ step_bintile_begin, int32_t* __restrict__ tile_group,
+                           int32_t* __restrict__ tile_q0, int32_t* __restrict__ bin_group,
+                           int32_t* __restrict__ bin_q0) {
+  const int32_t s = blockIdx.x;
+  if (s >= n_steps) return;
+  for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
+    if (seg_start[g] < 0) continue;
+    const int32_t rows = group_begin[g + 1] - group_begin[g];
+    const int32_t nt = (rows * kImg + kTileM - 1) / kTileM;
+    for (int32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+      const int32_t ti = step_tile_begin[s] + group_tile0[g] + i;
+      tile_group[ti] = g;
+      tile_q0[ti] = seg_start[g] + i * kTileM;
+      if (group_bintile0[g] >= 0) {
+        const int32_t bi = step_bintile_begin[s] + group_bintile0[g] + i;
+        bin_group[bi] = g;
+        bin_q0[bi] = seg_start[g] + i * kTileM;
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------- gather
+// Packs each expensive member's operand maps (fp32 plane maps of its
+// children; leaves read the example's input map) into the step's bf16
+// staging: unary → stage_x (16 planes), binary → stage_cat (32 planes: child
+// 0 then child 1, i.e. the channel concat of [x; y] fused into the gather).
+// Pads and the alignment gap after each group's last image are zero-filled.
+__global__ void __launch_bounds__(256) k_rb_gather(
+    int32_t step, const int32_t* __restrict__ sgb, const int32_t* __restrict__ group_fid,
+    const int32_t* __restrict__ group_begin, const int32_t* __restrict__ seg_start,
+    const int32_t* __restrict__ member_g, const int32_t* __restrict__ arity_of,
+    const int32_t* __restrict__ fid, const int32_t* __restrict__ child0,
+    const int32_t* __restrict__ child1, const int32_t* __restrict__ example,
+    const float* __restrict__ inputs, const float* __restrict__ values,
+    uint8_t* __restrict__ stage_x, uint8_t* __restrict__ stage_cat, int64_t ps) {
+  const int32_t g_lo = sgb[step], g_hi = sgb[step + 1];
+  const int32_t m_lo = group_begin[g_lo], m_hi = group_begin[g_hi];
+  for (int32_t m = m_lo + blockIdx.x; m < m_hi; m += gridDim.x) {
+    int32_t g = g_lo;
+    while (group_begin[g + 1] <= m) ++g;
+    const int32_t f = group_fid[g];
+    const int32_t arity = arity_of[f];
+    if (arity == 0 || seg_start[g] < 0) continue;
+    const int32_t img = m - group_begin[g];
+    const int32_t rows = group_begin[g + 1] - group_begin[g];
+    const int32_t node = member_g[m];
+    const int32_t base = kGuard + seg_start[g] + img * kImg;
+    uint8_t* dst = arity == 2 ? stage_cat : stage_x;
+    const int planes = arity == 2 ? 32 : 16;
+    const float* src_map[2];
+    for (int k = 0; k < arity; ++k) {
+      const int32_t ch = k == 0 ? child0[node] : child1[node];
+      src_map[k] = arity_of[fid[ch]] == 0 ? inputs + static_cast<int64_t>(example[ch]) * kFmap
+                                          : values + static_cast<int64_t>(ch) * kFmap;
+    }
+    for (int idx = threadIdx.x; idx < planes * kImg; idx += blockDim.x) {
+      const int p = idx / kImg, rem = idx - p * kImg;
+      const int r = rem / 15, c = rem - r * 15;
+      uint4 pk = make_uint4(0, 0, 0, 0);
+      if (r < 14 && c < 14) {
+        const float* sp = src_map[p >> 4] + ((p & 15) * kPx + r * 14 + c) * 8;
+        const float4 lo = *reinterpret_cast<const float4*>(sp);
+        const float4 hi = *reinterpret_cast<const float4*>(sp + 4);
+        pk.x = pack_bf16x2(lo.x, lo.y);
+        pk.y = pack_bf16x2(lo.z, lo.w);
+        pk.z = pack_bf16x2(hi.x, hi.y);
+        pk.w = pack_bf16x2(hi.z, hi.w);
+      }
+      *reinterpret_cast<uint4*>(dst + (static_cast<int64_t>(p) * ps + base + rem) * 16) = pk;
+    }
+    if (img == rows - 1) {  // zero the alignment gap after the group's last image
+      const int32_t gap0 = base + kImg;
+      const int32_t gap1 = kGuard + seg_start[g] + ((rows * kImg + kTileM - 1) / kTileM) * kTileM;
+      const int32_t gap = gap1 - gap0;
+      for (int idx = threadIdx.x; idx < planes * gap; idx += blockDim.x) {
+        const int p = idx / gap, q = gap0 + idx - p * gap;
+        *reinterpret_cast<uint4*>(dst + (static_cast<int64_t>(p) * ps + q) * 16) = make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+}
+
+// CHW fp32 rows (reference row layout, element c·196 + h·14 + w) → plane maps.
+__global__ void k_chw_to_planes(int64_t rows, const float* __restrict__ chw, float* __restrict__ planes) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= rows * kFmap) return;
+  const int64_t row = i / kFmap;
+  const int rem = static_cast<int>(i - row * kFmap);
+  const int p = rem / (kPx * 8), pr = rem - p * kPx * 8, px = pr >> 3, lane = pr & 7;
+  planes[i] = chw[row * kFmap + (p * 8 + lane) * kPx + px];
+}
+
+__global__ void k_roots_to_chw(int64_t b, const int32_t* __restrict__ root_g, const int32_t* __restrict__ fid,
+                               const int32_t* __restrict__ arity_of, const int32_t* __restrict__ example,
+                               const float* __restrict__ inputs, const float* __restrict__ values,
+                               float* __restrict__ chw) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= b * kFmap) return;
+  const int64_t e = i / kFmap;
+  const int rem = static_cast<int>(i - e * kFmap);  // CHW index: c*196 + px
+  const int c = rem / kPx, px = rem - c * kPx;
+  const int32_t r = root_g[e];
+  const float* map = arity_of[fid[r]] == 0 ? inputs + static_cast<int64_t>(example[r]) * kFmap
+                                          : values + static_cast<int64_t>(r) * kFmap;
+  chw[i] = map[((c >> 3) * kPx + px) * 8 + (c & 7)];
+}
+
+template <int KIND>
+int launch_conv(const ConvParams& p, int num_sms, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_rb_conv<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<KIND>());
+    configured = true;
+  }
+  k_rb_conv<KIND><<<num_sms, kThreads, smem_bytes<KIND>(), s>>>(p);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
+                           const int32_t* group_begin, const int32_t* arity_of, int32_t* seg_start,
+                           int32_t* group_tile0, int32_t* group_bintile0, int32_t* step_tile_begin,
+                           int32_t* step_bintile_begin, int32_t* step_positions, int32_t* tile_group,
+                           int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n_steps <= 0) return 0;
+  k_rb_plan<<<1, 1024, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
+                               group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
+                               step_positions);
+  k_rb_tiles<<<n_steps, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of,
+                                     seg_start, group_tile0, group_bintile0, step_tile_begin,
+                                     step_bintile_begin, tile_group, tile_q0, bin_group, bin_q0);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_fid,
+                             const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
+                             const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
+                             const int32_t* child1, const int32_t* example, const float* inputs,
+                             const float* values, void* stage_x, void* stage_cat, int64_t plane_stride,
+                             int32_t blocks, void* stream) {
+  k_rb_gather<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      step, step_group_begin, group_fid, group_begin, seg_start, member_g, arity_of, fid, child0, child1,
+      example, inputs, values, static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_cat), plane_stride);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
+                           const int32_t* tile_group, const int32_t* tile_q0, const int32_t* group_fid,
+                           const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
+                           const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
+                           const int32_t* example, const void* stage_in, void* stage_out,
+                           int64_t plane_stride, const float* inputs, float* values,
+                           const void* const* wpack, const float* const* bias, int32_t num_sms,
+                           void* stream) {
+  ConvParams p{step, step_tile_begin, tile_group, tile_q0, group_fid, group_begin, seg_start, member_g,
+               arity_of, fid, child0, example, static_cast<const __nv_bfloat16*>(stage_in),
+               static_cast<__nv_bfloat16*>(stage_out), plane_stride, inputs, values,
+               reinterpret_cast<const __nv_bfloat16* const*>(wpack), bias};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (kind) {
+    case 0: return launch_conv<0>(p, num_sms, s);
+    case 1: return launch_conv<1>(p, num_sms, s);
+    case 2: return launch_conv<2>(p, num_sms, s);
+  }
+  return static_cast<int>(cudaErrorInvalidValue);
+}
+
+extern "C" int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream) {
+  const int64_t total = rows * kFmap;
+  if (total <= 0) return 0;
+  k_chw_to_planes<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      rows, chw, planes);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int32_t* fid,
+                                     const int32_t* arity_of, const int32_t* example, const float* inputs,
+                                     const float* values, float* chw, void* stream) {
+  const int64_t total = b * kFmap;
+  if (total <= 0) return 0;
+  k_roots_to_chw<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      b, root_g, fid, arity_of, example, inputs, values, chw);
+  return static_cast<int>(cudaGetLastError());
+}
