@@ -53,7 +53,25 @@ typedef struct {
   double algorithmic_bytes; /* minimum HBM bytes of one forward */
 } db_session_stats_t;
 
+/* Per-kernel-class device time of a timed loop (CUDA events on the session
+ * stream around every launch of the class). Classes: 0 scheduler, 1 plan,
+ * 2 gather, 3 conv1x1 / moe gate+sort, 4 conv3x3#1 / moe GEMM1, 5 conv3x3#2 /
+ * moe GEMM2, 6 layout / combine, 7 dense step. */
+typedef struct {
+  double ms[8];
+  int64_t launches[8];
+  double flops[8]; /* algorithmic FLOPs of those launches */
+  double bytes[8]; /* algorithmic HBM bytes of those launches */
+} db_kernel_times_t;
+
 DYNBATCH_API int32_t db_device_count(void);
+/* Pinned (page-locked) host memory for end-to-end transfers. */
+DYNBATCH_API void* db_host_alloc(int64_t bytes);
+DYNBATCH_API void db_host_free(void* p);
+/* Programs [first, last) of gen_batch(opts), bit-identical to those rows of
+ * db_batch_generate (for data-parallel shards). */
+DYNBATCH_API db_status db_batch_generate_range(const db_workload_opts* opts, int64_t first,
+                                               int64_t last, db_batch** out);
 /* Binds the calling thread to `device` and checks it is sm_100. */
 DYNBATCH_API db_status db_device_open(int32_t device);
 
@@ -83,6 +101,11 @@ DYNBATCH_API db_status db_iep_session_schedule(db_iep_session* s, db_schedule** 
 DYNBATCH_API db_status db_iep_session_run(db_iep_session* s, db_run** out);
 /* Device level labels of the last forward (total_nodes int32, CSR order). */
 DYNBATCH_API db_status db_iep_session_labels(db_iep_session* s, int32_t* labels, int64_t n);
+/* Runs `iters` forwards between two CUDA events on the session stream and
+ * returns the elapsed device milliseconds; with profile != 0 also fills
+ * per-kernel-class times (events around every launch). */
+DYNBATCH_API db_status db_iep_session_time(db_iep_session* s, int32_t iters, int32_t profile,
+                                           double* ms, db_kernel_times_t* kt);
 DYNBATCH_API void db_iep_session_free(db_iep_session* s);
 
 /* db_execute with a module kind; schedule NULL = device improved scheduler. */
@@ -110,6 +133,8 @@ DYNBATCH_API db_status db_moe_session_stats(db_moe_session* s, db_session_stats_
 DYNBATCH_API db_status db_moe_session_routing(db_moe_session* s, int32_t* ids, double* weights,
                                               int32_t* expert_offsets, int32_t* items);
 DYNBATCH_API db_status db_moe_session_run(db_moe_session* s, db_run** out);
+DYNBATCH_API db_status db_moe_session_time(db_moe_session* s, int32_t iters, int32_t profile,
+                                           double* ms, db_kernel_times_t* kt);
 DYNBATCH_API void db_moe_session_free(db_moe_session* s);
 
 /* db_moe_run with a precision (batched only). */

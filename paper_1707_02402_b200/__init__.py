@@ -77,6 +77,14 @@ class SessionStats(C.Structure):
                [("algorithmic_flops", C.c_double), ("algorithmic_bytes", C.c_double)]
 
 
+class KernelTimes(C.Structure):
+    _fields_ = [("ms", C.c_double * 8), ("launches", C.c_int64 * 8), ("flops", C.c_double * 8),
+                ("bytes", C.c_double * 8)]
+
+
+KERNEL_CLASSES = ["scheduler", "plan", "gather", "conv1x1|moe_gate_sort", "conv3x3_1|moe_gemm1",
+                  "conv3x3_2|moe_gemm2", "layout|combine", "dense_step"]
+
 LOG_FN = C.CFUNCTYPE(None, C.c_char_p, C.c_void_p)
 VP = C.c_void_p
 PVP = C.POINTER(C.c_void_p)
@@ -115,6 +123,13 @@ SIGNATURES = {
     # device extensions (dynbatch_device.h)
     "db_device_count": (C.c_int32, []),
     "db_device_open": (C.c_int32, [C.c_int32]),
+    "db_host_alloc": (VP, [C.c_int64]),
+    "db_host_free": (None, [VP]),
+    "db_batch_generate_range": (C.c_int32, [C.POINTER(WorkloadOpts), C.c_int64, C.c_int64, PVP]),
+    "db_iep_session_time": (C.c_int32, [VP, C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                        C.POINTER(KernelTimes)]),
+    "db_moe_session_time": (C.c_int32, [VP, C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                        C.POINTER(KernelTimes)]),
     "db_iep_session_create": (C.c_int32, [VP, C.c_int64, C.c_int64, C.c_uint64,
                                           C.POINTER(ModuleOpts), PVP]),
     "db_iep_session_set_schedule": (C.c_int32, [VP, VP]),
@@ -208,6 +223,16 @@ class Batch(_Handle):
                          depth, length, branch_prob, seed)
         h = C.c_void_p()
         check(lib().db_batch_generate(C.byref(o), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def generate_range(cls, first, last, kind="chain", batch=8, vocab=40, width=128, depth=4,
+                       length=16, branch_prob=0.1, seed=0):
+        """Programs [first, last) of generate(...), bit-identical to those rows."""
+        o = WorkloadOpts(WORKLOAD[kind] if isinstance(kind, str) else kind, batch, vocab, width,
+                         depth, length, branch_prob, seed)
+        h = C.c_void_p()
+        check(lib().db_batch_generate_range(C.byref(o), first, last, C.byref(h)))
         return cls(h)
 
     @classmethod
@@ -322,6 +347,7 @@ def verify_run(seeds=6, batch=6, vocab=9, length=10, width=8, seed=0, parallel=F
 class IepSession(_Handle):
     """Device-resident IEP batch: forward = device scheduler + step kernels."""
     _free = "db_iep_session_free"
+    _time = "db_iep_session_time"
 
     def __init__(self, batch: Batch, module_seed: int, module_kind=MODULE_DENSE, first=0, last=0):
         h = C.c_void_p()
@@ -329,6 +355,15 @@ class IepSession(_Handle):
         check(lib().db_iep_session_create(batch.h, first, last, module_seed, C.byref(opts),
                                           C.byref(h)))
         super().__init__(h)
+
+    def time(self, iters: int, profile: bool = False):
+        """Device ms of `iters` forwards (CUDA events on the session stream)
+        and, with profile, per-kernel-class times."""
+        ms = C.c_double()
+        kt = KernelTimes()
+        check(getattr(lib(), self._time)(self.h, iters, 1 if profile else 0, C.byref(ms),
+                                         C.byref(kt)))
+        return ms.value, kt
 
     def set_schedule(self, schedule):
         check(lib().db_iep_session_set_schedule(self.h, schedule.h if schedule else None))
@@ -369,6 +404,7 @@ class IepSession(_Handle):
 
 class MoeSession(_Handle):
     _free = "db_moe_session_free"
+    _time = "db_moe_session_time"
 
     def __init__(self, experts, k, batch, data_dim, hidden, seed=0, precision=MOE_BF16, first=0,
                  last=0):
@@ -381,6 +417,15 @@ class MoeSession(_Handle):
 
     def forward(self):
         check(lib().db_moe_session_forward(self.h))
+
+    def time(self, iters: int, profile: bool = False):
+        """Device ms of `iters` forwards (CUDA events on the session stream)
+        and, with profile, per-kernel-class times."""
+        ms = C.c_double()
+        kt = KernelTimes()
+        check(getattr(lib(), self._time)(self.h, iters, 1 if profile else 0, C.byref(ms),
+                                         C.byref(kt)))
+        return ms.value, kt
 
     def forward_host(self, inputs, scores, outputs):
         check(lib().db_moe_session_forward_host(self.h, _ptr(inputs), _ptr(scores), _ptr(outputs)))
@@ -417,3 +462,25 @@ def device_count() -> int:
 
 def device_open(device: int):
     check(lib().db_device_open(device))
+
+
+class PinnedArray:
+    """numpy view of page-locked host memory from db_host_alloc."""
+
+    def __init__(self, shape, dtype=np.float32):
+        dtype = np.dtype(dtype)
+        n = int(np.prod(shape)) * dtype.itemsize
+        self.ptr = lib().db_host_alloc(n)
+        if not self.ptr:
+            raise MemoryError("db_host_alloc failed")
+        buf = (C.c_char * n).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.array = None
+                lib().db_host_free(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass

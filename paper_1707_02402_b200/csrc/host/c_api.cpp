@@ -344,6 +344,71 @@ int32_t db_device_count(void) {
   return n;
 }
 
+void* db_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (bytes <= 0 || cudaHostAlloc(&p, static_cast<size_t>(bytes), cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    t_error = "cudaHostAlloc failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void db_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+db_status db_batch_generate_range(const db_workload_opts* opts, int64_t first, int64_t last, db_batch** out) {
+  if (!opts || !out) return null_arg();
+  return guarded([&] {
+    dynbatch::WorkloadSpec spec;
+    switch (opts->kind) {
+      case DB_WORKLOAD_BALANCED_TREE: spec.kind = dynbatch::WorkloadKind::balanced_tree; break;
+      case DB_WORKLOAD_CHAIN_HEAVY: spec.kind = dynbatch::WorkloadKind::chain_heavy; break;
+      case DB_WORKLOAD_RANDOM_DAG: spec.kind = dynbatch::WorkloadKind::random_dag; break;
+      default: dynbatch::throw_error(Errc::invalid_argument, "unknown workload kind");
+    }
+    spec.b = opts->batch;
+    spec.p = opts->vocab;
+    spec.width = opts->width;
+    spec.depth = opts->depth;
+    spec.length = opts->length;
+    spec.branch_prob = opts->branch_prob;
+    spec.seed = opts->seed;
+    dynbatch::GeneratedBatch g = dynbatch::gen_batch_range(spec, first, last);
+    *out = new db_batch{std::move(g.vocab), std::move(g.programs), std::move(g.inputs)};
+  });
+}
+
+static void copy_times(const dynbatch::dev::KernelTimes& k, db_kernel_times_t* out) {
+  for (int c = 0; c < 8; ++c) {
+    out->ms[c] = k.ms[c];
+    out->launches[c] = k.launches[c];
+    out->flops[c] = k.flops[c];
+    out->bytes[c] = k.bytes[c];
+  }
+}
+
+db_status db_iep_session_time(db_iep_session* s, int32_t iters, int32_t profile, double* ms,
+                              db_kernel_times_t* kt) {
+  if (!s || !ms) return null_arg();
+  return guarded([&] {
+    dynbatch::dev::KernelTimes k;
+    *ms = s->s->time_forwards(iters, profile != 0, &k);
+    if (kt) copy_times(k, kt);
+  });
+}
+
+db_status db_moe_session_time(db_moe_session* s, int32_t iters, int32_t profile, double* ms,
+                              db_kernel_times_t* kt) {
+  if (!s || !ms) return null_arg();
+  return guarded([&] {
+    dynbatch::dev::KernelTimes k;
+    *ms = s->s->time_forwards(iters, profile != 0, &k);
+    if (kt) copy_times(k, kt);
+  });
+}
+
 db_status db_device_open(int32_t device) {
   return guarded([&] {
     dynbatch::dev::check(cudaSetDevice(device), "cudaSetDevice");

@@ -50,6 +50,49 @@ int sm_count() {
   return g_sm_count;
 }
 
+// --------------------------------------------------------------- Profiler
+Profiler::~Profiler() {
+  for (cudaEvent_t e : pool_) cudaEventDestroy(e);
+}
+
+cudaEvent_t Profiler::next_event() {
+  if (used_ == pool_.size()) {
+    cudaEvent_t e;
+    check(cudaEventCreate(&e), "cudaEventCreate");
+    pool_.push_back(e);
+  }
+  return pool_[used_++];
+}
+
+void Profiler::begin(int cls, cudaStream_t s) {
+  if (!on) return;
+  Rec r{cls, next_event(), next_event()};
+  check(cudaEventRecord(r.a, s), "event");
+  recs_.push_back(r);
+}
+
+void Profiler::end(cudaStream_t s) {
+  if (!on) return;
+  check(cudaEventRecord(recs_.back().b, s), "event");
+}
+
+KernelTimes Profiler::collect() {
+  KernelTimes kt;
+  for (const Rec& r : recs_) {
+    float ms = 0.f;
+    check(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+    kt.ms[r.cls] += ms;
+    ++kt.launches[r.cls];
+  }
+  for (int c = 0; c < 8; ++c) {
+    kt.flops[c] = work_flops_[c];
+    kt.bytes[c] = work_bytes_[c];
+    work_flops_[c] = work_bytes_[c] = 0.0;
+  }
+  reset();
+  return kt;
+}
+
 HostCSR make_csr(std::span<const Program> programs, const FunctionVocab& vocab) {
   HostCSR c;
   c.b = static_cast<std::int64_t>(programs.size());
@@ -272,22 +315,75 @@ void IepSession::forward() {
   check(cudaMemsetAsync(err_.get(), 0, sizeof(std::int32_t) * 4, stream_), "memset err");
   check(cudaMemsetAsync(present_.get(), 0, present_.size() * sizeof(std::int32_t), stream_), "memset present");
   if (!host_schedule_) {
+    prof_.begin(0, stream_);
     batch_->run_scheduler(stream_);
+    prof_.end(stream_);
     launches_ += 4;  // labels, histogram, scan, scatter
   }
   if (kind_ == ModuleKind::dense) forward_dense(); else forward_resblock();
+  if (prof_.on) add_forward_work();
+}
+
+// Algorithmic work per kernel class of one forward: FLOPs are
+// 2·MAC of the module contractions; bytes are the minimum HBM traffic of
+// each kernel (operands read once, results written once).
+void IepSession::add_forward_work() {
+  const HostCSR& c = batch_->csr();
+  double n_un = 0, n_bin = 0, dense_flops = 0, dense_bytes = 0;
+  for (std::int64_t g = 0; g < c.N; ++g) {
+    const int a = c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])];
+    if (a == 1) n_un += 1;
+    if (a == 2) n_bin += 1;
+    if (a > 0) {
+      dense_flops += 2.0 * a * width_ * static_cast<double>(width_);
+      dense_bytes += 8.0 * (a + 1) * width_;
+    }
+  }
+  if (kind_ == ModuleKind::dense) {
+    prof_.add_work(7, dense_flops, dense_bytes);
+    return;
+  }
+  const double map32 = 100352.0, stage16 = 225.0 * 16 * 16;  // fp32 node map, bf16 staged image
+  const double n_exp = n_un + n_bin;
+  prof_.add_work(2, 0.0, n_un * (map32 + stage16) + n_bin * (2 * map32 + 2 * stage16));
+  prof_.add_work(3, n_bin * 12845056.0, n_bin * (2 * stage16 + stage16 + map32));
+  prof_.add_work(4, n_exp * 57802752.0, n_exp * 2 * stage16);
+  prof_.add_work(5, n_exp * 57802752.0, n_exp * (stage16 + 2 * map32));
+}
+
+double IepSession::time_forwards(int iters, bool profile, KernelTimes* kt) {
+  synchronize();
+  prof_.on = profile;
+  prof_.reset();
+  cudaEvent_t a, b;
+  check(cudaEventCreate(&a), "event");
+  check(cudaEventCreate(&b), "event");
+  check(cudaEventRecord(a, stream_), "event");
+  for (int i = 0; i < iters; ++i) forward();
+  check(cudaEventRecord(b, stream_), "event");
+  check(cudaEventSynchronize(b), "event sync");
+  float ms = 0.f;
+  check(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  check_errors();
+  if (profile && kt) *kt = prof_.collect();
+  prof_.on = false;
+  return ms;
 }
 
 void IepSession::forward_dense() {
   const HostCSR& c = batch_->csr();
   const int blocks = std::min<std::int64_t>(std::max<std::int64_t>(1, (c.N + 7) / 8), sm_count() * 16);
   for (int st = 0; st < batch_->steps; ++st) {
+    prof_.begin(7, stream_);
     check(dbk_dense_step(st, width_, batch_->step_group_begin.get(), batch_->group_fid.get(),
                          batch_->group_begin.get(), batch_->member_g.get(), batch_->arity_of.get(),
                          batch_->child_off.get(), batch_->child_list.get(), batch_->example.get(),
                          in64_.get(), values64_.get(), present_.get(), wtab_.get(), btab_.get(),
                          err_.get(), std::max(1, c.max_arity), blocks, stream_),
           "dbk_dense_step");
+    prof_.end(stream_);
     ++launches_;
   }
   check(dbk_dense_gather_roots(c.b, width_, batch_->root_g.get(), present_.get(),

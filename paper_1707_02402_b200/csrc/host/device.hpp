@@ -69,6 +69,35 @@ class Buf {
   size_t n_ = 0;
 };
 
+// Per-kernel-class timing with CUDA events around launches (mirrors
+// db_kernel_times_t). Events are pooled; results are read after a sync.
+struct KernelTimes {
+  double ms[8] = {};
+  std::int64_t launches[8] = {};
+  double flops[8] = {};
+  double bytes[8] = {};
+};
+
+class Profiler {
+ public:
+  ~Profiler();
+  bool on = false;
+  void reset() { recs_.clear(); used_ = 0; }
+  void begin(int cls, cudaStream_t s);
+  void end(cudaStream_t s);
+  void add_work(int cls, double flops, double bytes) { work_flops_[cls] += flops; work_bytes_[cls] += bytes; }
+  KernelTimes collect();
+
+ private:
+  cudaEvent_t next_event();
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs_;
+  std::vector<cudaEvent_t> pool_;
+  size_t used_ = 0;
+  double work_flops_[8] = {};
+  double work_bytes_[8] = {};
+};
+
 // Batch in CSR form (global node g = prog_off[e] + local id).
 struct HostCSR {
   std::int64_t b = 0, N = 0;
@@ -130,6 +159,7 @@ class IepSession {
   ModuleKind kind() const { return kind_; }
   std::int64_t h2d_bytes() const;
   std::int64_t d2h_bytes() const;
+  double time_forwards(int iters, bool profile, KernelTimes* kt);
 
  private:
   void forward_dense();
@@ -155,8 +185,8 @@ class IepSession {
   // resblock
   struct RB;
   std::unique_ptr<RB> rb_;
-  std::vector<cudaEvent_t> step_events_;
-  float total_ms_ = 0.f;
+  Profiler prof_;
+  void add_forward_work();
 };
 
 // MoE session (fp64 reference order or bf16 tensor-core grouped GEMMs).
@@ -178,6 +208,8 @@ class MoeSession {
   std::int64_t tokens() const { return T_; }
   std::int64_t h2d_bytes() const;
   std::int64_t d2h_bytes() const;
+  double time_forwards(int iters, bool profile, KernelTimes* kt);
+  Profiler prof_;
 
  private:
   struct Impl;

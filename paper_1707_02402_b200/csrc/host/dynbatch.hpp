@@ -394,6 +394,7 @@ struct GeneratedBatch {
   TensorBatch inputs;
 };
 GeneratedBatch gen_batch(const WorkloadSpec& spec);
+GeneratedBatch gen_batch_range(const WorkloadSpec& spec, std::int64_t first, std::int64_t last);
 TensorBatch random_batch(std::int64_t rows, std::int64_t width, std::uint64_t seed);
 
 struct MoeWorkload {

@@ -11,7 +11,6 @@
 namespace dynbatch::dev {
 
 IepSession::~IepSession() {
-  for (cudaEvent_t e : step_events_) cudaEventDestroy(e);
   if (stream_) {
     cudaStreamSynchronize(stream_);
     cudaStreamDestroy(stream_);
@@ -139,41 +138,53 @@ void IepSession::forward_resblock() {
   const int S = B.steps;
   if (S == 0) return;
   const int sms = sm_count();
-  check(dbk_rb_plan(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
+  prof_.begin(1, stream_);
+    check(dbk_rb_plan(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
                     R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(), R.step_tile_begin.get(),
                     R.step_bintile_begin.get(), R.step_positions.get(), R.tile_group.get(), R.tile_q0.get(),
                     R.bin_group.get(), R.bin_q0.get(), stream_),
         "dbk_rb_plan");
+    prof_.end(stream_);
   launches_ += 2;
   const int gather_blocks = static_cast<int>(std::min<std::int64_t>(std::max<std::int64_t>(R.n_expensive, 1), sms * 8));
   for (int s = 0; s < S; ++s) {
+    prof_.begin(2, stream_);
     check(dbk_rb_gather(s, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), R.seg_start.get(),
                         B.member_g.get(), B.arity_of.get(), B.fid.get(), B.child0.get(), B.child1.get(),
                         B.example.get(), R.inputs.get(), R.values.get(), R.stage_x.get(), R.stage_cat.get(),
                         R.plane_stride, gather_blocks, stream_),
           "dbk_rb_gather");
+    prof_.end(stream_);
     // conv1x1 over the binary groups' [x; y] → z (stage_x + parked fp32)
+    prof_.begin(3, stream_);
     check(dbk_rb_conv(0, s, R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.example.get(), R.stage_cat.get(), R.stage_x.get(), R.plane_stride,
                       R.inputs.get(), R.values.get(), R.w0tab.get(), R.b0tab.get(), sms, stream_),
           "conv1x1");
+    prof_.end(stream_);
+    prof_.begin(4, stream_);
     check(dbk_rb_conv(1, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.example.get(), R.stage_x.get(), R.stage_mid.get(), R.plane_stride,
                       R.inputs.get(), R.values.get(), R.w1tab.get(), R.b1tab.get(), sms, stream_),
           "conv3x3 #1");
+    prof_.end(stream_);
+    prof_.begin(5, stream_);
     check(dbk_rb_conv(2, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.example.get(), R.stage_mid.get(), nullptr, R.plane_stride,
                       R.inputs.get(), R.values.get(), R.w2tab.get(), R.b2tab.get(), sms, stream_),
           "conv3x3 #2");
+    prof_.end(stream_);
     launches_ += 4;
   }
   const HostCSR& c = B.csr();
-  check(dbk_rb_outputs_to_chw(c.b, B.root_g.get(), B.fid.get(), B.arity_of.get(), B.example.get(), R.inputs.get(),
+  prof_.begin(6, stream_);
+    check(dbk_rb_outputs_to_chw(c.b, B.root_g.get(), B.fid.get(), B.arity_of.get(), B.example.get(), R.inputs.get(),
                               R.values.get(), R.chw_out.get(), stream_),
         "outputs layout");
+    prof_.end(stream_);
   launches_ += 1;
 }
 

@@ -12,7 +12,7 @@ MoeBf16::MoeBf16(const MoeConfig&, std::int64_t, std::uint64_t, cudaStream_t) {
 }
 MoeBf16::~MoeBf16() = default;
 void MoeBf16::upload_inputs(const float*, cudaStream_t) {}
-int MoeBf16::forward(const std::int32_t*, const double*, const std::int32_t*, const std::int32_t*, cudaStream_t) { return 0; }
+int MoeBf16::forward(const std::int32_t*, const double*, const std::int32_t*, const std::int32_t*, cudaStream_t, Profiler*) { return 0; }
 void MoeBf16::download_outputs(float*, cudaStream_t) {}
 
 }  // namespace dynbatch::dev

@@ -6,7 +6,7 @@
 #include <cstdint>
 #include <memory>
 
-#include "dynbatch.hpp"
+#include "device.hpp"
 
 namespace dynbatch::dev {
 
@@ -17,7 +17,7 @@ class MoeBf16 {
   void upload_inputs(const float* x, cudaStream_t s);
   // Dispatch → GEMM1+ReLU → GEMM2 → combine; returns kernels launched.
   int forward(const std::int32_t* ids, const double* wts, const std::int32_t* order,
-              const std::int32_t* offsets, cudaStream_t s);
+              const std::int32_t* offsets, cudaStream_t s, Profiler* prof);
   void download_outputs(float* out, cudaStream_t s);
 
  private:

@@ -168,16 +168,56 @@ MoeSession::~MoeSession() {
 void MoeSession::forward() {
   MoeDev& D = impl_->dev;
   launches_ = 0;
+  prof_.begin(3, stream_);
   D.gate(stream_);
   D.sort(stream_);
+  prof_.end(stream_);
   launches_ += 1 + 3;
   if (impl_->precision == 0) {
+    prof_.begin(4, stream_);
     D.experts_fp64(stream_);
+    prof_.end(stream_);
+    prof_.begin(6, stream_);
     D.combine_fp64(stream_);
+    prof_.end(stream_);
     launches_ += 3 + 1;
   } else {
-    launches_ += impl_->bf16->forward(D.ids.get(), D.wts.get(), D.order.get(), D.offsets.get(), stream_);
+    launches_ += impl_->bf16->forward(D.ids.get(), D.wts.get(), D.order.get(), D.offsets.get(), stream_,
+                                      &prof_);
   }
+  if (prof_.on) {
+    const MoeConfig& c = impl_->cfg;
+    const double T = static_cast<double>(T_), k = static_cast<double>(c.active_per_example);
+    const double es = impl_->precision == 0 ? 8.0 : 2.0;
+    const double gemm = 2.0 * T * k * c.data_dim * static_cast<double>(c.hidden);
+    prof_.add_work(3, 0.0, T * c.experts * 8.0 + T * k * 12.0);
+    prof_.add_work(4, gemm, T * k * c.data_dim * es + c.experts * c.data_dim * static_cast<double>(c.hidden) * es +
+                                T * k * c.hidden * es);
+    prof_.add_work(5, gemm, T * k * c.hidden * es + c.experts * c.data_dim * static_cast<double>(c.hidden) * es +
+                                T * k * c.data_dim * 4.0);
+    prof_.add_work(6, 0.0, T * k * c.data_dim * 4.0 + T * c.data_dim * 4.0);
+  }
+}
+
+double MoeSession::time_forwards(int iters, bool profile, KernelTimes* kt) {
+  synchronize();
+  prof_.on = profile;
+  prof_.reset();
+  cudaEvent_t a, b;
+  check(cudaEventCreate(&a), "event");
+  check(cudaEventCreate(&b), "event");
+  check(cudaEventRecord(a, stream_), "event");
+  for (int i = 0; i < iters; ++i) forward();
+  check(cudaEventRecord(b, stream_), "event");
+  check(cudaEventSynchronize(b), "event sync");
+  float ms = 0.f;
+  check(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  synchronize();
+  if (profile && kt) *kt = prof_.collect();
+  prof_.on = false;
+  return ms;
 }
 
 void MoeSession::forward_host(const float* inputs, const double* scores, float* outputs) {
