@@ -237,6 +237,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
             }
           }
         }
+        if constexpr (KIND == 2) {
+          // Residual rows are fetched one 32-channel chunk ahead of the TMEM
+          // loads so the epilogue keeps 8 independent 16-byte loads in flight
+          // (the residual may alias the destination for binary modules, so
+          // every chunk is fully loaded before any of its stores).
+          const float* rbase = valid ? res + px * 8 : nullptr;
+          float* dbase = valid ? dst32 + px * 8 : nullptr;
+          float4 rcur[8], rnext[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) rcur[i] = rnext[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid) {
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp) {
+              rcur[2 * pp] = *reinterpret_cast<const float4*>(rbase + pp * kPx * 8);
+              rcur[2 * pp + 1] = *reinterpret_cast<const float4*>(rbase + pp * kPx * 8 + 4);
+            }
+          }
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            float v[32];
+            tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * 256 + a * 128 + cb * 32, v);
+            if (valid && cb < 3) {
+#pragma unroll
+              for (int pp = 0; pp < 4; ++pp) {
+                const float* rp = rbase + ((cb + 1) * 4 + pp) * kPx * 8;
+                rnext[2 * pp] = *reinterpret_cast<const float4*>(rp);
+                rnext[2 * pp + 1] = *reinterpret_cast<const float4*>(rp + 4);
+              }
+            }
+            if (valid) {
+#pragma unroll
+              for (int pp = 0; pp < 4; ++pp) {
+                const int plane = cb * 4 + pp;
+                const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias + plane * 8));
+                const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias + plane * 8 + 4));
+                const float4 r0 = rcur[2 * pp], r1 = rcur[2 * pp + 1];
+                const float4 o0 = make_float4(fmaxf(v[pp * 8 + 0] + b_lo.x + r0.x, 0.f),
+                                              fmaxf(v[pp * 8 + 1] + b_lo.y + r0.y, 0.f),
+                                              fmaxf(v[pp * 8 + 2] + b_lo.z + r0.z, 0.f),
+                                              fmaxf(v[pp * 8 + 3] + b_lo.w + r0.w, 0.f));
+                const float4 o1 = make_float4(fmaxf(v[pp * 8 + 4] + b_hi.x + r1.x, 0.f),
+                                              fmaxf(v[pp * 8 + 5] + b_hi.y + r1.y, 0.f),
+                                              fmaxf(v[pp * 8 + 6] + b_hi.z + r1.z, 0.f),
+                                              fmaxf(v[pp * 8 + 7] + b_hi.w + r1.w, 0.f));
+                float* dp = dbase + plane * kPx * 8;
+                *reinterpret_cast<float4*>(dp) = o0;
+                *reinterpret_cast<float4*>(dp + 4) = o1;
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) rcur[i] = rnext[i];
+          }
+          continue;
+        }
         uint8_t* out16 = reinterpret_cast<uint8_t*>(P.stage_out) + static_cast<int64_t>(kGuard + q) * 16;
 #pragma unroll 1
         for (int cb = 0; cb < 4; ++cb) {
