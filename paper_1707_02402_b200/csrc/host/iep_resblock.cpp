@@ -29,28 +29,27 @@ std::uint16_t to_bf16(double v) {
   return static_cast<std::uint16_t>(u >> 16);
 }
 
-// One 32 KB B stage per (tap | K-half): element (n = co, k = ci) of the
-// N=128 × K=128 block at ((k/8)·128 + n)·8 + k%8 (K-major, no swizzle).
-std::vector<std::uint16_t> pack_conv3(const std::vector<double>& w, int C) {
-  std::vector<std::uint16_t> out(static_cast<size_t>(9) * C * C);
-  for (int tap = 0; tap < 9; ++tap)
-    for (int ci = 0; ci < C; ++ci)
+// Weights are streamed as 16 KB blocks, one per (64-channel K chunk, tap) in
+// that order (rb_conv.cu); element (n = co, k = ci mod 64) of a block sits at
+// ((k/8)·128 + n)·8 + k%8 (K-major, no swizzle).
+constexpr int kKChunk = 64;
+
+std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int cin, int taps) {
+  std::vector<std::uint16_t> out(static_cast<size_t>(taps) * cin * C);
+  const size_t block = static_cast<size_t>(kKChunk) * C;
+  for (int tap = 0; tap < taps; ++tap)
+    for (int ci = 0; ci < cin; ++ci) {
+      const int chunk = ci / kKChunk, k = ci % kKChunk;
+      const size_t base = static_cast<size_t>(chunk * taps + tap) * block;
       for (int co = 0; co < C; ++co)
-        out[static_cast<size_t>(tap) * C * C + (static_cast<size_t>(ci / 8) * C + co) * 8 + ci % 8] =
-            to_bf16(w[(static_cast<size_t>(tap) * C + ci) * C + co]);
+        out[base + (static_cast<size_t>(k / 8) * C + co) * 8 + k % 8] =
+            to_bf16(w[(static_cast<size_t>(tap) * cin + ci) * C + co]);
+    }
   return out;
 }
 
-std::vector<std::uint16_t> pack_conv1(const std::vector<double>& w, int C) {
-  std::vector<std::uint16_t> out(static_cast<size_t>(2) * C * C);
-  for (int ci = 0; ci < 2 * C; ++ci) {
-    const int kb = ci / C, k = ci % C;
-    for (int co = 0; co < C; ++co)
-      out[static_cast<size_t>(kb) * C * C + (static_cast<size_t>(k / 8) * C + co) * 8 + k % 8] =
-          to_bf16(w[static_cast<size_t>(ci) * C + co]);
-  }
-  return out;
-}
+std::vector<std::uint16_t> pack_conv3(const std::vector<double>& w, int C) { return pack_blocks(w, C, C, 9); }
+std::vector<std::uint16_t> pack_conv1(const std::vector<double>& w, int C) { return pack_blocks(w, C, 2 * C, 1); }
 
 }  // namespace
 

@@ -51,18 +51,24 @@ constexpr int kPx = 196;             // 14 × 14
 constexpr int kFmap = kPlanes * kPx * 8;  // 25,088 floats per node map
 constexpr int kGuard = 32;           // zero positions before position 0
 constexpr int kTileM = 256;          // positions per CTA tile (2 accumulators)
-constexpr int kBStage = 128 * 128 * 2;  // 32 KB: N=128 × K=128 bf16
+constexpr int kChunkPlanes = 8;      // K chunk = 64 input channels = 8 planes
+constexpr int kBStage = 128 * 64 * 2;  // 16 KB: N=128 × K=64 bf16 weight block
+constexpr int kASlots = 2;           // A window double-buffered per K chunk
 constexpr int kThreads = 192;
 
+// K is streamed in 64-channel chunks: for each chunk the producer loads one
+// A slot (8 planes × the position window) and then one 16 KB weight block
+// per tap; the MMA warp consumes (chunk, tap) blocks in that order, so the
+// next chunk's (or next tile's) window loads while the current one computes.
 template <int KIND>
 struct Cfg;
 template <>
 struct Cfg<0> {  // conv1x1 over [x; y] (256 → 128)
-  static constexpr int kInPlanes = 32, kHalo = 0, kKB = 2, kStages = 2;
+  static constexpr int kChunks = 4, kTaps = 1, kHalo = 0, kBStages = 6;
 };
 template <>
 struct Cfg<1> {  // conv3x3 #1 (128 → 128)
-  static constexpr int kInPlanes = 16, kHalo = 16, kKB = 9, kStages = 4;
+  static constexpr int kChunks = 2, kTaps = 9, kHalo = 16, kBStages = 8;
 };
 template <>
 struct Cfg<2> : Cfg<1> {};  // conv3x3 #2 + residual
@@ -70,10 +76,10 @@ struct Cfg<2> : Cfg<1> {};  // conv3x3 #2 + residual
 template <int KIND>
 constexpr int win() { return kTileM + 2 * Cfg<KIND>::kHalo; }
 template <int KIND>
-constexpr int a_bytes() { return Cfg<KIND>::kInPlanes * win<KIND>() * 16; }
+constexpr int a_slot_bytes() { return kChunkPlanes * win<KIND>() * 16; }
 template <int KIND>
 constexpr int smem_bytes() {
-  return a_bytes<KIND>() + Cfg<KIND>::kStages * kBStage + 256;
+  return kASlots * a_slot_bytes<KIND>() + Cfg<KIND>::kBStages * kBStage + 256;
 }
 
 struct ConvParams {
@@ -105,21 +111,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
   constexpr uint32_t IDESC = idesc_bf16_f32(128, 128);
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
-  uint8_t* sB = smem + a_bytes<KIND>();
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + K::kStages * kBStage);
+  uint8_t* sB = smem + kASlots * a_slot_bytes<KIND>();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + K::kBStages * kBStage);
   uint64_t* a_full = bars;
-  uint64_t* a_empty = bars + 1;
-  uint64_t* b_full = bars + 2;
-  uint64_t* b_empty = b_full + K::kStages;
-  uint64_t* acc_full = b_empty + K::kStages;
+  uint64_t* a_empty = a_full + kASlots;
+  uint64_t* b_full = a_empty + kASlots;
+  uint64_t* b_empty = b_full + K::kBStages;
+  uint64_t* acc_full = b_empty + K::kBStages;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(a_full, 1);
-    mbar_init(a_empty, 1);
-    for (int s = 0; s < K::kStages; ++s) {
+    for (int s = 0; s < kASlots; ++s) {
+      mbar_init(a_full + s, 1);
+      mbar_init(a_empty + s, 1);
+    }
+    for (int s = 0; s < K::kBStages; ++s) {
       mbar_init(b_full + s, 1);
       mbar_init(b_empty + s, 1);
     }
@@ -140,60 +148,64 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------ producer
-      uint32_t kbi = 0;
-      int it = 0;
-      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      uint32_t ai = 0, bi = 0;
+      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int32_t g = P.tile_group[t_begin + t];
         const int32_t q0 = P.tile_q0[t_begin + t];
         const uint8_t* w = reinterpret_cast<const uint8_t*>(P.wpack[P.group_fid[g]]);
-        mbar_wait(a_empty, (it & 1) ^ 1);
-        mbar_expect_tx(a_full, a_bytes<KIND>());
         const uint8_t* src = reinterpret_cast<const uint8_t*>(P.stage_in) +
                              static_cast<int64_t>(kGuard + q0 - K::kHalo) * 16;
-        for (int j = 0; j < K::kInPlanes; ++j) {
-          bulk_g2s(sA + j * WIN * 16, src + static_cast<int64_t>(j) * P.ps * 16, WIN * 16, a_full);
-        }
-        for (int kb = 0; kb < K::kKB; ++kb, ++kbi) {
-          const uint32_t s = kbi % K::kStages, ph = (kbi / K::kStages) & 1;
-          mbar_wait(b_empty + s, ph ^ 1);
-          mbar_expect_tx(b_full + s, kBStage);
-          bulk_g2s(sB + s * kBStage, w + static_cast<int64_t>(kb) * kBStage, kBStage, b_full + s);
+        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
+          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+          mbar_wait(a_empty + sa, pa ^ 1);
+          mbar_expect_tx(a_full + sa, a_slot_bytes<KIND>());
+          for (int j = 0; j < kChunkPlanes; ++j) {
+            bulk_g2s(sA + sa * a_slot_bytes<KIND>() + j * WIN * 16,
+                     src + static_cast<int64_t>(ch * kChunkPlanes + j) * P.ps * 16, WIN * 16, a_full + sa);
+          }
+          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
+            const uint32_t s = bi % K::kBStages, ph = (bi / K::kBStages) & 1;
+            mbar_wait(b_empty + s, ph ^ 1);
+            mbar_expect_tx(b_full + s, kBStage);
+            bulk_g2s(sB + s * kBStage, w + static_cast<int64_t>(ch * K::kTaps + tap) * kBStage, kBStage,
+                     b_full + s);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------------------------------- MMA issuer
-      uint32_t kbi = 0;
+      uint32_t ai = 0, bi = 0;
       int it = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
         const int abuf = it & 1;
         mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
-        mbar_wait(a_full, it & 1);
         tc_fence_after();
-        for (int kb = 0; kb < K::kKB; ++kb, ++kbi) {
-          const uint32_t s = kbi % K::kStages, ph = (kbi / K::kStages) & 1;
-          mbar_wait(b_full + s, ph);
+        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
+          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+          mbar_wait(a_full + sa, pa);
           tc_fence_after();
-          int shift = 0, plane0 = 0;
-          if (K::kKB == 9) {
-            shift = (kb / 3 - 1) * 15 + (kb % 3 - 1);
-          } else {
-            plane0 = kb * 16;
-          }
+          const uint32_t a_slot = a_base + sa * a_slot_bytes<KIND>();
+          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
+            const uint32_t s = bi % K::kBStages, ph = (bi / K::kBStages) & 1;
+            mbar_wait(b_full + s, ph);
+            tc_fence_after();
+            const int shift = K::kTaps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
 #pragma unroll
-          for (int a = 0; a < kTileM / 128; ++a) {
+            for (int a = 0; a < kTileM / 128; ++a) {
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t arow = static_cast<uint32_t>(K::kHalo + shift + a * 128);
-              const uint64_t ad = smem_desc(a_base + ((plane0 + 2 * kk) * WIN + arow) * 16, WIN * 16, 128);
-              const uint64_t bd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
-              mma_bf16(tmem_base + abuf * 256 + a * 128, ad, bd, IDESC, (kb | kk) != 0);
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t arow = static_cast<uint32_t>(K::kHalo + shift + a * 128);
+                const uint64_t ad = smem_desc(a_slot + ((2 * kk) * WIN + arow) * 16, WIN * 16, 128);
+                const uint64_t bd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
+                mma_bf16(tmem_base + abuf * 256 + a * 128, ad, bd, IDESC, (ch | tap | kk) != 0);
+              }
             }
+            mma_commit(b_empty + s);
           }
-          mma_commit(b_empty + s);
+          mma_commit(a_empty + sa);
         }
-        mma_commit(a_empty);
         mma_commit(acc_full + abuf);
       }
     }
