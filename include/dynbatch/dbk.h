@@ -73,25 +73,30 @@ int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t*
                 const int32_t* group_begin, const int32_t* arity_of, int32_t* seg_start,
                 int32_t* group_tile0, int32_t* group_bintile0, int32_t* step_tile_begin,
                 int32_t* step_bintile_begin, int32_t* step_positions, int32_t* tile_group,
-                int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, void* stream);
-/* Gather (+ fused channel concat for binary groups) of step `step` into the
- * bf16 staging planes; plane_stride in positions. */
+                int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, int64_t n_nodes,
+                const int32_t* member_g, const int32_t* child0, const int32_t* child1,
+                const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, void* stream);
+/* Gather of the operands of step `step` that no child epilogue forwarded
+ * (leaves, shared children) into the bf16 staging planes, with the binary
+ * channel concat fused into the write; plane_stride in positions. */
 int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_fid,
                   const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
                   const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
-                  const int32_t* child1, const int32_t* example, const float* inputs,
-                  const float* values, void* stage_x, void* stage_cat, int64_t plane_stride,
-                  int32_t blocks, void* stream);
+                  const int32_t* child1, const int32_t* example, const int32_t* fwd_ok,
+                  const float* inputs, const float* values, void* stage_x, void* stage_cat,
+                  int64_t plane_stride, int32_t blocks, void* stream);
 /* tcgen05 implicit-GEMM convolutions: kind 0 = conv1x1 over [x; y] → z
  * (bf16 staging + fp32 parked in the node slot), 1 = conv3x3 #1 → mid
- * (bf16), 2 = conv3x3 #2 + residual + ReLU → fp32 node values. */
+ * (bf16), 2 = conv3x3 #2 + residual + ReLU → fp32 node values (when a
+ * reader needs them) and the bf16 operand image of the parent's call. */
 int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
                 const int32_t* tile_group, const int32_t* tile_q0, const int32_t* group_fid,
                 const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
                 const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
                 const int32_t* example, const void* stage_in, void* stage_out,
                 int64_t plane_stride, const float* inputs, float* values,
-                const void* const* wpack, const float* const* bias, int32_t num_sms,
+                const void* const* wpack, const float* const* bias, const int32_t* fwd_pos,
+                const int32_t* fwd_slot, void* stage_x, void* stage_cat, int32_t num_sms,
                 void* stream);
 int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream);
 int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int32_t* fid,

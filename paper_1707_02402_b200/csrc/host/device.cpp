@@ -300,6 +300,7 @@ IepSession::IepSession(const FunctionVocab& vocab, std::span<const Program> prog
 
 
 void IepSession::set_schedule(const Schedule* schedule) {
+  layout_dirty_ = true;
   if (schedule) {
     batch_->load_schedule(*schedule, stream_);
     host_schedule_ = true;

@@ -22,7 +22,7 @@ struct IepSession::RB {
   Buf<const void*> w0tab, w1tab, w2tab;
   Buf<const float*> b0tab, b1tab, b2tab;
   Buf<std::int32_t> seg_start, group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
-      step_positions, tile_group, tile_q0, bin_group, bin_q0;
+      step_positions, tile_group, tile_q0, bin_group, bin_q0, fwd_ok, fwd_pos, fwd_slot;
   std::int64_t n_expensive = 0;
 };
 

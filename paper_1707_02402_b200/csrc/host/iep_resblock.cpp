@@ -73,8 +73,21 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   for (size_t i = 0; i < tmp.size(); ++i) tmp[i] = static_cast<float>(inputs.data()[i]);
   check(cudaMemcpyAsync(R.chw_in.get(), tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   check(dbk_rb_inputs_from_chw(c.b, R.chw_in.get(), R.inputs.get(), stream_), "inputs layout");
-  // staging: worst case every expensive node in one step, ≤ p groups per step
-  R.plane_stride = RB::kGuard + R.n_expensive * 225 + static_cast<std::int64_t>(c.p + 2) * RB::kTileM + 64;
+  // staging: every step owns its range (results are forwarded into their
+  // parent's operand image); ≤ one 256-position alignment gap per group
+  const std::int64_t max_groups = std::min<std::int64_t>(R.n_expensive, static_cast<std::int64_t>(std::max(1, c.s_max)) * c.p);
+  R.plane_stride = RB::kGuard + R.n_expensive * 225 + (max_groups + 2) * RB::kTileM + 64;
+  // forwarding eligibility: expensive nodes with exactly one parent
+  {
+    std::vector<std::int32_t> parents(static_cast<size_t>(N), 0), ok(static_cast<size_t>(N), 0);
+    for (std::int32_t ch : c.child_list) ++parents[static_cast<size_t>(ch)];
+    for (std::int64_t g = 0; g < c.N; ++g)
+      ok[static_cast<size_t>(g)] = c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0 &&
+                                   parents[static_cast<size_t>(g)] == 1;
+    R.fwd_ok.upload(ok, stream_);
+    R.fwd_pos.alloc(N);
+    R.fwd_slot.alloc(N);
+  }
   const size_t ps = static_cast<size_t>(R.plane_stride);
   R.stage_x.alloc(ps * 16 * 8);
   R.stage_cat.alloc(ps * 32 * 8);
@@ -91,7 +104,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   R.group_bintile0.alloc(std::max(G, N + 2));
   R.step_tile_begin.alloc(S);
   R.step_bintile_begin.alloc(S);
-  R.step_positions.alloc(S);
+  R.step_positions.alloc(S + 1);
   R.tile_group.alloc(T + N);
   R.tile_q0.alloc(T + N);
   R.bin_group.alloc(T + N);
@@ -137,20 +150,28 @@ void IepSession::forward_resblock() {
   const int S = B.steps;
   if (S == 0) return;
   const int sms = sm_count();
+  if (layout_dirty_) {  // a new image layout: pads / gaps must read as zeros
+    R.stage_x.zero(stream_);
+    R.stage_cat.zero(stream_);
+    R.stage_mid.zero(stream_);
+    layout_dirty_ = false;
+  }
   prof_.begin(1, stream_);
     check(dbk_rb_plan(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
                     R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(), R.step_tile_begin.get(),
                     R.step_bintile_begin.get(), R.step_positions.get(), R.tile_group.get(), R.tile_q0.get(),
-                    R.bin_group.get(), R.bin_q0.get(), stream_),
+                    R.bin_group.get(), R.bin_q0.get(), B.csr().N, B.member_g.get(), B.child0.get(),
+                    B.child1.get(), R.fwd_ok.get(), R.fwd_pos.get(), R.fwd_slot.get(), stream_),
         "dbk_rb_plan");
     prof_.end(stream_);
-  launches_ += 2;
+  launches_ += 4;
   const int gather_blocks = static_cast<int>(std::min<std::int64_t>(std::max<std::int64_t>(R.n_expensive, 1), sms * 8));
   for (int s = 0; s < S; ++s) {
     prof_.begin(2, stream_);
     check(dbk_rb_gather(s, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), R.seg_start.get(),
                         B.member_g.get(), B.arity_of.get(), B.fid.get(), B.child0.get(), B.child1.get(),
-                        B.example.get(), R.inputs.get(), R.values.get(), R.stage_x.get(), R.stage_cat.get(),
+                        B.example.get(), R.fwd_ok.get(), R.inputs.get(), R.values.get(), R.stage_x.get(),
+                        R.stage_cat.get(),
                         R.plane_stride, gather_blocks, stream_),
           "dbk_rb_gather");
     prof_.end(stream_);
@@ -159,21 +180,24 @@ void IepSession::forward_resblock() {
     check(dbk_rb_conv(0, s, R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.example.get(), R.stage_cat.get(), R.stage_x.get(), R.plane_stride,
-                      R.inputs.get(), R.values.get(), R.w0tab.get(), R.b0tab.get(), sms, stream_),
+                      R.inputs.get(), R.values.get(), R.w0tab.get(), R.b0tab.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.stage_x.get(),
+                      R.stage_cat.get(), sms, stream_),
           "conv1x1");
     prof_.end(stream_);
     prof_.begin(4, stream_);
     check(dbk_rb_conv(1, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.example.get(), R.stage_x.get(), R.stage_mid.get(), R.plane_stride,
-                      R.inputs.get(), R.values.get(), R.w1tab.get(), R.b1tab.get(), sms, stream_),
+                      R.inputs.get(), R.values.get(), R.w1tab.get(), R.b1tab.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.stage_x.get(),
+                      R.stage_cat.get(), sms, stream_),
           "conv3x3 #1");
     prof_.end(stream_);
     prof_.begin(5, stream_);
     check(dbk_rb_conv(2, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.example.get(), R.stage_mid.get(), nullptr, R.plane_stride,
-                      R.inputs.get(), R.values.get(), R.w2tab.get(), R.b2tab.get(), sms, stream_),
+                      R.inputs.get(), R.values.get(), R.w2tab.get(), R.b2tab.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.stage_x.get(),
+                      R.stage_cat.get(), sms, stream_),
           "conv3x3 #2");
     prof_.end(stream_);
     launches_ += 4;

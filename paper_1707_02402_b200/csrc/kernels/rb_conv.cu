@@ -102,6 +102,14 @@ struct ConvParams {
   float* values;
   const __nv_bfloat16* const* wpack;
   const float* const* bias;
+  // conv3x3 #2 only: forwarding of each result as the bf16 operand image of
+  // its (unique) parent's call — fwd_pos[g] = absolute staging position of
+  // the parent's image (-1: none), fwd_slot[g] = buffer (bit 0: 0 stage_x,
+  // 1 stage_cat) | first plane << 1 | keep-fp32-value << 8.
+  const int32_t* fwd_pos;
+  const int32_t* fwd_slot;
+  __nv_bfloat16* stage_x;
+  __nv_bfloat16* stage_cat;
 };
 
 template <int KIND>
@@ -256,6 +264,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
           // every chunk is fully loaded before any of its stores).
           const float* rbase = valid ? res + px * 8 : nullptr;
           float* dbase = valid ? dst32 + px * 8 : nullptr;
+          // forwarding target: the parent's bf16 operand image (if unique parent)
+          int32_t slot = 0;
+          uint8_t* fbase = nullptr;
+          if (valid) {
+            const int32_t tgt = P.fwd_pos[node];
+            slot = P.fwd_slot[node];
+            if (tgt >= 0) {
+              fbase = reinterpret_cast<uint8_t*>((slot & 1) ? P.stage_cat : P.stage_x) +
+                      (static_cast<int64_t>((slot >> 1) & 31) * P.ps + kGuard + tgt + rem) * 16;
+            }
+          }
+          const bool keep32 = (slot >> 8) & 1;
           float4 rcur[8], rnext[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) rcur[i] = rnext[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -293,9 +313,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
                                               fmaxf(v[pp * 8 + 5] + b_hi.y + r1.y, 0.f),
                                               fmaxf(v[pp * 8 + 6] + b_hi.z + r1.z, 0.f),
                                               fmaxf(v[pp * 8 + 7] + b_hi.w + r1.w, 0.f));
-                float* dp = dbase + plane * kPx * 8;
-                *reinterpret_cast<float4*>(dp) = o0;
-                *reinterpret_cast<float4*>(dp + 4) = o1;
+                if (keep32) {
+                  float* dp = dbase + plane * kPx * 8;
+                  *reinterpret_cast<float4*>(dp) = o0;
+                  *reinterpret_cast<float4*>(dp + 4) = o1;
+                }
+                if (fbase) {
+                  uint4 pk;
+                  pk.x = pack_bf16x2(o0.x, o0.y);
+                  pk.y = pack_bf16x2(o0.z, o0.w);
+                  pk.z = pack_bf16x2(o1.x, o1.y);
+                  pk.w = pack_bf16x2(o1.z, o1.w);
+                  *reinterpret_cast<uint4*>(fbase + static_cast<int64_t>(plane) * P.ps * 16) = pk;
+                }
               }
             }
 #pragma unroll
@@ -394,9 +424,59 @@ __global__ void k_rb_plan(int32_t n_steps, const int32_t* __restrict__ sgb,
   if (threadIdx.x == 0) {
     step_tile_begin[0] = 0;
     step_bintile_begin[0] = 0;
+    int32_t base = 0;
     for (int32_t s = 0; s < n_steps; ++s) {
       step_tile_begin[s + 1] += step_tile_begin[s];
       step_bintile_begin[s + 1] += step_bintile_begin[s];
+      const int32_t n = step_positions[s];
+      step_positions[s] = base;  // becomes the step's position origin
+      base += n;
+    }
+    step_positions[n_steps] = base;
+  }
+  __syncthreads();
+  // Every step owns its own staging range, so a result can be written
+  // straight into the operand image of its parent's (later) step.
+  for (int32_t s = threadIdx.x; s < n_steps; s += blockDim.x) {
+    const int32_t base = step_positions[s];
+    for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g)
+      if (seg_start[g] >= 0) seg_start[g] += base;
+  }
+}
+
+// Forwarding table for conv3x3 #2 epilogues: for every expensive member,
+// each child with a unique parent (fwd_ok) receives the absolute staging
+// position of that parent's image and which buffer / planes it fills.
+__global__ void k_rb_fwd_init(int64_t n, int32_t* __restrict__ fwd_pos, int32_t* __restrict__ fwd_slot) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) {
+    fwd_pos[i] = -1;
+    fwd_slot[i] = 1 << 8;  // keep the fp32 value (roots, shared children)
+  }
+}
+
+__global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const int32_t* __restrict__ group_fid,
+                         const int32_t* __restrict__ group_begin, const int32_t* __restrict__ arity_of,
+                         const int32_t* __restrict__ seg_start, const int32_t* __restrict__ member_g,
+                         const int32_t* __restrict__ child0, const int32_t* __restrict__ child1,
+                         const int32_t* __restrict__ fwd_ok, int32_t* __restrict__ fwd_pos,
+                         int32_t* __restrict__ fwd_slot) {
+  const int32_t s = blockIdx.x;
+  if (s >= n_steps) return;
+  for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
+    if (seg_start[g] < 0) continue;
+    const int32_t arity = arity_of[group_fid[g]];
+    const int32_t rows = group_begin[g + 1] - group_begin[g];
+    for (int32_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      const int32_t node = member_g[group_begin[g] + i];
+      for (int k = 0; k < arity; ++k) {
+        const int32_t c = k == 0 ? child0[node] : child1[node];
+        if (!fwd_ok[c]) continue;
+        fwd_pos[c] = seg_start[g] + i * kImg;
+        // unary parent: conv3x3 #2 of the parent reads the child's fp32 value
+        // as its residual, so keep it; binary parents use their own z.
+        fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1) | ((arity == 1 ? 1 : 0) << 8);
+      }
     }
   }
 }
@@ -429,61 +509,48 @@ __global__ void k_rb_tiles(int32_t n_steps, const int32_t* __restrict__ sgb,
 }
 
 // --------------------------------------------------------------- gather
-// Packs each expensive member's operand maps (fp32 plane maps of its
-// children; leaves read the example's input map) into the step's bf16
-// staging: unary → stage_x (16 planes), binary → stage_cat (32 planes: child
-// 0 then child 1, i.e. the channel concat of [x; y] fused into the gather).
-// Pads and the alignment gap after each group's last image are zero-filled.
+// Packs the operand maps that were NOT forwarded by a child's conv3x3 #2
+// epilogue — leaves (the example's input map) and children shared by
+// several parents — into the member's bf16 staging image: unary → stage_x
+// (16 planes), binary → stage_cat planes 16k.. (the channel concat of
+// [x; y] is fused into the write). Only the 196 data positions are written;
+// pads and alignment gaps were zeroed once at session creation.
 __global__ void __launch_bounds__(256) k_rb_gather(
     int32_t step, const int32_t* __restrict__ sgb, const int32_t* __restrict__ group_fid,
     const int32_t* __restrict__ group_begin, const int32_t* __restrict__ seg_start,
     const int32_t* __restrict__ member_g, const int32_t* __restrict__ arity_of,
     const int32_t* __restrict__ fid, const int32_t* __restrict__ child0,
     const int32_t* __restrict__ child1, const int32_t* __restrict__ example,
-    const float* __restrict__ inputs, const float* __restrict__ values,
-    uint8_t* __restrict__ stage_x, uint8_t* __restrict__ stage_cat, int64_t ps) {
+    const int32_t* __restrict__ fwd_ok, const float* __restrict__ inputs,
+    const float* __restrict__ values, uint8_t* __restrict__ stage_x, uint8_t* __restrict__ stage_cat,
+    int64_t ps) {
   const int32_t g_lo = sgb[step], g_hi = sgb[step + 1];
   const int32_t m_lo = group_begin[g_lo], m_hi = group_begin[g_hi];
   for (int32_t m = m_lo + blockIdx.x; m < m_hi; m += gridDim.x) {
     int32_t g = g_lo;
     while (group_begin[g + 1] <= m) ++g;
-    const int32_t f = group_fid[g];
-    const int32_t arity = arity_of[f];
+    const int32_t arity = arity_of[group_fid[g]];
     if (arity == 0 || seg_start[g] < 0) continue;
-    const int32_t img = m - group_begin[g];
-    const int32_t rows = group_begin[g + 1] - group_begin[g];
     const int32_t node = member_g[m];
-    const int32_t base = kGuard + seg_start[g] + img * kImg;
+    const int32_t base = kGuard + seg_start[g] + (m - group_begin[g]) * kImg;
     uint8_t* dst = arity == 2 ? stage_cat : stage_x;
-    const int planes = arity == 2 ? 32 : 16;
-    const float* src_map[2];
     for (int k = 0; k < arity; ++k) {
       const int32_t ch = k == 0 ? child0[node] : child1[node];
-      src_map[k] = arity_of[fid[ch]] == 0 ? inputs + static_cast<int64_t>(example[ch]) * kFmap
-                                          : values + static_cast<int64_t>(ch) * kFmap;
-    }
-    for (int idx = threadIdx.x; idx < planes * kImg; idx += blockDim.x) {
-      const int p = idx / kImg, rem = idx - p * kImg;
-      const int r = rem / 15, c = rem - r * 15;
-      uint4 pk = make_uint4(0, 0, 0, 0);
-      if (r < 14 && c < 14) {
-        const float* sp = src_map[p >> 4] + ((p & 15) * kPx + r * 14 + c) * 8;
+      if (fwd_ok[ch]) continue;  // written by the child's epilogue
+      const float* src = arity_of[fid[ch]] == 0 ? inputs + static_cast<int64_t>(example[ch]) * kFmap
+                                                : values + static_cast<int64_t>(ch) * kFmap;
+      for (int idx = threadIdx.x; idx < kPlanes * kPx; idx += blockDim.x) {
+        const int p = idx / kPx, px = idx - p * kPx;
+        const int r = px / 14, c = px - r * 14;
+        const float* sp = src + (p * kPx + px) * 8;
         const float4 lo = *reinterpret_cast<const float4*>(sp);
         const float4 hi = *reinterpret_cast<const float4*>(sp + 4);
+        uint4 pk;
         pk.x = pack_bf16x2(lo.x, lo.y);
         pk.y = pack_bf16x2(lo.z, lo.w);
         pk.z = pack_bf16x2(hi.x, hi.y);
         pk.w = pack_bf16x2(hi.z, hi.w);
-      }
-      *reinterpret_cast<uint4*>(dst + (static_cast<int64_t>(p) * ps + base + rem) * 16) = pk;
-    }
-    if (img == rows - 1) {  // zero the alignment gap after the group's last image
-      const int32_t gap0 = base + kImg;
-      const int32_t gap1 = kGuard + seg_start[g] + ((rows * kImg + kTileM - 1) / kTileM) * kTileM;
-      const int32_t gap = gap1 - gap0;
-      for (int idx = threadIdx.x; idx < planes * gap; idx += blockDim.x) {
-        const int p = idx / gap, q = gap0 + idx - p * gap;
-        *reinterpret_cast<uint4*>(dst + (static_cast<int64_t>(p) * ps + q) * 16) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dst + (static_cast<int64_t>(16 * k + p) * ps + base + r * 15 + c) * 16) = pk;
       }
     }
   }
@@ -541,7 +608,9 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
                            const int32_t* group_begin, const int32_t* arity_of, int32_t* seg_start,
                            int32_t* group_tile0, int32_t* group_bintile0, int32_t* step_tile_begin,
                            int32_t* step_bintile_begin, int32_t* step_positions, int32_t* tile_group,
-                           int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, void* stream) {
+                           int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, int64_t n_nodes,
+                           const int32_t* member_g, const int32_t* child0, const int32_t* child1,
+                           const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n_steps <= 0) return 0;
   k_rb_plan<<<1, 1024, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
@@ -550,18 +619,22 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
   k_rb_tiles<<<n_steps, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of,
                                      seg_start, group_tile0, group_bintile0, step_tile_begin,
                                      step_bintile_begin, tile_group, tile_q0, bin_group, bin_q0);
+  k_rb_fwd_init<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_nodes, fwd_pos, fwd_slot);
+  k_rb_fwd<<<n_steps, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
+                                   member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_fid,
                              const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
                              const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
-                             const int32_t* child1, const int32_t* example, const float* inputs,
-                             const float* values, void* stage_x, void* stage_cat, int64_t plane_stride,
-                             int32_t blocks, void* stream) {
+                             const int32_t* child1, const int32_t* example, const int32_t* fwd_ok,
+                             const float* inputs, const float* values, void* stage_x, void* stage_cat,
+                             int64_t plane_stride, int32_t blocks, void* stream) {
   k_rb_gather<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       step, step_group_begin, group_fid, group_begin, seg_start, member_g, arity_of, fid, child0, child1,
-      example, inputs, values, static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_cat), plane_stride);
+      example, fwd_ok, inputs, values, static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_cat),
+      plane_stride);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -571,12 +644,14 @@ extern "C" int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_
                            const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
                            const int32_t* example, const void* stage_in, void* stage_out,
                            int64_t plane_stride, const float* inputs, float* values,
-                           const void* const* wpack, const float* const* bias, int32_t num_sms,
+                           const void* const* wpack, const float* const* bias, const int32_t* fwd_pos,
+                           const int32_t* fwd_slot, void* stage_x, void* stage_cat, int32_t num_sms,
                            void* stream) {
   ConvParams p{step, step_tile_begin, tile_group, tile_q0, group_fid, group_begin, seg_start, member_g,
                arity_of, fid, child0, example, static_cast<const __nv_bfloat16*>(stage_in),
                static_cast<__nv_bfloat16*>(stage_out), plane_stride, inputs, values,
-               reinterpret_cast<const __nv_bfloat16* const*>(wpack), bias};
+               reinterpret_cast<const __nv_bfloat16* const*>(wpack), bias, fwd_pos, fwd_slot,
+               static_cast<__nv_bfloat16*>(stage_x), static_cast<__nv_bfloat16*>(stage_cat)};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (kind) {
     case 0: return launch_conv<0>(p, num_sms, s);
