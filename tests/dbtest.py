@@ -11,10 +11,10 @@ import paper_1707_02402_b200 as db
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def header_symbols():
+def header_symbols(headers=("dynbatch.h", "dynbatch_device.h")):
     """Every DYNBATCH_API function declared in include/dynbatch/*.h."""
     names = []
-    for h in ("dynbatch.h", "dynbatch_device.h"):
+    for h in headers:
         text = open(os.path.join(ROOT, "include", "dynbatch", h)).read()
         names += re.findall(r"DYNBATCH_API[^;]*?\b(db_\w+)\s*\(", text, re.S)
     return names
