@@ -84,20 +84,22 @@ class Dist:
 
 # --------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi samples of SM clock and throttle reasons during timing."""
+    """nvidia-smi samples (SM clock, throttle reasons) tagged with the driver's
+    own timestamps; summary() keeps the samples inside the timed window."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu):
-        self.gpu, self.rows, self.proc = gpu, [], None
+        self.gpu, self.rows, self.proc, self.window = gpu, [], None, None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -106,27 +108,44 @@ class ClockSampler:
         return self
 
     def _read(self):
+        import datetime
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                t = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                self.rows.append((t, float(f[1]), float(f[2]), f[4:8]))
+            except ValueError:
+                continue
 
-    def __exit__(self, *a):
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def stop(self):
         if self.proc:
+            time.sleep(0.2)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.thread.join(timeout=2)
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4)
-                          if r[3 + i].lower().startswith("active")})
-        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
-        return {"sm_mhz": statistics.median(loaded) if loaded else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        rows = self.rows
+        if self.window and rows:
+            t0, t1 = self.window
+            inside = [r for r in rows if t0 - 0.06 <= r[0] <= t1 + 0.06]
+            if not inside:  # window shorter than the sampling period: nearest sample
+                inside = [min(rows, key=lambda r: abs(r[0] - 0.5 * (t0 + t1)))]
+            rows = inside
+        sm = [r[1] for r in rows]
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4)
+                          if r[3][i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(r[2] for r in rows) if rows else None,
+                "reasons": reasons, "samples": len(rows)}
 
 
 def measured_peaks():
@@ -200,6 +219,7 @@ def run_ours(args, dist):
     N = max(1, dist.world)
     per = cfg["per_gpu"]
     db.device_open(dist.local)
+    clk = ClockSampler(dist.local).start()
     first, last = dist.rank * per, (dist.rank + 1) * per
     batch = db.Batch.generate_range(first, last, cfg["kind"], batch=per * N, vocab=cfg["vocab"],
                                     width=F, depth=cfg["depth"], length=cfg["length"],
@@ -211,10 +231,10 @@ def run_ours(args, dist):
     stats = sess.stats()
 
     dist.barrier()
-    with ClockSampler(dist.local) as clk:
-        dist.barrier()
-        ms, kt = sess.time(args.steps, profile=True)
-        dist.barrier()
+    t0 = time.time()
+    ms, kt = sess.time(args.steps, profile=True)
+    dist.barrier()
+    clk.mark(t0, time.time())
     ms_step = dist.max(ms / args.steps)
     value = per * N / (ms_step / 1e3)
 
@@ -270,7 +290,7 @@ def run_ours(args, dist):
                         "expensive_calls": stats.expensive_calls,
                         "peak_group_rows": stats.peak_group_rows},
            "algorithmic_flops_per_step": stats.algorithmic_flops * N,
-           "clocks": clk.summary()}
+           "clocks": None}
 
     # naive per-example execution on the GPU (same kernels, one node per step)
     try:
@@ -291,6 +311,8 @@ def run_ours(args, dist):
     except Exception as e:  # reported, not fatal
         out["naive_gpu"] = {"error": str(e)}
 
+    clk.stop()
+    out["clocks"] = clk.summary()
     if dist.rank == 0 and N == 1 and not args.no_cpu_baseline:
         threads, n = calibrate_cpu(cfg, args.cpu_seconds)
         dt, n = cpu_sample_run(cfg, n, threads)

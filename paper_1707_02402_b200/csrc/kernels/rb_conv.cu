@@ -54,7 +54,8 @@ constexpr int kTileM = 256;          // positions per CTA tile (2 accumulators)
 constexpr int kChunkPlanes = 8;      // K chunk = 64 input channels = 8 planes
 constexpr int kBStage = 128 * 64 * 2;  // 16 KB: N=128 × K=64 bf16 weight block
 constexpr int kASlots = 2;           // A window double-buffered per K chunk
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;       // two warps per TMEM lane quarter, two column chunks each
+constexpr int kThreads = 64 + kEpiWarps * 32;
 
 // K is streamed in 64-channel chunks: for each chunk the producer loads one
 // A slot (8 planes × the position window) and then one 16 KB weight block
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, 128);
+      mbar_init(acc_empty + s, kEpiWarps * 32);
     }
     fence_barrier_init();
   }
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
     }
   } else {  // ------------------------------------------------------ epilogue
     const int quarter = warp & 3;
+    const int cb0 = ((warp - 2) >> 2) * 2;  // this warp's first 32-column chunk
     int it = 0;
     for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
       const int abuf = it & 1;
@@ -282,15 +284,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
           if (valid) {
 #pragma unroll
             for (int pp = 0; pp < 4; ++pp) {
-              rcur[2 * pp] = *reinterpret_cast<const float4*>(rbase + pp * kPx * 8);
-              rcur[2 * pp + 1] = *reinterpret_cast<const float4*>(rbase + pp * kPx * 8 + 4);
+              rcur[2 * pp] = *reinterpret_cast<const float4*>(rbase + (cb0 * 4 + pp) * kPx * 8);
+              rcur[2 * pp + 1] = *reinterpret_cast<const float4*>(rbase + (cb0 * 4 + pp) * kPx * 8 + 4);
             }
           }
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) {
+          for (int cbi = 0; cbi < 2; ++cbi) {
+            const int cb = cb0 + cbi;
             float v[32];
             tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * 256 + a * 128 + cb * 32, v);
-            if (valid && cb < 3) {
+            if (valid && cbi == 0) {
 #pragma unroll
               for (int pp = 0; pp < 4; ++pp) {
                 const float* rp = rbase + ((cb + 1) * 4 + pp) * kPx * 8;
@@ -335,7 +338,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
         }
         uint8_t* out16 = reinterpret_cast<uint8_t*>(P.stage_out) + static_cast<int64_t>(kGuard + q) * 16;
 #pragma unroll 1
-        for (int cb = 0; cb < 4; ++cb) {
+        for (int cbi = 0; cbi < 2; ++cbi) {
+          const int cb = cb0 + cbi;
           float v[32];
           tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * 256 + a * 128 + cb * 32, v);
 #pragma unroll
