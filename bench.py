@@ -35,6 +35,10 @@ CFG = {
     "cfg1": dict(kind="chain", per_gpu=64, vocab=40, length=16, branch_prob=0.1, depth=4),
     "cfg2": dict(kind="balanced", per_gpu=512, vocab=40, length=16, branch_prob=0.1, depth=6),
 }
+MOE = {
+    "cfg4": dict(experts=64, k=2, tokens_per_gpu=65536, d=1024, h=1024),
+    "cfg5": dict(experts=1024, k=4, tokens_per_gpu=131072, d=2048, h=2048),
+}
 
 
 def parse():
@@ -43,7 +47,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg3", choices=sorted(CFG))
+    ap.add_argument("--workload", default="cfg3", choices=sorted(CFG) + sorted(MOE))
+    ap.add_argument("--no-moe", action="store_true", help="skip the secondary cfg4 MoE measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the bounded CPU-baseline sample")
@@ -311,6 +316,11 @@ def run_ours(args, dist):
     except Exception as e:  # reported, not fatal
         out["naive_gpu"] = {"error": str(e)}
 
+    if not args.no_moe:
+        try:
+            out["moe"] = run_moe(args, dist, "cfg4", secondary=True)
+        except Exception as e:  # reported, not fatal
+            out["moe"] = {"error": str(e)}
     clk.stop()
     out["clocks"] = clk.summary()
     if dist.rank == 0 and N == 1 and not args.no_cpu_baseline:
@@ -322,6 +332,59 @@ def run_ours(args, dist):
                                          f"(oracle/dynbatch_oracle.c) sharded over {threads} threads, "
                                          f"{dt:.1f} s"}
     return out
+
+
+def run_moe(args, dist, name, secondary=False):
+    """MoE layer forward (gate → stable expert sort → dispatch → grouped
+    tcgen05 GEMM1+ReLU → GEMM2 → slot-order combine), bf16 operands. Token
+    shard per rank (weak scaling); tokens/s."""
+    import numpy as np
+    import paper_1707_02402_b200 as db
+    c = MOE[name]
+    N = max(1, dist.world)
+    T = c["tokens_per_gpu"]
+    sess = db.MoeSession(c["experts"], c["k"], T * N, c["d"], c["h"], seed=0, precision=db.MOE_BF16,
+                         first=dist.rank * T, last=(dist.rank + 1) * T)
+    sess.time(3)
+    st = sess.stats()
+    dist.barrier()
+    ms, kt = sess.time(args.steps, profile=True)
+    dist.barrier()
+    ms_step = dist.max(ms / args.steps)
+    peaks, src = measured_peaks()
+    g_ms, g_fl = kt.ms[4] + kt.ms[5], kt.flops[4] + kt.flops[5]
+    gemm_tf = g_fl / (g_ms / 1e3) / 1e12 if g_ms else 0.0
+    res = {"metric": "MoE tokens/sec", "value": T * N / (ms_step / 1e3), "unit": "tokens/s",
+           "ms_per_step": ms_step, "dtype": "bf16",
+           "config": {"workload": f"{name}: n={c['experts']} top-{c['k']} d={c['d']} h={c['h']}, "
+                                  f"{T} tokens/GPU", "global_tokens": T * N},
+           "roofline": {"kernel": "k_moe_gemm (grouped tcgen05 GEMM1+GEMM2)", "bound": "tensor",
+                        "achieved": round(gemm_tf, 1),
+                        "peak": peaks.get("bf16_tflops_sustained"), "unit": "TFLOP/s",
+                        "frac": round(gemm_tf / peaks.get("bf16_tflops_sustained", 1), 4)},
+           "kernels": {name_: {"ms_per_step": kt.ms[c_] / args.steps,
+                               "gbs": (kt.bytes[c_] / (kt.ms[c_] / 1e3) / 1e9) if kt.ms[c_] and kt.bytes[c_] else None,
+                               "hbm_frac": ((kt.bytes[c_] / (kt.ms[c_] / 1e3) / 1e9) / peaks.get("hbm_gbs", 6450))
+                               if kt.ms[c_] and kt.bytes[c_] else None}
+                       for c_, name_ in ((3, "gate+sort+dispatch"), (4, "gemm1_relu"), (5, "gemm2"),
+                                         (6, "combine")) if kt.launches[c_]},
+           "gpu_launches_per_step": int(st.kernel_launches)}
+    # end-to-end: host fp32 inputs + fp64 scores → outputs
+    xin = db.PinnedArray((T, c["d"]), np.float32)
+    sc = db.PinnedArray((T, c["experts"]), np.float64)
+    yout = db.PinnedArray((T, c["d"]), np.float32)
+    rng = np.random.default_rng(dist.rank)
+    xin.array[:] = rng.uniform(-1, 1, size=(T, c["d"])).astype(np.float32)
+    sc.array[:] = rng.uniform(-1, 1, size=(T, c["experts"]))
+    sess.forward_host(xin.array, sc.array, yout.array)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sess.forward_host(xin.array, sc.array, yout.array)
+    e2e_s = dist.max((time.perf_counter() - t0) / args.steps)
+    res["e2e"] = {"value": T * N / e2e_s, "unit": "tokens/s",
+                  "h2d_bytes_per_step": T * (c["d"] * 4 + c["experts"] * 8),
+                  "d2h_bytes_per_step": T * c["d"] * 4}
+    return res
 
 
 def _mix_seed(seed, stream):
@@ -376,6 +439,16 @@ def main():
             print(json.dumps(run_reference(args, Dist(1))), flush=True)
         return
     dist = Dist(args.gpus)
+    if args.workload in MOE:
+        r = run_moe(args, dist, args.workload)
+        r.update({"n_gpus": max(1, dist.world), "steps": args.steps, "warmup": 3,
+                  "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                  "data": "synthetic (reference generators, seed 0; random-init experts)",
+                  "metric": METRIC, "gpu_launches": r["gpu_launches_per_step"] * args.steps})
+        if dist.rank == 0:
+            print(json.dumps(r), flush=True)
+        dist.close()
+        return
     out = run_ours(args, dist)
     if dist.rank == 0:
         print(json.dumps(out), flush=True)

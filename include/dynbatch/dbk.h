@@ -116,6 +116,21 @@ int dbk_moe_expert_fp64(int64_t T, int32_t n, int32_t k, int32_t d, int32_t h,
 int dbk_moe_combine_fp64(int64_t T, int32_t k, int32_t d, const double* weights,
                          const double* staged, double* out, void* stream);
 
+/* bf16 tensor-core experts (moe_gemm.cu): per-expert 128-row padded
+ * layout and tile list; dispatch of x rows (fp32 → bf16, pre-tiled operand);
+ * grouped tcgen05 GEMM (epi 0: ReLU → tiled bf16 H, epi 1: fp32 Y rows);
+ * slot-order combine. */
+int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int32_t* tile_expert,
+                        int32_t* tile_rb, int32_t* n_tiles, void* stream);
+int dbk_moe_bf16_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* offsets,
+                          const int32_t* pstart, const int32_t* order, const float* x, void* A,
+                          int32_t* row_of_item, int32_t blocks, void* stream);
+int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
+                      const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
+                      const void* const* W, void* H, float* Y, int32_t sms, void* stream);
+int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const double* weights,
+                         const int32_t* row_of_item, const float* Y, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,18 +1,155 @@
-// moe_bf16.cpp — host side of the bf16 grouped-GEMM MoE path.
+// moe_bf16.cpp — host side of the bf16 tensor-core MoE expert path.
+//
+// Expert weights follow ExpertSet (src/moe.cpp:71-88): Rng(mix_seed(seed, e)),
+// w1 [d × h] then w2 [h × d], uniform(-0.5, 0.5)/sqrt(fan_in); they are
+// generated on host threads (one Rng stream per expert, so the split is
+// exact), rounded to bf16 and pre-tiled for the grouped tcgen05 GEMMs
+// (moe_gemm.cu): B operand of GEMM1 = W1ᵀ [N = h][K = d], of GEMM2 = W2ᵀ
+// [N = d][K = h], as 32 KB blocks per (256-column N tile, 64-wide K chunk).
 #include "moe_bf16.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <thread>
 
 #include "device.hpp"
 
+#include "dynbatch/dbk.h"
+
 namespace dynbatch::dev {
 
-struct MoeBf16::Impl {};
+namespace {
 
-MoeBf16::MoeBf16(const MoeConfig&, std::int64_t, std::uint64_t, cudaStream_t) {
-  throw std::runtime_error("bf16 MoE path not built yet");
+std::uint16_t bf16(double v) {
+  float f = static_cast<float>(v);
+  std::uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<std::uint16_t>(u >> 16);
 }
+
+// Element (n, kk) of the N × K operand, stored input-major in `w` as
+// w[kk * N + n], into [N/256][K/64] blocks of [8][256][8].
+void tile_weights(const std::vector<double>& w, int K, int N, std::uint16_t* out) {
+  const int n_kc = K / 64;
+  for (int kk = 0; kk < K; ++kk) {
+    const int kc = kk / 64, k8 = (kk % 64) / 8, ke = kk % 8;
+    for (int n = 0; n < N; ++n) {
+      const int nt = n / 256, nn = n % 256;
+      const size_t blk = static_cast<size_t>(nt) * n_kc + kc;
+      out[blk * 256 * 64 + (static_cast<size_t>(k8) * 256 + nn) * 8 + ke] = bf16(w[static_cast<size_t>(kk) * N + n]);
+    }
+  }
+}
+
+}  // namespace
+
+struct MoeBf16::Impl {
+  std::int64_t T = 0;
+  int n = 0, k = 0, d = 0, h = 0, sms = 148;
+  Buf<float> x, Y, out;
+  Buf<std::uint8_t> A, H;
+  Buf<std::uint16_t> w1, w2;  // all experts, tiled
+  Buf<const void*> w1tab, w2tab;
+  Buf<std::int32_t> pstart, tile_expert, tile_rb, n_tiles, row_of_item;
+};
+
+MoeBf16::MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed, cudaStream_t s)
+    : impl_(std::make_unique<Impl>()) {
+  Impl& I = *impl_;
+  I.T = T;
+  I.n = static_cast<int>(cfg.experts);
+  I.k = static_cast<int>(cfg.active_per_example);
+  I.d = static_cast<int>(cfg.data_dim);
+  I.h = static_cast<int>(cfg.hidden);
+  if (I.d % 256 != 0 || I.h % 256 != 0) {
+    throw_error(Errc::invalid_argument, "bf16 MoE path needs data_dim and hidden multiples of 256");
+  }
+  I.sms = sm_count();
+  const std::int64_t rows = T * I.k + static_cast<std::int64_t>(I.n) * 128;
+  I.x.alloc(static_cast<size_t>(T) * I.d);
+  I.A.alloc(static_cast<size_t>(rows) * I.d * 2);
+  I.H.alloc(static_cast<size_t>(rows) * I.h * 2);
+  I.Y.alloc(static_cast<size_t>(rows) * I.d);
+  I.out.alloc(static_cast<size_t>(T) * I.d);
+  I.pstart.alloc(static_cast<size_t>(I.n) + 1);
+  I.tile_expert.alloc(static_cast<size_t>(rows / 128 + 1));
+  I.tile_rb.alloc(static_cast<size_t>(rows / 128 + 1));
+  I.n_tiles.alloc(1);
+  I.row_of_item.alloc(static_cast<size_t>(T) * I.k);
+  const size_t per = static_cast<size_t>(I.d) * I.h;
+  I.w1.alloc(per * I.n);
+  I.w2.alloc(per * I.n);
+  // Weights: experts are independent Rng streams → generate on host threads.
+  const double s1 = 1.0 / std::sqrt(static_cast<double>(I.d)), s2 = 1.0 / std::sqrt(static_cast<double>(I.h));
+  const int chunk = 16;
+  std::vector<std::uint16_t> h1(per * chunk), h2(per * chunk);
+  for (int e0 = 0; e0 < I.n; e0 += chunk) {
+    const int ne = std::min(chunk, I.n - e0);
+    std::vector<std::thread> pool;
+    for (int j = 0; j < ne; ++j) {
+      pool.emplace_back([&, j] {
+        Rng rng(mix_seed(expert_seed, static_cast<std::uint64_t>(e0 + j)));
+        std::vector<double> w(per);
+        for (double& v : w) v = rng.uniform(-0.5, 0.5) * s1;  // w1 [d][h]
+        tile_weights(w, I.d, I.h, h1.data() + per * j);
+        for (double& v : w) v = rng.uniform(-0.5, 0.5) * s2;  // w2 [h][d]
+        tile_weights(w, I.h, I.d, h2.data() + per * j);
+      });
+    }
+    for (auto& t : pool) t.join();
+    check(cudaMemcpy(I.w1.get() + per * e0, h1.data(), per * ne * 2, cudaMemcpyHostToDevice), "H2D w1");
+    check(cudaMemcpy(I.w2.get() + per * e0, h2.data(), per * ne * 2, cudaMemcpyHostToDevice), "H2D w2");
+  }
+  std::vector<const void*> t1(static_cast<size_t>(I.n)), t2(static_cast<size_t>(I.n));
+  for (int e = 0; e < I.n; ++e) {
+    t1[static_cast<size_t>(e)] = I.w1.get() + per * e;
+    t2[static_cast<size_t>(e)] = I.w2.get() + per * e;
+  }
+  I.w1tab.upload(t1, s);
+  I.w2tab.upload(t2, s);
+  check(cudaStreamSynchronize(s), "sync");
+}
+
 MoeBf16::~MoeBf16() = default;
-void MoeBf16::upload_inputs(const float*, cudaStream_t) {}
-int MoeBf16::forward(const std::int32_t*, const double*, const std::int32_t*, const std::int32_t*, cudaStream_t, Profiler*) { return 0; }
-void MoeBf16::download_outputs(float*, cudaStream_t) {}
+
+void MoeBf16::upload_inputs(const float* x, cudaStream_t s) {
+  check(cudaMemcpyAsync(impl_->x.get(), x, sizeof(float) * static_cast<size_t>(impl_->T) * impl_->d,
+                        cudaMemcpyHostToDevice, s), "H2D inputs");
+}
+
+int MoeBf16::forward(const std::int32_t* /*ids*/, const double* wts, const std::int32_t* order,
+                     const std::int32_t* offsets, cudaStream_t s, Profiler* prof) {
+  Impl& I = *impl_;
+  const int blocks = I.sms * 8;
+  if (prof) prof->begin(3, s);
+  check(dbk_moe_bf16_layout(I.n, offsets, I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(), I.n_tiles.get(), s),
+        "moe layout");
+  check(dbk_moe_bf16_dispatch(I.n, I.k, I.d, offsets, I.pstart.get(), order, I.x.get(), I.A.get(),
+                              I.row_of_item.get(), blocks, s),
+        "moe dispatch");
+  if (prof) prof->end(s);
+  if (prof) prof->begin(4, s);
+  check(dbk_moe_bf16_gemm(0, I.n, I.d, I.h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
+                          I.w1tab.get(), I.H.get(), nullptr, I.sms, s),
+        "moe gemm1");
+  if (prof) prof->end(s);
+  if (prof) prof->begin(5, s);
+  check(dbk_moe_bf16_gemm(1, I.n, I.h, I.d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
+                          I.w2tab.get(), nullptr, I.Y.get(), I.sms, s),
+        "moe gemm2");
+  if (prof) prof->end(s);
+  if (prof) prof->begin(6, s);
+  check(dbk_moe_bf16_combine(I.T, I.k, I.d, wts, I.row_of_item.get(), I.Y.get(), I.out.get(), s), "moe combine");
+  if (prof) prof->end(s);
+  return 5;
+}
+
+void MoeBf16::download_outputs(float* out, cudaStream_t s) {
+  check(cudaMemcpyAsync(out, impl_->out.get(), sizeof(float) * static_cast<size_t>(impl_->T) * impl_->d,
+                        cudaMemcpyDeviceToHost, s), "D2H outputs");
+  check(cudaStreamSynchronize(s), "sync");
+}
 
 }  // namespace dynbatch::dev

@@ -1,0 +1,303 @@
+// moe_gemm.cu — bf16 tensor-core MoE experts: dispatch → grouped GEMM1+ReLU
+// → grouped GEMM2 → slot-order combine (sm_100a, tcgen05/TMEM).
+//
+// Reference semantics: ExpertSet::apply (src/moe.cpp:98-145) on each
+// occupied expert's stacked rows, staged at token·k + slot (:244-251),
+// combined per token in slot order (:254-264). Routing (ids, weights, the
+// stable per-expert item order and offsets) comes from moe.cu / sched.cu and
+// is bit-identical to the reference; the arithmetic here is bf16 operands
+// with fp32 accumulation.
+//
+// Layout: rows of expert e occupy a 128-aligned padded range starting at
+// pstart[e]. Activations are stored pre-tiled in the K-major SWIZZLE_NONE
+// operand layout: tile (row block rb, K chunk kc) is a contiguous 16 KB block
+// [8 k-groups][128 rows][8 elements], so each pipeline stage is one bulk copy.
+// Weights are pre-tiled the same way per (N tile, K chunk): [8][256 n][8].
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dynbatch/dbk.h"
+#include "tc_common.cuh"
+
+namespace {
+
+using namespace dbk;
+
+constexpr int kBM = 128;         // rows per tile
+constexpr int kBN = 256;         // output columns per tile
+constexpr int kBK = 64;          // K chunk
+constexpr int kABytes = kBM * kBK * 2;   // 16 KB
+constexpr int kBBytes = kBN * kBK * 2;   // 32 KB
+constexpr int kStages = 4;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + kEpiWarps * 32;
+constexpr int kSmem = kStages * (kABytes + kBBytes) + 256;
+
+// padded starts and (expert, row block) tile list; single block.
+__global__ void k_moe_layout(int32_t n, const int32_t* __restrict__ offsets, int32_t* __restrict__ pstart,
+                             int32_t* __restrict__ tile_expert, int32_t* __restrict__ tile_rb,
+                             int32_t* __restrict__ n_tiles) {
+  if (threadIdx.x != 0) return;
+  int32_t rows_acc = 0, t = 0;
+  for (int32_t e = 0; e < n; ++e) {
+    pstart[e] = rows_acc;
+    const int32_t rows = offsets[e + 1] - offsets[e];
+    const int32_t nb = (rows + kBM - 1) / kBM;
+    for (int32_t b = 0; b < nb; ++b) {
+      tile_expert[t] = e;
+      tile_rb[t] = rows_acc / kBM + b;
+      ++t;
+    }
+    rows_acc += nb * kBM;
+  }
+  pstart[n] = rows_acc;
+  *n_tiles = t;
+}
+
+// One warp per padded row: row r of expert e holds item order[off_e + r]
+// (token = item / k); copies x[token] (fp32) → bf16 tiled A. Padding rows
+// are zero. row_of_item[item] = padded row (for the combine).
+__global__ void k_moe_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* __restrict__ offsets,
+                               const int32_t* __restrict__ pstart, const int32_t* __restrict__ order,
+                               const float* __restrict__ x, uint8_t* __restrict__ A,
+                               int32_t* __restrict__ row_of_item) {
+  const int32_t total_rows = pstart[n];
+  const int lane = threadIdx.x & 31;
+  const int32_t kchunks = d / kBK;
+  for (int32_t row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < total_rows;
+       row += gridDim.x * (blockDim.x >> 5)) {
+    int32_t lo = 0, hi = n;  // expert e with pstart[e] <= row < pstart[e+1]
+    while (hi - lo > 1) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (pstart[mid] <= row) lo = mid; else hi = mid;
+    }
+    const int32_t e = lo;
+    const int32_t local = row - pstart[e];
+    const bool valid = local < offsets[e + 1] - offsets[e];
+    int32_t token = 0;
+    if (valid) {
+      const int32_t item = order[offsets[e] + local];
+      token = item / k;
+      if (lane == 0) row_of_item[item] = row;
+    }
+    const int32_t rb = row / kBM, rr = row % kBM;
+    const float* src = x + static_cast<int64_t>(token) * d;
+    // 8-element groups: group gi covers k = gi*8 .. gi*8+7
+    for (int32_t gi = lane; gi < d / 8; gi += 32) {
+      uint4 pk = make_uint4(0, 0, 0, 0);
+      if (valid) {
+        const float4 a = *reinterpret_cast<const float4*>(src + gi * 8);
+        const float4 b = *reinterpret_cast<const float4*>(src + gi * 8 + 4);
+        pk.x = pack_bf16x2(a.x, a.y);
+        pk.y = pack_bf16x2(a.z, a.w);
+        pk.z = pack_bf16x2(b.x, b.y);
+        pk.w = pack_bf16x2(b.z, b.w);
+      }
+      const int32_t kc = gi / 8, k8 = gi % 8;
+      uint8_t* blk = A + (static_cast<int64_t>(rb) * kchunks + kc) * kABytes;
+      *reinterpret_cast<uint4*>(blk + (k8 * kBM + rr) * 16) = pk;
+    }
+  }
+}
+
+struct GemmParams {
+  int32_t n_experts;
+  int32_t K;                    // reduction length (multiple of 64)
+  int32_t N;                    // output columns (multiple of 256)
+  const int32_t* n_tiles;       // device scalar: row tiles
+  const int32_t* tile_expert;
+  const int32_t* tile_rb;
+  const uint8_t* A;             // tiled activations [rb][K/64][16 KB]
+  const uint8_t* const* W;      // per expert tiled weights [N/256][K/64][32 KB]
+  uint8_t* H;                   // EPI 0: tiled bf16 output [rb][N/64][16 KB]
+  float* Y;                     // EPI 1: fp32 row-major [row][N]
+};
+
+// Grouped GEMM over (row tile, N tile) pairs; EPI 0 = ReLU → bf16 tiled
+// (next GEMM's A operand), EPI 1 = fp32 rows.
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant__ GemmParams P) {
+  constexpr uint32_t IDESC = idesc_bf16_f32(kBM, kBN);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, kEpiWarps * 32);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int32_t n_nt = P.N / kBN, n_kc = P.K / kBK;
+  const int32_t total = *P.n_tiles * n_nt;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      uint32_t si = 0;
+      for (int32_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const int32_t rt = t / n_nt, nt = t % n_nt;
+        const int32_t e = P.tile_expert[rt], rb = P.tile_rb[rt];
+        const uint8_t* a = P.A + static_cast<int64_t>(rb) * n_kc * kABytes;
+        const uint8_t* w = P.W[e] + static_cast<int64_t>(nt) * n_kc * kBBytes;
+        for (int32_t kc = 0; kc < n_kc; ++kc, ++si) {
+          const uint32_t s = si % kStages, ph = (si / kStages) & 1;
+          mbar_wait(empty + s, ph ^ 1);
+          mbar_expect_tx(full + s, kABytes + kBBytes);
+          bulk_g2s(sA + s * kABytes, a + static_cast<int64_t>(kc) * kABytes, kABytes, full + s);
+          bulk_g2s(sB + s * kBBytes, w + static_cast<int64_t>(kc) * kBBytes, kBBytes, full + s);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      uint32_t si = 0;
+      int it = 0;
+      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      for (int32_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        const int abuf = it & 1;
+        mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int32_t kc = 0; kc < n_kc; ++kc, ++si) {
+          const uint32_t s = si % kStages, ph = (si / kStages) & 1;
+          mbar_wait(full + s, ph);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t ad = smem_desc(a_base + s * kABytes + (2 * kk) * kBM * 16, kBM * 16, 128);
+            const uint64_t bd = smem_desc(b_base + s * kBBytes + (2 * kk) * kBN * 16, kBN * 16, 128);
+            mma_bf16(tmem_base + abuf * kBN, ad, bd, IDESC, (kc | kk) != 0);
+          }
+          mma_commit(empty + s);
+        }
+        mma_commit(acc_full + abuf);
+      }
+    }
+  } else {  // epilogue: 8 warps, two per TMEM lane quarter, 128 columns each
+    const int quarter = warp & 3;
+    const int col0 = ((warp - 2) >> 2) * (kBN / 2);
+    int it = 0;
+    for (int32_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      const int abuf = it & 1;
+      const int32_t rt = t / n_nt, nt = t % n_nt;
+      const int32_t rb = P.tile_rb[rt];
+      mbar_wait(acc_full + abuf, (it >> 1) & 1);
+      tc_fence_after();
+      const int32_t rr = quarter * 32 + lane;
+      const int64_t row = static_cast<int64_t>(rb) * kBM + rr;
+#pragma unroll 1
+      for (int c = 0; c < kBN / 2; c += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * kBN + col0 + c, v);
+        const int32_t n0 = nt * kBN + col0 + c;  // global output column of v[0]
+        if (EPI == 0) {
+          const int32_t n_kc_out = P.N / kBK;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const int32_t col = n0 + g * 8;
+            uint4 pk;
+            pk.x = pack_bf16x2(fmaxf(v[g * 8 + 0], 0.f), fmaxf(v[g * 8 + 1], 0.f));
+            pk.y = pack_bf16x2(fmaxf(v[g * 8 + 2], 0.f), fmaxf(v[g * 8 + 3], 0.f));
+            pk.z = pack_bf16x2(fmaxf(v[g * 8 + 4], 0.f), fmaxf(v[g * 8 + 5], 0.f));
+            pk.w = pack_bf16x2(fmaxf(v[g * 8 + 6], 0.f), fmaxf(v[g * 8 + 7], 0.f));
+            uint8_t* blk = P.H + (static_cast<int64_t>(rb) * n_kc_out + col / kBK) * kABytes;
+            *reinterpret_cast<uint4*>(blk + (((col % kBK) / 8) * kBM + rr) * 16) = pk;
+          }
+        } else {
+          float* dst = P.Y + row * P.N + n0;
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            *reinterpret_cast<float4*>(dst + g * 4) = make_float4(v[g * 4], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty + abuf);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// out[t] = Σ_slot w[t·k + slot] · Y[row_of_item[t·k + slot]] in slot order.
+__global__ void k_moe_combine_f32(int64_t T, int32_t k, int32_t d, const double* __restrict__ w,
+                                  const int32_t* __restrict__ row_of_item, const float* __restrict__ Y,
+                                  float* __restrict__ out) {
+  const int64_t t = blockIdx.x;
+  if (t >= T) return;
+  for (int32_t j = threadIdx.x * 4; j < d; j += blockDim.x * 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int32_t s = 0; s < k; ++s) {
+      const float ws = static_cast<float>(w[t * k + s]);
+      const float4 y = *reinterpret_cast<const float4*>(Y + static_cast<int64_t>(row_of_item[t * k + s]) * d + j);
+      acc.x = fmaf(ws, y.x, acc.x);
+      acc.y = fmaf(ws, y.y, acc.y);
+      acc.z = fmaf(ws, y.z, acc.z);
+      acc.w = fmaf(ws, y.w, acc.w);
+    }
+    *reinterpret_cast<float4*>(out + t * d + j) = acc;
+  }
+}
+
+template <int EPI>
+int launch_gemm(const GemmParams& p, int sms, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_moe_gemm<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    configured = true;
+  }
+  k_moe_gemm<EPI><<<sms, kThreads, kSmem, s>>>(p);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int32_t* tile_expert,
+                                   int32_t* tile_rb, int32_t* n_tiles, void* stream) {
+  k_moe_layout<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(n, offsets, pstart, tile_expert, tile_rb, n_tiles);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_moe_bf16_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* offsets, const int32_t* pstart,
+                                     const int32_t* order, const float* x, void* A, int32_t* row_of_item,
+                                     int32_t blocks, void* stream) {
+  k_moe_dispatch<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(n, k, d, offsets, pstart, order, x,
+                                                                        static_cast<uint8_t*>(A), row_of_item);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
+                                 const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
+                                 const void* const* W, void* H, float* Y, int32_t sms, void* stream) {
+  if (K % kBK != 0 || N % kBN != 0) return static_cast<int>(cudaErrorInvalidValue);
+  GemmParams p{n, K, N, n_tiles, tile_expert, tile_rb, static_cast<const uint8_t*>(A),
+               reinterpret_cast<const uint8_t* const*>(W), static_cast<uint8_t*>(H), Y};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return epi == 0 ? launch_gemm<0>(p, sms, s) : launch_gemm<1>(p, sms, s);
+}
+
+extern "C" int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const double* weights,
+                                    const int32_t* row_of_item, const float* Y, float* out, void* stream) {
+  if (T <= 0) return 0;
+  k_moe_combine_f32<<<static_cast<unsigned>(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(T, k, d, weights,
+                                                                                             row_of_item, Y, out);
+  return static_cast<int>(cudaGetLastError());
+}

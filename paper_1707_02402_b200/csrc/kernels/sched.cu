@@ -18,7 +18,7 @@
 
 namespace {
 
-constexpr int kSeg = 256;        // nodes per warp segment
+constexpr int kSeg = 1024;       // items per warp segment (32 rounds of 32)
 constexpr int kWarpsPerBlock = 8;
 
 // One thread per program: Kahn's algorithm from the root with the queue and
