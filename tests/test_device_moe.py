@@ -75,3 +75,23 @@ def test_topk_ties():
     xi, sc = O.moe_inputs(8, 16, 4, 1)
     rid, rw = O.topk(sc, 3, use_ref=True)
     assert np.array_equal(ids, rid)
+
+
+@pytest.mark.parametrize("n,k,T,d,h", [(64, 2, 2048, 256, 512), (16, 4, 300, 256, 256),
+                                       (8, 1, 100, 512, 256), (40, 3, 777, 256, 768)])
+def test_moe_bf16_matches_reference(n, k, T, d, h):
+    """bf16 grouped tcgen05 GEMMs vs the fp64 reference arithmetic.
+    Routing (ids, dispatch order) stays bit-exact; outputs within the stated
+    bf16 tolerance max|a-b|/max|ref| <= 2e-2."""
+    from dbtest import max_norm_err
+    s = db.MoeSession(n, k, T, d, h, seed=5, precision=db.MOE_BF16)
+    s.forward()
+    out = s.run().outputs()
+    xi, sc = O.moe_inputs(T, n, d, 5)
+    ids, w = O.topk(sc, k)
+    ref, trace, _ = O.moe_forward(xi, ids, w, n, h, O.mix_seed(5, 0xe4be27))
+    dev_ids, dev_w, off, items = s.routing()
+    assert np.array_equal(dev_ids, ids)
+    assert np.array_equal(items, np.argsort(ids.ravel(), kind="stable").astype(np.int32))
+    err = max_norm_err(out, ref)
+    assert err <= 2e-2, err
