@@ -32,11 +32,14 @@ int dbk_sched_labels(int64_t b, int64_t N, const int32_t* prog_off, const int32_
  * over CSR order; writes member_g[N] (sorted global ids), and the group
  * tables: group_fid[G], group_begin[G+1], step_group_begin[S+1] with
  * dev_scalars[2] = G. seg_hist must hold max_keys · n_segments ints with
- * max_keys ≥ (d_max+1)·p; n_segments = ceil(N / 256). */
+ * max_keys ≥ (d_max+1)·p; size from dbk_bucket_sort_scratch(N, max_keys). */
 int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, const int32_t* fid,
                           const int32_t* labels, int32_t* dev_scalars, int32_t* seg_hist,
                           int32_t* member_g, int32_t* group_fid, int32_t* group_begin,
                           int32_t* step_group_begin, void* stream);
+
+/* Scratch (int32 count) the bucket sorts need in seg_hist. */
+int64_t dbk_bucket_sort_scratch(int64_t n_items, int32_t max_keys);
 
 /* Generic stable counting sort by an explicit key in [0, n_keys): order[]
  * receives item indices sorted by key, stable in index order; offsets[n_keys+1]
@@ -118,18 +121,19 @@ int dbk_moe_combine_fp64(int64_t T, int32_t k, int32_t d, const double* weights,
 
 /* bf16 tensor-core experts (moe_gemm.cu): per-expert 128-row padded
  * layout and tile list; dispatch of x rows (fp32 → bf16, pre-tiled operand);
- * grouped tcgen05 GEMM (epi 0: ReLU → tiled bf16 H, epi 1: fp32 Y rows);
+ * grouped tcgen05 GEMM (epi 0: ReLU → tiled bf16 H, epi 1: bf16 Y rows);
  * slot-order combine. */
 int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int32_t* tile_expert,
                         int32_t* tile_rb, int32_t* n_tiles, void* stream);
 int dbk_moe_bf16_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* offsets,
-                          const int32_t* pstart, const int32_t* order, const float* x, void* A,
+                          const int32_t* pstart, const int32_t* tile_expert, const int32_t* order,
+                          const float* x, void* A,
                           int32_t* row_of_item, int32_t blocks, void* stream);
 int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
                       const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
-                      const void* const* W, void* H, float* Y, int32_t sms, void* stream);
+                      const void* const* W, void* H, void* Y, int32_t sms, void* stream);
 int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const double* weights,
-                         const int32_t* row_of_item, const float* Y, float* out, void* stream);
+                         const int32_t* row_of_item, const void* Y, float* out, void* stream);
 
 #ifdef __cplusplus
 }

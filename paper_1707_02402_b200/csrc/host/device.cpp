@@ -151,8 +151,7 @@ DeviceProgramBatch::DeviceProgramBatch(const HostCSR& csr, cudaStream_t s) : csr
   member_g.alloc(N);
   // d_max + 1 <= s_max, so at most s_max * p (step, fid) keys / groups.
   max_keys_ = std::max(1, csr.s_max) * csr.p;
-  const size_t nseg = (N + 255) / 256;
-  seg_hist.alloc(static_cast<size_t>(max_keys_) * nseg);
+  seg_hist.alloc(static_cast<size_t>(dbk_bucket_sort_scratch(csr.N, max_keys_)));
   group_fid.alloc(static_cast<size_t>(max_keys_) + 1);
   group_begin.alloc(static_cast<size_t>(max_keys_) + 2);
   step_group_begin.alloc(static_cast<size_t>(std::max(1, csr.s_max)) + 2);

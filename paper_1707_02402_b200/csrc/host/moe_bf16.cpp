@@ -48,7 +48,8 @@ void tile_weights(const std::vector<double>& w, int K, int N, std::uint16_t* out
 struct MoeBf16::Impl {
   std::int64_t T = 0;
   int n = 0, k = 0, d = 0, h = 0, sms = 148;
-  Buf<float> x, Y, out;
+  Buf<float> x, out;
+  Buf<std::uint16_t> Y;  // bf16 expert outputs, padded rows
   Buf<std::uint8_t> A, H;
   Buf<std::uint16_t> w1, w2;  // all experts, tiled
   Buf<const void*> w1tab, w2tab;
@@ -126,7 +127,7 @@ int MoeBf16::forward(const std::int32_t* /*ids*/, const double* wts, const std::
   if (prof) prof->begin(3, s);
   check(dbk_moe_bf16_layout(I.n, offsets, I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(), I.n_tiles.get(), s),
         "moe layout");
-  check(dbk_moe_bf16_dispatch(I.n, I.k, I.d, offsets, I.pstart.get(), order, I.x.get(), I.A.get(),
+  check(dbk_moe_bf16_dispatch(I.n, I.k, I.d, offsets, I.pstart.get(), I.tile_expert.get(), order, I.x.get(), I.A.get(),
                               I.row_of_item.get(), blocks, s),
         "moe dispatch");
   if (prof) prof->end(s);

@@ -32,7 +32,7 @@ struct MoeDev {
     ids.alloc(items);
     order.alloc(items);
     offsets.alloc(static_cast<size_t>(n) + 1);
-    seg_hist.alloc(static_cast<size_t>(n) * ((items + 255) / 256 + 1));
+    seg_hist.alloc(static_cast<size_t>(dbk_bucket_sort_scratch(static_cast<std::int64_t>(items), n)));
     tiles.alloc(static_cast<size_t>(n) + 1);
     err.alloc(4);
   }

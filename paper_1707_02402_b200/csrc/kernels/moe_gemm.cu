@@ -59,7 +59,8 @@ __global__ void k_moe_layout(int32_t n, const int32_t* __restrict__ offsets, int
 // (token = item / k); copies x[token] (fp32) → bf16 tiled A. Padding rows
 // are zero. row_of_item[item] = padded row (for the combine).
 __global__ void k_moe_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* __restrict__ offsets,
-                               const int32_t* __restrict__ pstart, const int32_t* __restrict__ order,
+                               const int32_t* __restrict__ pstart, const int32_t* __restrict__ tile_expert,
+                               const int32_t* __restrict__ order,
                                const float* __restrict__ x, uint8_t* __restrict__ A,
                                int32_t* __restrict__ row_of_item) {
   const int32_t total_rows = pstart[n];
@@ -67,12 +68,7 @@ __global__ void k_moe_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* _
   const int32_t kchunks = d / kBK;
   for (int32_t row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < total_rows;
        row += gridDim.x * (blockDim.x >> 5)) {
-    int32_t lo = 0, hi = n;  // expert e with pstart[e] <= row < pstart[e+1]
-    while (hi - lo > 1) {
-      const int32_t mid = (lo + hi) >> 1;
-      if (pstart[mid] <= row) lo = mid; else hi = mid;
-    }
-    const int32_t e = lo;
+    const int32_t e = tile_expert[row / kBM];  // row blocks never straddle experts
     const int32_t local = row - pstart[e];
     const bool valid = local < offsets[e + 1] - offsets[e];
     int32_t token = 0;
@@ -111,7 +107,7 @@ struct GemmParams {
   const uint8_t* A;             // tiled activations [rb][K/64][16 KB]
   const uint8_t* const* W;      // per expert tiled weights [N/256][K/64][32 KB]
   uint8_t* H;                   // EPI 0: tiled bf16 output [rb][N/64][16 KB]
-  float* Y;                     // EPI 1: fp32 row-major [row][N]
+  __nv_bfloat16* Y;             // EPI 1: bf16 row-major [row][N]
 };
 
 // Grouped GEMM over (row tile, N tile) pairs; EPI 0 = ReLU → bf16 tiled
@@ -220,10 +216,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant_
             *reinterpret_cast<uint4*>(blk + (((col % kBK) / 8) * kBM + rr) * 16) = pk;
           }
         } else {
-          float* dst = P.Y + row * P.N + n0;
+          __nv_bfloat16* dst = P.Y + row * P.N + n0;
 #pragma unroll
-          for (int g = 0; g < 8; ++g)
-            *reinterpret_cast<float4*>(dst + g * 4) = make_float4(v[g * 4], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]);
+          for (int g = 0; g < 4; ++g) {
+            uint4 pk;
+            pk.x = pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]);
+            pk.y = pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]);
+            pk.z = pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]);
+            pk.w = pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]);
+            *reinterpret_cast<uint4*>(dst + g * 8) = pk;
+          }
         }
       }
       tc_fence_before();
@@ -239,21 +241,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant_
 
 // out[t] = Σ_slot w[t·k + slot] · Y[row_of_item[t·k + slot]] in slot order.
 __global__ void k_moe_combine_f32(int64_t T, int32_t k, int32_t d, const double* __restrict__ w,
-                                  const int32_t* __restrict__ row_of_item, const float* __restrict__ Y,
+                                  const int32_t* __restrict__ row_of_item, const __nv_bfloat16* __restrict__ Y,
                                   float* __restrict__ out) {
   const int64_t t = blockIdx.x;
   if (t >= T) return;
-  for (int32_t j = threadIdx.x * 4; j < d; j += blockDim.x * 4) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int32_t j = threadIdx.x * 8; j < d; j += blockDim.x * 8) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int32_t s = 0; s < k; ++s) {
       const float ws = static_cast<float>(w[t * k + s]);
-      const float4 y = *reinterpret_cast<const float4*>(Y + static_cast<int64_t>(row_of_item[t * k + s]) * d + j);
-      acc.x = fmaf(ws, y.x, acc.x);
-      acc.y = fmaf(ws, y.y, acc.y);
-      acc.z = fmaf(ws, y.z, acc.z);
-      acc.w = fmaf(ws, y.w, acc.w);
+      const uint4 raw = *reinterpret_cast<const uint4*>(Y + static_cast<int64_t>(row_of_item[t * k + s]) * d + j);
+      const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(y2[q]);
+        acc[2 * q] = fmaf(ws, f.x, acc[2 * q]);
+        acc[2 * q + 1] = fmaf(ws, f.y, acc[2 * q + 1]);
+      }
     }
-    *reinterpret_cast<float4*>(out + t * d + j) = acc;
+    *reinterpret_cast<float4*>(out + t * d + j) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(out + t * d + j + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
 }
 
@@ -277,27 +283,28 @@ extern "C" int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* p
 }
 
 extern "C" int dbk_moe_bf16_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* offsets, const int32_t* pstart,
-                                     const int32_t* order, const float* x, void* A, int32_t* row_of_item,
+                                     const int32_t* tile_expert, const int32_t* order, const float* x, void* A, int32_t* row_of_item,
                                      int32_t blocks, void* stream) {
-  k_moe_dispatch<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(n, k, d, offsets, pstart, order, x,
+  k_moe_dispatch<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(n, k, d, offsets, pstart, tile_expert, order, x,
                                                                         static_cast<uint8_t*>(A), row_of_item);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
                                  const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
-                                 const void* const* W, void* H, float* Y, int32_t sms, void* stream) {
+                                 const void* const* W, void* H, void* Y, int32_t sms, void* stream) {
   if (K % kBK != 0 || N % kBN != 0) return static_cast<int>(cudaErrorInvalidValue);
   GemmParams p{n, K, N, n_tiles, tile_expert, tile_rb, static_cast<const uint8_t*>(A),
-               reinterpret_cast<const uint8_t* const*>(W), static_cast<uint8_t*>(H), Y};
+               reinterpret_cast<const uint8_t* const*>(W), static_cast<uint8_t*>(H),
+               static_cast<__nv_bfloat16*>(Y)};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return epi == 0 ? launch_gemm<0>(p, sms, s) : launch_gemm<1>(p, sms, s);
 }
 
 extern "C" int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const double* weights,
-                                    const int32_t* row_of_item, const float* Y, float* out, void* stream) {
+                                    const int32_t* row_of_item, const void* Y, float* out, void* stream) {
   if (T <= 0) return 0;
-  k_moe_combine_f32<<<static_cast<unsigned>(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(T, k, d, weights,
-                                                                                             row_of_item, Y, out);
+  k_moe_combine_f32<<<static_cast<unsigned>(T), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      T, k, d, weights, row_of_item, static_cast<const __nv_bfloat16*>(Y), out);
   return static_cast<int>(cudaGetLastError());
 }

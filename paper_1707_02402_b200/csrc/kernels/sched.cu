@@ -18,7 +18,8 @@
 
 namespace {
 
-constexpr int kSeg = 1024;       // items per warp segment (32 rounds of 32)
+constexpr int kSeg = 256;        // items per warp segment (8 rounds of 32)
+constexpr int kScanChunk = 4096; // table entries per block of the multi-block scan
 constexpr int kWarpsPerBlock = 8;
 
 // One thread per program: Kahn's algorithm from the root with the queue and
@@ -87,6 +88,90 @@ __global__ void k_seg_hist(int64_t n, int32_t nseg, Key key, int32_t* __restrict
   }
 }
 
+// Block-wide exclusive scan of one value per thread; *total = block sum.
+__device__ __forceinline__ int32_t block_scan_excl(int32_t v, int32_t* total, int32_t* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = lane < nw ? sh[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    sh[lane] = w;
+  }
+  __syncthreads();
+  const int32_t excl = (warp > 0 ? sh[warp - 1] : 0) + x - v;
+  *total = sh[nw - 1];
+  __syncthreads();
+  return excl;
+}
+
+__device__ __forceinline__ int64_t table_len(int32_t nseg, int32_t p, const int32_t* scal,
+                                             int32_t fixed_keys) {
+  const int32_t n_keys = fixed_keys > 0 ? fixed_keys : (scal[0] + 1) * p;
+  return static_cast<int64_t>(n_keys) * nseg;
+}
+
+// Multi-block exclusive scan of hist[0 .. len): (1) each block scans its
+// kScanChunk entries in place and records its total, (2) one block scans the
+// totals, (3) each block adds its carry-in.
+__global__ void __launch_bounds__(1024) k_scan_partial(int32_t nseg, int32_t p, const int32_t* __restrict__ scal,
+                                                       int32_t fixed_keys, int32_t* __restrict__ hist,
+                                                       int32_t* __restrict__ totals) {
+  __shared__ int32_t sh[32];
+  const int64_t len = table_len(nseg, p, scal, fixed_keys);
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanChunk;
+  if (base >= len) return;
+  int32_t v[4], sum = 0;
+  const int64_t i0 = base + threadIdx.x * 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v[j] = i0 + j < len ? hist[i0 + j] : 0;
+    sum += v[j];
+  }
+  int32_t total;
+  int32_t run = block_scan_excl(sum, &total, sh);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (i0 + j < len) hist[i0 + j] = run;
+    run += v[j];
+  }
+  if (threadIdx.x == 0) totals[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_totals(int32_t nseg, int32_t p, const int32_t* __restrict__ scal,
+                                                      int32_t fixed_keys, int32_t* __restrict__ totals) {
+  __shared__ int32_t sh[32];
+  const int64_t len = table_len(nseg, p, scal, fixed_keys);
+  const int32_t nblk = static_cast<int32_t>((len + kScanChunk - 1) / kScanChunk);
+  int32_t carry = 0;
+  for (int32_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
+    const int32_t i = b0 + threadIdx.x;
+    const int32_t v = i < nblk ? totals[i] : 0;
+    int32_t total;
+    const int32_t e = block_scan_excl(v, &total, sh);
+    if (i < nblk) totals[i] = carry + e;
+    carry += total;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_add(int32_t nseg, int32_t p, const int32_t* __restrict__ scal,
+                                                   int32_t fixed_keys, int32_t* __restrict__ hist,
+                                                   const int32_t* __restrict__ totals) {
+  const int64_t len = table_len(nseg, p, scal, fixed_keys);
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanChunk;
+  if (base >= len || blockIdx.x == 0) return;
+  const int32_t add = totals[blockIdx.x];
+  for (int64_t i = base + threadIdx.x; i < base + kScanChunk && i < len; i += blockDim.x) hist[i] += add;
+}
+
 // Single-block exclusive scan over hist[0 .. n_keys*nseg) (key-major), then
 // the group table: one group per non-empty key, in key order.
 __global__ void k_scan_groups(int64_t n, int32_t nseg, int32_t p, int32_t* __restrict__ hist,
@@ -101,33 +186,7 @@ __global__ void k_scan_groups(int64_t n, int32_t nseg, int32_t p, int32_t* __res
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthreads = blockDim.x;
   if (tid == 0) carry_s = 0;
   __syncthreads();
-  // Pass 1: exclusive scan in tiles of blockDim elements.
-  for (int64_t base = 0; base < total; base += nthreads) {
-    const int64_t i = base + tid;
-    const int32_t v = i < total ? hist[i] : 0;
-    int32_t x = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_tot[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      int32_t w = lane < (nthreads >> 5) ? warp_tot[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      warp_tot[lane] = w;  // inclusive
-    }
-    __syncthreads();
-    const int32_t carry = carry_s;
-    const int32_t excl = carry + (warp > 0 ? warp_tot[warp - 1] : 0) + x - v;
-    if (i < total) hist[i] = excl;
-    __syncthreads();
-    if (tid == nthreads - 1) carry_s = excl + v;
-    __syncthreads();
-  }
+  (void)total;  // the table was scanned by k_scan_partial / k_scan_totals / k_scan_add
   // Pass 2: key k's bucket is [hist[k*nseg], hist[(k+1)*nseg]) (n at the end).
   if (offsets) {  // generic sort: bucket starts only
     for (int32_t k = tid; k <= n_keys; k += nthreads)
@@ -237,7 +296,13 @@ extern "C" int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, con
   LevelKey key{fid, labels, dev_scalars, p};
   const int blocks = (nseg + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (nseg > 0) k_seg_hist<<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist);
-  k_scan_groups<<<1, 1024, 0, s>>>(N, nseg > 0 ? nseg : 1, p, seg_hist, dev_scalars, 0, group_fid,
+  const int32_t ns = nseg > 0 ? nseg : 1;
+  int32_t* totals = seg_hist + static_cast<int64_t>(max_keys) * ns;
+  const unsigned sblk = static_cast<unsigned>((static_cast<int64_t>(max_keys) * ns + kScanChunk - 1) / kScanChunk);
+  k_scan_partial<<<sblk, 1024, 0, s>>>(ns, p, dev_scalars, 0, seg_hist, totals);
+  k_scan_totals<<<1, 1024, 0, s>>>(ns, p, dev_scalars, 0, totals);
+  k_scan_add<<<sblk, 1024, 0, s>>>(ns, p, dev_scalars, 0, seg_hist, totals);
+  k_scan_groups<<<1, 1024, 0, s>>>(N, ns, p, seg_hist, dev_scalars, 0, group_fid,
                                    group_begin, step_group_begin, nullptr);
   if (nseg > 0) k_seg_scatter<<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist, member_g);
   return static_cast<int>(cudaGetLastError());
@@ -252,8 +317,19 @@ extern "C" int dbk_stable_bucket_sort(int64_t n_items, int32_t n_keys, const int
   ExplicitKey key{keys};
   const int blocks = (nseg + kWarpsPerBlock - 1) / kWarpsPerBlock;
   k_seg_hist<<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist);
+  int32_t* totals = seg_hist + static_cast<int64_t>(n_keys) * nseg;
+  const unsigned sblk = static_cast<unsigned>((static_cast<int64_t>(n_keys) * nseg + kScanChunk - 1) / kScanChunk);
+  k_scan_partial<<<sblk, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, seg_hist, totals);
+  k_scan_totals<<<1, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, totals);
+  k_scan_add<<<sblk, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, seg_hist, totals);
   k_scan_groups<<<1, 1024, 0, s>>>(n_items, nseg, 1, seg_hist, nullptr, n_keys, nullptr, nullptr,
                                    nullptr, offsets);
   k_seg_scatter<<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist, order);
   return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int64_t dbk_bucket_sort_scratch(int64_t n_items, int32_t max_keys) {
+  const int64_t nseg = n_items > 0 ? (n_items + kSeg - 1) / kSeg : 1;
+  const int64_t table = static_cast<int64_t>(max_keys) * nseg;
+  return table + table / kScanChunk + 64;
 }
