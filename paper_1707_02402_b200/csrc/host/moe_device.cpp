@@ -172,7 +172,7 @@ void MoeSession::forward() {
   D.gate(stream_);
   D.sort(stream_);
   prof_.end(stream_);
-  launches_ += 1 + 3;
+  launches_ += 1 + 6;  // top-k; histogram, 3-pass scan, offsets, stable scatter
   if (impl_->precision == 0) {
     prof_.begin(4, stream_);
     D.experts_fp64(stream_);

@@ -63,36 +63,38 @@ __global__ void k_moe_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* _
                                const int32_t* __restrict__ order,
                                const float* __restrict__ x, uint8_t* __restrict__ A,
                                int32_t* __restrict__ row_of_item) {
+  // One block (128 threads) per 128-row block; thread = row, so each warp's
+  // 16-byte stores for a given 8-element group are 512 contiguous bytes of
+  // the tiled operand, and each lane reads whole 32-byte sectors of its row.
   const int32_t total_rows = pstart[n];
-  const int lane = threadIdx.x & 31;
   const int32_t kchunks = d / kBK;
-  for (int32_t row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < total_rows;
-       row += gridDim.x * (blockDim.x >> 5)) {
-    const int32_t e = tile_expert[row / kBM];  // row blocks never straddle experts
+  for (int32_t rb = blockIdx.x; rb * kBM < total_rows; rb += gridDim.x) {
+    const int32_t rr = threadIdx.x;
+    const int32_t row = rb * kBM + rr;
+    const int32_t e = tile_expert[rb];  // row blocks never straddle experts
     const int32_t local = row - pstart[e];
     const bool valid = local < offsets[e + 1] - offsets[e];
     int32_t token = 0;
     if (valid) {
       const int32_t item = order[offsets[e] + local];
       token = item / k;
-      if (lane == 0) row_of_item[item] = row;
+      row_of_item[item] = row;
     }
-    const int32_t rb = row / kBM, rr = row % kBM;
     const float* src = x + static_cast<int64_t>(token) * d;
-    // 8-element groups: group gi covers k = gi*8 .. gi*8+7
-    for (int32_t gi = lane; gi < d / 8; gi += 32) {
+    uint8_t* dst = A + static_cast<int64_t>(rb) * kchunks * kABytes + rr * 16;
+#pragma unroll 4
+    for (int32_t gi = 0; gi < d / 8; ++gi) {  // 8-element group gi = k gi*8 .. gi*8+7
       uint4 pk = make_uint4(0, 0, 0, 0);
       if (valid) {
-        const float4 a = *reinterpret_cast<const float4*>(src + gi * 8);
-        const float4 b = *reinterpret_cast<const float4*>(src + gi * 8 + 4);
+        const float4 a = __ldg(reinterpret_cast<const float4*>(src + gi * 8));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(src + gi * 8 + 4));
         pk.x = pack_bf16x2(a.x, a.y);
         pk.y = pack_bf16x2(a.z, a.w);
         pk.z = pack_bf16x2(b.x, b.y);
         pk.w = pack_bf16x2(b.z, b.w);
       }
-      const int32_t kc = gi / 8, k8 = gi % 8;
-      uint8_t* blk = A + (static_cast<int64_t>(rb) * kchunks + kc) * kABytes;
-      *reinterpret_cast<uint4*>(blk + (k8 * kBM + rr) * 16) = pk;
+      // block (kc = gi/8) at kc·16 KB, k-group (gi%8) at ·kBM·16
+      *reinterpret_cast<uint4*>(dst + (gi >> 3) * kABytes + (gi & 7) * kBM * 16) = pk;
     }
   }
 }
@@ -285,7 +287,7 @@ extern "C" int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* p
 extern "C" int dbk_moe_bf16_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* offsets, const int32_t* pstart,
                                      const int32_t* tile_expert, const int32_t* order, const float* x, void* A, int32_t* row_of_item,
                                      int32_t blocks, void* stream) {
-  k_moe_dispatch<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(n, k, d, offsets, pstart, tile_expert, order, x,
+  k_moe_dispatch<<<blocks, kBM, 0, static_cast<cudaStream_t>(stream)>>>(n, k, d, offsets, pstart, tile_expert, order, x,
                                                                         static_cast<uint8_t*>(A), row_of_item);
   return static_cast<int>(cudaGetLastError());
 }
