@@ -72,6 +72,9 @@ DYNBATCH_API void db_host_free(void* p);
  * db_batch_generate (for data-parallel shards). */
 DYNBATCH_API db_status db_batch_generate_range(const db_workload_opts* opts, int64_t first,
                                                int64_t last, db_batch** out);
+/* Borrowing view of the batch's b × width input rows (valid until free). */
+DYNBATCH_API db_status db_batch_inputs(const db_batch* batch, const double** data, int64_t* rows,
+                                       int64_t* width);
 /* Binds the calling thread to `device` and checks it is sm_100. */
 DYNBATCH_API db_status db_device_open(int32_t device);
 

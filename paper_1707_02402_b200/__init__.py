@@ -126,6 +126,8 @@ SIGNATURES = {
     "db_host_alloc": (VP, [C.c_int64]),
     "db_host_free": (None, [VP]),
     "db_batch_generate_range": (C.c_int32, [C.POINTER(WorkloadOpts), C.c_int64, C.c_int64, PVP]),
+    "db_batch_inputs": (C.c_int32, [VP, C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int64)]),
     "db_iep_session_time": (C.c_int32, [VP, C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                         C.POINTER(KernelTimes)]),
     "db_moe_session_time": (C.c_int32, [VP, C.c_int32, C.c_int32, C.POINTER(C.c_double),
@@ -250,6 +252,14 @@ class Batch(_Handle):
         s = BatchStats()
         check(lib().db_batch_stats(self.h, C.byref(s)))
         return s
+
+    def inputs(self) -> np.ndarray:
+        d = C.POINTER(C.c_double)()
+        r, w = C.c_int64(), C.c_int64()
+        check(lib().db_batch_inputs(self.h, C.byref(d), C.byref(r), C.byref(w)))
+        if r.value * w.value == 0:
+            return np.zeros((r.value, w.value))
+        return np.ctypeslib.as_array(d, shape=(r.value, w.value)).copy()
 
     def schedule(self, strategy="improved") -> "Schedule":
         h = C.c_void_p()

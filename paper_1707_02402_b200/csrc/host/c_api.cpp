@@ -380,6 +380,14 @@ db_status db_batch_generate_range(const db_workload_opts* opts, int64_t first, i
   });
 }
 
+db_status db_batch_inputs(const db_batch* batch, const double** data, int64_t* rows, int64_t* width) {
+  if (!batch || !data || !rows || !width) return null_arg();
+  *data = batch->inputs.data().data();
+  *rows = batch->inputs.rows();
+  *width = batch->inputs.width();
+  return DB_OK;
+}
+
 static void copy_times(const dynbatch::dev::KernelTimes& k, db_kernel_times_t* out) {
   for (int c = 0; c < 8; ++c) {
     out->ms[c] = k.ms[c];
