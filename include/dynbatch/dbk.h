@@ -78,7 +78,8 @@ int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t*
                 int32_t* step_bintile_begin, int32_t* step_positions, int32_t* tile_group,
                 int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, int64_t n_nodes,
                 const int32_t* member_g, const int32_t* child0, const int32_t* child1,
-                const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, void* stream);
+                const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t tile_m,
+                void* stream);
 /* Gather of the operands of step `step` that no child epilogue forwarded
  * (leaves, shared children) into the bf16 staging planes, with the binary
  * channel concat fused into the write; plane_stride in positions. */
@@ -91,7 +92,9 @@ int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* 
 /* tcgen05 implicit-GEMM convolutions: kind 0 = conv1x1 over [x; y] → z
  * (bf16 staging + fp32 parked in the node slot), 1 = conv3x3 #1 → mid
  * (bf16), 2 = conv3x3 #2 + residual + ReLU → fp32 node values (when a
- * reader needs them) and the bf16 operand image of the parent's call. */
+ * reader needs them) and the bf16 operand image of the parent's call.
+ * kind + 16 selects the CTA-pair (cta_group::2) variant, which needs a plan
+ * with tile_m = 512 and weights packed as two 64-channel halves per block. */
 int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
                 const int32_t* tile_group, const int32_t* tile_q0, const int32_t* group_fid,
                 const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,

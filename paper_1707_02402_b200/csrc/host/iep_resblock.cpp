@@ -2,6 +2,7 @@
 // weight packing for the tcgen05 kernels, buffer sizing and the per-step
 // launch sequence  plan → [gather → conv1x1 → conv3x3#1 → conv3x3#2]×steps.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "device.hpp"
@@ -34,22 +35,23 @@ std::uint16_t to_bf16(double v) {
 // ((k/8)·128 + n)·8 + k%8 (K-major, no swizzle).
 constexpr int kKChunk = 64;
 
-std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int cin, int taps) {
+// pair = true (CTA-pair kernels): each block is two contiguous 8 KB halves
+// of 64 output channels, [half][k/8][64][8], one per CTA of the pair.
+std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int cin, int taps, bool pair) {
   std::vector<std::uint16_t> out(static_cast<size_t>(taps) * cin * C);
   const size_t block = static_cast<size_t>(kKChunk) * C;
   for (int tap = 0; tap < taps; ++tap)
     for (int ci = 0; ci < cin; ++ci) {
       const int chunk = ci / kKChunk, k = ci % kKChunk;
       const size_t base = static_cast<size_t>(chunk * taps + tap) * block;
-      for (int co = 0; co < C; ++co)
-        out[base + (static_cast<size_t>(k / 8) * C + co) * 8 + k % 8] =
-            to_bf16(w[(static_cast<size_t>(tap) * cin + ci) * C + co]);
+      for (int co = 0; co < C; ++co) {
+        const size_t off = pair ? static_cast<size_t>(co / 64) * (block / 2) + (static_cast<size_t>(k / 8) * 64 + co % 64) * 8 + k % 8
+                                : (static_cast<size_t>(k / 8) * C + co) * 8 + k % 8;
+        out[base + off] = to_bf16(w[(static_cast<size_t>(tap) * cin + ci) * C + co]);
+      }
     }
   return out;
 }
-
-std::vector<std::uint16_t> pack_conv3(const std::vector<double>& w, int C) { return pack_blocks(w, C, C, 9); }
-std::vector<std::uint16_t> pack_conv1(const std::vector<double>& w, int C) { return pack_blocks(w, C, 2 * C, 1); }
 
 }  // namespace
 
@@ -60,6 +62,10 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   if (c.max_arity > 2) throw_error(Errc::arity_mismatch, "resblock modules support arity <= 2");
   rb_ = std::make_unique<RB>();
   RB& R = *rb_;
+  // CTA-pair (cta_group::2) conv kernels unless DYNBATCH_CONV_PAIR=0.
+  const char* pe = std::getenv("DYNBATCH_CONV_PAIR");
+  R.pair = !(pe && pe[0] == '0');
+  R.tile_m = R.pair ? 2 * RB::kTileM : RB::kTileM;
   for (std::int64_t g = 0; g < c.N; ++g)
     if (c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0) ++R.n_expensive;
   const size_t b = static_cast<size_t>(std::max<std::int64_t>(c.b, 1));
@@ -76,7 +82,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   // staging: every step owns its range (results are forwarded into their
   // parent's operand image); ≤ one 256-position alignment gap per group
   const std::int64_t max_groups = std::min<std::int64_t>(R.n_expensive, static_cast<std::int64_t>(std::max(1, c.s_max)) * c.p);
-  R.plane_stride = RB::kGuard + R.n_expensive * 225 + (max_groups + 2) * RB::kTileM + 64;
+  R.plane_stride = RB::kGuard + R.n_expensive * 225 + (max_groups + 2) * R.tile_m + 64;
   // forwarding eligibility: expensive nodes with exactly one parent
   {
     std::vector<std::int32_t> parents(static_cast<size_t>(N), 0), ok(static_cast<size_t>(N), 0);
@@ -98,7 +104,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   // schedule-derived tables (G ≤ max keys; tiles ≤ N_exp·225/256 + G)
   const size_t G = static_cast<size_t>(std::max(1, c.s_max)) * c.p + 2;
   const size_t S = static_cast<size_t>(std::max<std::int64_t>(c.N, 1)) + 2;  // naive: S = N
-  const size_t T = static_cast<size_t>(R.n_expensive) * 225 / RB::kTileM + G + 2;
+  const size_t T = static_cast<size_t>(R.n_expensive) * 225 / RB::kTileM + G + 2;  // bound for either tile size
   R.seg_start.alloc(std::max(G, N + 2));
   R.group_tile0.alloc(std::max(G, N + 2));
   R.group_bintile0.alloc(std::max(G, N + 2));
@@ -128,12 +134,12 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
       return static_cast<const float*>(R.bbuf.back().get());
     };
     if (a == 2) {
-      w0[static_cast<size_t>(f)] = put_w(pack_conv1(m.w0, C));
+      w0[static_cast<size_t>(f)] = put_w(pack_blocks(m.w0, C, 2 * C, 1, R.pair));
       b0[static_cast<size_t>(f)] = put_b(m.b0);
     }
-    w1[static_cast<size_t>(f)] = put_w(pack_conv3(m.w1, C));
+    w1[static_cast<size_t>(f)] = put_w(pack_blocks(m.w1, C, C, 9, R.pair));
     b1[static_cast<size_t>(f)] = put_b(m.b1);
-    w2[static_cast<size_t>(f)] = put_w(pack_conv3(m.w2, C));
+    w2[static_cast<size_t>(f)] = put_w(pack_blocks(m.w2, C, C, 9, R.pair));
     b2[static_cast<size_t>(f)] = put_b(m.b2);
   }
   R.w0tab.upload(w0, stream_);
@@ -161,7 +167,7 @@ void IepSession::forward_resblock() {
                     R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(), R.step_tile_begin.get(),
                     R.step_bintile_begin.get(), R.step_positions.get(), R.tile_group.get(), R.tile_q0.get(),
                     R.bin_group.get(), R.bin_q0.get(), B.csr().N, B.member_g.get(), B.child0.get(),
-                    B.child1.get(), R.fwd_ok.get(), R.fwd_pos.get(), R.fwd_slot.get(), stream_),
+                    B.child1.get(), R.fwd_ok.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.tile_m, stream_),
         "dbk_rb_plan");
     prof_.end(stream_);
   launches_ += 4;
@@ -177,7 +183,8 @@ void IepSession::forward_resblock() {
     prof_.end(stream_);
     // conv1x1 over the binary groups' [x; y] → z (stage_x + parked fp32)
     prof_.begin(3, stream_);
-    check(dbk_rb_conv(0, s, R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
+    const int kp = R.pair ? 16 : 0;
+    check(dbk_rb_conv(0 + kp, s, R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.example.get(), R.stage_cat.get(), R.stage_x.get(), R.plane_stride,
                       R.inputs.get(), R.values.get(), R.w0tab.get(), R.b0tab.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.stage_x.get(),
@@ -185,7 +192,7 @@ void IepSession::forward_resblock() {
           "conv1x1");
     prof_.end(stream_);
     prof_.begin(4, stream_);
-    check(dbk_rb_conv(1, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
+    check(dbk_rb_conv(1 + kp, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.example.get(), R.stage_x.get(), R.stage_mid.get(), R.plane_stride,
                       R.inputs.get(), R.values.get(), R.w1tab.get(), R.b1tab.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.stage_x.get(),
@@ -193,7 +200,7 @@ void IepSession::forward_resblock() {
           "conv3x3 #1");
     prof_.end(stream_);
     prof_.begin(5, stream_);
-    check(dbk_rb_conv(2, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
+    check(dbk_rb_conv(2 + kp, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.example.get(), R.stage_mid.get(), nullptr, R.plane_stride,
                       R.inputs.get(), R.values.get(), R.w2tab.get(), R.b2tab.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.stage_x.get(),

@@ -113,127 +113,17 @@ struct ConvParams {
   __nv_bfloat16* stage_cat;
 };
 
+// Epilogue of one tile (256 positions = 2 TMEM accumulators) for this warp's
+// lane quarter and two 32-column chunks.
 template <int KIND>
-__global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__ ConvParams P) {
-  using K = Cfg<KIND>;
-  constexpr int WIN = win<KIND>();
-  constexpr uint32_t IDESC = idesc_bf16_f32(128, 128);
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kASlots * a_slot_bytes<KIND>();
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + K::kBStages * kBStage);
-  uint64_t* a_full = bars;
-  uint64_t* a_empty = a_full + kASlots;
-  uint64_t* b_full = a_empty + kASlots;
-  uint64_t* b_empty = b_full + K::kBStages;
-  uint64_t* acc_full = b_empty + K::kBStages;
-  uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kASlots; ++s) {
-      mbar_init(a_full + s, 1);
-      mbar_init(a_empty + s, 1);
-    }
-    for (int s = 0; s < K::kBStages; ++s) {
-      mbar_init(b_full + s, 1);
-      mbar_init(b_empty + s, 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, kEpiWarps * 32);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  const int32_t t_begin = P.step_tile_begin[P.step];
-  const int32_t n_tiles = P.step_tile_begin[P.step + 1] - t_begin;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------ producer
-      uint32_t ai = 0, bi = 0;
-      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int32_t g = P.tile_group[t_begin + t];
-        const int32_t q0 = P.tile_q0[t_begin + t];
-        const uint8_t* w = reinterpret_cast<const uint8_t*>(P.wpack[P.group_fid[g]]);
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.stage_in) +
-                             static_cast<int64_t>(kGuard + q0 - K::kHalo) * 16;
-        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
-          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
-          mbar_wait(a_empty + sa, pa ^ 1);
-          mbar_expect_tx(a_full + sa, a_slot_bytes<KIND>());
-          for (int j = 0; j < kChunkPlanes; ++j) {
-            bulk_g2s(sA + sa * a_slot_bytes<KIND>() + j * WIN * 16,
-                     src + static_cast<int64_t>(ch * kChunkPlanes + j) * P.ps * 16, WIN * 16, a_full + sa);
-          }
-          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
-            const uint32_t s = bi % K::kBStages, ph = (bi / K::kBStages) & 1;
-            mbar_wait(b_empty + s, ph ^ 1);
-            mbar_expect_tx(b_full + s, kBStage);
-            bulk_g2s(sB + s * kBStage, w + static_cast<int64_t>(ch * K::kTaps + tap) * kBStage, kBStage,
-                     b_full + s);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------------------------------- MMA issuer
-      uint32_t ai = 0, bi = 0;
-      int it = 0;
-      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-        const int abuf = it & 1;
-        mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
-          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
-          mbar_wait(a_full + sa, pa);
-          tc_fence_after();
-          const uint32_t a_slot = a_base + sa * a_slot_bytes<KIND>();
-          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
-            const uint32_t s = bi % K::kBStages, ph = (bi / K::kBStages) & 1;
-            mbar_wait(b_full + s, ph);
-            tc_fence_after();
-            const int shift = K::kTaps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
-#pragma unroll
-            for (int a = 0; a < kTileM / 128; ++a) {
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint32_t arow = static_cast<uint32_t>(K::kHalo + shift + a * 128);
-                const uint64_t ad = smem_desc(a_slot + ((2 * kk) * WIN + arow) * 16, WIN * 16, 128);
-                const uint64_t bd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
-                mma_bf16(tmem_base + abuf * 256 + a * 128, ad, bd, IDESC, (ch | tap | kk) != 0);
-              }
-            }
-            mma_commit(b_empty + s);
-          }
-          mma_commit(a_empty + sa);
-        }
-        mma_commit(acc_full + abuf);
-      }
-    }
-  } else {  // ------------------------------------------------------ epilogue
-    const int quarter = warp & 3;
-    const int cb0 = ((warp - 2) >> 2) * 2;  // this warp's first 32-column chunk
-    int it = 0;
-    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-      const int abuf = it & 1;
-      const int32_t g = P.tile_group[t_begin + t];
-      const int32_t q0 = P.tile_q0[t_begin + t];
+__device__ __forceinline__ void rb_epilogue(const ConvParams& P, uint32_t tmem_base, int abuf, int32_t g,
+                                            int32_t q0, int quarter, int cb0, int lane) {
       const int32_t f = P.group_fid[g];
       const int32_t gb0 = P.group_begin[g];
       const int32_t rows = P.group_begin[g + 1] - gb0;
       const int32_t seg = P.seg_start[g];
       const float* __restrict__ bias = P.bias[f];
       const bool binary = P.arity_of[f] == 2;
-      mbar_wait(acc_full + abuf, (it >> 1) & 1);
-      tc_fence_after();
 #pragma unroll 1
       for (int a = 0; a < kTileM / 128; ++a) {
         const int row = a * 128 + quarter * 32 + lane;
@@ -381,6 +271,124 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
           }
         }
       }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__ ConvParams P) {
+  using K = Cfg<KIND>;
+  constexpr int WIN = win<KIND>();
+  constexpr uint32_t IDESC = idesc_bf16_f32(128, 128);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kASlots * a_slot_bytes<KIND>();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + K::kBStages * kBStage);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kASlots;
+  uint64_t* b_full = a_empty + kASlots;
+  uint64_t* b_empty = b_full + K::kBStages;
+  uint64_t* acc_full = b_empty + K::kBStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kASlots; ++s) {
+      mbar_init(a_full + s, 1);
+      mbar_init(a_empty + s, 1);
+    }
+    for (int s = 0; s < K::kBStages; ++s) {
+      mbar_init(b_full + s, 1);
+      mbar_init(b_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, kEpiWarps * 32);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int32_t t_begin = P.step_tile_begin[P.step];
+  const int32_t n_tiles = P.step_tile_begin[P.step + 1] - t_begin;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------ producer
+      uint32_t ai = 0, bi = 0;
+      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int32_t g = P.tile_group[t_begin + t];
+        const int32_t q0 = P.tile_q0[t_begin + t];
+        const uint8_t* w = reinterpret_cast<const uint8_t*>(P.wpack[P.group_fid[g]]);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.stage_in) +
+                             static_cast<int64_t>(kGuard + q0 - K::kHalo) * 16;
+        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
+          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+          mbar_wait(a_empty + sa, pa ^ 1);
+          mbar_expect_tx(a_full + sa, a_slot_bytes<KIND>());
+          for (int j = 0; j < kChunkPlanes; ++j) {
+            bulk_g2s(sA + sa * a_slot_bytes<KIND>() + j * WIN * 16,
+                     src + static_cast<int64_t>(ch * kChunkPlanes + j) * P.ps * 16, WIN * 16, a_full + sa);
+          }
+          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
+            const uint32_t s = bi % K::kBStages, ph = (bi / K::kBStages) & 1;
+            mbar_wait(b_empty + s, ph ^ 1);
+            mbar_expect_tx(b_full + s, kBStage);
+            bulk_g2s(sB + s * kBStage, w + static_cast<int64_t>(ch * K::kTaps + tap) * kBStage, kBStage,
+                     b_full + s);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------------------------------- MMA issuer
+      uint32_t ai = 0, bi = 0;
+      int it = 0;
+      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+        const int abuf = it & 1;
+        mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
+          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+          mbar_wait(a_full + sa, pa);
+          tc_fence_after();
+          const uint32_t a_slot = a_base + sa * a_slot_bytes<KIND>();
+          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
+            const uint32_t s = bi % K::kBStages, ph = (bi / K::kBStages) & 1;
+            mbar_wait(b_full + s, ph);
+            tc_fence_after();
+            const int shift = K::kTaps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
+#pragma unroll
+            for (int a = 0; a < kTileM / 128; ++a) {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t arow = static_cast<uint32_t>(K::kHalo + shift + a * 128);
+                const uint64_t ad = smem_desc(a_slot + ((2 * kk) * WIN + arow) * 16, WIN * 16, 128);
+                const uint64_t bd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
+                mma_bf16(tmem_base + abuf * 256 + a * 128, ad, bd, IDESC, (ch | tap | kk) != 0);
+              }
+            }
+            mma_commit(b_empty + s);
+          }
+          mma_commit(a_empty + sa);
+        }
+        mma_commit(acc_full + abuf);
+      }
+    }
+  } else {  // ------------------------------------------------------ epilogue
+    const int quarter = warp & 3;
+    const int cb0 = ((warp - 2) >> 2) * 2;  // this warp's first 32-column chunk
+    int it = 0;
+    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const int abuf = it & 1;
+      const int32_t g = P.tile_group[t_begin + t];
+      const int32_t q0 = P.tile_q0[t_begin + t];
+      mbar_wait(acc_full + abuf, (it >> 1) & 1);
+      tc_fence_after();
+      rb_epilogue<KIND>(P, tmem_base, abuf, g, q0, quarter, cb0, lane);
       tc_fence_before();
       mbar_arrive(acc_empty + abuf);
     }
@@ -389,6 +397,183 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ------------------------------------------------------- CTA-pair kernel
+// Cluster of two CTAs on one TPC computes a 512-position pair tile with
+// tcgen05.mma.cta_group::2 (M = 256 = 128 rows from each CTA's window,
+// N = 128): each CTA stages its own 256-position A window and HALF of every
+// weight block (64 output channels), so per-SM shared-memory reads per MMA
+// drop from 8 KB to 6 KB and weight traffic per SM halves. The even CTA
+// issues the MMAs; the odd CTA relays its "data landed" events to the even
+// CTA's barriers (remote mbarrier arrives), and commits multicast back to
+// both CTAs' empty / accumulator-full barriers. Each CTA's epilogue reads the
+// accumulator rows of its own positions from its own TMEM.
+constexpr int kPairBStage = 64 * 64 * 2;  // 8 KB: N=64 (half) × K=64
+
+template <int KIND>
+struct PairCfg;
+template <>
+struct PairCfg<0> { static constexpr int kBStages = 8; };
+template <>
+struct PairCfg<1> { static constexpr int kBStages = 16; };
+template <>
+struct PairCfg<2> : PairCfg<1> {};
+
+template <int KIND>
+constexpr int pair_smem_bytes() {
+  return kASlots * a_slot_bytes<KIND>() + PairCfg<KIND>::kBStages * kPairBStage + 512;
+}
+
+template <int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_rb_conv_pair(const __grid_constant__ ConvParams P) {
+  using K = Cfg<KIND>;
+  constexpr int NB = PairCfg<KIND>::kBStages;
+  constexpr int WIN = win<KIND>();
+  constexpr uint32_t IDESC = idesc_bf16_f32(256, 128);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kASlots * a_slot_bytes<KIND>();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NB * kPairBStage);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kASlots;
+  uint64_t* b_full = a_empty + kASlots;
+  uint64_t* b_empty = b_full + NB;
+  uint64_t* acc_full = b_empty + NB;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  if (threadIdx.x == 0) {
+    const uint32_t full_count = leader ? 2 : 1;  // own copies + the peer's relay
+    for (int s = 0; s < kASlots; ++s) {
+      mbar_init(a_full + s, full_count);
+      mbar_init(a_empty + s, 1);
+    }
+    for (int s = 0; s < NB; ++s) {
+      mbar_init(b_full + s, full_count);
+      mbar_init(b_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int32_t t_begin = P.step_tile_begin[P.step];
+  const int32_t n_tiles = P.step_tile_begin[P.step + 1] - t_begin;
+  const int32_t pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------- producer (both CTAs)
+      uint32_t ai = 0, bi = 0;
+      for (int32_t t = pair; t < n_tiles; t += n_pairs) {
+        const int32_t g = P.tile_group[t_begin + t];
+        const int32_t q0 = P.tile_q0[t_begin + t] + static_cast<int32_t>(rank) * kTileM;
+        const uint8_t* w = reinterpret_cast<const uint8_t*>(P.wpack[P.group_fid[g]]) + rank * kPairBStage;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.stage_in) +
+                             static_cast<int64_t>(kGuard + q0 - K::kHalo) * 16;
+        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
+          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+          mbar_wait(a_empty + sa, pa ^ 1);
+          mbar_expect_tx(a_full + sa, a_slot_bytes<KIND>());
+          for (int j = 0; j < kChunkPlanes; ++j) {
+            bulk_g2s(sA + sa * a_slot_bytes<KIND>() + j * WIN * 16,
+                     src + static_cast<int64_t>(ch * kChunkPlanes + j) * P.ps * 16, WIN * 16, a_full + sa);
+          }
+          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
+            const uint32_t s = bi % NB, ph = (bi / NB) & 1;
+            mbar_wait(b_empty + s, ph ^ 1);
+            mbar_expect_tx(b_full + s, kPairBStage);
+            bulk_g2s(sB + s * kPairBStage, w + static_cast<int64_t>(ch * K::kTaps + tap) * 2 * kPairBStage,
+                     kPairBStage, b_full + s);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ------------------- MMA issuer (even CTA)
+      uint32_t ai = 0, bi = 0;
+      int it = 0;
+      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      for (int32_t t = pair; t < n_tiles; t += n_pairs, ++it) {
+        const int abuf = it & 1;
+        mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
+          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+          mbar_wait(a_full + sa, pa);
+          tc_fence_after();
+          const uint32_t a_slot = a_base + sa * a_slot_bytes<KIND>();
+          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
+            const uint32_t s = bi % NB, ph = (bi / NB) & 1;
+            mbar_wait(b_full + s, ph);
+            tc_fence_after();
+            const int shift = K::kTaps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
+#pragma unroll
+            for (int a = 0; a < kTileM / 128; ++a) {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t arow = static_cast<uint32_t>(K::kHalo + shift + a * 128);
+                const uint64_t ad = smem_desc(a_slot + ((2 * kk) * WIN + arow) * 16, WIN * 16, 128);
+                const uint64_t bd = smem_desc(b_base + s * kPairBStage + (2 * kk) * 1024, 1024, 128);
+                mma_bf16_pair(tmem_base + abuf * 256 + a * 128, ad, bd, IDESC, (ch | tap | kk) != 0);
+              }
+            }
+            mma_commit_pair(b_empty + s, 0x3);
+          }
+          mma_commit_pair(a_empty + sa, 0x3);
+        }
+        mma_commit_pair(acc_full + abuf, 0x3);
+      }
+    } else if (lane == 0) {  // ---------------- relay (odd CTA): data landed
+      uint32_t ai = 0, bi = 0;
+      for (int32_t t = pair; t < n_tiles; t += n_pairs) {
+        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
+          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+          mbar_wait(a_full + sa, pa);
+          mbar_arrive_remote(a_full + sa, 0);
+          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
+            const uint32_t s = bi % NB, ph = (bi / NB) & 1;
+            mbar_wait(b_full + s, ph);
+            mbar_arrive_remote(b_full + s, 0);
+          }
+        }
+      }
+    }
+  } else {  // ---------------------------------------------- epilogue (both)
+    const int quarter = warp & 3;
+    const int cb0 = ((warp - 2) >> 2) * 2;
+    int it = 0;
+    for (int32_t t = pair; t < n_tiles; t += n_pairs, ++it) {
+      const int abuf = it & 1;
+      const int32_t g = P.tile_group[t_begin + t];
+      const int32_t q0 = P.tile_q0[t_begin + t] + static_cast<int32_t>(rank) * kTileM;
+      mbar_wait(acc_full + abuf, (it >> 1) & 1);
+      tc_fence_after();
+      rb_epilogue<KIND>(P, tmem_base, abuf, g, q0, quarter, cb0, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(acc_empty + abuf); else mbar_arrive_remote(acc_empty + abuf, 0);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
   }
 }
 
@@ -401,7 +586,7 @@ __global__ void k_rb_plan(int32_t n_steps, const int32_t* __restrict__ sgb,
                           const int32_t* __restrict__ arity_of, int32_t* __restrict__ seg_start,
                           int32_t* __restrict__ group_tile0, int32_t* __restrict__ group_bintile0,
                           int32_t* __restrict__ step_tile_begin, int32_t* __restrict__ step_bintile_begin,
-                          int32_t* __restrict__ step_positions) {
+                          int32_t* __restrict__ step_positions, int32_t tile_m) {
   // One thread per step computes its segment starts; tile prefixes over
   // steps are then accumulated serially (steps are few for improved schedules).
   for (int32_t s = threadIdx.x; s < n_steps; s += blockDim.x) {
@@ -412,11 +597,11 @@ __global__ void k_rb_plan(int32_t n_steps, const int32_t* __restrict__ sgb,
         seg_start[g] = -1;
         continue;
       }
-      const int32_t nt = (rows * kImg + kTileM - 1) / kTileM;
+      const int32_t nt = (rows * kImg + tile_m - 1) / tile_m;
       seg_start[g] = cursor;
       group_tile0[g] = tiles;
       group_bintile0[g] = arity_of[group_fid[g]] == 2 ? bintiles : -1;
-      cursor += nt * kTileM;
+      cursor += nt * tile_m;
       tiles += nt;
       if (arity_of[group_fid[g]] == 2) bintiles += nt;
     }
@@ -492,21 +677,21 @@ __global__ void k_rb_tiles(int32_t n_steps, const int32_t* __restrict__ sgb,
                            const int32_t* __restrict__ step_tile_begin,
                            const int32_t* __restrict__ step_bintile_begin, int32_t* __restrict__ tile_group,
                            int32_t* __restrict__ tile_q0, int32_t* __restrict__ bin_group,
-                           int32_t* __restrict__ bin_q0) {
+                           int32_t* __restrict__ bin_q0, int32_t tile_m) {
   const int32_t s = blockIdx.x;
   if (s >= n_steps) return;
   for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
     if (seg_start[g] < 0) continue;
     const int32_t rows = group_begin[g + 1] - group_begin[g];
-    const int32_t nt = (rows * kImg + kTileM - 1) / kTileM;
+    const int32_t nt = (rows * kImg + tile_m - 1) / tile_m;
     for (int32_t i = threadIdx.x; i < nt; i += blockDim.x) {
       const int32_t ti = step_tile_begin[s] + group_tile0[g] + i;
       tile_group[ti] = g;
-      tile_q0[ti] = seg_start[g] + i * kTileM;
+      tile_q0[ti] = seg_start[g] + i * tile_m;
       if (group_bintile0[g] >= 0) {
         const int32_t bi = step_bintile_begin[s] + group_bintile0[g] + i;
         bin_group[bi] = g;
-        bin_q0[bi] = seg_start[g] + i * kTileM;
+        bin_q0[bi] = seg_start[g] + i * tile_m;
       }
     }
   }
@@ -606,6 +791,17 @@ int launch_conv(const ConvParams& p, int num_sms, cudaStream_t s) {
   return static_cast<int>(cudaGetLastError());
 }
 
+template <int KIND>
+int launch_conv_pair(const ConvParams& p, int num_sms, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_rb_conv_pair<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem_bytes<KIND>());
+    configured = true;
+  }
+  k_rb_conv_pair<KIND><<<(num_sms / 2) * 2, kThreads, pair_smem_bytes<KIND>(), s>>>(p);
+  return static_cast<int>(cudaGetLastError());
+}
+
 }  // namespace
 
 extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
@@ -614,15 +810,16 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
                            int32_t* step_bintile_begin, int32_t* step_positions, int32_t* tile_group,
                            int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, int64_t n_nodes,
                            const int32_t* member_g, const int32_t* child0, const int32_t* child1,
-                           const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, void* stream) {
+                           const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t tile_m,
+                           void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n_steps <= 0) return 0;
   k_rb_plan<<<1, 1024, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
                                group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
-                               step_positions);
+                               step_positions, tile_m);
   k_rb_tiles<<<n_steps, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of,
                                      seg_start, group_tile0, group_bintile0, step_tile_begin,
-                                     step_bintile_begin, tile_group, tile_q0, bin_group, bin_q0);
+                                     step_bintile_begin, tile_group, tile_q0, bin_group, bin_q0, tile_m);
   k_rb_fwd_init<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_nodes, fwd_pos, fwd_slot);
   k_rb_fwd<<<n_steps, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
                                    member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot);
@@ -661,6 +858,9 @@ extern "C" int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_
     case 0: return launch_conv<0>(p, num_sms, s);
     case 1: return launch_conv<1>(p, num_sms, s);
     case 2: return launch_conv<2>(p, num_sms, s);
+    case 0 + 16: return launch_conv_pair<0>(p, num_sms, s);  // CTA-pair variants
+    case 1 + 16: return launch_conv_pair<1>(p, num_sms, s);
+    case 2 + 16: return launch_conv_pair<2>(p, num_sms, s);
   }
   return static_cast<int>(cudaErrorInvalidValue);
 }
