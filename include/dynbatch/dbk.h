@@ -104,6 +104,7 @@ int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
                 const void* const* wpack, const float* const* bias, const int32_t* fwd_pos,
                 const int32_t* fwd_slot, void* stage_x, void* stage_cat, int32_t num_sms,
                 void* stream);
+int dbk_rb_debug(unsigned long long* out24, int32_t reset, int32_t enable);
 int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream);
 int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int32_t* fid,
                           const int32_t* arity_of, const int32_t* example, const float* inputs,

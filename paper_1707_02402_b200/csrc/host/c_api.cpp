@@ -16,6 +16,7 @@
 #include "dynbatch.hpp"
 #include "dynbatch/dynbatch.h"
 #include "dynbatch/dynbatch_device.h"
+#include "dynbatch/dbk.h"
 
 struct db_batch {
   dynbatch::FunctionVocab vocab;
@@ -377,6 +378,14 @@ db_status db_batch_generate_range(const db_workload_opts* opts, int64_t first, i
     spec.seed = opts->seed;
     dynbatch::GeneratedBatch g = dynbatch::gen_batch_range(spec, first, last);
     *out = new db_batch{std::move(g.vocab), std::move(g.programs), std::move(g.inputs)};
+  });
+}
+
+db_status db_debug_conv_waits(uint64_t* out24, int32_t reset, int32_t enable) {
+  return guarded([&] {
+    dynbatch::dev::require_device();
+    dynbatch::dev::check(dbk_rb_debug(reinterpret_cast<unsigned long long*>(out24), reset, enable),
+                         "dbk_rb_debug");
   });
 }
 

@@ -111,7 +111,13 @@ struct ConvParams {
   const int32_t* fwd_slot;
   __nv_bfloat16* stage_x;
   __nv_bfloat16* stage_cat;
+  int32_t debug;  // nonzero: the MMA thread accumulates its wait cycles in g_conv_dbg
 };
+
+// MMA-thread wait accounting per kernel kind (pair kinds at +3):
+// [waiting for a drained accumulator, for an A window, for a weight stage,
+// total cycles of the MMA loop]. Read/reset with dbk_rb_debug().
+__device__ unsigned long long g_conv_dbg[6 * 4];
 
 // Epilogue of one tile (256 positions = 2 TMEM accumulators) for this warp's
 // lane quarter and two 32-column chunks.
@@ -344,21 +350,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------------------------------- MMA issuer
+      long long w_acc = 0, w_a = 0, w_b = 0;
+      const long long t_start = clock64();
       uint32_t ai = 0, bi = 0;
       int it = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
         const int abuf = it & 1;
+        long long c0 = clock64();
         mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
+        w_acc += clock64() - c0;
         tc_fence_after();
         for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
           const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+          c0 = clock64();
           mbar_wait(a_full + sa, pa);
+          w_a += clock64() - c0;
           tc_fence_after();
           const uint32_t a_slot = a_base + sa * a_slot_bytes<KIND>();
           for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
             const uint32_t s = bi % K::kBStages, ph = (bi / K::kBStages) & 1;
+            c0 = clock64();
             mbar_wait(b_full + s, ph);
+            w_b += clock64() - c0;
             tc_fence_after();
             const int shift = K::kTaps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
 #pragma unroll
@@ -376,6 +390,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
           mma_commit(a_empty + sa);
         }
         mma_commit(acc_full + abuf);
+      }
+      if (P.debug) {
+        atomicAdd(&g_conv_dbg[KIND * 4 + 0], static_cast<unsigned long long>(w_acc));
+        atomicAdd(&g_conv_dbg[KIND * 4 + 1], static_cast<unsigned long long>(w_a));
+        atomicAdd(&g_conv_dbg[KIND * 4 + 2], static_cast<unsigned long long>(w_b));
+        atomicAdd(&g_conv_dbg[KIND * 4 + 3], static_cast<unsigned long long>(clock64() - t_start));
       }
     }
   } else {  // ------------------------------------------------------ epilogue
@@ -503,21 +523,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ------------------- MMA issuer (even CTA)
+      long long w_acc = 0, w_a = 0, w_b = 0;
+      const long long t_start = clock64();
       uint32_t ai = 0, bi = 0;
       int it = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       for (int32_t t = pair; t < n_tiles; t += n_pairs, ++it) {
         const int abuf = it & 1;
+        long long c0 = clock64();
         mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
+        w_acc += clock64() - c0;
         tc_fence_after();
         for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
           const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+          c0 = clock64();
           mbar_wait(a_full + sa, pa);
+          w_a += clock64() - c0;
           tc_fence_after();
           const uint32_t a_slot = a_base + sa * a_slot_bytes<KIND>();
           for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
             const uint32_t s = bi % NB, ph = (bi / NB) & 1;
+            c0 = clock64();
             mbar_wait(b_full + s, ph);
+            w_b += clock64() - c0;
             tc_fence_after();
             const int shift = K::kTaps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
 #pragma unroll
@@ -535,6 +563,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mma_commit_pair(a_empty + sa, 0x3);
         }
         mma_commit_pair(acc_full + abuf, 0x3);
+      }
+      if (P.debug) {
+        atomicAdd(&g_conv_dbg[12 + KIND * 4 + 0], static_cast<unsigned long long>(w_acc));
+        atomicAdd(&g_conv_dbg[12 + KIND * 4 + 1], static_cast<unsigned long long>(w_a));
+        atomicAdd(&g_conv_dbg[12 + KIND * 4 + 2], static_cast<unsigned long long>(w_b));
+        atomicAdd(&g_conv_dbg[12 + KIND * 4 + 3], static_cast<unsigned long long>(clock64() - t_start));
       }
     } else if (lane == 0) {  // ---------------- relay (odd CTA): data landed
       uint32_t ai = 0, bi = 0;
@@ -780,6 +814,8 @@ __global__ void __launch_bounds__(256) k_roots_to_chw(const int32_t* __restrict_
   for (int i = threadIdx.x; i < 8 * kPx; i += blockDim.x) dst[i] = t[i / kPx][i % kPx];
 }
 
+int32_t g_debug_flag = 0;
+
 template <int KIND>
 int launch_conv(const ConvParams& p, int num_sms, cudaStream_t s) {
   static bool configured = false;
@@ -852,7 +888,7 @@ extern "C" int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_
                arity_of, fid, child0, example, static_cast<const __nv_bfloat16*>(stage_in),
                static_cast<__nv_bfloat16*>(stage_out), plane_stride, inputs, values,
                reinterpret_cast<const __nv_bfloat16* const*>(wpack), bias, fwd_pos, fwd_slot,
-               static_cast<__nv_bfloat16*>(stage_x), static_cast<__nv_bfloat16*>(stage_cat)};
+               static_cast<__nv_bfloat16*>(stage_x), static_cast<__nv_bfloat16*>(stage_cat), g_debug_flag};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (kind) {
     case 0: return launch_conv<0>(p, num_sms, s);
@@ -880,5 +916,17 @@ extern "C" int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int
   if (total <= 0) return 0;
   k_roots_to_chw<<<static_cast<unsigned>(b * kPlanes), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       root_g, fid, arity_of, example, inputs, values, chw);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Copies (and optionally zeroes) the MMA-thread wait counters; enable != 0
+// turns accounting on for subsequent launches.
+extern "C" int dbk_rb_debug(unsigned long long* out, int32_t reset, int32_t enable) {
+  g_debug_flag = enable;
+  if (out) cudaMemcpyFromSymbol(out, g_conv_dbg, sizeof(unsigned long long) * 24);
+  if (reset) {
+    unsigned long long z[24] = {};
+    cudaMemcpyToSymbol(g_conv_dbg, z, sizeof(z));
+  }
   return static_cast<int>(cudaGetLastError());
 }
