@@ -120,162 +120,163 @@ struct ConvParams {
 __device__ unsigned long long g_conv_dbg[6 * 4];
 
 // Epilogue of one tile (256 positions = 2 TMEM accumulators) for this warp's
-// lane quarter and two 32-column chunks, in two phases: everything that does
-// not depend on the accumulator (row decoding, the member / residual /
-// forwarding pointer chase, the first residual chunk) is issued BEFORE the
-// wait for the MMAs, so its latency hides behind them.
-struct EpiRow {
-  int32_t q;
-  int32_t px;
-  int32_t rem;
-  bool valid;
-  bool keep32;
-  const float* res;   // residual row base (KIND 2), + px*8 applied
-  float* dst32;       // fp32 node-value row base, + px*8 applied
-  uint8_t* fbase;     // forwarded bf16 operand image row (KIND 2) or nullptr
-};
-
+// lane quarter and two 32-column chunks.
 template <int KIND>
-__device__ __forceinline__ void rb_epi_prepare(const ConvParams& P, int32_t g, int32_t q0, int quarter, int lane,
-                                               EpiRow (&rw)[2], const float*& bias) {
-  const int32_t f = P.group_fid[g];
-  const int32_t gb0 = P.group_begin[g];
-  const int32_t rows = P.group_begin[g + 1] - gb0;
-  const int32_t seg = P.seg_start[g];
-  bias = P.bias[f];
-  const bool binary = P.arity_of[f] == 2;
-#pragma unroll
-  for (int a = 0; a < 2; ++a) {
-    EpiRow& e = rw[a];
-    e.q = q0 + a * 128 + quarter * 32 + lane;
-    const int32_t local = e.q - seg;
-    const int32_t img = local / kImg;
-    e.rem = local - img * kImg;
-    const int32_t r = e.rem / 15, c = e.rem - r * 15;
-    e.valid = img < rows && r < 14 && c < 14;
-    e.px = r * 14 + c;
-    e.res = nullptr;
-    e.dst32 = nullptr;
-    e.fbase = nullptr;
-    e.keep32 = true;
-    if (e.valid && KIND != 1) {
-      const int32_t node = P.member_g[gb0 + img];
-      e.dst32 = P.values + static_cast<int64_t>(node) * kFmap + e.px * 8;
-      if (KIND == 2) {
-        if (binary) {
-          e.res = e.dst32;  // z was parked in the node's own slot by conv1x1
-        } else {
-          const int32_t ch = P.child0[node];
-          e.res = (P.arity_of[P.fid[ch]] == 0 ? P.inputs + static_cast<int64_t>(P.example[ch]) * kFmap
-                                              : P.values + static_cast<int64_t>(ch) * kFmap) + e.px * 8;
+__device__ __forceinline__ void rb_epilogue(const ConvParams& P, uint32_t tmem_base, int abuf, int32_t g,
+                                            int32_t q0, int quarter, int cb0, int lane) {
+      const int32_t f = P.group_fid[g];
+      const int32_t gb0 = P.group_begin[g];
+      const int32_t rows = P.group_begin[g + 1] - gb0;
+      const int32_t seg = P.seg_start[g];
+      const float* __restrict__ bias = P.bias[f];
+      const bool binary = P.arity_of[f] == 2;
+#pragma unroll 1
+      for (int a = 0; a < kTileM / 128; ++a) {
+        const int row = a * 128 + quarter * 32 + lane;
+        const int32_t q = q0 + row;
+        const int32_t local = q - seg;
+        const int32_t img = local / kImg, rem = local - img * kImg;
+        const int32_t r = rem / 15, c = rem - r * 15;
+        const bool valid = img < rows && r < 14 && c < 14;
+        const int32_t px = r * 14 + c;
+        int32_t node = 0;
+        const float* res = nullptr;
+        float* dst32 = nullptr;
+        if (valid && KIND != 1) {
+          node = P.member_g[gb0 + img];
+          dst32 = P.values + static_cast<int64_t>(node) * kFmap;
+          if (KIND == 2) {
+            if (binary) {
+              res = dst32;  // z was parked in the node's own slot by conv1x1
+            } else {
+              const int32_t ch = P.child0[node];
+              res = P.arity_of[P.fid[ch]] == 0 ? P.inputs + static_cast<int64_t>(P.example[ch]) * kFmap
+                                               : P.values + static_cast<int64_t>(ch) * kFmap;
+            }
+          }
         }
-        const int32_t tgt = P.fwd_pos[node];
-        const int32_t slot = P.fwd_slot[node];
-        e.keep32 = (slot >> 8) & 1;
-        if (tgt >= 0) {
-          e.fbase = reinterpret_cast<uint8_t*>((slot & 1) ? P.stage_cat : P.stage_x) +
-                    (static_cast<int64_t>((slot >> 1) & 31) * P.ps + kGuard + tgt + e.rem) * 16;
+        if constexpr (KIND == 2) {
+          // Residual rows are fetched one 32-channel chunk ahead of the TMEM
+          // loads so the epilogue keeps 8 independent 16-byte loads in flight
+          // (the residual may alias the destination for binary modules, so
+          // every chunk is fully loaded before any of its stores).
+          const float* rbase = valid ? res + px * 8 : nullptr;
+          float* dbase = valid ? dst32 + px * 8 : nullptr;
+          // forwarding target: the parent's bf16 operand image (if unique parent)
+          int32_t slot = 0;
+          uint8_t* fbase = nullptr;
+          if (valid) {
+            const int32_t tgt = P.fwd_pos[node];
+            slot = P.fwd_slot[node];
+            if (tgt >= 0) {
+              fbase = reinterpret_cast<uint8_t*>((slot & 1) ? P.stage_cat : P.stage_x) +
+                      (static_cast<int64_t>((slot >> 1) & 31) * P.ps + kGuard + tgt + rem) * 16;
+            }
+          }
+          const bool keep32 = (slot >> 8) & 1;
+          float4 rcur[8], rnext[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) rcur[i] = rnext[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid) {
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp) {
+              rcur[2 * pp] = *reinterpret_cast<const float4*>(rbase + (cb0 * 4 + pp) * kPx * 8);
+              rcur[2 * pp + 1] = *reinterpret_cast<const float4*>(rbase + (cb0 * 4 + pp) * kPx * 8 + 4);
+            }
+          }
+#pragma unroll
+          for (int cbi = 0; cbi < 2; ++cbi) {
+            const int cb = cb0 + cbi;
+            float v[32];
+            tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * 256 + a * 128 + cb * 32, v);
+            if (valid && cbi == 0) {
+#pragma unroll
+              for (int pp = 0; pp < 4; ++pp) {
+                const float* rp = rbase + ((cb + 1) * 4 + pp) * kPx * 8;
+                rnext[2 * pp] = *reinterpret_cast<const float4*>(rp);
+                rnext[2 * pp + 1] = *reinterpret_cast<const float4*>(rp + 4);
+              }
+            }
+            if (valid) {
+#pragma unroll
+              for (int pp = 0; pp < 4; ++pp) {
+                const int plane = cb * 4 + pp;
+                const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias + plane * 8));
+                const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias + plane * 8 + 4));
+                const float4 r0 = rcur[2 * pp], r1 = rcur[2 * pp + 1];
+                const float4 o0 = make_float4(fmaxf(v[pp * 8 + 0] + b_lo.x + r0.x, 0.f),
+                                              fmaxf(v[pp * 8 + 1] + b_lo.y + r0.y, 0.f),
+                                              fmaxf(v[pp * 8 + 2] + b_lo.z + r0.z, 0.f),
+                                              fmaxf(v[pp * 8 + 3] + b_lo.w + r0.w, 0.f));
+                const float4 o1 = make_float4(fmaxf(v[pp * 8 + 4] + b_hi.x + r1.x, 0.f),
+                                              fmaxf(v[pp * 8 + 5] + b_hi.y + r1.y, 0.f),
+                                              fmaxf(v[pp * 8 + 6] + b_hi.z + r1.z, 0.f),
+                                              fmaxf(v[pp * 8 + 7] + b_hi.w + r1.w, 0.f));
+                if (keep32) {
+                  float* dp = dbase + plane * kPx * 8;
+                  *reinterpret_cast<float4*>(dp) = o0;
+                  *reinterpret_cast<float4*>(dp + 4) = o1;
+                }
+                if (fbase) {
+                  uint4 pk;
+                  pk.x = pack_bf16x2(o0.x, o0.y);
+                  pk.y = pack_bf16x2(o0.z, o0.w);
+                  pk.z = pack_bf16x2(o1.x, o1.y);
+                  pk.w = pack_bf16x2(o1.z, o1.w);
+                  *reinterpret_cast<uint4*>(fbase + static_cast<int64_t>(plane) * P.ps * 16) = pk;
+                }
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) rcur[i] = rnext[i];
+          }
+          continue;
+        }
+        uint8_t* out16 = reinterpret_cast<uint8_t*>(P.stage_out) + static_cast<int64_t>(kGuard + q) * 16;
+#pragma unroll 1
+        for (int cbi = 0; cbi < 2; ++cbi) {
+          const int cb = cb0 + cbi;
+          float v[32];
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * 256 + a * 128 + cb * 32, v);
+#pragma unroll
+          for (int pp = 0; pp < 4; ++pp) {
+            const int plane = cb * 4 + pp;
+            const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias + plane * 8));
+            const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias + plane * 8 + 4));
+            float o[8] = {v[pp * 8 + 0] + b_lo.x, v[pp * 8 + 1] + b_lo.y, v[pp * 8 + 2] + b_lo.z,
+                          v[pp * 8 + 3] + b_lo.w, v[pp * 8 + 4] + b_hi.x, v[pp * 8 + 5] + b_hi.y,
+                          v[pp * 8 + 6] + b_hi.z, v[pp * 8 + 7] + b_hi.w};
+            if (KIND == 2) {
+              if (valid) {
+                const float* rp = res + (plane * kPx + px) * 8;
+                const float4 r0 = *reinterpret_cast<const float4*>(rp);
+                const float4 r1 = *reinterpret_cast<const float4*>(rp + 4);
+                o[0] += r0.x; o[1] += r0.y; o[2] += r0.z; o[3] += r0.w;
+                o[4] += r1.x; o[5] += r1.y; o[6] += r1.z; o[7] += r1.w;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] = fmaxf(o[i], 0.0f);
+                float* dp = dst32 + (plane * kPx + px) * 8;
+                *reinterpret_cast<float4*>(dp) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4*>(dp + 4) = make_float4(o[4], o[5], o[6], o[7]);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) o[i] = valid ? fmaxf(o[i], 0.0f) : 0.0f;
+              uint4 pk;
+              pk.x = pack_bf16x2(o[0], o[1]);
+              pk.y = pack_bf16x2(o[2], o[3]);
+              pk.z = pack_bf16x2(o[4], o[5]);
+              pk.w = pack_bf16x2(o[6], o[7]);
+              *reinterpret_cast<uint4*>(out16 + static_cast<int64_t>(plane) * P.ps * 16) = pk;
+              if (KIND == 0 && valid) {  // fp32 z for the residual of the block
+                float* dp = dst32 + (plane * kPx + px) * 8;
+                *reinterpret_cast<float4*>(dp) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4*>(dp + 4) = make_float4(o[4], o[5], o[6], o[7]);
+              }
+            }
+          }
         }
       }
-    }
-  }
-}
-
-// Residual chunk (4 planes × 8 channels of one row) into 8 float4.
-__device__ __forceinline__ void load_res_chunk(const EpiRow& e, int cb, float4 (&dst)[8]) {
-  if (!e.valid) return;
-#pragma unroll
-  for (int pp = 0; pp < 4; ++pp) {
-    const float* rp = e.res + (cb * 4 + pp) * kPx * 8;
-    dst[2 * pp] = *reinterpret_cast<const float4*>(rp);
-    dst[2 * pp + 1] = *reinterpret_cast<const float4*>(rp + 4);
-  }
-}
-
-template <int KIND>
-__device__ __forceinline__ void rb_epi_run(const ConvParams& P, uint32_t tmem_base, int abuf, int quarter, int cb0,
-                                           const EpiRow (&rw)[2], const float* __restrict__ bias,
-                                           float4 (&cur)[8]) {
-  // chunk order (a, cbi): (0,0) (0,1) (1,0) (1,1); cur holds the residual of
-  // the chunk being processed, nxt the prefetch of the following one.
-#pragma unroll
-  for (int step = 0; step < 4; ++step) {
-    const int a = step >> 1, cb = cb0 + (step & 1);
-    const EpiRow& e = rw[a];
-    float v[32];
-    tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * 256 + a * 128 + cb * 32, v);
-    float4 nxt[8];
-    if (KIND == 2 && step < 3) {
-      const int na = (step + 1) >> 1, ncb = cb0 + ((step + 1) & 1);
-      load_res_chunk(rw[na], ncb, nxt);
-    }
-#pragma unroll
-    for (int pp = 0; pp < 4; ++pp) {
-      const int plane = cb * 4 + pp;
-      const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias + plane * 8));
-      const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias + plane * 8 + 4));
-      float o[8] = {v[pp * 8 + 0] + b_lo.x, v[pp * 8 + 1] + b_lo.y, v[pp * 8 + 2] + b_lo.z,
-                    v[pp * 8 + 3] + b_lo.w, v[pp * 8 + 4] + b_hi.x, v[pp * 8 + 5] + b_hi.y,
-                    v[pp * 8 + 6] + b_hi.z, v[pp * 8 + 7] + b_hi.w};
-      if (KIND == 2) {
-        if (!e.valid) continue;
-        const float4 r0 = cur[2 * pp], r1 = cur[2 * pp + 1];
-        o[0] += r0.x; o[1] += r0.y; o[2] += r0.z; o[3] += r0.w;
-        o[4] += r1.x; o[5] += r1.y; o[6] += r1.z; o[7] += r1.w;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = fmaxf(o[i], 0.0f);
-        if (e.keep32) {
-          float* dp = e.dst32 + plane * kPx * 8;
-          *reinterpret_cast<float4*>(dp) = make_float4(o[0], o[1], o[2], o[3]);
-          *reinterpret_cast<float4*>(dp + 4) = make_float4(o[4], o[5], o[6], o[7]);
-        }
-        if (e.fbase) {
-          uint4 pk;
-          pk.x = pack_bf16x2(o[0], o[1]);
-          pk.y = pack_bf16x2(o[2], o[3]);
-          pk.z = pack_bf16x2(o[4], o[5]);
-          pk.w = pack_bf16x2(o[6], o[7]);
-          *reinterpret_cast<uint4*>(e.fbase + static_cast<int64_t>(plane) * P.ps * 16) = pk;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = e.valid ? fmaxf(o[i], 0.0f) : 0.0f;
-        uint4 pk;
-        pk.x = pack_bf16x2(o[0], o[1]);
-        pk.y = pack_bf16x2(o[2], o[3]);
-        pk.z = pack_bf16x2(o[4], o[5]);
-        pk.w = pack_bf16x2(o[6], o[7]);
-        uint8_t* out16 = reinterpret_cast<uint8_t*>(P.stage_out) + static_cast<int64_t>(kGuard + e.q) * 16;
-        *reinterpret_cast<uint4*>(out16 + static_cast<int64_t>(plane) * P.ps * 16) = pk;
-        if (KIND == 0 && e.valid) {  // fp32 z for the residual of the block
-          float* dp = e.dst32 + plane * kPx * 8;
-          *reinterpret_cast<float4*>(dp) = make_float4(o[0], o[1], o[2], o[3]);
-          *reinterpret_cast<float4*>(dp + 4) = make_float4(o[4], o[5], o[6], o[7]);
-        }
-      }
-    }
-    if (KIND == 2 && step < 3) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
-    }
-  }
-}
-
-// Full epilogue loop body for one tile: prepare → wait(acc_full) → run.
-template <int KIND>
-__device__ __forceinline__ void rb_epilogue_tile(const ConvParams& P, uint32_t tmem_base, int abuf, uint32_t parity,
-                                                 uint64_t* acc_full, int32_t g, int32_t q0, int quarter, int cb0,
-                                                 int lane) {
-  EpiRow rw[2];
-  const float* bias;
-  rb_epi_prepare<KIND>(P, g, q0, quarter, lane, rw, bias);
-  float4 cur[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) cur[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (KIND == 2) load_res_chunk(rw[0], cb0, cur);
-  mbar_wait(acc_full, parity);
-  tc_fence_after();
-  rb_epi_run<KIND>(P, tmem_base, abuf, quarter, cb0, rw, bias, cur);
 }
 
 template <int KIND>
@@ -405,7 +406,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
       const int abuf = it & 1;
       const int32_t g = P.tile_group[t_begin + t];
       const int32_t q0 = P.tile_q0[t_begin + t];
-      rb_epilogue_tile<KIND>(P, tmem_base, abuf, (it >> 1) & 1, acc_full + abuf, g, q0, quarter, cb0, lane);
+      mbar_wait(acc_full + abuf, (it >> 1) & 1);
+      tc_fence_after();
+      rb_epilogue<KIND>(P, tmem_base, abuf, g, q0, quarter, cb0, lane);
       tc_fence_before();
       mbar_arrive(acc_empty + abuf);
     }
@@ -590,7 +593,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int abuf = it & 1;
       const int32_t g = P.tile_group[t_begin + t];
       const int32_t q0 = P.tile_q0[t_begin + t] + static_cast<int32_t>(rank) * kTileM;
-      rb_epilogue_tile<KIND>(P, tmem_base, abuf, (it >> 1) & 1, acc_full + abuf, g, q0, quarter, cb0, lane);
+      mbar_wait(acc_full + abuf, (it >> 1) & 1);
+      tc_fence_after();
+      rb_epilogue<KIND>(P, tmem_base, abuf, g, q0, quarter, cb0, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
