@@ -20,14 +20,31 @@ IepSession::~IepSession() {
 
 namespace {
 
-std::uint16_t to_bf16(double v) {
-  // round-to-nearest-even of the fp32 value, as __float2bfloat16_rn does
-  float f = static_cast<float>(v);
-  std::uint32_t u;
-  std::memcpy(&u, &f, 4);
-  const std::uint32_t lsb = (u >> 16) & 1u;
-  u += 0x7FFFu + lsb;
-  return static_cast<std::uint16_t>(u >> 16);
+// fp32 → fp16 bits, round to nearest even, subnormals kept (the tensor-core
+// operands of the conv kernels are fp16: 2^-11 relative rounding vs bf16's 2^-9).
+std::uint16_t to_f16(double v) {
+  const float f = static_cast<float>(v);
+  std::uint32_t x;
+  std::memcpy(&x, &f, 4);
+  const std::uint32_t sign = (x >> 16) & 0x8000u;
+  const std::uint32_t e8 = (x >> 23) & 0xffu;
+  std::uint32_t mant = x & 0x7fffffu;
+  if (e8 == 0xffu) return static_cast<std::uint16_t>(sign | 0x7c00u | (mant ? 0x200u : 0u));
+  const std::int32_t e = static_cast<std::int32_t>(e8) - 127 + 15;
+  if (e >= 31) return static_cast<std::uint16_t>(sign | 0x7c00u);
+  if (e <= 0) {
+    if (e < -10) return static_cast<std::uint16_t>(sign);
+    mant |= 0x800000u;
+    const std::uint32_t shift = static_cast<std::uint32_t>(14 - e);
+    std::uint32_t h = mant >> shift;
+    const std::uint32_t rem = mant & ((1u << shift) - 1u), halfway = 1u << (shift - 1u);
+    if (rem > halfway || (rem == halfway && (h & 1u))) ++h;
+    return static_cast<std::uint16_t>(sign | h);
+  }
+  std::uint32_t h = (static_cast<std::uint32_t>(e) << 10) | (mant >> 13);
+  const std::uint32_t rem = mant & 0x1fffu;
+  if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;
+  return static_cast<std::uint16_t>(sign | h);
 }
 
 // Weights are streamed as 16 KB blocks, one per (64-channel K chunk, tap) in
@@ -47,7 +64,7 @@ std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int 
       for (int co = 0; co < C; ++co) {
         const size_t off = pair ? static_cast<size_t>(co / 64) * (block / 2) + (static_cast<size_t>(k / 8) * 64 + co % 64) * 8 + k % 8
                                 : (static_cast<size_t>(k / 8) * C + co) * 8 + k % 8;
-        out[base + off] = to_bf16(w[(static_cast<size_t>(tap) * cin + ci) * C + co]);
+        out[base + off] = to_f16(w[(static_cast<size_t>(tap) * cin + ci) * C + co]);
       }
     }
   return out;

@@ -11,7 +11,7 @@
 // Data layout:
 //   * node values / inputs: fp32 "plane maps" [16 planes][196 px][8 ch]
 //     (plane j = channels 8j..8j+7) — 100,352 B per node;
-//   * per-step staging: bf16 planes over a packed position axis. Each image
+//   * per-step staging: fp16 planes over a packed position axis. Each image
 //     occupies a 15×15 grid (225 positions; row 14 and column 14 are zero
 //     pads shared with the next image / row), so a 3×3 tap (dh, dw) is the
 //     row shift dh·15 + dw of the same array. Images of one call group are
@@ -219,10 +219,10 @@ __device__ __forceinline__ void rb_epilogue(const ConvParams& P, uint32_t tmem_b
                 }
                 if (fbase) {
                   uint4 pk;
-                  pk.x = pack_bf16x2(o0.x, o0.y);
-                  pk.y = pack_bf16x2(o0.z, o0.w);
-                  pk.z = pack_bf16x2(o1.x, o1.y);
-                  pk.w = pack_bf16x2(o1.z, o1.w);
+                  pk.x = pack_f16x2(o0.x, o0.y);
+                  pk.y = pack_f16x2(o0.z, o0.w);
+                  pk.z = pack_f16x2(o1.x, o1.y);
+                  pk.w = pack_f16x2(o1.z, o1.w);
                   *reinterpret_cast<uint4*>(fbase + static_cast<int64_t>(plane) * P.ps * 16) = pk;
                 }
               }
@@ -263,10 +263,10 @@ __device__ __forceinline__ void rb_epilogue(const ConvParams& P, uint32_t tmem_b
 #pragma unroll
               for (int i = 0; i < 8; ++i) o[i] = valid ? fmaxf(o[i], 0.0f) : 0.0f;
               uint4 pk;
-              pk.x = pack_bf16x2(o[0], o[1]);
-              pk.y = pack_bf16x2(o[2], o[3]);
-              pk.z = pack_bf16x2(o[4], o[5]);
-              pk.w = pack_bf16x2(o[6], o[7]);
+              pk.x = pack_f16x2(o[0], o[1]);
+              pk.y = pack_f16x2(o[2], o[3]);
+              pk.z = pack_f16x2(o[4], o[5]);
+              pk.w = pack_f16x2(o[6], o[7]);
               *reinterpret_cast<uint4*>(out16 + static_cast<int64_t>(plane) * P.ps * 16) = pk;
               if (KIND == 0 && valid) {  // fp32 z for the residual of the block
                 float* dp = dst32 + (plane * kPx + px) * 8;
@@ -283,7 +283,7 @@ template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__ ConvParams P) {
   using K = Cfg<KIND>;
   constexpr int WIN = win<KIND>();
-  constexpr uint32_t IDESC = idesc_bf16_f32(128, 128);
+  constexpr uint32_t IDESC = idesc_f16_f32(128, 128);
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + kASlots * a_slot_bytes<KIND>();
@@ -452,7 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   using K = Cfg<KIND>;
   constexpr int NB = PairCfg<KIND>::kBStages;
   constexpr int WIN = win<KIND>();
-  constexpr uint32_t IDESC = idesc_bf16_f32(256, 128);
+  constexpr uint32_t IDESC = idesc_f16_f32(256, 128);
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + kASlots * a_slot_bytes<KIND>();
@@ -769,10 +769,10 @@ __global__ void __launch_bounds__(256) k_rb_gather(
         const float4 lo = *reinterpret_cast<const float4*>(sp);
         const float4 hi = *reinterpret_cast<const float4*>(sp + 4);
         uint4 pk;
-        pk.x = pack_bf16x2(lo.x, lo.y);
-        pk.y = pack_bf16x2(lo.z, lo.w);
-        pk.z = pack_bf16x2(hi.x, hi.y);
-        pk.w = pack_bf16x2(hi.z, hi.w);
+        pk.x = pack_f16x2(lo.x, lo.y);
+        pk.y = pack_f16x2(lo.z, lo.w);
+        pk.z = pack_f16x2(hi.x, hi.y);
+        pk.w = pack_f16x2(hi.z, hi.w);
         *reinterpret_cast<uint4*>(dst + (static_cast<int64_t>(16 * k + p) * ps + base + r * 15 + c) * 16) = pk;
       }
     }
