@@ -237,11 +237,14 @@ def run_ours(args, dist):
 
     dist.barrier()
     t0 = time.time()
-    ms, kt = sess.time(args.steps, profile=True)
+    ms, _ = sess.time(args.steps)  # headline: no per-launch events inside the timed loop
     dist.barrier()
     clk.mark(t0, time.time())
     ms_step = dist.max(ms / args.steps)
     value = per * N / (ms_step / 1e3)
+    # second pass with events around every launch: per-kernel-class times
+    # for the roofline and the breakdown (not the headline)
+    pms, kt = sess.time(args.steps, profile=True)
 
     # end-to-end through the public API: pinned host fp32 inputs → H2D →
     # forward → D2H of the root outputs, every step (wall clock, max over ranks)
@@ -272,7 +275,7 @@ def run_ours(args, dist):
                 "traffic": traffic,
                 "algorithmic_flops_per_launch": conv_flops / max(conv_launches, 1),
                 "avg_launch_ms": conv_ms / max(conv_launches, 1),
-                "share_of_step": round(conv_ms / ms, 4) if ms > 0 else None}
+                "share_of_step": round(conv_ms / pms, 4) if pms > 0 else None}
     kernels = {db.KERNEL_CLASSES[c]: {"ms_per_step": kt.ms[c] / args.steps,
                                       "launches_per_step": kt.launches[c] / args.steps,
                                       "tflops": (kt.flops[c] / (kt.ms[c] / 1e3) / 1e12) if kt.ms[c] and kt.flops[c] else None,
@@ -281,7 +284,8 @@ def run_ours(args, dist):
 
     out = {"metric": METRIC, "value": value, "unit": "programs/s", "n_gpus": N,
            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "fp16 tensor-core operands, fp32 accumulate and node values",
            "data": "synthetic (reference generators, seed 0; random-init weights)",
            "config": {"workload": f"{args.workload}: IEP forward, {cfg['kind']} programs p={cfg['vocab']} "
                                   f"len<={cfg['length']} branch={cfg['branch_prob']}, residual conv "
@@ -290,6 +294,7 @@ def run_ours(args, dist):
                       "parallelism": f"dp{N} (program shards, no collective)",
                       "l2": "inputs (411 MB) and node values (4.9 GB) exceed the 126 MB L2"},
            "e2e": e2e, "roofline": roofline, "kernels": kernels,
+           "profiled_ms_per_step": pms / args.steps,
            "gpu_launches": int(stats.kernel_launches) * args.steps,
            "schedule": {"steps": stats.steps, "groups": stats.groups,
                         "expensive_calls": stats.expensive_calls,
@@ -348,9 +353,10 @@ def run_moe(args, dist, name, secondary=False):
     sess.time(3)
     st = sess.stats()
     dist.barrier()
-    ms, kt = sess.time(args.steps, profile=True)
+    ms, _ = sess.time(args.steps)
     dist.barrier()
     ms_step = dist.max(ms / args.steps)
+    _, kt = sess.time(args.steps, profile=True)
     peaks, src = measured_peaks()
     g_ms, g_fl = kt.ms[4] + kt.ms[5], kt.flops[4] + kt.flops[5]
     gemm_tf = g_fl / (g_ms / 1e3) / 1e12 if g_ms else 0.0

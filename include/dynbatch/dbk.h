@@ -67,7 +67,7 @@ int dbk_dense_gather_roots(int64_t b, int32_t width, const int32_t* root_g,
 
 /* ------------------------------------------------------- resblock (Tier B)
  * Maps are C=128 × 14 × 14. Node values / inputs are fp32 "plane maps"
- * [16 planes][196 px][8 ch]; per-step staging is bf16 planes over a packed,
+ * [16 planes][196 px][8 ch]; per-step staging is fp16 planes over a packed,
  * zero-padded 15×15 position grid (rb_conv.cu header). */
 
 /* Per step: segment starts (seg_start[g], -1 for leaf groups), tile lists
@@ -81,7 +81,7 @@ int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t*
                 const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t tile_m,
                 void* stream);
 /* Gather of the operands of step `step` that no child epilogue forwarded
- * (leaves, shared children) into the bf16 staging planes, with the binary
+ * (leaves, shared children) into the fp16 staging planes, with the binary
  * channel concat fused into the write; plane_stride in positions. */
 int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_fid,
                   const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
@@ -90,9 +90,9 @@ int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* 
                   const float* inputs, const float* values, void* stage_x, void* stage_cat,
                   int64_t plane_stride, int32_t blocks, void* stream);
 /* tcgen05 implicit-GEMM convolutions: kind 0 = conv1x1 over [x; y] → z
- * (bf16 staging + fp32 parked in the node slot), 1 = conv3x3 #1 → mid
- * (bf16), 2 = conv3x3 #2 + residual + ReLU → fp32 node values (when a
- * reader needs them) and the bf16 operand image of the parent's call.
+ * (fp16 staging + fp32 parked in the node slot), 1 = conv3x3 #1 → mid
+ * (fp16), 2 = conv3x3 #2 + residual + ReLU → fp32 node values (when a
+ * reader needs them) and the fp16 operand image of the parent's call.
  * kind + 16 selects the CTA-pair (cta_group::2) variant, which needs a plan
  * with tile_m = 512 and weights packed as two 64-channel halves per block. */
 int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,

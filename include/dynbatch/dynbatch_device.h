@@ -14,7 +14,7 @@
  *   DB_MODULE_RESBLOCK — the north-star IEP residual block on C×H×W maps
  *                        (C = 128, 14×14): unary y = relu(x + conv3(relu(conv3(x)))),
  *                        binary z = relu(conv1x1([x;y])) then the unary block;
- *                        tcgen05/TMEM implicit-GEMM kernels, bf16 operands,
+ *                        tcgen05/TMEM implicit-GEMM kernels, fp16 operands,
  *                        fp32 accumulation and fp32 node values.
  * MoE precisions:
  *   DB_MOE_FP64 — reference arithmetic order (src/moe.cpp:98-145, 254-264).

@@ -16,8 +16,8 @@ struct IepSession::RB {
   Buf<float> inputs;              // [b][kFmap] plane maps
   Buf<float> values;              // [N][kFmap] node values (and parked z)
   Buf<float> chw_in, chw_out;     // reference-layout rows for host I/O
-  Buf<std::uint16_t> stage_x, stage_cat, stage_mid;  // bf16 staging
-  std::vector<Buf<std::uint16_t>> wbuf;              // packed bf16 weights
+  Buf<std::uint16_t> stage_x, stage_cat, stage_mid;  // fp16 staging
+  std::vector<Buf<std::uint16_t>> wbuf;              // packed fp16 weights
   std::vector<Buf<float>> bbuf;
   Buf<const void*> w0tab, w1tab, w2tab;
   Buf<const float*> b0tab, b1tab, b2tab;

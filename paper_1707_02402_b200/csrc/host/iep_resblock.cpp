@@ -79,9 +79,11 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   if (c.max_arity > 2) throw_error(Errc::arity_mismatch, "resblock modules support arity <= 2");
   rb_ = std::make_unique<RB>();
   RB& R = *rb_;
-  // CTA-pair (cta_group::2) conv kernels unless DYNBATCH_CONV_PAIR=0.
+  // Single-CTA conv kernels; DYNBATCH_CONV_PAIR=1 selects the CTA-pair
+  // (cta_group::2) variants (measured slower on these M=256-tile shapes,
+  // profiles/r01_conv_waits.txt).
   const char* pe = std::getenv("DYNBATCH_CONV_PAIR");
-  R.pair = !(pe && pe[0] == '0');
+  R.pair = pe && pe[0] == '1';
   R.tile_m = R.pair ? 2 * RB::kTileM : RB::kTileM;
   for (std::int64_t g = 0; g < c.N; ++g)
     if (c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0) ++R.n_expensive;

@@ -30,7 +30,7 @@
 //   warp 1 — TMEM allocator + single-thread tcgen05.mma issuer
 //            (M = 128 per accumulator, N = 128, K = 16 per instruction);
 //   warps 2-5 — epilogue: tcgen05.ld of the fp32 accumulators, bias, ReLU,
-//            residual, pad masking, bf16 staging / fp32 node-value stores.
+//            residual, pad masking, fp16 staging / fp32 node-value stores.
 // Accumulators are double-buffered in TMEM (2 × 256 columns) so the epilogue
 // of tile i overlaps the MMAs of tile i+1.
 #include <cuda_bf16.h>
@@ -52,7 +52,7 @@ constexpr int kFmap = kPlanes * kPx * 8;  // 25,088 floats per node map
 constexpr int kGuard = 32;           // zero positions before position 0
 constexpr int kTileM = 256;          // positions per CTA tile (2 accumulators)
 constexpr int kChunkPlanes = 8;      // K chunk = 64 input channels = 8 planes
-constexpr int kBStage = 128 * 64 * 2;  // 16 KB: N=128 × K=64 bf16 weight block
+constexpr int kBStage = 128 * 64 * 2;  // 16 KB: N=128 × K=64 fp16 weight block
 constexpr int kASlots = 2;           // A window double-buffered per K chunk
 constexpr int kEpiWarps = 8;       // two warps per TMEM lane quarter, two column chunks each
 constexpr int kThreads = 64 + kEpiWarps * 32;
@@ -103,7 +103,7 @@ struct ConvParams {
   float* values;
   const __nv_bfloat16* const* wpack;
   const float* const* bias;
-  // conv3x3 #2 only: forwarding of each result as the bf16 operand image of
+  // conv3x3 #2 only: forwarding of each result as the fp16 operand image of
   // its (unique) parent's call — fwd_pos[g] = absolute staging position of
   // the parent's image (-1: none), fwd_slot[g] = buffer (bit 0: 0 stage_x,
   // 1 stage_cat) | first plane << 1 | keep-fp32-value << 8.
@@ -162,7 +162,7 @@ __device__ __forceinline__ void rb_epilogue(const ConvParams& P, uint32_t tmem_b
           // every chunk is fully loaded before any of its stores).
           const float* rbase = valid ? res + px * 8 : nullptr;
           float* dbase = valid ? dst32 + px * 8 : nullptr;
-          // forwarding target: the parent's bf16 operand image (if unique parent)
+          // forwarding target: the parent's fp16 operand image (if unique parent)
           int32_t slot = 0;
           uint8_t* fbase = nullptr;
           if (valid) {
@@ -734,7 +734,7 @@ __global__ void k_rb_tiles(int32_t n_steps, const int32_t* __restrict__ sgb,
 // --------------------------------------------------------------- gather
 // Packs the operand maps that were NOT forwarded by a child's conv3x3 #2
 // epilogue — leaves (the example's input map) and children shared by
-// several parents — into the member's bf16 staging image: unary → stage_x
+// several parents — into the member's fp16 staging image: unary → stage_x
 // (16 planes), binary → stage_cat planes 16k.. (the channel concat of
 // [x; y] is fused into the write). Only the 196 data positions are written;
 // pads and alignment gaps were zeroed once at session creation.

@@ -101,7 +101,7 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// D[tmem] (+)= A[smem] · B[smem]^T, kind::f16 (bf16 in, fp32 accumulate).
+// D[tmem] (+)= A[smem] · B[smem]^T, kind::f16 (bf16 or fp16 in per idesc, fp32 accumulate).
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(

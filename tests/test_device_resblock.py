@@ -1,14 +1,14 @@
 """GPU parity of the Tier-B module body (residual conv blocks on 128×14×14
-maps, tcgen05 implicit GEMM, bf16 operands / fp32 accumulation and fp32
+maps, tcgen05 implicit GEMM, fp16 operands / fp32 accumulation and fp32
 node values) against the fp64 CPU oracle (oracle/dynbatch_oracle.c,
 orc_execute kind=resblock — parity unpinned by the reference, which has no
 conv module; executor semantics pinned).
 
-Stated tolerance: max|dev − ref| / max|ref| ≤ 5e-3 per batch,
-and per element |dev − ref| ≤ 2e-2·(|ref| + rms(ref)). The bf16 operand
-rounding (2^-9 relative) bounds one conv's relative error near 2e-3; the
-fp32 residual stream keeps the chain from compounding it (measured ≈2e-3
-normalised over 15 levels in a torch fp64 simulation).
+Stated tolerance: max|dev − ref| / max|ref| ≤ 1e-3 per batch
+(the north star's figure), and per element |dev − ref| ≤ 5e-3·(|ref| +
+rms(ref)). fp16 operand rounding is 2^-11 relative; the fp32 residual stream
+keeps a chain from compounding it (measured on B200: 1.1e-4 normalised and
+8.7e-4 element-wise over 11–14 levels, profiles/resblock_error.py).
 """
 import numpy as np
 import pytest
@@ -28,8 +28,10 @@ def conv_variant(request, monkeypatch):
     the single-CTA kernels (DYNBATCH_CONV_PAIR=0)."""
     monkeypatch.setenv("DYNBATCH_CONV_PAIR", "1" if request.param == "pair" else "0")
     return request.param
-TOL_NORM = 5e-3
-TOL_ELEM = 2e-2
+
+
+TOL_NORM = 1e-3
+TOL_ELEM = 5e-3
 
 
 def _check(dev, ref):
