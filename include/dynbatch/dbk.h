@@ -93,17 +93,20 @@ int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* 
  * (fp16 staging + fp32 parked in the node slot), 1 = conv3x3 #1 → mid
  * (fp16), 2 = conv3x3 #2 + residual + ReLU → fp32 node values (when a
  * reader needs them) and the fp16 operand image of the parent's call.
- * kind + 16 selects the CTA-pair (cta_group::2) variant, which needs a plan
- * with tile_m = 512 and weights packed as two 64-channel halves per block. */
+ * One CTA per SM, D[128 channels][256 positions] per tile (MMA N = 256). */
 int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
                 const int32_t* tile_group, const int32_t* tile_q0, const int32_t* group_fid,
-                const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
-                const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
-                const int32_t* example, const void* stage_in, void* stage_out,
-                int64_t plane_stride, const float* inputs, float* values,
-                const void* const* wpack, const float* const* bias, const int32_t* fwd_pos,
-                const int32_t* fwd_slot, void* stage_x, void* stage_cat, int32_t num_sms,
-                void* stream);
+                const int32_t* group_begin, const int32_t* seg_start, const void* memtab,
+                const void* stage_in, void* stage_out, int64_t plane_stride, const void* const* wpack,
+                const float* const* bias, int32_t num_sms, void* stream);
+/* Per-member epilogue table (32 bytes per member, schedule order: residual
+ * source, own slot, forwarding target, keep-fp32 flag), built after
+ * dbk_rb_plan from its forwarding tables. */
+int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
+                  const int32_t* group_begin, const int32_t* arity_of, const int32_t* seg_start,
+                  const int32_t* member_g, const int32_t* fid, const int32_t* child0, const int32_t* example,
+                  const int32_t* fwd_pos, const int32_t* fwd_slot, const float* inputs, float* values,
+                  void* stage_x, void* stage_cat, int64_t plane_stride, void* memtab, void* stream);
 int dbk_rb_debug(unsigned long long* out24, int32_t reset, int32_t enable);
 int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream);
 int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int32_t* fid,

@@ -23,9 +23,9 @@ struct IepSession::RB {
   Buf<const float*> b0tab, b1tab, b2tab;
   Buf<std::int32_t> seg_start, group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
       step_positions, tile_group, tile_q0, bin_group, bin_q0, fwd_ok, fwd_pos, fwd_slot;
+  Buf<std::uint64_t> memtab;  // per-member epilogue metadata, 32 bytes each (rb_conv.cu MemberEntry)
   std::int64_t n_expensive = 0;
-  bool pair = true;   // CTA-pair conv kernels
-  int tile_m = 512;   // positions per scheduled tile (per pair when pair)
+  int tile_m = kTileM;  // positions per scheduled tile
 };
 
 }  // namespace dynbatch::dev

@@ -52,9 +52,8 @@ std::uint16_t to_f16(double v) {
 // ((k/8)·128 + n)·8 + k%8 (K-major, no swizzle).
 constexpr int kKChunk = 64;
 
-// pair = true (CTA-pair kernels): each block is two contiguous 8 KB halves
-// of 64 output channels, [half][k/8][64][8], one per CTA of the pair.
-std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int cin, int taps, bool pair) {
+// The block is the A operand (M = 128 output channels) of the conv MMAs.
+std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int cin, int taps) {
   std::vector<std::uint16_t> out(static_cast<size_t>(taps) * cin * C);
   const size_t block = static_cast<size_t>(kKChunk) * C;
   for (int tap = 0; tap < taps; ++tap)
@@ -62,8 +61,7 @@ std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int 
       const int chunk = ci / kKChunk, k = ci % kKChunk;
       const size_t base = static_cast<size_t>(chunk * taps + tap) * block;
       for (int co = 0; co < C; ++co) {
-        const size_t off = pair ? static_cast<size_t>(co / 64) * (block / 2) + (static_cast<size_t>(k / 8) * 64 + co % 64) * 8 + k % 8
-                                : (static_cast<size_t>(k / 8) * C + co) * 8 + k % 8;
+        const size_t off = (static_cast<size_t>(k / 8) * C + co) * 8 + k % 8;
         out[base + off] = to_f16(w[(static_cast<size_t>(tap) * cin + ci) * C + co]);
       }
     }
@@ -79,12 +77,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   if (c.max_arity > 2) throw_error(Errc::arity_mismatch, "resblock modules support arity <= 2");
   rb_ = std::make_unique<RB>();
   RB& R = *rb_;
-  // Single-CTA conv kernels; DYNBATCH_CONV_PAIR=1 selects the CTA-pair
-  // (cta_group::2) variants (measured slower on these M=256-tile shapes,
-  // profiles/r01_conv_waits.txt).
-  const char* pe = std::getenv("DYNBATCH_CONV_PAIR");
-  R.pair = pe && pe[0] == '1';
-  R.tile_m = R.pair ? 2 * RB::kTileM : RB::kTileM;
+  R.tile_m = RB::kTileM;
   for (std::int64_t g = 0; g < c.N; ++g)
     if (c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0) ++R.n_expensive;
   const size_t b = static_cast<size_t>(std::max<std::int64_t>(c.b, 1));
@@ -112,6 +105,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
     R.fwd_ok.upload(ok, stream_);
     R.fwd_pos.alloc(N);
     R.fwd_slot.alloc(N);
+    R.memtab.alloc(N * 4);
   }
   const size_t ps = static_cast<size_t>(R.plane_stride);
   R.stage_x.alloc(ps * 16 * 8);
@@ -123,7 +117,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   // schedule-derived tables (G ≤ max keys; tiles ≤ N_exp·225/256 + G)
   const size_t G = static_cast<size_t>(std::max(1, c.s_max)) * c.p + 2;
   const size_t S = static_cast<size_t>(std::max<std::int64_t>(c.N, 1)) + 2;  // naive: S = N
-  const size_t T = static_cast<size_t>(R.n_expensive) * 225 / RB::kTileM + G + 2;  // bound for either tile size
+  const size_t T = static_cast<size_t>(R.n_expensive) * 225 / RB::kTileM + G + 2;
   R.seg_start.alloc(std::max(G, N + 2));
   R.group_tile0.alloc(std::max(G, N + 2));
   R.group_bintile0.alloc(std::max(G, N + 2));
@@ -153,12 +147,12 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
       return static_cast<const float*>(R.bbuf.back().get());
     };
     if (a == 2) {
-      w0[static_cast<size_t>(f)] = put_w(pack_blocks(m.w0, C, 2 * C, 1, R.pair));
+      w0[static_cast<size_t>(f)] = put_w(pack_blocks(m.w0, C, 2 * C, 1));
       b0[static_cast<size_t>(f)] = put_b(m.b0);
     }
-    w1[static_cast<size_t>(f)] = put_w(pack_blocks(m.w1, C, C, 9, R.pair));
+    w1[static_cast<size_t>(f)] = put_w(pack_blocks(m.w1, C, C, 9));
     b1[static_cast<size_t>(f)] = put_b(m.b1);
-    w2[static_cast<size_t>(f)] = put_w(pack_blocks(m.w2, C, C, 9, R.pair));
+    w2[static_cast<size_t>(f)] = put_w(pack_blocks(m.w2, C, C, 9));
     b2[static_cast<size_t>(f)] = put_b(m.b2);
   }
   R.w0tab.upload(w0, stream_);
@@ -182,14 +176,19 @@ void IepSession::forward_resblock() {
     layout_dirty_ = false;
   }
   prof_.begin(1, stream_);
-    check(dbk_rb_plan(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
+  check(dbk_rb_plan(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
                     R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(), R.step_tile_begin.get(),
                     R.step_bintile_begin.get(), R.step_positions.get(), R.tile_group.get(), R.tile_q0.get(),
                     R.bin_group.get(), R.bin_q0.get(), B.csr().N, B.member_g.get(), B.child0.get(),
                     B.child1.get(), R.fwd_ok.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.tile_m, stream_),
         "dbk_rb_plan");
-    prof_.end(stream_);
-  launches_ += 4;
+  check(dbk_rb_memtab(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
+                      R.seg_start.get(), B.member_g.get(), B.fid.get(), B.child0.get(), B.example.get(),
+                      R.fwd_pos.get(), R.fwd_slot.get(), R.inputs.get(), R.values.get(), R.stage_x.get(),
+                      R.stage_cat.get(), R.plane_stride, R.memtab.get(), stream_),
+        "dbk_rb_memtab");
+  prof_.end(stream_);
+  launches_ += 5;
   const int gather_blocks = static_cast<int>(std::min<std::int64_t>(std::max<std::int64_t>(R.n_expensive, 1), sms * 8));
   for (int s = 0; s < S; ++s) {
     prof_.begin(2, stream_);
@@ -202,28 +201,21 @@ void IepSession::forward_resblock() {
     prof_.end(stream_);
     // conv1x1 over the binary groups' [x; y] → z (stage_x + parked fp32)
     prof_.begin(3, stream_);
-    const int kp = R.pair ? 16 : 0;
-    check(dbk_rb_conv(0 + kp, s, R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
-                      B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
-                      B.child0.get(), B.example.get(), R.stage_cat.get(), R.stage_x.get(), R.plane_stride,
-                      R.inputs.get(), R.values.get(), R.w0tab.get(), R.b0tab.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.stage_x.get(),
-                      R.stage_cat.get(), sms, stream_),
+    check(dbk_rb_conv(0, s, R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
+                      B.group_begin.get(), R.seg_start.get(), R.memtab.get(), R.stage_cat.get(), R.stage_x.get(),
+                      R.plane_stride, R.w0tab.get(), R.b0tab.get(), sms, stream_),
           "conv1x1");
     prof_.end(stream_);
     prof_.begin(4, stream_);
-    check(dbk_rb_conv(1 + kp, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
-                      B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
-                      B.child0.get(), B.example.get(), R.stage_x.get(), R.stage_mid.get(), R.plane_stride,
-                      R.inputs.get(), R.values.get(), R.w1tab.get(), R.b1tab.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.stage_x.get(),
-                      R.stage_cat.get(), sms, stream_),
+    check(dbk_rb_conv(1, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
+                      B.group_begin.get(), R.seg_start.get(), R.memtab.get(), R.stage_x.get(), R.stage_mid.get(),
+                      R.plane_stride, R.w1tab.get(), R.b1tab.get(), sms, stream_),
           "conv3x3 #1");
     prof_.end(stream_);
     prof_.begin(5, stream_);
-    check(dbk_rb_conv(2 + kp, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
-                      B.group_begin.get(), R.seg_start.get(), B.member_g.get(), B.arity_of.get(), B.fid.get(),
-                      B.child0.get(), B.example.get(), R.stage_mid.get(), nullptr, R.plane_stride,
-                      R.inputs.get(), R.values.get(), R.w2tab.get(), R.b2tab.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.stage_x.get(),
-                      R.stage_cat.get(), sms, stream_),
+    check(dbk_rb_conv(2, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
+                      B.group_begin.get(), R.seg_start.get(), R.memtab.get(), R.stage_mid.get(), nullptr,
+                      R.plane_stride, R.w2tab.get(), R.b2tab.get(), sms, stream_),
           "conv3x3 #2");
     prof_.end(stream_);
     launches_ += 4;

@@ -19,21 +19,26 @@
 //     tile never mixes weights. Plane j of position q lives at
 //     ((j·PS) + GUARD + q) · 16 bytes.
 //   * tensor-core operands use the K-major SWIZZLE_NONE canonical layout
-//     (tc_common.cuh): the shared-memory A window [plane][position][8] is a
-//     valid operand starting at ANY position, so all nine taps read the same
-//     window at different row offsets — the im2col never materialises.
+//     (tc_common.cuh): the shared-memory activation window
+//     [plane][position][8] is a valid operand starting at ANY position, so
+//     all nine taps read the same window at different row offsets — the
+//     im2col never materialises.
 //
 // Kernel (one CTA per SM, persistent over the step's tile list):
-//   warp 0 — producer: bulk async copies (TMA engine) of the A window
-//            (TILE_M + 32 positions × all input planes) and a ring of 32 KB
-//            weight stages (one 3×3 tap, or one 128-channel half of the 1×1);
-//   warp 1 — TMEM allocator + single-thread tcgen05.mma issuer
-//            (M = 128 per accumulator, N = 128, K = 16 per instruction);
-//   warps 2-5 — epilogue: tcgen05.ld of the fp32 accumulators, bias, ReLU,
+//   warp 0 — producer: bulk async copies (TMA engine) of the activation
+//            window per 64-channel K chunk (TILE_M + 2·halo positions × 8
+//            planes, double-buffered) and a ring of 16 KB weight stages
+//            (one (chunk, tap) block each);
+//   warp 1 — TMEM allocator + single-thread tcgen05.mma issuer:
+//            D[128 out channels][256 positions] (M = 128, N = 256, K = 16),
+//            A = weight stage, B = window at the tap's row shift;
+//   warps 2-9 — epilogue: per-tile position table in shared memory, then
+//            tcgen05.ld (lane = channel, 32 positions per load), bias, ReLU,
 //            residual, pad masking, fp16 staging / fp32 node-value stores.
 // Accumulators are double-buffered in TMEM (2 × 256 columns) so the epilogue
 // of tile i overlaps the MMAs of tile i+1.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -50,12 +55,13 @@ constexpr int kImg = 225;            // 15 × 15 packed grid per image
 constexpr int kPx = 196;             // 14 × 14
 constexpr int kFmap = kPlanes * kPx * 8;  // 25,088 floats per node map
 constexpr int kGuard = 32;           // zero positions before position 0
-constexpr int kTileM = 256;          // positions per CTA tile (2 accumulators)
+constexpr int kTileM = 256;          // positions per CTA tile (MMA N)
 constexpr int kChunkPlanes = 8;      // K chunk = 64 input channels = 8 planes
-constexpr int kBStage = 128 * 64 * 2;  // 16 KB: N=128 × K=64 fp16 weight block
+constexpr int kBStage = 128 * 64 * 2;  // 16 KB: 128 out channels × K=64 fp16 weight block
 constexpr int kASlots = 2;           // A window double-buffered per K chunk
-constexpr int kEpiWarps = 8;       // two warps per TMEM lane quarter, two column chunks each
-constexpr int kThreads = 64 + kEpiWarps * 32;
+constexpr int kEpiWarps = 8;         // two warps per TMEM lane quarter, 128 positions each
+constexpr int kTableWarp = 2 + kEpiWarps;  // fills the per-tile position tables ahead of the epilogue
+constexpr int kThreads = (kTableWarp + 1) * 32;
 
 // K is streamed in 64-channel chunks: for each chunk the producer loads one
 // A slot (8 planes × the position window) and then one 16 KB weight block
@@ -78,10 +84,17 @@ template <int KIND>
 constexpr int win() { return kTileM + 2 * Cfg<KIND>::kHalo; }
 template <int KIND>
 constexpr int a_slot_bytes() { return kChunkPlanes * win<KIND>() * 16; }
-template <int KIND>
-constexpr int smem_bytes() {
-  return kASlots * a_slot_bytes<KIND>() + Cfg<KIND>::kBStages * kBStage + 256;
-}
+
+
+// Per-member epilogue metadata (schedule order), built once per forward by
+// k_rb_memtab from the forwarding tables.
+struct MemberEntry {
+  const float* res;  // residual map of conv3x3 #2 (binary: own slot = z; unary: child / input)
+  float* slot;       // the node's own fp32 plane map
+  uint8_t* fwd;      // parent's fp16 operand image of this node (plane 0, position 0) or null
+  int32_t keep32;    // conv3x3 #2 stores the fp32 value (a reader needs it)
+  int32_t pad;
+};
 
 struct ConvParams {
   int32_t step;
@@ -91,210 +104,211 @@ struct ConvParams {
   const int32_t* group_fid;
   const int32_t* group_begin;
   const int32_t* seg_start;
-  const int32_t* member_g;
-  const int32_t* arity_of;
-  const int32_t* fid;
-  const int32_t* child0;
-  const int32_t* example;
-  const __nv_bfloat16* stage_in;
-  __nv_bfloat16* stage_out;
+  const MemberEntry* memtab;
+  const __half* stage_in;
+  __half* stage_out;
   int64_t ps;  // plane stride in positions
-  const float* inputs;
-  float* values;
-  const __nv_bfloat16* const* wpack;
+  const __half* const* wpack;
   const float* const* bias;
-  // conv3x3 #2 only: forwarding of each result as the fp16 operand image of
-  // its (unique) parent's call — fwd_pos[g] = absolute staging position of
-  // the parent's image (-1: none), fwd_slot[g] = buffer (bit 0: 0 stage_x,
-  // 1 stage_cat) | first plane << 1 | keep-fp32-value << 8.
-  const int32_t* fwd_pos;
-  const int32_t* fwd_slot;
-  __nv_bfloat16* stage_x;
-  __nv_bfloat16* stage_cat;
   int32_t debug;  // nonzero: the MMA thread accumulates its wait cycles in g_conv_dbg
 };
 
-// MMA-thread wait accounting per kernel kind (pair kinds at +3):
-// [waiting for a drained accumulator, for an A window, for a weight stage,
-// total cycles of the MMA loop]. Read/reset with dbk_rb_debug().
+// MMA-thread wait accounting per kernel kind: [waiting for a drained
+// accumulator, for an A window, for a weight stage, total cycles of the MMA
+// loop] (entries 12..23 are unused). Read/reset with dbk_rb_debug().
 __device__ unsigned long long g_conv_dbg[6 * 4];
 
-// Epilogue of one tile (256 positions = 2 TMEM accumulators) for this warp's
-// lane quarter and two 32-column chunks.
+// Residual source of positions that are not real pixels (read, never used).
+__device__ float4 g_zero_res[2 * kPlanes * kPx];
+
+// Per-position epilogue table of one tile (built by the 256 epilogue threads,
+// one position each, read warp-uniformly by the 8 epilogue warps).
+struct PosEntry {
+  const float* res;  // KIND 2: residual map + px·8 (plane 0, channel 0)
+  float* dst;        // KIND 0/2: node plane map + px·8 (nullptr: no fp32 store)
+  uint8_t* fwd;      // KIND 2: parent's fp16 operand image at this position (plane 0)
+  int32_t valid;     // a real pixel of a real member
+  int32_t pad;
+};
+constexpr int kTableBytes = 2 * kTileM * static_cast<int>(sizeof(PosEntry));  // double-buffered
+
 template <int KIND>
-__device__ __forceinline__ void rb_epilogue(const ConvParams& P, uint32_t tmem_base, int abuf, int32_t g,
-                                            int32_t q0, int quarter, int cb0, int lane) {
-      const int32_t f = P.group_fid[g];
-      const int32_t gb0 = P.group_begin[g];
-      const int32_t rows = P.group_begin[g + 1] - gb0;
-      const int32_t seg = P.seg_start[g];
-      const float* __restrict__ bias = P.bias[f];
-      const bool binary = P.arity_of[f] == 2;
-#pragma unroll 1
-      for (int a = 0; a < kTileM / 128; ++a) {
-        const int row = a * 128 + quarter * 32 + lane;
-        const int32_t q = q0 + row;
-        const int32_t local = q - seg;
-        const int32_t img = local / kImg, rem = local - img * kImg;
-        const int32_t r = rem / 15, c = rem - r * 15;
-        const bool valid = img < rows && r < 14 && c < 14;
-        const int32_t px = r * 14 + c;
-        int32_t node = 0;
-        const float* res = nullptr;
-        float* dst32 = nullptr;
-        if (valid && KIND != 1) {
-          node = P.member_g[gb0 + img];
-          dst32 = P.values + static_cast<int64_t>(node) * kFmap;
-          if (KIND == 2) {
-            if (binary) {
-              res = dst32;  // z was parked in the node's own slot by conv1x1
-            } else {
-              const int32_t ch = P.child0[node];
-              res = P.arity_of[P.fid[ch]] == 0 ? P.inputs + static_cast<int64_t>(P.example[ch]) * kFmap
-                                               : P.values + static_cast<int64_t>(ch) * kFmap;
-            }
-          }
-        }
-        if constexpr (KIND == 2) {
-          // Residual rows are fetched one 32-channel chunk ahead of the TMEM
-          // loads so the epilogue keeps 8 independent 16-byte loads in flight
-          // (the residual may alias the destination for binary modules, so
-          // every chunk is fully loaded before any of its stores).
-          const float* rbase = valid ? res + px * 8 : nullptr;
-          float* dbase = valid ? dst32 + px * 8 : nullptr;
-          // forwarding target: the parent's fp16 operand image (if unique parent)
-          int32_t slot = 0;
-          uint8_t* fbase = nullptr;
-          if (valid) {
-            const int32_t tgt = P.fwd_pos[node];
-            slot = P.fwd_slot[node];
-            if (tgt >= 0) {
-              fbase = reinterpret_cast<uint8_t*>((slot & 1) ? P.stage_cat : P.stage_x) +
-                      (static_cast<int64_t>((slot >> 1) & 31) * P.ps + kGuard + tgt + rem) * 16;
-            }
-          }
-          const bool keep32 = (slot >> 8) & 1;
-          float4 rcur[8], rnext[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) rcur[i] = rnext[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (valid) {
-#pragma unroll
-            for (int pp = 0; pp < 4; ++pp) {
-              rcur[2 * pp] = *reinterpret_cast<const float4*>(rbase + (cb0 * 4 + pp) * kPx * 8);
-              rcur[2 * pp + 1] = *reinterpret_cast<const float4*>(rbase + (cb0 * 4 + pp) * kPx * 8 + 4);
-            }
-          }
-#pragma unroll
-          for (int cbi = 0; cbi < 2; ++cbi) {
-            const int cb = cb0 + cbi;
-            float v[32];
-            tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * 256 + a * 128 + cb * 32, v);
-            if (valid && cbi == 0) {
-#pragma unroll
-              for (int pp = 0; pp < 4; ++pp) {
-                const float* rp = rbase + ((cb + 1) * 4 + pp) * kPx * 8;
-                rnext[2 * pp] = *reinterpret_cast<const float4*>(rp);
-                rnext[2 * pp + 1] = *reinterpret_cast<const float4*>(rp + 4);
-              }
-            }
-            if (valid) {
-#pragma unroll
-              for (int pp = 0; pp < 4; ++pp) {
-                const int plane = cb * 4 + pp;
-                const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias + plane * 8));
-                const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias + plane * 8 + 4));
-                const float4 r0 = rcur[2 * pp], r1 = rcur[2 * pp + 1];
-                const float4 o0 = make_float4(fmaxf(v[pp * 8 + 0] + b_lo.x + r0.x, 0.f),
-                                              fmaxf(v[pp * 8 + 1] + b_lo.y + r0.y, 0.f),
-                                              fmaxf(v[pp * 8 + 2] + b_lo.z + r0.z, 0.f),
-                                              fmaxf(v[pp * 8 + 3] + b_lo.w + r0.w, 0.f));
-                const float4 o1 = make_float4(fmaxf(v[pp * 8 + 4] + b_hi.x + r1.x, 0.f),
-                                              fmaxf(v[pp * 8 + 5] + b_hi.y + r1.y, 0.f),
-                                              fmaxf(v[pp * 8 + 6] + b_hi.z + r1.z, 0.f),
-                                              fmaxf(v[pp * 8 + 7] + b_hi.w + r1.w, 0.f));
-                if (keep32) {
-                  float* dp = dbase + plane * kPx * 8;
-                  *reinterpret_cast<float4*>(dp) = o0;
-                  *reinterpret_cast<float4*>(dp + 4) = o1;
-                }
-                if (fbase) {
-                  uint4 pk;
-                  pk.x = pack_f16x2(o0.x, o0.y);
-                  pk.y = pack_f16x2(o0.z, o0.w);
-                  pk.z = pack_f16x2(o1.x, o1.y);
-                  pk.w = pack_f16x2(o1.z, o1.w);
-                  *reinterpret_cast<uint4*>(fbase + static_cast<int64_t>(plane) * P.ps * 16) = pk;
-                }
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) rcur[i] = rnext[i];
-          }
-          continue;
-        }
-        uint8_t* out16 = reinterpret_cast<uint8_t*>(P.stage_out) + static_cast<int64_t>(kGuard + q) * 16;
-#pragma unroll 1
-        for (int cbi = 0; cbi < 2; ++cbi) {
-          const int cb = cb0 + cbi;
-          float v[32];
-          tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * 256 + a * 128 + cb * 32, v);
-#pragma unroll
-          for (int pp = 0; pp < 4; ++pp) {
-            const int plane = cb * 4 + pp;
-            const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias + plane * 8));
-            const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias + plane * 8 + 4));
-            float o[8] = {v[pp * 8 + 0] + b_lo.x, v[pp * 8 + 1] + b_lo.y, v[pp * 8 + 2] + b_lo.z,
-                          v[pp * 8 + 3] + b_lo.w, v[pp * 8 + 4] + b_hi.x, v[pp * 8 + 5] + b_hi.y,
-                          v[pp * 8 + 6] + b_hi.z, v[pp * 8 + 7] + b_hi.w};
-            if (KIND == 2) {
-              if (valid) {
-                const float* rp = res + (plane * kPx + px) * 8;
-                const float4 r0 = *reinterpret_cast<const float4*>(rp);
-                const float4 r1 = *reinterpret_cast<const float4*>(rp + 4);
-                o[0] += r0.x; o[1] += r0.y; o[2] += r0.z; o[3] += r0.w;
-                o[4] += r1.x; o[5] += r1.y; o[6] += r1.z; o[7] += r1.w;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) o[i] = fmaxf(o[i], 0.0f);
-                float* dp = dst32 + (plane * kPx + px) * 8;
-                *reinterpret_cast<float4*>(dp) = make_float4(o[0], o[1], o[2], o[3]);
-                *reinterpret_cast<float4*>(dp + 4) = make_float4(o[4], o[5], o[6], o[7]);
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) o[i] = valid ? fmaxf(o[i], 0.0f) : 0.0f;
-              uint4 pk;
-              pk.x = pack_f16x2(o[0], o[1]);
-              pk.y = pack_f16x2(o[2], o[3]);
-              pk.z = pack_f16x2(o[4], o[5]);
-              pk.w = pack_f16x2(o[6], o[7]);
-              *reinterpret_cast<uint4*>(out16 + static_cast<int64_t>(plane) * P.ps * 16) = pk;
-              if (KIND == 0 && valid) {  // fp32 z for the residual of the block
-                float* dp = dst32 + (plane * kPx + px) * 8;
-                *reinterpret_cast<float4*>(dp) = make_float4(o[0], o[1], o[2], o[3]);
-                *reinterpret_cast<float4*>(dp + 4) = make_float4(o[4], o[5], o[6], o[7]);
-              }
-            }
-          }
-        }
-      }
+constexpr int smem_bytes() {
+  return kASlots * a_slot_bytes<KIND>() + Cfg<KIND>::kBStages * kBStage + kTableBytes + 256;
 }
 
+// Fills the table entries of positions lane + 32k (k = 0..7) of a tile from
+// the per-member table: one independent 32-byte load per position, all
+// issued before any entry is stored.
+template <int KIND>
+__device__ __forceinline__ void rb_fill_table(const ConvParams& P, PosEntry* tab, int32_t g, int32_t q0,
+                                              int lane) {
+  constexpr int kPer = kTileM / 32;
+  const int32_t gb0 = P.group_begin[g];
+  const int32_t rows = P.group_begin[g + 1] - gb0;
+  const int32_t base = q0 - P.seg_start[g];
+  MemberEntry me[kPer];
+  int32_t rem[kPer], px[kPer];
+  bool valid[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int32_t local = base + lane + 32 * k;
+    const int32_t img = local / kImg;
+    rem[k] = local - img * kImg;
+    const int32_t r = rem[k] / 15, c = rem[k] - r * 15;
+    valid[k] = img < rows && r < 14 && c < 14;
+    px[k] = r * 14 + c;
+    if (KIND != 1 && valid[k]) me[k] = P.memtab[gb0 + img];
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    PosEntry e{nullptr, nullptr, nullptr, valid[k] ? 1 : 0, 0};
+    if (KIND != 1 && valid[k]) {
+      float* slot = me[k].slot + px[k] * 8;
+      if (KIND == 0) {
+        e.dst = slot;  // fp32 z, the residual of the binary block
+      } else {
+        e.res = me[k].res + px[k] * 8;
+        e.dst = me[k].keep32 ? slot : nullptr;
+        e.fwd = me[k].fwd ? me[k].fwd + rem[k] * 16 : nullptr;
+      }
+    }
+    tab[lane + 32 * k] = e;
+  }
+}
+
+// 8×8 transpose across the 8 lanes of a plane group (three butterfly
+// stages): in, lane e holds x[i] = D[channel 8g+e][position i]; out, lane e
+// holds x[k] = D[channel 8g+k][position e].
+__device__ __forceinline__ void transpose8(float* x, int e) {
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const bool up = (e & s) != 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i & s) continue;
+      const float send = up ? x[i] : x[i + s];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, s);
+      x[i] = up ? recv : x[i];
+      x[i + s] = up ? x[i + s] : recv;
+    }
+  }
+}
+
+// Epilogue of one tile for this warp: TMEM lanes = output channels
+// 32·quarter + lane, columns = the tile's positions; the warp covers
+// positions [128·half, 128·half + 128) in eight 16-column chunks. After the
+// in-register transpose, lane (g = lane/8, e = lane%8) owns positions
+// 8m + e (m = 0, 1) of each chunk with the 8 channels of plane 4·quarter + g,
+// so every global access is a 16-byte vector (fp16 image: one, fp32 map:
+// two) and a warp instruction covers 4 planes × 8 consecutive positions.
+struct EpiLane {
+  int quarter, half, e, plane;
+  int64_t plane_off16;  // fp16 staging offset of this lane's plane
+  int plane_off32;      // fp32 plane-map offset of this lane's plane
+};
+
+constexpr int kChunk = 16;                 // positions per epilogue chunk
+constexpr int kChunks = 128 / kChunk;      // chunks per warp and tile
+constexpr int kResAhead = 3;               // residual prefetch distance (chunks)
+
+// Residual rows of chunk cb of a tile for this lane (2 positions × 8 ch).
+// Unconditional loads (invalid positions read a zero record) followed by a
+// warp sync, so ptxas issues them here instead of sinking them to the uses.
+__device__ __forceinline__ void rb_load_res(const PosEntry* tab, const EpiLane& L, int cb, float4* r) {
+  const float* zero = reinterpret_cast<const float*>(g_zero_res);
+  const PosEntry* my = tab + L.half * 128 + cb * kChunk + L.e;
+#pragma unroll
+  for (int m = 0; m < kChunk / 8; ++m) {
+    const PosEntry& pe = my[8 * m];
+    const float4* rp = reinterpret_cast<const float4*>((pe.valid ? pe.res : zero) + L.plane_off32);
+    r[2 * m] = __ldg(rp);
+    r[2 * m + 1] = __ldg(rp + 1);
+  }
+  __syncwarp();
+}
+
+// One 16-position chunk: TMEM → transpose → bias (+ residual) → ReLU → stores.
+template <int KIND>
+__device__ __forceinline__ void rb_chunk(const ConvParams& P, const PosEntry* tab, const EpiLane& L,
+                                         uint32_t taddr, const float* bias, int32_t q0, int cb,
+                                         const float4* res) {
+  float v[kChunk];
+  tmem_ld16(taddr + cb * kChunk, v);
+  const PosEntry* my = tab + L.half * 128 + cb * kChunk + L.e;
+#pragma unroll
+  for (int m = 0; m < kChunk / 8; ++m) {
+    float* x = v + 8 * m;
+    transpose8(x, L.e);
+    const PosEntry& pe = my[8 * m];
+    if constexpr (KIND == 2) {
+      if (pe.valid) {
+        const float4 r0 = res[2 * m], r1 = res[2 * m + 1];
+        const float o[8] = {fmaxf(x[0] + bias[0] + r0.x, 0.f), fmaxf(x[1] + bias[1] + r0.y, 0.f),
+                            fmaxf(x[2] + bias[2] + r0.z, 0.f), fmaxf(x[3] + bias[3] + r0.w, 0.f),
+                            fmaxf(x[4] + bias[4] + r1.x, 0.f), fmaxf(x[5] + bias[5] + r1.y, 0.f),
+                            fmaxf(x[6] + bias[6] + r1.z, 0.f), fmaxf(x[7] + bias[7] + r1.w, 0.f)};
+        if (pe.dst) {
+          float4* dp = reinterpret_cast<float4*>(pe.dst + L.plane_off32);
+          dp[0] = make_float4(o[0], o[1], o[2], o[3]);
+          dp[1] = make_float4(o[4], o[5], o[6], o[7]);
+        }
+        if (pe.fwd) {
+          uint4 pk;
+          pk.x = pack_f16x2(o[0], o[1]);
+          pk.y = pack_f16x2(o[2], o[3]);
+          pk.z = pack_f16x2(o[4], o[5]);
+          pk.w = pack_f16x2(o[6], o[7]);
+          *reinterpret_cast<uint4*>(pe.fwd + L.plane_off16) = pk;
+        }
+      }
+    } else {
+      float o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = pe.valid ? fmaxf(x[k] + bias[k], 0.f) : 0.f;
+      uint4 pk;
+      pk.x = pack_f16x2(o[0], o[1]);
+      pk.y = pack_f16x2(o[2], o[3]);
+      pk.z = pack_f16x2(o[4], o[5]);
+      pk.w = pack_f16x2(o[6], o[7]);
+      uint8_t* out16 = reinterpret_cast<uint8_t*>(P.stage_out) +
+                       static_cast<int64_t>(kGuard + q0 + L.half * 128 + cb * kChunk + 8 * m + L.e) * 16 +
+                       L.plane_off16;
+      *reinterpret_cast<uint4*>(out16) = pk;
+      if (KIND == 0 && pe.valid) {  // fp32 z, the residual of the binary block
+        float4* dp = reinterpret_cast<float4*>(pe.dst + L.plane_off32);
+        dp[0] = make_float4(o[0], o[1], o[2], o[3]);
+        dp[1] = make_float4(o[4], o[5], o[6], o[7]);
+      }
+    }
+  }
+}
+
+// Implicit-GEMM conv, operands swapped so every MMA is N = 256 wide:
+// D[128 out channels][256 positions] += W[128][k16] · X[256 positions][k16]^T
+// (A = the weight stage, B = the activation window at the tap's row shift).
+// N = 128 MMAs are issue-bound once the per-tap commit / barrier traffic is
+// added (tools/mma_rate.cu: 88–97 cycles vs 64 ideal); N = 256 MMAs run at
+// the ideal 128 cycles with the same per-tap overhead.
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__ ConvParams P) {
   using K = Cfg<KIND>;
   constexpr int WIN = win<KIND>();
-  constexpr uint32_t IDESC = idesc_f16_f32(128, 128);
+  constexpr uint32_t IDESC = idesc_f16_f32(128, kTileM);
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + kASlots * a_slot_bytes<KIND>();
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + K::kBStages * kBStage);
+  PosEntry* tables = reinterpret_cast<PosEntry*>(sB + K::kBStages * kBStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tables) + kTableBytes);
   uint64_t* a_full = bars;
   uint64_t* a_empty = a_full + kASlots;
   uint64_t* b_full = a_empty + kASlots;
   uint64_t* b_empty = b_full + K::kBStages;
   uint64_t* acc_full = b_empty + K::kBStages;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* tab_full = acc_empty + 2;
+  uint64_t* tab_empty = tab_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tab_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -309,6 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
       mbar_init(acc_empty + s, kEpiWarps * 32);
+      mbar_init(tab_full + s, 32);
+      mbar_init(tab_empty + s, kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -375,15 +391,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
             w_b += clock64() - c0;
             tc_fence_after();
             const int shift = K::kTaps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
+            const uint32_t xrow = static_cast<uint32_t>(K::kHalo + shift);
 #pragma unroll
-            for (int a = 0; a < kTileM / 128; ++a) {
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint32_t arow = static_cast<uint32_t>(K::kHalo + shift + a * 128);
-                const uint64_t ad = smem_desc(a_slot + ((2 * kk) * WIN + arow) * 16, WIN * 16, 128);
-                const uint64_t bd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
-                mma_bf16(tmem_base + abuf * 256 + a * 128, ad, bd, IDESC, (ch | tap | kk) != 0);
-              }
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t wd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
+              const uint64_t xd = smem_desc(a_slot + ((2 * kk) * WIN + xrow) * 16, WIN * 16, 128);
+              mma_bf16(tmem_base + abuf * kTileM, wd, xd, IDESC, (ch | tap | kk) != 0);
             }
             mma_commit(b_empty + s);
           }
@@ -398,216 +411,73 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
         atomicAdd(&g_conv_dbg[KIND * 4 + 3], static_cast<unsigned long long>(clock64() - t_start));
       }
     }
-  } else {  // ------------------------------------------------------ epilogue
-    const int quarter = warp & 3;
-    const int cb0 = ((warp - 2) >> 2) * 2;  // this warp's first 32-column chunk
+  } else if (warp == kTableWarp) {  // ------------------------ table filler
     int it = 0;
     for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const int32_t g = P.tile_group[t_begin + t];
+      const int32_t q0 = P.tile_q0[t_begin + t];
+      mbar_wait(tab_empty + buf, ((it >> 1) & 1) ^ 1);
+      rb_fill_table<KIND>(P, tables + buf * kTileM, g, q0, lane);
+      mbar_arrive(tab_full + buf);  // release: the entries are visible to the waiters
+    }
+  } else {  // ------------------------------------------------------ epilogue
+    EpiLane L;
+    L.quarter = warp & 3;
+    L.half = (warp - 2) >> 2;
+    L.e = lane & 7;
+    L.plane = L.quarter * 4 + (lane >> 3);
+    L.plane_off16 = static_cast<int64_t>(L.plane) * P.ps * 16;
+    L.plane_off32 = L.plane * kPx * 8;
+    const uint32_t lane_addr = (static_cast<uint32_t>(L.quarter * 32) << 16) + L.half * 128;
+    // residual chunks are loaded kResAhead ahead, across tile boundaries
+    // (ring of 4 buffers, so every index is a compile-time constant)
+    float4 rbuf[4][kChunk / 4];
+    int it = 0;
+    int32_t t = blockIdx.x;
+    if (KIND == 2 && t < n_tiles) {
+      mbar_wait(tab_full + 0, 0);
+#pragma unroll
+      for (int c = 0; c < kResAhead; ++c) rb_load_res(tables, L, c, rbuf[c]);
+    }
+    for (; t < n_tiles; t += gridDim.x, ++it) {
       const int abuf = it & 1;
       const int32_t g = P.tile_group[t_begin + t];
       const int32_t q0 = P.tile_q0[t_begin + t];
+      const PosEntry* tab = tables + abuf * kTileM;
+      const float* bias_p = P.bias[P.group_fid[g]] + L.plane * 8;
+      const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias_p));
+      const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias_p + 4));
+      const float bias[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
+      mbar_wait(tab_full + abuf, (it >> 1) & 1);
       mbar_wait(acc_full + abuf, (it >> 1) & 1);
       tc_fence_after();
-      rb_epilogue<KIND>(P, tmem_base, abuf, g, q0, quarter, cb0, lane);
+      const uint32_t taddr = tmem_base + abuf * kTileM + lane_addr;
+      const bool has_next = t + static_cast<int32_t>(gridDim.x) < n_tiles;
+#pragma unroll
+      for (int cb = 0; cb < kChunks; ++cb) {
+        if (KIND == 2) {
+          constexpr int A = kResAhead;
+          if (cb + A < kChunks) {
+            rb_load_res(tab, L, cb + A, rbuf[(cb + A) & 3]);
+          } else if (has_next) {
+            const int nb = (it + 1) & 1;
+            if (cb + A == kChunks) mbar_wait(tab_full + nb, ((it + 1) >> 1) & 1);
+            rb_load_res(tables + nb * kTileM, L, cb + A - kChunks, rbuf[(cb + A) & 3]);
+          }
+        }
+        rb_chunk<KIND>(P, tab, L, taddr, bias, q0, cb, rbuf[cb & 3]);
+      }
       tc_fence_before();
       mbar_arrive(acc_empty + abuf);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tab_empty + abuf);
     }
   }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
-  }
-}
-
-// ------------------------------------------------------- CTA-pair kernel
-// Cluster of two CTAs on one TPC computes a 512-position pair tile with
-// tcgen05.mma.cta_group::2 (M = 256 = 128 rows from each CTA's window,
-// N = 128): each CTA stages its own 256-position A window and HALF of every
-// weight block (64 output channels), so per-SM shared-memory reads per MMA
-// drop from 8 KB to 6 KB and weight traffic per SM halves. The even CTA
-// issues the MMAs; the odd CTA relays its "data landed" events to the even
-// CTA's barriers (remote mbarrier arrives), and commits multicast back to
-// both CTAs' empty / accumulator-full barriers. Each CTA's epilogue reads the
-// accumulator rows of its own positions from its own TMEM.
-constexpr int kPairBStage = 64 * 64 * 2;  // 8 KB: N=64 (half) × K=64
-
-template <int KIND>
-struct PairCfg;
-template <>
-struct PairCfg<0> { static constexpr int kBStages = 8; };
-template <>
-struct PairCfg<1> { static constexpr int kBStages = 16; };
-template <>
-struct PairCfg<2> : PairCfg<1> {};
-
-template <int KIND>
-constexpr int pair_smem_bytes() {
-  return kASlots * a_slot_bytes<KIND>() + PairCfg<KIND>::kBStages * kPairBStage + 512;
-}
-
-template <int KIND>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    k_rb_conv_pair(const __grid_constant__ ConvParams P) {
-  using K = Cfg<KIND>;
-  constexpr int NB = PairCfg<KIND>::kBStages;
-  constexpr int WIN = win<KIND>();
-  constexpr uint32_t IDESC = idesc_f16_f32(256, 128);
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kASlots * a_slot_bytes<KIND>();
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NB * kPairBStage);
-  uint64_t* a_full = bars;
-  uint64_t* a_empty = a_full + kASlots;
-  uint64_t* b_full = a_empty + kASlots;
-  uint64_t* b_empty = b_full + NB;
-  uint64_t* acc_full = b_empty + NB;
-  uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
-  if (threadIdx.x == 0) {
-    const uint32_t full_count = leader ? 2 : 1;  // own copies + the peer's relay
-    for (int s = 0; s < kASlots; ++s) {
-      mbar_init(a_full + s, full_count);
-      mbar_init(a_empty + s, 1);
-    }
-    for (int s = 0; s < NB; ++s) {
-      mbar_init(b_full + s, full_count);
-      mbar_init(b_empty + s, 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, 2 * kEpiWarps);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  const int32_t t_begin = P.step_tile_begin[P.step];
-  const int32_t n_tiles = P.step_tile_begin[P.step + 1] - t_begin;
-  const int32_t pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------------------- producer (both CTAs)
-      uint32_t ai = 0, bi = 0;
-      for (int32_t t = pair; t < n_tiles; t += n_pairs) {
-        const int32_t g = P.tile_group[t_begin + t];
-        const int32_t q0 = P.tile_q0[t_begin + t] + static_cast<int32_t>(rank) * kTileM;
-        const uint8_t* w = reinterpret_cast<const uint8_t*>(P.wpack[P.group_fid[g]]) + rank * kPairBStage;
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.stage_in) +
-                             static_cast<int64_t>(kGuard + q0 - K::kHalo) * 16;
-        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
-          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
-          mbar_wait(a_empty + sa, pa ^ 1);
-          mbar_expect_tx(a_full + sa, a_slot_bytes<KIND>());
-          for (int j = 0; j < kChunkPlanes; ++j) {
-            bulk_g2s(sA + sa * a_slot_bytes<KIND>() + j * WIN * 16,
-                     src + static_cast<int64_t>(ch * kChunkPlanes + j) * P.ps * 16, WIN * 16, a_full + sa);
-          }
-          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
-            const uint32_t s = bi % NB, ph = (bi / NB) & 1;
-            mbar_wait(b_empty + s, ph ^ 1);
-            mbar_expect_tx(b_full + s, kPairBStage);
-            bulk_g2s(sB + s * kPairBStage, w + static_cast<int64_t>(ch * K::kTaps + tap) * 2 * kPairBStage,
-                     kPairBStage, b_full + s);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ------------------- MMA issuer (even CTA)
-      long long w_acc = 0, w_a = 0, w_b = 0;
-      const long long t_start = clock64();
-      uint32_t ai = 0, bi = 0;
-      int it = 0;
-      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-      for (int32_t t = pair; t < n_tiles; t += n_pairs, ++it) {
-        const int abuf = it & 1;
-        long long c0 = clock64();
-        mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
-        w_acc += clock64() - c0;
-        tc_fence_after();
-        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
-          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
-          c0 = clock64();
-          mbar_wait(a_full + sa, pa);
-          w_a += clock64() - c0;
-          tc_fence_after();
-          const uint32_t a_slot = a_base + sa * a_slot_bytes<KIND>();
-          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
-            const uint32_t s = bi % NB, ph = (bi / NB) & 1;
-            c0 = clock64();
-            mbar_wait(b_full + s, ph);
-            w_b += clock64() - c0;
-            tc_fence_after();
-            const int shift = K::kTaps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
-#pragma unroll
-            for (int a = 0; a < kTileM / 128; ++a) {
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint32_t arow = static_cast<uint32_t>(K::kHalo + shift + a * 128);
-                const uint64_t ad = smem_desc(a_slot + ((2 * kk) * WIN + arow) * 16, WIN * 16, 128);
-                const uint64_t bd = smem_desc(b_base + s * kPairBStage + (2 * kk) * 1024, 1024, 128);
-                mma_bf16_pair(tmem_base + abuf * 256 + a * 128, ad, bd, IDESC, (ch | tap | kk) != 0);
-              }
-            }
-            mma_commit_pair(b_empty + s, 0x3);
-          }
-          mma_commit_pair(a_empty + sa, 0x3);
-        }
-        mma_commit_pair(acc_full + abuf, 0x3);
-      }
-      if (P.debug) {
-        atomicAdd(&g_conv_dbg[12 + KIND * 4 + 0], static_cast<unsigned long long>(w_acc));
-        atomicAdd(&g_conv_dbg[12 + KIND * 4 + 1], static_cast<unsigned long long>(w_a));
-        atomicAdd(&g_conv_dbg[12 + KIND * 4 + 2], static_cast<unsigned long long>(w_b));
-        atomicAdd(&g_conv_dbg[12 + KIND * 4 + 3], static_cast<unsigned long long>(clock64() - t_start));
-      }
-    } else if (lane == 0) {  // ---------------- relay (odd CTA): data landed
-      uint32_t ai = 0, bi = 0;
-      for (int32_t t = pair; t < n_tiles; t += n_pairs) {
-        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
-          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
-          mbar_wait(a_full + sa, pa);
-          mbar_arrive_remote(a_full + sa, 0);
-          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
-            const uint32_t s = bi % NB, ph = (bi / NB) & 1;
-            mbar_wait(b_full + s, ph);
-            mbar_arrive_remote(b_full + s, 0);
-          }
-        }
-      }
-    }
-  } else {  // ---------------------------------------------- epilogue (both)
-    const int quarter = warp & 3;
-    const int cb0 = ((warp - 2) >> 2) * 2;
-    int it = 0;
-    for (int32_t t = pair; t < n_tiles; t += n_pairs, ++it) {
-      const int abuf = it & 1;
-      const int32_t g = P.tile_group[t_begin + t];
-      const int32_t q0 = P.tile_q0[t_begin + t] + static_cast<int32_t>(rank) * kTileM;
-      mbar_wait(acc_full + abuf, (it >> 1) & 1);
-      tc_fence_after();
-      rb_epilogue<KIND>(P, tmem_base, abuf, g, q0, quarter, cb0, lane);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (leader) mbar_arrive(acc_empty + abuf); else mbar_arrive_remote(acc_empty + abuf, 0);
-      }
-    }
-  }
-  tc_fence_before();
-  cluster_sync();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc_pair(tmem_base, 512);
   }
 }
 
@@ -700,6 +570,41 @@ __global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const
         // as its residual, so keep it; binary parents use their own z.
         fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1) | ((arity == 1 ? 1 : 0) << 8);
       }
+    }
+  }
+}
+
+__global__ void k_rb_memtab(int32_t n_steps, const int32_t* __restrict__ sgb,
+                            const int32_t* __restrict__ group_fid, const int32_t* __restrict__ group_begin,
+                            const int32_t* __restrict__ arity_of, const int32_t* __restrict__ seg_start,
+                            const int32_t* __restrict__ member_g, const int32_t* __restrict__ fid,
+                            const int32_t* __restrict__ child0, const int32_t* __restrict__ example,
+                            const int32_t* __restrict__ fwd_pos, const int32_t* __restrict__ fwd_slot,
+                            const float* inputs, float* values, uint8_t* stage_x, uint8_t* stage_cat,
+                            int64_t ps, MemberEntry* __restrict__ memtab) {
+  const int32_t s = blockIdx.x;
+  if (s >= n_steps) return;
+  for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
+    if (seg_start[g] < 0) continue;
+    const int32_t arity = arity_of[group_fid[g]];
+    for (int32_t m = group_begin[g] + threadIdx.x; m < group_begin[g + 1]; m += blockDim.x) {
+      const int32_t node = member_g[m];
+      MemberEntry e;
+      e.slot = values + static_cast<int64_t>(node) * kFmap;
+      if (arity == 2) {
+        e.res = e.slot;
+      } else {
+        const int32_t ch = child0[node];
+        e.res = arity_of[fid[ch]] == 0 ? inputs + static_cast<int64_t>(example[ch]) * kFmap
+                                       : values + static_cast<int64_t>(ch) * kFmap;
+      }
+      const int32_t sw = fwd_slot[node];
+      const int32_t tgt = fwd_pos[node];
+      e.keep32 = (sw >> 8) & 1;
+      e.fwd = tgt >= 0 ? ((sw & 1) ? stage_cat : stage_x) + (static_cast<int64_t>((sw >> 1) & 31) * ps + kGuard + tgt) * 16
+                       : nullptr;
+      e.pad = 0;
+      memtab[m] = e;
     }
   }
 }
@@ -827,17 +732,6 @@ int launch_conv(const ConvParams& p, int num_sms, cudaStream_t s) {
   return static_cast<int>(cudaGetLastError());
 }
 
-template <int KIND>
-int launch_conv_pair(const ConvParams& p, int num_sms, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_rb_conv_pair<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem_bytes<KIND>());
-    configured = true;
-  }
-  k_rb_conv_pair<KIND><<<(num_sms / 2) * 2, kThreads, pair_smem_bytes<KIND>(), s>>>(p);
-  return static_cast<int>(cudaGetLastError());
-}
-
 }  // namespace
 
 extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
@@ -875,28 +769,45 @@ extern "C" int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, cons
   return static_cast<int>(cudaGetLastError());
 }
 
+extern "C" int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
+                             const int32_t* group_begin, const int32_t* arity_of, const int32_t* seg_start,
+                             const int32_t* member_g, const int32_t* fid, const int32_t* child0,
+                             const int32_t* example, const int32_t* fwd_pos, const int32_t* fwd_slot,
+                             const float* inputs, float* values, void* stage_x, void* stage_cat,
+                             int64_t plane_stride, void* memtab, void* stream) {
+  if (n_steps <= 0) return 0;
+  k_rb_memtab<<<n_steps, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start, member_g, fid, child0, example,
+      fwd_pos, fwd_slot, inputs, values, static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_cat),
+      plane_stride, static_cast<MemberEntry*>(memtab));
+  return static_cast<int>(cudaGetLastError());
+}
+
 extern "C" int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
                            const int32_t* tile_group, const int32_t* tile_q0, const int32_t* group_fid,
-                           const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
-                           const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
-                           const int32_t* example, const void* stage_in, void* stage_out,
-                           int64_t plane_stride, const float* inputs, float* values,
-                           const void* const* wpack, const float* const* bias, const int32_t* fwd_pos,
-                           const int32_t* fwd_slot, void* stage_x, void* stage_cat, int32_t num_sms,
+                           const int32_t* group_begin, const int32_t* seg_start, const void* memtab,
+                           const void* stage_in, void* stage_out, int64_t plane_stride,
+                           const void* const* wpack, const float* const* bias, int32_t num_sms,
                            void* stream) {
-  ConvParams p{step, step_tile_begin, tile_group, tile_q0, group_fid, group_begin, seg_start, member_g,
-               arity_of, fid, child0, example, static_cast<const __nv_bfloat16*>(stage_in),
-               static_cast<__nv_bfloat16*>(stage_out), plane_stride, inputs, values,
-               reinterpret_cast<const __nv_bfloat16* const*>(wpack), bias, fwd_pos, fwd_slot,
-               static_cast<__nv_bfloat16*>(stage_x), static_cast<__nv_bfloat16*>(stage_cat), g_debug_flag};
+  ConvParams p{step,
+               step_tile_begin,
+               tile_group,
+               tile_q0,
+               group_fid,
+               group_begin,
+               seg_start,
+               static_cast<const MemberEntry*>(memtab),
+               static_cast<const __half*>(stage_in),
+               static_cast<__half*>(stage_out),
+               plane_stride,
+               reinterpret_cast<const __half* const*>(wpack),
+               bias,
+               g_debug_flag};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (kind) {
     case 0: return launch_conv<0>(p, num_sms, s);
     case 1: return launch_conv<1>(p, num_sms, s);
     case 2: return launch_conv<2>(p, num_sms, s);
-    case 0 + 16: return launch_conv_pair<0>(p, num_sms, s);  // CTA-pair variants
-    case 1 + 16: return launch_conv_pair<1>(p, num_sms, s);
-    case 2 + 16: return launch_conv_pair<2>(p, num_sms, s);
   }
   return static_cast<int>(cudaErrorInvalidValue);
 }

@@ -22,14 +22,6 @@ pytestmark = pytest.mark.gpu
 F = 128 * 14 * 14
 
 
-@pytest.fixture(autouse=True, params=["pair", "single"])
-def conv_variant(request, monkeypatch):
-    """Every test runs with the CTA-pair (cta_group::2) conv kernels and with
-    the single-CTA kernels (DYNBATCH_CONV_PAIR=0)."""
-    monkeypatch.setenv("DYNBATCH_CONV_PAIR", "1" if request.param == "pair" else "0")
-    return request.param
-
-
 TOL_NORM = 1e-3
 TOL_ELEM = 5e-3
 
