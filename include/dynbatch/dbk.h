@@ -81,32 +81,39 @@ int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t*
                 const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t tile_m,
                 void* stream);
 /* Gather of the operands of step `step` that no child epilogue forwarded
- * (leaves, shared children) into the fp16 staging planes, with the binary
- * channel concat fused into the write; plane_stride in positions. */
+ * (leaves, shared children) into the fp16 staging planes: unary members get
+ * the hi image in stage_x and the lo image (x − hi, the block's residual) in
+ * stage_lo; binary members get hi in stage_cat planes 16k.. (the channel
+ * concat is fused into the write); plane_stride in positions. */
 int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_fid,
                   const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
                   const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
                   const int32_t* child1, const int32_t* example, const int32_t* fwd_ok,
-                  const float* inputs, const float* values, void* stage_x, void* stage_cat,
+                  const float* inputs, const float* values, void* stage_x, void* stage_lo, void* stage_cat,
                   int64_t plane_stride, int32_t blocks, void* stream);
-/* tcgen05 implicit-GEMM convolutions: kind 0 = conv1x1 over [x; y] → z
- * (fp16 staging + fp32 parked in the node slot), 1 = conv3x3 #1 → mid
- * (fp16), 2 = conv3x3 #2 + residual + ReLU → fp32 node values (when a
- * reader needs them) and the fp16 operand image of the parent's call.
- * One CTA per SM, D[128 channels][256 positions] per tile (MMA N = 256). */
-int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
-                const int32_t* tile_group, const int32_t* tile_q0, const int32_t* group_fid,
-                const int32_t* group_begin, const int32_t* seg_start, const void* memtab,
-                const void* stage_in, void* stage_out, int64_t plane_stride, const void* const* wpack,
-                const float* const* bias, int32_t num_sms, void* stream);
-/* Per-member epilogue table (32 bytes per member, schedule order: residual
- * source, own slot, forwarding target, keep-fp32 flag), built after
- * dbk_rb_plan from its forwarding tables. */
+/* One persistent launch per step (one CTA per SM) over a device work queue
+ * of the step's tiles: conv1x1 over [x; y] → z hi/lo (stage_x / stage_lo),
+ * conv3x3 #1 → mid (stage_mid), conv3x3 #2 + residual (accumulated on the
+ * tensor cores from the hi/lo images through the identity blocks `ident`) →
+ * hi/lo images of the parent's call and fp32 values where a reader needs
+ * them. Tile-level dependencies through done flags (done0 per bin tile,
+ * done1 per tile; == epoch means done); queue[step] must be 0 at launch.
+ * D[128 channels][256 positions] per tile (tcgen05.mma M = 128, N = 256). */
+int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile_begin, const int32_t* tile_group,
+                const int32_t* tile_q0, const int32_t* step_bintile_begin, const int32_t* bin_group,
+                const int32_t* bin_q0, const int32_t* group_fid, const int32_t* group_begin,
+                const int32_t* seg_start, const int32_t* group_tile0, const int32_t* group_bintile0,
+                const void* memtab, void* stage_x, void* stage_lo, void* stage_cat, void* stage_mid,
+                int64_t plane_stride, const void* const* w0, const void* const* w1, const void* const* w2,
+                const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
+                int32_t* done0, int32_t* done1, int32_t* queue, int32_t num_sms, void* stream);
+/* Per-member epilogue table (32 bytes per member, schedule order: own fp32
+ * slot, hi / lo forwarding targets, keep-fp32 flag), built after dbk_rb_plan
+ * from its forwarding tables. */
 int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
-                  const int32_t* group_begin, const int32_t* arity_of, const int32_t* seg_start,
-                  const int32_t* member_g, const int32_t* fid, const int32_t* child0, const int32_t* example,
-                  const int32_t* fwd_pos, const int32_t* fwd_slot, const float* inputs, float* values,
-                  void* stage_x, void* stage_cat, int64_t plane_stride, void* memtab, void* stream);
+                  const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
+                  const int32_t* fwd_pos, const int32_t* fwd_slot, float* values, void* stage_x,
+                  void* stage_lo, void* stage_cat, int64_t plane_stride, void* memtab, void* stream);
 int dbk_rb_debug(unsigned long long* out24, int32_t reset, int32_t enable);
 int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream);
 int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int32_t* fid,

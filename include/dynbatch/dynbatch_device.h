@@ -55,8 +55,8 @@ typedef struct {
 
 /* Per-kernel-class device time of a timed loop (CUDA events on the session
  * stream around every launch of the class). Classes: 0 scheduler, 1 plan,
- * 2 gather, 3 conv1x1 / moe gate+sort, 4 conv3x3#1 / moe GEMM1, 5 conv3x3#2 /
- * moe GEMM2, 6 layout / combine, 7 dense step. */
+ * 2 gather, 3 moe gate+sort, 4 fused conv step (conv1x1 + conv3x3 ×2) / moe
+ * GEMM1, 5 moe GEMM2, 6 layout / combine, 7 dense step. */
 typedef struct {
   double ms[8];
   int64_t launches[8];

@@ -17,7 +17,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdynbatch.so")
+# DYNBATCH_LIB selects another build of the library (A/B timing of variants)
+LIB_PATH = os.environ.get("DYNBATCH_LIB") or os.path.join(_HERE, "libdynbatch.so")
 
 DB_OK = 0
 STATUS = {0: "DB_OK", 1: "DB_ERR_INVALID_ARG", 2: "DB_ERR_UNKNOWN_FUNCTION",
@@ -82,8 +83,11 @@ class KernelTimes(C.Structure):
                 ("bytes", C.c_double * 8)]
 
 
-KERNEL_CLASSES = ["scheduler", "plan", "gather", "conv1x1|moe_gate_sort", "conv3x3_1|moe_gemm1",
-                  "conv3x3_2|moe_gemm2", "layout|combine", "dense_step"]
+# Profiler classes (db_kernel_times_t): IEP uses scheduler, plan, gather and
+# the fused conv step (class 4); MoE uses gate+sort (3), GEMM1 (4), GEMM2 (5)
+# and combine (6).
+KERNEL_CLASSES = ["scheduler", "plan", "gather", "moe_gate_sort", "conv_step|moe_gemm1",
+                  "moe_gemm2", "layout|combine", "dense_step"]
 
 LOG_FN = C.CFUNCTYPE(None, C.c_char_p, C.c_void_p)
 VP = C.c_void_p

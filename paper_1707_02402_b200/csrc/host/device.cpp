@@ -343,12 +343,20 @@ void IepSession::add_forward_work() {
     prof_.add_work(7, dense_flops, dense_bytes);
     return;
   }
-  const double map32 = 100352.0, stage16 = 225.0 * 16 * 16;  // fp32 node map, bf16 staged image
+  // Tier B: fp32 maps for inputs / roots / shared children, fp16 staged
+  // images (225 positions × 256 B) for everything else; block inputs are
+  // staged as hi + lo images (the residual).
+  const double map32 = 100352.0, stage16 = 225.0 * 16 * 16;
   const double n_exp = n_un + n_bin;
-  prof_.add_work(2, 0.0, n_un * (map32 + stage16) + n_bin * (2 * map32 + 2 * stage16));
-  prof_.add_work(3, n_bin * 12845056.0, n_bin * (2 * stage16 + stage16 + map32));
-  prof_.add_work(4, n_exp * 57802752.0, n_exp * 2 * stage16);
-  prof_.add_work(5, n_exp * 57802752.0, n_exp * (stage16 + 2 * map32));
+  const double b = static_cast<double>(c.b);
+  // gather: leaf / shared operands, fp32 map → hi (+ lo for unary members)
+  prof_.add_work(2, 0.0, n_un * (map32 + 2 * stage16) + n_bin * 2 * (map32 + stage16));
+  // fused conv step: conv1x1 (binary) + conv3x3 #1 + conv3x3 #2 with the
+  // residual; reads x hi, mid, hi/lo; writes mid, hi/lo images (roots: fp32)
+  const double conv_flops = n_bin * 12845056.0 + n_exp * 2 * 57802752.0;
+  const double conv_bytes = n_bin * (2 * stage16 + 2 * stage16) + n_exp * (stage16 + stage16) +
+                            n_exp * (3 * stage16) + (n_exp - b) * 2 * stage16 + b * map32;
+  prof_.add_work(4, conv_flops, conv_bytes);
 }
 
 double IepSession::time_forwards(int iters, bool profile, KernelTimes* kt) {

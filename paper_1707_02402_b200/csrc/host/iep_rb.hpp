@@ -16,7 +16,8 @@ struct IepSession::RB {
   Buf<float> inputs;              // [b][kFmap] plane maps
   Buf<float> values;              // [N][kFmap] node values (and parked z)
   Buf<float> chw_in, chw_out;     // reference-layout rows for host I/O
-  Buf<std::uint16_t> stage_x, stage_cat, stage_mid;  // fp16 staging
+  Buf<std::uint16_t> stage_x, stage_lo, stage_cat, stage_mid;  // fp16 staging (hi, lo, [x; y], mid)
+  Buf<std::uint16_t> ident;  // two 16 KB identity weight blocks (residual through the MMA)
   std::vector<Buf<std::uint16_t>> wbuf;              // packed fp16 weights
   std::vector<Buf<float>> bbuf;
   Buf<const void*> w0tab, w1tab, w2tab;
@@ -24,6 +25,8 @@ struct IepSession::RB {
   Buf<std::int32_t> seg_start, group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
       step_positions, tile_group, tile_q0, bin_group, bin_q0, fwd_ok, fwd_pos, fwd_slot;
   Buf<std::uint64_t> memtab;  // per-member epilogue metadata, 32 bytes each (rb_conv.cu MemberEntry)
+  Buf<std::int32_t> done0, done1, queue;  // fused step kernel: tile done flags, claim counters
+  std::int32_t epoch = 0;                 // forward counter stamped into the done flags
   std::int64_t n_expensive = 0;
   int tile_m = kTileM;  // positions per scheduled tile
 };

@@ -109,11 +109,18 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   }
   const size_t ps = static_cast<size_t>(R.plane_stride);
   R.stage_x.alloc(ps * 16 * 8);
+  R.stage_lo.alloc(ps * 16 * 8);
   R.stage_cat.alloc(ps * 32 * 8);
   R.stage_mid.alloc(ps * 16 * 8);
   R.stage_x.zero(stream_);
+  R.stage_lo.zero(stream_);
   R.stage_cat.zero(stream_);
   R.stage_mid.zero(stream_);
+  {  // identity weights: conv3x3 #2 adds the residual hi + lo on the tensor cores
+    std::vector<double> eye(static_cast<size_t>(C) * C, 0.0);
+    for (int c = 0; c < C; ++c) eye[static_cast<size_t>(c) * C + c] = 1.0;
+    R.ident.upload(pack_blocks(eye, C, C, 1), stream_);
+  }
   // schedule-derived tables (G ≤ max keys; tiles ≤ N_exp·225/256 + G)
   const size_t G = static_cast<size_t>(std::max(1, c.s_max)) * c.p + 2;
   const size_t S = static_cast<size_t>(std::max<std::int64_t>(c.N, 1)) + 2;  // naive: S = N
@@ -128,6 +135,11 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   R.tile_q0.alloc(T + N);
   R.bin_group.alloc(T + N);
   R.bin_q0.alloc(T + N);
+  R.done0.alloc(T + N);
+  R.done1.alloc(T + N);
+  R.done0.zero(stream_);
+  R.done1.zero(stream_);
+  R.queue.alloc(S + 1);
   // weights
   std::vector<const void*> w0(static_cast<size_t>(c.p), nullptr), w1 = w0, w2 = w0;
   std::vector<const float*> b0(static_cast<size_t>(c.p), nullptr), b1 = b0, b2 = b0;
@@ -171,6 +183,7 @@ void IepSession::forward_resblock() {
   const int sms = sm_count();
   if (layout_dirty_) {  // a new image layout: pads / gaps must read as zeros
     R.stage_x.zero(stream_);
+    R.stage_lo.zero(stream_);
     R.stage_cat.zero(stream_);
     R.stage_mid.zero(stream_);
     layout_dirty_ = false;
@@ -182,43 +195,34 @@ void IepSession::forward_resblock() {
                     R.bin_group.get(), R.bin_q0.get(), B.csr().N, B.member_g.get(), B.child0.get(),
                     B.child1.get(), R.fwd_ok.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.tile_m, stream_),
         "dbk_rb_plan");
-  check(dbk_rb_memtab(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
-                      R.seg_start.get(), B.member_g.get(), B.fid.get(), B.child0.get(), B.example.get(),
-                      R.fwd_pos.get(), R.fwd_slot.get(), R.inputs.get(), R.values.get(), R.stage_x.get(),
-                      R.stage_cat.get(), R.plane_stride, R.memtab.get(), stream_),
+  check(dbk_rb_memtab(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), R.seg_start.get(),
+                      B.member_g.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.values.get(), R.stage_x.get(),
+                      R.stage_lo.get(), R.stage_cat.get(), R.plane_stride, R.memtab.get(), stream_),
         "dbk_rb_memtab");
   prof_.end(stream_);
   launches_ += 5;
   const int gather_blocks = static_cast<int>(std::min<std::int64_t>(std::max<std::int64_t>(R.n_expensive, 1), sms * 8));
+  check(cudaMemsetAsync(R.queue.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_), "queue reset");
+  ++R.epoch;
   for (int s = 0; s < S; ++s) {
     prof_.begin(2, stream_);
     check(dbk_rb_gather(s, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), R.seg_start.get(),
                         B.member_g.get(), B.arity_of.get(), B.fid.get(), B.child0.get(), B.child1.get(),
                         B.example.get(), R.fwd_ok.get(), R.inputs.get(), R.values.get(), R.stage_x.get(),
-                        R.stage_cat.get(),
-                        R.plane_stride, gather_blocks, stream_),
+                        R.stage_lo.get(), R.stage_cat.get(), R.plane_stride, gather_blocks, stream_),
           "dbk_rb_gather");
     prof_.end(stream_);
-    // conv1x1 over the binary groups' [x; y] → z (stage_x + parked fp32)
-    prof_.begin(3, stream_);
-    check(dbk_rb_conv(0, s, R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
-                      B.group_begin.get(), R.seg_start.get(), R.memtab.get(), R.stage_cat.get(), R.stage_x.get(),
-                      R.plane_stride, R.w0tab.get(), R.b0tab.get(), sms, stream_),
-          "conv1x1");
-    prof_.end(stream_);
+    // conv1x1 + conv3x3 #1 + conv3x3 #2 (+ residual) of the step, one launch
     prof_.begin(4, stream_);
-    check(dbk_rb_conv(1, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
-                      B.group_begin.get(), R.seg_start.get(), R.memtab.get(), R.stage_x.get(), R.stage_mid.get(),
-                      R.plane_stride, R.w1tab.get(), R.b1tab.get(), sms, stream_),
-          "conv3x3 #1");
+    check(dbk_rb_step(s, R.epoch, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(),
+                      R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
+                      B.group_begin.get(), R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(),
+                      R.memtab.get(), R.stage_x.get(), R.stage_lo.get(), R.stage_cat.get(), R.stage_mid.get(),
+                      R.plane_stride, R.w0tab.get(), R.w1tab.get(), R.w2tab.get(), R.b0tab.get(), R.b1tab.get(),
+                      R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.queue.get(), sms, stream_),
+          "conv step");
     prof_.end(stream_);
-    prof_.begin(5, stream_);
-    check(dbk_rb_conv(2, s, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(), B.group_fid.get(),
-                      B.group_begin.get(), R.seg_start.get(), R.memtab.get(), R.stage_mid.get(), nullptr,
-                      R.plane_stride, R.w2tab.get(), R.b2tab.get(), sms, stream_),
-          "conv3x3 #2");
-    prof_.end(stream_);
-    launches_ += 4;
+    launches_ += 2;
   }
 }
 

@@ -9,38 +9,50 @@
 // example's input map instead of being copied.
 //
 // Data layout:
-//   * node values / inputs: fp32 "plane maps" [16 planes][196 px][8 ch]
-//     (plane j = channels 8j..8j+7) — 100,352 B per node;
+//   * fp32 "plane maps" [16 planes][196 px][8 ch] (plane j = channels
+//     8j..8j+7), 100,352 B per map: the inputs, and the values of roots and
+//     of children shared by several parents (the only values read later);
 //   * per-step staging: fp16 planes over a packed position axis. Each image
 //     occupies a 15×15 grid (225 positions; row 14 and column 14 are zero
 //     pads shared with the next image / row), so a 3×3 tap (dh, dw) is the
 //     row shift dh·15 + dw of the same array. Images of one call group are
 //     contiguous; each group's segment starts on a TILE_M boundary so a CTA
 //     tile never mixes weights. Plane j of position q lives at
-//     ((j·PS) + GUARD + q) · 16 bytes.
+//     ((j·PS) + GUARD + q) · 16 bytes. A block input x is staged twice:
+//     hi = fp16(x) in stage_x (the conv3x3 #1 operand) and lo = fp16(x − hi)
+//     in stage_lo; hi + lo carries x to ≈2^-22 relative (fp32-equivalent);
 //   * tensor-core operands use the K-major SWIZZLE_NONE canonical layout
 //     (tc_common.cuh): the shared-memory activation window
 //     [plane][position][8] is a valid operand starting at ANY position, so
 //     all nine taps read the same window at different row offsets — the
 //     im2col never materialises.
 //
-// Kernel (one CTA per SM, persistent over the step's tile list):
-//   warp 0 — producer: bulk async copies (TMA engine) of the activation
-//            window per 64-channel K chunk (TILE_M + 2·halo positions × 8
-//            planes, double-buffered) and a ring of 16 KB weight stages
-//            (one (chunk, tap) block each);
-//   warp 1 — TMEM allocator + single-thread tcgen05.mma issuer:
-//            D[128 out channels][256 positions] (M = 128, N = 256, K = 16),
-//            A = weight stage, B = window at the tap's row shift;
-//   warps 2-9 — epilogue: per-tile position table in shared memory, then
-//            tcgen05.ld (lane = channel, 32 positions per load), bias, ReLU,
-//            residual, pad masking, fp16 staging / fp32 node-value stores.
+// The residual is added on the tensor cores: conv3x3 #2 accumulates
+// W2·mid + I·hi + I·lo (I = identity weight blocks, exact products, fp32
+// accumulation), so every operand arrives by TMA and every epilogue is
+// store-only: bias, ReLU, fp16 hi/lo images for the parent's call and fp32
+// values only where a later reader needs them.
+//
+// One persistent launch per step (k_rb_step, one CTA per SM) runs the
+// step's conv1x1, conv3x3 #1 and conv3x3 #2 tiles from a device work queue:
+//   warp 0   — scheduler + window producer: claims items, waits for the
+//              tiles an item's window reads (done flags), bulk-copies (TMA
+//              engine) the activation window per 64-channel K chunk;
+//   warp 1   — TMEM allocator + single-thread tcgen05.mma issuer:
+//              D[128 out channels][256 positions] (M = 128, N = 256, K = 16),
+//              A = weight stage, B = window at the tap's row shift;
+//   warps 2-9 — epilogue: tcgen05.ld (lane = channel), 8×8 lane transposes
+//              to position-major 16-byte vectors, bias, ReLU, stores;
+//   warp 10  — fills each tile's per-position table (targets, validity)
+//              ahead of the epilogue;
+//   warp 11  — streams the weight stages, decoupled from the windows.
 // Accumulators are double-buffered in TMEM (2 × 256 columns) so the epilogue
-// of tile i overlaps the MMAs of tile i+1.
+// of one tile overlaps the MMAs of the next.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "dynbatch/dbk.h"
 #include "tc_common.cuh"
@@ -49,104 +61,180 @@ namespace {
 
 using namespace dbk;
 
-constexpr int kC = 128;              // channels
-constexpr int kPlanes = kC / 8;      // 16
-constexpr int kImg = 225;            // 15 × 15 packed grid per image
-constexpr int kPx = 196;             // 14 × 14
-constexpr int kFmap = kPlanes * kPx * 8;  // 25,088 floats per node map
-constexpr int kGuard = 32;           // zero positions before position 0
-constexpr int kTileM = 256;          // positions per CTA tile (MMA N)
-constexpr int kChunkPlanes = 8;      // K chunk = 64 input channels = 8 planes
-constexpr int kBStage = 128 * 64 * 2;  // 16 KB: 128 out channels × K=64 fp16 weight block
-constexpr int kASlots = 2;           // A window double-buffered per K chunk
-constexpr int kEpiWarps = 8;         // two warps per TMEM lane quarter, 128 positions each
+constexpr int kC = 128;                    // channels
+constexpr int kPlanes = kC / 8;            // 16
+constexpr int kImg = 225;                  // 15 × 15 packed grid per image
+constexpr int kPx = 196;                   // 14 × 14
+constexpr int kFmap = kPlanes * kPx * 8;   // 25,088 floats per node map
+constexpr int kGuard = 32;                 // zero positions before position 0
+constexpr int kTileM = 256;                // positions per CTA tile (MMA N)
+constexpr int kHalo = 16;                  // 3×3 window halo (15 + 1 positions)
+constexpr int kWin = kTileM + 2 * kHalo;   // window rows (row stride of every A slot)
+constexpr int kChunkPlanes = 8;            // K chunk = 64 input channels = 8 planes
+constexpr int kASlot = kChunkPlanes * kWin * 16;  // 36 KB activation window slot
+constexpr int kASlots = 4;                 // window slots (short hi/lo and 1×1 chunks need depth)
+constexpr int kBStage = 128 * 64 * 2;      // 16 KB: 128 out channels × K=64 fp16 weight block
+constexpr int kBStages = 4;
+constexpr int kEpiWarps = 8;               // two warps per TMEM lane quarter, 128 positions each
 constexpr int kTableWarp = 2 + kEpiWarps;  // fills the per-tile position tables ahead of the epilogue
-constexpr int kThreads = (kTableWarp + 1) * 32;
-
-// K is streamed in 64-channel chunks: for each chunk the producer loads one
-// A slot (8 planes × the position window) and then one 16 KB weight block
-// per tap; the MMA warp consumes (chunk, tap) blocks in that order, so the
-// next chunk's (or next tile's) window loads while the current one computes.
-template <int KIND>
-struct Cfg;
-template <>
-struct Cfg<0> {  // conv1x1 over [x; y] (256 → 128)
-  static constexpr int kChunks = 4, kTaps = 1, kHalo = 0, kBStages = 6;
-};
-template <>
-struct Cfg<1> {  // conv3x3 #1 (128 → 128)
-  static constexpr int kChunks = 2, kTaps = 9, kHalo = 16, kBStages = 8;
-};
-template <>
-struct Cfg<2> : Cfg<1> {};  // conv3x3 #2 + residual
-
-template <int KIND>
-constexpr int win() { return kTileM + 2 * Cfg<KIND>::kHalo; }
-template <int KIND>
-constexpr int a_slot_bytes() { return kChunkPlanes * win<KIND>() * 16; }
-
+constexpr int kWeightWarp = kTableWarp + 1;  // streams the weight stages
+constexpr int kThreads = (kWeightWarp + 1) * 32;
+constexpr int kItemSlots = 4;              // work items in flight between the roles
+constexpr int kChunk = 16;                 // positions per epilogue chunk
+constexpr int kChunks = 128 / kChunk;      // chunks per warp and tile
 
 // Per-member epilogue metadata (schedule order), built once per forward by
 // k_rb_memtab from the forwarding tables.
 struct MemberEntry {
-  const float* res;  // residual map of conv3x3 #2 (binary: own slot = z; unary: child / input)
-  float* slot;       // the node's own fp32 plane map
-  uint8_t* fwd;      // parent's fp16 operand image of this node (plane 0, position 0) or null
-  int32_t keep32;    // conv3x3 #2 stores the fp32 value (a reader needs it)
+  float* slot;      // the node's fp32 plane map (written only when keep32)
+  uint8_t* fwd;     // parent's fp16 operand image of this node (plane 0, position 0) or null
+  uint8_t* fwd_lo;  // its lo image (unary parents: the residual) or null
+  int32_t keep32;   // a later reader needs the fp32 value (root, shared child)
   int32_t pad;
 };
 
-struct ConvParams {
-  int32_t step;
-  const int32_t* step_tile_begin;
-  const int32_t* tile_group;
-  const int32_t* tile_q0;
-  const int32_t* group_fid;
-  const int32_t* group_begin;
-  const int32_t* seg_start;
-  const MemberEntry* memtab;
-  const __half* stage_in;
-  __half* stage_out;
-  int64_t ps;  // plane stride in positions
-  const __half* const* wpack;
-  const float* const* bias;
-  int32_t debug;  // nonzero: the MMA thread accumulates its wait cycles in g_conv_dbg
-};
-
-// MMA-thread wait accounting per kernel kind: [waiting for a drained
-// accumulator, for an A window, for a weight stage, total cycles of the MMA
-// loop] (entries 12..23 are unused). Read/reset with dbk_rb_debug().
-__device__ unsigned long long g_conv_dbg[6 * 4];
-
-// Residual source of positions that are not real pixels (read, never used).
-__device__ float4 g_zero_res[2 * kPlanes * kPx];
-
-// Per-position epilogue table of one tile (built by the 256 epilogue threads,
-// one position each, read warp-uniformly by the 8 epilogue warps).
+// Per-position epilogue table of one tile.
 struct PosEntry {
-  const float* res;  // KIND 2: residual map + px·8 (plane 0, channel 0)
-  float* dst;        // KIND 0/2: node plane map + px·8 (nullptr: no fp32 store)
-  uint8_t* fwd;      // KIND 2: parent's fp16 operand image at this position (plane 0)
-  int32_t valid;     // a real pixel of a real member
+  float* dst;       // fp32 store target (plane 0 of this pixel) or null
+  uint8_t* fwd;     // hi image target (plane 0 of this position) or null
+  uint8_t* fwd_lo;  // lo image target or null
+  int32_t valid;    // a real pixel of a real member
   int32_t pad;
 };
 constexpr int kTableBytes = 2 * kTileM * static_cast<int>(sizeof(PosEntry));  // double-buffered
 
-template <int KIND>
-constexpr int smem_bytes() {
-  return kASlots * a_slot_bytes<KIND>() + Cfg<KIND>::kBStages * kBStage + kTableBytes + 256;
+struct Item {
+  int32_t kind;  // 0 conv1x1, 1 conv3x3 #1, 2 conv3x3 #2, -1 end
+  int32_t tile;  // global tile index (bin-tile list for kind 0)
+  int32_t g, q0;
+};
+
+struct StepParams {
+  int32_t step, epoch, lookahead, debug;
+  const int32_t* step_tile_begin;
+  const int32_t* tile_group;
+  const int32_t* tile_q0;
+  const int32_t* step_bintile_begin;
+  const int32_t* bin_group;
+  const int32_t* bin_q0;
+  const int32_t* group_fid;
+  const int32_t* group_begin;
+  const int32_t* seg_start;
+  const int32_t* group_tile0;
+  const int32_t* group_bintile0;
+  const MemberEntry* memtab;
+  uint8_t* stage_x;    // block inputs (hi) / conv1x1 output z (hi)
+  uint8_t* stage_lo;   // their lo images
+  uint8_t* stage_cat;  // binary operands [x; y] (hi)
+  uint8_t* stage_mid;  // conv3x3 #1 output
+  int64_t ps;          // plane stride in positions
+  const uint8_t* const* wpack[3];
+  const float* const* bias[3];
+  const uint8_t* ident;  // two 16 KB identity blocks (the residual's weights)
+  int32_t* done0;        // per bin tile: conv1x1 done (== epoch)
+  int32_t* done1;        // per tile: conv3x3 #1 done (== epoch)
+  int32_t* queue;        // per-step claim counters (zeroed each forward)
+};
+
+// MMA-thread wait accounting: [waiting for a drained accumulator, for an A
+// window, for a weight stage, total cycles of the MMA loop] (slots 3..5 of
+// six; read/reset with dbk_rb_debug()).
+__device__ unsigned long long g_conv_dbg[6 * 4];
+
+// ------------------------------------------------------------ K phases
+// A tile's K loop is one to three phases of (window source, weights, chunks,
+// taps, halo): conv1x1 [x; y] (4 chunks × 1 tap); conv3x3 #1 over x
+// (2 × 9, halo 16); conv3x3 #2 over mid (2 × 9, halo 16) + I·hi + I·lo
+// (2 × 1 each, no halo).
+struct Phase {
+  const uint8_t* src;  // staging base (position 0 of plane 0)
+  const uint8_t* w;    // weight blocks
+  int chunks, taps, halo;
+};
+
+__device__ __forceinline__ int n_phases(int kind) { return kind == 2 ? 3 : 1; }
+
+__device__ __forceinline__ Phase phase_of(const StepParams& P, const Item& it, int p) {
+  const int32_t f = P.group_fid[it.g];
+  if (it.kind == 0) return Phase{P.stage_cat, P.wpack[0][f], 4, 1, 0};
+  if (it.kind == 1) return Phase{P.stage_x, P.wpack[1][f], 2, 9, kHalo};
+  if (p == 0) return Phase{P.stage_mid, P.wpack[2][f], 2, 9, kHalo};
+  return Phase{p == 1 ? P.stage_x : P.stage_lo, P.ident, 2, 1, 0};
 }
 
+// ------------------------------------------------------- work queue
+// Queue order: all conv1x1 tiles, then conv3x3 #1 tiles interleaved with
+// conv3x3 #2 tiles `lookahead` positions behind, so each SM alternates
+// MMA-heavy and store-heavy tiles and a #2 tile's inputs are usually done
+// when it is claimed.
+__device__ __forceinline__ Item step_item(const StepParams& P, int32_t k, int32_t n0, int32_t n1) {
+  int32_t kind, local;
+  if (k < n0) {
+    kind = 0;
+    local = k;
+  } else {
+    const int32_t u = k - n0;
+    const int32_t D = min(P.lookahead, n1);
+    const int32_t R = n1 - D;
+    if (u < D) {
+      kind = 1;
+      local = u;
+    } else if (u - D < 2 * R) {
+      const int32_t v = u - D;
+      kind = (v & 1) ? 1 : 2;
+      local = (v & 1) ? D + (v >> 1) : (v >> 1);
+    } else {
+      kind = 2;
+      local = R + (u - D - 2 * R);
+    }
+  }
+  Item it;
+  it.kind = kind;
+  if (kind == 0) {
+    it.tile = P.step_bintile_begin[P.step] + local;
+    it.g = P.bin_group[it.tile];
+    it.q0 = P.bin_q0[it.tile];
+  } else {
+    it.tile = P.step_tile_begin[P.step] + local;
+    it.g = P.tile_group[it.tile];
+    it.q0 = P.tile_q0[it.tile];
+  }
+  return it;
+}
+
+// Producer side: wait until the tiles this item's windows read are written
+// in this launch (earlier launches are ordered by the stream). conv3x3 #1 of
+// a binary group reads z (conv1x1 tiles i-1..i+1); conv3x3 #2 reads mid
+// (conv3x3 #1 tiles i-1..i+1) and, for a binary group, z hi/lo (conv1x1
+// tile i). Halo positions in other segments only feed outputs never stored.
+__device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& it) {
+  if (it.kind == 0) return;
+  const int32_t g = it.g;
+  const int32_t rows = P.group_begin[g + 1] - P.group_begin[g];
+  const int32_t nt = (rows * kImg + kTileM - 1) / kTileM;
+  const int32_t i = (it.q0 - P.seg_start[g]) / kTileM;
+  const bool binary = P.group_bintile0[g] >= 0;
+  const int32_t b0 = binary ? P.step_bintile_begin[P.step] + P.group_bintile0[g] : 0;
+  if (it.kind == 1) {
+    if (!binary) return;
+    for (int32_t j = max(i - 1, 0); j <= min(i + 1, nt - 1); ++j) wait_flag(P.done0 + b0 + j, P.epoch);
+  } else {
+    const int32_t t0 = P.step_tile_begin[P.step] + P.group_tile0[g];
+    for (int32_t j = max(i - 1, 0); j <= min(i + 1, nt - 1); ++j) wait_flag(P.done1 + t0 + j, P.epoch);
+    if (binary) wait_flag(P.done0 + b0 + i, P.epoch);
+  }
+  fence_proxy_async_global();
+}
+
+// ------------------------------------------------------------- tables
 // Fills the table entries of positions lane + 32k (k = 0..7) of a tile from
 // the per-member table: one independent 32-byte load per position, all
 // issued before any entry is stored.
-template <int KIND>
-__device__ __forceinline__ void rb_fill_table(const ConvParams& P, PosEntry* tab, int32_t g, int32_t q0,
-                                              int lane) {
+__device__ __forceinline__ void rb_fill_table(const StepParams& P, const Item& it, PosEntry* tab, int lane) {
   constexpr int kPer = kTileM / 32;
-  const int32_t gb0 = P.group_begin[g];
-  const int32_t rows = P.group_begin[g + 1] - gb0;
-  const int32_t base = q0 - P.seg_start[g];
+  const int32_t gb0 = P.group_begin[it.g];
+  const int32_t rows = P.group_begin[it.g + 1] - gb0;
+  const int32_t base = it.q0 - P.seg_start[it.g];
   MemberEntry me[kPer];
   int32_t rem[kPer], px[kPer];
   bool valid[kPer];
@@ -158,25 +246,21 @@ __device__ __forceinline__ void rb_fill_table(const ConvParams& P, PosEntry* tab
     const int32_t r = rem[k] / 15, c = rem[k] - r * 15;
     valid[k] = img < rows && r < 14 && c < 14;
     px[k] = r * 14 + c;
-    if (KIND != 1 && valid[k]) me[k] = P.memtab[gb0 + img];
+    if (it.kind == 2 && valid[k]) me[k] = P.memtab[gb0 + img];
   }
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     PosEntry e{nullptr, nullptr, nullptr, valid[k] ? 1 : 0, 0};
-    if (KIND != 1 && valid[k]) {
-      float* slot = me[k].slot + px[k] * 8;
-      if (KIND == 0) {
-        e.dst = slot;  // fp32 z, the residual of the binary block
-      } else {
-        e.res = me[k].res + px[k] * 8;
-        e.dst = me[k].keep32 ? slot : nullptr;
-        e.fwd = me[k].fwd ? me[k].fwd + rem[k] * 16 : nullptr;
-      }
+    if (it.kind == 2 && valid[k]) {
+      e.dst = me[k].keep32 ? me[k].slot + px[k] * 8 : nullptr;
+      e.fwd = me[k].fwd ? me[k].fwd + rem[k] * 16 : nullptr;
+      e.fwd_lo = me[k].fwd_lo ? me[k].fwd_lo + rem[k] * 16 : nullptr;
     }
     tab[lane + 32 * k] = e;
   }
 }
 
+// ----------------------------------------------------------- epilogue
 // 8×8 transpose across the 8 lanes of a plane group (three butterfly
 // stages): in, lane e holds x[i] = D[channel 8g+e][position i]; out, lane e
 // holds x[k] = D[channel 8g+k][position e].
@@ -195,120 +279,106 @@ __device__ __forceinline__ void transpose8(float* x, int e) {
   }
 }
 
-// Epilogue of one tile for this warp: TMEM lanes = output channels
-// 32·quarter + lane, columns = the tile's positions; the warp covers
-// positions [128·half, 128·half + 128) in eight 16-column chunks. After the
-// in-register transpose, lane (g = lane/8, e = lane%8) owns positions
-// 8m + e (m = 0, 1) of each chunk with the 8 channels of plane 4·quarter + g,
-// so every global access is a 16-byte vector (fp16 image: one, fp32 map:
-// two) and a warp instruction covers 4 planes × 8 consecutive positions.
+// hi = fp16(o), lo = fp16(o − hi) of 8 channels, as two 16-byte vectors.
+__device__ __forceinline__ void split_f16x8(const float* o, uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const __half2 hh = __floats2half2_rn(o[2 * j], o[2 * j + 1]);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(o[2 * j] - hf.x, o[2 * j + 1] - hf.y);
+    h[j] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[j] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// Epilogue lane geometry: TMEM lanes = output channels 32·quarter + lane,
+// columns = the tile's positions; the warp covers positions
+// [128·half, 128·half + 128) in eight 16-column chunks. After the transpose,
+// lane (g = lane/8, e = lane%8) owns positions 8m + e (m = 0, 1) of each
+// chunk with the 8 channels of plane 4·quarter + g, so every global store is
+// a 16-byte vector and a warp instruction covers 4 planes × 8 positions.
 struct EpiLane {
   int quarter, half, e, plane;
   int64_t plane_off16;  // fp16 staging offset of this lane's plane
   int plane_off32;      // fp32 plane-map offset of this lane's plane
 };
 
-constexpr int kChunk = 16;                 // positions per epilogue chunk
-constexpr int kChunks = 128 / kChunk;      // chunks per warp and tile
-constexpr int kResAhead = 3;               // residual prefetch distance (chunks)
-
-// Residual rows of chunk cb of a tile for this lane (2 positions × 8 ch).
-// Unconditional loads (invalid positions read a zero record) followed by a
-// warp sync, so ptxas issues them here instead of sinking them to the uses.
-__device__ __forceinline__ void rb_load_res(const PosEntry* tab, const EpiLane& L, int cb, float4* r) {
-  const float* zero = reinterpret_cast<const float*>(g_zero_res);
-  const PosEntry* my = tab + L.half * 128 + cb * kChunk + L.e;
-#pragma unroll
-  for (int m = 0; m < kChunk / 8; ++m) {
-    const PosEntry& pe = my[8 * m];
-    const float4* rp = reinterpret_cast<const float4*>((pe.valid ? pe.res : zero) + L.plane_off32);
-    r[2 * m] = __ldg(rp);
-    r[2 * m + 1] = __ldg(rp + 1);
-  }
-  __syncwarp();
-}
-
-// One 16-position chunk: TMEM → transpose → bias (+ residual) → ReLU → stores.
 template <int KIND>
-__device__ __forceinline__ void rb_chunk(const ConvParams& P, const PosEntry* tab, const EpiLane& L,
-                                         uint32_t taddr, const float* bias, int32_t q0, int cb,
-                                         const float4* res) {
-  float v[kChunk];
-  tmem_ld16(taddr + cb * kChunk, v);
-  const PosEntry* my = tab + L.half * 128 + cb * kChunk + L.e;
+__device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntry* tab, const EpiLane& L,
+                                              uint32_t taddr, const Item& it) {
+  const float* bias_p = P.bias[KIND][P.group_fid[it.g]] + L.plane * 8;
+  const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias_p));
+  const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias_p + 4));
+  const float bias[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
+  // own-position outputs (conv1x1 → z hi/lo, conv3x3 #1 → mid)
+  uint8_t* own = (KIND == 0 ? P.stage_x : P.stage_mid) +
+                 static_cast<int64_t>(kGuard + it.q0 + L.half * 128 + L.e) * 16 + L.plane_off16;
+  uint8_t* own_lo = P.stage_lo + static_cast<int64_t>(kGuard + it.q0 + L.half * 128 + L.e) * 16 + L.plane_off16;
+#pragma unroll 2
+  for (int cb = 0; cb < kChunks; ++cb) {
+    float v[kChunk];
+    tmem_ld16(taddr + cb * kChunk, v);
+    const PosEntry* my = tab + L.half * 128 + cb * kChunk + L.e;
 #pragma unroll
-  for (int m = 0; m < kChunk / 8; ++m) {
-    float* x = v + 8 * m;
-    transpose8(x, L.e);
-    const PosEntry& pe = my[8 * m];
-    if constexpr (KIND == 2) {
-      if (pe.valid) {
-        const float4 r0 = res[2 * m], r1 = res[2 * m + 1];
-        const float o[8] = {fmaxf(x[0] + bias[0] + r0.x, 0.f), fmaxf(x[1] + bias[1] + r0.y, 0.f),
-                            fmaxf(x[2] + bias[2] + r0.z, 0.f), fmaxf(x[3] + bias[3] + r0.w, 0.f),
-                            fmaxf(x[4] + bias[4] + r1.x, 0.f), fmaxf(x[5] + bias[5] + r1.y, 0.f),
-                            fmaxf(x[6] + bias[6] + r1.z, 0.f), fmaxf(x[7] + bias[7] + r1.w, 0.f)};
+    for (int m = 0; m < kChunk / 8; ++m) {
+      float* x = v + 8 * m;
+      transpose8(x, L.e);
+      const PosEntry& pe = my[8 * m];
+      float o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = pe.valid ? fmaxf(x[k] + bias[k], 0.f) : 0.f;
+      const int64_t off = static_cast<int64_t>(cb * kChunk + 8 * m) * 16;
+      if (KIND == 1) {
+        uint4 pk;
+        pk.x = pack_f16x2(o[0], o[1]);
+        pk.y = pack_f16x2(o[2], o[3]);
+        pk.z = pack_f16x2(o[4], o[5]);
+        pk.w = pack_f16x2(o[6], o[7]);
+        *reinterpret_cast<uint4*>(own + off) = pk;
+      } else if (KIND == 0) {
+        uint4 hi, lo;
+        split_f16x8(o, hi, lo);
+        *reinterpret_cast<uint4*>(own + off) = hi;
+        *reinterpret_cast<uint4*>(own_lo + off) = lo;
+      } else if (pe.valid) {
+        if (pe.fwd) {
+          uint4 hi, lo;
+          split_f16x8(o, hi, lo);
+          *reinterpret_cast<uint4*>(pe.fwd + L.plane_off16) = hi;
+          if (pe.fwd_lo) *reinterpret_cast<uint4*>(pe.fwd_lo + L.plane_off16) = lo;
+        }
         if (pe.dst) {
           float4* dp = reinterpret_cast<float4*>(pe.dst + L.plane_off32);
           dp[0] = make_float4(o[0], o[1], o[2], o[3]);
           dp[1] = make_float4(o[4], o[5], o[6], o[7]);
         }
-        if (pe.fwd) {
-          uint4 pk;
-          pk.x = pack_f16x2(o[0], o[1]);
-          pk.y = pack_f16x2(o[2], o[3]);
-          pk.z = pack_f16x2(o[4], o[5]);
-          pk.w = pack_f16x2(o[6], o[7]);
-          *reinterpret_cast<uint4*>(pe.fwd + L.plane_off16) = pk;
-        }
-      }
-    } else {
-      float o[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) o[k] = pe.valid ? fmaxf(x[k] + bias[k], 0.f) : 0.f;
-      uint4 pk;
-      pk.x = pack_f16x2(o[0], o[1]);
-      pk.y = pack_f16x2(o[2], o[3]);
-      pk.z = pack_f16x2(o[4], o[5]);
-      pk.w = pack_f16x2(o[6], o[7]);
-      uint8_t* out16 = reinterpret_cast<uint8_t*>(P.stage_out) +
-                       static_cast<int64_t>(kGuard + q0 + L.half * 128 + cb * kChunk + 8 * m + L.e) * 16 +
-                       L.plane_off16;
-      *reinterpret_cast<uint4*>(out16) = pk;
-      if (KIND == 0 && pe.valid) {  // fp32 z, the residual of the binary block
-        float4* dp = reinterpret_cast<float4*>(pe.dst + L.plane_off32);
-        dp[0] = make_float4(o[0], o[1], o[2], o[3]);
-        dp[1] = make_float4(o[4], o[5], o[6], o[7]);
       }
     }
   }
 }
 
-// Implicit-GEMM conv, operands swapped so every MMA is N = 256 wide:
-// D[128 out channels][256 positions] += W[128][k16] · X[256 positions][k16]^T
-// (A = the weight stage, B = the activation window at the tap's row shift).
-// N = 128 MMAs are issue-bound once the per-tap commit / barrier traffic is
-// added (tools/mma_rate.cu: 88–97 cycles vs 64 ideal); N = 256 MMAs run at
-// the ideal 128 cycles with the same per-tap overhead.
-template <int KIND>
-__global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__ ConvParams P) {
-  using K = Cfg<KIND>;
-  constexpr int WIN = win<KIND>();
-  constexpr uint32_t IDESC = idesc_f16_f32(128, kTileM);
+// --------------------------------------------------------------- kernel
+__global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__ StepParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kASlots * a_slot_bytes<KIND>();
-  PosEntry* tables = reinterpret_cast<PosEntry*>(sB + K::kBStages * kBStage);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tables) + kTableBytes);
+  uint8_t* sB = smem + kASlots * kASlot;
+  PosEntry* tables = reinterpret_cast<PosEntry*>(sB + kBStages * kBStage);
+  Item* items = reinterpret_cast<Item*>(reinterpret_cast<uint8_t*>(tables) + kTableBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(items + kItemSlots);
   uint64_t* a_full = bars;
   uint64_t* a_empty = a_full + kASlots;
   uint64_t* b_full = a_empty + kASlots;
-  uint64_t* b_empty = b_full + K::kBStages;
-  uint64_t* acc_full = b_empty + K::kBStages;
+  uint64_t* b_empty = b_full + kBStages;
+  uint64_t* acc_full = b_empty + kBStages;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* tab_full = acc_empty + 2;
   uint64_t* tab_empty = tab_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tab_empty + 2);
+  uint64_t* item_full = tab_empty + 2;
+  uint64_t* item_empty = item_full + kItemSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_empty + kItemSlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -316,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
       mbar_init(a_full + s, 1);
       mbar_init(a_empty + s, 1);
     }
-    for (int s = 0; s < K::kBStages; ++s) {
+    for (int s = 0; s < kBStages; ++s) {
       mbar_init(b_full + s, 1);
       mbar_init(b_empty + s, 1);
     }
@@ -326,6 +396,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
       mbar_init(tab_full + s, 32);
       mbar_init(tab_empty + s, kEpiWarps);
     }
+    for (int s = 0; s < kItemSlots; ++s) {
+      mbar_init(item_full + s, 1);
+      mbar_init(item_empty + s, 3 + kEpiWarps);  // MMA thread, table warp, weight warp, epilogue warps
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -333,92 +407,130 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  const int32_t t_begin = P.step_tile_begin[P.step];
-  const int32_t n_tiles = P.step_tile_begin[P.step + 1] - t_begin;
+  const int32_t n0 = P.step_bintile_begin[P.step + 1] - P.step_bintile_begin[P.step];
+  const int32_t n1 = P.step_tile_begin[P.step + 1] - P.step_tile_begin[P.step];
+  const int32_t total = n0 + 2 * n1;
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------ producer
-      uint32_t ai = 0, bi = 0;
-      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int32_t g = P.tile_group[t_begin + t];
-        const int32_t q0 = P.tile_q0[t_begin + t];
-        const uint8_t* w = reinterpret_cast<const uint8_t*>(P.wpack[P.group_fid[g]]);
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.stage_in) +
-                             static_cast<int64_t>(kGuard + q0 - K::kHalo) * 16;
-        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
-          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
-          mbar_wait(a_empty + sa, pa ^ 1);
-          mbar_expect_tx(a_full + sa, a_slot_bytes<KIND>());
-          for (int j = 0; j < kChunkPlanes; ++j) {
-            bulk_g2s(sA + sa * a_slot_bytes<KIND>() + j * WIN * 16,
-                     src + static_cast<int64_t>(ch * kChunkPlanes + j) * P.ps * 16, WIN * 16, a_full + sa);
-          }
-          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
-            const uint32_t s = bi % K::kBStages, ph = (bi / K::kBStages) & 1;
-            mbar_wait(b_empty + s, ph ^ 1);
-            mbar_expect_tx(b_full + s, kBStage);
-            bulk_g2s(sB + s * kBStage, w + static_cast<int64_t>(ch * K::kTaps + tap) * kBStage, kBStage,
-                     b_full + s);
+    if (lane == 0) {  // ---------------------- scheduler + activation windows
+      uint32_t ai = 0;
+      for (int32_t n = 0;; ++n) {
+        const int32_t k = atomicAdd(P.queue + P.step, 1);
+        const Item it = k < total ? step_item(P, k, n0, n1) : Item{-1, 0, 0, 0};
+        const int slot = n % kItemSlots;
+        mbar_wait(item_empty + slot, ((n / kItemSlots) & 1) ^ 1);
+        items[slot] = it;
+        mbar_arrive(item_full + slot);
+        if (it.kind < 0) break;
+        step_wait_deps(P, it);
+        for (int p = 0; p < n_phases(it.kind); ++p) {
+          const Phase ph = phase_of(P, it, p);
+          const uint32_t rows = kTileM + 2 * ph.halo;
+          const uint8_t* src = ph.src + static_cast<int64_t>(kGuard + it.q0 - ph.halo) * 16;
+          for (int ch = 0; ch < ph.chunks; ++ch, ++ai) {
+            const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+            mbar_wait(a_empty + sa, pa ^ 1);
+            mbar_expect_tx(a_full + sa, kChunkPlanes * rows * 16);
+            for (int j = 0; j < kChunkPlanes; ++j)
+              bulk_g2s(sA + sa * kASlot + j * kWin * 16,
+                       src + static_cast<int64_t>(ch * kChunkPlanes + j) * P.ps * 16, rows * 16, a_full + sa);
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------------------------------- MMA issuer
+      constexpr uint32_t IDESC = idesc_f16_f32(128, kTileM);
       long long w_acc = 0, w_a = 0, w_b = 0;
       const long long t_start = clock64();
       uint32_t ai = 0, bi = 0;
-      int it = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-        const int abuf = it & 1;
+      for (int n = 0;; ++n) {
+        const int slot = n % kItemSlots;
+        mbar_wait(item_full + slot, (n / kItemSlots) & 1);
+        const Item it = items[slot];
+        mbar_arrive(item_empty + slot);
+        if (it.kind < 0) break;
+        const int abuf = n & 1;
         long long c0 = clock64();
-        mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
+        mbar_wait(acc_empty + abuf, ((n >> 1) & 1) ^ 1);
         w_acc += clock64() - c0;
         tc_fence_after();
-        for (int ch = 0; ch < K::kChunks; ++ch, ++ai) {
-          const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
-          c0 = clock64();
-          mbar_wait(a_full + sa, pa);
-          w_a += clock64() - c0;
-          tc_fence_after();
-          const uint32_t a_slot = a_base + sa * a_slot_bytes<KIND>();
-          for (int tap = 0; tap < K::kTaps; ++tap, ++bi) {
-            const uint32_t s = bi % K::kBStages, ph = (bi / K::kBStages) & 1;
+        uint32_t acc = 0;
+        for (int p = 0; p < n_phases(it.kind); ++p) {
+          const int chunks = it.kind == 0 ? 4 : 2;
+          const int taps = (it.kind == 0 || p > 0) ? 1 : 9;
+          const int halo = (it.kind == 0 || p > 0) ? 0 : kHalo;
+          for (int ch = 0; ch < chunks; ++ch, ++ai) {
+            const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
             c0 = clock64();
-            mbar_wait(b_full + s, ph);
-            w_b += clock64() - c0;
+            mbar_wait(a_full + sa, pa);
+            w_a += clock64() - c0;
             tc_fence_after();
-            const int shift = K::kTaps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
-            const uint32_t xrow = static_cast<uint32_t>(K::kHalo + shift);
+            const uint32_t a_slot = a_base + sa * kASlot;
+            for (int tap = 0; tap < taps; ++tap, ++bi) {
+              const uint32_t s = bi % kBStages, par = (bi / kBStages) & 1;
+              c0 = clock64();
+              mbar_wait(b_full + s, par);
+              w_b += clock64() - c0;
+              tc_fence_after();
+              const int shift = taps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
+              const uint32_t xrow = static_cast<uint32_t>(halo + shift);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t wd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
-              const uint64_t xd = smem_desc(a_slot + ((2 * kk) * WIN + xrow) * 16, WIN * 16, 128);
-              mma_bf16(tmem_base + abuf * kTileM, wd, xd, IDESC, (ch | tap | kk) != 0);
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t wd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
+                const uint64_t xd = smem_desc(a_slot + ((2 * kk) * kWin + xrow) * 16, kWin * 16, 128);
+                mma_bf16(tmem_base + abuf * kTileM, wd, xd, IDESC, acc);
+                acc = 1;
+              }
+              mma_commit(b_empty + s);
             }
-            mma_commit(b_empty + s);
+            mma_commit(a_empty + sa);
           }
-          mma_commit(a_empty + sa);
         }
         mma_commit(acc_full + abuf);
       }
       if (P.debug) {
-        atomicAdd(&g_conv_dbg[KIND * 4 + 0], static_cast<unsigned long long>(w_acc));
-        atomicAdd(&g_conv_dbg[KIND * 4 + 1], static_cast<unsigned long long>(w_a));
-        atomicAdd(&g_conv_dbg[KIND * 4 + 2], static_cast<unsigned long long>(w_b));
-        atomicAdd(&g_conv_dbg[KIND * 4 + 3], static_cast<unsigned long long>(clock64() - t_start));
+        atomicAdd(&g_conv_dbg[12 + 0], static_cast<unsigned long long>(w_acc));
+        atomicAdd(&g_conv_dbg[12 + 1], static_cast<unsigned long long>(w_a));
+        atomicAdd(&g_conv_dbg[12 + 2], static_cast<unsigned long long>(w_b));
+        atomicAdd(&g_conv_dbg[12 + 3], static_cast<unsigned long long>(clock64() - t_start));
+      }
+    }
+  } else if (warp == kWeightWarp) {
+    if (lane == 0) {  // -------------------------------------- weight stages
+      uint32_t bi = 0;
+      for (int n = 0;; ++n) {
+        const int slot = n % kItemSlots;
+        mbar_wait(item_full + slot, (n / kItemSlots) & 1);
+        const Item it = items[slot];
+        mbar_arrive(item_empty + slot);
+        if (it.kind < 0) break;
+        for (int p = 0; p < n_phases(it.kind); ++p) {
+          const Phase ph = phase_of(P, it, p);
+          for (int ch = 0; ch < ph.chunks; ++ch) {
+            for (int tap = 0; tap < ph.taps; ++tap, ++bi) {
+              const uint32_t s = bi % kBStages, par = (bi / kBStages) & 1;
+              mbar_wait(b_empty + s, par ^ 1);
+              mbar_expect_tx(b_full + s, kBStage);
+              bulk_g2s(sB + s * kBStage, ph.w + static_cast<int64_t>(ch * ph.taps + tap) * kBStage, kBStage,
+                       b_full + s);
+            }
+          }
+        }
       }
     }
   } else if (warp == kTableWarp) {  // ------------------------ table filler
-    int it = 0;
-    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-      const int buf = it & 1;
-      const int32_t g = P.tile_group[t_begin + t];
-      const int32_t q0 = P.tile_q0[t_begin + t];
-      mbar_wait(tab_empty + buf, ((it >> 1) & 1) ^ 1);
-      rb_fill_table<KIND>(P, tables + buf * kTileM, g, q0, lane);
+    for (int n = 0;; ++n) {
+      const int slot = n % kItemSlots;
+      mbar_wait(item_full + slot, (n / kItemSlots) & 1);
+      const Item it = items[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(item_empty + slot);
+      if (it.kind < 0) break;
+      const int buf = n & 1;
+      mbar_wait(tab_empty + buf, ((n >> 1) & 1) ^ 1);
+      rb_fill_table(P, it, tables + buf * kTileM, lane);
       mbar_arrive(tab_full + buf);  // release: the entries are visible to the waiters
     }
   } else {  // ------------------------------------------------------ epilogue
@@ -430,48 +542,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
     L.plane_off16 = static_cast<int64_t>(L.plane) * P.ps * 16;
     L.plane_off32 = L.plane * kPx * 8;
     const uint32_t lane_addr = (static_cast<uint32_t>(L.quarter * 32) << 16) + L.half * 128;
-    // residual chunks are loaded kResAhead ahead, across tile boundaries
-    // (ring of 4 buffers, so every index is a compile-time constant)
-    float4 rbuf[4][kChunk / 4];
-    int it = 0;
-    int32_t t = blockIdx.x;
-    if (KIND == 2 && t < n_tiles) {
-      mbar_wait(tab_full + 0, 0);
-#pragma unroll
-      for (int c = 0; c < kResAhead; ++c) rb_load_res(tables, L, c, rbuf[c]);
-    }
-    for (; t < n_tiles; t += gridDim.x, ++it) {
-      const int abuf = it & 1;
-      const int32_t g = P.tile_group[t_begin + t];
-      const int32_t q0 = P.tile_q0[t_begin + t];
+    for (int n = 0;; ++n) {
+      const int slot = n % kItemSlots;
+      mbar_wait(item_full + slot, (n / kItemSlots) & 1);
+      const Item it = items[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(item_empty + slot);
+      if (it.kind < 0) break;
+      const int abuf = n & 1;
       const PosEntry* tab = tables + abuf * kTileM;
-      const float* bias_p = P.bias[P.group_fid[g]] + L.plane * 8;
-      const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias_p));
-      const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias_p + 4));
-      const float bias[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
-      mbar_wait(tab_full + abuf, (it >> 1) & 1);
-      mbar_wait(acc_full + abuf, (it >> 1) & 1);
+      mbar_wait(tab_full + abuf, (n >> 1) & 1);
+      mbar_wait(acc_full + abuf, (n >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + abuf * kTileM + lane_addr;
-      const bool has_next = t + static_cast<int32_t>(gridDim.x) < n_tiles;
-#pragma unroll
-      for (int cb = 0; cb < kChunks; ++cb) {
-        if (KIND == 2) {
-          constexpr int A = kResAhead;
-          if (cb + A < kChunks) {
-            rb_load_res(tab, L, cb + A, rbuf[(cb + A) & 3]);
-          } else if (has_next) {
-            const int nb = (it + 1) & 1;
-            if (cb + A == kChunks) mbar_wait(tab_full + nb, ((it + 1) >> 1) & 1);
-            rb_load_res(tables + nb * kTileM, L, cb + A - kChunks, rbuf[(cb + A) & 3]);
-          }
-        }
-        rb_chunk<KIND>(P, tab, L, taddr, bias, q0, cb, rbuf[cb & 3]);
-      }
+      if (it.kind == 0)
+        step_epilogue<0>(P, tab, L, taddr, it);
+      else if (it.kind == 1)
+        step_epilogue<1>(P, tab, L, taddr, it);
+      else
+        step_epilogue<2>(P, tab, L, taddr, it);
       tc_fence_before();
       mbar_arrive(acc_empty + abuf);
       __syncwarp();
       if (lane == 0) mbar_arrive(tab_empty + abuf);
+      if (it.kind < 2) {  // publish: the tile's outputs are complete
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (threadIdx.x == 64) {
+          __threadfence();
+          st_release_gpu((it.kind == 0 ? P.done0 : P.done1) + it.tile, P.epoch);
+        }
+      }
     }
   }
   __syncthreads();
@@ -480,6 +580,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_conv(const __grid_constant__
     tmem_dealloc(tmem_base, 512);
   }
 }
+
+constexpr int kStepSmem = kASlots * kASlot + kBStages * kBStage + kTableBytes +
+                          kItemSlots * static_cast<int>(sizeof(Item)) + 512;
 
 // ----------------------------------------------------------------- plan
 // Segment layout and tile lists for every step, from the group tables.
@@ -566,9 +669,9 @@ __global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const
         const int32_t c = k == 0 ? child0[node] : child1[node];
         if (!fwd_ok[c]) continue;
         fwd_pos[c] = seg_start[g] + i * kImg;
-        // unary parent: conv3x3 #2 of the parent reads the child's fp32 value
-        // as its residual, so keep it; binary parents use their own z.
-        fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1) | ((arity == 1 ? 1 : 0) << 8);
+        // buffer (bit 0: stage_x / stage_cat) and first plane; no fp32 copy:
+        // a unary parent reads its residual from the hi/lo images
+        fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1);
       }
     }
   }
@@ -576,33 +679,24 @@ __global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const
 
 __global__ void k_rb_memtab(int32_t n_steps, const int32_t* __restrict__ sgb,
                             const int32_t* __restrict__ group_fid, const int32_t* __restrict__ group_begin,
-                            const int32_t* __restrict__ arity_of, const int32_t* __restrict__ seg_start,
-                            const int32_t* __restrict__ member_g, const int32_t* __restrict__ fid,
-                            const int32_t* __restrict__ child0, const int32_t* __restrict__ example,
+                            const int32_t* __restrict__ seg_start, const int32_t* __restrict__ member_g,
                             const int32_t* __restrict__ fwd_pos, const int32_t* __restrict__ fwd_slot,
-                            const float* inputs, float* values, uint8_t* stage_x, uint8_t* stage_cat,
-                            int64_t ps, MemberEntry* __restrict__ memtab) {
+                            float* values, uint8_t* stage_x, uint8_t* stage_lo, uint8_t* stage_cat, int64_t ps,
+                            MemberEntry* __restrict__ memtab) {
   const int32_t s = blockIdx.x;
   if (s >= n_steps) return;
   for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
     if (seg_start[g] < 0) continue;
-    const int32_t arity = arity_of[group_fid[g]];
     for (int32_t m = group_begin[g] + threadIdx.x; m < group_begin[g + 1]; m += blockDim.x) {
       const int32_t node = member_g[m];
-      MemberEntry e;
-      e.slot = values + static_cast<int64_t>(node) * kFmap;
-      if (arity == 2) {
-        e.res = e.slot;
-      } else {
-        const int32_t ch = child0[node];
-        e.res = arity_of[fid[ch]] == 0 ? inputs + static_cast<int64_t>(example[ch]) * kFmap
-                                       : values + static_cast<int64_t>(ch) * kFmap;
-      }
       const int32_t sw = fwd_slot[node];
       const int32_t tgt = fwd_pos[node];
+      MemberEntry e;
+      e.slot = values + static_cast<int64_t>(node) * kFmap;
       e.keep32 = (sw >> 8) & 1;
-      e.fwd = tgt >= 0 ? ((sw & 1) ? stage_cat : stage_x) + (static_cast<int64_t>((sw >> 1) & 31) * ps + kGuard + tgt) * 16
-                       : nullptr;
+      const int64_t off = (static_cast<int64_t>((sw >> 1) & 31) * ps + kGuard + tgt) * 16;
+      e.fwd = tgt >= 0 ? ((sw & 1) ? stage_cat : stage_x) + off : nullptr;
+      e.fwd_lo = tgt >= 0 && !(sw & 1) ? stage_lo + off : nullptr;
       e.pad = 0;
       memtab[m] = e;
     }
@@ -640,8 +734,9 @@ __global__ void k_rb_tiles(int32_t n_steps, const int32_t* __restrict__ sgb,
 // Packs the operand maps that were NOT forwarded by a child's conv3x3 #2
 // epilogue — leaves (the example's input map) and children shared by
 // several parents — into the member's fp16 staging image: unary → stage_x
-// (16 planes), binary → stage_cat planes 16k.. (the channel concat of
-// [x; y] is fused into the write). Only the 196 data positions are written;
+// (16 planes, plus the lo image in stage_lo: the block's residual), binary →
+// stage_cat planes 16k.. (the channel concat of [x; y] is fused into the
+// write). Only the 196 data positions are written;
 // pads and alignment gaps were zeroed once at session creation.
 __global__ void __launch_bounds__(256) k_rb_gather(
     int32_t step, const int32_t* __restrict__ sgb, const int32_t* __restrict__ group_fid,
@@ -650,8 +745,8 @@ __global__ void __launch_bounds__(256) k_rb_gather(
     const int32_t* __restrict__ fid, const int32_t* __restrict__ child0,
     const int32_t* __restrict__ child1, const int32_t* __restrict__ example,
     const int32_t* __restrict__ fwd_ok, const float* __restrict__ inputs,
-    const float* __restrict__ values, uint8_t* __restrict__ stage_x, uint8_t* __restrict__ stage_cat,
-    int64_t ps) {
+    const float* __restrict__ values, uint8_t* __restrict__ stage_x, uint8_t* __restrict__ stage_lo,
+    uint8_t* __restrict__ stage_cat, int64_t ps) {
   const int32_t g_lo = sgb[step], g_hi = sgb[step + 1];
   const int32_t m_lo = group_begin[g_lo], m_hi = group_begin[g_hi];
   for (int32_t m = m_lo + blockIdx.x; m < m_hi; m += gridDim.x) {
@@ -671,14 +766,14 @@ __global__ void __launch_bounds__(256) k_rb_gather(
         const int p = idx / kPx, px = idx - p * kPx;
         const int r = px / 14, c = px - r * 14;
         const float* sp = src + (p * kPx + px) * 8;
-        const float4 lo = *reinterpret_cast<const float4*>(sp);
-        const float4 hi = *reinterpret_cast<const float4*>(sp + 4);
-        uint4 pk;
-        pk.x = pack_f16x2(lo.x, lo.y);
-        pk.y = pack_f16x2(lo.z, lo.w);
-        pk.z = pack_f16x2(hi.x, hi.y);
-        pk.w = pack_f16x2(hi.z, hi.w);
-        *reinterpret_cast<uint4*>(dst + (static_cast<int64_t>(16 * k + p) * ps + base + r * 15 + c) * 16) = pk;
+        const float4 a = *reinterpret_cast<const float4*>(sp);
+        const float4 b = *reinterpret_cast<const float4*>(sp + 4);
+        const float o[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        uint4 hi, lo;
+        split_f16x8(o, hi, lo);
+        const int64_t off = (static_cast<int64_t>(16 * k + p) * ps + base + r * 15 + c) * 16;
+        *reinterpret_cast<uint4*>(dst + off) = hi;
+        if (arity == 1) *reinterpret_cast<uint4*>(stage_lo + off) = lo;  // the block's residual
       }
     }
   }
@@ -721,17 +816,6 @@ __global__ void __launch_bounds__(256) k_roots_to_chw(const int32_t* __restrict_
 
 int32_t g_debug_flag = 0;
 
-template <int KIND>
-int launch_conv(const ConvParams& p, int num_sms, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_rb_conv<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<KIND>());
-    configured = true;
-  }
-  k_rb_conv<KIND><<<num_sms, kThreads, smem_bytes<KIND>(), s>>>(p);
-  return static_cast<int>(cudaGetLastError());
-}
-
 }  // namespace
 
 extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
@@ -760,56 +844,77 @@ extern "C" int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, cons
                              const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
                              const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
                              const int32_t* child1, const int32_t* example, const int32_t* fwd_ok,
-                             const float* inputs, const float* values, void* stage_x, void* stage_cat,
-                             int64_t plane_stride, int32_t blocks, void* stream) {
+                             const float* inputs, const float* values, void* stage_x, void* stage_lo,
+                             void* stage_cat, int64_t plane_stride, int32_t blocks, void* stream) {
   k_rb_gather<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       step, step_group_begin, group_fid, group_begin, seg_start, member_g, arity_of, fid, child0, child1,
-      example, fwd_ok, inputs, values, static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_cat),
-      plane_stride);
+      example, fwd_ok, inputs, values, static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_lo),
+      static_cast<uint8_t*>(stage_cat), plane_stride);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
-                             const int32_t* group_begin, const int32_t* arity_of, const int32_t* seg_start,
-                             const int32_t* member_g, const int32_t* fid, const int32_t* child0,
-                             const int32_t* example, const int32_t* fwd_pos, const int32_t* fwd_slot,
-                             const float* inputs, float* values, void* stage_x, void* stage_cat,
-                             int64_t plane_stride, void* memtab, void* stream) {
+                             const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
+                             const int32_t* fwd_pos, const int32_t* fwd_slot, float* values, void* stage_x,
+                             void* stage_lo, void* stage_cat, int64_t plane_stride, void* memtab,
+                             void* stream) {
   if (n_steps <= 0) return 0;
   k_rb_memtab<<<n_steps, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start, member_g, fid, child0, example,
-      fwd_pos, fwd_slot, inputs, values, static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_cat),
+      n_steps, step_group_begin, group_fid, group_begin, seg_start, member_g, fwd_pos, fwd_slot, values,
+      static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_lo), static_cast<uint8_t*>(stage_cat),
       plane_stride, static_cast<MemberEntry*>(memtab));
   return static_cast<int>(cudaGetLastError());
 }
 
-extern "C" int dbk_rb_conv(int32_t kind, int32_t step, const int32_t* step_tile_begin,
-                           const int32_t* tile_group, const int32_t* tile_q0, const int32_t* group_fid,
-                           const int32_t* group_begin, const int32_t* seg_start, const void* memtab,
-                           const void* stage_in, void* stage_out, int64_t plane_stride,
-                           const void* const* wpack, const float* const* bias, int32_t num_sms,
-                           void* stream) {
-  ConvParams p{step,
-               step_tile_begin,
-               tile_group,
-               tile_q0,
-               group_fid,
-               group_begin,
-               seg_start,
-               static_cast<const MemberEntry*>(memtab),
-               static_cast<const __half*>(stage_in),
-               static_cast<__half*>(stage_out),
-               plane_stride,
-               reinterpret_cast<const __half* const*>(wpack),
-               bias,
-               g_debug_flag};
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  switch (kind) {
-    case 0: return launch_conv<0>(p, num_sms, s);
-    case 1: return launch_conv<1>(p, num_sms, s);
-    case 2: return launch_conv<2>(p, num_sms, s);
+extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile_begin, const int32_t* tile_group,
+                           const int32_t* tile_q0, const int32_t* step_bintile_begin, const int32_t* bin_group,
+                           const int32_t* bin_q0, const int32_t* group_fid, const int32_t* group_begin,
+                           const int32_t* seg_start, const int32_t* group_tile0, const int32_t* group_bintile0,
+                           const void* memtab, void* stage_x, void* stage_lo, void* stage_cat, void* stage_mid,
+                           int64_t plane_stride, const void* const* w0, const void* const* w1,
+                           const void* const* w2, const float* const* b0, const float* const* b1,
+                           const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
+                           int32_t* queue, int32_t num_sms, void* stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_rb_step, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    configured = true;
   }
-  return static_cast<int>(cudaErrorInvalidValue);
+  StepParams p{};
+  p.step = step;
+  p.epoch = epoch;
+  const char* la = std::getenv("DYNBATCH_LOOKAHEAD");
+  p.lookahead = (la ? std::atoi(la) : 8) * num_sms;
+  p.debug = g_debug_flag;
+  p.step_tile_begin = step_tile_begin;
+  p.tile_group = tile_group;
+  p.tile_q0 = tile_q0;
+  p.step_bintile_begin = step_bintile_begin;
+  p.bin_group = bin_group;
+  p.bin_q0 = bin_q0;
+  p.group_fid = group_fid;
+  p.group_begin = group_begin;
+  p.seg_start = seg_start;
+  p.group_tile0 = group_tile0;
+  p.group_bintile0 = group_bintile0;
+  p.memtab = static_cast<const MemberEntry*>(memtab);
+  p.stage_x = static_cast<uint8_t*>(stage_x);
+  p.stage_lo = static_cast<uint8_t*>(stage_lo);
+  p.stage_cat = static_cast<uint8_t*>(stage_cat);
+  p.stage_mid = static_cast<uint8_t*>(stage_mid);
+  p.ps = plane_stride;
+  p.wpack[0] = reinterpret_cast<const uint8_t* const*>(w0);
+  p.wpack[1] = reinterpret_cast<const uint8_t* const*>(w1);
+  p.wpack[2] = reinterpret_cast<const uint8_t* const*>(w2);
+  p.bias[0] = b0;
+  p.bias[1] = b1;
+  p.bias[2] = b2;
+  p.ident = static_cast<const uint8_t*>(ident);
+  p.done0 = done0;
+  p.done1 = done1;
+  p.queue = queue;
+  k_rb_step<<<num_sms, kThreads, kStepSmem, static_cast<cudaStream_t>(stream)>>>(p);
+  return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream) {

@@ -71,6 +71,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ------------------------------------------------- inter-CTA done flags
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Generic-proxy global writes observed (acquired) by this thread become
+// visible to its later async-proxy (TMA) reads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Spins until *flag == want (with the same 4 s watchdog as mbar_wait).
+__device__ __forceinline__ void wait_flag(const int32_t* flag, int32_t want) {
+  if (ld_acquire_gpu(flag) == want) return;
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_gpu(flag) != want) {
+    __nanosleep(64);
+    if (global_ns() - t0 > 4000000000ull) __trap();
+  }
+}
+
 // ------------------------------------------------------ bulk async copy
 // Global → shared, completion counted on `bar` (complete_tx bytes).
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,
@@ -138,6 +165,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Bulk prefetch of [p, p + bytes) into L2 (TMA engine; bytes % 16 == 0).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // 16 consecutive fp32 columns of this thread's TMEM lane (32x32b.x16).

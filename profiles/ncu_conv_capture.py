@@ -1,8 +1,8 @@
 """One cfg3 forward (bench.py's workload, same seeds) for an ncu capture of
 the conv kernels:
 
-  ncu --set full --clock-control none --import-source on -k regex:k_rb_conv \
-      -c 48 -o gpurun_out/conv python profiles/ncu_conv_capture.py
+  ncu --set full --clock-control none --import-source on -k regex:k_rb_step \
+      -c 16 -o gpurun_out/conv python profiles/ncu_conv_capture.py
   python profiles/summarize_ncu.py gpurun_out/conv.ncu-rep --traffic profiles/ncu_traffic.json
 
 Also prints the algorithmic work of the captured forward, per conv kind."""

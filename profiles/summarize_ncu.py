@@ -1,7 +1,7 @@
 """Summarise an ncu --set full report into a small JSON/markdown table.
 
 usage: python profiles/summarize_ncu.py <report.ncu-rep> [--json out.json] [--traffic out.json]
---traffic writes the per-launch DRAM traffic of the conv3x3 launches
+--traffic writes the per-launch DRAM traffic of the fused conv step launches
 (bench.py's roofline.traffic).
 Reads `ncu -i <rep> --page raw --csv` (ncu must be on PATH)."""
 import csv
@@ -50,13 +50,13 @@ if __name__ == "__main__":
     for e in res:
         print(json.dumps(e))
     if "--traffic" in sys.argv:
-        conv = [e for e in res if e["kernel"].startswith("k_rb_conv") and e["kernel"][-2:] in ("1>", "2>")]
-        n = max(len(conv), 1)
-        t = {"conv3x3_launches": len(conv),
-             "conv3x3_bytes_per_launch": sum(e["dram_read_bytes"] + e["dram_write_bytes"] for e in conv) / n,
-             "conv3x3_read_bytes_per_launch": sum(e["dram_read_bytes"] for e in conv) / n,
-             "conv3x3_write_bytes_per_launch": sum(e["dram_write_bytes"] for e in conv) / n,
-             "conv3x3_us_per_launch_cold": sum(e["time_us"] for e in conv) / n,
+        step = [e for e in res if e["kernel"].startswith("k_rb_step")]
+        n = max(len(step), 1)
+        t = {"step_launches": len(step),
+             "step_bytes_per_launch": sum(e["dram_read_bytes"] + e["dram_write_bytes"] for e in step) / n,
+             "step_read_bytes_per_launch": sum(e["dram_read_bytes"] for e in step) / n,
+             "step_write_bytes_per_launch": sum(e["dram_write_bytes"] for e in step) / n,
+             "step_us_per_launch_cold": sum(e["time_us"] for e in step) / n,
              "source": sys.argv[1]}
         with open(sys.argv[sys.argv.index("--traffic") + 1], "w") as f:
             json.dump(t, f, indent=1)
