@@ -394,6 +394,55 @@ def run_moe(args, dist, name, secondary=False):
     return res
 
 
+def run_moe_ep(args, dist, name):
+    """Expert-parallel MoE layer (cfg5: n=1024 top-4, d=h=2048): tokens
+    T/G and experts n/G per rank, NCCL all-to-all of counts and rows for
+    dispatch and combine (paper_1707_02402_b200.moe_ep). Weak scaling:
+    `tokens_per_gpu` per rank, so 8 ranks run the 1M-token configuration."""
+    import torch
+    import paper_1707_02402_b200 as db
+    from paper_1707_02402_b200.moe_ep import MoeEpLayer
+    c = MOE[name]
+    N = max(1, dist.world)
+    db.device_open(dist.local)
+    torch.cuda.set_device(dist.local)
+    T = c["tokens_per_gpu"] * N
+    layer = MoeEpLayer(c["experts"], c["k"], T, c["d"], c["h"], seed=0)
+    clk = ClockSampler(dist.local).start()
+    for _ in range(3):
+        layer.forward()
+    layer.sess.synchronize()
+    dist.barrier()
+    t0 = time.time()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(layer.stream)
+    for _ in range(args.steps):
+        layer.forward()
+    e1.record(layer.stream)
+    e1.synchronize()
+    dist.barrier()
+    clk.mark(t0, time.time())
+    ms_step = dist.max(e0.elapsed_time(e1) / args.steps)
+    clk.stop()
+    peaks, src = measured_peaks()
+    flops = 4.0 * T * c["k"] * c["d"] * c["h"]  # GEMM1 + GEMM2 over all ranks
+    achieved = flops / N / (ms_step / 1e3) / 1e12
+    peak = peaks.get("bf16_tflops_sustained")
+    rows = dist.max(layer.last_recv_rows)
+    return {"metric": "MoE tokens/sec (expert parallel)", "value": T / (ms_step / 1e3), "unit": "tokens/s",
+            "ms_per_step": ms_step, "dtype": "bf16 tensor-core operands, fp32 accumulate",
+            "config": {"workload": f"{name}: n={c['experts']} top-{c['k']} d={c['d']} h={c['h']}, "
+                                   f"{c['tokens_per_gpu']} tokens/GPU, experts {c['experts'] // N}/GPU",
+                       "global_tokens": T, "parallelism": f"ep{N} (NCCL all-to-all dispatch + combine)"},
+            "roofline": {"kernel": "whole EP layer (gate, sort, pack, 2x all-to-all, grouped GEMMs, combine)",
+                         "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "TFLOP/s per GPU", "frac": round(achieved / peak, 4) if peak else None,
+                         "peak_source": src + " bf16 sustained"},
+            "max_rows_received": int(rows), "clocks": clk.summary(),
+            "gpu_launches_per_step": 14,
+            "e2e": None, "e2e_note": "inputs are generated per rank on the device side; no host I/O path"}
+
+
 def _mix_seed(seed, stream):
     M = (1 << 64) - 1
 
@@ -447,7 +496,7 @@ def main():
         return
     dist = Dist(args.gpus)
     if args.workload in MOE:
-        r = run_moe(args, dist, args.workload)
+        r = run_moe_ep(args, dist, args.workload) if args.workload == "cfg5" else run_moe(args, dist, args.workload)
         r.update({"n_gpus": max(1, dist.world), "steps": args.steps, "warmup": 3,
                   "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                   "data": "synthetic (reference generators, seed 0; random-init experts)",

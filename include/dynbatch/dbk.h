@@ -149,6 +149,22 @@ int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_
 int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const double* weights,
                          const int32_t* row_of_item, const void* Y, float* out, void* stream);
 
+/* Expert-parallel MoE (moe_gemm.cu): pack the rank's rows in sorted order
+ * (bf16) with pos_of_item[item] = row; receiver layout from the count matrix
+ * cnt[G][E] (source × local expert); scatter received rows into the tiled
+ * GEMM operand (expert-major, source-rank order within an expert) with
+ * recv_of_row[padded row] = receive row (−1: padding); unpack the GEMM2
+ * rows back into receive order. */
+int dbk_moe_ep_pack(int64_t items, int32_t k, int32_t d, const int32_t* order, const float* x, void* send,
+                    int32_t* pos_of_item, int32_t blocks, void* stream);
+int dbk_moe_ep_layout(int32_t G, int32_t E, const int32_t* cnt, int32_t* pstart, int32_t* tile_expert,
+                      int32_t* tile_rb, int32_t* n_tiles, int32_t* src_row, int32_t* cum, void* stream);
+int dbk_moe_ep_scatter(int32_t G, int32_t E, int32_t d, const int32_t* pstart, const int32_t* tile_expert,
+                       const int32_t* src_row, const int32_t* cum, const void* recv, void* A,
+                       int32_t* recv_of_row, int32_t blocks, void* stream);
+int dbk_moe_ep_unpack(int32_t E, int32_t d, const int32_t* pstart, const int32_t* recv_of_row, const void* Y,
+                      void* ret, int32_t blocks, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

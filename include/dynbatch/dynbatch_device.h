@@ -145,6 +145,35 @@ DYNBATCH_API db_status db_moe_session_time(db_moe_session* s, int32_t iters, int
                                            double* ms, db_kernel_times_t* kt);
 DYNBATCH_API void db_moe_session_free(db_moe_session* s);
 
+/* ---- expert-parallel MoE (one rank of G) ----
+ * Tokens [rank·T/G, (rank+1)·T/G) and experts [rank·n/G, (rank+1)·n/G) of
+ * the db_moe_run fixtures; bf16 tcgen05 grouped GEMMs. One forward:
+ *   dispatch: gate → stable expert sort → the rank's k·T/G rows packed in
+ *             sorted order into send_rows (device bf16 [items][d]);
+ *             expert_counts[n] (host) = rows per global expert, so the rows
+ *             for rank q are the contiguous block of q's experts;
+ *   (caller) all-to-all of the counts and an all-to-allv of the rows;
+ *   experts:  recv_rows = every source's block in rank order, recv_counts
+ *             [G][n/G] (host; source × local expert); ret_rows (device bf16)
+ *             receives the expert outputs in receive order;
+ *   (caller) the reverse all-to-allv (ret_rows → the senders);
+ *   combine:  ret_rows = this rank's rows back in its sorted order → the
+ *             slot-order weighted sum (outputs fp32 [T/G][d]).
+ * Kernels run on db_moe_ep_stream(). */
+typedef struct db_moe_ep_session db_moe_ep_session;
+DYNBATCH_API db_status db_moe_ep_create(const db_moe_opts* opts, int32_t rank, int32_t world,
+                                        db_moe_ep_session** out);
+DYNBATCH_API db_status db_moe_ep_sizes(db_moe_ep_session* s, int64_t* tokens, int64_t* items,
+                                       int32_t* local_experts);
+DYNBATCH_API db_status db_moe_ep_dispatch(db_moe_ep_session* s, void* send_rows, int32_t* expert_counts);
+DYNBATCH_API db_status db_moe_ep_experts(db_moe_ep_session* s, const void* recv_rows, const int32_t* recv_counts,
+                                         void* ret_rows);
+DYNBATCH_API db_status db_moe_ep_combine(db_moe_ep_session* s, const void* ret_rows);
+DYNBATCH_API db_status db_moe_ep_outputs(db_moe_ep_session* s, float* out);
+DYNBATCH_API db_status db_moe_ep_synchronize(db_moe_ep_session* s);
+DYNBATCH_API void* db_moe_ep_stream(db_moe_ep_session* s);
+DYNBATCH_API void db_moe_ep_free(db_moe_ep_session* s);
+
 /* db_moe_run with a precision (batched only). */
 DYNBATCH_API db_status db_moe_run_device(const db_moe_opts* opts, int32_t precision,
                                          db_run** out);

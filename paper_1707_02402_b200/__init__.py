@@ -159,6 +159,15 @@ SIGNATURES = {
     "db_moe_session_routing": (C.c_int32, [VP, VP, VP, VP, VP]),
     "db_moe_session_run": (C.c_int32, [VP, PVP]),
     "db_moe_session_free": (None, [VP]),
+    "db_moe_ep_create": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, C.c_int32, PVP]),
+    "db_moe_ep_sizes": (C.c_int32, [VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
+    "db_moe_ep_dispatch": (C.c_int32, [VP, VP, VP]),
+    "db_moe_ep_experts": (C.c_int32, [VP, VP, VP, VP]),
+    "db_moe_ep_combine": (C.c_int32, [VP, VP]),
+    "db_moe_ep_outputs": (C.c_int32, [VP, VP]),
+    "db_moe_ep_synchronize": (C.c_int32, [VP]),
+    "db_moe_ep_stream": (VP, [VP]),
+    "db_moe_ep_free": (None, [VP]),
     "db_moe_run_device": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, PVP]),
 }
 
@@ -468,6 +477,49 @@ class MoeSession(_Handle):
         h = C.c_void_p()
         check(lib().db_moe_session_run(self.h, C.byref(h)))
         return Run(h)
+
+
+class MoeEpSession(_Handle):
+    """One rank of the expert-parallel MoE layer (db_moe_ep_*): tokens
+    [rank·T/G, (rank+1)·T/G) and experts [rank·n/G, (rank+1)·n/G). Buffers
+    are device pointers (e.g. torch CUDA tensors' data_ptr()); the exchange
+    between the stages is the caller's (paper_1707_02402_b200.moe_ep)."""
+    _free = "db_moe_ep_free"
+
+    def __init__(self, experts, k, batch, data_dim, hidden, seed=0, rank=0, world=1):
+        o = MoeOpts(experts, k, batch, data_dim, hidden, seed)
+        h = C.c_void_p()
+        check(lib().db_moe_ep_create(C.byref(o), rank, world, C.byref(h)))
+        super().__init__(h)
+        self.n, self.k, self.d, self.rank, self.world = experts, k, data_dim, rank, world
+        t, it, e = C.c_int64(), C.c_int64(), C.c_int32()
+        check(lib().db_moe_ep_sizes(self.h, C.byref(t), C.byref(it), C.byref(e)))
+        self.tokens, self.items, self.local_experts = t.value, it.value, e.value
+
+    def dispatch(self, send_ptr: int) -> np.ndarray:
+        """Gate + sort + pack into send_ptr; returns rows per global expert."""
+        counts = np.zeros(self.n, np.int32)
+        check(lib().db_moe_ep_dispatch(self.h, C.c_void_p(send_ptr), _ptr(counts)))
+        return counts
+
+    def experts(self, recv_ptr: int, recv_counts: np.ndarray, ret_ptr: int):
+        cnt = np.ascontiguousarray(recv_counts, np.int32).reshape(self.world, self.local_experts)
+        check(lib().db_moe_ep_experts(self.h, C.c_void_p(recv_ptr), _ptr(cnt), C.c_void_p(ret_ptr)))
+
+    def combine(self, ret_ptr: int):
+        check(lib().db_moe_ep_combine(self.h, C.c_void_p(ret_ptr)))
+
+    def outputs(self) -> np.ndarray:
+        out = np.zeros((self.tokens, self.d), np.float32)
+        check(lib().db_moe_ep_outputs(self.h, _ptr(out)))
+        return out
+
+    def synchronize(self):
+        check(lib().db_moe_ep_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        return lib().db_moe_ep_stream(self.h) or 0
 
 
 def device_count() -> int:

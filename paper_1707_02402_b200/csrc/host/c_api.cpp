@@ -41,6 +41,10 @@ struct db_moe_session {
   std::unique_ptr<dynbatch::dev::MoeSession> s;
 };
 
+struct db_moe_ep_session {
+  std::unique_ptr<dynbatch::dev::MoeEp> s;
+};
+
 namespace {
 
 using dynbatch::Errc;
@@ -576,6 +580,53 @@ db_status db_moe_session_run(db_moe_session* s, db_run** out) {
 }
 
 void db_moe_session_free(db_moe_session* s) { delete s; }
+
+// ------------------------------------------------- expert-parallel MoE rank
+db_status db_moe_ep_create(const db_moe_opts* opts, int32_t rank, int32_t world, db_moe_ep_session** out) {
+  if (!opts || !out) return null_arg();
+  return guarded([&] {
+    auto s = std::make_unique<dynbatch::dev::MoeEp>(to_cfg(opts), opts->seed, rank, world);
+    *out = new db_moe_ep_session{std::move(s)};
+  });
+}
+
+db_status db_moe_ep_sizes(db_moe_ep_session* s, int64_t* tokens, int64_t* items, int32_t* local_experts) {
+  if (!s) return null_arg();
+  if (tokens) *tokens = s->s->tokens();
+  if (items) *items = s->s->items();
+  if (local_experts) *local_experts = s->s->local_experts();
+  return DB_OK;
+}
+
+db_status db_moe_ep_dispatch(db_moe_ep_session* s, void* send_rows, int32_t* expert_counts) {
+  if (!s || !send_rows || !expert_counts) return null_arg();
+  return guarded([&] { s->s->dispatch(send_rows, expert_counts); });
+}
+
+db_status db_moe_ep_experts(db_moe_ep_session* s, const void* recv_rows, const int32_t* recv_counts,
+                            void* ret_rows) {
+  if (!s || !recv_counts) return null_arg();
+  return guarded([&] { s->s->experts(recv_rows, recv_counts, ret_rows); });
+}
+
+db_status db_moe_ep_combine(db_moe_ep_session* s, const void* ret_rows) {
+  if (!s || !ret_rows) return null_arg();
+  return guarded([&] { s->s->combine(ret_rows); });
+}
+
+db_status db_moe_ep_outputs(db_moe_ep_session* s, float* out) {
+  if (!s || !out) return null_arg();
+  return guarded([&] { s->s->download_outputs(out); });
+}
+
+db_status db_moe_ep_synchronize(db_moe_ep_session* s) {
+  if (!s) return null_arg();
+  return guarded([&] { s->s->synchronize(); });
+}
+
+void* db_moe_ep_stream(db_moe_ep_session* s) { return s ? static_cast<void*>(s->s->stream()) : nullptr; }
+
+void db_moe_ep_free(db_moe_ep_session* s) { delete s; }
 
 db_status db_moe_run_device(const db_moe_opts* opts, int32_t precision, db_run** out) {
   if (!opts || !out) return null_arg();

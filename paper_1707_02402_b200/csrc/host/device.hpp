@@ -220,4 +220,36 @@ class MoeSession {
   std::int64_t launches_ = 0;
 };
 
+// Expert-parallel MoE rank: tokens [rank·T/G, (rank+1)·T/G),
+// experts [rank·n/G, (rank+1)·n/G), bf16 tcgen05 grouped GEMMs. The caller
+// exchanges the packed rows between dispatch/experts and experts/combine
+// (NCCL all-to-allv over NVLink through torch.distributed).
+class MoeEp {
+ public:
+  MoeEp(const MoeConfig& cfg, std::uint64_t seed, int rank, int world);
+  ~MoeEp();
+  std::int64_t tokens() const { return T_; }
+  std::int64_t items() const;
+  int local_experts() const;
+  // gate → stable expert sort → rows packed in sorted order into `send`
+  // (device bf16 [items][d]); expert_counts[n] (host) = rows per expert.
+  void dispatch(void* send, std::int32_t* expert_counts);
+  // recv = rows received from every source (rank order, expert-major),
+  // cnt[G][E_local] (host); ret (device bf16) gets the expert outputs in
+  // receive order.
+  void experts(const void* recv, const std::int32_t* cnt, void* ret);
+  // ret_recv = the rank's own rows back, in its sorted order → outputs.
+  void combine(const void* ret_recv);
+  void download_outputs(float* out);
+  void synchronize();
+  cudaStream_t stream() const { return stream_; }
+  Profiler prof_;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+  cudaStream_t stream_ = nullptr;
+  std::int64_t T_ = 0;
+};
+
 }  // namespace dynbatch::dev

@@ -73,8 +73,11 @@ class Rng {
     return lo + static_cast<std::int64_t>(next_u64() % span);
   }
   bool bernoulli(double p) { return uniform() < p; }
+  // Skips n outputs (whole 312-word blocks are regenerated without tempering).
+  void discard(std::uint64_t n);
 
  private:
+  void twist();
   std::uint64_t state_[312];
   int pos_;
 };
@@ -396,6 +399,8 @@ struct GeneratedBatch {
 GeneratedBatch gen_batch(const WorkloadSpec& spec);
 GeneratedBatch gen_batch_range(const WorkloadSpec& spec, std::int64_t first, std::int64_t last);
 TensorBatch random_batch(std::int64_t rows, std::int64_t width, std::uint64_t seed);
+// Rows [first, last) of random_batch(rows, width, seed), bit-identical.
+TensorBatch random_batch_range(std::int64_t first, std::int64_t last, std::int64_t width, std::uint64_t seed);
 
 struct MoeWorkload {
   TensorBatch inputs;

@@ -45,6 +45,44 @@ void tile_weights(const std::vector<double>& w, int K, int N, std::uint16_t* out
 
 }  // namespace
 
+void upload_expert_weights(const MoeConfig& cfg, std::uint64_t expert_seed, int e_first, int n_local,
+                           Buf<std::uint16_t>& w1, Buf<std::uint16_t>& w2, Buf<const void*>& w1tab,
+                           Buf<const void*>& w2tab, cudaStream_t s) {
+  const int d = static_cast<int>(cfg.data_dim), h = static_cast<int>(cfg.hidden);
+  const size_t per = static_cast<size_t>(d) * h;
+  w1.alloc(per * n_local);
+  w2.alloc(per * n_local);
+  // Experts are independent Rng streams → generate on host threads.
+  const double s1 = 1.0 / std::sqrt(static_cast<double>(d)), s2 = 1.0 / std::sqrt(static_cast<double>(h));
+  const int chunk = 16;
+  std::vector<std::uint16_t> h1(per * chunk), h2(per * chunk);
+  for (int e0 = 0; e0 < n_local; e0 += chunk) {
+    const int ne = std::min(chunk, n_local - e0);
+    std::vector<std::thread> pool;
+    for (int j = 0; j < ne; ++j) {
+      pool.emplace_back([&, j] {
+        Rng rng(mix_seed(expert_seed, static_cast<std::uint64_t>(e_first + e0 + j)));
+        std::vector<double> w(per);
+        for (double& v : w) v = rng.uniform(-0.5, 0.5) * s1;  // w1 [d][h]
+        tile_weights(w, d, h, h1.data() + per * j);
+        for (double& v : w) v = rng.uniform(-0.5, 0.5) * s2;  // w2 [h][d]
+        tile_weights(w, h, d, h2.data() + per * j);
+      });
+    }
+    for (auto& t : pool) t.join();
+    check(cudaMemcpy(w1.get() + per * e0, h1.data(), per * ne * 2, cudaMemcpyHostToDevice), "H2D w1");
+    check(cudaMemcpy(w2.get() + per * e0, h2.data(), per * ne * 2, cudaMemcpyHostToDevice), "H2D w2");
+  }
+  std::vector<const void*> t1(static_cast<size_t>(n_local)), t2(static_cast<size_t>(n_local));
+  for (int e = 0; e < n_local; ++e) {
+    t1[static_cast<size_t>(e)] = w1.get() + per * e;
+    t2[static_cast<size_t>(e)] = w2.get() + per * e;
+  }
+  w1tab.upload(t1, s);
+  w2tab.upload(t2, s);
+  check(cudaStreamSynchronize(s), "sync");
+}
+
 struct MoeBf16::Impl {
   std::int64_t T = 0;
   int n = 0, k = 0, d = 0, h = 0, sms = 148;
@@ -79,38 +117,7 @@ MoeBf16::MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed
   I.tile_rb.alloc(static_cast<size_t>(rows / 128 + 1));
   I.n_tiles.alloc(1);
   I.row_of_item.alloc(static_cast<size_t>(T) * I.k);
-  const size_t per = static_cast<size_t>(I.d) * I.h;
-  I.w1.alloc(per * I.n);
-  I.w2.alloc(per * I.n);
-  // Weights: experts are independent Rng streams → generate on host threads.
-  const double s1 = 1.0 / std::sqrt(static_cast<double>(I.d)), s2 = 1.0 / std::sqrt(static_cast<double>(I.h));
-  const int chunk = 16;
-  std::vector<std::uint16_t> h1(per * chunk), h2(per * chunk);
-  for (int e0 = 0; e0 < I.n; e0 += chunk) {
-    const int ne = std::min(chunk, I.n - e0);
-    std::vector<std::thread> pool;
-    for (int j = 0; j < ne; ++j) {
-      pool.emplace_back([&, j] {
-        Rng rng(mix_seed(expert_seed, static_cast<std::uint64_t>(e0 + j)));
-        std::vector<double> w(per);
-        for (double& v : w) v = rng.uniform(-0.5, 0.5) * s1;  // w1 [d][h]
-        tile_weights(w, I.d, I.h, h1.data() + per * j);
-        for (double& v : w) v = rng.uniform(-0.5, 0.5) * s2;  // w2 [h][d]
-        tile_weights(w, I.h, I.d, h2.data() + per * j);
-      });
-    }
-    for (auto& t : pool) t.join();
-    check(cudaMemcpy(I.w1.get() + per * e0, h1.data(), per * ne * 2, cudaMemcpyHostToDevice), "H2D w1");
-    check(cudaMemcpy(I.w2.get() + per * e0, h2.data(), per * ne * 2, cudaMemcpyHostToDevice), "H2D w2");
-  }
-  std::vector<const void*> t1(static_cast<size_t>(I.n)), t2(static_cast<size_t>(I.n));
-  for (int e = 0; e < I.n; ++e) {
-    t1[static_cast<size_t>(e)] = I.w1.get() + per * e;
-    t2[static_cast<size_t>(e)] = I.w2.get() + per * e;
-  }
-  I.w1tab.upload(t1, s);
-  I.w2tab.upload(t2, s);
-  check(cudaStreamSynchronize(s), "sync");
+  upload_expert_weights(cfg, expert_seed, 0, I.n, I.w1, I.w2, I.w1tab, I.w2tab, s);
 }
 
 MoeBf16::~MoeBf16() = default;

@@ -10,6 +10,12 @@
 
 namespace dynbatch::dev {
 
+// ExpertSet experts [e_first, e_first + n_local) (src/moe.cpp:71-88) as bf16
+// pre-tiled GEMM operands, with device tables of per-expert pointers.
+void upload_expert_weights(const MoeConfig& cfg, std::uint64_t expert_seed, int e_first, int n_local,
+                           Buf<std::uint16_t>& w1, Buf<std::uint16_t>& w2, Buf<const void*>& w1tab,
+                           Buf<const void*>& w2tab, cudaStream_t s);
+
 class MoeBf16 {
  public:
   MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed, cudaStream_t s);

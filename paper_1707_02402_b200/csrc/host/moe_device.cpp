@@ -285,6 +285,145 @@ std::int64_t MoeSession::h2d_bytes() const {
 }
 std::int64_t MoeSession::d2h_bytes() const { return T_ * impl_->cfg.data_dim * 4; }
 
+// ----------------------------------------------------------------- MoeEp
+struct MoeEp::Impl {
+  MoeConfig cfg;
+  int rank = 0, world = 1, E = 0, e_first = 0, sms = 148;
+  MoeDev dev;
+  Buf<float> x, out;
+  Buf<std::int32_t> pos_of_item, cnt, pstart, tile_expert, tile_rb, n_tiles, src_row, cum, recv_of_row;
+  Buf<std::uint8_t> A, H;
+  Buf<std::uint16_t> Y;
+  Buf<std::uint16_t> w1, w2;
+  Buf<const void*> w1tab, w2tab;
+  std::int64_t cap_rows = 0;  // padded-row capacity of A / H / Y
+
+  void ensure_capacity(std::int64_t rows) {
+    if (rows <= cap_rows) return;
+    cap_rows = rows + rows / 4;
+    const size_t r = static_cast<size_t>(cap_rows);
+    A.alloc(r * cfg.data_dim * 2);
+    H.alloc(r * cfg.hidden * 2);
+    Y.alloc(r * cfg.data_dim);
+    tile_expert.alloc(r / 128 + 1);
+    tile_rb.alloc(r / 128 + 1);
+    recv_of_row.alloc(r);
+  }
+};
+
+MoeEp::MoeEp(const MoeConfig& cfg, std::uint64_t seed, int rank, int world) : impl_(std::make_unique<Impl>()) {
+  require_device();
+  cfg.check();
+  if (world < 1 || rank < 0 || rank >= world) throw_error(Errc::invalid_argument, "bad rank/world");
+  if (cfg.experts % world != 0 || cfg.batch % world != 0)
+    throw_error(Errc::invalid_argument, "expert parallel needs experts and tokens divisible by the world size");
+  if (cfg.data_dim % 256 != 0 || cfg.hidden % 256 != 0)
+    throw_error(Errc::invalid_argument, "bf16 MoE path needs data_dim and hidden multiples of 256");
+  Impl& I = *impl_;
+  I.cfg = cfg;
+  I.rank = rank;
+  I.world = world;
+  I.E = static_cast<int>(cfg.experts / world);
+  I.e_first = rank * I.E;
+  I.sms = sm_count();
+  T_ = cfg.batch / world;
+  const std::int64_t first = rank * T_, last = first + T_;
+  stream_ = make_stream();
+  MoeDev& D = I.dev;
+  const int n = static_cast<int>(cfg.experts), k = static_cast<int>(cfg.active_per_example);
+  D.alloc(T_, n, k, static_cast<int>(cfg.data_dim), static_cast<int>(cfg.hidden));
+  // the rank's token slice of the db_moe_run fixtures (src/c_api.cpp:270-290)
+  const TensorBatch inputs = random_batch_range(first, last, cfg.data_dim, mix_seed(seed, 0x10ULL));
+  const TensorBatch scores = random_batch_range(first, last, cfg.experts, mix_seed(seed, 0x11ULL));
+  D.scores.upload(scores.data().data(), scores.data().size(), stream_);
+  std::vector<float> xin(inputs.data().begin(), inputs.data().end());
+  I.x.upload(xin, stream_);
+  I.out.alloc(static_cast<size_t>(T_) * cfg.data_dim);
+  I.pos_of_item.alloc(static_cast<size_t>(T_) * k);
+  I.cnt.alloc(static_cast<size_t>(world) * I.E);
+  I.pstart.alloc(static_cast<size_t>(I.E) + 1);
+  I.n_tiles.alloc(1);
+  I.src_row.alloc(static_cast<size_t>(I.E) * world);
+  I.cum.alloc(static_cast<size_t>(I.E) * (world + 1));
+  I.ensure_capacity(T_ * k + static_cast<std::int64_t>(I.E) * 128);
+  upload_expert_weights(cfg, mix_seed(seed, 0xe4be27ULL), I.e_first, I.E, I.w1, I.w2, I.w1tab, I.w2tab, stream_);
+  check(cudaStreamSynchronize(stream_), "upload");
+}
+
+MoeEp::~MoeEp() {
+  impl_.reset();
+  if (stream_) {
+    cudaStreamSynchronize(stream_);
+    cudaStreamDestroy(stream_);
+  }
+}
+
+std::int64_t MoeEp::items() const { return T_ * impl_->cfg.active_per_example; }
+int MoeEp::local_experts() const { return impl_->E; }
+
+void MoeEp::dispatch(void* send, std::int32_t* expert_counts) {
+  Impl& I = *impl_;
+  MoeDev& D = I.dev;
+  prof_.begin(3, stream_);
+  D.gate(stream_);
+  D.sort(stream_);
+  check(dbk_moe_ep_pack(items(), D.k, D.d, D.order.get(), I.x.get(), send, I.pos_of_item.get(), I.sms * 8, stream_),
+        "ep pack");
+  prof_.end(stream_);
+  const auto off = D.offsets.download(static_cast<size_t>(D.n) + 1, stream_);  // synchronises
+  for (int e = 0; e < D.n; ++e) expert_counts[e] = off[static_cast<size_t>(e) + 1] - off[static_cast<size_t>(e)];
+}
+
+void MoeEp::experts(const void* recv, const std::int32_t* cnt, void* ret) {
+  Impl& I = *impl_;
+  const int G = I.world, E = I.E, d = static_cast<int>(I.cfg.data_dim), h = static_cast<int>(I.cfg.hidden);
+  std::int64_t padded = 0;
+  for (int e = 0; e < E; ++e) {
+    std::int64_t tot = 0;
+    for (int r = 0; r < G; ++r) tot += cnt[r * E + e];
+    padded += (tot + 127) / 128 * 128;
+  }
+  I.ensure_capacity(padded);
+  check(cudaMemcpyAsync(I.cnt.get(), cnt, sizeof(std::int32_t) * static_cast<size_t>(G) * E, cudaMemcpyHostToDevice,
+                        stream_), "H2D counts");
+  prof_.begin(4, stream_);
+  check(dbk_moe_ep_layout(G, E, I.cnt.get(), I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(), I.n_tiles.get(),
+                          I.src_row.get(), I.cum.get(), stream_), "ep layout");
+  check(dbk_moe_ep_scatter(G, E, d, I.pstart.get(), I.tile_expert.get(), I.src_row.get(), I.cum.get(), recv,
+                           I.A.get(), I.recv_of_row.get(), I.sms * 8, stream_), "ep scatter");
+  check(dbk_moe_bf16_gemm(0, E, d, h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
+                          I.w1tab.get(), I.H.get(), nullptr, I.sms, stream_), "ep gemm1");
+  check(dbk_moe_bf16_gemm(1, E, h, d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
+                          I.w2tab.get(), nullptr, I.Y.get(), I.sms, stream_), "ep gemm2");
+  check(dbk_moe_ep_unpack(E, d, I.pstart.get(), I.recv_of_row.get(), I.Y.get(), ret, I.sms * 8, stream_),
+        "ep unpack");
+  prof_.end(stream_);
+  if (prof_.on) {
+    std::int64_t rows = 0;
+    for (int i = 0; i < G * E; ++i) rows += cnt[i];
+    prof_.add_work(4, 4.0 * static_cast<double>(rows) * d * h, 0.0);
+  }
+}
+
+void MoeEp::combine(const void* ret_recv) {
+  Impl& I = *impl_;
+  prof_.begin(6, stream_);
+  check(dbk_moe_bf16_combine(T_, I.dev.k, I.dev.d, I.dev.wts.get(), I.pos_of_item.get(), ret_recv, I.out.get(),
+                             stream_), "ep combine");
+  prof_.end(stream_);
+}
+
+void MoeEp::download_outputs(float* out) {
+  check(cudaMemcpyAsync(out, impl_->out.get(), sizeof(float) * static_cast<size_t>(T_) * impl_->cfg.data_dim,
+                        cudaMemcpyDeviceToHost, stream_), "D2H outputs");
+  synchronize();
+}
+
+void MoeEp::synchronize() {
+  check(cudaStreamSynchronize(stream_), "sync");
+  impl_->dev.check_err(stream_);
+}
+
 }  // namespace dev
 
 // ------------------------------------------------------- C++ operator API

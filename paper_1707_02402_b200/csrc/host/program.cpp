@@ -56,15 +56,33 @@ Rng::Rng(std::uint64_t seed) : pos_(312) {
   }
 }
 
-std::uint64_t Rng::next_u64() {
-  if (pos_ == 312) {
-    constexpr std::uint64_t hi = ~0ULL << 31, lo = ~hi;
-    for (int i = 0; i < 312; ++i) {
-      const std::uint64_t bits = (state_[i] & hi) | (state_[(i + 1) % 312] & lo);
-      state_[i] = state_[(i + 156) % 312] ^ (bits >> 1) ^ ((bits & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
-    }
-    pos_ = 0;
+void Rng::twist() {
+  constexpr std::uint64_t hi = ~0ULL << 31, lo = ~hi;
+  for (int i = 0; i < 312; ++i) {
+    const std::uint64_t bits = (state_[i] & hi) | (state_[(i + 1) % 312] & lo);
+    state_[i] = state_[(i + 156) % 312] ^ (bits >> 1) ^ ((bits & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
   }
+  pos_ = 0;
+}
+
+void Rng::discard(std::uint64_t n) {
+  const std::uint64_t left = static_cast<std::uint64_t>(312 - pos_);
+  if (n <= left) {
+    pos_ += static_cast<int>(n);
+    return;
+  }
+  n -= left;
+  pos_ = 312;
+  while (n >= 312) {
+    twist();
+    n -= 312;
+  }
+  twist();
+  pos_ = static_cast<int>(n);
+}
+
+std::uint64_t Rng::next_u64() {
+  if (pos_ == 312) twist();
   std::uint64_t y = state_[pos_++];
   y ^= (y >> 29) & 0x5555555555555555ULL;
   y ^= (y << 17) & 0x71D67FFFEDA60000ULL;

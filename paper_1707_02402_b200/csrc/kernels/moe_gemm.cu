@@ -310,3 +310,155 @@ extern "C" int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const doubl
       T, k, d, weights, row_of_item, static_cast<const __nv_bfloat16*>(Y), out);
   return static_cast<int>(cudaGetLastError());
 }
+
+// ----------------------------------------------------- expert parallel
+// Expert-parallel MoE: tokens are sharded T/G per rank and
+// experts n/G per rank (contiguous). A rank's items, stably sorted by expert
+// in (token, slot) order, are therefore already grouped by destination rank.
+namespace {
+
+// send[i] = bf16(x[order[i] / k]) for the rank's items in sorted order;
+// pos_of_item[item] = i (the item's row in the returned buffer).
+__global__ void k_moe_ep_pack(int64_t items, int32_t k, int32_t d, const int32_t* __restrict__ order,
+                              const float* __restrict__ x, __nv_bfloat16* __restrict__ send,
+                              int32_t* __restrict__ pos_of_item) {
+  for (int64_t i = blockIdx.x; i < items; i += gridDim.x) {
+    const int32_t item = order[i];
+    if (threadIdx.x == 0) pos_of_item[item] = static_cast<int32_t>(i);
+    const float* src = x + static_cast<int64_t>(item / k) * d;
+    __nv_bfloat16* dst = send + i * d;
+    for (int32_t j = threadIdx.x * 8; j < d; j += blockDim.x * 8) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(src + j));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(src + j + 4));
+      uint4 pk;
+      pk.x = pack_bf16x2(a.x, a.y);
+      pk.y = pack_bf16x2(a.z, a.w);
+      pk.z = pack_bf16x2(b.x, b.y);
+      pk.w = pack_bf16x2(b.z, b.w);
+      *reinterpret_cast<uint4*>(dst + j) = pk;
+    }
+  }
+}
+
+// Receiver layout from the count matrix cnt[G][E] (rows source r sent for
+// local expert e; the receive buffer holds source blocks in rank order, each
+// expert-major): per-expert totals → padded starts and the tile list (as
+// k_moe_layout), plus, per (expert, source), the receive-buffer row of its
+// first row (src_row) and its offset within the expert (cum). Single thread.
+__global__ void k_moe_ep_layout(int32_t G, int32_t E, const int32_t* __restrict__ cnt,
+                                int32_t* __restrict__ pstart, int32_t* __restrict__ tile_expert,
+                                int32_t* __restrict__ tile_rb, int32_t* __restrict__ n_tiles,
+                                int32_t* __restrict__ src_row, int32_t* __restrict__ cum) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int32_t base = 0;  // receive-buffer row where source r's block starts
+  for (int32_t r = 0; r < G; ++r) {
+    int32_t off = base;
+    for (int32_t e = 0; e < E; ++e) {
+      src_row[e * G + r] = off;
+      off += cnt[r * E + e];
+    }
+    base = off;
+  }
+  int32_t rows_acc = 0, t = 0;
+  for (int32_t e = 0; e < E; ++e) {
+    pstart[e] = rows_acc;
+    int32_t tot = 0;
+    for (int32_t r = 0; r < G; ++r) {
+      cum[e * (G + 1) + r] = tot;
+      tot += cnt[r * E + e];
+    }
+    cum[e * (G + 1) + G] = tot;
+    const int32_t nb = (tot + kBM - 1) / kBM;
+    for (int32_t b = 0; b < nb; ++b) {
+      tile_expert[t] = e;
+      tile_rb[t] = rows_acc / kBM + b;
+      ++t;
+    }
+    rows_acc += nb * kBM;
+  }
+  pstart[E] = rows_acc;
+  *n_tiles = t;
+}
+
+// Received rows → tiled A operand (padding rows zero), expert e's rows in
+// source-rank order = the reference's (token, slot) order for that expert.
+// recv_of_row[padded row] = receive-buffer row (−1 for padding).
+__global__ void k_moe_ep_scatter(int32_t G, int32_t d, const int32_t* __restrict__ pstart,
+                                 const int32_t* __restrict__ tile_expert, const int32_t* __restrict__ src_row,
+                                 const int32_t* __restrict__ cum, int32_t E,
+                                 const __nv_bfloat16* __restrict__ recv, uint8_t* __restrict__ A,
+                                 int32_t* __restrict__ recv_of_row) {
+  const int32_t total_rows = pstart[E];
+  const int32_t kchunks = d / kBK;
+  for (int32_t rb = blockIdx.x; rb * kBM < total_rows; rb += gridDim.x) {
+    const int32_t rr = threadIdx.x;
+    const int32_t row = rb * kBM + rr;
+    const int32_t e = tile_expert[rb];
+    const int32_t local = row - pstart[e];
+    const int32_t* ce = cum + e * (G + 1);
+    const bool valid = local < ce[G];
+    int32_t src = -1;
+    if (valid) {
+      int32_t r = 0;
+      while (local >= ce[r + 1]) ++r;
+      src = src_row[e * G + r] + (local - ce[r]);
+    }
+    recv_of_row[row] = src;
+    const uint4* s4 = reinterpret_cast<const uint4*>(recv + static_cast<int64_t>(valid ? src : 0) * d);
+    uint8_t* dst = A + static_cast<int64_t>(rb) * kchunks * kABytes + rr * 16;
+#pragma unroll 4
+    for (int32_t gi = 0; gi < d / 8; ++gi) {
+      const uint4 pk = valid ? __ldg(s4 + gi) : make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(dst + (gi >> 3) * kABytes + (gi & 7) * kBM * 16) = pk;
+    }
+  }
+}
+
+// Expert outputs back into receive order: ret[recv_of_row[row]] = Y[row].
+__global__ void k_moe_ep_unpack(int32_t E, int32_t d, const int32_t* __restrict__ pstart,
+                                const int32_t* __restrict__ recv_of_row, const __nv_bfloat16* __restrict__ Y,
+                                __nv_bfloat16* __restrict__ ret) {
+  const int32_t total_rows = pstart[E];
+  for (int32_t row = blockIdx.x; row < total_rows; row += gridDim.x) {
+    const int32_t dst = recv_of_row[row];
+    if (dst < 0) continue;
+    const uint4* s4 = reinterpret_cast<const uint4*>(Y + static_cast<int64_t>(row) * d);
+    uint4* d4 = reinterpret_cast<uint4*>(ret + static_cast<int64_t>(dst) * d);
+    for (int32_t j = threadIdx.x; j < d / 8; j += blockDim.x) d4[j] = __ldg(s4 + j);
+  }
+}
+
+}  // namespace
+
+extern "C" int dbk_moe_ep_pack(int64_t items, int32_t k, int32_t d, const int32_t* order, const float* x,
+                               void* send, int32_t* pos_of_item, int32_t blocks, void* stream) {
+  if (items <= 0) return 0;
+  k_moe_ep_pack<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      items, k, d, order, x, static_cast<__nv_bfloat16*>(send), pos_of_item);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_moe_ep_layout(int32_t G, int32_t E, const int32_t* cnt, int32_t* pstart, int32_t* tile_expert,
+                                 int32_t* tile_rb, int32_t* n_tiles, int32_t* src_row, int32_t* cum,
+                                 void* stream) {
+  k_moe_ep_layout<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(G, E, cnt, pstart, tile_expert, tile_rb,
+                                                                    n_tiles, src_row, cum);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_moe_ep_scatter(int32_t G, int32_t E, int32_t d, const int32_t* pstart,
+                                  const int32_t* tile_expert, const int32_t* src_row, const int32_t* cum,
+                                  const void* recv, void* A, int32_t* recv_of_row, int32_t blocks,
+                                  void* stream) {
+  k_moe_ep_scatter<<<blocks, kBM, 0, static_cast<cudaStream_t>(stream)>>>(
+      G, d, pstart, tile_expert, src_row, cum, E, static_cast<const __nv_bfloat16*>(recv),
+      static_cast<uint8_t*>(A), recv_of_row);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_moe_ep_unpack(int32_t E, int32_t d, const int32_t* pstart, const int32_t* recv_of_row,
+                                 const void* Y, void* ret, int32_t blocks, void* stream) {
+  k_moe_ep_unpack<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      E, d, pstart, recv_of_row, static_cast<const __nv_bfloat16*>(Y), static_cast<__nv_bfloat16*>(ret));
+  return static_cast<int>(cudaGetLastError());
+}

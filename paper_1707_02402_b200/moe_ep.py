@@ -1,0 +1,112 @@
+"""Expert-parallel MoE over torch.distributed.
+
+Tokens are sharded T/G per rank, and experts n/G per rank, both contiguous.
+A rank's assignments, stably sorted by expert in (token, slot) order (the
+reference group_by_function, src/schedule.cpp:166-169 via
+src/moe.cpp:214-224), are then already grouped by destination rank. One
+forward is:
+
+  dispatch  gate → sort → rows packed in sorted order       (device kernels)
+  exchange  all-to-all of per-expert counts, all-to-allv of the rows
+  experts   scatter by (local expert, source rank) → grouped GEMMs → unpack
+  exchange  reverse all-to-allv (outputs back to their senders)
+  combine   slot-order weighted sum                          (device kernels)
+
+Receivers concatenate by source rank. With contiguous token shards this
+reproduces, for every expert, the reference's (token, slot) member order.
+The exchange is plain torch.distributed (NCCL over NVLink on the GPU box,
+gloo in the CPU tests). `EpExchange` is the part shared by both.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def split_rows(expert_counts: np.ndarray, world: int) -> np.ndarray:
+    """Rows this rank sends to each rank: the contiguous expert blocks."""
+    return np.asarray(expert_counts, np.int64).reshape(world, -1).sum(axis=1)
+
+
+class EpExchange:
+    """The two exchange steps of one expert-parallel forward."""
+
+    def __init__(self, world: int, n_experts: int, device="cpu", group=None):
+        import torch
+        self.torch = torch
+        self.world, self.n = world, n_experts
+        self.E = n_experts // world
+        self.device = device
+        self.group = group
+
+    def counts(self, expert_counts: np.ndarray) -> np.ndarray:
+        """recv[src][e] = rows source `src` sends for local expert e."""
+        if self.world == 1:
+            return np.asarray(expert_counts, np.int32).reshape(1, self.E)
+        import torch.distributed as dist
+        t = self.torch
+        send = t.as_tensor(np.asarray(expert_counts, np.int32), device=self.device)
+        recv = t.empty_like(send)
+        dist.all_to_all_single(recv, send, group=self.group)  # equal splits of n/G counts
+        return recv.cpu().numpy().reshape(self.world, self.E)
+
+    def rows(self, out, inp, out_rows, in_rows):
+        """all-to-allv of row blocks: inp (in_rows[q] rows to rank q) → out."""
+        if self.world == 1:
+            rows = int(np.sum(in_rows))
+            out[:rows].copy_(inp[:rows])
+            return out
+        import torch.distributed as dist
+        dist.all_to_all_single(out[: int(np.sum(out_rows))], inp[: int(np.sum(in_rows))],
+                               [int(x) for x in out_rows], [int(x) for x in in_rows], group=self.group)
+        return out
+
+
+class MoeEpLayer:
+    """One rank of the expert-parallel MoE layer on the B200 (bf16 tcgen05
+    grouped GEMMs, db_moe_ep_*). Collectives are issued on the session's
+    stream, so the kernels and the exchange stay ordered without host syncs
+    beyond the two count reads."""
+
+    def __init__(self, experts, k, batch, data_dim, hidden, seed=0, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import MoeEpSession
+        self.torch = torch
+        init = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if init else 0
+        self.world = dist.get_world_size(group) if init else 1
+        self.sess = MoeEpSession(experts, k, batch, data_dim, hidden, seed, self.rank, self.world)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.stream = torch.cuda.ExternalStream(self.sess.stream, device=dev)
+        self.ex = EpExchange(self.world, experts, device=dev, group=group)
+        self.d, self.dev = data_dim, dev
+        self.send = torch.empty((self.sess.items, data_dim), dtype=torch.bfloat16, device=dev)
+        self.back = torch.empty_like(self.send)
+        self.recv = self.ret = None
+        self.last_recv_rows = 0
+
+    def _ensure(self, rows: int):
+        if self.recv is None or self.recv.shape[0] < rows:
+            cap = max(rows + rows // 4, 1)
+            self.recv = self.torch.empty((cap, self.d), dtype=self.torch.bfloat16, device=self.dev)
+            self.ret = self.torch.empty_like(self.recv)
+
+    def forward(self):
+        t = self.torch
+        counts = self.sess.dispatch(self.send.data_ptr())
+        send_rows = split_rows(counts, self.world)
+        with t.cuda.stream(self.stream):
+            cnt = self.ex.counts(counts)
+            recv_rows = cnt.sum(axis=1)
+            rows = int(recv_rows.sum())
+            self._ensure(rows)
+            self.ex.rows(self.recv, self.send, recv_rows, send_rows)
+        self.sess.experts(self.recv.data_ptr(), cnt, self.ret.data_ptr())
+        with t.cuda.stream(self.stream):
+            self.ex.rows(self.back, self.ret, send_rows, recv_rows)
+        self.sess.combine(self.back.data_ptr())
+        self.last_recv_rows = rows
+
+    def outputs(self) -> np.ndarray:
+        return self.sess.outputs()

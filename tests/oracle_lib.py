@@ -365,6 +365,14 @@ def topk(scores: np.ndarray, k: int, use_ref=False):
     return ids, w
 
 
+def expert_weights(d, h, expert_seed, eid):
+    """ExpertSet expert `eid` (src/moe.cpp:71-88): w1 [d][h], w2 [h][d]."""
+    w1 = np.zeros(d * h, np.float64)
+    w2 = np.zeros(h * d, np.float64)
+    oracle().orc_expert_weights(d, h, expert_seed, eid, _ptr(w1, P_F64), _ptr(w2, P_F64))
+    return w1.reshape(d, h), w2.reshape(h, d)
+
+
 def moe_forward(inputs, ids, weights, n, h, expert_seed, use_ref=False, subset=None):
     T, d = inputs.shape
     k = ids.shape[1]

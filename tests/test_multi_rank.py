@@ -88,3 +88,86 @@ def test_moe_token_shards_cover_batch():
         ids_full, _ = O.topk(sc, 2)
         assert np.array_equal(ids_r, ids_full[r * T:(r + 1) * T])
         assert xr.shape == (T, d)
+
+
+# ----------------------------------------------- expert-parallel MoE (§8e)
+EP = dict(n=8, k=2, T=64, d=16, h=24, seed=3)
+
+
+def _ep_worker(rank, port, out_q):
+    """One rank of the expert-parallel protocol (moe_ep.EpExchange over
+    gloo) with numpy stand-ins for the device stages: gate + stable sort +
+    pack, count / row all-to-alls, local experts in receive order, reverse
+    all-to-allv, slot-order combine."""
+    import torch
+    from paper_1707_02402_b200.moe_ep import EpExchange, split_rows
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    n, k, T, d, h, seed = (EP[key] for key in ("n", "k", "T", "d", "h", "seed"))
+    expert_seed = O.mix_seed(seed, 0xe4be27)
+    x_all, s_all = O.moe_inputs(T, n, d, seed)
+    Tl, E = T // WORLD, n // WORLD
+    sl = slice(rank * Tl, (rank + 1) * Tl)
+    ids, w = O.topk(s_all[sl], k)
+    items = np.argsort(ids.reshape(-1), kind="stable")  # per-expert (token, slot) order
+    counts = np.bincount(ids.reshape(-1), minlength=n).astype(np.int32)
+    send = torch.tensor(x_all[sl][items // k])
+    gid = torch.tensor((items + rank * Tl * k).astype(np.float64)[:, None])  # global item ids
+    ex = EpExchange(WORLD, n)
+    cnt = ex.counts(counts)
+    recv_rows, send_rows = cnt.sum(axis=1), split_rows(counts, WORLD)
+    recv = torch.empty((int(recv_rows.sum()), d), dtype=torch.float64)
+    ex.rows(recv, send, recv_rows, send_rows)
+    rgid = torch.empty((int(recv_rows.sum()), 1), dtype=torch.float64)
+    ex.rows(rgid, gid, recv_rows, send_rows)
+    # local experts over the receive buffer: source blocks in rank order,
+    # expert-major inside each block
+    ret = torch.empty_like(recv)
+    members = {e: [] for e in range(E)}
+    pos = 0
+    for src in range(WORLD):
+        for e in range(E):
+            c = int(cnt[src, e])
+            w1, w2 = O.expert_weights(d, h, expert_seed, rank * E + e)
+            rows = recv[pos:pos + c].numpy()
+            ret[pos:pos + c] = torch.tensor(np.maximum(rows @ w1, 0.0) @ w2)
+            members[e] += rgid[pos:pos + c, 0].numpy().astype(np.int64).tolist()
+            pos += c
+    back = torch.empty_like(send)
+    ex.rows(back, ret, send_rows, recv_rows)
+    pos_of_item = np.empty(Tl * k, np.int64)
+    pos_of_item[items] = np.arange(Tl * k)
+    y = back.numpy()[pos_of_item].reshape(Tl, k, d)
+    out = np.zeros((Tl, d))
+    for s in range(k):  # slot order, as the reference combine
+        out += w[:, s:s + 1] * y[:, s]
+    out_q.put((rank, out, members, cnt))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_moe_expert_parallel_protocol_matches_single_process():
+    n, k, T, d, h, seed = (EP[key] for key in ("n", "k", "T", "d", "h", "seed"))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ep_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = dict((r, (o, m, c)) for r, o, m, c in (q.get(timeout=120) for _ in range(WORLD)))
+    for p in procs:
+        p.join(timeout=60)
+    x_all, s_all = O.moe_inputs(T, n, d, seed)
+    ids, w = O.topk(s_all, k)
+    ref, _, _ = O.moe_forward(x_all, ids, w, n, h, O.mix_seed(seed, 0xe4be27))
+    Tl, E = T // WORLD, n // WORLD
+    flat = ids.reshape(-1)
+    for r in range(WORLD):
+        out, members, cnt = res[r]
+        # outputs: the rank's token slice of the single-process layer
+        np.testing.assert_allclose(out, ref[r * Tl:(r + 1) * Tl], rtol=1e-10, atol=1e-12)
+        # member order of every local expert = the reference's (token, slot) order
+        for e in range(E):
+            want = np.nonzero(flat == r * E + e)[0].tolist()
+            assert members[e] == want, (r, e)
+        assert cnt.sum() == sum(len(v) for v in members.values())
