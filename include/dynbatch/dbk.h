@@ -80,17 +80,14 @@ int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t*
                 const int32_t* member_g, const int32_t* child0, const int32_t* child1,
                 const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t tile_m,
                 void* stream);
-/* Gather of the operands of step `step` that no child epilogue forwarded
- * (leaves, shared children) into the fp16 staging planes: unary members get
- * the hi image in stage_x and the lo image (x − hi, the block's residual) in
- * stage_lo; binary members get hi in stage_cat planes 16k.. (the channel
- * concat is fused into the write); plane_stride in positions. */
-int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_fid,
-                  const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
-                  const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
-                  const int32_t* child1, const int32_t* example, const int32_t* fwd_ok,
-                  const float* inputs, const float* values, void* stage_x, void* stage_lo, void* stage_cat,
-                  int64_t plane_stride, int32_t blocks, void* stream);
+/* Gather of operands no child epilogue forwards, from the task lists that
+ * dbk_rb_memtab emits (32-byte tasks, list 0 = leaves of every step, list 1
+ * = children shared by several parents, processed for `step` only): fp32
+ * plane maps → staged fp16 images (hi; plus the lo image, the block's
+ * residual, in stage_lo for unary members); plane_stride in rows. */
+int dbk_rb_gather(const void* tasks, const int32_t* n_tasks, int32_t list, int32_t step, int64_t task_cap,
+                  void* stage_x, void* stage_lo, void* stage_cat, int64_t plane_stride, int32_t blocks,
+                  void* stream);
 /* One persistent launch per step (one CTA per SM) over a device work queue
  * of the step's tiles: conv1x1 over [x; y] → z hi/lo (stage_x / stage_lo),
  * conv3x3 #1 → mid (stage_mid), conv3x3 #2 + residual (accumulated on the
@@ -108,12 +105,15 @@ int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile_begin, con
                 const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
                 int32_t* done0, int32_t* done1, int32_t* queue, int32_t num_sms, void* stream);
 /* Per-member epilogue table (32 bytes per member, schedule order: own fp32
- * slot, hi / lo forwarding targets, keep-fp32 flag), built after dbk_rb_plan
- * from its forwarding tables. */
+ * slot, forwarding target row / buffer, keep-fp32 flag) and the gather task
+ * lists (n_tasks[2] counters, reset here; capacity task_cap per list), built
+ * after dbk_rb_plan from its forwarding tables. */
 int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
                   const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
-                  const int32_t* fwd_pos, const int32_t* fwd_slot, float* values, void* stage_x,
-                  void* stage_lo, void* stage_cat, int64_t plane_stride, void* memtab, void* stream);
+                  const int32_t* fwd_pos, const int32_t* fwd_slot, const int32_t* arity_of, const int32_t* fid,
+                  const int32_t* child0, const int32_t* child1, const int32_t* example, const int32_t* fwd_ok,
+                  const float* inputs, float* values, void* memtab, void* tasks, int32_t* n_tasks,
+                  int64_t task_cap, void* stream);
 int dbk_rb_debug(unsigned long long* out24, int32_t reset, int32_t enable);
 int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream);
 int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int32_t* fid,

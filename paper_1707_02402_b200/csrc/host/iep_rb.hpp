@@ -25,9 +25,13 @@ struct IepSession::RB {
   Buf<std::int32_t> seg_start, group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
       step_positions, tile_group, tile_q0, bin_group, bin_q0, fwd_ok, fwd_pos, fwd_slot;
   Buf<std::uint64_t> memtab;  // per-member epilogue metadata, 32 bytes each (rb_conv.cu MemberEntry)
+  Buf<std::uint64_t> tasks;   // gather tasks, 32 bytes each: 2 lists × task_cap
+  Buf<std::int32_t> n_tasks;
+  std::int64_t task_cap = 0;
   Buf<std::int32_t> done0, done1, queue;  // fused step kernel: tile done flags, claim counters
   std::int32_t epoch = 0;                 // forward counter stamped into the done flags
   std::int64_t n_expensive = 0;
+  std::int64_t n_shared = 0;  // expensive children with several parents (gathered per step)
   int tile_m = kTileM;  // positions per scheduled tile
 };
 

@@ -48,11 +48,12 @@ std::uint16_t to_f16(double v) {
 }
 
 // Weights are streamed as 16 KB blocks, one per (64-channel K chunk, tap) in
-// that order (rb_conv.cu); element (n = co, k = ci mod 64) of a block sits at
-// ((k/8)·128 + n)·8 + k%8 (K-major, no swizzle).
+// that order (rb_conv.cu). A block is the A operand (M = 128 output channels)
+// in the K-major 128-byte-swizzle layout: output channel n is the 128-byte
+// row n, input channel k (mod 64) sits in the 16-byte slot (k/8) ^ (n & 7)
+// at element k % 8.
 constexpr int kKChunk = 64;
 
-// The block is the A operand (M = 128 output channels) of the conv MMAs.
 std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int cin, int taps) {
   std::vector<std::uint16_t> out(static_cast<size_t>(taps) * cin * C);
   const size_t block = static_cast<size_t>(kKChunk) * C;
@@ -61,7 +62,7 @@ std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int 
       const int chunk = ci / kKChunk, k = ci % kKChunk;
       const size_t base = static_cast<size_t>(chunk * taps + tap) * block;
       for (int co = 0; co < C; ++co) {
-        const size_t off = (static_cast<size_t>(k / 8) * C + co) * 8 + k % 8;
+        const size_t off = static_cast<size_t>(co) * kKChunk + static_cast<size_t>(((k / 8) ^ (co & 7)) * 8 + k % 8);
         out[base + off] = to_f16(w[(static_cast<size_t>(tap) * cin + ci) * C + co]);
       }
     }
@@ -99,13 +100,18 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   {
     std::vector<std::int32_t> parents(static_cast<size_t>(N), 0), ok(static_cast<size_t>(N), 0);
     for (std::int32_t ch : c.child_list) ++parents[static_cast<size_t>(ch)];
-    for (std::int64_t g = 0; g < c.N; ++g)
-      ok[static_cast<size_t>(g)] = c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0 &&
-                                   parents[static_cast<size_t>(g)] == 1;
+    for (std::int64_t g = 0; g < c.N; ++g) {
+      const bool exp = c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0;
+      ok[static_cast<size_t>(g)] = exp && parents[static_cast<size_t>(g)] == 1;
+      if (exp && parents[static_cast<size_t>(g)] > 1) R.n_shared += parents[static_cast<size_t>(g)];
+    }
     R.fwd_ok.upload(ok, stream_);
     R.fwd_pos.alloc(N);
     R.fwd_slot.alloc(N);
     R.memtab.alloc(N * 4);
+    R.task_cap = static_cast<std::int64_t>(c.child_list.size()) + 1;  // ≤ one task per operand
+    R.tasks.alloc(static_cast<size_t>(R.task_cap) * 2 * 4);
+    R.n_tasks.alloc(2);
   }
   const size_t ps = static_cast<size_t>(R.plane_stride);
   R.stage_x.alloc(ps * 16 * 8);
@@ -196,22 +202,31 @@ void IepSession::forward_resblock() {
                     B.child1.get(), R.fwd_ok.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.tile_m, stream_),
         "dbk_rb_plan");
   check(dbk_rb_memtab(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), R.seg_start.get(),
-                      B.member_g.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.values.get(), R.stage_x.get(),
-                      R.stage_lo.get(), R.stage_cat.get(), R.plane_stride, R.memtab.get(), stream_),
+                      B.member_g.get(), R.fwd_pos.get(), R.fwd_slot.get(), B.arity_of.get(), B.fid.get(),
+                      B.child0.get(), B.child1.get(), B.example.get(), R.fwd_ok.get(), R.inputs.get(),
+                      R.values.get(), R.memtab.get(), R.tasks.get(), R.n_tasks.get(), R.task_cap, stream_),
         "dbk_rb_memtab");
   prof_.end(stream_);
   launches_ += 5;
-  const int gather_blocks = static_cast<int>(std::min<std::int64_t>(std::max<std::int64_t>(R.n_expensive, 1), sms * 8));
+  const int gather_blocks = sms * 16;  // grid-stride over the step's (member, operand, chunk, pixel) items
   check(cudaMemsetAsync(R.queue.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_), "queue reset");
   ++R.epoch;
+  // leaf operands of every step in one launch (they only read the inputs)
+  prof_.begin(2, stream_);
+  check(dbk_rb_gather(R.tasks.get(), R.n_tasks.get(), 0, 0, R.task_cap, R.stage_x.get(), R.stage_lo.get(),
+                      R.stage_cat.get(), R.plane_stride, gather_blocks, stream_),
+        "dbk_rb_gather leaves");
+  prof_.end(stream_);
+  ++launches_;
   for (int s = 0; s < S; ++s) {
-    prof_.begin(2, stream_);
-    check(dbk_rb_gather(s, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), R.seg_start.get(),
-                        B.member_g.get(), B.arity_of.get(), B.fid.get(), B.child0.get(), B.child1.get(),
-                        B.example.get(), R.fwd_ok.get(), R.inputs.get(), R.values.get(), R.stage_x.get(),
-                        R.stage_lo.get(), R.stage_cat.get(), R.plane_stride, gather_blocks, stream_),
-          "dbk_rb_gather");
-    prof_.end(stream_);
+    if (R.n_shared > 0) {  // children shared by several parents: values of earlier steps
+      prof_.begin(2, stream_);
+      check(dbk_rb_gather(R.tasks.get(), R.n_tasks.get(), 1, s, R.task_cap, R.stage_x.get(), R.stage_lo.get(),
+                          R.stage_cat.get(), R.plane_stride, gather_blocks, stream_),
+            "dbk_rb_gather shared");
+      prof_.end(stream_);
+      ++launches_;
+    }
     // conv1x1 + conv3x3 #1 + conv3x3 #2 (+ residual) of the step, one launch
     prof_.begin(4, stream_);
     check(dbk_rb_step(s, R.epoch, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(),
@@ -222,7 +237,7 @@ void IepSession::forward_resblock() {
                       R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.queue.get(), sms, stream_),
           "conv step");
     prof_.end(stream_);
-    launches_ += 2;
+    ++launches_;
   }
 }
 

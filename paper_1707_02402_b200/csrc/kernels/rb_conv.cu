@@ -12,19 +12,24 @@
 //   * fp32 "plane maps" [16 planes][196 px][8 ch] (plane j = channels
 //     8j..8j+7), 100,352 B per map: the inputs, and the values of roots and
 //     of children shared by several parents (the only values read later);
-//   * per-step staging: fp16 planes over a packed position axis. Each image
+//   * per-step staging: fp16 rows over a packed position axis. Each image
 //     occupies a 15×15 grid (225 positions; row 14 and column 14 are zero
 //     pads shared with the next image / row), so a 3×3 tap (dh, dw) is the
 //     row shift dh·15 + dw of the same array. Images of one call group are
 //     contiguous; each group's segment starts on a TILE_M boundary so a CTA
-//     tile never mixes weights. Plane j of position q lives at
-//     ((j·PS) + GUARD + q) · 16 bytes. A block input x is staged twice:
-//     hi = fp16(x) in stage_x (the conv3x3 #1 operand) and lo = fp16(x − hi)
-//     in stage_lo; hi + lo carries x to ≈2^-22 relative (fp32-equivalent);
-//   * tensor-core operands use the K-major SWIZZLE_NONE canonical layout
-//     (tc_common.cuh): the shared-memory activation window
-//     [plane][position][8] is a valid operand starting at ANY position, so
-//     all nine taps read the same window at different row offsets — the
+//     tile never mixes weights. A 64-channel chunk c of staging row
+//     r = GUARD + q is one 128-byte row at (c·PS + r)·128, its 8 planes
+//     (8 channels, 16 B each) XOR-swizzled: plane j at ((j ^ (r & 7))·16) —
+//     the 128-byte-swizzle K-major canonical layout keyed to the row, so a
+//     window of consecutive rows is ONE bulk copy that lands correctly
+//     swizzled in shared memory (window starts are 8-row aligned). A block
+//     input x is staged twice: hi = fp16(x) in stage_x (the conv3x3 #1
+//     operand) and lo = fp16(x − hi) in stage_lo; hi + lo carries x to
+//     ≈2^-22 relative (fp32-equivalent);
+//   * tensor-core operands use SWIZZLE_128B K-major descriptors with base
+//     offset 0: the swizzle is keyed to absolute shared-memory addresses, so
+//     a descriptor may start at ANY row of the window (tools/sw128_test.cu)
+//     and all nine taps read the same window at different row offsets — the
 //     im2col never materialises.
 //
 // The residual is added on the tensor cores: conv3x3 #2 accumulates
@@ -71,7 +76,7 @@ constexpr int kTileM = 256;                // positions per CTA tile (MMA N)
 constexpr int kHalo = 16;                  // 3×3 window halo (15 + 1 positions)
 constexpr int kWin = kTileM + 2 * kHalo;   // window rows (row stride of every A slot)
 constexpr int kChunkPlanes = 8;            // K chunk = 64 input channels = 8 planes
-constexpr int kASlot = kChunkPlanes * kWin * 16;  // 36 KB activation window slot
+constexpr int kASlot = kWin * 128;         // 36 KB activation window slot (rows of 128 B)
 constexpr int kASlots = 4;                 // window slots (short hi/lo and 1×1 chunks need depth)
 constexpr int kBStage = 128 * 64 * 2;      // 16 KB: 128 out channels × K=64 fp16 weight block
 constexpr int kBStages = 4;
@@ -86,18 +91,28 @@ constexpr int kChunks = 128 / kChunk;      // chunks per warp and tile
 // Per-member epilogue metadata (schedule order), built once per forward by
 // k_rb_memtab from the forwarding tables.
 struct MemberEntry {
-  float* slot;      // the node's fp32 plane map (written only when keep32)
-  uint8_t* fwd;     // parent's fp16 operand image of this node (plane 0, position 0) or null
-  uint8_t* fwd_lo;  // its lo image (unary parents: the residual) or null
-  int32_t keep32;   // a later reader needs the fp32 value (root, shared child)
-  int32_t pad;
+  float* slot;       // the node's fp32 plane map (written only when keep32)
+  int32_t fwd_row;   // staging row of the parent's operand image of this node (position 0), −1: none
+  int32_t fwd_buf;   // 0: stage_x (+ lo in stage_lo), 1 / 2: stage_cat operand 0 / 1 (chunks 0-1 / 2-3)
+  int32_t keep32;    // a later reader needs the fp32 value (root, shared child)
+  int32_t pad[3];
+};
+
+// One gathered operand (leaf input map or shared child's value → a member's
+// staged image), emitted by k_rb_memtab.
+struct GatherTask {
+  const float* src;  // fp32 plane map
+  int64_t row;       // staging row of the member's image (position 0)
+  int32_t buf;       // 0: stage_x (+ lo), 1 / 2: stage_cat operand 0 / 1
+  int32_t step;      // shared children: the member's step (leaves: unused)
+  int64_t pad;
 };
 
 // Per-position epilogue table of one tile.
 struct PosEntry {
   float* dst;       // fp32 store target (plane 0 of this pixel) or null
-  uint8_t* fwd;     // hi image target (plane 0 of this position) or null
-  uint8_t* fwd_lo;  // lo image target or null
+  int32_t fwd_row;  // staging row of the forwarded image at this position, −1: none
+  int32_t fwd_buf;  // as MemberEntry::fwd_buf
   int32_t valid;    // a real pixel of a real member
   int32_t pad;
 };
@@ -136,9 +151,9 @@ struct StepParams {
   int32_t* queue;        // per-step claim counters (zeroed each forward)
 };
 
-// MMA-thread wait accounting: [waiting for a drained accumulator, for an A
-// window, for a weight stage, total cycles of the MMA loop] (slots 3..5 of
-// six; read/reset with dbk_rb_debug()).
+// Wait accounting (read/reset with dbk_rb_debug()): slot 3 = MMA thread
+// [drained accumulator, A window, weight stage, loop total]; slot 4 =
+// window producer [item ring, dependency flags, free window slot, total].
 __device__ unsigned long long g_conv_dbg[6 * 4];
 
 // ------------------------------------------------------------ K phases
@@ -250,11 +265,11 @@ __device__ __forceinline__ void rb_fill_table(const StepParams& P, const Item& i
   }
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
-    PosEntry e{nullptr, nullptr, nullptr, valid[k] ? 1 : 0, 0};
+    PosEntry e{nullptr, -1, 0, valid[k] ? 1 : 0, 0};
     if (it.kind == 2 && valid[k]) {
       e.dst = me[k].keep32 ? me[k].slot + px[k] * 8 : nullptr;
-      e.fwd = me[k].fwd ? me[k].fwd + rem[k] * 16 : nullptr;
-      e.fwd_lo = me[k].fwd_lo ? me[k].fwd_lo + rem[k] * 16 : nullptr;
+      e.fwd_row = me[k].fwd_row >= 0 ? me[k].fwd_row + rem[k] : -1;
+      e.fwd_buf = me[k].fwd_buf;
     }
     tab[lane + 32 * k] = e;
   }
@@ -294,6 +309,12 @@ __device__ __forceinline__ void split_f16x8(const float* o, uint4& hi, uint4& lo
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
+// Byte offset of plane p (16 B: 8 channels) of staging row r (chunk-row
+// layout with the 128-byte swizzle, see the file header).
+__device__ __forceinline__ int64_t stage_off(int64_t ps, int p, int64_t r) {
+  return ((static_cast<int64_t>(p >> 3) * ps + r) << 7) + (((p & 7) ^ static_cast<int>(r & 7)) << 4);
+}
+
 // Epilogue lane geometry: TMEM lanes = output channels 32·quarter + lane,
 // columns = the tile's positions; the warp covers positions
 // [128·half, 128·half + 128) in eight 16-column chunks. After the transpose,
@@ -302,8 +323,9 @@ __device__ __forceinline__ void split_f16x8(const float* o, uint4& hi, uint4& lo
 // a 16-byte vector and a warp instruction covers 4 planes × 8 positions.
 struct EpiLane {
   int quarter, half, e, plane;
-  int64_t plane_off16;  // fp16 staging offset of this lane's plane
-  int plane_off32;      // fp32 plane-map offset of this lane's plane
+  int64_t chunk_off;  // (plane / 8) · PS · 128: this lane's chunk in a staging buffer
+  int sub;            // (plane % 8) ^ e: swizzled 16-byte slot in own-position rows (row & 7 == e)
+  int plane_off32;    // fp32 plane-map offset of this lane's plane
 };
 
 template <int KIND>
@@ -313,10 +335,11 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
   const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias_p));
   const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias_p + 4));
   const float bias[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
-  // own-position outputs (conv1x1 → z hi/lo, conv3x3 #1 → mid)
-  uint8_t* own = (KIND == 0 ? P.stage_x : P.stage_mid) +
-                 static_cast<int64_t>(kGuard + it.q0 + L.half * 128 + L.e) * 16 + L.plane_off16;
-  uint8_t* own_lo = P.stage_lo + static_cast<int64_t>(kGuard + it.q0 + L.half * 128 + L.e) * 16 + L.plane_off16;
+  // own-position outputs (conv1x1 → z hi/lo, conv3x3 #1 → mid): row
+  // kGuard + q0 + 128·half + 16·cb + 8m + e, so (row & 7) == e
+  const int64_t own_off = L.chunk_off + (static_cast<int64_t>(kGuard + it.q0 + L.half * 128 + L.e) << 7) + (L.sub << 4);
+  uint8_t* own = (KIND == 0 ? P.stage_x : P.stage_mid) + own_off;
+  uint8_t* own_lo = P.stage_lo + own_off;
 #pragma unroll 2
   for (int cb = 0; cb < kChunks; ++cb) {
     float v[kChunk];
@@ -330,7 +353,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
       float o[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) o[k] = pe.valid ? fmaxf(x[k] + bias[k], 0.f) : 0.f;
-      const int64_t off = static_cast<int64_t>(cb * kChunk + 8 * m) * 16;
+      const int64_t off = static_cast<int64_t>(cb * kChunk + 8 * m) << 7;
       if (KIND == 1) {
         uint4 pk;
         pk.x = pack_f16x2(o[0], o[1]);
@@ -344,11 +367,13 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
         *reinterpret_cast<uint4*>(own + off) = hi;
         *reinterpret_cast<uint4*>(own_lo + off) = lo;
       } else if (pe.valid) {
-        if (pe.fwd) {
+        if (pe.fwd_row >= 0) {
           uint4 hi, lo;
           split_f16x8(o, hi, lo);
-          *reinterpret_cast<uint4*>(pe.fwd + L.plane_off16) = hi;
-          if (pe.fwd_lo) *reinterpret_cast<uint4*>(pe.fwd_lo + L.plane_off16) = lo;
+          const int p = L.plane + (pe.fwd_buf == 2 ? 16 : 0);
+          const int64_t off = stage_off(P.ps, p, pe.fwd_row);
+          *reinterpret_cast<uint4*>((pe.fwd_buf == 0 ? P.stage_x : P.stage_cat) + off) = hi;
+          if (pe.fwd_buf == 0) *reinterpret_cast<uint4*>(P.stage_lo + off) = lo;
         }
         if (pe.dst) {
           float4* dp = reinterpret_cast<float4*>(pe.dst + L.plane_off32);
@@ -414,28 +439,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {  // ---------------------- scheduler + activation windows
       uint32_t ai = 0;
+      long long w_item = 0, w_dep = 0, w_slot = 0;
+      const long long t_start = clock64();
       for (int32_t n = 0;; ++n) {
         const int32_t k = atomicAdd(P.queue + P.step, 1);
         const Item it = k < total ? step_item(P, k, n0, n1) : Item{-1, 0, 0, 0};
         const int slot = n % kItemSlots;
+        long long c0 = clock64();
         mbar_wait(item_empty + slot, ((n / kItemSlots) & 1) ^ 1);
+        w_item += clock64() - c0;
         items[slot] = it;
         mbar_arrive(item_full + slot);
         if (it.kind < 0) break;
+        c0 = clock64();
         step_wait_deps(P, it);
+        w_dep += clock64() - c0;
         for (int p = 0; p < n_phases(it.kind); ++p) {
           const Phase ph = phase_of(P, it, p);
           const uint32_t rows = kTileM + 2 * ph.halo;
-          const uint8_t* src = ph.src + static_cast<int64_t>(kGuard + it.q0 - ph.halo) * 16;
+          const uint8_t* src = ph.src + (static_cast<int64_t>(kGuard + it.q0 - ph.halo) << 7);
           for (int ch = 0; ch < ph.chunks; ++ch, ++ai) {
             const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
+            const long long c1 = clock64();
             mbar_wait(a_empty + sa, pa ^ 1);
-            mbar_expect_tx(a_full + sa, kChunkPlanes * rows * 16);
-            for (int j = 0; j < kChunkPlanes; ++j)
-              bulk_g2s(sA + sa * kASlot + j * kWin * 16,
-                       src + static_cast<int64_t>(ch * kChunkPlanes + j) * P.ps * 16, rows * 16, a_full + sa);
+            w_slot += clock64() - c1;
+            mbar_expect_tx(a_full + sa, rows * 128);
+            bulk_g2s(sA + sa * kASlot, src + static_cast<int64_t>(ch) * P.ps * 128, rows * 128, a_full + sa);
           }
         }
+      }
+      if (P.debug) {
+        atomicAdd(&g_conv_dbg[16 + 0], static_cast<unsigned long long>(w_item));
+        atomicAdd(&g_conv_dbg[16 + 1], static_cast<unsigned long long>(w_dep));
+        atomicAdd(&g_conv_dbg[16 + 2], static_cast<unsigned long long>(w_slot));
+        atomicAdd(&g_conv_dbg[16 + 3], static_cast<unsigned long long>(clock64() - t_start));
       }
     }
   } else if (warp == 1) {
@@ -478,8 +515,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
               const uint32_t xrow = static_cast<uint32_t>(halo + shift);
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t wd = smem_desc(b_base + s * kBStage + (2 * kk) * 2048, 2048, 128);
-                const uint64_t xd = smem_desc(a_slot + ((2 * kk) * kWin + xrow) * 16, kWin * 16, 128);
+                const uint64_t wd = smem_desc_sw128(b_base + s * kBStage + kk * 32);
+                const uint64_t xd = smem_desc_sw128(a_slot + xrow * 128 + kk * 32);
                 mma_bf16(tmem_base + abuf * kTileM, wd, xd, IDESC, acc);
                 acc = 1;
               }
@@ -539,7 +576,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
     L.half = (warp - 2) >> 2;
     L.e = lane & 7;
     L.plane = L.quarter * 4 + (lane >> 3);
-    L.plane_off16 = static_cast<int64_t>(L.plane) * P.ps * 16;
+    L.chunk_off = static_cast<int64_t>(L.plane >> 3) * P.ps * 128;
+    L.sub = (L.plane & 7) ^ L.e;
     L.plane_off32 = L.plane * kPx * 8;
     const uint32_t lane_addr = (static_cast<uint32_t>(L.quarter * 32) << 16) + L.half * 128;
     for (int n = 0;; ++n) {
@@ -681,24 +719,41 @@ __global__ void k_rb_memtab(int32_t n_steps, const int32_t* __restrict__ sgb,
                             const int32_t* __restrict__ group_fid, const int32_t* __restrict__ group_begin,
                             const int32_t* __restrict__ seg_start, const int32_t* __restrict__ member_g,
                             const int32_t* __restrict__ fwd_pos, const int32_t* __restrict__ fwd_slot,
-                            float* values, uint8_t* stage_x, uint8_t* stage_lo, uint8_t* stage_cat, int64_t ps,
-                            MemberEntry* __restrict__ memtab) {
+                            const int32_t* __restrict__ arity_of, const int32_t* __restrict__ fid,
+                            const int32_t* __restrict__ child0, const int32_t* __restrict__ child1,
+                            const int32_t* __restrict__ example, const int32_t* __restrict__ fwd_ok,
+                            const float* inputs, float* values, MemberEntry* __restrict__ memtab,
+                            GatherTask* __restrict__ tasks, int32_t* __restrict__ n_tasks, int64_t task_cap) {
   const int32_t s = blockIdx.x;
   if (s >= n_steps) return;
   for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
     if (seg_start[g] < 0) continue;
+    const int32_t arity = arity_of[group_fid[g]];
     for (int32_t m = group_begin[g] + threadIdx.x; m < group_begin[g + 1]; m += blockDim.x) {
       const int32_t node = member_g[m];
       const int32_t sw = fwd_slot[node];
       const int32_t tgt = fwd_pos[node];
-      MemberEntry e;
+      MemberEntry e{};
       e.slot = values + static_cast<int64_t>(node) * kFmap;
       e.keep32 = (sw >> 8) & 1;
-      const int64_t off = (static_cast<int64_t>((sw >> 1) & 31) * ps + kGuard + tgt) * 16;
-      e.fwd = tgt >= 0 ? ((sw & 1) ? stage_cat : stage_x) + off : nullptr;
-      e.fwd_lo = tgt >= 0 && !(sw & 1) ? stage_lo + off : nullptr;
-      e.pad = 0;
+      e.fwd_row = tgt >= 0 ? kGuard + tgt : -1;
+      e.fwd_buf = (sw & 1) ? 1 + (((sw >> 1) & 31) >> 4) : 0;
       memtab[m] = e;
+      // operands no child epilogue forwards: leaves (list 0) and children
+      // shared by several parents (list 1), one gather task each
+      for (int k = 0; k < arity; ++k) {
+        const int32_t ch = k == 0 ? child0[node] : child1[node];
+        if (fwd_ok[ch]) continue;
+        const bool leaf = arity_of[fid[ch]] == 0;
+        GatherTask t{};
+        t.src = leaf ? inputs + static_cast<int64_t>(example[ch]) * kFmap : values + static_cast<int64_t>(ch) * kFmap;
+        t.row = kGuard + seg_start[g] + static_cast<int64_t>(m - group_begin[g]) * kImg;
+        t.buf = arity == 2 ? 1 + k : 0;
+        t.step = s;
+        const int list = leaf ? 0 : 1;
+        const int32_t i = atomicAdd(n_tasks + list, 1);
+        if (i < task_cap) tasks[list * task_cap + i] = t;
+      }
     }
   }
 }
@@ -738,44 +793,39 @@ __global__ void k_rb_tiles(int32_t n_steps, const int32_t* __restrict__ sgb,
 // stage_cat planes 16k.. (the channel concat of [x; y] is fused into the
 // write). Only the 196 data positions are written;
 // pads and alignment gaps were zeroed once at session creation.
-__global__ void __launch_bounds__(256) k_rb_gather(
-    int32_t step, const int32_t* __restrict__ sgb, const int32_t* __restrict__ group_fid,
-    const int32_t* __restrict__ group_begin, const int32_t* __restrict__ seg_start,
-    const int32_t* __restrict__ member_g, const int32_t* __restrict__ arity_of,
-    const int32_t* __restrict__ fid, const int32_t* __restrict__ child0,
-    const int32_t* __restrict__ child1, const int32_t* __restrict__ example,
-    const int32_t* __restrict__ fwd_ok, const float* __restrict__ inputs,
-    const float* __restrict__ values, uint8_t* __restrict__ stage_x, uint8_t* __restrict__ stage_lo,
-    uint8_t* __restrict__ stage_cat, int64_t ps) {
-  const int32_t g_lo = sgb[step], g_hi = sgb[step + 1];
-  const int32_t m_lo = group_begin[g_lo], m_hi = group_begin[g_hi];
-  for (int32_t m = m_lo + blockIdx.x; m < m_hi; m += gridDim.x) {
-    int32_t g = g_lo;
-    while (group_begin[g + 1] <= m) ++g;
-    const int32_t arity = arity_of[group_fid[g]];
-    if (arity == 0 || seg_start[g] < 0) continue;
-    const int32_t node = member_g[m];
-    const int32_t base = kGuard + seg_start[g] + (m - group_begin[g]) * kImg;
-    uint8_t* dst = arity == 2 ? stage_cat : stage_x;
-    for (int k = 0; k < arity; ++k) {
-      const int32_t ch = k == 0 ? child0[node] : child1[node];
-      if (fwd_ok[ch]) continue;  // written by the child's epilogue
-      const float* src = arity_of[fid[ch]] == 0 ? inputs + static_cast<int64_t>(example[ch]) * kFmap
-                                                : values + static_cast<int64_t>(ch) * kFmap;
-      for (int idx = threadIdx.x; idx < kPlanes * kPx; idx += blockDim.x) {
-        const int p = idx / kPx, px = idx - p * kPx;
-        const int r = px / 14, c = px - r * 14;
-        const float* sp = src + (p * kPx + px) * 8;
-        const float4 a = *reinterpret_cast<const float4*>(sp);
-        const float4 b = *reinterpret_cast<const float4*>(sp + 4);
-        const float o[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        uint4 hi, lo;
-        split_f16x8(o, hi, lo);
-        const int64_t off = (static_cast<int64_t>(16 * k + p) * ps + base + r * 15 + c) * 16;
-        *reinterpret_cast<uint4*>(dst + off) = hi;
-        if (arity == 1) *reinterpret_cast<uint4*>(stage_lo + off) = lo;  // the block's residual
-      }
-    }
+// Gathered operands → staged images. One thread per (task, 64-channel
+// chunk, pixel, plane of the chunk): 8 consecutive lanes read the 8 planes'
+// 32-byte pixel records and write the 8 swizzled 16-byte slots of one
+// 128-byte staging row, so a warp store covers 4 whole rows (and the lo
+// rows for unary members: the block's residual). list 0 = leaf tasks of
+// every step (inputs only); list 1 = shared-child tasks, restricted to `step`.
+__global__ void __launch_bounds__(256) k_rb_gather(const GatherTask* __restrict__ tasks,
+                                                   const int32_t* __restrict__ n_tasks, int32_t list,
+                                                   int32_t step, int64_t task_cap,
+                                                   uint8_t* __restrict__ stage_x, uint8_t* __restrict__ stage_lo,
+                                                   uint8_t* __restrict__ stage_cat, int64_t ps) {
+  constexpr int kPer = 2 * kPx * 8;
+  const int64_t nt = min(static_cast<int64_t>(n_tasks[list]), task_cap);
+  const GatherTask* T = tasks + list * task_cap;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < nt * kPer;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const GatherTask t = T[idx / kPer];
+    if (list == 1 && t.step != step) continue;
+    const int rem = static_cast<int>(idx % kPer);
+    const int j = rem & 7, q = rem >> 3;
+    const int cc = q >= kPx ? 1 : 0, px = q - cc * kPx;
+    const int r = px / 14, c = px - r * 14;
+    const int64_t row = t.row + r * 15 + c;
+    const int64_t off = ((static_cast<int64_t>((t.buf == 2 ? 2 : 0) + cc) * ps + row) << 7) +
+                        ((j ^ static_cast<int>(row & 7)) << 4);
+    const float* sp = t.src + ((8 * cc + j) * kPx + px) * 8;
+    const float4 a = __ldg(reinterpret_cast<const float4*>(sp));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(sp + 4));
+    const float o[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint4 h, l;
+    split_f16x8(o, h, l);
+    *reinterpret_cast<uint4*>((t.buf == 0 ? stage_x : stage_cat) + off) = h;
+    if (t.buf == 0) *reinterpret_cast<uint4*>(stage_lo + off) = l;
   }
 }
 
@@ -840,29 +890,28 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
   return static_cast<int>(cudaGetLastError());
 }
 
-extern "C" int dbk_rb_gather(int32_t step, const int32_t* step_group_begin, const int32_t* group_fid,
-                             const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
-                             const int32_t* arity_of, const int32_t* fid, const int32_t* child0,
-                             const int32_t* child1, const int32_t* example, const int32_t* fwd_ok,
-                             const float* inputs, const float* values, void* stage_x, void* stage_lo,
-                             void* stage_cat, int64_t plane_stride, int32_t blocks, void* stream) {
+extern "C" int dbk_rb_gather(const void* tasks, const int32_t* n_tasks, int32_t list, int32_t step,
+                             int64_t task_cap, void* stage_x, void* stage_lo, void* stage_cat, int64_t plane_stride,
+                             int32_t blocks, void* stream) {
   k_rb_gather<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      step, step_group_begin, group_fid, group_begin, seg_start, member_g, arity_of, fid, child0, child1,
-      example, fwd_ok, inputs, values, static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_lo),
-      static_cast<uint8_t*>(stage_cat), plane_stride);
+      static_cast<const GatherTask*>(tasks), n_tasks, list, step, task_cap, static_cast<uint8_t*>(stage_x),
+      static_cast<uint8_t*>(stage_lo), static_cast<uint8_t*>(stage_cat), plane_stride);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
                              const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
-                             const int32_t* fwd_pos, const int32_t* fwd_slot, float* values, void* stage_x,
-                             void* stage_lo, void* stage_cat, int64_t plane_stride, void* memtab,
-                             void* stream) {
+                             const int32_t* fwd_pos, const int32_t* fwd_slot, const int32_t* arity_of,
+                             const int32_t* fid, const int32_t* child0, const int32_t* child1,
+                             const int32_t* example, const int32_t* fwd_ok, const float* inputs, float* values,
+                             void* memtab, void* tasks, int32_t* n_tasks, int64_t task_cap, void* stream) {
   if (n_steps <= 0) return 0;
-  k_rb_memtab<<<n_steps, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      n_steps, step_group_begin, group_fid, group_begin, seg_start, member_g, fwd_pos, fwd_slot, values,
-      static_cast<uint8_t*>(stage_x), static_cast<uint8_t*>(stage_lo), static_cast<uint8_t*>(stage_cat),
-      plane_stride, static_cast<MemberEntry*>(memtab));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(n_tasks, 0, 2 * sizeof(int32_t), s);
+  k_rb_memtab<<<n_steps, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, seg_start, member_g,
+                                      fwd_pos, fwd_slot, arity_of, fid, child0, child1, example, fwd_ok, inputs,
+                                      values, static_cast<MemberEntry*>(memtab), static_cast<GatherTask*>(tasks),
+                                      n_tasks, task_cap);
   return static_cast<int>(cudaGetLastError());
 }
 

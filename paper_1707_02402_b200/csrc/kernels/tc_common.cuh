@@ -187,6 +187,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// K-major SWIZZLE_128B descriptor: rows of 128 B (64 fp16 of K), 8-row groups
+// 1024 B apart, 16-byte chunks XOR-swizzled by absolute address bits [7:10)
+// (base offset 0), so the start may be any row and any 32-byte K offset
+// within the row (verified by tools/sw128_test.cu).
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;          // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;  // SBO: 8 rows × 128 B
+  d |= static_cast<uint64_t>(1) << 46;          // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;          // layout: SWIZZLE_128B
+  return d;
+}
+
 // Shared-memory matrix descriptor, K-major SWIZZLE_NONE (see file header).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes,
                                               uint32_t sbo_bytes) {

@@ -1,6 +1,7 @@
 """Interleaved A/B forward timing of library builds on one box:
-python profiles/ab_time.py lib_a.so lib_b.so [rounds]. Each round runs each
-build in a fresh process (cfg3, 10 timed forwards after 3 warm-ups)."""
+python profiles/ab_time.py lib_a.so lib_b.so [...] [--rounds R]. Each round
+runs each build in a fresh process (cfg3, 10 timed forwards after 3
+warm-ups, best of 3)."""
 import os
 import subprocess
 import sys
@@ -17,8 +18,13 @@ s.time(3)
 print(min(s.time(10)[0] / 10 for _ in range(3)))
 """ % ROOT
 
-libs = sys.argv[1:3]
-rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+args = sys.argv[1:]
+rounds = 3
+if "--rounds" in args:
+    i = args.index("--rounds")
+    rounds = int(args[i + 1])
+    args = args[:i] + args[i + 2:]
+libs = args
 res = {l: [] for l in libs}
 for _ in range(rounds):
     for l in libs:

@@ -18,3 +18,6 @@ acc, a, bb, tot = (int(x) for x in w[3])
 cover = tot / (148 * kt.ms[4] * 1e-3 * CLK_GHZ * 1e9)
 print(f"step kernel ms/fwd {kt.ms[4] / 5:.3f}: acc_wait {acc/tot:6.1%}  A_wait {a/tot:6.1%}  B_wait {bb/tot:6.1%}  "
       f"busy {(tot-acc-a-bb)/tot:6.1%}  loop/kernel {cover:6.1%}")
+it, dep, sl, ptot = (int(x) for x in w[4])
+print(f"window producer: item-ring wait {it/ptot:6.1%}  dependency wait {dep/ptot:6.1%}  "
+      f"slot wait {sl/ptot:6.1%}  issuing {(ptot-it-dep-sl)/ptot:6.1%}")
