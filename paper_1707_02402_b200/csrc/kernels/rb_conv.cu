@@ -126,6 +126,8 @@ struct Item {
 
 struct StepParams {
   int32_t step, epoch, lookahead, debug;
+  int32_t diag;  // timing diagnostics only (wrong results): bit 0 skips weight reloads, bit 1 window
+                 // reloads, bit 2 the epilogue work (TMEM loads, transposes, stores)
   const int32_t* step_tile_begin;
   const int32_t* tile_group;
   const int32_t* tile_q0;
@@ -386,6 +388,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
 }
 
 // --------------------------------------------------------------- kernel
+template <bool DBG>
 __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__ StepParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
@@ -445,30 +448,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         const int32_t k = atomicAdd(P.queue + P.step, 1);
         const Item it = k < total ? step_item(P, k, n0, n1) : Item{-1, 0, 0, 0};
         const int slot = n % kItemSlots;
-        long long c0 = clock64();
+        long long c0 = DBG ? clock64() : 0;
         mbar_wait(item_empty + slot, ((n / kItemSlots) & 1) ^ 1);
-        w_item += clock64() - c0;
+        if (DBG) w_item += clock64() - c0;
         items[slot] = it;
         mbar_arrive(item_full + slot);
         if (it.kind < 0) break;
-        c0 = clock64();
+        if (DBG) c0 = clock64();
         step_wait_deps(P, it);
-        w_dep += clock64() - c0;
+        if (DBG) w_dep += clock64() - c0;
         for (int p = 0; p < n_phases(it.kind); ++p) {
           const Phase ph = phase_of(P, it, p);
           const uint32_t rows = kTileM + 2 * ph.halo;
           const uint8_t* src = ph.src + (static_cast<int64_t>(kGuard + it.q0 - ph.halo) << 7);
           for (int ch = 0; ch < ph.chunks; ++ch, ++ai) {
             const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
-            const long long c1 = clock64();
+            const long long c1 = DBG ? clock64() : 0;
             mbar_wait(a_empty + sa, pa ^ 1);
-            w_slot += clock64() - c1;
+            if (DBG) w_slot += clock64() - c1;
+            if ((P.diag & 2) && ai >= kASlots) {
+              mbar_arrive(a_full + sa);
+              continue;
+            }
             mbar_expect_tx(a_full + sa, rows * 128);
             bulk_g2s(sA + sa * kASlot, src + static_cast<int64_t>(ch) * P.ps * 128, rows * 128, a_full + sa);
           }
         }
       }
-      if (P.debug) {
+      if (DBG) {
         atomicAdd(&g_conv_dbg[16 + 0], static_cast<unsigned long long>(w_item));
         atomicAdd(&g_conv_dbg[16 + 1], static_cast<unsigned long long>(w_dep));
         atomicAdd(&g_conv_dbg[16 + 2], static_cast<unsigned long long>(w_slot));
@@ -489,9 +496,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         mbar_arrive(item_empty + slot);
         if (it.kind < 0) break;
         const int abuf = n & 1;
-        long long c0 = clock64();
+        long long c0 = DBG ? clock64() : 0;
         mbar_wait(acc_empty + abuf, ((n >> 1) & 1) ^ 1);
-        w_acc += clock64() - c0;
+        if (DBG) w_acc += clock64() - c0;
         tc_fence_after();
         uint32_t acc = 0;
         for (int p = 0; p < n_phases(it.kind); ++p) {
@@ -500,16 +507,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           const int halo = (it.kind == 0 || p > 0) ? 0 : kHalo;
           for (int ch = 0; ch < chunks; ++ch, ++ai) {
             const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
-            c0 = clock64();
+            if (DBG) c0 = clock64();
             mbar_wait(a_full + sa, pa);
-            w_a += clock64() - c0;
+            if (DBG) w_a += clock64() - c0;
             tc_fence_after();
             const uint32_t a_slot = a_base + sa * kASlot;
             for (int tap = 0; tap < taps; ++tap, ++bi) {
               const uint32_t s = bi % kBStages, par = (bi / kBStages) & 1;
-              c0 = clock64();
+              if (DBG) c0 = clock64();
               mbar_wait(b_full + s, par);
-              w_b += clock64() - c0;
+              if (DBG) w_b += clock64() - c0;
               tc_fence_after();
               const int shift = taps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
               const uint32_t xrow = static_cast<uint32_t>(halo + shift);
@@ -527,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         }
         mma_commit(acc_full + abuf);
       }
-      if (P.debug) {
+      if (DBG) {
         atomicAdd(&g_conv_dbg[12 + 0], static_cast<unsigned long long>(w_acc));
         atomicAdd(&g_conv_dbg[12 + 1], static_cast<unsigned long long>(w_a));
         atomicAdd(&g_conv_dbg[12 + 2], static_cast<unsigned long long>(w_b));
@@ -549,6 +556,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
             for (int tap = 0; tap < ph.taps; ++tap, ++bi) {
               const uint32_t s = bi % kBStages, par = (bi / kBStages) & 1;
               mbar_wait(b_empty + s, par ^ 1);
+              if ((P.diag & 1) && bi >= kBStages) {
+                mbar_arrive(b_full + s);
+                continue;
+              }
               mbar_expect_tx(b_full + s, kBStage);
               bulk_g2s(sB + s * kBStage, ph.w + static_cast<int64_t>(ch * ph.taps + tap) * kBStage, kBStage,
                        b_full + s);
@@ -593,12 +604,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       mbar_wait(acc_full + abuf, (n >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + abuf * kTileM + lane_addr;
-      if (it.kind == 0)
+      if (P.diag & 4) {
+      } else if (it.kind == 0) {
         step_epilogue<0>(P, tab, L, taddr, it);
-      else if (it.kind == 1)
+      } else if (it.kind == 1) {
         step_epilogue<1>(P, tab, L, taddr, it);
-      else
+      } else {
         step_epilogue<2>(P, tab, L, taddr, it);
+      }
       tc_fence_before();
       mbar_arrive(acc_empty + abuf);
       __syncwarp();
@@ -689,28 +702,37 @@ __global__ void k_rb_fwd_init(int64_t n, int32_t* __restrict__ fwd_pos, int32_t*
   }
 }
 
+// Last index i in [lo, hi] with v[i] <= x (v ascending, v[lo] <= x).
+__device__ __forceinline__ int32_t last_le(const int32_t* __restrict__ v, int32_t lo, int32_t hi, int32_t x) {
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (v[mid] <= x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Forwarding targets: one thread per member of every step; each child with
+// a unique parent (fwd_ok) gets the parent's image position and buffer.
 __global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const int32_t* __restrict__ group_fid,
                          const int32_t* __restrict__ group_begin, const int32_t* __restrict__ arity_of,
                          const int32_t* __restrict__ seg_start, const int32_t* __restrict__ member_g,
                          const int32_t* __restrict__ child0, const int32_t* __restrict__ child1,
                          const int32_t* __restrict__ fwd_ok, int32_t* __restrict__ fwd_pos,
                          int32_t* __restrict__ fwd_slot) {
-  const int32_t s = blockIdx.x;
-  if (s >= n_steps) return;
-  for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
+  const int32_t g0 = sgb[0], g1 = sgb[n_steps];
+  const int32_t m0 = group_begin[g0], m1 = group_begin[g1];
+  for (int32_t m = m0 + blockIdx.x * blockDim.x + threadIdx.x; m < m1; m += gridDim.x * blockDim.x) {
+    const int32_t g = last_le(group_begin, g0, g1 - 1, m);
     if (seg_start[g] < 0) continue;
     const int32_t arity = arity_of[group_fid[g]];
-    const int32_t rows = group_begin[g + 1] - group_begin[g];
-    for (int32_t i = threadIdx.x; i < rows; i += blockDim.x) {
-      const int32_t node = member_g[group_begin[g] + i];
-      for (int k = 0; k < arity; ++k) {
-        const int32_t c = k == 0 ? child0[node] : child1[node];
-        if (!fwd_ok[c]) continue;
-        fwd_pos[c] = seg_start[g] + i * kImg;
-        // buffer (bit 0: stage_x / stage_cat) and first plane; no fp32 copy:
-        // a unary parent reads its residual from the hi/lo images
-        fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1);
-      }
+    const int32_t node = member_g[m];
+    for (int k = 0; k < arity; ++k) {
+      const int32_t c = k == 0 ? child0[node] : child1[node];
+      if (!fwd_ok[c]) continue;
+      fwd_pos[c] = seg_start[g] + (m - group_begin[g]) * kImg;
+      // buffer (bit 0: stage_x / stage_cat) and first plane; no fp32 copy:
+      // a unary parent reads its residual from the hi/lo images
+      fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1);
     }
   }
 }
@@ -724,36 +746,35 @@ __global__ void k_rb_memtab(int32_t n_steps, const int32_t* __restrict__ sgb,
                             const int32_t* __restrict__ example, const int32_t* __restrict__ fwd_ok,
                             const float* inputs, float* values, MemberEntry* __restrict__ memtab,
                             GatherTask* __restrict__ tasks, int32_t* __restrict__ n_tasks, int64_t task_cap) {
-  const int32_t s = blockIdx.x;
-  if (s >= n_steps) return;
-  for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
+  const int32_t g0 = sgb[0], g1 = sgb[n_steps];
+  const int32_t m0 = group_begin[g0], m1 = group_begin[g1];
+  for (int32_t m = m0 + blockIdx.x * blockDim.x + threadIdx.x; m < m1; m += gridDim.x * blockDim.x) {
+    const int32_t g = last_le(group_begin, g0, g1 - 1, m);
     if (seg_start[g] < 0) continue;
     const int32_t arity = arity_of[group_fid[g]];
-    for (int32_t m = group_begin[g] + threadIdx.x; m < group_begin[g + 1]; m += blockDim.x) {
-      const int32_t node = member_g[m];
-      const int32_t sw = fwd_slot[node];
-      const int32_t tgt = fwd_pos[node];
-      MemberEntry e{};
-      e.slot = values + static_cast<int64_t>(node) * kFmap;
-      e.keep32 = (sw >> 8) & 1;
-      e.fwd_row = tgt >= 0 ? kGuard + tgt : -1;
-      e.fwd_buf = (sw & 1) ? 1 + (((sw >> 1) & 31) >> 4) : 0;
-      memtab[m] = e;
-      // operands no child epilogue forwards: leaves (list 0) and children
-      // shared by several parents (list 1), one gather task each
-      for (int k = 0; k < arity; ++k) {
-        const int32_t ch = k == 0 ? child0[node] : child1[node];
-        if (fwd_ok[ch]) continue;
-        const bool leaf = arity_of[fid[ch]] == 0;
-        GatherTask t{};
-        t.src = leaf ? inputs + static_cast<int64_t>(example[ch]) * kFmap : values + static_cast<int64_t>(ch) * kFmap;
-        t.row = kGuard + seg_start[g] + static_cast<int64_t>(m - group_begin[g]) * kImg;
-        t.buf = arity == 2 ? 1 + k : 0;
-        t.step = s;
-        const int list = leaf ? 0 : 1;
-        const int32_t i = atomicAdd(n_tasks + list, 1);
-        if (i < task_cap) tasks[list * task_cap + i] = t;
-      }
+    const int32_t node = member_g[m];
+    const int32_t sw = fwd_slot[node];
+    const int32_t tgt = fwd_pos[node];
+    MemberEntry e{};
+    e.slot = values + static_cast<int64_t>(node) * kFmap;
+    e.keep32 = (sw >> 8) & 1;
+    e.fwd_row = tgt >= 0 ? kGuard + tgt : -1;
+    e.fwd_buf = (sw & 1) ? 1 + (((sw >> 1) & 31) >> 4) : 0;
+    memtab[m] = e;
+    // operands no child epilogue forwards: leaves (list 0) and children
+    // shared by several parents (list 1), one gather task each
+    for (int k = 0; k < arity; ++k) {
+      const int32_t ch = k == 0 ? child0[node] : child1[node];
+      if (fwd_ok[ch]) continue;
+      const bool leaf = arity_of[fid[ch]] == 0;
+      GatherTask t{};
+      t.src = leaf ? inputs + static_cast<int64_t>(example[ch]) * kFmap : values + static_cast<int64_t>(ch) * kFmap;
+      t.row = kGuard + seg_start[g] + static_cast<int64_t>(m - group_begin[g]) * kImg;
+      t.buf = arity == 2 ? 1 + k : 0;
+      t.step = last_le(sgb, 0, n_steps - 1, g);
+      const int list = leaf ? 0 : 1;
+      const int32_t i = atomicAdd(n_tasks + list, 1);
+      if (i < task_cap) tasks[list * task_cap + i] = t;
     }
   }
 }
@@ -885,7 +906,7 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
                                      seg_start, group_tile0, group_bintile0, step_tile_begin,
                                      step_bintile_begin, tile_group, tile_q0, bin_group, bin_q0, tile_m);
   k_rb_fwd_init<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_nodes, fwd_pos, fwd_slot);
-  k_rb_fwd<<<n_steps, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
+  k_rb_fwd<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
                                    member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot);
   return static_cast<int>(cudaGetLastError());
 }
@@ -908,7 +929,7 @@ extern "C" int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, c
   if (n_steps <= 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaMemsetAsync(n_tasks, 0, 2 * sizeof(int32_t), s);
-  k_rb_memtab<<<n_steps, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, seg_start, member_g,
+  k_rb_memtab<<<148 * 4, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, seg_start, member_g,
                                       fwd_pos, fwd_slot, arity_of, fid, child0, child1, example, fwd_ok, inputs,
                                       values, static_cast<MemberEntry*>(memtab), static_cast<GatherTask*>(tasks),
                                       n_tasks, task_cap);
@@ -926,7 +947,8 @@ extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile
                            int32_t* queue, int32_t num_sms, void* stream) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_rb_step, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     configured = true;
   }
   StepParams p{};
@@ -935,6 +957,8 @@ extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile
   const char* la = std::getenv("DYNBATCH_LOOKAHEAD");
   p.lookahead = (la ? std::atoi(la) : 8) * num_sms;
   p.debug = g_debug_flag;
+  const char* dg = std::getenv("DYNBATCH_DIAG");
+  p.diag = dg ? std::atoi(dg) : 0;
   p.step_tile_begin = step_tile_begin;
   p.tile_group = tile_group;
   p.tile_q0 = tile_q0;
@@ -962,7 +986,10 @@ extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile
   p.done0 = done0;
   p.done1 = done1;
   p.queue = queue;
-  k_rb_step<<<num_sms, kThreads, kStepSmem, static_cast<cudaStream_t>(stream)>>>(p);
+  if (p.debug)
+    k_rb_step<true><<<num_sms, kThreads, kStepSmem, static_cast<cudaStream_t>(stream)>>>(p);
+  else
+    k_rb_step<false><<<num_sms, kThreads, kStepSmem, static_cast<cudaStream_t>(stream)>>>(p);
   return static_cast<int>(cudaGetLastError());
 }
 
