@@ -155,6 +155,55 @@ DeviceProgramBatch::DeviceProgramBatch(const HostCSR& csr, cudaStream_t s) : csr
   group_fid.alloc(static_cast<size_t>(max_keys_) + 1);
   group_begin.alloc(static_cast<size_t>(max_keys_) + 2);
   step_group_begin.alloc(static_cast<size_t>(std::max(1, csr.s_max)) + 2);
+  detect_static_shape(s);
+}
+
+// Balanced-tree static schedule (SURVEY.md §3 balanced_static_schedule):
+// when every program has the same tree shape (node count, local child lists,
+// root), the longest-root-distance labels are one per-shape table, computed
+// here once with the reference's rule (src/program.cpp:239-272); the device
+// scheduler then only fills labels from it and buckets by fid per level.
+void DeviceProgramBatch::detect_static_shape(cudaStream_t s) {
+  const HostCSR& c = csr_;
+  if (c.b < 2) return;
+  const std::int32_t n = c.prog_off[1] - c.prog_off[0];
+  if (n <= 0 || static_cast<std::int64_t>(n) * c.b != c.N) return;
+  for (std::int64_t e = 0; e < c.b; ++e) {
+    const std::int32_t base = static_cast<std::int32_t>(e) * n;
+    if (c.prog_off[static_cast<size_t>(e)] != base) return;
+    if (c.root_g[static_cast<size_t>(e)] - base != c.root_g[0]) return;
+    for (std::int32_t i = 0; i < n; ++i) {
+      const size_t g = static_cast<size_t>(base + i), g0 = static_cast<size_t>(i);
+      const std::int32_t a = c.child_off[g + 1] - c.child_off[g];
+      if (a != c.child_off[g0 + 1] - c.child_off[g0]) return;
+      for (std::int32_t k = 0; k < a; ++k) {
+        if (c.child_list[static_cast<size_t>(c.child_off[g] + k)] - base !=
+            c.child_list[static_cast<size_t>(c.child_off[g0] + k)])
+          return;
+      }
+    }
+  }
+  // labels of the shape: longest distance from the root (Kahn over the DAG)
+  std::vector<std::int32_t> lab(static_cast<size_t>(n), -1), indeg(static_cast<size_t>(n), 0), queue;
+  for (std::int32_t i = 0; i < n; ++i)
+    for (std::int32_t k = c.child_off[static_cast<size_t>(i)]; k < c.child_off[static_cast<size_t>(i) + 1]; ++k)
+      ++indeg[static_cast<size_t>(c.child_list[static_cast<size_t>(k)])];
+  const std::int32_t root = c.root_g[0];
+  if (indeg[static_cast<size_t>(root)] != 0) return;
+  lab[static_cast<size_t>(root)] = 0;
+  queue.push_back(root);
+  for (size_t h = 0; h < queue.size(); ++h) {
+    const std::int32_t u = queue[h];
+    for (std::int32_t k = c.child_off[static_cast<size_t>(u)]; k < c.child_off[static_cast<size_t>(u) + 1]; ++k) {
+      const std::int32_t v = c.child_list[static_cast<size_t>(k)];
+      lab[static_cast<size_t>(v)] = std::max(lab[static_cast<size_t>(v)], lab[static_cast<size_t>(u)] + 1);
+      if (--indeg[static_cast<size_t>(v)] == 0) queue.push_back(v);
+    }
+  }
+  if (static_cast<std::int32_t>(queue.size()) != n) return;  // unreachable node: the dynamic path reports it
+  shape_dmax_ = *std::max_element(lab.begin(), lab.end());
+  shape_labels_.upload(lab, s);
+  shape_n_ = n;
 }
 
 int DeviceProgramBatch::run_scheduler(cudaStream_t s) {
@@ -164,13 +213,23 @@ int DeviceProgramBatch::run_scheduler(cudaStream_t s) {
     return 0;
   }
   check(cudaMemsetAsync(scalars.get(), 0, sizeof(std::int32_t) * 8, s), "memset");
-  check(dbk_sched_labels(csr_.b, csr_.N, prog_off.get(), child_off.get(), child_list.get(),
-                         root_g.get(), labels.get(), scratch.get(), scalars.get(), s),
-        "dbk_sched_labels");
+  if (static_shape()) {  // balanced-tree (shared shape) static schedule: labels from the shape table
+    check(dbk_sched_labels_static(csr_.N, shape_n_, shape_labels_.get(), shape_dmax_, labels.get(), scalars.get(), s),
+          "dbk_sched_labels_static");
+  } else {
+    check(dbk_sched_labels(csr_.b, csr_.N, prog_off.get(), child_off.get(), child_list.get(),
+                           root_g.get(), labels.get(), scratch.get(), scalars.get(), s),
+          "dbk_sched_labels");
+  }
   check(dbk_sched_bucket_sort(csr_.N, csr_.p, max_keys_, fid.get(), labels.get(), scalars.get(),
                               seg_hist.get(), member_g.get(), group_fid.get(), group_begin.get(),
                               step_group_begin.get(), s),
         "dbk_sched_bucket_sort");
+  if (static_shape()) {  // the step count is known: no host sync in the forward
+    steps = shape_dmax_ + 1;
+    groups_pending_ = true;
+    return steps;
+  }
   std::int32_t host_scal[3];
   check(cudaMemcpyAsync(host_scal, scalars.get(), sizeof(host_scal), cudaMemcpyDeviceToHost, s),
         "D2H scalars");
@@ -178,7 +237,19 @@ int DeviceProgramBatch::run_scheduler(cudaStream_t s) {
   if (host_scal[1]) throw_error(Errc::invalid_program, "cycle or unreachable node");
   steps = host_scal[0] + 1;
   groups = host_scal[2];
+  groups_pending_ = false;
   return steps;
+}
+
+std::int64_t DeviceProgramBatch::group_count(cudaStream_t s) const {
+  if (groups_pending_) {
+    std::int32_t g = 0;
+    check(cudaMemcpyAsync(&g, scalars.get() + 2, sizeof(g), cudaMemcpyDeviceToHost, s), "D2H groups");
+    check(cudaStreamSynchronize(s), "sync");
+    groups = g;
+    groups_pending_ = false;
+  }
+  return groups;
 }
 
 int DeviceProgramBatch::load_schedule(const Schedule& schedule, cudaStream_t s) {
@@ -212,12 +283,14 @@ int DeviceProgramBatch::load_schedule(const Schedule& schedule, cudaStream_t s) 
   step_group_begin.upload(sgb, s);
   steps = static_cast<int>(schedule.steps.size());
   groups = static_cast<std::int64_t>(gf.size());
+  groups_pending_ = false;
   return steps;
 }
 
 Schedule DeviceProgramBatch::download_schedule(Strategy strategy, cudaStream_t s) const {
   Schedule out{strategy, {}};
   if (steps == 0) return out;
+  group_count(s);
   const auto sgb = step_group_begin.download(static_cast<size_t>(steps) + 1, s);
   const auto gf = group_fid.download(static_cast<size_t>(groups), s);
   const auto gb = group_begin.download(static_cast<size_t>(groups) + 1, s);
@@ -242,6 +315,7 @@ ExecutionTrace DeviceProgramBatch::trace_counts(cudaStream_t s) const {
   ExecutionTrace t;
   t.per_function_calls.assign(static_cast<size_t>(csr_.p), 0);
   if (steps == 0) return t;
+  group_count(s);
   const auto gf = group_fid.download(static_cast<size_t>(groups), s);
   const auto gb = group_begin.download(static_cast<size_t>(groups) + 1, s);
   for (std::int64_t g = 0; g < groups; ++g) {

@@ -122,15 +122,24 @@ class DeviceProgramBatch {
   std::vector<std::int32_t> download_labels(cudaStream_t s) const { return labels.download(csr_.N, s); }
   ExecutionTrace trace_counts(cudaStream_t s) const;
 
+  // Group count of the last schedule (the device scheduler's value is read
+  // lazily: a static-shape schedule needs no host sync).
+  std::int64_t group_count(cudaStream_t s) const;
+  bool static_shape() const { return shape_n_ > 0; }
+
   int steps = 0;
-  std::int64_t groups = 0;
+  mutable std::int64_t groups = 0;
   Buf<std::int32_t> prog_off, fid, child_off, child_list, child0, child1, example, root_g;
   Buf<std::int32_t> arity_of, labels, scratch, scalars, seg_hist;
   Buf<std::int32_t> member_g, group_fid, group_begin, step_group_begin;
 
  private:
+  void detect_static_shape(cudaStream_t s);
   HostCSR csr_;
   int max_keys_ = 0;
+  mutable bool groups_pending_ = false;
+  int shape_n_ = 0, shape_dmax_ = 0;  // programs share one tree shape (static schedule)
+  Buf<std::int32_t> shape_labels_;
 };
 
 enum class ModuleKind { dense = 0, resblock = 1 };
