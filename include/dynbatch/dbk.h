@@ -28,20 +28,23 @@ int dbk_sched_labels(int64_t b, int64_t N, const int32_t* prog_off, const int32_
                      const int32_t* child_list, const int32_t* root_g, int32_t* labels,
                      int32_t* scratch, int32_t* dev_scalars, void* stream);
 
-/* Stable counting sort of all N nodes by key = (d_max - label)·p + fid
- * over CSR order; writes member_g[N] (sorted global ids), and the group
- * tables: group_fid[G], group_begin[G+1], step_group_begin[S+1] with
- * dev_scalars[2] = G. seg_hist must hold max_keys · n_segments ints with
- * max_keys ≥ (d_max+1)·p; size from dbk_bucket_sort_scratch(N, max_keys). */
 /* Labels of a batch whose programs all share one tree shape (programs of n
  * nodes, shape labels table[n], depth dmax): the balanced-tree static
  * schedule (SURVEY.md §3 balanced_static_schedule); sets dev_scalars[0] = dmax. */
 int dbk_sched_labels_static(int64_t N, int32_t n, const int32_t* table, int32_t dmax, int32_t* labels,
                             int32_t* dev_scalars, void* stream);
+
+/* Stable counting sort of all N nodes by key = (d_max - label)·p + fid
+ * over CSR order; writes member_g[N] (sorted global ids), and the group
+ * tables: group_fid[G], group_begin[G+1], step_group_begin[S+1] (and empty
+ * steps up to steps_cap, so a host may launch per-step work for an upper
+ * bound of S) with dev_scalars[2] = G. seg_hist must hold max_keys ·
+ * n_segments ints with max_keys ≥ (d_max+1)·p; size from
+ * dbk_bucket_sort_scratch(N, max_keys). */
 int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, const int32_t* fid,
                           const int32_t* labels, int32_t* dev_scalars, int32_t* seg_hist,
                           int32_t* member_g, int32_t* group_fid, int32_t* group_begin,
-                          int32_t* step_group_begin, void* stream);
+                          int32_t* step_group_begin, int32_t steps_cap, void* stream);
 
 /* Scratch (int32 count) the bucket sorts need in seg_hist. */
 int64_t dbk_bucket_sort_scratch(int64_t n_items, int32_t max_keys);

@@ -100,6 +100,12 @@ DYNBATCH_API db_status db_iep_session_forward(db_iep_session* s);
  * CHW for RESBLOCK) → H2D → forward → D2H of the root outputs (fp32). */
 DYNBATCH_API db_status db_iep_session_forward_host(db_iep_session* s, const float* inputs,
                                                    float* outputs);
+/* Pipelined form of …_forward_host: returns once the call is enqueued. The
+ * upload of this call and the download of the previous one overlap the
+ * forward (copy streams, double-buffered device rows). The host buffers must
+ * stay valid, and should be pinned, until db_iep_session_synchronize. */
+DYNBATCH_API db_status db_iep_session_forward_host_async(db_iep_session* s, const float* inputs,
+                                                         float* outputs);
 DYNBATCH_API db_status db_iep_session_synchronize(db_iep_session* s);
 DYNBATCH_API void* db_iep_session_stream(db_iep_session* s);
 DYNBATCH_API db_status db_iep_session_stats(db_iep_session* s, db_session_stats_t* out);

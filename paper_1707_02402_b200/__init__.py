@@ -141,6 +141,7 @@ SIGNATURES = {
     "db_iep_session_set_schedule": (C.c_int32, [VP, VP]),
     "db_iep_session_forward": (C.c_int32, [VP]),
     "db_iep_session_forward_host": (C.c_int32, [VP, VP, VP]),
+    "db_iep_session_forward_host_async": (C.c_int32, [VP, VP, VP]),
     "db_iep_session_synchronize": (C.c_int32, [VP]),
     "db_iep_session_stream": (VP, [VP]),
     "db_iep_session_stats": (C.c_int32, [VP, C.POINTER(SessionStats)]),
@@ -393,6 +394,11 @@ class IepSession(_Handle):
 
     def forward(self):
         check(lib().db_iep_session_forward(self.h))
+
+    def forward_host_async(self, inputs: np.ndarray, outputs: np.ndarray):
+        """Pipelined forward_host (overlaps the copies with the neighbouring
+        calls' forwards); keep the arrays alive until synchronize()."""
+        check(lib().db_iep_session_forward_host_async(self.h, _ptr(inputs), _ptr(outputs)))
 
     def forward_host(self, inputs: np.ndarray, outputs: np.ndarray):
         check(lib().db_iep_session_forward_host(self.h, _ptr(inputs), _ptr(outputs)))

@@ -469,6 +469,11 @@ db_status db_iep_session_forward_host(db_iep_session* s, const float* inputs, fl
   return guarded([&] { s->s->forward_host(inputs, outputs); });
 }
 
+db_status db_iep_session_forward_host_async(db_iep_session* s, const float* inputs, float* outputs) {
+  if (!s || !inputs || !outputs) return null_arg();
+  return guarded([&] { s->s->forward_host_async(inputs, outputs); });
+}
+
 db_status db_iep_session_synchronize(db_iep_session* s) {
   if (!s) return null_arg();
   return guarded([&] { s->s->synchronize(); });

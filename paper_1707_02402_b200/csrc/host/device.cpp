@@ -206,7 +206,7 @@ void DeviceProgramBatch::detect_static_shape(cudaStream_t s) {
   shape_n_ = n;
 }
 
-int DeviceProgramBatch::run_scheduler(cudaStream_t s) {
+int DeviceProgramBatch::run_scheduler(cudaStream_t s, bool upper_bound) {
   if (csr_.b == 0) {
     steps = 0;
     groups = 0;
@@ -221,13 +221,20 @@ int DeviceProgramBatch::run_scheduler(cudaStream_t s) {
                            root_g.get(), labels.get(), scratch.get(), scalars.get(), s),
           "dbk_sched_labels");
   }
+  const int cap = std::max(1, csr_.s_max);
   check(dbk_sched_bucket_sort(csr_.N, csr_.p, max_keys_, fid.get(), labels.get(), scalars.get(),
                               seg_hist.get(), member_g.get(), group_fid.get(), group_begin.get(),
-                              step_group_begin.get(), s),
+                              step_group_begin.get(), cap, s),
         "dbk_sched_bucket_sort");
   if (static_shape()) {  // the step count is known: no host sync in the forward
     steps = shape_dmax_ + 1;
     groups_pending_ = true;
+    return steps;
+  }
+  if (upper_bound) {  // no host sync: per-step work for s_max steps, the empty ones exit on the device
+    steps = cap;
+    groups_pending_ = true;
+    errors_pending_ = true;
     return steps;
   }
   std::int32_t host_scal[3];
@@ -241,14 +248,25 @@ int DeviceProgramBatch::run_scheduler(cudaStream_t s) {
   return steps;
 }
 
+// Reads the device scheduler's scalars (d_max, error flag, group count)
+// when the last forward did not: the real step count replaces the upper
+// bound once the forward is done.
+void DeviceProgramBatch::resolve(cudaStream_t s) const {
+  if (!groups_pending_ && !errors_pending_) return;
+  std::int32_t scal[3] = {0, 0, 0};
+  check(cudaMemcpyAsync(scal, scalars.get(), sizeof(scal), cudaMemcpyDeviceToHost, s), "D2H scalars");
+  check(cudaStreamSynchronize(s), "sync");
+  const bool check_err = errors_pending_;
+  groups_pending_ = errors_pending_ = false;
+  groups = scal[2];
+  steps = scal[0] + 1;
+  if (check_err && scal[1]) throw_error(Errc::invalid_program, "cycle or unreachable node");
+}
+
+void DeviceProgramBatch::check_scheduler_error(cudaStream_t s) const { resolve(s); }
+
 std::int64_t DeviceProgramBatch::group_count(cudaStream_t s) const {
-  if (groups_pending_) {
-    std::int32_t g = 0;
-    check(cudaMemcpyAsync(&g, scalars.get() + 2, sizeof(g), cudaMemcpyDeviceToHost, s), "D2H groups");
-    check(cudaStreamSynchronize(s), "sync");
-    groups = g;
-    groups_pending_ = false;
-  }
+  resolve(s);
   return groups;
 }
 
@@ -390,7 +408,7 @@ void IepSession::forward() {
   check(cudaMemsetAsync(present_.get(), 0, present_.size() * sizeof(std::int32_t), stream_), "memset present");
   if (!host_schedule_) {
     prof_.begin(0, stream_);
-    batch_->run_scheduler(stream_);
+    batch_->run_scheduler(stream_, kind_ == ModuleKind::resblock);  // resblock: no host sync
     prof_.end(stream_);
     launches_ += 4;  // labels, histogram, scan, scatter
   }
@@ -475,6 +493,7 @@ void IepSession::forward_dense() {
 }
 
 void IepSession::check_errors() {
+  batch_->check_scheduler_error(stream_);
   std::int32_t e = 0;
   check(cudaMemcpyAsync(&e, err_.get(), sizeof(e), cudaMemcpyDeviceToHost, stream_), "D2H err");
   check(cudaStreamSynchronize(stream_), "sync");
@@ -489,6 +508,7 @@ void IepSession::check_errors() {
 
 void IepSession::synchronize() {
   check(cudaStreamSynchronize(stream_), "sync");
+  sync_pipeline();
   check_errors();
 }
 

@@ -114,8 +114,10 @@ class DeviceProgramBatch {
   DeviceProgramBatch(const HostCSR& csr, cudaStream_t s);
   const HostCSR& csr() const { return csr_; }
 
-  // Device improved scheduler; returns the step count (one small D2H).
-  int run_scheduler(cudaStream_t s);
+  // Device improved scheduler; returns the step count (one small D2H), or,
+  // with upper_bound, s_max without a host sync (empty trailing steps).
+  int run_scheduler(cudaStream_t s, bool upper_bound = false);
+  void check_scheduler_error(cudaStream_t s) const;
   // Installs a host-built schedule in the same table format.
   int load_schedule(const Schedule& schedule, cudaStream_t s);
   Schedule download_schedule(Strategy strategy, cudaStream_t s) const;
@@ -127,7 +129,9 @@ class DeviceProgramBatch {
   std::int64_t group_count(cudaStream_t s) const;
   bool static_shape() const { return shape_n_ > 0; }
 
-  int steps = 0;
+  void resolve(cudaStream_t s) const;
+
+  mutable int steps = 0;
   mutable std::int64_t groups = 0;
   Buf<std::int32_t> prog_off, fid, child_off, child_list, child0, child1, example, root_g;
   Buf<std::int32_t> arity_of, labels, scratch, scalars, seg_hist;
@@ -138,6 +142,7 @@ class DeviceProgramBatch {
   HostCSR csr_;
   int max_keys_ = 0;
   mutable bool groups_pending_ = false;
+  mutable bool errors_pending_ = false;
   int shape_n_ = 0, shape_dmax_ = 0;  // programs share one tree shape (static schedule)
   Buf<std::int32_t> shape_labels_;
 };
@@ -153,6 +158,8 @@ class IepSession {
   void set_schedule(const Schedule* schedule);
   void forward();
   void forward_host(const float* inputs, float* outputs);
+  void forward_host_async(const float* inputs, float* outputs);
+  void sync_pipeline();
   void synchronize();
   cudaStream_t stream() const { return stream_; }
 

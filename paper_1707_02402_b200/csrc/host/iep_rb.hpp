@@ -1,7 +1,9 @@
 // iep_rb.hpp — device state of the Tier-B residual-block IEP path.
 #pragma once
 
+#include <array>
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "device.hpp"
@@ -30,6 +32,27 @@ struct IepSession::RB {
   std::int64_t task_cap = 0;
   Buf<std::int32_t> done0, done1, queue;  // fused step kernel: tile done flags, claim counters
   std::int32_t epoch = 0;                 // forward counter stamped into the done flags
+  // forward_host_async: copy streams, double-buffered CHW rows, events
+  struct Pipe {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    Buf<float> in[2], out[2];
+    cudaEvent_t h2d_done[2] = {}, in_free[2] = {}, out_ready[2] = {}, out_free[2] = {};
+    std::uint64_t calls = 0;
+    // DYNBATCH_PIPE_TRACE: timing events per call (h2d start/end, main
+    // start/forward end, d2h start/end), printed by sync_pipeline()
+    bool trace = false;
+    std::vector<std::array<cudaEvent_t, 6>> tev;
+    ~Pipe() {
+      if (h2d) cudaStreamSynchronize(h2d);
+      if (d2h) cudaStreamSynchronize(d2h);
+      for (int k = 0; k < 2; ++k)
+        for (cudaEvent_t e : {h2d_done[k], in_free[k], out_ready[k], out_free[k]})
+          if (e) cudaEventDestroy(e);
+      if (h2d) cudaStreamDestroy(h2d);
+      if (d2h) cudaStreamDestroy(d2h);
+    }
+  };
+  std::unique_ptr<Pipe> pipe;
   std::int64_t n_expensive = 0;
   std::int64_t n_shared = 0;  // expensive children with several parents (gathered per step)
   int tile_m = kTileM;  // positions per scheduled tile

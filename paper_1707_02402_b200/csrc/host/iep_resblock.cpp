@@ -2,6 +2,7 @@
 // weight packing for the tcgen05 kernels, buffer sizing and the per-step
 // launch sequence  plan → [gather → conv1x1 → conv3x3#1 → conv3x3#2]×steps.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -269,6 +270,91 @@ void IepSession::forward_host(const float* inputs, float* outputs) {
   forward();
   download_resblock_outputs(outputs);
   check_errors();
+}
+
+void IepSession::sync_pipeline() {
+  if (!rb_ || !rb_->pipe) return;
+  RB::Pipe& Q = *rb_->pipe;
+  check(cudaStreamSynchronize(Q.h2d), "sync h2d");
+  check(cudaStreamSynchronize(Q.d2h), "sync d2h");
+  if (Q.trace && !Q.tev.empty()) {
+    const cudaEvent_t base = Q.tev.front()[0];
+    for (size_t c = 0; c < Q.tev.size(); ++c) {
+      float t[6] = {-1, -1, -1, -1, -1, -1};
+      for (int i = 0; i < 6; ++i) {
+        const cudaError_t err = cudaEventElapsedTime(&t[i], base, Q.tev[c][static_cast<size_t>(i)]);
+        if (err != cudaSuccess) {
+          t[i] = -1;
+          cudaGetLastError();
+        }
+      }
+      std::fprintf(stderr, "call %zu: h2d %.2f-%.2f  main %.2f-%.2f  d2h %.2f-%.2f ms\n", c, t[0], t[1], t[2], t[3],
+                   t[4], t[5]);
+    }
+    for (auto& te : Q.tev)
+      for (auto e : te) cudaEventDestroy(e);
+    Q.tev.clear();
+    Q.trace = false;
+  }
+}
+
+// Pipelined end-to-end call: the H2D of this call's inputs and the D2H of
+// its outputs run on their own streams into double-buffered device rows, so
+// consecutive calls overlap upload(N+1) and download(N−1) with forward(N)
+// (PCIe is full duplex). Ordering is by events only; synchronize() waits for
+// everything. Host buffers must stay valid (and should be pinned) until then.
+void IepSession::forward_host_async(const float* inputs, float* outputs) {
+  if (kind_ != ModuleKind::resblock) throw_error(Errc::invalid_argument, "forward_host needs a resblock session");
+  RB& R = *rb_;
+  DeviceProgramBatch& B = *batch_;
+  const std::int64_t b = B.csr().b;
+  const size_t bytes = sizeof(float) * static_cast<size_t>(b) * RB::kFmap;
+  if (!R.pipe) {
+    R.pipe = std::make_unique<RB::Pipe>();
+    RB::Pipe& Q = *R.pipe;
+    check(cudaStreamCreateWithFlags(&Q.h2d, cudaStreamNonBlocking), "stream");
+    check(cudaStreamCreateWithFlags(&Q.d2h, cudaStreamNonBlocking), "stream");
+    for (int k = 0; k < 2; ++k) {
+      Q.in[k].alloc(static_cast<size_t>(b) * RB::kFmap);
+      Q.out[k].alloc(static_cast<size_t>(b) * RB::kFmap);
+      for (cudaEvent_t* e : {&Q.h2d_done[k], &Q.in_free[k], &Q.out_ready[k], &Q.out_free[k]}) {
+        check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+        check(cudaEventRecord(*e, stream_), "event");
+      }
+    }
+  }
+  RB::Pipe& Q = *R.pipe;
+  const int k = static_cast<int>(Q.calls++ & 1);
+  std::array<cudaEvent_t, 6> te{};
+  if (Q.trace || std::getenv("DYNBATCH_PIPE_TRACE")) {
+    Q.trace = true;
+    for (auto& e : te) check(cudaEventCreate(&e), "event");
+    Q.tev.push_back(te);
+  }
+  auto mark = [&](int i, cudaStream_t st) {
+    if (Q.trace) check(cudaEventRecord(te[static_cast<size_t>(i)], st), "event");
+  };
+  check(cudaStreamWaitEvent(Q.h2d, Q.in_free[k]), "wait");
+  mark(0, Q.h2d);
+  check(cudaMemcpyAsync(Q.in[k].get(), inputs, bytes, cudaMemcpyHostToDevice, Q.h2d), "H2D inputs");
+  mark(1, Q.h2d);
+  check(cudaEventRecord(Q.h2d_done[k], Q.h2d), "event");
+  check(cudaStreamWaitEvent(stream_, Q.h2d_done[k]), "wait");
+  mark(2, stream_);
+  check(dbk_rb_inputs_from_chw(b, Q.in[k].get(), R.inputs.get(), stream_), "inputs layout");
+  check(cudaEventRecord(Q.in_free[k], stream_), "event");
+  forward();
+  mark(3, stream_);
+  check(cudaStreamWaitEvent(stream_, Q.out_free[k]), "wait");
+  check(dbk_rb_outputs_to_chw(b, B.root_g.get(), B.fid.get(), B.arity_of.get(), B.example.get(), R.inputs.get(),
+                              R.values.get(), Q.out[k].get(), stream_),
+        "outputs layout");
+  check(cudaEventRecord(Q.out_ready[k], stream_), "event");
+  check(cudaStreamWaitEvent(Q.d2h, Q.out_ready[k]), "wait");
+  mark(4, Q.d2h);
+  check(cudaMemcpyAsync(outputs, Q.out[k].get(), bytes, cudaMemcpyDeviceToHost, Q.d2h), "D2H outputs");
+  mark(5, Q.d2h);
+  check(cudaEventRecord(Q.out_free[k], Q.d2h), "event");
 }
 
 }  // namespace dynbatch::dev

@@ -178,7 +178,7 @@ __global__ void k_scan_groups(int64_t n, int32_t nseg, int32_t p, int32_t* __res
                               int32_t* __restrict__ scal, int32_t fixed_keys,
                               int32_t* __restrict__ group_fid, int32_t* __restrict__ group_begin,
                               int32_t* __restrict__ step_group_begin,
-                              int32_t* __restrict__ offsets) {
+                              int32_t* __restrict__ offsets, int32_t steps_cap = 0) {
   __shared__ int32_t warp_tot[32];
   __shared__ int32_t carry_s;
   const int32_t n_keys = fixed_keys > 0 ? fixed_keys : (scal[0] + 1) * p;
@@ -235,7 +235,9 @@ __global__ void k_scan_groups(int64_t n, int32_t nseg, int32_t p, int32_t* __res
   if (tid == 0) {
     const int32_t G = carry_s;
     group_begin[G] = static_cast<int32_t>(n);
-    step_group_begin[n_keys / p] = G;
+    // steps [d_max + 1, steps_cap] are empty (the host may launch per-step
+    // work for an upper bound of the step count without reading d_max)
+    for (int32_t st = n_keys / p; st <= max(steps_cap, n_keys / p); ++st) step_group_begin[st] = G;
     scal[2] = G;
   }
 }
@@ -309,7 +311,7 @@ extern "C" int dbk_sched_labels_static(int64_t N, int32_t n, const int32_t* tabl
 extern "C" int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, const int32_t* fid,
                                      const int32_t* labels, int32_t* dev_scalars,
                                      int32_t* seg_hist, int32_t* member_g, int32_t* group_fid,
-                                     int32_t* group_begin, int32_t* step_group_begin,
+                                     int32_t* group_begin, int32_t* step_group_begin, int32_t steps_cap,
                                      void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int32_t nseg = n_segments(N);
@@ -324,7 +326,7 @@ extern "C" int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, con
   k_scan_totals<<<1, 1024, 0, s>>>(ns, p, dev_scalars, 0, totals);
   k_scan_add<<<sblk, 1024, 0, s>>>(ns, p, dev_scalars, 0, seg_hist, totals);
   k_scan_groups<<<1, 1024, 0, s>>>(N, ns, p, seg_hist, dev_scalars, 0, group_fid,
-                                   group_begin, step_group_begin, nullptr);
+                                   group_begin, step_group_begin, nullptr, steps_cap);
   if (nseg > 0) k_seg_scatter<<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist, member_g);
   return static_cast<int>(cudaGetLastError());
 }

@@ -99,3 +99,24 @@ def test_resblock_forward_host_end_to_end():
     s.forward_host(x, out)
     ref = _oracle("chain", 6, 10, 4, 6, 0.4, 1, 77)
     _check(out.astype(np.float64), ref.outputs)
+
+
+def test_resblock_forward_host_async_pipeline_equals_sync_calls():
+    """Pipelined calls (copy streams, double-buffered rows) with different
+    inputs each give exactly the synchronous call's outputs."""
+    batch = db.Batch.generate("chain", batch=12, vocab=10, width=F, length=6, branch_prob=0.4,
+                              seed=2)
+    s = db.IepSession(batch, 78, db.MODULE_RESBLOCK)
+    rng = np.random.default_rng(5)
+    n = 5
+    xs = [db.PinnedArray((12, F), np.float32) for _ in range(n)]
+    outs = [db.PinnedArray((12, F), np.float32) for _ in range(n)]
+    for x in xs:
+        x.array[:] = rng.uniform(-1, 1, size=(12, F)).astype(np.float32)
+    for x, o in zip(xs, outs):
+        s.forward_host_async(x.array, o.array)
+    s.synchronize()
+    want = np.zeros((12, F), np.float32)
+    for x, o in zip(xs, outs):
+        s.forward_host(x.array, want)
+        assert np.array_equal(o.array, want)
