@@ -34,23 +34,19 @@ __global__ void k_topk(int64_t T, int32_t n, int32_t k, const double* __restrict
   if (t >= T) return;
   const double* row = scores + t * n;
   double* my_sel = sel_v + static_cast<int64_t>(warp) * k;
-  // Non-finite scores are rejected before any ranking (src/moe.cpp:41).
-  bool bad = false;
-  for (int32_t j = lane; j < n; j += 32) bad |= !isfinite(row[j]);
-  if (__any_sync(0xffffffffu, bad)) {
-    if (lane == 0) atomicCAS(err, 0, 9);
-    return;
-  }
   double thr_v = INFINITY;
   int thr_i = -1;  // items must rank strictly after (thr_v, thr_i)
   int32_t taken = 0;
+  bool first = true;
   while (taken < k) {
     double lv[kLocal];
     int li[kLocal];
 #pragma unroll
     for (int q = 0; q < kLocal; ++q) { lv[q] = -INFINITY; li[q] = 0x7fffffff; }
+    bool bad = false;
     for (int32_t j = lane; j < n; j += 32) {
-      const double v = row[j];
+      const double v = __ldg(row + j);
+      bad |= !isfinite(v);
       if (thr_i >= 0 && !ranks_before(thr_v, thr_i, v, j)) continue;
       if (!ranks_before(v, j, lv[kLocal - 1], li[kLocal - 1])) continue;
       // insertion into the lane's sorted candidate list
@@ -65,6 +61,13 @@ __global__ void k_topk(int64_t T, int32_t n, int32_t k, const double* __restrict
         }
       }
     }
+    // Non-finite scores are rejected before any result is written
+    // (src/moe.cpp:41); the first pass reads every score.
+    if (first && __any_sync(0xffffffffu, bad)) {
+      if (lane == 0) atomicCAS(err, 0, 9);
+      return;
+    }
+    first = false;
     const int32_t rounds = min(kLocal, k - taken);
     int head = 0;
     for (int32_t r = 0; r < rounds; ++r) {
@@ -94,11 +97,73 @@ __global__ void k_topk(int64_t T, int32_t n, int32_t k, const double* __restrict
     taken += rounds;
   }
   __syncwarp();
-  if (lane == 0) {
-    const double top = my_sel[0];
-    double denom = 0.0;
-    for (int32_t r = 0; r < k; ++r) denom += exp(my_sel[r] - top);
-    for (int32_t r = 0; r < k; ++r) weights[t * k + r] = exp(my_sel[r] - top) / denom;
+  // weight_r = exp(s_r − s_0) / Σ_{j<k} exp(s_j − s_0), the denominator
+  // summed in rank order as the reference does; the exps run in parallel
+  // (lane r holds rank r, chunks of 32 for k > 32).
+  const double top = my_sel[0];
+  double denom = 0.0;
+  for (int32_t base = 0; base < k; base += 32) {
+    const double e = base + lane < k ? exp(my_sel[base + lane] - top) : 0.0;
+    const int32_t m = min(32, k - base);
+    for (int32_t r = 0; r < m; ++r) denom += __shfl_sync(0xffffffffu, e, r);
+  }
+  for (int32_t r = lane; r < k; r += 32) weights[t * k + r] = exp(my_sel[r] - top) / denom;
+}
+
+// Small gates (n ≤ 128 even, k ≤ 8): one thread per token, reading its own
+// score row with 16-byte loads (eight in flight per 16-score chunk) and
+// keeping its top-k in registers in the reference's rank order; the weights
+// use the denominator summed in rank order. Non-finite scores are rejected
+// before anything is written (src/moe.cpp:41).
+template <int K>
+__global__ void __launch_bounds__(128) k_topk_small(int64_t T, int32_t n, const double* __restrict__ scores,
+                                                    int32_t* __restrict__ ids, double* __restrict__ weights,
+                                                    int32_t* __restrict__ err) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool live = t < T;
+  const double2* row = reinterpret_cast<const double2*>(scores + (live ? t : 0) * n);
+  double tv[K];
+  int ti[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) { tv[q] = -INFINITY; ti[q] = 0x7fffffff; }
+  bool bad = false;
+  for (int32_t j0 = 0; j0 < n; j0 += 16) {
+    double2 c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) c[u] = j0 + 2 * u < n ? __ldg(row + j0 / 2 + u) : make_double2(-INFINITY, -INFINITY);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int32_t j = j0 + u;
+      if (j >= n) break;
+      double cv = (u & 1) ? c[u >> 1].y : c[u >> 1].x;
+      bad |= !isfinite(cv);
+      int ci = j;
+      if (!ranks_before(cv, ci, tv[K - 1], ti[K - 1])) continue;
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        if (ranks_before(cv, ci, tv[q], ti[q])) {
+          const double sv = tv[q];
+          const int si = ti[q];
+          tv[q] = cv; ti[q] = ci; cv = sv; ci = si;
+        }
+      }
+    }
+  }
+  if (__syncthreads_or(live && bad)) {
+    if (threadIdx.x == 0) atomicCAS(err, 0, 9);
+    return;
+  }
+  if (!live) return;
+  double e[K], denom = 0.0;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    e[q] = exp(tv[q] - tv[0]);
+    denom += e[q];
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    ids[t * K + q] = ti[q];
+    weights[t * K + q] = e[q] / denom;
   }
 }
 
@@ -203,9 +268,27 @@ __global__ void k_combine_fp64(int64_t T, int32_t k, int32_t d, const double* __
 
 }  // namespace
 
+template <int K>
+int launch_topk_small(int64_t T, int32_t n, const double* scores, int32_t* ids, double* weights, int32_t* err,
+                      cudaStream_t s) {
+  k_topk_small<K><<<static_cast<unsigned>((T + 127) / 128), 128, 0, s>>>(T, n, scores, ids, weights, err);
+  return static_cast<int>(cudaGetLastError());
+}
+
 extern "C" int dbk_moe_topk(int64_t T, int32_t n, int32_t k, const double* scores, int32_t* ids,
                             double* weights, int32_t* err, void* stream) {
   if (T <= 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n <= 128 && n % 2 == 0 && k <= n) {
+    switch (k) {
+      case 1: return launch_topk_small<1>(T, n, scores, ids, weights, err, st);
+      case 2: return launch_topk_small<2>(T, n, scores, ids, weights, err, st);
+      case 3: return launch_topk_small<3>(T, n, scores, ids, weights, err, st);
+      case 4: return launch_topk_small<4>(T, n, scores, ids, weights, err, st);
+      case 8: return launch_topk_small<8>(T, n, scores, ids, weights, err, st);
+      default: break;
+    }
+  }
   const int warps = 8;
   const size_t smem = sizeof(double) * static_cast<size_t>(warps) * k;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

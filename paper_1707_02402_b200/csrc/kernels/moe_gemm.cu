@@ -34,25 +34,51 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + kEpiWarps * 32;
 constexpr int kSmem = kStages * (kABytes + kBBytes) + 256;
 
-// padded starts and (expert, row block) tile list; single block.
-__global__ void k_moe_layout(int32_t n, const int32_t* __restrict__ offsets, int32_t* __restrict__ pstart,
-                             int32_t* __restrict__ tile_expert, int32_t* __restrict__ tile_rb,
-                             int32_t* __restrict__ n_tiles) {
-  if (threadIdx.x != 0) return;
-  int32_t rows_acc = 0, t = 0;
-  for (int32_t e = 0; e < n; ++e) {
-    pstart[e] = rows_acc;
-    const int32_t rows = offsets[e + 1] - offsets[e];
-    const int32_t nb = (rows + kBM - 1) / kBM;
-    for (int32_t b = 0; b < nb; ++b) {
-      tile_expert[t] = e;
-      tile_rb[t] = rows_acc / kBM + b;
-      ++t;
+// Padded starts and the (expert, row block) tile list: one thread per
+// expert, a block-wide scan of the row blocks (single block, n ≤ 1024 × k).
+__global__ void __launch_bounds__(1024) k_moe_layout(int32_t n, const int32_t* __restrict__ offsets,
+                                                     int32_t* __restrict__ pstart, int32_t* __restrict__ tile_expert,
+                                                     int32_t* __restrict__ tile_rb, int32_t* __restrict__ n_tiles) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int32_t base = 0; base < n; base += blockDim.x) {
+    const int32_t e = base + static_cast<int32_t>(threadIdx.x);
+    const int32_t nb = e < n ? (offsets[e + 1] - offsets[e] + kBM - 1) / kBM : 0;
+    int32_t x = nb;  // inclusive warp scan, then across warps
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    rows_acc += nb * kBM;
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int32_t first = carry + (warp > 0 ? wsum[warp - 1] : 0) + x - nb;  // exclusive prefix (row blocks)
+    if (e < n) {
+      pstart[e] = first * kBM;
+      for (int32_t b = 0; b < nb; ++b) {
+        tile_expert[first + b] = e;
+        tile_rb[first + b] = first + b;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = first + nb;
+    __syncthreads();
   }
-  pstart[n] = rows_acc;
-  *n_tiles = t;
+  if (threadIdx.x == 0) {
+    pstart[n] = carry * kBM;
+    *n_tiles = carry;
+  }
 }
 
 // One warp per padded row: row r of expert e holds item order[off_e + r]
@@ -280,7 +306,7 @@ int launch_gemm(const GemmParams& p, int sms, cudaStream_t s) {
 
 extern "C" int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int32_t* tile_expert,
                                    int32_t* tile_rb, int32_t* n_tiles, void* stream) {
-  k_moe_layout<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(n, offsets, pstart, tile_expert, tile_rb, n_tiles);
+  k_moe_layout<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, offsets, pstart, tile_expert, tile_rb, n_tiles);
   return static_cast<int>(cudaGetLastError());
 }
 
