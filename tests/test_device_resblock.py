@@ -120,3 +120,39 @@ def test_resblock_forward_host_async_pipeline_equals_sync_calls():
     for x, o in zip(xs, outs):
         s.forward_host(x.array, want)
         assert np.array_equal(o.array, want)
+
+
+def test_cfg3_full_size_properties():
+    """BASELINE configs[2] at its full per-GPU size (4096 chain programs,
+    p = 40, 128×14×14 maps): the device schedule is bit-exact with the
+    oracle's schedule_improved, a sample of rows run alone reproduce their
+    in-batch outputs bit for bit (every position runs the same MMA chain),
+    the outputs are finite, and a row checked against the fp64 oracle meets
+    the stated tolerance."""
+    import bench
+    cfg = bench.CFG["cfg3"]
+    b = db.Batch.generate(cfg["kind"], batch=cfg["per_gpu"], vocab=cfg["vocab"], width=F, depth=cfg["depth"],
+                          length=cfg["length"], branch_prob=cfg["branch_prob"], seed=0)
+    sess = db.IepSession(b, 1234, db.MODULE_RESBLOCK)
+    sess.forward()
+    sess.synchronize()
+    ob = O.gen_batch(cfg["kind"], cfg["per_gpu"], p=cfg["vocab"], depth=cfg["depth"], length=cfg["length"],
+                     bp=cfg["branch_prob"], seed=0)
+    from test_device_iep import _flat_from_json
+    assert _flat_from_json(sess.schedule().to_json()) == O.schedule_improved(ob)
+    full = sess.run().outputs()
+    assert np.isfinite(full).all()
+    for r in (0, 1234, 4095):
+        one = db.IepSession(b, 1234, db.MODULE_RESBLOCK, first=r, last=r + 1)
+        one.forward()
+        assert np.array_equal(one.run().outputs()[0], full[r])
+    # one row against the fp64 oracle (its own program, same module seed)
+    r = 1234
+    sub = db.Batch.generate_range(r, r + 1, cfg["kind"], batch=cfg["per_gpu"], vocab=cfg["vocab"], width=F,
+                                  depth=cfg["depth"], length=cfg["length"], branch_prob=cfg["branch_prob"], seed=0)
+    x = sub.inputs()
+    obs = O.Batch(ob.prog_off[r:r + 2] - ob.prog_off[r], ob.fid[ob.prog_off[r]:ob.prog_off[r + 1]],
+                  ob.child0[ob.prog_off[r]:ob.prog_off[r + 1]], ob.child1[ob.prog_off[r]:ob.prog_off[r + 1]],
+                  ob.root[r:r + 1], ob.p)
+    ref = O.execute(obs, O.schedule_improved(obs), x, 1234, "resblock").outputs
+    _check(full[r:r + 1], ref)
