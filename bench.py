@@ -260,14 +260,17 @@ def run_ours(args, dist):
         sess.forward_host_async(xin[i % 2].array, xout[i % 2].array)
     sess.synchronize()
     dist.barrier()
+    e2e_steps = max(args.steps, 20)  # amortises the pipeline fill and drain
     t0 = time.perf_counter()
-    for i in range(args.steps):
+    for i in range(e2e_steps):
         sess.forward_host_async(xin[i % 2].array, xout[i % 2].array)
     sess.synchronize()
-    e2e_s = dist.max((time.perf_counter() - t0) / args.steps)
+    e2e_s = dist.max((time.perf_counter() - t0) / e2e_steps)
     e2e = {"value": per * N / e2e_s, "unit": "programs/s",
            "h2d_bytes_per_step": per * F * 4, "d2h_bytes_per_step": per * F * 4,
-           "ms_per_step": e2e_s * 1e3}
+           "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
+           "api": "db_iep_session_forward_host_async (pinned fp32 CHW rows in, root rows out; copies overlap "
+                  "the neighbouring steps' forwards)"}
 
     # roofline of the dominant kernel: the fused conv step (conv1x1 + conv3x3
     # #1 + conv3x3 #2 with the residual on the tensor cores), class 4
