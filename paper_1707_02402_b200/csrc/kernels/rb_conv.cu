@@ -161,8 +161,8 @@ __device__ unsigned long long g_conv_dbg[6 * 4];
 // ------------------------------------------------------------ K phases
 // A tile's K loop is one to three phases of (window source, weights, chunks,
 // taps, halo): conv1x1 [x; y] (4 chunks × 1 tap); conv3x3 #1 over x
-// (2 × 9, halo 16); conv3x3 #2 over mid (2 × 9, halo 16) + I·hi + I·lo
-// (2 × 1 each, no halo).
+// (2 × 9, halo 16); conv3x3 #2: I·hi + I·lo (2 × 1 each, no halo), then
+// W2 over mid (2 × 9, halo 16).
 struct Phase {
   const uint8_t* src;  // staging base (position 0 of plane 0)
   const uint8_t* w;    // weight blocks
@@ -175,8 +175,11 @@ __device__ __forceinline__ Phase phase_of(const StepParams& P, const Item& it, i
   const int32_t f = P.group_fid[it.g];
   if (it.kind == 0) return Phase{P.stage_cat, P.wpack[0][f], 4, 1, 0};
   if (it.kind == 1) return Phase{P.stage_x, P.wpack[1][f], 2, 9, kHalo};
-  if (p == 0) return Phase{P.stage_mid, P.wpack[2][f], 2, 9, kHalo};
-  return Phase{p == 1 ? P.stage_x : P.stage_lo, P.ident, 2, 1, 0};
+  // conv3x3 #2: the residual phases first — they read this block's input
+  // images, which this launch's conv3x3 #1 tiles do not write, so they load
+  // and run while the producer waits for the mid tiles
+  if (p == 2) return Phase{P.stage_mid, P.wpack[2][f], 2, 9, kHalo};
+  return Phase{p == 0 ? P.stage_x : P.stage_lo, P.ident, 2, 1, 0};
 }
 
 // ------------------------------------------------------- work queue
@@ -224,7 +227,7 @@ __device__ __forceinline__ Item step_item(const StepParams& P, int32_t k, int32_
 // a binary group reads z (conv1x1 tiles i-1..i+1); conv3x3 #2 reads mid
 // (conv3x3 #1 tiles i-1..i+1) and, for a binary group, z hi/lo (conv1x1
 // tile i). Halo positions in other segments only feed outputs never stored.
-__device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& it) {
+__device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& it, int phase) {
   if (it.kind == 0) return;
   const int32_t g = it.g;
   const int32_t rows = P.group_begin[g + 1] - P.group_begin[g];
@@ -235,10 +238,12 @@ __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& 
   if (it.kind == 1) {
     if (!binary) return;
     for (int32_t j = max(i - 1, 0); j <= min(i + 1, nt - 1); ++j) wait_flag(P.done0 + b0 + j, P.epoch);
-  } else {
+  } else if (phase == 0) {  // conv3x3 #2, residual phases: z hi/lo of a binary group
+    if (!binary) return;
+    wait_flag(P.done0 + b0 + i, P.epoch);
+  } else {  // conv3x3 #2, W2 phase: mid of tiles i-1..i+1
     const int32_t t0 = P.step_tile_begin[P.step] + P.group_tile0[g];
     for (int32_t j = max(i - 1, 0); j <= min(i + 1, nt - 1); ++j) wait_flag(P.done1 + t0 + j, P.epoch);
-    if (binary) wait_flag(P.done0 + b0 + i, P.epoch);
   }
   fence_proxy_async_global();
 }
@@ -454,10 +459,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         items[slot] = it;
         mbar_arrive(item_full + slot);
         if (it.kind < 0) break;
-        if (DBG) c0 = clock64();
-        step_wait_deps(P, it);
-        if (DBG) w_dep += clock64() - c0;
         for (int p = 0; p < n_phases(it.kind); ++p) {
+          if (p == 0 || p == 2) {  // conv3x3 #2 waits for the mid tiles only before its W2 phase
+            if (DBG) c0 = clock64();
+            step_wait_deps(P, it, p);
+            if (DBG) w_dep += clock64() - c0;
+          }
           const Phase ph = phase_of(P, it, p);
           const uint32_t rows = kTileM + 2 * ph.halo;
           const uint8_t* src = ph.src + (static_cast<int64_t>(kGuard + it.q0 - ph.halo) << 7);
@@ -503,8 +510,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         uint32_t acc = 0;
         for (int p = 0; p < n_phases(it.kind); ++p) {
           const int chunks = it.kind == 0 ? 4 : 2;
-          const int taps = (it.kind == 0 || p > 0) ? 1 : 9;
-          const int halo = (it.kind == 0 || p > 0) ? 0 : kHalo;
+          const bool conv3 = it.kind == 1 || (it.kind == 2 && p == 2);
+          const int taps = conv3 ? 9 : 1;
+          const int halo = conv3 ? kHalo : 0;
           for (int ch = 0; ch < chunks; ++ch, ++ai) {
             const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
             if (DBG) c0 = clock64();
