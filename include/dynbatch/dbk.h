@@ -46,6 +46,17 @@ int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, const int32_t*
                           int32_t* member_g, int32_t* group_fid, int32_t* group_begin,
                           int32_t* step_group_begin, int32_t steps_cap, void* stream);
 
+/* build_program_from_prefix (src/program.cpp:95-142) for b concatenated
+ * prefix sequences (tokens, seq_off[b+1]), one thread per program: writes
+ * the CSR (prog_off, fid, child_off[N+1], child_list, child0/1, example,
+ * root_g) and fwd_ok (expensive non-root node). stack: N int2 scratch.
+ * *err (first error wins): 1 empty sequence, 2 unknown function,
+ * 3 underfull, 4 overfull. */
+int dbk_build_prefix(int64_t b, const int32_t* tokens, const int32_t* seq_off, int32_t p, const int32_t* arity_of,
+                     int32_t* prog_off, int32_t* fid, int32_t* child_off, int32_t* child_list, int32_t* child0,
+                     int32_t* child1, int32_t* example, int32_t* root_g, int32_t* fwd_ok, void* stack,
+                     int32_t* err, void* stream);
+
 /* Scratch (int32 count) the bucket sorts need in seg_hist. */
 int64_t dbk_bucket_sort_scratch(int64_t n_items, int32_t max_keys);
 
@@ -112,6 +123,11 @@ int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile_begin, con
                 int64_t plane_stride, const void* const* w0, const void* const* w1, const void* const* w2,
                 const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
                 int32_t* done0, int32_t* done1, int32_t* queue, int32_t num_sms, void* stream);
+/* Zeroes stage_x rows between each segment's last image and its tile end
+ * (read as top / left pads by the next segment's first image), every
+ * forward, so a new layout needs no full re-zeroing. */
+int dbk_rb_zero_gaps(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_begin,
+                     const int32_t* seg_start, void* stage_x, int64_t plane_stride, int32_t tile_m, void* stream);
 /* Per-member epilogue table (32 bytes per member, schedule order: own fp32
  * slot, forwarding target row / buffer, keep-fp32 flag) and the gather task
  * lists (n_tasks[2] counters, reset here; capacity task_cap per list), built

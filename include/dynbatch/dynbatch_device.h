@@ -37,6 +37,12 @@ typedef struct {
   int32_t channels;    /* RESBLOCK: C (must be 128) */
   int32_t height;      /* RESBLOCK: H (must be 14)  */
   int32_t width_px;    /* RESBLOCK: W (must be 14)  */
+  /* Capacity for later db_iep_session_set_programs batches (0: the initial
+   * batch's size): programs, total nodes, longest program. */
+  int64_t program_capacity;
+  int64_t node_capacity;
+  int32_t length_capacity;
+  int32_t reserved;
 } db_module_opts;
 
 /* Session statistics (db_iep_session_stats / db_moe_session_stats). */
@@ -107,6 +113,15 @@ DYNBATCH_API db_status db_iep_session_forward_host(db_iep_session* s, const floa
 DYNBATCH_API db_status db_iep_session_forward_host_async(db_iep_session* s, const float* inputs,
                                                          float* outputs);
 DYNBATCH_API db_status db_iep_session_synchronize(db_iep_session* s);
+/* RESBLOCK sessions: replace the programs by b prefix function sequences
+ * (build_program_from_prefix order; tokens concatenated, seq_off[b+1]),
+ * built into the CSR on the device. Within the session
+ * capacity; an empty sequence is reported at once (DB_ERR_INVALID_ARGUMENT),
+ * the device build's errors (unknown function / underfull / overfull) at the
+ * next synchronize. tokens may be NULL only when seq_off[b] == 0. The next forward uses them; its inputs
+ * are the next …_forward_host(_async) call's rows (b of them). */
+DYNBATCH_API db_status db_iep_session_set_programs(db_iep_session* s, const int32_t* tokens,
+                                                   const int32_t* seq_off, int64_t b);
 DYNBATCH_API void* db_iep_session_stream(db_iep_session* s);
 DYNBATCH_API db_status db_iep_session_stats(db_iep_session* s, db_session_stats_t* out);
 /* Copies the device schedule of the last forward into a host handle. */

@@ -11,6 +11,7 @@ compute path: if the shared library is missing this import fails loudly.
 from __future__ import annotations
 
 import ctypes as C
+import json
 import os
 from dataclasses import dataclass
 
@@ -69,7 +70,8 @@ class VerifyOpts(C.Structure):
 
 class ModuleOpts(C.Structure):
     _fields_ = [("module_kind", C.c_int32), ("channels", C.c_int32), ("height", C.c_int32),
-                ("width_px", C.c_int32)]
+                ("width_px", C.c_int32), ("program_capacity", C.c_int64), ("node_capacity", C.c_int64),
+                ("length_capacity", C.c_int32), ("reserved", C.c_int32)]
 
 
 class SessionStats(C.Structure):
@@ -142,6 +144,7 @@ SIGNATURES = {
     "db_iep_session_forward": (C.c_int32, [VP]),
     "db_iep_session_forward_host": (C.c_int32, [VP, VP, VP]),
     "db_iep_session_forward_host_async": (C.c_int32, [VP, VP, VP]),
+    "db_iep_session_set_programs": (C.c_int32, [VP, VP, VP, C.c_int64]),
     "db_iep_session_synchronize": (C.c_int32, [VP]),
     "db_iep_session_stream": (VP, [VP]),
     "db_iep_session_stats": (C.c_int32, [VP, C.POINTER(SessionStats)]),
@@ -275,6 +278,15 @@ class Batch(_Handle):
             return np.zeros((r.value, w.value))
         return np.ctypeslib.as_array(d, shape=(r.value, w.value)).copy()
 
+    def prefix_tokens(self):
+        """The programs as concatenated prefix function sequences and their
+        offsets (the JSON wire format's programs, src/serialize.cpp:37-80)."""
+        progs = json.loads(self.to_json())["programs"]
+        off = np.zeros(len(progs) + 1, np.int32)
+        off[1:] = np.cumsum([len(p) for p in progs])
+        toks = np.fromiter((f for p in progs for f in p), np.int32, count=int(off[-1]))
+        return toks, off
+
     def schedule(self, strategy="improved") -> "Schedule":
         h = C.c_void_p()
         check(lib().db_schedule_build(self.h, STRATEGY[strategy], C.byref(h)))
@@ -373,9 +385,10 @@ class IepSession(_Handle):
     _free = "db_iep_session_free"
     _time = "db_iep_session_time"
 
-    def __init__(self, batch: Batch, module_seed: int, module_kind=MODULE_DENSE, first=0, last=0):
+    def __init__(self, batch: Batch, module_seed: int, module_kind=MODULE_DENSE, first=0, last=0,
+                 program_capacity=0, node_capacity=0, length_capacity=0):
         h = C.c_void_p()
-        opts = ModuleOpts(module_kind, 128, 14, 14)
+        opts = ModuleOpts(module_kind, 128, 14, 14, program_capacity, node_capacity, length_capacity, 0)
         check(lib().db_iep_session_create(batch.h, first, last, module_seed, C.byref(opts),
                                           C.byref(h)))
         super().__init__(h)
@@ -391,6 +404,13 @@ class IepSession(_Handle):
 
     def set_schedule(self, schedule):
         check(lib().db_iep_session_set_schedule(self.h, schedule.h if schedule else None))
+
+    def set_programs(self, tokens: np.ndarray, seq_off: np.ndarray):
+        """Replace the programs by prefix function sequences (concatenated
+        tokens, offsets[b+1]); the CSR is built on the device."""
+        t = np.ascontiguousarray(tokens, np.int32)
+        o = np.ascontiguousarray(seq_off, np.int32)
+        check(lib().db_iep_session_set_programs(self.h, _ptr(t), _ptr(o), len(o) - 1))
 
     def forward(self):
         check(lib().db_iep_session_forward(self.h))

@@ -449,7 +449,10 @@ db_status db_iep_session_create(const db_batch* batch, int64_t first, int64_t la
     dynbatch::TensorBatch in(last - first, batch->inputs.width());
     std::memcpy(in.data().data(), batch->inputs.data().data() + first * batch->inputs.width(),
                 sizeof(double) * in.data().size());
-    auto s = std::make_unique<dynbatch::dev::IepSession>(batch->vocab, progs, in, module_seed, kind);
+    auto s = std::make_unique<dynbatch::dev::IepSession>(batch->vocab, progs, in, module_seed, kind,
+                                                         opts ? opts->program_capacity : 0,
+                                                         opts ? opts->node_capacity : 0,
+                                                         opts ? opts->length_capacity : 0);
     *out = new db_iep_session{std::move(s)};
   });
 }
@@ -467,6 +470,12 @@ db_status db_iep_session_forward(db_iep_session* s) {
 db_status db_iep_session_forward_host(db_iep_session* s, const float* inputs, float* outputs) {
   if (!s || !inputs || !outputs) return null_arg();
   return guarded([&] { s->s->forward_host(inputs, outputs); });
+}
+
+db_status db_iep_session_set_programs(db_iep_session* s, const int32_t* tokens, const int32_t* seq_off, int64_t b) {
+  // tokens may be NULL for an all-empty batch (reported as the empty-sequence error)
+  if (!s || !seq_off || (!tokens && b > 0 && seq_off[b] > 0)) return null_arg();
+  return guarded([&] { s->s->set_programs(tokens, seq_off, b); });
 }
 
 db_status db_iep_session_forward_host_async(db_iep_session* s, const float* inputs, float* outputs) {

@@ -130,11 +130,24 @@ HostCSR make_csr(std::span<const Program> programs, const FunctionVocab& vocab) 
   }
   c.prog_off.push_back(off);
   c.child_off.push_back(static_cast<std::int32_t>(c.child_list.size()));
+  c.cap_b = c.b;
+  c.cap_N = c.N;
+  c.cap_s = c.s_max;
   return c;
 }
 
 // ------------------------------------------------------ DeviceProgramBatch
 DeviceProgramBatch::DeviceProgramBatch(const HostCSR& csr, cudaStream_t s) : csr_(csr) {
+  const size_t cb = static_cast<size_t>(std::max<std::int64_t>(std::max(csr.cap_b, csr.b), 1));
+  const size_t N = static_cast<size_t>(std::max<std::int64_t>(std::max(csr.cap_N, csr.N), 1));
+  csr_.cap_b = static_cast<std::int64_t>(cb);
+  csr_.cap_N = static_cast<std::int64_t>(N);
+  csr_.cap_s = std::max(csr.cap_s, csr.s_max);
+  prog_off.alloc(cb + 1);
+  root_g.alloc(cb);
+  for (Buf<std::int32_t>* bf : {&fid, &child0, &child1, &example, &fwd_ok}) bf->alloc(N);
+  child_off.alloc(N + 1);
+  child_list.alloc(N);
   prog_off.upload(csr.prog_off, s);
   fid.upload(csr.fid, s);
   child_off.upload(csr.child_off, s);
@@ -144,18 +157,61 @@ DeviceProgramBatch::DeviceProgramBatch(const HostCSR& csr, cudaStream_t s) : csr
   example.upload(csr.example, s);
   root_g.upload(csr.root_g, s);
   arity_of.upload(csr.arity_of, s);
-  const size_t N = static_cast<size_t>(std::max<std::int64_t>(csr.N, 1));
   labels.alloc(N);
   scratch.alloc(2 * N);
   scalars.alloc(8);
   member_g.alloc(N);
   // d_max + 1 <= s_max, so at most s_max * p (step, fid) keys / groups.
-  max_keys_ = std::max(1, csr.s_max) * csr.p;
-  seg_hist.alloc(static_cast<size_t>(dbk_bucket_sort_scratch(csr.N, max_keys_)));
+  max_keys_ = std::max(1, csr_.cap_s) * csr.p;
+  seg_hist.alloc(static_cast<size_t>(dbk_bucket_sort_scratch(static_cast<std::int64_t>(N), max_keys_)));
   group_fid.alloc(static_cast<size_t>(max_keys_) + 1);
   group_begin.alloc(static_cast<size_t>(max_keys_) + 2);
-  step_group_begin.alloc(static_cast<size_t>(std::max(1, csr.s_max)) + 2);
+  step_group_begin.alloc(static_cast<size_t>(std::max(1, csr_.cap_s)) + 2);
   detect_static_shape(s);
+}
+
+void DeviceProgramBatch::set_prefix_programs(const std::int32_t* tokens, const std::int32_t* seq_off,
+                                             std::int64_t b, cudaStream_t s) {
+  if (b <= 0) throw_error(Errc::invalid_argument, "empty program batch");
+  if (b > csr_.cap_b) throw_error(Errc::invalid_argument, "more programs than the session capacity");
+  const std::int64_t N = seq_off[b];
+  int s_max = 0;
+  for (std::int64_t e = 0; e < b; ++e) {
+    const std::int32_t n = seq_off[e + 1] - seq_off[e];
+    if (n < 0) throw_error(Errc::invalid_argument, "sequence offsets must be non-decreasing");
+    if (n == 0) throw_error(Errc::invalid_argument, "empty function sequence");
+    s_max = std::max(s_max, n);
+  }
+  if (N > csr_.cap_N || s_max > csr_.cap_s)
+    throw_error(Errc::invalid_argument, "batch exceeds the session capacity (nodes or program length)");
+  tokens_dev_.ensure(static_cast<size_t>(csr_.cap_N));
+  seq_off_dev_.ensure(static_cast<size_t>(csr_.cap_b) + 1);
+  build_stack_.ensure(static_cast<size_t>(csr_.cap_N));
+  build_err_.ensure(1);
+  check(cudaMemcpyAsync(tokens_dev_.get(), tokens, sizeof(std::int32_t) * static_cast<size_t>(N), cudaMemcpyHostToDevice,
+                        s), "H2D tokens");
+  check(cudaMemcpyAsync(seq_off_dev_.get(), seq_off, sizeof(std::int32_t) * static_cast<size_t>(b + 1),
+                        cudaMemcpyHostToDevice, s), "H2D offsets");
+  check(cudaMemsetAsync(build_err_.get(), 0, sizeof(std::int32_t), s), "memset");
+  check(dbk_build_prefix(b, tokens_dev_.get(), seq_off_dev_.get(), csr_.p, arity_of.get(), prog_off.get(), fid.get(),
+                         child_off.get(), child_list.get(), child0.get(), child1.get(), example.get(), root_g.get(),
+                         fwd_ok.get(), build_stack_.get(), build_err_.get(), s),
+        "dbk_build_prefix");
+  csr_.b = b;
+  csr_.N = N;
+  csr_.s_max = s_max;
+  shape_n_ = 0;  // the static-shape table described the old batch
+  build_pending_ = true;
+  steps = 0;
+}
+
+void DeviceProgramBatch::replace_host_csr(const HostCSR& csr) {
+  const std::int64_t cb = csr_.cap_b, cn = csr_.cap_N;
+  const int cs = csr_.cap_s;
+  csr_ = csr;
+  csr_.cap_b = cb;
+  csr_.cap_N = cn;
+  csr_.cap_s = cs;
 }
 
 // Balanced-tree static schedule (SURVEY.md §3 balanced_static_schedule):
@@ -252,6 +308,19 @@ int DeviceProgramBatch::run_scheduler(cudaStream_t s, bool upper_bound) {
 // when the last forward did not: the real step count replaces the upper
 // bound once the forward is done.
 void DeviceProgramBatch::resolve(cudaStream_t s) const {
+  if (build_pending_) {
+    std::int32_t e = 0;
+    check(cudaMemcpyAsync(&e, build_err_.get(), sizeof(e), cudaMemcpyDeviceToHost, s), "D2H build error");
+    check(cudaStreamSynchronize(s), "sync");
+    build_pending_ = false;
+    switch (e) {
+      case 0: break;
+      case 1: throw_error(Errc::invalid_argument, "empty function sequence");
+      case 2: throw_error(Errc::unknown_function, "a sequence names an unknown function id");
+      case 3: throw_error(Errc::underfull_sequence, "a sequence ends with unfilled arities");
+      default: throw_error(Errc::overfull_sequence, "tokens remain after the root closes");
+    }
+  }
   if (!groups_pending_ && !errors_pending_) return;
   std::int32_t scal[3] = {0, 0, 0};
   check(cudaMemcpyAsync(scal, scalars.get(), sizeof(scal), cudaMemcpyDeviceToHost, s), "D2H scalars");
@@ -348,8 +417,9 @@ ExecutionTrace DeviceProgramBatch::trace_counts(cudaStream_t s) const {
 
 // ------------------------------------------------------------- IepSession
 IepSession::IepSession(const FunctionVocab& vocab, std::span<const Program> programs,
-                       const TensorBatch& inputs, std::uint64_t module_seed, ModuleKind kind)
-    : kind_(kind), width_(vocab.width()) {
+                       const TensorBatch& inputs, std::uint64_t module_seed, ModuleKind kind,
+                       std::int64_t cap_programs, std::int64_t cap_nodes, int cap_length)
+    : kind_(kind), width_(vocab.width()), vocab_(vocab) {
   require_device();
   require_valid_batch(programs, vocab);
   if (inputs.rows() != static_cast<std::int64_t>(programs.size())) {
@@ -361,13 +431,16 @@ IepSession::IepSession(const FunctionVocab& vocab, std::span<const Program> prog
   }
   if (!inputs.all_finite()) throw_error(Errc::non_finite_value, "non-finite input");
   check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
-  const HostCSR csr = make_csr(programs, vocab);
+  HostCSR csr = make_csr(programs, vocab);
+  csr.cap_b = std::max(csr.b, cap_programs);
+  csr.cap_N = std::max(csr.N, cap_nodes);
+  csr.cap_s = std::max(csr.s_max, cap_length);
   batch_ = std::make_unique<DeviceProgramBatch>(csr, stream_);
   err_.alloc(4);
-  present_.alloc(static_cast<size_t>(std::max<std::int64_t>(csr.N, 1)));
+  present_.alloc(static_cast<size_t>(std::max<std::int64_t>(batch_->csr().cap_N, 1)));
   if (kind_ == ModuleKind::dense) {
     in64_.upload(inputs.data().data(), inputs.data().size(), stream_);
-    values64_.alloc(static_cast<size_t>(std::max<std::int64_t>(csr.N, 1)) * static_cast<size_t>(width_));
+    values64_.alloc(static_cast<size_t>(std::max<std::int64_t>(batch_->csr().cap_N, 1)) * static_cast<size_t>(width_));
     out64_.alloc(static_cast<size_t>(std::max<std::int64_t>(csr.b, 1)) * static_cast<size_t>(width_));
     ModuleSet modules(vocab, module_seed);
     std::vector<const double*> wt(static_cast<size_t>(vocab.size()), nullptr), bt = wt;
@@ -420,6 +493,7 @@ void IepSession::forward() {
 // 2·MAC of the module contractions; bytes are the minimum HBM traffic of
 // each kernel (operands read once, results written once).
 void IepSession::add_forward_work() {
+  ensure_host_mirror();
   const HostCSR& c = batch_->csr();
   double n_un = 0, n_bin = 0, dense_flops = 0, dense_bytes = 0;
   for (std::int64_t g = 0; g < c.N; ++g) {
@@ -513,6 +587,8 @@ void IepSession::synchronize() {
 }
 
 Schedule IepSession::download_schedule() {
+  batch_->resolve(stream_);
+  ensure_host_mirror();
   return batch_->download_schedule(strategy_, stream_);
 }
 

@@ -102,6 +102,10 @@ class Profiler {
 struct HostCSR {
   std::int64_t b = 0, N = 0;
   int p = 0, max_arity = 0, s_max = 0;
+  // Allocation capacities (≥ b, N, s_max): a session can take later batches
+  // up to these sizes (IepSession::set_programs).
+  std::int64_t cap_b = 0, cap_N = 0;
+  int cap_s = 0;
   std::vector<std::int32_t> prog_off, fid, child_off, child_list, child0, child1, example, root_g;
   std::vector<std::int32_t> arity_of, expensive_of;
 };
@@ -113,6 +117,14 @@ class DeviceProgramBatch {
  public:
   DeviceProgramBatch(const HostCSR& csr, cudaStream_t s);
   const HostCSR& csr() const { return csr_; }
+
+  // Replaces the programs by b prefix function sequences (host arrays),
+  // built into the CSR on the device (dbk_build_prefix); within capacity.
+  // Build errors surface at the next resolve(). The host CSR arrays go stale
+  // (sizes stay current) until replace_host_csr().
+  void set_prefix_programs(const std::int32_t* tokens, const std::int32_t* seq_off, std::int64_t b, cudaStream_t s);
+  void replace_host_csr(const HostCSR& csr);
+  Buf<std::int32_t> fwd_ok;  // expensive node with one parent (written by the prefix build)
 
   // Device improved scheduler; returns the step count (one small D2H), or,
   // with upper_bound, s_max without a host sync (empty trailing steps).
@@ -143,6 +155,9 @@ class DeviceProgramBatch {
   int max_keys_ = 0;
   mutable bool groups_pending_ = false;
   mutable bool errors_pending_ = false;
+  mutable bool build_pending_ = false;  // a device prefix build's error flag is unread
+  Buf<std::int32_t> tokens_dev_, seq_off_dev_, build_err_;
+  Buf<std::int64_t> build_stack_;
   int shape_n_ = 0, shape_dmax_ = 0;  // programs share one tree shape (static schedule)
   Buf<std::int32_t> shape_labels_;
 };
@@ -151,15 +166,24 @@ enum class ModuleKind { dense = 0, resblock = 1 };
 
 class IepSession {
  public:
+  // cap_* (0: the initial batch's size) bound the batches set_programs accepts.
   IepSession(const FunctionVocab& vocab, std::span<const Program> programs,
-             const TensorBatch& inputs, std::uint64_t module_seed, ModuleKind kind);
+             const TensorBatch& inputs, std::uint64_t module_seed, ModuleKind kind,
+             std::int64_t cap_programs = 0, std::int64_t cap_nodes = 0, int cap_length = 0);
   ~IepSession();
+
+  // Resblock sessions: replace the programs by b prefix function sequences
+  // (concatenated tokens, seq_off[b+1]), built into the CSR on the device;
+  // the next forward schedules and executes them. Inputs come with the next
+  // forward_host / forward_host_async call.
+  void set_programs(const std::int32_t* tokens, const std::int32_t* seq_off, std::int64_t b);
 
   void set_schedule(const Schedule* schedule);
   void forward();
   void forward_host(const float* inputs, float* outputs);
   void forward_host_async(const float* inputs, float* outputs);
   void sync_pipeline();
+  void ensure_host_mirror();  // host CSR arrays of programs set on the device
   void synchronize();
   cudaStream_t stream() const { return stream_; }
 
@@ -178,6 +202,9 @@ class IepSession {
   double time_forwards(int iters, bool profile, KernelTimes* kt);
 
  private:
+  FunctionVocab vocab_;
+  std::vector<std::int32_t> host_tokens_, host_seq_off_;
+  bool mirror_stale_ = false;
   void forward_dense();
   void forward_resblock();
   void check_errors();

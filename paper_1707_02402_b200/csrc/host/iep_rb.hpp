@@ -14,6 +14,7 @@ struct IepSession::RB {
   static constexpr int kFmap = 25088;  // floats per 128×14×14 plane map
   static constexpr int kTileM = 256;
   static constexpr int kGuard = 32;
+  static constexpr int kLead = 16;  // zero rows before each segment's first image (rb_conv.cu)
   std::int64_t plane_stride = 0;  // staging positions per plane
   Buf<float> inputs;              // [b][kFmap] plane maps
   Buf<float> values;              // [N][kFmap] node values (and parked z)

@@ -82,8 +82,10 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   R.tile_m = RB::kTileM;
   for (std::int64_t g = 0; g < c.N; ++g)
     if (c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0) ++R.n_expensive;
-  const size_t b = static_cast<size_t>(std::max<std::int64_t>(c.b, 1));
-  const size_t N = static_cast<size_t>(std::max<std::int64_t>(c.N, 1));
+  // buffers are sized for the session capacity (later set_programs batches)
+  const size_t b = static_cast<size_t>(std::max<std::int64_t>(c.cap_b, 1));
+  const size_t N = static_cast<size_t>(std::max<std::int64_t>(c.cap_N, 1));
+  const std::int64_t n_exp_cap = std::max<std::int64_t>(R.n_expensive, c.cap_N - c.cap_b);  // trees: ≤ N − b
   R.inputs.alloc(b * RB::kFmap);
   R.values.alloc(N * RB::kFmap);
   R.chw_in.alloc(b * RB::kFmap);
@@ -94,9 +96,10 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   check(cudaMemcpyAsync(R.chw_in.get(), tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   check(dbk_rb_inputs_from_chw(c.b, R.chw_in.get(), R.inputs.get(), stream_), "inputs layout");
   // staging: every step owns its range (results are forwarded into their
-  // parent's operand image); ≤ one 256-position alignment gap per group
-  const std::int64_t max_groups = std::min<std::int64_t>(R.n_expensive, static_cast<std::int64_t>(std::max(1, c.s_max)) * c.p);
-  R.plane_stride = RB::kGuard + R.n_expensive * 225 + (max_groups + 2) * R.tile_m + 64;
+  // parent's operand image); per group a kLead-row lead and ≤ one
+  // 256-position alignment gap
+  const std::int64_t max_groups = std::min<std::int64_t>(n_exp_cap, static_cast<std::int64_t>(std::max(1, c.cap_s)) * c.p);
+  R.plane_stride = RB::kGuard + n_exp_cap * 225 + (max_groups + 2) * (R.tile_m + RB::kLead) + 64;
   // forwarding eligibility: expensive nodes with exactly one parent
   {
     std::vector<std::int32_t> parents(static_cast<size_t>(N), 0), ok(static_cast<size_t>(N), 0);
@@ -106,11 +109,12 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
       ok[static_cast<size_t>(g)] = exp && parents[static_cast<size_t>(g)] == 1;
       if (exp && parents[static_cast<size_t>(g)] > 1) R.n_shared += parents[static_cast<size_t>(g)];
     }
+    R.fwd_ok.alloc(N);
     R.fwd_ok.upload(ok, stream_);
     R.fwd_pos.alloc(N);
     R.fwd_slot.alloc(N);
     R.memtab.alloc(N * 4);
-    R.task_cap = static_cast<std::int64_t>(c.child_list.size()) + 1;  // ≤ one task per operand
+    R.task_cap = std::max<std::int64_t>(static_cast<std::int64_t>(c.child_list.size()), c.cap_N) + 1;  // ≤ one task per operand
     R.tasks.alloc(static_cast<size_t>(R.task_cap) * 2 * 4);
     R.n_tasks.alloc(2);
   }
@@ -129,9 +133,9 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
     R.ident.upload(pack_blocks(eye, C, C, 1), stream_);
   }
   // schedule-derived tables (G ≤ max keys; tiles ≤ N_exp·225/256 + G)
-  const size_t G = static_cast<size_t>(std::max(1, c.s_max)) * c.p + 2;
-  const size_t S = static_cast<size_t>(std::max<std::int64_t>(c.N, 1)) + 2;  // naive: S = N
-  const size_t T = static_cast<size_t>(R.n_expensive) * 225 / RB::kTileM + G + 2;
+  const size_t G = static_cast<size_t>(std::max(1, c.cap_s)) * c.p + 2;
+  const size_t S = N + 2;  // naive: S = N
+  const size_t T = static_cast<size_t>(n_exp_cap) * 225 / RB::kTileM + G + 2;
   R.seg_start.alloc(std::max(G, N + 2));
   R.group_tile0.alloc(std::max(G, N + 2));
   R.group_bintile0.alloc(std::max(G, N + 2));
@@ -188,13 +192,10 @@ void IepSession::forward_resblock() {
   const int S = B.steps;
   if (S == 0) return;
   const int sms = sm_count();
-  if (layout_dirty_) {  // a new image layout: pads / gaps must read as zeros
-    R.stage_x.zero(stream_);
-    R.stage_lo.zero(stream_);
-    R.stage_cat.zero(stream_);
-    R.stage_mid.zero(stream_);
-    layout_dirty_ = false;
-  }
+  // Every writer of a staged image writes its pads as zeros and the plan
+  // zeroes the segment gaps, so a new layout (host schedule, set_programs)
+  // needs no re-zeroing of the staging buffers.
+  layout_dirty_ = false;
   prof_.begin(1, stream_);
   check(dbk_rb_plan(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
                     R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(), R.step_tile_begin.get(),
@@ -207,8 +208,11 @@ void IepSession::forward_resblock() {
                       B.child0.get(), B.child1.get(), B.example.get(), R.fwd_ok.get(), R.inputs.get(),
                       R.values.get(), R.memtab.get(), R.tasks.get(), R.n_tasks.get(), R.task_cap, stream_),
         "dbk_rb_memtab");
+  check(dbk_rb_zero_gaps(S, B.step_group_begin.get(), B.group_begin.get(), R.seg_start.get(), R.stage_x.get(),
+                         R.plane_stride, R.tile_m, stream_),
+        "dbk_rb_zero_gaps");
   prof_.end(stream_);
-  launches_ += 5;
+  launches_ += 6;  // plan, tiles, fwd init, fwd, memtab, zero gaps
   const int gather_blocks = sms * 16;  // grid-stride over the step's (member, operand, chunk, pixel) items
   check(cudaMemsetAsync(R.queue.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_), "queue reset");
   ++R.epoch;
@@ -272,6 +276,37 @@ void IepSession::forward_host(const float* inputs, float* outputs) {
   check_errors();
 }
 
+void IepSession::set_programs(const std::int32_t* tokens, const std::int32_t* seq_off, std::int64_t b) {
+  if (kind_ != ModuleKind::resblock) throw_error(Errc::invalid_argument, "set_programs needs a resblock session");
+  RB& R = *rb_;
+  DeviceProgramBatch& B = *batch_;
+  B.set_prefix_programs(tokens, seq_off, b, stream_);
+  const std::int64_t N = B.csr().N;
+  check(cudaMemcpyAsync(R.fwd_ok.get(), B.fwd_ok.get(), sizeof(std::int32_t) * static_cast<size_t>(N),
+                        cudaMemcpyDeviceToDevice, stream_), "fwd_ok");
+  R.n_shared = 0;  // prefix sequences describe trees: no child has two parents
+  host_schedule_ = false;
+  strategy_ = Strategy::improved;
+  host_tokens_.assign(tokens, tokens + N);
+  host_seq_off_.assign(seq_off, seq_off + b + 1);
+  mirror_stale_ = true;
+}
+
+// Host CSR arrays of the programs last set on the device (schedule download,
+// profiling): rebuilt from the host copies of the sequences on demand.
+void IepSession::ensure_host_mirror() {
+  if (!mirror_stale_) return;
+  std::vector<Program> progs;
+  progs.reserve(host_seq_off_.size() - 1);
+  for (size_t e = 0; e + 1 < host_seq_off_.size(); ++e) {
+    const std::span<const int> seq(host_tokens_.data() + host_seq_off_[e],
+                                   static_cast<size_t>(host_seq_off_[e + 1] - host_seq_off_[e]));
+    progs.push_back(build_program_from_prefix(seq, vocab_));
+  }
+  batch_->replace_host_csr(make_csr(progs, vocab_));
+  mirror_stale_ = false;
+}
+
 void IepSession::sync_pipeline() {
   if (!rb_ || !rb_->pipe) return;
   RB::Pipe& Q = *rb_->pipe;
@@ -314,9 +349,10 @@ void IepSession::forward_host_async(const float* inputs, float* outputs) {
     RB::Pipe& Q = *R.pipe;
     check(cudaStreamCreateWithFlags(&Q.h2d, cudaStreamNonBlocking), "stream");
     check(cudaStreamCreateWithFlags(&Q.d2h, cudaStreamNonBlocking), "stream");
+    const size_t rows = static_cast<size_t>(std::max<std::int64_t>(B.csr().cap_b, b));
     for (int k = 0; k < 2; ++k) {
-      Q.in[k].alloc(static_cast<size_t>(b) * RB::kFmap);
-      Q.out[k].alloc(static_cast<size_t>(b) * RB::kFmap);
+      Q.in[k].alloc(rows * RB::kFmap);
+      Q.out[k].alloc(rows * RB::kFmap);
       for (cudaEvent_t* e : {&Q.h2d_done[k], &Q.in_free[k], &Q.out_ready[k], &Q.out_free[k]}) {
         check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
         check(cudaEventRecord(*e, stream_), "event");

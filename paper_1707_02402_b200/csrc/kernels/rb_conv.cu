@@ -74,6 +74,7 @@ constexpr int kFmap = kPlanes * kPx * 8;   // 25,088 floats per node map
 constexpr int kGuard = 32;                 // zero positions before position 0
 constexpr int kTileM = 256;                // positions per CTA tile (MMA N)
 constexpr int kHalo = 16;                  // 3×3 window halo (15 + 1 positions)
+constexpr int kLead = 16;                  // zero rows before a segment's first image (its top / left pads)
 constexpr int kWin = kTileM + 2 * kHalo;   // window rows (row stride of every A slot)
 constexpr int kChunkPlanes = 8;            // K chunk = 64 input channels = 8 planes
 constexpr int kASlot = kWin * 128;         // 36 KB activation window slot (rows of 128 B)
@@ -231,8 +232,8 @@ __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& 
   if (it.kind == 0) return;
   const int32_t g = it.g;
   const int32_t rows = P.group_begin[g + 1] - P.group_begin[g];
-  const int32_t nt = (rows * kImg + kTileM - 1) / kTileM;
-  const int32_t i = (it.q0 - P.seg_start[g]) / kTileM;
+  const int32_t nt = (kLead + rows * kImg + kTileM - 1) / kTileM;
+  const int32_t i = (it.q0 - P.seg_start[g] + kLead) / kTileM;
   const bool binary = P.group_bintile0[g] >= 0;
   const int32_t b0 = binary ? P.step_bintile_begin[P.step] + P.group_bintile0[g] : 0;
   if (it.kind == 1) {
@@ -259,22 +260,25 @@ __device__ __forceinline__ void rb_fill_table(const StepParams& P, const Item& i
   const int32_t base = it.q0 - P.seg_start[it.g];
   MemberEntry me[kPer];
   int32_t rem[kPer], px[kPer];
-  bool valid[kPer];
+  bool valid[kPer], in_img[kPer];
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
-    const int32_t local = base + lane + 32 * k;
-    const int32_t img = local / kImg;
+    const int32_t local = base + lane + 32 * k;  // negative in the segment's lead rows
+    const int32_t img = local >= 0 ? local / kImg : rows;
     rem[k] = local - img * kImg;
     const int32_t r = rem[k] / 15, c = rem[k] - r * 15;
-    valid[k] = img < rows && r < 14 && c < 14;
+    in_img[k] = local >= 0 && img < rows;
+    valid[k] = in_img[k] && r < 14 && c < 14;
     px[k] = r * 14 + c;
-    if (it.kind == 2 && valid[k]) me[k] = P.memtab[gb0 + img];
+    if (it.kind == 2 && in_img[k]) me[k] = P.memtab[gb0 + img];
   }
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     PosEntry e{nullptr, -1, 0, valid[k] ? 1 : 0, 0};
-    if (it.kind == 2 && valid[k]) {
-      e.dst = me[k].keep32 ? me[k].slot + px[k] * 8 : nullptr;
+    if (it.kind == 2 && in_img[k]) {
+      // pad positions of a real image keep their forwarding target: the
+      // epilogue writes them as zeros (any earlier layout's data is gone)
+      e.dst = valid[k] && me[k].keep32 ? me[k].slot + px[k] * 8 : nullptr;
       e.fwd_row = me[k].fwd_row >= 0 ? me[k].fwd_row + rem[k] : -1;
       e.fwd_buf = me[k].fwd_buf;
     }
@@ -373,7 +377,13 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
         split_f16x8(o, hi, lo);
         *reinterpret_cast<uint4*>(own + off) = hi;
         *reinterpret_cast<uint4*>(own_lo + off) = lo;
-      } else if (pe.valid) {
+      } else if (!pe.valid) {
+        // pad position of a forwarded image: zero in the parent's conv3x3 #1
+        // operand (its taps read the pads); lo and [x; y] pads only reach
+        // outputs that are never stored
+        if (pe.fwd_row >= 0 && pe.fwd_buf == 0)
+          *reinterpret_cast<uint4*>(P.stage_x + stage_off(P.ps, L.plane, pe.fwd_row)) = make_uint4(0, 0, 0, 0);
+      } else {
         if (pe.fwd_row >= 0) {
           uint4 hi, lo;
           split_f16x8(o, hi, lo);
@@ -663,8 +673,8 @@ __global__ void k_rb_plan(int32_t n_steps, const int32_t* __restrict__ sgb,
         seg_start[g] = -1;
         continue;
       }
-      const int32_t nt = (rows * kImg + tile_m - 1) / tile_m;
-      seg_start[g] = cursor;
+      const int32_t nt = (kLead + rows * kImg + tile_m - 1) / tile_m;
+      seg_start[g] = cursor + kLead;  // the first image; its tiles start kLead rows earlier
       group_tile0[g] = tiles;
       group_bintile0[g] = arity_of[group_fid[g]] == 2 ? bintiles : -1;
       cursor += nt * tile_m;
@@ -800,15 +810,15 @@ __global__ void k_rb_tiles(int32_t n_steps, const int32_t* __restrict__ sgb,
   for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
     if (seg_start[g] < 0) continue;
     const int32_t rows = group_begin[g + 1] - group_begin[g];
-    const int32_t nt = (rows * kImg + tile_m - 1) / tile_m;
+    const int32_t nt = (kLead + rows * kImg + tile_m - 1) / tile_m;
     for (int32_t i = threadIdx.x; i < nt; i += blockDim.x) {
       const int32_t ti = step_tile_begin[s] + group_tile0[g] + i;
       tile_group[ti] = g;
-      tile_q0[ti] = seg_start[g] + i * tile_m;
+      tile_q0[ti] = seg_start[g] - kLead + i * tile_m;
       if (group_bintile0[g] >= 0) {
         const int32_t bi = step_bintile_begin[s] + group_bintile0[g] + i;
         bin_group[bi] = g;
-        bin_q0[bi] = seg_start[g] + i * tile_m;
+        bin_q0[bi] = seg_start[g] - kLead + i * tile_m;
       }
     }
   }
@@ -833,7 +843,7 @@ __global__ void __launch_bounds__(256) k_rb_gather(const GatherTask* __restrict_
                                                    int32_t step, int64_t task_cap,
                                                    uint8_t* __restrict__ stage_x, uint8_t* __restrict__ stage_lo,
                                                    uint8_t* __restrict__ stage_cat, int64_t ps) {
-  constexpr int kPer = 2 * kPx * 8;
+  constexpr int kPer = 2 * kImg * 8;  // chunks × image positions (pads written as zeros) × planes
   const int64_t nt = min(static_cast<int64_t>(n_tasks[list]), task_cap);
   const GatherTask* T = tasks + list * task_cap;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < nt * kPer;
@@ -842,19 +852,47 @@ __global__ void __launch_bounds__(256) k_rb_gather(const GatherTask* __restrict_
     if (list == 1 && t.step != step) continue;
     const int rem = static_cast<int>(idx % kPer);
     const int j = rem & 7, q = rem >> 3;
-    const int cc = q >= kPx ? 1 : 0, px = q - cc * kPx;
-    const int r = px / 14, c = px - r * 14;
-    const int64_t row = t.row + r * 15 + c;
+    const int cc = q >= kImg ? 1 : 0, pos = q - cc * kImg;
+    const int r = pos / 15, c = pos - r * 15;
+    const int64_t row = t.row + pos;
     const int64_t off = ((static_cast<int64_t>((t.buf == 2 ? 2 : 0) + cc) * ps + row) << 7) +
                         ((j ^ static_cast<int>(row & 7)) << 4);
-    const float* sp = t.src + ((8 * cc + j) * kPx + px) * 8;
-    const float4 a = __ldg(reinterpret_cast<const float4*>(sp));
-    const float4 b = __ldg(reinterpret_cast<const float4*>(sp + 4));
-    const float o[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    uint4 h, l;
-    split_f16x8(o, h, l);
+    uint4 h = make_uint4(0, 0, 0, 0), l = make_uint4(0, 0, 0, 0);
+    if (r < 14 && c < 14) {
+      const float* sp = t.src + ((8 * cc + j) * kPx + r * 14 + c) * 8;
+      const float4 a = __ldg(reinterpret_cast<const float4*>(sp));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(sp + 4));
+      const float o[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      split_f16x8(o, h, l);
+    }
     *reinterpret_cast<uint4*>((t.buf == 0 ? stage_x : stage_cat) + off) = h;
     if (t.buf == 0) *reinterpret_cast<uint4*>(stage_lo + off) = l;
+  }
+}
+
+// A segment's lead rows (the first image's top / left pads) and the rows
+// after its last image up to its tile end, zeroed in stage_x every forward:
+// no image writer touches them, and a new layout must not see old data.
+// With the lead, a valid output's taps never leave its own segment, so no
+// cross-segment ordering is needed inside a step.
+__global__ void k_rb_zero_gaps(int32_t n_steps, const int32_t* __restrict__ sgb, const int32_t* __restrict__ group_begin,
+                               const int32_t* __restrict__ seg_start, uint8_t* __restrict__ stage_x, int64_t ps,
+                               int32_t tile_m) {
+  const int32_t g0 = sgb[0], g1 = sgb[n_steps];
+  for (int32_t g = g0 + blockIdx.x; g < g1; g += gridDim.x) {
+    if (seg_start[g] < 0) continue;
+    const int32_t rows = group_begin[g + 1] - group_begin[g];
+    const int32_t used = rows * kImg, span = (kLead + used + tile_m - 1) / tile_m * tile_m;
+    const int64_t base = kGuard + static_cast<int64_t>(seg_start[g]) - kLead;  // the segment's first tile row
+    const int32_t tail = span - kLead - used;                                // gap rows after the last image
+    const int32_t n16 = (kLead + tail) * 8;                                  // 16-byte pieces per chunk
+    for (int32_t i = threadIdx.x; i < 2 * n16; i += blockDim.x) {
+      const int cc = i >= n16 ? 1 : 0, k = i - cc * n16;
+      const int32_t r = k >> 3;
+      const int64_t row = r < kLead ? base + r : base + kLead + used + (r - kLead);
+      *reinterpret_cast<uint4*>(stage_x + ((static_cast<int64_t>(cc) * ps + row) << 7) + ((k & 7) << 4)) =
+          make_uint4(0, 0, 0, 0);
+    }
   }
 }
 
@@ -925,6 +963,15 @@ extern "C" int dbk_rb_gather(const void* tasks, const int32_t* n_tasks, int32_t 
   k_rb_gather<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const GatherTask*>(tasks), n_tasks, list, step, task_cap, static_cast<uint8_t*>(stage_x),
       static_cast<uint8_t*>(stage_lo), static_cast<uint8_t*>(stage_cat), plane_stride);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_rb_zero_gaps(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_begin,
+                                const int32_t* seg_start, void* stage_x, int64_t plane_stride, int32_t tile_m,
+                                void* stream) {
+  if (n_steps <= 0) return 0;
+  k_rb_zero_gaps<<<148 * 2, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      n_steps, step_group_begin, group_begin, seg_start, static_cast<uint8_t*>(stage_x), plane_stride, tile_m);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -356,3 +356,78 @@ extern "C" int64_t dbk_bucket_sort_scratch(int64_t n_items, int32_t max_keys) {
   const int64_t table = static_cast<int64_t>(max_keys) * nseg;
   return table + table / kScanChunk + 64;
 }
+
+// ------------------------------------------- program build from prefixes
+// build_program_from_prefix (src/program.cpp:95-142) for a batch of
+// concatenated prefix function sequences, one thread per program: the
+// reference's explicit stack of (node, remaining arity), kept in the
+// per-program slice of `stack` (≤ one entry per node). Writes the CSR the
+// device scheduler and executors read, with node ids in sequence order
+// (root = position 0). A tree of n nodes has n − 1 child edges, so program
+// e's child list starts at seq_off[e] − e. fwd_ok[g] = expensive node with
+// exactly one parent (every non-root node of a tree). Errors (first wins,
+// Errc codes): 1 empty sequence, 2 unknown function, 3 underfull, 4 overfull.
+__global__ void k_build_prefix(int64_t b, const int32_t* __restrict__ tokens, const int32_t* __restrict__ seq_off,
+                               int32_t p, const int32_t* __restrict__ arity_of, int32_t* __restrict__ prog_off,
+                               int32_t* __restrict__ fid, int32_t* __restrict__ child_off,
+                               int32_t* __restrict__ child_list, int32_t* __restrict__ child0,
+                               int32_t* __restrict__ child1, int32_t* __restrict__ example,
+                               int32_t* __restrict__ root_g, int32_t* __restrict__ fwd_ok,
+                               int2* __restrict__ stack, int32_t* __restrict__ err) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= b) return;
+  const int32_t off = seq_off[e], n = seq_off[e + 1] - off;
+  prog_off[e] = off;
+  if (e == b - 1) {
+    prog_off[b] = seq_off[b];
+    child_off[seq_off[b]] = seq_off[b] - static_cast<int32_t>(b);
+  }
+  root_g[e] = off;
+  if (n <= 0) {
+    atomicCAS(err, 0, 1);
+    return;
+  }
+  int2* st = stack + off;
+  int32_t top = 0, cursor = off - static_cast<int32_t>(e);  // next free child-list slot
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t g = off + i;
+    if (i > 0 && top == 0) {  // tokens remain after the root closed (checked first, as the reference)
+      atomicCAS(err, 0, 4);
+      return;
+    }
+    const int32_t f = tokens[g];
+    if (f < 0 || f >= p) {
+      atomicCAS(err, 0, 2);
+      return;
+    }
+    const int32_t a = arity_of[f];
+    fid[g] = f;
+    example[g] = static_cast<int32_t>(e);
+    child0[g] = -1;
+    child1[g] = -1;
+    child_off[g] = cursor;
+    cursor += a;
+    fwd_ok[g] = a > 0 && i > 0;
+    if (i > 0) {
+      int2& parent = st[top - 1];  // (node, children already attached)
+      const int32_t k = parent.y++;
+      child_list[child_off[parent.x] + k] = g;
+      if (k == 0) child0[parent.x] = g;
+      if (k == 1) child1[parent.x] = g;
+      if (parent.y == arity_of[fid[parent.x]]) --top;
+    }
+    if (a > 0) st[top++] = make_int2(g, 0);
+  }
+  if (top != 0) atomicCAS(err, 0, 3);  // the sequence ends with unfilled arities
+}
+
+extern "C" int dbk_build_prefix(int64_t b, const int32_t* tokens, const int32_t* seq_off, int32_t p,
+                                const int32_t* arity_of, int32_t* prog_off, int32_t* fid, int32_t* child_off,
+                                int32_t* child_list, int32_t* child0, int32_t* child1, int32_t* example,
+                                int32_t* root_g, int32_t* fwd_ok, void* stack, int32_t* err, void* stream) {
+  if (b <= 0) return 0;
+  k_build_prefix<<<static_cast<unsigned>((b + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      b, tokens, seq_off, p, arity_of, prog_off, fid, child_off, child_list, child0, child1, example, root_g,
+      fwd_ok, static_cast<int2*>(stack), err);
+  return static_cast<int>(cudaGetLastError());
+}

@@ -1,0 +1,69 @@
+"""Device program build from prefix function sequences (SURVEY.md §8f item 1:
+build_program_from_prefix, src/program.cpp:95-142) and per-call program
+updates of a resblock session (db_iep_session_set_programs)."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import paper_1707_02402_b200 as db
+
+pytestmark = pytest.mark.gpu
+
+F = 128 * 14 * 14
+
+
+def _batch(seed, b=12, length=8):
+    return db.Batch.generate("chain", batch=b, vocab=10, width=F, length=length, branch_prob=0.4, seed=seed)
+
+
+def _rows(b, seed):
+    return np.random.default_rng(seed).uniform(-1, 1, size=(b, F)).astype(np.float32)
+
+
+def test_set_programs_equals_fresh_session():
+    a, bb = _batch(1), _batch(2, b=10)
+    toks, off = bb.prefix_tokens()
+    s = db.IepSession(a, 5, db.MODULE_RESBLOCK, program_capacity=16, node_capacity=400, length_capacity=16)
+    xa = _rows(12, 0)
+    out_a = np.zeros_like(xa)
+    s.forward_host(xa, out_a)
+    s.set_programs(toks, off)
+    xb = _rows(10, 1)
+    out = np.zeros_like(xb)
+    s.forward_host(xb, out)
+    fresh = db.IepSession(bb, 5, db.MODULE_RESBLOCK)
+    want = np.zeros_like(xb)
+    fresh.forward_host(xb, want)
+    assert np.array_equal(out, want)
+    # the device-built CSR schedules exactly like the reference
+    ob = O.gen_batch("chain", 10, p=10, length=8, bp=0.4, seed=2)
+    from test_device_iep import _flat_from_json
+    assert _flat_from_json(s.schedule().to_json()) == O.schedule_improved(ob)
+    # and back to the first programs, pipelined
+    ta, oa = a.prefix_tokens()
+    s.set_programs(ta, oa)
+    again = np.zeros_like(xa)
+    s.forward_host_async(xa, again)
+    s.synchronize()
+    assert np.array_equal(again, out_a)
+
+
+@pytest.mark.parametrize("toks,off,code", [
+    ([], [0, 0], "DB_ERR_INVALID_ARG"),               # empty sequence
+    ([99], [0, 1], "DB_ERR_UNKNOWN_FUNCTION"),        # unknown function id
+    ([4], [0, 1], "DB_ERR_UNDERFULL_SEQUENCE"),       # unary root without its child
+    ([0, 0], [0, 2], "DB_ERR_OVERFULL_SEQUENCE"),     # token after the root closed
+])
+def test_set_programs_reports_reference_errors(toks, off, code):
+    s = db.IepSession(_batch(3), 5, db.MODULE_RESBLOCK)
+    with pytest.raises(db.DynbatchError) as ei:
+        s.set_programs(np.array(toks, np.int32), np.array(off, np.int32))
+        s.synchronize()
+    assert code in str(ei.value)
+
+
+def test_set_programs_capacity_is_enforced():
+    s = db.IepSession(_batch(4, b=4), 5, db.MODULE_RESBLOCK)
+    toks, off = _batch(5, b=12).prefix_tokens()
+    with pytest.raises(db.DynbatchError):
+        s.set_programs(toks, off)
