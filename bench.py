@@ -214,6 +214,30 @@ def calibrate_cpu(cfg, target_s):
     return threads, threads * rounds
 
 
+def pcie_duplex_seconds(nbytes, reps=3):
+    """Seconds per simultaneous H2D + D2H of nbytes each (pinned host
+    buffers, two streams): the e2e pipeline's bound on this box."""
+    import torch
+    n = nbytes // 4
+    h_in = torch.empty(n, dtype=torch.float32).pin_memory()
+    h_out = torch.empty(n, dtype=torch.float32).pin_memory()
+    d_in = torch.empty(n, dtype=torch.float32, device="cuda")
+    d_out = torch.empty(n, dtype=torch.float32, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    best = float("inf")
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s1):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    del h_in, h_out, d_in, d_out
+    return best
+
+
 # ------------------------------------------------------------- our arm
 def run_ours(args, dist):
     import numpy as np
@@ -231,7 +255,16 @@ def run_ours(args, dist):
                                     branch_prob=cfg["branch_prob"], seed=0)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     module_seed = int.from_bytes(_mix_seed(0, 0xd00d).to_bytes(8, "little"), "little")
-    sess = db.IepSession(batch, module_seed, db.MODULE_RESBLOCK)
+    # a second batch of programs (the next seed's), for the end-to-end pass
+    # where every call brings new programs; the session is sized for both
+    batch2 = db.Batch.generate_range(first, last, cfg["kind"], batch=per * N, vocab=cfg["vocab"],
+                                     width=F, depth=cfg["depth"], length=cfg["length"],
+                                     branch_prob=cfg["branch_prob"], seed=1)
+    seqs = [batch.prefix_tokens(), batch2.prefix_tokens()]
+    cap_nodes = max(int(o[-1]) for _, o in seqs)
+    cap_len = max(int(np.diff(o).max()) for _, o in seqs)
+    sess = db.IepSession(batch, module_seed, db.MODULE_RESBLOCK, program_capacity=per,
+                         node_capacity=cap_nodes, length_capacity=cap_len)
     sess.time(max(3, args.warmup))  # warm-up (≥ 3 steps)
     stats = sess.stats()
 
@@ -246,31 +279,58 @@ def run_ours(args, dist):
     # for the roofline and the breakdown (not the headline)
     pms, kt = sess.time(args.steps, profile=True)
 
-    # end-to-end through the public API: pinned host fp32 inputs → H2D →
-    # forward → D2H of the root outputs, every step. The pipelined call
-    # overlaps step i's forward with the upload of step i+1 and the download
-    # of step i−1 (copy streams, full-duplex PCIe); wall clock over K steps,
-    # max over ranks.
+    # end-to-end through the public API, every call a new batch: the
+    # programs as prefix function sequences (db_iep_session_set_programs:
+    # CSR built on the device) and pinned host fp32 input rows → H2D →
+    # device scheduler + forward → D2H of the root outputs. The pipelined
+    # call overlaps step i's forward with the upload of step i+1 and the
+    # download of step i−1 (copy streams, full-duplex PCIe). The two program
+    # sets alternate; wall clock over K steps, max over ranks.
     xin = [db.PinnedArray((per, F), np.float32) for _ in range(2)]
     xout = [db.PinnedArray((per, F), np.float32) for _ in range(2)]
+    toks, offs = [], []
+    for t, o in seqs:
+        pt, po = db.PinnedArray(t.shape, np.int32), db.PinnedArray(o.shape, np.int32)
+        pt.array[:] = t
+        po.array[:] = o
+        toks.append(pt)
+        offs.append(po)
     rng = np.random.default_rng(dist.rank)
     for x in xin:
         x.array[:] = rng.uniform(-1, 1, size=(per, F)).astype(np.float32)
-    for i in range(2):  # warm-up: creates the copy streams and double buffers
-        sess.forward_host_async(xin[i % 2].array, xout[i % 2].array)
-    sess.synchronize()
+
+    def e2e_pass(steps, new_programs):
+        for i in range(steps):
+            if new_programs:
+                sess.set_programs(toks[i % 2].array, offs[i % 2].array)
+            sess.forward_host_async(xin[i % 2].array, xout[i % 2].array)
+        sess.synchronize()
+
+    e2e_pass(2, True)  # warm-up: creates the copy streams and double buffers
     dist.barrier()
-    e2e_steps = max(args.steps, 20)  # amortises the pipeline fill and drain
+    e2e_steps = max(args.steps, 40)  # amortises the pipeline fill and drain
     t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        sess.forward_host_async(xin[i % 2].array, xout[i % 2].array)
-    sess.synchronize()
+    e2e_pass(e2e_steps, True)
     e2e_s = dist.max((time.perf_counter() - t0) / e2e_steps)
+    prog_bytes = sum(t.array.nbytes + o.array.nbytes for t, o in zip(toks, offs)) / 2
+    dist.barrier()
+    t0 = time.perf_counter()
+    e2e_pass(e2e_steps, False)
+    fixed_s = dist.max((time.perf_counter() - t0) / e2e_steps)
     e2e = {"value": per * N / e2e_s, "unit": "programs/s",
-           "h2d_bytes_per_step": per * F * 4, "d2h_bytes_per_step": per * F * 4,
+           "h2d_bytes_per_step": int(per * F * 4 + prog_bytes), "d2h_bytes_per_step": per * F * 4,
            "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
-           "api": "db_iep_session_forward_host_async (pinned fp32 CHW rows in, root rows out; copies overlap "
-                  "the neighbouring steps' forwards)"}
+           "api": "db_iep_session_set_programs (new prefix sequences every call, CSR built on the device) + "
+                  "db_iep_session_forward_host_async (pinned fp32 CHW rows in, root rows out; copies overlap "
+                  "the neighbouring steps' forwards)",
+           "same_programs_every_call": {"value": per * N / fixed_s, "ms_per_step": fixed_s * 1e3}}
+    # the e2e bound: this box's PCIe with both directions busy (pinned
+    # 411 MB each way on two streams, as the pipeline runs them)
+    link_s = pcie_duplex_seconds(per * F * 4)
+    e2e["roofline"] = {"bound": "pcie (H2D and D2H concurrent)",
+                       "achieved": round((per * F * 4) / e2e_s / 1e9, 1),
+                       "peak": round((per * F * 4) / link_s / 1e9, 1), "unit": "GB/s per direction",
+                       "frac": round(link_s / e2e_s, 4)}
 
     # roofline of the dominant kernel: the fused conv step (conv1x1 + conv3x3
     # #1 + conv3x3 #2 with the residual on the tensor cores), class 4

@@ -170,10 +170,10 @@ DeviceProgramBatch::DeviceProgramBatch(const HostCSR& csr, cudaStream_t s) : csr
   detect_static_shape(s);
 }
 
-void DeviceProgramBatch::set_prefix_programs(const std::int32_t* tokens, const std::int32_t* seq_off,
-                                             std::int64_t b, cudaStream_t s) {
+std::int64_t DeviceProgramBatch::begin_prefix_programs(const std::int32_t* seq_off, std::int64_t b) {
   if (b <= 0) throw_error(Errc::invalid_argument, "empty program batch");
   if (b > csr_.cap_b) throw_error(Errc::invalid_argument, "more programs than the session capacity");
+  if (seq_off[0] != 0) throw_error(Errc::invalid_argument, "sequence offsets must start at 0");
   const std::int64_t N = seq_off[b];
   int s_max = 0;
   for (std::int64_t e = 0; e < b; ++e) {
@@ -184,25 +184,36 @@ void DeviceProgramBatch::set_prefix_programs(const std::int32_t* tokens, const s
   }
   if (N > csr_.cap_N || s_max > csr_.cap_s)
     throw_error(Errc::invalid_argument, "batch exceeds the session capacity (nodes or program length)");
-  tokens_dev_.ensure(static_cast<size_t>(csr_.cap_N));
-  seq_off_dev_.ensure(static_cast<size_t>(csr_.cap_b) + 1);
-  build_stack_.ensure(static_cast<size_t>(csr_.cap_N));
-  build_err_.ensure(1);
-  check(cudaMemcpyAsync(tokens_dev_.get(), tokens, sizeof(std::int32_t) * static_cast<size_t>(N), cudaMemcpyHostToDevice,
-                        s), "H2D tokens");
-  check(cudaMemcpyAsync(seq_off_dev_.get(), seq_off, sizeof(std::int32_t) * static_cast<size_t>(b + 1),
-                        cudaMemcpyHostToDevice, s), "H2D offsets");
-  check(cudaMemsetAsync(build_err_.get(), 0, sizeof(std::int32_t), s), "memset");
-  check(dbk_build_prefix(b, tokens_dev_.get(), seq_off_dev_.get(), csr_.p, arity_of.get(), prog_off.get(), fid.get(),
-                         child_off.get(), child_list.get(), child0.get(), child1.get(), example.get(), root_g.get(),
-                         fwd_ok.get(), build_stack_.get(), build_err_.get(), s),
-        "dbk_build_prefix");
   csr_.b = b;
   csr_.N = N;
   csr_.s_max = s_max;
   shape_n_ = 0;  // the static-shape table described the old batch
-  build_pending_ = true;
   steps = 0;
+  build_err_.ensure(1);
+  build_stack_.ensure(static_cast<size_t>(csr_.cap_N));
+  return N;
+}
+
+void DeviceProgramBatch::build_prefix_programs(const std::int32_t* tokens_dev, const std::int32_t* seq_off_dev,
+                                               cudaStream_t s) {
+  check(cudaMemsetAsync(build_err_.get(), 0, sizeof(std::int32_t), s), "memset");
+  check(dbk_build_prefix(csr_.b, tokens_dev, seq_off_dev, csr_.p, arity_of.get(), prog_off.get(), fid.get(),
+                         child_off.get(), child_list.get(), child0.get(), child1.get(), example.get(), root_g.get(),
+                         fwd_ok.get(), build_stack_.get(), build_err_.get(), s),
+        "dbk_build_prefix");
+  build_pending_ = true;
+}
+
+void DeviceProgramBatch::set_prefix_programs(const std::int32_t* tokens, const std::int32_t* seq_off,
+                                             std::int64_t b, cudaStream_t s) {
+  const std::int64_t N = begin_prefix_programs(seq_off, b);
+  tokens_dev_.ensure(static_cast<size_t>(csr_.cap_N));
+  seq_off_dev_.ensure(static_cast<size_t>(csr_.cap_b) + 1);
+  check(cudaMemcpyAsync(tokens_dev_.get(), tokens, sizeof(std::int32_t) * static_cast<size_t>(N), cudaMemcpyHostToDevice,
+                        s), "H2D tokens");
+  check(cudaMemcpyAsync(seq_off_dev_.get(), seq_off, sizeof(std::int32_t) * static_cast<size_t>(b + 1),
+                        cudaMemcpyHostToDevice, s), "H2D offsets");
+  build_prefix_programs(tokens_dev_.get(), seq_off_dev_.get(), s);
 }
 
 void DeviceProgramBatch::replace_host_csr(const HostCSR& csr) {
@@ -476,6 +487,7 @@ void IepSession::set_schedule(const Schedule* schedule) {
 }
 
 void IepSession::forward() {
+  flush_programs();
   launches_ = 0;
   check(cudaMemsetAsync(err_.get(), 0, sizeof(std::int32_t) * 4, stream_), "memset err");
   check(cudaMemsetAsync(present_.get(), 0, present_.size() * sizeof(std::int32_t), stream_), "memset present");

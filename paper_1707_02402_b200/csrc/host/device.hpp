@@ -69,6 +69,32 @@ class Buf {
   size_t n_ = 0;
 };
 
+// Page-locked host array (grow-only), for copies that overlap compute.
+template <typename T>
+class Pinned {
+ public:
+  Pinned() = default;
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+  ~Pinned() {
+    if (p_) cudaFreeHost(p_);
+  }
+  void ensure(size_t n) {
+    if (n <= n_) return;
+    if (p_) cudaFreeHost(p_);
+    p_ = nullptr;
+    n_ = 0;
+    check(cudaHostAlloc(reinterpret_cast<void**>(&p_), sizeof(T) * std::max<size_t>(n, 1), cudaHostAllocPortable),
+          "cudaHostAlloc");
+    n_ = n;
+  }
+  T* get() const { return p_; }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
 // Per-kernel-class timing with CUDA events around launches (mirrors
 // db_kernel_times_t). Events are pooled; results are read after a sync.
 struct KernelTimes {
@@ -123,6 +149,11 @@ class DeviceProgramBatch {
   // Build errors surface at the next resolve(). The host CSR arrays go stale
   // (sizes stay current) until replace_host_csr().
   void set_prefix_programs(const std::int32_t* tokens, const std::int32_t* seq_off, std::int64_t b, cudaStream_t s);
+  // The same in two halves, for callers that upload the sequences
+  // themselves: host checks + new sizes (returns the node count), then the
+  // device build from device copies of the sequences.
+  std::int64_t begin_prefix_programs(const std::int32_t* seq_off, std::int64_t b);
+  void build_prefix_programs(const std::int32_t* tokens_dev, const std::int32_t* seq_off_dev, cudaStream_t s);
   void replace_host_csr(const HostCSR& csr);
   Buf<std::int32_t> fwd_ok;  // expensive node with one parent (written by the prefix build)
 
@@ -208,6 +239,8 @@ class IepSession {
   void forward_dense();
   void forward_resblock();
   void check_errors();
+  void flush_programs();                       // builds sequences staged by a pipelined set_programs
+  void programs_built();                       // session state that follows a device prefix build
   void init_resblock(const TensorBatch& inputs, std::uint64_t module_seed);
   void upload_resblock_inputs(const float* chw_rows);
   void download_resblock_outputs(float* chw_rows);

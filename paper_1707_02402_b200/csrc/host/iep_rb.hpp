@@ -39,6 +39,12 @@ struct IepSession::RB {
     Buf<float> in[2], out[2];
     cudaEvent_t h2d_done[2] = {}, in_free[2] = {}, out_ready[2] = {}, out_free[2] = {};
     std::uint64_t calls = 0;
+    // set_programs while pipelined: the sequences wait in pinned staging
+    // slot (calls & 1) and ride the next call's input upload on the h2d
+    // stream; the build runs on the main stream after that upload
+    Pinned<std::int32_t> tok_pin[2], off_pin[2];
+    Buf<std::int32_t> tok[2], off[2];
+    bool programs_pending = false;
     // DYNBATCH_PIPE_TRACE: timing events per call (h2d start/end, main
     // start/forward end, d2h start/end), printed by sync_pipeline()
     bool trace = false;

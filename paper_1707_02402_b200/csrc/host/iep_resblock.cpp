@@ -280,16 +280,58 @@ void IepSession::set_programs(const std::int32_t* tokens, const std::int32_t* se
   if (kind_ != ModuleKind::resblock) throw_error(Errc::invalid_argument, "set_programs needs a resblock session");
   RB& R = *rb_;
   DeviceProgramBatch& B = *batch_;
-  B.set_prefix_programs(tokens, seq_off, b, stream_);
+  if (R.pipe) {
+    // pipelined: stage the sequences in pinned memory; the next
+    // forward_host_async uploads them with its inputs (one copy queue, no
+    // small copy stuck behind a large one) and builds on the main stream
+    RB::Pipe& Q = *R.pipe;
+    const int k = static_cast<int>(Q.calls & 1);
+    const std::int64_t N = B.begin_prefix_programs(seq_off, b);
+    check(cudaEventSynchronize(Q.h2d_done[k]), "staging slot");  // the slot's last upload has finished
+    Q.tok_pin[k].ensure(static_cast<size_t>(B.csr().cap_N));
+    Q.off_pin[k].ensure(static_cast<size_t>(B.csr().cap_b) + 1);
+    std::memcpy(Q.tok_pin[k].get(), tokens, sizeof(std::int32_t) * static_cast<size_t>(N));
+    std::memcpy(Q.off_pin[k].get(), seq_off, sizeof(std::int32_t) * static_cast<size_t>(b + 1));
+    Q.programs_pending = true;
+  } else {
+    B.set_prefix_programs(tokens, seq_off, b, stream_);
+    programs_built();
+  }
   const std::int64_t N = B.csr().N;
-  check(cudaMemcpyAsync(R.fwd_ok.get(), B.fwd_ok.get(), sizeof(std::int32_t) * static_cast<size_t>(N),
+  host_tokens_.assign(tokens, tokens + N);
+  host_seq_off_.assign(seq_off, seq_off + b + 1);
+  mirror_stale_ = true;
+}
+
+void IepSession::programs_built() {
+  RB& R = *rb_;
+  DeviceProgramBatch& B = *batch_;
+  check(cudaMemcpyAsync(R.fwd_ok.get(), B.fwd_ok.get(), sizeof(std::int32_t) * static_cast<size_t>(B.csr().N),
                         cudaMemcpyDeviceToDevice, stream_), "fwd_ok");
   R.n_shared = 0;  // prefix sequences describe trees: no child has two parents
   host_schedule_ = false;
   strategy_ = Strategy::improved;
-  host_tokens_.assign(tokens, tokens + N);
-  host_seq_off_.assign(seq_off, seq_off + b + 1);
-  mirror_stale_ = true;
+}
+
+// A plain forward() after a pipelined set_programs: upload the staged
+// sequences on the main stream and build.
+void IepSession::flush_programs() {
+  if (!rb_ || !rb_->pipe || !rb_->pipe->programs_pending) return;
+  RB::Pipe& Q = *rb_->pipe;
+  DeviceProgramBatch& B = *batch_;
+  const int k = static_cast<int>(Q.calls & 1);
+  Q.tok[k].ensure(static_cast<size_t>(B.csr().cap_N));
+  Q.off[k].ensure(static_cast<size_t>(B.csr().cap_b) + 1);
+  check(cudaMemcpyAsync(Q.tok[k].get(), Q.tok_pin[k].get(), sizeof(std::int32_t) * static_cast<size_t>(B.csr().N),
+                        cudaMemcpyHostToDevice, stream_), "H2D tokens");
+  check(cudaMemcpyAsync(Q.off[k].get(), Q.off_pin[k].get(), sizeof(std::int32_t) * static_cast<size_t>(B.csr().b + 1),
+                        cudaMemcpyHostToDevice, stream_), "H2D offsets");
+  B.build_prefix_programs(Q.tok[k].get(), Q.off[k].get(), stream_);
+  programs_built();
+  Q.programs_pending = false;
+  // the pinned slot is reused by a later set_programs only after this slot's
+  // h2d_done: record it here, after the copies
+  check(cudaEventRecord(Q.h2d_done[k], stream_), "event");
 }
 
 // Host CSR arrays of the programs last set on the device (schedule download,
@@ -372,11 +414,25 @@ void IepSession::forward_host_async(const float* inputs, float* outputs) {
   };
   check(cudaStreamWaitEvent(Q.h2d, Q.in_free[k]), "wait");
   mark(0, Q.h2d);
+  const bool build = Q.programs_pending;
+  if (build) {  // sequences staged by set_programs ride this call's upload
+    Q.tok[k].ensure(static_cast<size_t>(B.csr().cap_N));
+    Q.off[k].ensure(static_cast<size_t>(B.csr().cap_b) + 1);
+    check(cudaMemcpyAsync(Q.tok[k].get(), Q.tok_pin[k].get(), sizeof(std::int32_t) * static_cast<size_t>(B.csr().N),
+                          cudaMemcpyHostToDevice, Q.h2d), "H2D tokens");
+    check(cudaMemcpyAsync(Q.off[k].get(), Q.off_pin[k].get(), sizeof(std::int32_t) * static_cast<size_t>(b + 1),
+                          cudaMemcpyHostToDevice, Q.h2d), "H2D offsets");
+    Q.programs_pending = false;
+  }
   check(cudaMemcpyAsync(Q.in[k].get(), inputs, bytes, cudaMemcpyHostToDevice, Q.h2d), "H2D inputs");
   mark(1, Q.h2d);
   check(cudaEventRecord(Q.h2d_done[k], Q.h2d), "event");
   check(cudaStreamWaitEvent(stream_, Q.h2d_done[k]), "wait");
   mark(2, stream_);
+  if (build) {
+    B.build_prefix_programs(Q.tok[k].get(), Q.off[k].get(), stream_);
+    programs_built();
+  }
   check(dbk_rb_inputs_from_chw(b, Q.in[k].get(), R.inputs.get(), stream_), "inputs layout");
   check(cudaEventRecord(Q.in_free[k], stream_), "event");
   forward();

@@ -67,3 +67,36 @@ def test_set_programs_capacity_is_enforced():
     toks, off = _batch(5, b=12).prefix_tokens()
     with pytest.raises(db.DynbatchError):
         s.set_programs(toks, off)
+
+
+def test_pipelined_new_programs_every_call():
+    """set_programs before every forward_host_async (the sequences ride the
+    call's input upload): each call's outputs equal a fresh session's for
+    that call's programs and rows, and a plain forward after a staged
+    set_programs builds it too."""
+    batches = [_batch(s, b=8 + s) for s in range(3)]
+    seqs = [b.prefix_tokens() for b in batches]
+    s = db.IepSession(batches[0], 6, db.MODULE_RESBLOCK, program_capacity=16, node_capacity=400,
+                      length_capacity=16)
+    calls = [0, 1, 2, 1, 0, 2, 2]
+    xs = [db.PinnedArray((8 + c, F), np.float32) for c in calls]
+    outs = [db.PinnedArray(x.array.shape, np.float32) for x in xs]
+    for i, (c, x) in enumerate(zip(calls, xs)):
+        x.array[:] = _rows(8 + c, 10 + i)
+    for c, x, o in zip(calls, xs, outs):
+        s.set_programs(*seqs[c])
+        s.forward_host_async(x.array, o.array)
+    s.synchronize()
+    for i, (c, x, o) in enumerate(zip(calls, xs, outs)):
+        fresh = db.IepSession(batches[c], 6, db.MODULE_RESBLOCK)
+        want = np.zeros((8 + c, F), np.float32)
+        fresh.forward_host(x.array, want)
+        assert np.array_equal(o.array, want), i
+    # staged by a pipelined set_programs, built by a plain forward
+    s.set_programs(*seqs[1])
+    s.forward()
+    s.synchronize()
+    fresh = db.IepSession(batches[1], 6, db.MODULE_RESBLOCK)
+    fresh.forward()
+    from test_device_iep import _flat_from_json
+    assert _flat_from_json(s.schedule().to_json()) == _flat_from_json(fresh.schedule().to_json())
