@@ -21,12 +21,16 @@ extern "C" {
  * Replaces max_root_distance_labels + schedule_improved/make_step
  * (src/program.cpp:239-272, src/schedule.cpp:66-79,135-164). */
 
-/* labels[g] = longest root→g distance (Kahn per program, one thread per
- * program); dev_scalars[0] = d_max (atomicMax), dev_scalars[1] |= 1 on a
+/* Per-node step labels, one thread per program; strategy (db_strategy):
+ *   2 improved: labels[g] = longest root→g distance (Kahn from the root);
+ *   1 standard: labels[g] = g's position in postorder_flatten
+ *               (src/program.cpp:274-303; schedule_standard's column);
+ *   3 online:   labels[g] = g's height (schedule_online_full's round).
+ * dev_scalars[0] = largest label (atomicMax), dev_scalars[1] |= 1 on a
  * cycle / unreachable node. scratch: 2·N int32. child*: global ids or -1. */
 int dbk_sched_labels(int64_t b, int64_t N, const int32_t* prog_off, const int32_t* child_off,
                      const int32_t* child_list, const int32_t* root_g, int32_t* labels,
-                     int32_t* scratch, int32_t* dev_scalars, void* stream);
+                     int32_t* scratch, int32_t* dev_scalars, int32_t strategy, void* stream);
 
 /* Labels of a batch whose programs all share one tree shape (programs of n
  * nodes, shape labels table[n], depth dmax): the balanced-tree static
@@ -34,8 +38,9 @@ int dbk_sched_labels(int64_t b, int64_t N, const int32_t* prog_off, const int32_
 int dbk_sched_labels_static(int64_t N, int32_t n, const int32_t* table, int32_t dmax, int32_t* labels,
                             int32_t* dev_scalars, void* stream);
 
-/* Stable counting sort of all N nodes by key = (d_max - label)·p + fid
- * over CSR order; writes member_g[N] (sorted global ids), and the group
+/* Stable counting sort of all N nodes by key = step·p + fid over CSR
+ * order, step = label (ascending: standard, online) or d_max − label
+ * (improved); writes member_g[N] (sorted global ids), and the group
  * tables: group_fid[G], group_begin[G+1], step_group_begin[S+1] (and empty
  * steps up to steps_cap, so a host may launch per-step work for an upper
  * bound of S) with dev_scalars[2] = G. seg_hist must hold max_keys ·
@@ -44,7 +49,7 @@ int dbk_sched_labels_static(int64_t N, int32_t n, const int32_t* table, int32_t 
 int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, const int32_t* fid,
                           const int32_t* labels, int32_t* dev_scalars, int32_t* seg_hist,
                           int32_t* member_g, int32_t* group_fid, int32_t* group_begin,
-                          int32_t* step_group_begin, int32_t steps_cap, void* stream);
+                          int32_t* step_group_begin, int32_t steps_cap, int32_t ascending, void* stream);
 
 /* build_program_from_prefix (src/program.cpp:95-142) for b concatenated
  * prefix sequences (tokens, seq_off[b+1]), one thread per program: writes

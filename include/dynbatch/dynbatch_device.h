@@ -100,6 +100,10 @@ DYNBATCH_API db_status db_iep_session_create(const db_batch* batch, int64_t firs
 /* Executes a host-built schedule (any strategy) instead of the device
  * scheduler; NULL restores the device improved scheduler. */
 DYNBATCH_API db_status db_iep_session_set_schedule(db_iep_session* s, const db_schedule* schedule);
+/* Strategy of the device scheduler run by every forward: IMPROVED (the
+ * default), STANDARD or ONLINE (same schedules as db_schedule_build, built
+ * on the device); NAIVE is DB_ERR_INVALID_ARG (load it with set_schedule). */
+DYNBATCH_API db_status db_iep_session_set_strategy(db_iep_session* s, db_strategy strategy);
 /* Enqueues one forward on the session stream (schedule + execute). */
 DYNBATCH_API db_status db_iep_session_forward(db_iep_session* s);
 /* End-to-end: pinned-host fp32 inputs (rows × width, reference row layout,
@@ -137,6 +141,9 @@ DYNBATCH_API db_status db_iep_session_time(db_iep_session* s, int32_t iters, int
                                            double* ms, db_kernel_times_t* kt);
 DYNBATCH_API void db_iep_session_free(db_iep_session* s);
 
+/* db_schedule_build on the device scheduler: IMPROVED, STANDARD or ONLINE
+ * (bit-identical to the host builders; sched.cu); NAIVE is DB_ERR_INVALID_ARG. */
+DYNBATCH_API db_status db_schedule_build_device(const db_batch* batch, db_strategy strategy, db_schedule** out);
 /* db_execute with a module kind; schedule NULL = device improved scheduler. */
 DYNBATCH_API db_status db_execute_device(const db_batch* batch, const db_schedule* schedule,
                                          uint64_t module_seed, const db_module_opts* opts,

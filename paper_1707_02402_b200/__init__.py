@@ -106,6 +106,7 @@ SIGNATURES = {
     "db_batch_stats": (C.c_int32, [VP, C.POINTER(BatchStats)]),
     "db_batch_free": (None, [VP]),
     "db_schedule_build": (C.c_int32, [VP, C.c_int, PVP]),
+    "db_schedule_build_device": (C.c_int32, [VP, C.c_int, PVP]),
     "db_schedule_verify": (C.c_int32, [VP, VP]),
     "db_schedule_step_count": (C.c_int64, [VP]),
     "db_schedule_expensive_calls": (C.c_int32, [VP, VP, C.POINTER(C.c_int64)]),
@@ -141,6 +142,7 @@ SIGNATURES = {
     "db_iep_session_create": (C.c_int32, [VP, C.c_int64, C.c_int64, C.c_uint64,
                                           C.POINTER(ModuleOpts), PVP]),
     "db_iep_session_set_schedule": (C.c_int32, [VP, VP]),
+    "db_iep_session_set_strategy": (C.c_int32, [VP, C.c_int]),
     "db_iep_session_forward": (C.c_int32, [VP]),
     "db_iep_session_forward_host": (C.c_int32, [VP, VP, VP]),
     "db_iep_session_forward_host_async": (C.c_int32, [VP, VP, VP]),
@@ -292,6 +294,12 @@ class Batch(_Handle):
         check(lib().db_schedule_build(self.h, STRATEGY[strategy], C.byref(h)))
         return Schedule(h)
 
+    def schedule_device(self, strategy="improved") -> "Schedule":
+        """The schedule built by the device scheduler (improved, standard or online)."""
+        h = C.c_void_p()
+        check(lib().db_schedule_build_device(self.h, STRATEGY[strategy], C.byref(h)))
+        return Schedule(h)
+
     def execute(self, schedule: "Schedule", module_seed: int) -> "Run":
         h = C.c_void_p()
         check(lib().db_execute(self.h, schedule.h, module_seed, C.byref(h)))
@@ -404,6 +412,10 @@ class IepSession(_Handle):
 
     def set_schedule(self, schedule):
         check(lib().db_iep_session_set_schedule(self.h, schedule.h if schedule else None))
+
+    def set_strategy(self, strategy: str):
+        """Device scheduler strategy for every forward: improved, standard or online."""
+        check(lib().db_iep_session_set_strategy(self.h, STRATEGY[strategy]))
 
     def set_programs(self, tokens: np.ndarray, seq_off: np.ndarray):
         """Replace the programs by prefix function sequences (concatenated

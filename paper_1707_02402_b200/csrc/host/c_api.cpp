@@ -215,6 +215,13 @@ db_status db_schedule_build(const db_batch* batch, db_strategy strategy, db_sche
   });
 }
 
+db_status db_schedule_build_device(const db_batch* batch, db_strategy strategy, db_schedule** out) {
+  if (!batch || !out) return null_arg();
+  return guarded([&] {
+    *out = new db_schedule{dynbatch::schedule_device(to_strategy(strategy), batch->programs, batch->vocab)};
+  });
+}
+
 db_status db_schedule_verify(const db_schedule* schedule, const db_batch* batch) {
   if (!schedule || !batch) return null_arg();
   return guarded([&] {
@@ -460,6 +467,11 @@ db_status db_iep_session_create(const db_batch* batch, int64_t first, int64_t la
 db_status db_iep_session_set_schedule(db_iep_session* s, const db_schedule* schedule) {
   if (!s) return null_arg();
   return guarded([&] { s->s->set_schedule(schedule ? &schedule->schedule : nullptr); });
+}
+
+db_status db_iep_session_set_strategy(db_iep_session* s, db_strategy strategy) {
+  if (!s) return null_arg();
+  return guarded([&] { s->s->set_strategy(to_strategy(strategy)); });
 }
 
 db_status db_iep_session_forward(db_iep_session* s) {

@@ -273,27 +273,30 @@ void DeviceProgramBatch::detect_static_shape(cudaStream_t s) {
   shape_n_ = n;
 }
 
-int DeviceProgramBatch::run_scheduler(cudaStream_t s, bool upper_bound) {
+int DeviceProgramBatch::run_scheduler(cudaStream_t s, bool upper_bound, Strategy strategy) {
+  if (strategy == Strategy::naive) throw_error(Errc::invalid_argument, "the naive schedule is host-built");
   if (csr_.b == 0) {
     steps = 0;
     groups = 0;
     return 0;
   }
   check(cudaMemsetAsync(scalars.get(), 0, sizeof(std::int32_t) * 8, s), "memset");
-  if (static_shape()) {  // balanced-tree (shared shape) static schedule: labels from the shape table
+  const bool shape = static_shape() && strategy == Strategy::improved;
+  if (shape) {  // balanced-tree (shared shape) static schedule: labels from the shape table
     check(dbk_sched_labels_static(csr_.N, shape_n_, shape_labels_.get(), shape_dmax_, labels.get(), scalars.get(), s),
           "dbk_sched_labels_static");
   } else {
-    check(dbk_sched_labels(csr_.b, csr_.N, prog_off.get(), child_off.get(), child_list.get(),
-                           root_g.get(), labels.get(), scratch.get(), scalars.get(), s),
+    check(dbk_sched_labels(csr_.b, csr_.N, prog_off.get(), child_off.get(), child_list.get(), root_g.get(),
+                           labels.get(), scratch.get(), scalars.get(), static_cast<std::int32_t>(strategy), s),
           "dbk_sched_labels");
   }
+  // improved, standard and online all take ≤ s_max steps
   const int cap = std::max(1, csr_.s_max);
   check(dbk_sched_bucket_sort(csr_.N, csr_.p, max_keys_, fid.get(), labels.get(), scalars.get(),
                               seg_hist.get(), member_g.get(), group_fid.get(), group_begin.get(),
-                              step_group_begin.get(), cap, s),
+                              step_group_begin.get(), cap, strategy == Strategy::improved ? 0 : 1, s),
         "dbk_sched_bucket_sort");
-  if (static_shape()) {  // the step count is known: no host sync in the forward
+  if (shape) {  // the step count is known: no host sync in the forward
     steps = shape_dmax_ + 1;
     groups_pending_ = true;
     return steps;
@@ -430,7 +433,7 @@ ExecutionTrace DeviceProgramBatch::trace_counts(cudaStream_t s) const {
 IepSession::IepSession(const FunctionVocab& vocab, std::span<const Program> programs,
                        const TensorBatch& inputs, std::uint64_t module_seed, ModuleKind kind,
                        std::int64_t cap_programs, std::int64_t cap_nodes, int cap_length)
-    : kind_(kind), width_(vocab.width()), vocab_(vocab) {
+    : vocab_(vocab), kind_(kind), width_(vocab.width()) {
   require_device();
   require_valid_batch(programs, vocab);
   if (inputs.rows() != static_cast<std::int64_t>(programs.size())) {
@@ -474,6 +477,14 @@ IepSession::IepSession(const FunctionVocab& vocab, std::span<const Program> prog
 }
 
 
+void IepSession::set_strategy(Strategy strategy) {
+  if (strategy == Strategy::naive)
+    throw_error(Errc::invalid_argument, "naive runs one node per step: load it with set_schedule");
+  layout_dirty_ = true;
+  host_schedule_ = false;
+  strategy_ = strategy;
+}
+
 void IepSession::set_schedule(const Schedule* schedule) {
   layout_dirty_ = true;
   if (schedule) {
@@ -493,7 +504,7 @@ void IepSession::forward() {
   check(cudaMemsetAsync(present_.get(), 0, present_.size() * sizeof(std::int32_t), stream_), "memset present");
   if (!host_schedule_) {
     prof_.begin(0, stream_);
-    batch_->run_scheduler(stream_, kind_ == ModuleKind::resblock);  // resblock: no host sync
+    batch_->run_scheduler(stream_, kind_ == ModuleKind::resblock, strategy_);  // resblock: no host sync
     prof_.end(stream_);
     launches_ += 4;  // labels, histogram, scan, scatter
   }

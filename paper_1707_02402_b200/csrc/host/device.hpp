@@ -159,7 +159,9 @@ class DeviceProgramBatch {
 
   // Device improved scheduler; returns the step count (one small D2H), or,
   // with upper_bound, s_max without a host sync (empty trailing steps).
-  int run_scheduler(cudaStream_t s, bool upper_bound = false);
+  // strategy: improved (default), standard or online — the same bucket
+  // sort over per-strategy labels; naive stays host-built.
+  int run_scheduler(cudaStream_t s, bool upper_bound = false, Strategy strategy = Strategy::improved);
   void check_scheduler_error(cudaStream_t s) const;
   // Installs a host-built schedule in the same table format.
   int load_schedule(const Schedule& schedule, cudaStream_t s);
@@ -210,6 +212,7 @@ class IepSession {
   void set_programs(const std::int32_t* tokens, const std::int32_t* seq_off, std::int64_t b);
 
   void set_schedule(const Schedule* schedule);
+  void set_strategy(Strategy strategy);  // device scheduler strategy (improved / standard / online)
   void forward();
   void forward_host(const float* inputs, float* outputs);
   void forward_host_async(const float* inputs, float* outputs);

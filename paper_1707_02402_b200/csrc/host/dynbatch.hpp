@@ -239,6 +239,9 @@ Schedule schedule_naive(std::span<const Program> batch, const FunctionVocab& voc
 Schedule schedule_standard(std::span<const Program> batch, const FunctionVocab& vocab);
 // Device scheduler (dbk_schedule_*): bit-identical to the reference's.
 Schedule schedule_improved(std::span<const Program> batch, const FunctionVocab& vocab);
+// Device-built improved / standard / online schedule (same result as the
+// host builders, bit for bit).
+Schedule schedule_device(Strategy strategy, std::span<const Program> batch, const FunctionVocab& vocab);
 Step group_by_function(std::span<const FrontierItem> items);
 Step schedule_online(std::span<const Program> batch, std::span<const NodeRef> frontier,
                      const std::function<bool(NodeRef)>& already_executed,

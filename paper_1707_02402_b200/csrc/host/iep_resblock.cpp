@@ -309,8 +309,10 @@ void IepSession::programs_built() {
   check(cudaMemcpyAsync(R.fwd_ok.get(), B.fwd_ok.get(), sizeof(std::int32_t) * static_cast<size_t>(B.csr().N),
                         cudaMemcpyDeviceToDevice, stream_), "fwd_ok");
   R.n_shared = 0;  // prefix sequences describe trees: no child has two parents
-  host_schedule_ = false;
-  strategy_ = Strategy::improved;
+  if (host_schedule_) {  // a host schedule described the old programs
+    host_schedule_ = false;
+    strategy_ = Strategy::improved;
+  }
 }
 
 // A plain forward() after a pipelined set_programs: upload the staged

@@ -58,13 +58,98 @@ __global__ void k_labels(int64_t b, const int32_t* __restrict__ prog_off,
   if ((threadIdx.x & 31) == 0 && local_max > 0) atomicMax(&scal[0], local_max);
 }
 
+// schedule_standard's column of a node (src/schedule.cpp:107-133): its
+// position in postorder_flatten (src/program.cpp:274-303) — depth-first from
+// the root, children in operand order, a node emitted once after all its
+// children. One thread per program; the DFS stack (node, next child edge)
+// lives in the program's slices of the two scratch arrays. A cycle (stack
+// deeper than the program) or an unreachable node sets the error flag.
+__global__ void k_labels_postorder(int64_t b, const int32_t* __restrict__ prog_off,
+                                   const int32_t* __restrict__ child_off, const int32_t* __restrict__ child_list,
+                                   const int32_t* __restrict__ root_g, int32_t* __restrict__ labels,
+                                   int32_t* __restrict__ st_node, int32_t* __restrict__ st_next,
+                                   int32_t* __restrict__ scal) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int local_max = 0;
+  if (e < b) {
+    const int32_t base = prog_off[e], n = prog_off[e + 1] - base;
+    for (int32_t g = base; g < base + n; ++g) labels[g] = -1;
+    int32_t depth = 1, pos = 0;
+    bool bad = false;
+    st_node[base] = root_g[e];
+    st_next[base] = child_off[root_g[e]];
+    while (depth > 0) {
+      const int32_t v = st_node[base + depth - 1], nx = st_next[base + depth - 1];
+      if (nx < child_off[v + 1]) {
+        st_next[base + depth - 1] = nx + 1;
+        const int32_t c = child_list[nx];
+        if (labels[c] < 0) {
+          if (depth == n) {
+            bad = true;
+            break;
+          }
+          st_node[base + depth] = c;
+          st_next[base + depth] = child_off[c];
+          ++depth;
+        }
+      } else {
+        labels[v] = pos++;
+        --depth;
+      }
+    }
+    if (bad || pos != n) atomicOr(&scal[1], 1);
+    local_max = pos - 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  if ((threadIdx.x & 31) == 0 && local_max > 0) atomicMax(&scal[0], local_max);
+}
+
+// schedule_online_full's round of a node (src/schedule.cpp:171-241): a node
+// is ready once all its children ran, so it runs in round = its height
+// (0 for a leaf, else 1 + the largest child height). Kahn's order from the
+// root (parents first), then heights over that order reversed.
+__global__ void k_labels_height(int64_t b, const int32_t* __restrict__ prog_off,
+                                const int32_t* __restrict__ child_off, const int32_t* __restrict__ child_list,
+                                const int32_t* __restrict__ root_g, int32_t* __restrict__ labels,
+                                int32_t* __restrict__ indeg, int32_t* __restrict__ queue,
+                                int32_t* __restrict__ scal) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int local_max = 0;
+  if (e < b) {
+    const int32_t base = prog_off[e], end = prog_off[e + 1];
+    for (int32_t g = base; g < end; ++g) indeg[g] = 0;
+    for (int32_t g = base; g < end; ++g)
+      for (int32_t c = child_off[g]; c < child_off[g + 1]; ++c) ++indeg[child_list[c]];
+    int32_t head = base, tail = base;
+    queue[tail++] = root_g[e];
+    while (head < tail) {
+      const int32_t v = queue[head++];
+      for (int32_t c = child_off[v]; c < child_off[v + 1]; ++c)
+        if (--indeg[child_list[c]] == 0) queue[tail++] = child_list[c];
+    }
+    if (head != end) atomicOr(&scal[1], 1);
+    for (int32_t i = tail - 1; i >= base; --i) {
+      const int32_t v = queue[i];
+      int32_t h = 0;
+      for (int32_t c = child_off[v]; c < child_off[v + 1]; ++c) h = max(h, labels[child_list[c]] + 1);
+      labels[v] = h;
+      local_max = max(local_max, h);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  if ((threadIdx.x & 31) == 0 && local_max > 0) atomicMax(&scal[0], local_max);
+}
+
+// Step of node i: improved runs labels from d_max down (descending);
+// standard / online labels are the step itself (ascending).
 struct LevelKey {
   const int32_t* fid;
   const int32_t* labels;
   const int32_t* scal;
   int32_t p;
+  int32_t ascending;
   __device__ __forceinline__ int32_t operator()(int64_t i) const {
-    return (scal[0] - labels[i]) * p + fid[i];
+    return (ascending ? labels[i] : scal[0] - labels[i]) * p + fid[i];
   }
 };
 
@@ -276,14 +361,28 @@ inline int32_t n_segments(int64_t n) { return static_cast<int32_t>((n + kSeg - 1
 extern "C" int dbk_sched_labels(int64_t b, int64_t N, const int32_t* prog_off,
                                 const int32_t* child_off, const int32_t* child_list,
                                 const int32_t* root_g, int32_t* labels, int32_t* scratch,
-                                int32_t* dev_scalars, void* stream) {
+                                int32_t* dev_scalars, int32_t strategy, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (b <= 0) return 0;
   const int threads = 128;
   const int blocks = static_cast<int>((b + threads - 1) / threads);
-  // scratch = indeg[N] | queue[N]
-  k_labels<<<blocks, threads, 0, s>>>(b, prog_off, child_off, child_list, root_g, labels, scratch,
-                                      scratch + N, dev_scalars);
+  // scratch = indeg[N] | queue[N] (standard: DFS stack nodes | next edges)
+  switch (strategy) {
+    case 1:  // standard
+      k_labels_postorder<<<blocks, threads, 0, s>>>(b, prog_off, child_off, child_list, root_g, labels, scratch,
+                                                    scratch + N, dev_scalars);
+      break;
+    case 3:  // online
+      k_labels_height<<<blocks, threads, 0, s>>>(b, prog_off, child_off, child_list, root_g, labels, scratch,
+                                                 scratch + N, dev_scalars);
+      break;
+    case 2:  // improved
+      k_labels<<<blocks, threads, 0, s>>>(b, prog_off, child_off, child_list, root_g, labels, scratch,
+                                          scratch + N, dev_scalars);
+      break;
+    default:
+      return static_cast<int>(cudaErrorInvalidValue);
+  }
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -312,11 +411,11 @@ extern "C" int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, con
                                      const int32_t* labels, int32_t* dev_scalars,
                                      int32_t* seg_hist, int32_t* member_g, int32_t* group_fid,
                                      int32_t* group_begin, int32_t* step_group_begin, int32_t steps_cap,
-                                     void* stream) {
+                                     int32_t ascending, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int32_t nseg = n_segments(N);
   cudaMemsetAsync(seg_hist, 0, sizeof(int32_t) * static_cast<size_t>(max_keys) * (nseg > 0 ? nseg : 1), s);
-  LevelKey key{fid, labels, dev_scalars, p};
+  LevelKey key{fid, labels, dev_scalars, p, ascending};
   const int blocks = (nseg + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (nseg > 0) k_seg_hist<<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist);
   const int32_t ns = nseg > 0 ? nseg : 1;

@@ -52,6 +52,47 @@ def test_device_improved_schedule_matches_golden(golden, name):
     s.verify(b)
 
 
+@pytest.mark.parametrize("strategy", ["standard", "online"])
+@pytest.mark.parametrize("name", list(IEP))
+def test_device_standard_online_schedules_match_golden(golden, name, strategy):
+    """§8f item 2: standard (postorder columns) and online (ready rounds =
+    node heights) from the device scheduler, pinned to the compiled
+    reference's schedule_to_json fingerprints."""
+    fp, _ = golden
+    c = IEP[name]
+    b = db.Batch.generate(WK[c["kind"]], batch=c["b"], vocab=c["p"], width=8, depth=c["depth"],
+                          length=c["length"], branch_prob=c["bp"], seed=0)
+    s = b.schedule_device(strategy)
+    fs = _flat_from_json(s.to_json())
+    g = fp["iep"][name][strategy]
+    assert (fs.n_steps, fs.n_groups, fs.expensive_calls()) == (g["steps"], g["groups"],
+                                                                 g["expensive_calls"])
+    assert sched_fnv(fs) == g["sched_fnv"]
+    assert fs.strategy == strategy
+    s.verify(b)
+
+
+@pytest.mark.parametrize("strategy", ["improved", "standard", "online"])
+@pytest.mark.parametrize("kind,seed", [("chain", 3), ("dag", 4), ("balanced", 5), ("dag", 11)])
+def test_device_schedules_equal_host_builders(kind, seed, strategy):
+    b = db.Batch.generate(kind, batch=37, vocab=9, width=4, depth=4, length=11, branch_prob=0.5, seed=seed)
+    want = b.schedule(strategy).to_json()
+    assert b.schedule_device(strategy).to_json() == want
+    # a session's per-forward device scheduler with that strategy
+    sess = db.IepSession(b, 3)
+    sess.set_strategy(strategy)
+    sess.forward()
+    assert sess.schedule().to_json() == want
+
+
+def test_device_naive_strategy_is_rejected():
+    b = db.Batch.generate("chain", batch=4, vocab=9, width=4, length=6, branch_prob=0.5, seed=1)
+    with pytest.raises(db.DynbatchError):
+        b.schedule_device("naive")
+    with pytest.raises(db.DynbatchError):
+        db.IepSession(b, 3).set_strategy("naive")
+
+
 @pytest.mark.parametrize("seed", [0, 1, 7])
 @pytest.mark.parametrize("kind", ["chain", "balanced", "dag"])
 def test_device_schedule_and_labels_match_reference_fresh_seeds(kind, seed):

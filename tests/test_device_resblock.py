@@ -78,6 +78,12 @@ def test_resblock_host_schedules_give_same_outputs():
         # every position is computed by the same MMA chain whatever the tile
         # packing, so schedules agree bit for bit
         assert np.array_equal(other.outputs(), improved), strat
+    for strat in ("standard", "online"):  # the session's device scheduler
+        s = db.IepSession(batch, 3, db.MODULE_RESBLOCK)
+        s.set_strategy(strat)
+        s.forward()
+        assert np.array_equal(s.run().outputs(), improved), strat
+        assert s.schedule().to_json() == batch.schedule(strat).to_json()
 
 
 def test_resblock_row_alone_equals_row_in_batch():
