@@ -355,6 +355,18 @@ class Run(_Handle):
     def peak_group_rows(self):
         return lib().db_run_peak_group_rows(self.h)
 
+    @property
+    def module_seconds(self) -> float:
+        return lib().db_run_module_seconds(self.h)
+
+    @property
+    def stacking_seconds(self) -> float:
+        return lib().db_run_stacking_seconds(self.h)
+
+    @property
+    def total_seconds(self) -> float:
+        return lib().db_run_total_seconds(self.h)
+
     def trace_json(self) -> str:
         p = C.c_void_p()
         check(lib().db_run_trace_json(self.h, C.byref(p)))
