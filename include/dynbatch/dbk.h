@@ -168,9 +168,11 @@ int dbk_moe_combine_fp64(int64_t T, int32_t k, int32_t d, const double* weights,
  * slot-order combine. */
 int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int32_t* tile_expert,
                         int32_t* tile_rb, int32_t* n_tiles, void* stream);
-int dbk_moe_bf16_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* offsets,
-                          const int32_t* pstart, const int32_t* tile_expert, const int32_t* order,
-                          const float* x, void* A,
+/* dispatch: row_of_item[item] = the item's padded row, then one warp per
+ * token writes bf16(x[token]) into its k rows of the SWIZZLE_128B tiled A
+ * (k ≤ 8, d a multiple of 256). */
+int dbk_moe_bf16_dispatch(int64_t T, int32_t k, int32_t d, const int32_t* order, const int32_t* ids,
+                          const int32_t* offsets, const int32_t* pstart, const float* x, void* A,
                           int32_t* row_of_item, int32_t blocks, void* stream);
 int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
                       const int32_t* tile_expert, const int32_t* tile_rb, const void* A,

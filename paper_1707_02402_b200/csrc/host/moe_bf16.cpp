@@ -127,14 +127,14 @@ void MoeBf16::upload_inputs(const float* x, cudaStream_t s) {
                         cudaMemcpyHostToDevice, s), "H2D inputs");
 }
 
-int MoeBf16::forward(const std::int32_t* /*ids*/, const double* wts, const std::int32_t* order,
+int MoeBf16::forward(const std::int32_t* ids, const double* wts, const std::int32_t* order,
                      const std::int32_t* offsets, cudaStream_t s, Profiler* prof) {
   Impl& I = *impl_;
   const int blocks = I.sms * 8;
   if (prof) prof->begin(3, s);
   check(dbk_moe_bf16_layout(I.n, offsets, I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(), I.n_tiles.get(), s),
         "moe layout");
-  check(dbk_moe_bf16_dispatch(I.n, I.k, I.d, offsets, I.pstart.get(), I.tile_expert.get(), order, I.x.get(), I.A.get(),
+  check(dbk_moe_bf16_dispatch(I.T, I.k, I.d, order, ids, offsets, I.pstart.get(), I.x.get(), I.A.get(),
                               I.row_of_item.get(), blocks, s),
         "moe dispatch");
   if (prof) prof->end(s);

@@ -190,12 +190,17 @@ void MoeSession::forward() {
     const double T = static_cast<double>(T_), k = static_cast<double>(c.active_per_example);
     const double es = impl_->precision == 0 ? 8.0 : 2.0;
     const double gemm = 2.0 * T * k * c.data_dim * static_cast<double>(c.hidden);
-    prof_.add_work(3, 0.0, T * c.experts * 8.0 + T * k * 12.0);
+    // class 3: scores read + routing written; the bf16 path also dispatches
+    // (fp32 x rows read once, k bf16 rows written per token)
+    const double dispatch = impl_->precision == 0 ? 0.0 : T * c.data_dim * 4.0 + T * k * c.data_dim * es;
+    prof_.add_work(3, 0.0, T * c.experts * 8.0 + T * k * 12.0 + dispatch);
     prof_.add_work(4, gemm, T * k * c.data_dim * es + c.experts * c.data_dim * static_cast<double>(c.hidden) * es +
                                 T * k * c.hidden * es);
+    // GEMM2 writes Y rows (fp64 path: 8 B, bf16 path: 2 B per element)
     prof_.add_work(5, gemm, T * k * c.hidden * es + c.experts * c.data_dim * static_cast<double>(c.hidden) * es +
-                                T * k * c.data_dim * 4.0);
-    prof_.add_work(6, 0.0, T * k * c.data_dim * 4.0 + T * c.data_dim * 4.0);
+                                T * k * c.data_dim * es);
+    // combine: k Y rows read and one fp32 (fp64) output row written per token
+    prof_.add_work(6, 0.0, T * k * c.data_dim * es + T * c.data_dim * (impl_->precision == 0 ? 8.0 : 4.0));
   }
 }
 

@@ -9,10 +9,16 @@
 // with fp32 accumulation.
 //
 // Layout: rows of expert e occupy a 128-aligned padded range starting at
-// pstart[e]. Activations are stored pre-tiled in the K-major SWIZZLE_NONE
-// operand layout: tile (row block rb, K chunk kc) is a contiguous 16 KB block
-// [8 k-groups][128 rows][8 elements], so each pipeline stage is one bulk copy.
-// Weights are pre-tiled the same way per (N tile, K chunk): [8][256 n][8].
+// pstart[e]. Activations are stored pre-tiled, so each pipeline stage is one
+// bulk copy of a contiguous 16 KB block per (row block rb, K chunk kc):
+//  * GEMM1's A (the dispatched x rows) in the K-major SWIZZLE_128B layout:
+//    row r's 64 elements are the 128-byte line r, 16-byte piece j at slot
+//    j ^ (r & 7) — a dispatched row is written as whole lines;
+//  * GEMM2's A (H, written by GEMM1's epilogue) in the K-major SWIZZLE_NONE
+//    layout [8 k-groups][128 rows][8 elements].
+// Weights are pre-tiled SWIZZLE_NONE per (N tile, K chunk): [8][256 n][8].
+// Padding rows of A and H are never initialised: their GEMM rows are never
+// read (the combine and the EP unpack read valid rows only).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -81,46 +87,53 @@ __global__ void __launch_bounds__(1024) k_moe_layout(int32_t n, const int32_t* _
   }
 }
 
-// One warp per padded row: row r of expert e holds item order[off_e + r]
-// (token = item / k); copies x[token] (fp32) → bf16 tiled A. Padding rows
-// are zero. row_of_item[item] = padded row (for the combine).
-__global__ void k_moe_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* __restrict__ offsets,
-                               const int32_t* __restrict__ pstart, const int32_t* __restrict__ tile_expert,
-                               const int32_t* __restrict__ order,
-                               const float* __restrict__ x, uint8_t* __restrict__ A,
-                               int32_t* __restrict__ row_of_item) {
-  // One block (128 threads) per 128-row block; thread = row, so each warp's
-  // 16-byte stores for a given 8-element group are 512 contiguous bytes of
-  // the tiled operand, and each lane reads whole 32-byte sectors of its row.
-  const int32_t total_rows = pstart[n];
+// Padded row of every item: the item at sorted position pos belongs to
+// expert e = ids[item] and sits at row pstart[e] + (pos − offsets[e]).
+__global__ void k_moe_item_rows(int64_t items, const int32_t* __restrict__ order, const int32_t* __restrict__ ids,
+                                const int32_t* __restrict__ offsets, const int32_t* __restrict__ pstart,
+                                int32_t* __restrict__ row_of_item) {
+  for (int64_t pos = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; pos < items;
+       pos += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t item = order[pos];
+    const int32_t e = ids[item];
+    row_of_item[item] = pstart[e] + static_cast<int32_t>(pos) - offsets[e];
+  }
+}
+
+// Byte offset of 16-byte piece j (elements 8j..8j+7 of K chunk kc) of padded
+// row `row` in the SWIZZLE_128B tiled A.
+__device__ __forceinline__ int64_t a_sw128_off(int32_t row, int32_t kchunks, int32_t kc, int32_t j) {
+  const int32_t rb = row / kBM, rr = row % kBM;
+  return (static_cast<int64_t>(rb) * kchunks + kc) * kABytes + rr * 128 + ((j ^ (rr & 7)) << 4);
+}
+
+// Token-major dispatch: one warp per token reads its fp32 row once
+// (coalesced) and writes the bf16 row into each of its k items' padded rows,
+// whole 128-byte lines (lane group g = lane / 8 covers K chunk 4·it + g,
+// lane e = lane % 8 its 16-byte piece e).
+__global__ void k_moe_dispatch(int64_t T, int32_t k, int32_t d, const float* __restrict__ x,
+                               const int32_t* __restrict__ row_of_item, uint8_t* __restrict__ A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const int32_t kchunks = d / kBK;
-  for (int32_t rb = blockIdx.x; rb * kBM < total_rows; rb += gridDim.x) {
-    const int32_t rr = threadIdx.x;
-    const int32_t row = rb * kBM + rr;
-    const int32_t e = tile_expert[rb];  // row blocks never straddle experts
-    const int32_t local = row - pstart[e];
-    const bool valid = local < offsets[e + 1] - offsets[e];
-    int32_t token = 0;
-    if (valid) {
-      const int32_t item = order[offsets[e] + local];
-      token = item / k;
-      row_of_item[item] = row;
-    }
-    const float* src = x + static_cast<int64_t>(token) * d;
-    uint8_t* dst = A + static_cast<int64_t>(rb) * kchunks * kABytes + rr * 16;
-#pragma unroll 4
-    for (int32_t gi = 0; gi < d / 8; ++gi) {  // 8-element group gi = k gi*8 .. gi*8+7
-      uint4 pk = make_uint4(0, 0, 0, 0);
-      if (valid) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(src + gi * 8));
-        const float4 b = __ldg(reinterpret_cast<const float4*>(src + gi * 8 + 4));
-        pk.x = pack_bf16x2(a.x, a.y);
-        pk.y = pack_bf16x2(a.z, a.w);
-        pk.z = pack_bf16x2(b.x, b.y);
-        pk.w = pack_bf16x2(b.z, b.w);
-      }
-      // block (kc = gi/8) at kc·16 KB, k-group (gi%8) at ·kBM·16
-      *reinterpret_cast<uint4*>(dst + (gi >> 3) * kABytes + (gi & 7) * kBM * 16) = pk;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += warps) {
+    const float* src = x + t * d;
+    int32_t rows[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) rows[s] = s < k ? row_of_item[t * k + s] : 0;
+    for (int32_t it = 0; it * 256 < d; ++it) {
+      const int32_t col = it * 256 + lane * 8;
+      const float4 a = __ldg(reinterpret_cast<const float4*>(src + col));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(src + col + 4));
+      uint4 pk;
+      pk.x = pack_bf16x2(a.x, a.y);
+      pk.y = pack_bf16x2(a.z, a.w);
+      pk.z = pack_bf16x2(b.x, b.y);
+      pk.w = pack_bf16x2(b.z, b.w);
+      const int32_t kc = col / kBK, j = (col % kBK) / 8;
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < k) *reinterpret_cast<uint4*>(A + a_sw128_off(rows[s], kchunks, kc, j)) = pk;
     }
   }
 }
@@ -204,7 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant_
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint64_t ad = smem_desc(a_base + s * kABytes + (2 * kk) * kBM * 16, kBM * 16, 128);
+            const uint64_t ad = EPI == 0 ? smem_desc_sw128(a_base + s * kABytes + kk * 32)
+                                         : smem_desc(a_base + s * kABytes + (2 * kk) * kBM * 16, kBM * 16, 128);
             const uint64_t bd = smem_desc(b_base + s * kBBytes + (2 * kk) * kBN * 16, kBN * 16, 128);
             mma_bf16(tmem_base + abuf * kBN, ad, bd, IDESC, (kc | kk) != 0);
           }
@@ -310,11 +324,14 @@ extern "C" int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* p
   return static_cast<int>(cudaGetLastError());
 }
 
-extern "C" int dbk_moe_bf16_dispatch(int32_t n, int32_t k, int32_t d, const int32_t* offsets, const int32_t* pstart,
-                                     const int32_t* tile_expert, const int32_t* order, const float* x, void* A, int32_t* row_of_item,
-                                     int32_t blocks, void* stream) {
-  k_moe_dispatch<<<blocks, kBM, 0, static_cast<cudaStream_t>(stream)>>>(n, k, d, offsets, pstart, tile_expert, order, x,
-                                                                        static_cast<uint8_t*>(A), row_of_item);
+extern "C" int dbk_moe_bf16_dispatch(int64_t T, int32_t k, int32_t d, const int32_t* order, const int32_t* ids,
+                                     const int32_t* offsets, const int32_t* pstart, const float* x, void* A,
+                                     int32_t* row_of_item, int32_t blocks, void* stream) {
+  if (T <= 0) return 0;
+  if (k > 8 || d % 256 != 0) return static_cast<int>(cudaErrorInvalidValue);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k_moe_item_rows<<<blocks, 256, 0, s>>>(T * k, order, ids, offsets, pstart, row_of_item);
+  k_moe_dispatch<<<blocks, 256, 0, s>>>(T, k, d, x, row_of_item, static_cast<uint8_t*>(A));
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -406,9 +423,10 @@ __global__ void k_moe_ep_layout(int32_t G, int32_t E, const int32_t* __restrict_
   *n_tiles = t;
 }
 
-// Received rows → tiled A operand (padding rows zero), expert e's rows in
-// source-rank order = the reference's (token, slot) order for that expert.
-// recv_of_row[padded row] = receive-buffer row (−1 for padding).
+// Received rows → the SWIZZLE_128B tiled A operand (one warp per padded
+// row, whole 128-byte lines), expert e's rows in source-rank order = the
+// reference's (token, slot) order for that expert. recv_of_row[padded row]
+// = receive-buffer row (−1 for padding, whose A rows are left unwritten).
 __global__ void k_moe_ep_scatter(int32_t G, int32_t d, const int32_t* __restrict__ pstart,
                                  const int32_t* __restrict__ tile_expert, const int32_t* __restrict__ src_row,
                                  const int32_t* __restrict__ cum, int32_t E,
@@ -416,27 +434,23 @@ __global__ void k_moe_ep_scatter(int32_t G, int32_t d, const int32_t* __restrict
                                  int32_t* __restrict__ recv_of_row) {
   const int32_t total_rows = pstart[E];
   const int32_t kchunks = d / kBK;
-  for (int32_t rb = blockIdx.x; rb * kBM < total_rows; rb += gridDim.x) {
-    const int32_t rr = threadIdx.x;
-    const int32_t row = rb * kBM + rr;
-    const int32_t e = tile_expert[rb];
+  const int lane = threadIdx.x & 31;
+  const int32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (int32_t row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < total_rows; row += warps) {
+    const int32_t e = tile_expert[row / kBM];
     const int32_t local = row - pstart[e];
     const int32_t* ce = cum + e * (G + 1);
-    const bool valid = local < ce[G];
     int32_t src = -1;
-    if (valid) {
+    if (local < ce[G]) {
       int32_t r = 0;
       while (local >= ce[r + 1]) ++r;
       src = src_row[e * G + r] + (local - ce[r]);
     }
-    recv_of_row[row] = src;
-    const uint4* s4 = reinterpret_cast<const uint4*>(recv + static_cast<int64_t>(valid ? src : 0) * d);
-    uint8_t* dst = A + static_cast<int64_t>(rb) * kchunks * kABytes + rr * 16;
-#pragma unroll 4
-    for (int32_t gi = 0; gi < d / 8; ++gi) {
-      const uint4 pk = valid ? __ldg(s4 + gi) : make_uint4(0, 0, 0, 0);
-      *reinterpret_cast<uint4*>(dst + (gi >> 3) * kABytes + (gi & 7) * kBM * 16) = pk;
-    }
+    if (lane == 0) recv_of_row[row] = src;
+    if (src < 0) continue;
+    const uint4* s4 = reinterpret_cast<const uint4*>(recv + static_cast<int64_t>(src) * d);
+    for (int32_t gi = lane; gi < d / 8; gi += 32)
+      *reinterpret_cast<uint4*>(A + a_sw128_off(row, kchunks, gi >> 3, gi & 7)) = __ldg(s4 + gi);
   }
 }
 

@@ -128,7 +128,8 @@ struct Item {
 struct StepParams {
   int32_t step, epoch, lookahead, debug;
   int32_t diag;  // timing diagnostics only (wrong results): bit 0 skips weight reloads, bit 1 window
-                 // reloads, bit 2 the epilogue work (TMEM loads, transposes, stores)
+                 // reloads, bit 2 the epilogue work (TMEM loads, transposes, stores), bit 3 only its stores
+  int32_t cache;  // epilogue store hints: bit 0 streaming for next-launch data, bit 1 evict-last for this launch's
   const int32_t* step_tile_begin;
   const int32_t* tile_group;
   const int32_t* tile_q0;
@@ -351,6 +352,31 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
   const int64_t own_off = L.chunk_off + (static_cast<int64_t>(kGuard + it.q0 + L.half * 128 + L.e) << 7) + (L.sub << 4);
   uint8_t* own = (KIND == 0 ? P.stage_x : P.stage_mid) + own_off;
   uint8_t* own_lo = P.stage_lo + own_off;
+  const bool stream = (P.cache & 1) != 0, keep = (P.cache & 2) != 0;
+  // diag bit 4: every store lands in one L2-resident 16-byte slot per thread
+  // (same instructions, no DRAM traffic)
+  const bool l2sink = (P.diag & 16) != 0;
+  uint8_t* const sink_slot = P.stage_mid + ((static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) << 4);
+  const uint64_t pol = keep ? l2_policy_evict_last() : 0;
+  if (P.diag & 8) {  // timing diagnostic: TMEM loads, transposes and math, no stores
+    float sink = 0.f;
+#pragma unroll 2
+    for (int cb = 0; cb < kChunks; ++cb) {
+      float v[kChunk];
+      tmem_ld16(taddr + cb * kChunk, v);
+      const PosEntry* my = tab + L.half * 128 + cb * kChunk + L.e;
+#pragma unroll
+      for (int m = 0; m < kChunk / 8; ++m) {
+        float* x = v + 8 * m;
+        transpose8(x, L.e);
+        const PosEntry& pe = my[8 * m];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sink += pe.valid ? fmaxf(x[k] + bias[k], 0.f) : 0.f;
+      }
+    }
+    if (sink == 1.2345e-30f) *own = 0;
+    return;
+  }
 #pragma unroll 2
   for (int cb = 0; cb < kChunks; ++cb) {
     float v[kChunk];
@@ -371,12 +397,22 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
         pk.y = pack_f16x2(o[2], o[3]);
         pk.z = pack_f16x2(o[4], o[5]);
         pk.w = pack_f16x2(o[6], o[7]);
-        *reinterpret_cast<uint4*>(own + off) = pk;
+        if (l2sink) st_v4(sink_slot, pk);
+        else if (keep) st_hint_v4(own + off, pk, pol);
+        else *reinterpret_cast<uint4*>(own + off) = pk;
       } else if (KIND == 0) {
         uint4 hi, lo;
         split_f16x8(o, hi, lo);
-        *reinterpret_cast<uint4*>(own + off) = hi;
-        *reinterpret_cast<uint4*>(own_lo + off) = lo;
+        if (l2sink) {
+          st_v4(sink_slot, hi);
+          st_v4(sink_slot, lo);
+        } else if (keep) {
+          st_hint_v4(own + off, hi, pol);
+          st_hint_v4(own_lo + off, lo, pol);
+        } else {
+          *reinterpret_cast<uint4*>(own + off) = hi;
+          *reinterpret_cast<uint4*>(own_lo + off) = lo;
+        }
       } else if (!pe.valid) {
         // pad position of a forwarded image: zero in the parent's conv3x3 #1
         // operand (its taps read the pads); lo and [x; y] pads only reach
@@ -389,13 +425,31 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
           split_f16x8(o, hi, lo);
           const int p = L.plane + (pe.fwd_buf == 2 ? 16 : 0);
           const int64_t off = stage_off(P.ps, p, pe.fwd_row);
-          *reinterpret_cast<uint4*>((pe.fwd_buf == 0 ? P.stage_x : P.stage_cat) + off) = hi;
-          if (pe.fwd_buf == 0) *reinterpret_cast<uint4*>(P.stage_lo + off) = lo;
+          uint8_t* hp = (pe.fwd_buf == 0 ? P.stage_x : P.stage_cat) + off;
+          if (l2sink) {
+            st_v4(sink_slot, hi);
+            if (pe.fwd_buf == 0) st_v4(sink_slot, lo);
+          } else if (stream) {
+            st_cs_v4(hp, hi);
+            if (pe.fwd_buf == 0) st_cs_v4(P.stage_lo + off, lo);
+          } else {
+            *reinterpret_cast<uint4*>(hp) = hi;
+            if (pe.fwd_buf == 0) *reinterpret_cast<uint4*>(P.stage_lo + off) = lo;
+          }
         }
         if (pe.dst) {
           float4* dp = reinterpret_cast<float4*>(pe.dst + L.plane_off32);
-          dp[0] = make_float4(o[0], o[1], o[2], o[3]);
-          dp[1] = make_float4(o[4], o[5], o[6], o[7]);
+          const float4 d0 = make_float4(o[0], o[1], o[2], o[3]), d1 = make_float4(o[4], o[5], o[6], o[7]);
+          if (l2sink) {
+            st_v4(sink_slot, *reinterpret_cast<const uint4*>(&d0));
+            st_v4(sink_slot, *reinterpret_cast<const uint4*>(&d1));
+          } else if (stream) {
+            st_cs_v4(dp, *reinterpret_cast<const uint4*>(&d0));
+            st_cs_v4(dp + 1, *reinterpret_cast<const uint4*>(&d1));
+          } else {
+            dp[0] = d0;
+            dp[1] = d1;
+          }
         }
       }
     }
@@ -504,6 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       constexpr uint32_t IDESC = idesc_f16_f32(128, kTileM);
       long long w_acc = 0, w_a = 0, w_b = 0;
       const long long t_start = clock64();
+      const uint64_t ns_start = DBG ? global_ns() : 0;
       uint32_t ai = 0, bi = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       for (int n = 0;; ++n) {
@@ -557,6 +612,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         atomicAdd(&g_conv_dbg[12 + 1], static_cast<unsigned long long>(w_a));
         atomicAdd(&g_conv_dbg[12 + 2], static_cast<unsigned long long>(w_b));
         atomicAdd(&g_conv_dbg[12 + 3], static_cast<unsigned long long>(clock64() - t_start));
+        // effective SM clock over the loop: cycles / wall nanoseconds
+        atomicAdd(&g_conv_dbg[20], static_cast<unsigned long long>(clock64() - t_start));
+        atomicAdd(&g_conv_dbg[21], static_cast<unsigned long long>(global_ns() - ns_start));
       }
     }
   } else if (warp == kWeightWarp) {
@@ -1014,6 +1072,8 @@ extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile
   p.debug = g_debug_flag;
   const char* dg = std::getenv("DYNBATCH_DIAG");
   p.diag = dg ? std::atoi(dg) : 0;
+  const char* ch = std::getenv("DYNBATCH_CACHE");
+  p.cache = ch ? std::atoi(ch) : 0;
   p.step_tile_begin = step_tile_begin;
   p.tile_group = tile_group;
   p.tile_q0 = tile_q0;

@@ -159,13 +159,14 @@ struct ExplicitKey {
 };
 
 // Per-(key, segment) counts into hist[key * nseg + seg] (pre-zeroed).
-template <class Key>
+template <class Key, int SEG = kSeg>
 __global__ void k_seg_hist(int64_t n, int32_t nseg, Key key, int32_t* __restrict__ hist) {
   const int lane = threadIdx.x & 31;
   const int32_t seg = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (seg >= nseg) return;
-  const int64_t begin = static_cast<int64_t>(seg) * kSeg;
-  for (int it = 0; it < kSeg / 32; ++it) {
+  const int64_t begin = static_cast<int64_t>(seg) * SEG;
+#pragma unroll
+  for (int it = 0; it < SEG / 32; ++it) {
     const int64_t i = begin + it * 32 + lane;
     const int32_t k = i < n ? key(i) : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, k);
@@ -330,15 +331,16 @@ __global__ void k_scan_groups(int64_t n, int32_t nseg, int32_t p, int32_t* __res
 // Stable scatter: each warp walks its segment in order; the lowest lane of
 // each equal-key peer set claims popc(peers) slots from the (key, segment)
 // cursor, which no other warp touches.
-template <class Key>
+template <class Key, int SEG = kSeg>
 __global__ void k_seg_scatter(int64_t n, int32_t nseg, Key key, int32_t* __restrict__ hist,
                               int32_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int32_t seg = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (seg >= nseg) return;
-  const int64_t begin = static_cast<int64_t>(seg) * kSeg;
+  const int64_t begin = static_cast<int64_t>(seg) * SEG;
   const unsigned lt = (1u << lane) - 1u;
-  for (int it = 0; it < kSeg / 32; ++it) {
+#pragma unroll
+  for (int it = 0; it < SEG / 32; ++it) {
     const int64_t i = begin + it * 32 + lane;
     const int32_t k = i < n ? key(i) : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, k);
@@ -354,7 +356,12 @@ __global__ void k_seg_scatter(int64_t n, int32_t nseg, Key key, int32_t* __restr
   }
 }
 
-inline int32_t n_segments(int64_t n) { return static_cast<int32_t>((n + kSeg - 1) / kSeg); }
+inline int32_t n_segments(int64_t n, int seg = kSeg) { return static_cast<int32_t>((n + seg - 1) / seg); }
+
+// Generic stable sort segment: short segments (more warps in flight) when
+// the (key, segment) table stays small.
+constexpr int kSegSmall = 64;
+inline int generic_seg(int32_t n_keys) { return n_keys <= 128 ? kSegSmall : kSeg; }
 
 }  // namespace
 
@@ -434,11 +441,15 @@ extern "C" int dbk_stable_bucket_sort(int64_t n_items, int32_t n_keys, const int
                                       int32_t* seg_hist, int32_t* order, int32_t* offsets,
                                       void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int32_t nseg = n_segments(n_items) > 0 ? n_segments(n_items) : 1;
+  const int seg = generic_seg(n_keys);
+  const int32_t nseg = n_segments(n_items, seg) > 0 ? n_segments(n_items, seg) : 1;
   cudaMemsetAsync(seg_hist, 0, sizeof(int32_t) * static_cast<size_t>(n_keys) * nseg, s);
   ExplicitKey key{keys};
   const int blocks = (nseg + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  k_seg_hist<<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist);
+  if (seg == kSegSmall)
+    k_seg_hist<ExplicitKey, kSegSmall><<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist);
+  else
+    k_seg_hist<ExplicitKey, kSeg><<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist);
   int32_t* totals = seg_hist + static_cast<int64_t>(n_keys) * nseg;
   const unsigned sblk = static_cast<unsigned>((static_cast<int64_t>(n_keys) * nseg + kScanChunk - 1) / kScanChunk);
   k_scan_partial<<<sblk, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, seg_hist, totals);
@@ -446,12 +457,18 @@ extern "C" int dbk_stable_bucket_sort(int64_t n_items, int32_t n_keys, const int
   k_scan_add<<<sblk, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, seg_hist, totals);
   k_scan_groups<<<1, 1024, 0, s>>>(n_items, nseg, 1, seg_hist, nullptr, n_keys, nullptr, nullptr,
                                    nullptr, offsets);
-  k_seg_scatter<<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist, order);
+  if (seg == kSegSmall)
+    k_seg_scatter<ExplicitKey, kSegSmall><<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist, order);
+  else
+    k_seg_scatter<ExplicitKey, kSeg><<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist, order);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int64_t dbk_bucket_sort_scratch(int64_t n_items, int32_t max_keys) {
-  const int64_t nseg = n_items > 0 ? (n_items + kSeg - 1) / kSeg : 1;
+  // the larger of the scheduler's table (kSeg segments) and the generic
+  // sort's (generic_seg(max_keys) segments)
+  const int seg = generic_seg(max_keys) < kSeg ? generic_seg(max_keys) : kSeg;
+  const int64_t nseg = n_items > 0 ? (n_items + seg - 1) / seg : 1;
   const int64_t table = static_cast<int64_t>(max_keys) * nseg;
   return table + table / kScanChunk + 64;
 }

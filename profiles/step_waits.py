@@ -21,3 +21,5 @@ print(f"step kernel ms/fwd {kt.ms[4] / 5:.3f}: acc_wait {acc/tot:6.1%}  A_wait {
 it, dep, sl, ptot = (int(x) for x in w[4])
 print(f"window producer: item-ring wait {it/ptot:6.1%}  dependency wait {dep/ptot:6.1%}  "
       f"slot wait {sl/ptot:6.1%}  issuing {(ptot-it-dep-sl)/ptot:6.1%}")
+cyc, ns = int(w[5][0]), int(w[5][1])
+print(f"effective SM clock in the MMA loop: {cyc / max(ns, 1) * 1e3:.0f} MHz")
