@@ -116,7 +116,7 @@ __global__ void k_topk(int64_t T, int32_t n, int32_t k, const double* __restrict
 // use the denominator summed in rank order. Non-finite scores are rejected
 // before anything is written (src/moe.cpp:41).
 template <int K>
-__global__ void __launch_bounds__(128) k_topk_small(int64_t T, int32_t n, const double* __restrict__ scores,
+__global__ void __launch_bounds__(64) k_topk_small(int64_t T, int32_t n, const double* __restrict__ scores,
                                                     int32_t* __restrict__ ids, double* __restrict__ weights,
                                                     int32_t* __restrict__ err) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -127,10 +127,17 @@ __global__ void __launch_bounds__(128) k_topk_small(int64_t T, int32_t n, const 
 #pragma unroll
   for (int q = 0; q < K; ++q) { tv[q] = -INFINITY; ti[q] = 0x7fffffff; }
   bool bad = false;
+  // 128-byte rounds, the next round's loads issued before this one is ranked
+  double2 nx[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) nx[u] = 2 * u < n ? __ldg(row + u) : make_double2(-INFINITY, -INFINITY);
   for (int32_t j0 = 0; j0 < n; j0 += 16) {
     double2 c[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) c[u] = j0 + 2 * u < n ? __ldg(row + j0 / 2 + u) : make_double2(-INFINITY, -INFINITY);
+    for (int u = 0; u < 8; ++u) c[u] = nx[u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      nx[u] = j0 + 16 + 2 * u < n ? __ldg(row + (j0 + 16) / 2 + u) : make_double2(-INFINITY, -INFINITY);
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int32_t j = j0 + u;
@@ -271,7 +278,7 @@ __global__ void k_combine_fp64(int64_t T, int32_t k, int32_t d, const double* __
 template <int K>
 int launch_topk_small(int64_t T, int32_t n, const double* scores, int32_t* ids, double* weights, int32_t* err,
                       cudaStream_t s) {
-  k_topk_small<K><<<static_cast<unsigned>((T + 127) / 128), 128, 0, s>>>(T, n, scores, ids, weights, err);
+  k_topk_small<K><<<static_cast<unsigned>((T + 63) / 64), 64, 0, s>>>(T, n, scores, ids, weights, err);
   return static_cast<int>(cudaGetLastError());
 }
 
