@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--workload", default="cfg3", choices=sorted(CFG) + sorted(MOE))
     ap.add_argument("--no-moe", action="store_true", help="skip the secondary cfg4 MoE measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ep-chunks", type=int, default=0,
+                    help="cfg5: expert ranges the exchange is cut into (overlap with the GEMMs); 0 = 1 at one GPU, "
+                         "else 4")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the bounded CPU-baseline sample")
     return ap.parse_args()
@@ -479,16 +482,17 @@ def run_moe_ep(args, dist, name):
     torch.cuda.set_device(dist.local)
     T = c["tokens_per_gpu"] * N
     layer = MoeEpLayer(c["experts"], c["k"], T, c["d"], c["h"], seed=0)
+    chunks = args.ep_chunks or (1 if N == 1 else 4)
     clk = ClockSampler(dist.local).start()
     for _ in range(3):
-        layer.forward()
+        layer.forward(chunks)
     layer.sess.synchronize()
     dist.barrier()
     t0 = time.time()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(layer.stream)
     for _ in range(args.steps):
-        layer.forward()
+        layer.forward(chunks)
     e1.record(layer.stream)
     e1.synchronize()
     dist.barrier()
@@ -504,7 +508,8 @@ def run_moe_ep(args, dist, name):
             "ms_per_step": ms_step, "dtype": "bf16 tensor-core operands, fp32 accumulate",
             "config": {"workload": f"{name}: n={c['experts']} top-{c['k']} d={c['d']} h={c['h']}, "
                                    f"{c['tokens_per_gpu']} tokens/GPU, experts {c['experts'] // N}/GPU",
-                       "global_tokens": T, "parallelism": f"ep{N} (NCCL all-to-all dispatch + combine)"},
+                       "global_tokens": T, "parallelism": f"ep{N} (NCCL all-to-all dispatch + combine)",
+                       "exchange_chunks": chunks},
             "roofline": {"kernel": "whole EP layer (gate, sort, pack, 2x all-to-all, grouped GEMMs, combine)",
                          "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "TFLOP/s per GPU", "frac": round(achieved / peak, 4) if peak else None,

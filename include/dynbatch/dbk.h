@@ -174,9 +174,14 @@ int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int3
 int dbk_moe_bf16_dispatch(int64_t T, int32_t k, int32_t d, const int32_t* order, const int32_t* ids,
                           const int32_t* offsets, const int32_t* pstart, const float* x, void* A,
                           int32_t* row_of_item, int32_t blocks, void* stream);
+/* row tiles [tile_begin, tile_end) of the tile list (tile_end < 0: all
+ * *n_tiles); EP chunks run one contiguous expert range at a time. epi 1:
+ * padded row r's output goes to Y row out_row[r] (skipped when < 0; out_row
+ * NULL = row r) — the EP receive order directly, no unpack pass. */
 int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
                       const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
-                      const void* const* W, void* H, void* Y, int32_t sms, void* stream);
+                      const void* const* W, void* H, void* Y, int32_t tile_begin, int32_t tile_end,
+                      const int32_t* out_row, int32_t sms, void* stream);
 int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const double* weights,
                          const int32_t* row_of_item, const void* Y, float* out, void* stream);
 
@@ -184,17 +189,15 @@ int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const double* weights,
  * (bf16) with pos_of_item[item] = row; receiver layout from the count matrix
  * cnt[G][E] (source × local expert); scatter received rows into the tiled
  * GEMM operand (expert-major, source-rank order within an expert) with
- * recv_of_row[padded row] = receive row (−1: padding); unpack the GEMM2
- * rows back into receive order. */
+ * recv_of_row[padded row] = receive row (−1: padding), which GEMM2's
+ * epilogue uses to write its rows back in receive order (out_row). */
 int dbk_moe_ep_pack(int64_t items, int32_t k, int32_t d, const int32_t* order, const float* x, void* send,
                     int32_t* pos_of_item, int32_t blocks, void* stream);
 int dbk_moe_ep_layout(int32_t G, int32_t E, const int32_t* cnt, int32_t* pstart, int32_t* tile_expert,
                       int32_t* tile_rb, int32_t* n_tiles, int32_t* src_row, int32_t* cum, void* stream);
 int dbk_moe_ep_scatter(int32_t G, int32_t E, int32_t d, const int32_t* pstart, const int32_t* tile_expert,
                        const int32_t* src_row, const int32_t* cum, const void* recv, void* A,
-                       int32_t* recv_of_row, int32_t blocks, void* stream);
-int dbk_moe_ep_unpack(int32_t E, int32_t d, const int32_t* pstart, const int32_t* recv_of_row, const void* Y,
-                      void* ret, int32_t blocks, void* stream);
+                       int32_t* recv_of_row, int32_t row_begin, int32_t row_end, int32_t blocks, void* stream);
 
 #ifdef __cplusplus
 }

@@ -196,6 +196,13 @@ DYNBATCH_API db_status db_moe_ep_sizes(db_moe_ep_session* s, int64_t* tokens, in
 DYNBATCH_API db_status db_moe_ep_dispatch(db_moe_ep_session* s, void* send_rows, int32_t* expert_counts);
 DYNBATCH_API db_status db_moe_ep_experts(db_moe_ep_session* s, const void* recv_rows, const int32_t* recv_counts,
                                          void* ret_rows);
+/* db_moe_ep_experts in pieces, for exchanges chunked by expert: the layout
+ * from recv_counts once, then contiguous local-expert ranges [e_begin,
+ * e_end) as their rows arrive (recv_rows / ret_rows as for _experts; each
+ * call reads and writes only its experts' rows). */
+DYNBATCH_API db_status db_moe_ep_layout(db_moe_ep_session* s, const int32_t* recv_counts);
+DYNBATCH_API db_status db_moe_ep_experts_range(db_moe_ep_session* s, const void* recv_rows, void* ret_rows,
+                                               int32_t e_begin, int32_t e_end);
 DYNBATCH_API db_status db_moe_ep_combine(db_moe_ep_session* s, const void* ret_rows);
 DYNBATCH_API db_status db_moe_ep_outputs(db_moe_ep_session* s, float* out);
 DYNBATCH_API db_status db_moe_ep_synchronize(db_moe_ep_session* s);

@@ -169,6 +169,8 @@ SIGNATURES = {
     "db_moe_ep_sizes": (C.c_int32, [VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "db_moe_ep_dispatch": (C.c_int32, [VP, VP, VP]),
     "db_moe_ep_experts": (C.c_int32, [VP, VP, VP, VP]),
+    "db_moe_ep_layout": (C.c_int32, [VP, VP]),
+    "db_moe_ep_experts_range": (C.c_int32, [VP, VP, VP, C.c_int32, C.c_int32]),
     "db_moe_ep_combine": (C.c_int32, [VP, VP]),
     "db_moe_ep_outputs": (C.c_int32, [VP, VP]),
     "db_moe_ep_synchronize": (C.c_int32, [VP]),
@@ -555,6 +557,15 @@ class MoeEpSession(_Handle):
     def experts(self, recv_ptr: int, recv_counts: np.ndarray, ret_ptr: int):
         cnt = np.ascontiguousarray(recv_counts, np.int32).reshape(self.world, self.local_experts)
         check(lib().db_moe_ep_experts(self.h, C.c_void_p(recv_ptr), _ptr(cnt), C.c_void_p(ret_ptr)))
+
+    def layout(self, recv_counts: np.ndarray):
+        """Receive-side layout for the chunked form of experts()."""
+        cnt = np.ascontiguousarray(recv_counts, np.int32).reshape(self.world, self.local_experts)
+        check(lib().db_moe_ep_layout(self.h, _ptr(cnt)))
+
+    def experts_range(self, recv_ptr: int, ret_ptr: int, e_begin: int, e_end: int):
+        """Local experts [e_begin, e_end) only (after layout())."""
+        check(lib().db_moe_ep_experts_range(self.h, C.c_void_p(recv_ptr), C.c_void_p(ret_ptr), e_begin, e_end))
 
     def combine(self, ret_ptr: int):
         check(lib().db_moe_ep_combine(self.h, C.c_void_p(ret_ptr)))

@@ -635,6 +635,17 @@ db_status db_moe_ep_experts(db_moe_ep_session* s, const void* recv_rows, const i
   return guarded([&] { s->s->experts(recv_rows, recv_counts, ret_rows); });
 }
 
+db_status db_moe_ep_layout(db_moe_ep_session* s, const int32_t* recv_counts) {
+  if (!s || !recv_counts) return null_arg();
+  return guarded([&] { s->s->layout(recv_counts); });
+}
+
+db_status db_moe_ep_experts_range(db_moe_ep_session* s, const void* recv_rows, void* ret_rows, int32_t e_begin,
+                                  int32_t e_end) {
+  if (!s) return null_arg();
+  return guarded([&] { s->s->experts_range(recv_rows, ret_rows, e_begin, e_end); });
+}
+
 db_status db_moe_ep_combine(db_moe_ep_session* s, const void* ret_rows) {
   if (!s || !ret_rows) return null_arg();
   return guarded([&] { s->s->combine(ret_rows); });

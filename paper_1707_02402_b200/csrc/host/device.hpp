@@ -317,6 +317,11 @@ class MoeEp {
   // cnt[G][E_local] (host); ret (device bf16) gets the expert outputs in
   // receive order.
   void experts(const void* recv, const std::int32_t* cnt, void* ret);
+  // The same in pieces, for exchanges chunked by expert: layout(cnt) once,
+  // then experts_range for contiguous local-expert ranges, each as soon as
+  // its rows have arrived (rows of other experts may still be in flight).
+  void layout(const std::int32_t* cnt);
+  void experts_range(const void* recv, void* ret, int e_begin, int e_end);
   // ret_recv = the rank's own rows back, in its sorted order → outputs.
   void combine(const void* ret_recv);
   void download_outputs(float* out);

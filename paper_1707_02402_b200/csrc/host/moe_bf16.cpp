@@ -140,12 +140,12 @@ int MoeBf16::forward(const std::int32_t* ids, const double* wts, const std::int3
   if (prof) prof->end(s);
   if (prof) prof->begin(4, s);
   check(dbk_moe_bf16_gemm(0, I.n, I.d, I.h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
-                          I.w1tab.get(), I.H.get(), nullptr, I.sms, s),
+                          I.w1tab.get(), I.H.get(), nullptr, 0, -1, nullptr, I.sms, s),
         "moe gemm1");
   if (prof) prof->end(s);
   if (prof) prof->begin(5, s);
   check(dbk_moe_bf16_gemm(1, I.n, I.h, I.d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
-                          I.w2tab.get(), nullptr, I.Y.get(), I.sms, s),
+                          I.w2tab.get(), nullptr, I.Y.get(), 0, -1, nullptr, I.sms, s),
         "moe gemm2");
   if (prof) prof->end(s);
   if (prof) prof->begin(6, s);

@@ -298,10 +298,11 @@ struct MoeEp::Impl {
   Buf<float> x, out;
   Buf<std::int32_t> pos_of_item, cnt, pstart, tile_expert, tile_rb, n_tiles, src_row, cum, recv_of_row;
   Buf<std::uint8_t> A, H;
-  Buf<std::uint16_t> Y;
   Buf<std::uint16_t> w1, w2;
   Buf<const void*> w1tab, w2tab;
-  std::int64_t cap_rows = 0;  // padded-row capacity of A / H / Y
+  std::int64_t cap_rows = 0;  // padded-row capacity of A / H
+  std::vector<std::int32_t> cnt_h;    // last layout's counts [G][E]
+  std::vector<std::int64_t> pstart_h; // and its padded expert starts [E+1]
 
   void ensure_capacity(std::int64_t rows) {
     if (rows <= cap_rows) return;
@@ -309,7 +310,6 @@ struct MoeEp::Impl {
     const size_t r = static_cast<size_t>(cap_rows);
     A.alloc(r * cfg.data_dim * 2);
     H.alloc(r * cfg.hidden * 2);
-    Y.alloc(r * cfg.data_dim);
     tile_expert.alloc(r / 128 + 1);
     tile_rb.alloc(r / 128 + 1);
     recv_of_row.alloc(r);
@@ -379,35 +379,56 @@ void MoeEp::dispatch(void* send, std::int32_t* expert_counts) {
   for (int e = 0; e < D.n; ++e) expert_counts[e] = off[static_cast<size_t>(e) + 1] - off[static_cast<size_t>(e)];
 }
 
-void MoeEp::experts(const void* recv, const std::int32_t* cnt, void* ret) {
+void MoeEp::layout(const std::int32_t* cnt) {
   Impl& I = *impl_;
-  const int G = I.world, E = I.E, d = static_cast<int>(I.cfg.data_dim), h = static_cast<int>(I.cfg.hidden);
-  std::int64_t padded = 0;
+  const int G = I.world, E = I.E;
+  I.cnt_h.assign(cnt, cnt + static_cast<size_t>(G) * E);
+  I.pstart_h.assign(static_cast<size_t>(E) + 1, 0);
   for (int e = 0; e < E; ++e) {
     std::int64_t tot = 0;
     for (int r = 0; r < G; ++r) tot += cnt[r * E + e];
-    padded += (tot + 127) / 128 * 128;
+    I.pstart_h[static_cast<size_t>(e) + 1] = I.pstart_h[static_cast<size_t>(e)] + (tot + 127) / 128 * 128;
   }
-  I.ensure_capacity(padded);
+  I.ensure_capacity(I.pstart_h[static_cast<size_t>(E)]);
   check(cudaMemcpyAsync(I.cnt.get(), cnt, sizeof(std::int32_t) * static_cast<size_t>(G) * E, cudaMemcpyHostToDevice,
                         stream_), "H2D counts");
-  prof_.begin(4, stream_);
   check(dbk_moe_ep_layout(G, E, I.cnt.get(), I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(), I.n_tiles.get(),
                           I.src_row.get(), I.cum.get(), stream_), "ep layout");
+}
+
+// Local experts [e_begin, e_end): their padded rows are one contiguous
+// range, their row tiles too (the layout is expert-major).
+void MoeEp::experts_range(const void* recv, void* ret, int e_begin, int e_end) {
+  Impl& I = *impl_;
+  const int G = I.world, E = I.E, d = static_cast<int>(I.cfg.data_dim), h = static_cast<int>(I.cfg.hidden);
+  if (I.pstart_h.size() != static_cast<size_t>(E) + 1) throw_error(Errc::invalid_argument, "db_moe_ep_layout first");
+  if (e_begin < 0 || e_end > E || e_begin > e_end) throw_error(Errc::invalid_argument, "expert range out of bounds");
+  if (e_begin == e_end) return;
+  const std::int32_t r0 = static_cast<std::int32_t>(I.pstart_h[static_cast<size_t>(e_begin)]);
+  const std::int32_t r1 = static_cast<std::int32_t>(I.pstart_h[static_cast<size_t>(e_end)]);
+  if (r0 == r1) return;
+  prof_.begin(4, stream_);
   check(dbk_moe_ep_scatter(G, E, d, I.pstart.get(), I.tile_expert.get(), I.src_row.get(), I.cum.get(), recv,
-                           I.A.get(), I.recv_of_row.get(), I.sms * 8, stream_), "ep scatter");
+                           I.A.get(), I.recv_of_row.get(), r0, r1, I.sms * 8, stream_), "ep scatter");
   check(dbk_moe_bf16_gemm(0, E, d, h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
-                          I.w1tab.get(), I.H.get(), nullptr, I.sms, stream_), "ep gemm1");
+                          I.w1tab.get(), I.H.get(), nullptr, r0 / 128, r1 / 128, nullptr, I.sms, stream_),
+        "ep gemm1");
+  // GEMM2 writes each output row straight to its receive-order row of ret
   check(dbk_moe_bf16_gemm(1, E, h, d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
-                          I.w2tab.get(), nullptr, I.Y.get(), I.sms, stream_), "ep gemm2");
-  check(dbk_moe_ep_unpack(E, d, I.pstart.get(), I.recv_of_row.get(), I.Y.get(), ret, I.sms * 8, stream_),
-        "ep unpack");
+                          I.w2tab.get(), nullptr, ret, r0 / 128, r1 / 128, I.recv_of_row.get(), I.sms, stream_),
+        "ep gemm2");
   prof_.end(stream_);
   if (prof_.on) {
     std::int64_t rows = 0;
-    for (int i = 0; i < G * E; ++i) rows += cnt[i];
+    for (int r = 0; r < G; ++r)
+      for (int e = e_begin; e < e_end; ++e) rows += I.cnt_h[static_cast<size_t>(r) * E + e];
     prof_.add_work(4, 4.0 * static_cast<double>(rows) * d * h, 0.0);
   }
+}
+
+void MoeEp::experts(const void* recv, const std::int32_t* cnt, void* ret) {
+  layout(cnt);
+  experts_range(recv, ret, 0, impl_->E);
 }
 
 void MoeEp::combine(const void* ret_recv) {

@@ -17,7 +17,6 @@
 
 namespace {
 
-constexpr int kLocal = 8;  // per-lane candidate list length for one pass
 
 // Rank order of the reference: higher score first, lower id on ties; `==`
 // on doubles makes -0.0 tie with +0.0.
@@ -25,7 +24,8 @@ __device__ __forceinline__ bool ranks_before(double va, int ia, double vb, int i
   return va > vb || (va == vb && ia < ib);
 }
 
-__global__ void k_topk(int64_t T, int32_t n, int32_t k, const double* __restrict__ scores,
+template <int kLocal>
+__global__ void __launch_bounds__(256, kLocal == 4 ? 4 : 2) k_topk(int64_t T, int32_t n, int32_t k, const double* __restrict__ scores,
                        int32_t* __restrict__ ids, double* __restrict__ weights,
                        int32_t* __restrict__ err) {
   extern __shared__ double sel_v[];  // [warps][k]
@@ -44,11 +44,10 @@ __global__ void k_topk(int64_t T, int32_t n, int32_t k, const double* __restrict
 #pragma unroll
     for (int q = 0; q < kLocal; ++q) { lv[q] = -INFINITY; li[q] = 0x7fffffff; }
     bool bad = false;
-    for (int32_t j = lane; j < n; j += 32) {
-      const double v = __ldg(row + j);
+    auto consider = [&](double v, int j) {
       bad |= !isfinite(v);
-      if (thr_i >= 0 && !ranks_before(thr_v, thr_i, v, j)) continue;
-      if (!ranks_before(v, j, lv[kLocal - 1], li[kLocal - 1])) continue;
+      if (thr_i >= 0 && !ranks_before(thr_v, thr_i, v, j)) return;
+      if (!ranks_before(v, j, lv[kLocal - 1], li[kLocal - 1])) return;
       // insertion into the lane's sorted candidate list
       double cv = v;
       int ci = j;
@@ -60,6 +59,38 @@ __global__ void k_topk(int64_t T, int32_t n, int32_t k, const double* __restrict
           lv[q] = cv; li[q] = ci; cv = tv; ci = ti;
         }
       }
+    };
+    if ((n & 1) == 0) {
+      // 16-byte loads, 512 contiguous bytes per warp and round; the next
+      // round's loads are issued before this round is ranked
+      const double2* row2 = reinterpret_cast<const double2*>(row);
+      const int32_t n2 = n >> 1;
+      double2 nx[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t j2 = lane + 32 * u;
+        nx[u] = j2 < n2 ? __ldg(row2 + j2) : make_double2(-INFINITY, -INFINITY);
+      }
+      for (int32_t b2 = 0; b2 < n2; b2 += 128) {
+        double2 c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[u] = nx[u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int32_t j2 = b2 + 128 + lane + 32 * u;
+          nx[u] = j2 < n2 ? __ldg(row2 + j2) : make_double2(-INFINITY, -INFINITY);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int32_t j2 = b2 + lane + 32 * u;
+          if (j2 < n2) {
+            consider(c[u].x, 2 * j2);
+            consider(c[u].y, 2 * j2 + 1);
+          }
+        }
+      }
+    } else {
+      for (int32_t j = lane; j < n; j += 32) consider(__ldg(row + j), j);
     }
     // Non-finite scores are rejected before any result is written
     // (src/moe.cpp:41); the first pass reads every score.
@@ -298,9 +329,18 @@ extern "C" int dbk_moe_topk(int64_t T, int32_t n, int32_t k, const double* score
   }
   const int warps = 8;
   const size_t smem = sizeof(double) * static_cast<size_t>(warps) * k;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   const unsigned blocks = static_cast<unsigned>((T + warps - 1) / warps);
-  k_topk<<<blocks, warps * 32, smem, static_cast<cudaStream_t>(stream)>>>(T, n, k, scores, ids, weights, err);
+  // per-lane candidate lists: 4 deep when k ≤ 4 (shorter insertion chains,
+  // fewer registers), else 8 deep with further passes for k > 8
+  if (k <= 4) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_topk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_topk<4><<<blocks, warps * 32, smem, st>>>(T, n, k, scores, ids, weights, err);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_topk<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_topk<8><<<blocks, warps * 32, smem, st>>>(T, n, k, scores, ids, weights, err);
+  }
   return static_cast<int>(cudaGetLastError());
 }
 

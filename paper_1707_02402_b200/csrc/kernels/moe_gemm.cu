@@ -18,7 +18,7 @@
 //    layout [8 k-groups][128 rows][8 elements].
 // Weights are pre-tiled SWIZZLE_NONE per (N tile, K chunk): [8][256 n][8].
 // Padding rows of A and H are never initialised: their GEMM rows are never
-// read (the combine and the EP unpack read valid rows only).
+// read (the combine reads valid rows only; the EP GEMM2 skips them).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -149,6 +149,8 @@ struct GemmParams {
   const uint8_t* const* W;      // per expert tiled weights [N/256][K/64][32 KB]
   uint8_t* H;                   // EPI 0: tiled bf16 output [rb][N/64][16 KB]
   __nv_bfloat16* Y;             // EPI 1: bf16 row-major [row][N]
+  int32_t tile_begin, tile_end;  // row-tile range (tile_end < 0: up to *n_tiles)
+  const int32_t* out_row;        // EPI 1: Y row of padded row r = out_row[r] (< 0: skip); null = r
 };
 
 // Grouped GEMM over (row tile, N tile) pairs; EPI 0 = ReLU → bf16 tiled
@@ -183,12 +185,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant_
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int32_t n_nt = P.N / kBN, n_kc = P.K / kBK;
-  const int32_t total = *P.n_tiles * n_nt;
+  const int32_t t_first = P.tile_begin * n_nt;
+  const int32_t total = (P.tile_end < 0 ? *P.n_tiles : P.tile_end) * n_nt;
 
   if (warp == 0) {
     if (lane == 0) {  // producer
       uint32_t si = 0;
-      for (int32_t t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int32_t t = t_first + blockIdx.x; t < total; t += gridDim.x) {
         const int32_t rt = t / n_nt, nt = t % n_nt;
         const int32_t e = P.tile_expert[rt], rb = P.tile_rb[rt];
         const uint8_t* a = P.A + static_cast<int64_t>(rb) * n_kc * kABytes;
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant_
       uint32_t si = 0;
       int it = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-      for (int32_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      for (int32_t t = t_first + blockIdx.x; t < total; t += gridDim.x, ++it) {
         const int abuf = it & 1;
         mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant_
     const int quarter = warp & 3;
     const int col0 = ((warp - 2) >> 2) * (kBN / 2);
     int it = 0;
-    for (int32_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    for (int32_t t = t_first + blockIdx.x; t < total; t += gridDim.x, ++it) {
       const int abuf = it & 1;
       const int32_t rt = t / n_nt, nt = t % n_nt;
       const int32_t rb = P.tile_rb[rt];
@@ -258,7 +261,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant_
             *reinterpret_cast<uint4*>(blk + (((col % kBK) / 8) * kBM + rr) * 16) = pk;
           }
         } else {
-          __nv_bfloat16* dst = P.Y + row * P.N + n0;
+          const int64_t orow = P.out_row ? P.out_row[row] : row;
+          if (orow < 0) continue;  // padding row (EP: no receive row)
+          __nv_bfloat16* dst = P.Y + orow * P.N + n0;
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             uint4 pk;
@@ -337,11 +342,12 @@ extern "C" int dbk_moe_bf16_dispatch(int64_t T, int32_t k, int32_t d, const int3
 
 extern "C" int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
                                  const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
-                                 const void* const* W, void* H, void* Y, int32_t sms, void* stream) {
+                                 const void* const* W, void* H, void* Y, int32_t tile_begin, int32_t tile_end,
+                                 const int32_t* out_row, int32_t sms, void* stream) {
   if (K % kBK != 0 || N % kBN != 0) return static_cast<int>(cudaErrorInvalidValue);
   GemmParams p{n, K, N, n_tiles, tile_expert, tile_rb, static_cast<const uint8_t*>(A),
                reinterpret_cast<const uint8_t* const*>(W), static_cast<uint8_t*>(H),
-               static_cast<__nv_bfloat16*>(Y)};
+               static_cast<__nv_bfloat16*>(Y), tile_begin, tile_end, out_row};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return epi == 0 ? launch_gemm<0>(p, sms, s) : launch_gemm<1>(p, sms, s);
 }
@@ -360,17 +366,26 @@ extern "C" int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const doubl
 // in (token, slot) order, are therefore already grouped by destination rank.
 namespace {
 
-// send[i] = bf16(x[order[i] / k]) for the rank's items in sorted order;
-// pos_of_item[item] = i (the item's row in the returned buffer).
-__global__ void k_moe_ep_pack(int64_t items, int32_t k, int32_t d, const int32_t* __restrict__ order,
-                              const float* __restrict__ x, __nv_bfloat16* __restrict__ send,
-                              int32_t* __restrict__ pos_of_item) {
-  for (int64_t i = blockIdx.x; i < items; i += gridDim.x) {
-    const int32_t item = order[i];
-    if (threadIdx.x == 0) pos_of_item[item] = static_cast<int32_t>(i);
-    const float* src = x + static_cast<int64_t>(item / k) * d;
-    __nv_bfloat16* dst = send + i * d;
-    for (int32_t j = threadIdx.x * 8; j < d; j += blockDim.x * 8) {
+// pos_of_item[order[i]] = i: an item's row in the sorted send buffer.
+__global__ void k_moe_ep_positions(int64_t items, const int32_t* __restrict__ order,
+                                   int32_t* __restrict__ pos_of_item) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < items;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    pos_of_item[order[i]] = static_cast<int32_t>(i);
+}
+
+// send[pos_of_item[t·k + s]] = bf16(x[t]): one warp per token reads its fp32
+// row once and writes its k bf16 rows (row-contiguous, coalesced).
+__global__ void k_moe_ep_pack(int64_t T, int32_t k, int32_t d, const int32_t* __restrict__ pos_of_item,
+                              const float* __restrict__ x, __nv_bfloat16* __restrict__ send) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += warps) {
+    const float* src = x + t * d;
+    int32_t pos[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) pos[s] = s < k ? pos_of_item[t * k + s] : 0;
+    for (int32_t j = lane * 8; j < d; j += 256) {
       const float4 a = __ldg(reinterpret_cast<const float4*>(src + j));
       const float4 b = __ldg(reinterpret_cast<const float4*>(src + j + 4));
       uint4 pk;
@@ -378,49 +393,90 @@ __global__ void k_moe_ep_pack(int64_t items, int32_t k, int32_t d, const int32_t
       pk.y = pack_bf16x2(a.z, a.w);
       pk.z = pack_bf16x2(b.x, b.y);
       pk.w = pack_bf16x2(b.z, b.w);
-      *reinterpret_cast<uint4*>(dst + j) = pk;
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < k) *reinterpret_cast<uint4*>(send + static_cast<int64_t>(pos[s]) * d + j) = pk;
     }
   }
 }
 
+// Block-wide exclusive scan of one value per thread (all threads call);
+// *total = the block's sum.
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* total, int32_t* wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = lane < nw ? wsum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  const int32_t excl = (warp > 0 ? wsum[warp - 1] : 0) + x - v;
+  *total = wsum[nw - 1];
+  __syncthreads();
+  return excl;
+}
+
 // Receiver layout from the count matrix cnt[G][E] (rows source r sent for
 // local expert e; the receive buffer holds source blocks in rank order, each
-// expert-major): per-expert totals → padded starts and the tile list (as
-// k_moe_layout), plus, per (expert, source), the receive-buffer row of its
-// first row (src_row) and its offset within the expert (cum). Single thread.
-__global__ void k_moe_ep_layout(int32_t G, int32_t E, const int32_t* __restrict__ cnt,
-                                int32_t* __restrict__ pstart, int32_t* __restrict__ tile_expert,
-                                int32_t* __restrict__ tile_rb, int32_t* __restrict__ n_tiles,
-                                int32_t* __restrict__ src_row, int32_t* __restrict__ cum) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int32_t base = 0;  // receive-buffer row where source r's block starts
+// expert-major), one 1024-thread block: per (expert, source) the receive row
+// of its first row (src_row[e·G + r]) and its offset within the expert
+// (cum[e·(G+1) + r]); per-expert padded starts and the tile list, as
+// k_moe_layout.
+__global__ void __launch_bounds__(1024) k_moe_ep_layout(int32_t G, int32_t E, const int32_t* __restrict__ cnt,
+                                                        int32_t* __restrict__ pstart,
+                                                        int32_t* __restrict__ tile_expert,
+                                                        int32_t* __restrict__ tile_rb, int32_t* __restrict__ n_tiles,
+                                                        int32_t* __restrict__ src_row, int32_t* __restrict__ cum) {
+  __shared__ int32_t wsum[32];
+  int32_t base = 0;  // receive row where source r's block starts
   for (int32_t r = 0; r < G; ++r) {
-    int32_t off = base;
-    for (int32_t e = 0; e < E; ++e) {
-      src_row[e * G + r] = off;
-      off += cnt[r * E + e];
+    int32_t carry = 0;
+    for (int32_t e0 = 0; e0 < E; e0 += blockDim.x) {
+      const int32_t e = e0 + static_cast<int32_t>(threadIdx.x);
+      int32_t total;
+      const int32_t excl = block_excl_scan(e < E ? cnt[r * E + e] : 0, &total, wsum);
+      if (e < E) src_row[e * G + r] = base + carry + excl;
+      carry += total;
     }
-    base = off;
+    base += carry;
   }
-  int32_t rows_acc = 0, t = 0;
-  for (int32_t e = 0; e < E; ++e) {
-    pstart[e] = rows_acc;
+  int32_t carry = 0;  // row blocks so far
+  for (int32_t e0 = 0; e0 < E; e0 += blockDim.x) {
+    const int32_t e = e0 + static_cast<int32_t>(threadIdx.x);
     int32_t tot = 0;
-    for (int32_t r = 0; r < G; ++r) {
-      cum[e * (G + 1) + r] = tot;
-      tot += cnt[r * E + e];
+    if (e < E) {
+      for (int32_t r = 0; r < G; ++r) {
+        cum[e * (G + 1) + r] = tot;
+        tot += cnt[r * E + e];
+      }
+      cum[e * (G + 1) + G] = tot;
     }
-    cum[e * (G + 1) + G] = tot;
     const int32_t nb = (tot + kBM - 1) / kBM;
-    for (int32_t b = 0; b < nb; ++b) {
-      tile_expert[t] = e;
-      tile_rb[t] = rows_acc / kBM + b;
-      ++t;
+    int32_t total;
+    const int32_t first = carry + block_excl_scan(nb, &total, wsum);
+    if (e < E) {
+      pstart[e] = first * kBM;
+      for (int32_t b = 0; b < nb; ++b) {
+        tile_expert[first + b] = e;
+        tile_rb[first + b] = first + b;
+      }
     }
-    rows_acc += nb * kBM;
+    carry += total;
   }
-  pstart[E] = rows_acc;
-  *n_tiles = t;
+  if (threadIdx.x == 0) {
+    pstart[E] = carry * kBM;
+    *n_tiles = carry;
+  }
 }
 
 // Received rows → the SWIZZLE_128B tiled A operand (one warp per padded
@@ -431,12 +487,13 @@ __global__ void k_moe_ep_scatter(int32_t G, int32_t d, const int32_t* __restrict
                                  const int32_t* __restrict__ tile_expert, const int32_t* __restrict__ src_row,
                                  const int32_t* __restrict__ cum, int32_t E,
                                  const __nv_bfloat16* __restrict__ recv, uint8_t* __restrict__ A,
-                                 int32_t* __restrict__ recv_of_row) {
-  const int32_t total_rows = pstart[E];
+                                 int32_t* __restrict__ recv_of_row, int32_t row_begin, int32_t row_end) {
+  const int32_t total_rows = row_end < 0 ? pstart[E] : row_end;
   const int32_t kchunks = d / kBK;
   const int lane = threadIdx.x & 31;
   const int32_t warps = gridDim.x * (blockDim.x >> 5);
-  for (int32_t row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < total_rows; row += warps) {
+  for (int32_t row = row_begin + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < total_rows;
+       row += warps) {
     const int32_t e = tile_expert[row / kBM];
     const int32_t local = row - pstart[e];
     const int32_t* ce = cum + e * (G + 1);
@@ -454,51 +511,33 @@ __global__ void k_moe_ep_scatter(int32_t G, int32_t d, const int32_t* __restrict
   }
 }
 
-// Expert outputs back into receive order: ret[recv_of_row[row]] = Y[row].
-__global__ void k_moe_ep_unpack(int32_t E, int32_t d, const int32_t* __restrict__ pstart,
-                                const int32_t* __restrict__ recv_of_row, const __nv_bfloat16* __restrict__ Y,
-                                __nv_bfloat16* __restrict__ ret) {
-  const int32_t total_rows = pstart[E];
-  for (int32_t row = blockIdx.x; row < total_rows; row += gridDim.x) {
-    const int32_t dst = recv_of_row[row];
-    if (dst < 0) continue;
-    const uint4* s4 = reinterpret_cast<const uint4*>(Y + static_cast<int64_t>(row) * d);
-    uint4* d4 = reinterpret_cast<uint4*>(ret + static_cast<int64_t>(dst) * d);
-    for (int32_t j = threadIdx.x; j < d / 8; j += blockDim.x) d4[j] = __ldg(s4 + j);
-  }
-}
-
 }  // namespace
 
 extern "C" int dbk_moe_ep_pack(int64_t items, int32_t k, int32_t d, const int32_t* order, const float* x,
                                void* send, int32_t* pos_of_item, int32_t blocks, void* stream) {
   if (items <= 0) return 0;
-  k_moe_ep_pack<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      items, k, d, order, x, static_cast<__nv_bfloat16*>(send), pos_of_item);
+  if (k > 8 || d % 8 != 0) return static_cast<int>(cudaErrorInvalidValue);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k_moe_ep_positions<<<blocks, 256, 0, s>>>(items, order, pos_of_item);
+  k_moe_ep_pack<<<blocks, 256, 0, s>>>(items / k, k, d, pos_of_item, x, static_cast<__nv_bfloat16*>(send));
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int dbk_moe_ep_layout(int32_t G, int32_t E, const int32_t* cnt, int32_t* pstart, int32_t* tile_expert,
                                  int32_t* tile_rb, int32_t* n_tiles, int32_t* src_row, int32_t* cum,
                                  void* stream) {
-  k_moe_ep_layout<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(G, E, cnt, pstart, tile_expert, tile_rb,
+  k_moe_ep_layout<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(G, E, cnt, pstart, tile_expert, tile_rb,
                                                                     n_tiles, src_row, cum);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int dbk_moe_ep_scatter(int32_t G, int32_t E, int32_t d, const int32_t* pstart,
                                   const int32_t* tile_expert, const int32_t* src_row, const int32_t* cum,
-                                  const void* recv, void* A, int32_t* recv_of_row, int32_t blocks,
-                                  void* stream) {
+                                  const void* recv, void* A, int32_t* recv_of_row, int32_t row_begin,
+                                  int32_t row_end, int32_t blocks, void* stream) {
   k_moe_ep_scatter<<<blocks, kBM, 0, static_cast<cudaStream_t>(stream)>>>(
       G, d, pstart, tile_expert, src_row, cum, E, static_cast<const __nv_bfloat16*>(recv),
-      static_cast<uint8_t*>(A), recv_of_row);
+      static_cast<uint8_t*>(A), recv_of_row, row_begin, row_end);
   return static_cast<int>(cudaGetLastError());
 }
 
-extern "C" int dbk_moe_ep_unpack(int32_t E, int32_t d, const int32_t* pstart, const int32_t* recv_of_row,
-                                 const void* Y, void* ret, int32_t blocks, void* stream) {
-  k_moe_ep_unpack<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      E, d, pstart, recv_of_row, static_cast<const __nv_bfloat16*>(Y), static_cast<__nv_bfloat16*>(ret));
-  return static_cast<int>(cudaGetLastError());
-}

@@ -16,6 +16,16 @@ Receivers concatenate by source rank. With contiguous token shards this
 reproduces, for every expert, the reference's (token, slot) member order.
 The exchange is plain torch.distributed (NCCL over NVLink on the GPU box,
 gloo in the CPU tests). `EpExchange` is the part shared by both.
+
+With `chunks` > 1 the exchange overlaps the expert GEMMs:
+the local experts are cut into contiguous ranges, and each range's rows
+travel in their own batch of point-to-point sends/receives. The GEMMs of
+range c start as soon as range c has arrived, while later ranges are still
+in flight. Range c's outputs start back while range c+1 computes. Both
+buffers keep the unchunked layout. A send block is [destination q][q's
+local expert e], and a receive block is [source r][local expert e]. The
+pieces of a range are therefore contiguous slices of both, and the results
+are bit-identical to chunks = 1.
 """
 from __future__ import annotations
 
@@ -25,6 +35,25 @@ import numpy as np
 def split_rows(expert_counts: np.ndarray, world: int) -> np.ndarray:
     """Rows this rank sends to each rank: the contiguous expert blocks."""
     return np.asarray(expert_counts, np.int64).reshape(world, -1).sum(axis=1)
+
+
+def chunk_bounds(E: int, chunks: int):
+    """Contiguous local-expert ranges [(e0, e1), ...], as even as possible."""
+    chunks = max(1, min(int(chunks), E))
+    cuts = [E * c // chunks for c in range(chunks + 1)]
+    return [(cuts[c], cuts[c + 1]) for c in range(chunks)]
+
+
+def pieces(cnt2d: np.ndarray, bounds):
+    """Slices of a [peer][local expert] row-block buffer: off[c][q], rows[c][q]
+    for expert range c of peer q (cnt2d[q][e] = rows of (q, e))."""
+    cnt2d = np.asarray(cnt2d, np.int64)
+    G = cnt2d.shape[0]
+    peer0 = np.concatenate([[0], np.cumsum(cnt2d.sum(axis=1))])[:-1]
+    pre = np.concatenate([np.zeros((G, 1), np.int64), np.cumsum(cnt2d, axis=1)], axis=1)
+    off = np.stack([peer0 + pre[:, e0] for e0, _ in bounds])
+    rows = np.stack([pre[:, e1] - pre[:, e0] for e0, e1 in bounds])
+    return off, rows
 
 
 class EpExchange:
@@ -60,6 +89,30 @@ class EpExchange:
                                [int(x) for x in out_rows], [int(x) for x in in_rows], group=self.group)
         return out
 
+    def pieces_async(self, out, out_off, out_rows, inp, in_off, in_rows, rank):
+        """One chunk: rows inp[in_off[q] : +in_rows[q]] go to rank q, rows
+        from rank q land at out[out_off[q] : +out_rows[q]]. The own piece
+        is a local copy. Returns the works to wait on (one grouped batch of
+        point-to-point operations; none when nothing crosses ranks)."""
+        a, n = int(in_off[rank]), int(in_rows[rank])
+        if n:
+            b = int(out_off[rank])
+            out[b:b + n].copy_(inp[a:a + n])
+        if self.world == 1:
+            return []
+        import torch.distributed as dist
+        ops = []
+        for q in range(self.world):
+            if q == rank:
+                continue
+            if int(in_rows[q]):
+                a = int(in_off[q])
+                ops.append(dist.P2POp(dist.isend, inp[a:a + int(in_rows[q])], q, group=self.group))
+            if int(out_rows[q]):
+                b = int(out_off[q])
+                ops.append(dist.P2POp(dist.irecv, out[b:b + int(out_rows[q])], q, group=self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
 
 class MoeEpLayer:
     """One rank of the expert-parallel MoE layer on the B200 (bf16 tcgen05
@@ -92,7 +145,9 @@ class MoeEpLayer:
             self.recv = self.torch.empty((cap, self.d), dtype=self.torch.bfloat16, device=self.dev)
             self.ret = self.torch.empty_like(self.recv)
 
-    def forward(self):
+    def forward(self, chunks: int = 1):
+        if chunks > 1:
+            return self._forward_chunked(chunks)
         t = self.torch
         counts = self.sess.dispatch(self.send.data_ptr())
         send_rows = split_rows(counts, self.world)
@@ -110,3 +165,34 @@ class MoeEpLayer:
 
     def outputs(self) -> np.ndarray:
         return self.sess.outputs()
+
+    def _forward_chunked(self, chunks: int):
+        """The exchange in expert ranges, overlapped with the grouped GEMMs
+        (module docstring). Every operation is ordered on the session
+        stream: the point-to-point batches wait for it when issued, and it
+        waits for a batch through the batch's works."""
+        t = self.torch
+        counts = self.sess.dispatch(self.send.data_ptr())
+        G, E = self.world, self.sess.local_experts
+        with t.cuda.stream(self.stream):
+            cnt = self.ex.counts(counts)
+            rows = int(cnt.sum())
+            self._ensure(rows)
+            self.sess.layout(cnt)
+            bounds = chunk_bounds(E, chunks)
+            s_off, s_rows = pieces(np.asarray(counts).reshape(G, E), bounds)  # send side: [dest][e]
+            r_off, r_rows = pieces(cnt, bounds)                                # receive side: [src][e]
+            arrivals = [self.ex.pieces_async(self.recv, r_off[c], r_rows[c], self.send, s_off[c], s_rows[c],
+                                             self.rank) for c in range(len(bounds))]
+            returns = []
+            for c, (e0, e1) in enumerate(bounds):
+                for w in arrivals[c]:
+                    w.wait()  # the stream waits for range c's rows
+                self.sess.experts_range(self.recv.data_ptr(), self.ret.data_ptr(), e0, e1)
+                returns.append(self.ex.pieces_async(self.back, s_off[c], s_rows[c], self.ret, r_off[c], r_rows[c],
+                                                    self.rank))
+            for ws in returns:
+                for w in ws:
+                    w.wait()
+        self.sess.combine(self.back.data_ptr())
+        self.last_recv_rows = rows

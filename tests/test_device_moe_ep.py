@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-def _loopback(n, k, T, d, h, seed, G):
+def _loopback(n, k, T, d, h, seed, G, chunks=0):
     dev = torch.device("cuda", 0)
     sess = [db.MoeEpSession(n, k, T, d, h, seed, r, G) for r in range(G)]
     E = n // G
@@ -33,7 +33,13 @@ def _loopback(n, k, T, d, h, seed, G):
     rets = []
     for q in range(G):
         ret = torch.empty_like(recv[q])
-        sess[q].experts(recv[q].data_ptr(), cnts[q], ret.data_ptr())
+        if chunks:  # layout once, then contiguous expert ranges (chunked exchange)
+            from paper_1707_02402_b200.moe_ep import chunk_bounds
+            sess[q].layout(cnts[q])
+            for e0, e1 in reversed(chunk_bounds(E, chunks)):  # any order: ranges are independent
+                sess[q].experts_range(recv[q].data_ptr(), ret.data_ptr(), e0, e1)
+        else:
+            sess[q].experts(recv[q].data_ptr(), cnts[q], ret.data_ptr())
         sess[q].synchronize()
         rets.append(ret)
     outs = []
@@ -62,6 +68,17 @@ def test_ep_stages_equal_single_gpu_layer(G):
     assert sum(int(c.sum()) for c in cnts) == T * k
 
 
+@pytest.mark.parametrize("G,chunks", [(1, 3), (2, 2), (4, 2), (2, 8)])
+def test_ep_expert_ranges_equal_whole_experts_call(G, chunks):
+    """layout + experts_range over contiguous expert ranges (the chunked
+    exchange's receive side) = one experts() call, bit for bit."""
+    n, k, T, d, h, seed = 16, 2, 1024, 256, 512, 5
+    whole, _ = _loopback(n, k, T, d, h, seed, G)
+    ranged, _ = _loopback(n, k, T, d, h, seed, G, chunks=chunks)
+    for a, b in zip(whole, ranged):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_ep_counts_follow_reference_routing():
     """Counts a rank sends per expert = its token slice's routing."""
     import oracle_lib as O
@@ -85,6 +102,8 @@ def test_moe_ep_layer_world1_equals_session():
     full = db.MoeSession(n, k, T, d, h, seed=seed, precision=db.MOE_BF16)
     full.forward()
     np.testing.assert_array_equal(out, full.run().outputs().astype(np.float32))
+    layer.forward(chunks=3)  # the chunked, overlapped exchange (loopback at world 1)
+    np.testing.assert_array_equal(layer.outputs(), out)
 
 
 def test_ep_rejects_indivisible_shapes():

@@ -171,3 +171,69 @@ def test_moe_expert_parallel_protocol_matches_single_process():
             want = np.nonzero(flat == r * E + e)[0].tolist()
             assert members[e] == want, (r, e)
         assert cnt.sum() == sum(len(v) for v in members.values())
+
+
+def _ep_chunk_worker(rank, port, out_q):
+    """The chunked exchange (moe_ep.pieces / EpExchange.pieces_async) moves
+    exactly the rows of the single all-to-allv, range by range, both ways."""
+    import torch
+    from paper_1707_02402_b200.moe_ep import EpExchange, chunk_bounds, pieces, split_rows
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    n, d = 12, 3
+    E = n // WORLD
+    rng = np.random.default_rng(100 + rank)
+    counts = rng.integers(0, 5, size=n).astype(np.int32)
+    counts[rank] = 0  # an empty (destination, expert) piece
+    items = int(counts.sum())
+    send = torch.tensor(rank * 1000.0 + np.arange(items * d, dtype=np.float64).reshape(items, d))
+    ex = EpExchange(WORLD, n)
+    cnt = ex.counts(counts)
+    recv_rows, send_rows = cnt.sum(axis=1), split_rows(counts, WORLD)
+    full = torch.zeros((int(recv_rows.sum()), d), dtype=torch.float64)
+    ex.rows(full, send, recv_rows, send_rows)
+    ok = []
+    for chunks in (1, 2, 4, E):
+        bounds = chunk_bounds(E, chunks)
+        s_off, s_rows = pieces(counts.reshape(WORLD, E), bounds)
+        r_off, r_rows = pieces(cnt, bounds)
+        recv = torch.full_like(full, -1.0)
+        for c in range(len(bounds)):
+            for w in ex.pieces_async(recv, r_off[c], r_rows[c], send, s_off[c], s_rows[c], rank):
+                w.wait()
+        # outputs = received rows negated; back through the reverse pieces
+        ret = -recv
+        back = torch.full_like(send, 7.0)
+        for c in range(len(bounds)):
+            for w in ex.pieces_async(back, s_off[c], s_rows[c], ret, r_off[c], r_rows[c], rank):
+                w.wait()
+        ok.append((chunks, bool(torch.equal(recv, full)), bool(torch.equal(back, -send))))
+    out_q.put((rank, ok))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_moe_chunked_exchange_equals_all_to_allv():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ep_chunk_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(WORLD)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok in res:
+        for chunks, same_recv, same_back in ok:
+            assert same_recv and same_back, (rank, chunks)
+
+
+def test_chunk_bounds_and_pieces():
+    from paper_1707_02402_b200.moe_ep import chunk_bounds, pieces
+    assert chunk_bounds(8, 3) == [(0, 2), (2, 5), (5, 8)]
+    assert chunk_bounds(2, 5) == [(0, 1), (1, 2)]
+    cnt = np.array([[1, 2, 3], [4, 0, 6]])
+    off, rows = pieces(cnt, [(0, 1), (1, 3)])
+    # peer blocks start at 0 and 6; range (1, 3) of peer 1 starts after its expert 0
+    assert off.tolist() == [[0, 6], [1, 10]]
+    assert rows.tolist() == [[1, 4], [5, 6]]
