@@ -281,6 +281,14 @@ def run_ours(args, dist):
     # second pass with events around every launch: per-kernel-class times
     # for the roofline and the breakdown (not the headline)
     pms, kt = sess.time(args.steps, profile=True)
+    # the step kernel's own clock: clock64 cycles over globaltimer ns in its
+    # MMA loop (debug-counter build of the kernel, 3 forwards). nvidia-smi's
+    # clocks.sm reads the boost target; under the board power limit the
+    # delivered SM clock is lower, and this is the figure the kernel saw.
+    db.conv_wait_counters(reset=True, enable=True)
+    sess.time(3)
+    w = db.conv_wait_counters(reset=True, enable=False)
+    kernel_mhz = float(w[5][0]) / max(float(w[5][1]), 1.0) * 1e3
 
     # end-to-end through the public API, every call a new batch: the
     # programs as prefix function sequences (db_iep_session_set_programs:
@@ -403,6 +411,10 @@ def run_ours(args, dist):
             out["moe"] = {"error": str(e)}
     clk.stop()
     out["clocks"] = clk.summary()
+    out["clocks"]["step_kernel_sm_mhz"] = round(kernel_mhz)
+    out["clocks"]["note"] = ("sm_mhz is nvidia-smi's clocks.sm (boost target); step_kernel_sm_mhz is the clock the "
+                             "fused step kernel measured itself (clock64 / globaltimer): the board power limit "
+                             "holds it below sm_max_mhz while the tensor cores and HBM are busy")
     if dist.rank == 0 and N == 1 and not args.no_cpu_baseline:
         threads, n = calibrate_cpu(cfg, args.cpu_seconds)
         dt, n = cpu_sample_run(cfg, n, threads)

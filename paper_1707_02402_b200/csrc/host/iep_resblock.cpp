@@ -96,10 +96,10 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   check(cudaMemcpyAsync(R.chw_in.get(), tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   check(dbk_rb_inputs_from_chw(c.b, R.chw_in.get(), R.inputs.get(), stream_), "inputs layout");
   // staging: every step owns its range (results are forwarded into their
-  // parent's operand image); per group a kLead-row lead and ≤ one
-  // 256-position alignment gap
+  // parent's operand image); per group a kLead-row lead, ≤ one 256-position
+  // alignment gap and ≤ one more tile to round it to whole tile pairs
   const std::int64_t max_groups = std::min<std::int64_t>(n_exp_cap, static_cast<std::int64_t>(std::max(1, c.cap_s)) * c.p);
-  R.plane_stride = RB::kGuard + n_exp_cap * 225 + (max_groups + 2) * (R.tile_m + RB::kLead) + 64;
+  R.plane_stride = RB::kGuard + n_exp_cap * 225 + (2 * max_groups + 2) * (R.tile_m + RB::kLead) + 64;
   // forwarding eligibility: expensive nodes with exactly one parent
   {
     std::vector<std::int32_t> parents(static_cast<size_t>(N), 0), ok(static_cast<size_t>(N), 0);
@@ -142,12 +142,12 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   R.step_tile_begin.alloc(S);
   R.step_bintile_begin.alloc(S);
   R.step_positions.alloc(S + 1);
-  R.tile_group.alloc(T + N);
-  R.tile_q0.alloc(T + N);
-  R.bin_group.alloc(T + N);
-  R.bin_q0.alloc(T + N);
-  R.done0.alloc(T + N);
-  R.done1.alloc(T + N);
+  R.tile_group.alloc(T + 2 * N);  // ≤ 2 tiles per group beyond the images (pairs)
+  R.tile_q0.alloc(T + 2 * N);  // ≤ 2 tiles per group beyond the images (pairs)
+  R.bin_group.alloc(T + 2 * N);  // ≤ 2 tiles per group beyond the images (pairs)
+  R.bin_q0.alloc(T + 2 * N);  // ≤ 2 tiles per group beyond the images (pairs)
+  R.done0.alloc(T + 2 * N);  // ≤ 2 tiles per group beyond the images (pairs)
+  R.done1.alloc(T + 2 * N);  // ≤ 2 tiles per group beyond the images (pairs)
   R.done0.zero(stream_);
   R.done1.zero(stream_);
   R.queue.alloc(S + 1);

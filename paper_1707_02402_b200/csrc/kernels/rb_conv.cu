@@ -75,12 +75,26 @@ constexpr int kGuard = 32;                 // zero positions before position 0
 constexpr int kTileM = 256;                // positions per CTA tile (MMA N)
 constexpr int kHalo = 16;                  // 3×3 window halo (15 + 1 positions)
 constexpr int kLead = 16;                  // zero rows before a segment's first image (its top / left pads)
+#ifndef DYNBATCH_CLUSTER
+#define DYNBATCH_CLUSTER 2
+#endif
+// CTAs per cluster: the two CTAs of a pair take the two tiles of one tile
+// pair (same segment, same weights) and each loads half of every weight
+// stage, multicast to both — half the L2→SM weight traffic per CTA.
+constexpr int kCluster = DYNBATCH_CLUSTER;
+static_assert(kCluster == 1 || kCluster == 2, "cluster of 1 or 2 CTAs");
 constexpr int kWin = kTileM + 2 * kHalo;   // window rows (row stride of every A slot)
 constexpr int kChunkPlanes = 8;            // K chunk = 64 input channels = 8 planes
 constexpr int kASlot = kWin * 128;         // 36 KB activation window slot (rows of 128 B)
-constexpr int kASlots = 4;                 // window slots (short hi/lo and 1×1 chunks need depth)
+#ifndef DYNBATCH_ASLOTS
+#define DYNBATCH_ASLOTS 4
+#endif
+#ifndef DYNBATCH_BSTAGES
+#define DYNBATCH_BSTAGES 4
+#endif
+constexpr int kASlots = DYNBATCH_ASLOTS;   // window slots (short hi/lo and 1×1 chunks need depth)
 constexpr int kBStage = 128 * 64 * 2;      // 16 KB: 128 out channels × K=64 fp16 weight block
-constexpr int kBStages = 4;
+constexpr int kBStages = DYNBATCH_BSTAGES;
 constexpr int kEpiWarps = 8;               // two warps per TMEM lane quarter, 128 positions each
 constexpr int kTableWarp = 2 + kEpiWarps;  // fills the per-tile position tables ahead of the epilogue
 constexpr int kWeightWarp = kTableWarp + 1;  // streams the weight stages
@@ -184,19 +198,29 @@ __device__ __forceinline__ Phase phase_of(const StepParams& P, const Item& it, i
   return Phase{p == 0 ? P.stage_x : P.stage_lo, P.ident, 2, 1, 0};
 }
 
+// Tiles of a segment of `rows` images: its lead and images in 256-position
+// tiles, rounded up to whole tile pairs when CTAs run in pairs (the extra
+// tile has no image position: it computes zeros nobody reads).
+__host__ __device__ __forceinline__ int32_t seg_tiles(int32_t rows, int32_t tile_m) {
+  const int32_t nt = (kLead + rows * kImg + tile_m - 1) / tile_m;
+  return (nt + kCluster - 1) / kCluster * kCluster;
+}
+
 // ------------------------------------------------------- work queue
 // Queue order: all conv1x1 tiles, then conv3x3 #1 tiles interleaved with
 // conv3x3 #2 tiles `lookahead` positions behind, so each SM alternates
 // MMA-heavy and store-heavy tiles and a #2 tile's inputs are usually done
 // when it is claimed.
-__device__ __forceinline__ Item step_item(const StepParams& P, int32_t k, int32_t n0, int32_t n1) {
+// With CTA pairs, k, n0 and n1 count tile pairs and `crank` picks the tile.
+__device__ __forceinline__ Item step_item(const StepParams& P, int32_t k, int32_t n0, int32_t n1, int32_t crank) {
   int32_t kind, local;
   if (k < n0) {
     kind = 0;
     local = k;
   } else {
     const int32_t u = k - n0;
-    const int32_t D = min(P.lookahead, n1);
+    // ≥ 2 ahead: a #2 tile's right neighbour's #1 tile is claimed before it
+    const int32_t D = min(max(P.lookahead / kCluster, 2), n1);
     const int32_t R = n1 - D;
     if (u < D) {
       kind = 1;
@@ -212,6 +236,7 @@ __device__ __forceinline__ Item step_item(const StepParams& P, int32_t k, int32_
   }
   Item it;
   it.kind = kind;
+  local = local * kCluster + crank;
   if (kind == 0) {
     it.tile = P.step_bintile_begin[P.step] + local;
     it.g = P.bin_group[it.tile];
@@ -233,7 +258,7 @@ __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& 
   if (it.kind == 0) return;
   const int32_t g = it.g;
   const int32_t rows = P.group_begin[g + 1] - P.group_begin[g];
-  const int32_t nt = (kLead + rows * kImg + kTileM - 1) / kTileM;
+  const int32_t nt = seg_tiles(rows, kTileM);
   const int32_t i = (it.q0 - P.seg_start[g] + kLead) / kTileM;
   const bool binary = P.group_bintile0[g] >= 0;
   const int32_t b0 = binary ? P.step_bintile_begin[P.step] + P.group_bintile0[g] : 0;
@@ -475,7 +500,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
   uint64_t* tab_empty = tab_full + 2;
   uint64_t* item_full = tab_empty + 2;
   uint64_t* item_empty = item_full + kItemSlots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_empty + kItemSlots);
+  uint64_t* mail_full = item_empty + kItemSlots;  // CTA pairs: claimed pair index, leader → partner
+  uint64_t* mail_empty = mail_full + kItemSlots;
+  uint32_t* mail = reinterpret_cast<uint32_t*>(mail_empty + kItemSlots);
+  uint32_t* tmem_slot = mail + kItemSlots;
+  const uint32_t crank = kCluster > 1 ? cluster_rank() : 0;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -485,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
     }
     for (int s = 0; s < kBStages; ++s) {
       mbar_init(b_full + s, 1);
-      mbar_init(b_empty + s, 1);
+      mbar_init(b_empty + s, kCluster);  // both CTAs' MMAs release a shared weight stage
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
@@ -496,17 +525,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
     for (int s = 0; s < kItemSlots; ++s) {
       mbar_init(item_full + s, 1);
       mbar_init(item_empty + s, 3 + kEpiWarps);  // MMA thread, table warp, weight warp, epilogue warps
+      mbar_init(mail_full + s, 1);
+      mbar_init(mail_empty + s, 1);
     }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if (kCluster > 1) cluster_sync();  // the partner's barriers exist before any remote arrive / multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int32_t n0 = P.step_bintile_begin[P.step + 1] - P.step_bintile_begin[P.step];
   const int32_t n1 = P.step_tile_begin[P.step + 1] - P.step_tile_begin[P.step];
   const int32_t total = n0 + 2 * n1;
+  const int32_t n_units = total / kCluster;  // tiles, or tile pairs (segments hold whole pairs)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------------- scheduler + activation windows
@@ -514,9 +547,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       long long w_item = 0, w_dep = 0, w_slot = 0;
       const long long t_start = clock64();
       for (int32_t n = 0;; ++n) {
-        const int32_t k = atomicAdd(P.queue + P.step, 1);
-        const Item it = k < total ? step_item(P, k, n0, n1) : Item{-1, 0, 0, 0};
         const int slot = n % kItemSlots;
+        int32_t k;
+        if (kCluster == 1) {
+          k = atomicAdd(P.queue + P.step, 1);
+        } else if (crank == 0) {  // the leader claims a pair and posts it to the partner
+          k = atomicAdd(P.queue + P.step, 1);
+          mbar_wait_cluster(mail_empty + slot, ((n / kItemSlots) & 1) ^ 1);
+          st_remote_u32(mail + slot, 1, static_cast<uint32_t>(k));
+          mbar_arrive_remote(mail_full + slot, 1);
+        } else {
+          mbar_wait_cluster(mail_full + slot, (n / kItemSlots) & 1);
+          k = static_cast<int32_t>(*reinterpret_cast<volatile uint32_t*>(mail + slot));
+          mbar_arrive_remote(mail_empty + slot, 0);
+        }
+        const Item it = k < n_units ? step_item(P, k, n0 / kCluster, n1 / kCluster, static_cast<int32_t>(crank))
+                                    : Item{-1, 0, 0, 0};
         long long c0 = DBG ? clock64() : 0;
         mbar_wait(item_empty + slot, ((n / kItemSlots) & 1) ^ 1);
         if (DBG) w_item += clock64() - c0;
@@ -600,7 +646,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
                 mma_bf16(tmem_base + abuf * kTileM, wd, xd, IDESC, acc);
                 acc = 1;
               }
-              mma_commit(b_empty + s);
+              if (kCluster == 1) mma_commit(b_empty + s);
+              else mma_commit_mc(b_empty + s, 0x3);  // both CTAs' copies of the stage are free
             }
             mma_commit(a_empty + sa);
           }
@@ -637,8 +684,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
                 continue;
               }
               mbar_expect_tx(b_full + s, kBStage);
-              bulk_g2s(sB + s * kBStage, ph.w + static_cast<int64_t>(ch * ph.taps + tap) * kBStage, kBStage,
-                       b_full + s);
+              const uint8_t* src = ph.w + static_cast<int64_t>(ch * ph.taps + tap) * kBStage;
+              if (kCluster == 1) {
+                bulk_g2s(sB + s * kBStage, src, kBStage, b_full + s);
+              } else {  // this CTA's half of the stage, into both CTAs' smem
+                constexpr uint32_t kHalf = kBStage / 2;
+                bulk_g2s_mc(sB + s * kBStage + crank * kHalf, src + crank * kHalf, kHalf, b_full + s, 0x3);
+              }
             }
           }
         }
@@ -687,6 +739,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         step_epilogue<1>(P, tab, L, taddr, it);
       } else {
         step_epilogue<2>(P, tab, L, taddr, it);
+        if (P.cache & 4) {
+          // the interior mid rows [q0 + 16, q0 + 240) of this tile are read
+          // by this tile's conv3x3 #2 only (its neighbours' windows stop 16
+          // rows short), and its window is in shared memory by now: drop the
+          // dirty lines from L2 instead of writing them back; conv3x3 #1
+          // rewrites them (pads included) before any later read
+          const int et = threadIdx.x - 64;  // 0 .. 255 over the epilogue warps
+          for (int i = et; i < 2 * (kTileM - 2 * kHalo); i += kEpiWarps * 32) {
+            const int c = i / (kTileM - 2 * kHalo), r = kHalo + i % (kTileM - 2 * kHalo);
+            discard_l2_line(P.stage_mid + ((static_cast<int64_t>(c) * P.ps + kGuard + it.q0 + r) << 7));
+          }
+        }
       }
       tc_fence_before();
       mbar_arrive(acc_empty + abuf);
@@ -702,6 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
     }
   }
   __syncthreads();
+  if (kCluster > 1) cluster_sync();  // no remote arrive or multicast still targets this CTA
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
@@ -709,7 +774,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
 }
 
 constexpr int kStepSmem = kASlots * kASlot + kBStages * kBStage + kTableBytes +
-                          kItemSlots * static_cast<int>(sizeof(Item)) + 512;
+                          kItemSlots * static_cast<int>(sizeof(Item)) + 512;  // + barriers, mailbox, TMEM slot
 
 // ----------------------------------------------------------------- plan
 // Segment layout and tile lists for every step, from the group tables.
@@ -731,7 +796,7 @@ __global__ void k_rb_plan(int32_t n_steps, const int32_t* __restrict__ sgb,
         seg_start[g] = -1;
         continue;
       }
-      const int32_t nt = (kLead + rows * kImg + tile_m - 1) / tile_m;
+      const int32_t nt = seg_tiles(rows, tile_m);
       seg_start[g] = cursor + kLead;  // the first image; its tiles start kLead rows earlier
       group_tile0[g] = tiles;
       group_bintile0[g] = arity_of[group_fid[g]] == 2 ? bintiles : -1;
@@ -868,7 +933,7 @@ __global__ void k_rb_tiles(int32_t n_steps, const int32_t* __restrict__ sgb,
   for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
     if (seg_start[g] < 0) continue;
     const int32_t rows = group_begin[g + 1] - group_begin[g];
-    const int32_t nt = (kLead + rows * kImg + tile_m - 1) / tile_m;
+    const int32_t nt = seg_tiles(rows, tile_m);
     for (int32_t i = threadIdx.x; i < nt; i += blockDim.x) {
       const int32_t ti = step_tile_begin[s] + group_tile0[g] + i;
       tile_group[ti] = g;
@@ -940,7 +1005,7 @@ __global__ void k_rb_zero_gaps(int32_t n_steps, const int32_t* __restrict__ sgb,
   for (int32_t g = g0 + blockIdx.x; g < g1; g += gridDim.x) {
     if (seg_start[g] < 0) continue;
     const int32_t rows = group_begin[g + 1] - group_begin[g];
-    const int32_t used = rows * kImg, span = (kLead + used + tile_m - 1) / tile_m * tile_m;
+    const int32_t used = rows * kImg, span = seg_tiles(rows, tile_m) * tile_m;
     const int64_t base = kGuard + static_cast<int64_t>(seg_start[g]) - kLead;  // the segment's first tile row
     const int32_t tail = span - kLead - used;                                // gap rows after the last image
     const int32_t n16 = (kLead + tail) * 8;                                  // 16-byte pieces per chunk
@@ -1068,12 +1133,14 @@ extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile
   p.step = step;
   p.epoch = epoch;
   const char* la = std::getenv("DYNBATCH_LOOKAHEAD");
-  p.lookahead = (la ? std::atoi(la) : 8) * num_sms;
+  // one SM-row of tiles ahead: a conv3x3 #2 tile reads mid written ~2·SMs
+  // tiles earlier, still in L2 (profiles/cache_sweep.py: −40% DRAM traffic)
+  p.lookahead = (la ? std::atoi(la) : 1) * num_sms;
   p.debug = g_debug_flag;
   const char* dg = std::getenv("DYNBATCH_DIAG");
   p.diag = dg ? std::atoi(dg) : 0;
   const char* ch = std::getenv("DYNBATCH_CACHE");
-  p.cache = ch ? std::atoi(ch) : 0;
+  p.cache = ch ? std::atoi(ch) : 4;  // default: drop consumed interior mid lines from L2
   p.step_tile_begin = step_tile_begin;
   p.tile_group = tile_group;
   p.tile_q0 = tile_q0;
@@ -1101,11 +1168,21 @@ extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile
   p.done0 = done0;
   p.done1 = done1;
   p.queue = queue;
-  if (p.debug)
-    k_rb_step<true><<<num_sms, kThreads, kStepSmem, static_cast<cudaStream_t>(stream)>>>(p);
-  else
-    k_rb_step<false><<<num_sms, kThreads, kStepSmem, static_cast<cudaStream_t>(stream)>>>(p);
-  return static_cast<int>(cudaGetLastError());
+  // persistent: one CTA per SM, in clusters of kCluster
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(num_sms / kCluster * kCluster));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kStepSmem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = p.debug ? cudaLaunchKernelEx(&cfg, k_rb_step<true>, p) : cudaLaunchKernelEx(&cfg, k_rb_step<false>, p);
+  return static_cast<int>(e != cudaSuccess ? e : cudaGetLastError());
 }
 
 extern "C" int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream) {
