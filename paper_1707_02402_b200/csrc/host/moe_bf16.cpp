@@ -30,15 +30,18 @@ std::uint16_t bf16(double v) {
 }
 
 // Element (n, kk) of the N × K operand, stored input-major in `w` as
-// w[kk * N + n], into [N/256][K/64] blocks of [8][256][8].
+// w[kk * N + n], into [N/256][K/64] blocks of 32 KB, each two 16 KB halves
+// (columns 0-127 and 128-255 of the N tile: one per CTA of a pair) of
+// [8 k-groups][128 n][8] (moe_gemm.cu).
 void tile_weights(const std::vector<double>& w, int K, int N, std::uint16_t* out) {
   const int n_kc = K / 64;
   for (int kk = 0; kk < K; ++kk) {
     const int kc = kk / 64, k8 = (kk % 64) / 8, ke = kk % 8;
     for (int n = 0; n < N; ++n) {
-      const int nt = n / 256, nn = n % 256;
+      const int nt = n / 256, half = (n % 256) / 128, nn = n % 128;
       const size_t blk = static_cast<size_t>(nt) * n_kc + kc;
-      out[blk * 256 * 64 + (static_cast<size_t>(k8) * 256 + nn) * 8 + ke] = bf16(w[static_cast<size_t>(kk) * N + n]);
+      out[blk * 256 * 64 + ((static_cast<size_t>(half) * 8 + k8) * 128 + nn) * 8 + ke] =
+          bf16(w[static_cast<size_t>(kk) * N + n]);
     }
   }
 }
@@ -106,7 +109,7 @@ MoeBf16::MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed
     throw_error(Errc::invalid_argument, "bf16 MoE path needs data_dim and hidden multiples of 256");
   }
   I.sms = sm_count();
-  const std::int64_t rows = T * I.k + static_cast<std::int64_t>(I.n) * 128;
+  const std::int64_t rows = T * I.k + static_cast<std::int64_t>(I.n) * 256;  // experts padded to 256 rows
   I.x.alloc(static_cast<size_t>(T) * I.d);
   I.A.alloc(static_cast<size_t>(rows) * I.d * 2);
   I.H.alloc(static_cast<size_t>(rows) * I.h * 2);

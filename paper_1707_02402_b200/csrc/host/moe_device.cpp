@@ -350,7 +350,7 @@ MoeEp::MoeEp(const MoeConfig& cfg, std::uint64_t seed, int rank, int world) : im
   I.n_tiles.alloc(1);
   I.src_row.alloc(static_cast<size_t>(I.E) * world);
   I.cum.alloc(static_cast<size_t>(I.E) * (world + 1));
-  I.ensure_capacity(T_ * k + static_cast<std::int64_t>(I.E) * 128);
+  I.ensure_capacity(T_ * k + static_cast<std::int64_t>(I.E) * 256);
   upload_expert_weights(cfg, mix_seed(seed, 0xe4be27ULL), I.e_first, I.E, I.w1, I.w2, I.w1tab, I.w2tab, stream_);
   check(cudaStreamSynchronize(stream_), "upload");
 }
@@ -387,7 +387,7 @@ void MoeEp::layout(const std::int32_t* cnt) {
   for (int e = 0; e < E; ++e) {
     std::int64_t tot = 0;
     for (int r = 0; r < G; ++r) tot += cnt[r * E + e];
-    I.pstart_h[static_cast<size_t>(e) + 1] = I.pstart_h[static_cast<size_t>(e)] + (tot + 127) / 128 * 128;
+    I.pstart_h[static_cast<size_t>(e) + 1] = I.pstart_h[static_cast<size_t>(e)] + (tot + 255) / 256 * 256;
   }
   I.ensure_capacity(I.pstart_h[static_cast<size_t>(E)]);
   check(cudaMemcpyAsync(I.cnt.get(), cnt, sizeof(std::int32_t) * static_cast<size_t>(G) * E, cudaMemcpyHostToDevice,

@@ -35,10 +35,12 @@ constexpr int kBN = 256;         // output columns per tile
 constexpr int kBK = 64;          // K chunk
 constexpr int kABytes = kBM * kBK * 2;   // 16 KB
 constexpr int kBBytes = kBN * kBK * 2;   // 32 KB
-constexpr int kStages = 4;
+constexpr int kPairRows = 2 * kBM;  // experts are padded to whole 256-row tile pairs
+constexpr int kBHalf = kBBytes / 2;  // 16 KB: this CTA's 128 of the 256 output columns
+constexpr int kStages = 6;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + kEpiWarps * 32;
-constexpr int kSmem = kStages * (kABytes + kBBytes) + 256;
+constexpr int kSmem = kStages * (kABytes + kBHalf) + 256;
 
 // Padded starts and the (expert, row block) tile list: one thread per
 // expert, a block-wide scan of the row blocks (single block, n ≤ 1024 × k).
@@ -52,7 +54,7 @@ __global__ void __launch_bounds__(1024) k_moe_layout(int32_t n, const int32_t* _
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int32_t base = 0; base < n; base += blockDim.x) {
     const int32_t e = base + static_cast<int32_t>(threadIdx.x);
-    const int32_t nb = e < n ? (offsets[e + 1] - offsets[e] + kBM - 1) / kBM : 0;
+    const int32_t nb = e < n ? (offsets[e + 1] - offsets[e] + kPairRows - 1) / kPairRows * 2 : 0;
     int32_t x = nb;  // inclusive warp scan, then across warps
     for (int o = 1; o < 32; o <<= 1) {
       const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -153,64 +155,75 @@ struct GemmParams {
   const int32_t* out_row;        // EPI 1: Y row of padded row r = out_row[r] (< 0: skip); null = r
 };
 
-// Grouped GEMM over (row tile, N tile) pairs; EPI 0 = ReLU → bf16 tiled
-// (next GEMM's A operand), EPI 1 = fp32 rows.
+// Grouped GEMM over (row-tile pair, N tile) units on CTA pairs
+// (tcgen05.mma.cta_group::2): M = 256 rows, 128 from each CTA's A tile of
+// one expert, N = 256 columns, each CTA staging half of the weight tile, so
+// per SM the A + B bytes per MMA fall from 12 KB to 8 KB and the weight
+// reads from L2 halve. The even CTA issues the MMAs. The odd CTA relays its
+// "stage landed" events to the even CTA's barriers, and the commits arrive in
+// both CTAs. Each CTA's epilogue drains its own 128 accumulator lanes.
+// EPI 0 = ReLU → bf16 tiled H (GEMM2's A); EPI 1 = bf16 rows.
 template <int EPI>
-__global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant__ GemmParams P) {
-  constexpr uint32_t IDESC = idesc_bf16_f32(kBM, kBN);
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_moe_gemm(const __grid_constant__ GemmParams P) {
+  constexpr uint32_t IDESC = idesc_bf16_f32(2 * kBM, kBN);
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBHalf);
   uint64_t* full = bars;
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full + s, 1);
+      mbar_init(full + s, leader ? 2 : 1);  // own copies (+ the peer's relay on the leader)
       mbar_init(empty + s, 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, kEpiWarps * 32);
+      mbar_init(acc_empty + s, 2 * kEpiWarps);  // every epilogue warp of both CTAs
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int32_t n_nt = P.N / kBN, n_kc = P.K / kBK;
-  const int32_t t_first = P.tile_begin * n_nt;
-  const int32_t total = (P.tile_end < 0 ? *P.n_tiles : P.tile_end) * n_nt;
+  // units: (row-tile pair, N tile); tile ranges are whole pairs
+  const int32_t u_first = P.tile_begin / 2 * n_nt;
+  const int32_t u_end = (P.tile_end < 0 ? *P.n_tiles : P.tile_end) / 2 * n_nt;
+  const int32_t pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
 
   if (warp == 0) {
-    if (lane == 0) {  // producer
+    if (lane == 0) {  // producer (both CTAs): own A tile + own half of the weight tile
       uint32_t si = 0;
-      for (int32_t t = t_first + blockIdx.x; t < total; t += gridDim.x) {
-        const int32_t rt = t / n_nt, nt = t % n_nt;
+      for (int32_t u = u_first + pair; u < u_end; u += n_pairs) {
+        const int32_t rt = 2 * (u / n_nt) + static_cast<int32_t>(rank), nt = u % n_nt;
         const int32_t e = P.tile_expert[rt], rb = P.tile_rb[rt];
         const uint8_t* a = P.A + static_cast<int64_t>(rb) * n_kc * kABytes;
-        const uint8_t* w = P.W[e] + static_cast<int64_t>(nt) * n_kc * kBBytes;
+        const uint8_t* w = P.W[e] + static_cast<int64_t>(nt) * n_kc * kBBytes + rank * kBHalf;
         for (int32_t kc = 0; kc < n_kc; ++kc, ++si) {
           const uint32_t s = si % kStages, ph = (si / kStages) & 1;
           mbar_wait(empty + s, ph ^ 1);
-          mbar_expect_tx(full + s, kABytes + kBBytes);
+          mbar_expect_tx(full + s, kABytes + kBHalf);
           bulk_g2s(sA + s * kABytes, a + static_cast<int64_t>(kc) * kABytes, kABytes, full + s);
-          bulk_g2s(sB + s * kBBytes, w + static_cast<int64_t>(kc) * kBBytes, kBBytes, full + s);
+          bulk_g2s(sB + s * kBHalf, w + static_cast<int64_t>(kc) * kBBytes, kBHalf, full + s);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
+    if (lane == 0 && leader) {  // MMA issuer (even CTA)
       uint32_t si = 0;
       int it = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-      for (int32_t t = t_first + blockIdx.x; t < total; t += gridDim.x, ++it) {
+      for (int32_t u = u_first + pair; u < u_end; u += n_pairs, ++it) {
         const int abuf = it & 1;
         mbar_wait(acc_empty + abuf, ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -222,21 +235,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant_
           for (int kk = 0; kk < kBK / 16; ++kk) {
             const uint64_t ad = EPI == 0 ? smem_desc_sw128(a_base + s * kABytes + kk * 32)
                                          : smem_desc(a_base + s * kABytes + (2 * kk) * kBM * 16, kBM * 16, 128);
-            const uint64_t bd = smem_desc(b_base + s * kBBytes + (2 * kk) * kBN * 16, kBN * 16, 128);
-            mma_bf16(tmem_base + abuf * kBN, ad, bd, IDESC, (kc | kk) != 0);
+            const uint64_t bd = smem_desc(b_base + s * kBHalf + (2 * kk) * 128 * 16, 128 * 16, 128);
+            mma_bf16_pair(tmem_base + abuf * kBN, ad, bd, IDESC, (kc | kk) != 0);
           }
-          mma_commit(empty + s);
+          mma_commit_pair(empty + s, 0x3);
         }
-        mma_commit(acc_full + abuf);
+        mma_commit_pair(acc_full + abuf, 0x3);
       }
+    } else if (lane == 0) {  // relay (odd CTA): its stage landed
+      uint32_t si = 0;
+      for (int32_t u = u_first + pair; u < u_end; u += n_pairs)
+        for (int32_t kc = 0; kc < n_kc; ++kc, ++si) {
+          const uint32_t s = si % kStages, ph = (si / kStages) & 1;
+          mbar_wait(full + s, ph);
+          mbar_arrive_remote_relaxed(full + s, 0);
+        }
     }
   } else {  // epilogue: 8 warps, two per TMEM lane quarter, 128 columns each
     const int quarter = warp & 3;
     const int col0 = ((warp - 2) >> 2) * (kBN / 2);
     int it = 0;
-    for (int32_t t = t_first + blockIdx.x; t < total; t += gridDim.x, ++it) {
+    for (int32_t u = u_first + pair; u < u_end; u += n_pairs, ++it) {
       const int abuf = it & 1;
-      const int32_t rt = t / n_nt, nt = t % n_nt;
+      const int32_t rt = 2 * (u / n_nt) + static_cast<int32_t>(rank), nt = u % n_nt;
       const int32_t rb = P.tile_rb[rt];
       mbar_wait(acc_full + abuf, (it >> 1) & 1);
       tc_fence_after();
@@ -276,13 +297,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_moe_gemm(const __grid_constant_
         }
       }
       tc_fence_before();
-      mbar_arrive(acc_empty + abuf);
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(acc_empty + abuf);
+        else mbar_arrive_remote_relaxed(acc_empty + abuf, 0);
+      }
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    tmem_dealloc_pair(tmem_base, 512);
   }
 }
 
@@ -317,7 +343,7 @@ int launch_gemm(const GemmParams& p, int sms, cudaStream_t s) {
     cudaFuncSetAttribute(k_moe_gemm<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     configured = true;
   }
-  k_moe_gemm<EPI><<<sms, kThreads, kSmem, s>>>(p);
+  k_moe_gemm<EPI><<<sms / 2 * 2, kThreads, kSmem, s>>>(p);  // CTA pairs
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -461,7 +487,7 @@ __global__ void __launch_bounds__(1024) k_moe_ep_layout(int32_t G, int32_t E, co
       }
       cum[e * (G + 1) + G] = tot;
     }
-    const int32_t nb = (tot + kBM - 1) / kBM;
+    const int32_t nb = (tot + kPairRows - 1) / kPairRows * 2;
     int32_t total;
     const int32_t first = carry + block_excl_scan(nb, &total, wsum);
     if (e < E) {

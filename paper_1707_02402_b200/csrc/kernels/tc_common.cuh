@@ -280,6 +280,22 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Arrive on the mbarrier at the same shared-memory offset in CTA `cta`, with
+// no memory ordering of its own: for pure "stage landed / buffer drained"
+// signals whose data moves through the async proxy (TMA writes, tensor-core
+// reads), ordered by the mbarrier phase itself. (The release.cluster form
+// costs a MEMBAR.ALL.GPU per arrive.)
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+
 // Arrive on the mbarrier at the same shared-memory offset in CTA `cta` of
 // the cluster (release at cluster scope).
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
