@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--workload", default="cfg3", choices=sorted(CFG) + sorted(MOE))
     ap.add_argument("--no-moe", action="store_true", help="skip the secondary cfg4 MoE measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--depth", type=int, default=0, help="cfg2: balanced-tree depth (4-8; default 6)")
     ap.add_argument("--ep-chunks", type=int, default=0,
                     help="cfg5: expert ranges the exchange is cut into (overlap with the GEMMs); 0 = 1 at one GPU, "
                          "else 4")
@@ -247,7 +248,9 @@ def run_ours(args, dist):
     import paper_1707_02402_b200 as db
     import torch
 
-    cfg = CFG[args.workload]
+    cfg = dict(CFG[args.workload])
+    if args.depth:
+        cfg["depth"] = args.depth
     N = max(1, dist.world)
     per = cfg["per_gpu"]
     db.device_open(dist.local)
@@ -371,8 +374,9 @@ def run_ours(args, dist):
            "dtype": "fp16 tensor-core operands, fp32 accumulate and node values",
            "data": "synthetic (reference generators, seed 0; random-init weights)",
            "config": {"workload": f"{args.workload}: IEP forward, {cfg['kind']} programs p={cfg['vocab']} "
-                                  f"len<={cfg['length']} branch={cfg['branch_prob']}, residual conv "
-                                  f"modules on 128x14x14, {per} programs/GPU",
+                                  + (f"depth {cfg['depth']}" if cfg["kind"] == "balanced" else
+                                     f"len<={cfg['length']} branch={cfg['branch_prob']}")
+                                  + f", residual conv modules on 128x14x14, {per} programs/GPU",
                       "global_batch": per * N, "programs_per_gpu": per,
                       "parallelism": f"dp{N} (program shards, no collective)",
                       "l2": "inputs (411 MB) and node values (4.9 GB) exceed the 126 MB L2"},
@@ -550,7 +554,9 @@ def _mix_seed(seed, stream):
 
 # ------------------------------------------------------ reference arm
 def run_reference(args, dist):
-    cfg = CFG[args.workload]
+    cfg = dict(CFG[args.workload])
+    if args.depth:
+        cfg["depth"] = args.depth
     threads, n = calibrate_cpu(cfg, min(args.cpu_seconds, 6.0))
     for _ in range(max(0, args.warmup)):
         cpu_sample_run(cfg, n, threads)
