@@ -112,22 +112,26 @@ int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t*
 int dbk_rb_gather(const void* tasks, const int32_t* n_tasks, int32_t list, int32_t step, int64_t task_cap,
                   void* stage_x, void* stage_lo, void* stage_cat, int64_t plane_stride, int32_t blocks,
                   void* stream);
-/* One persistent launch per step (one CTA per SM) over a device work queue
- * of the step's tiles: conv1x1 over [x; y] → z hi/lo (stage_x / stage_lo),
+/* One persistent launch (one CTA per SM, CTA pairs) for steps [step,
+ * step_end) over a device work queue of their tiles, step s + 1's after
+ * all of step s (step_done[s] counts step s's finished conv3x3 #2 tiles): conv1x1 over [x; y] → z hi/lo (stage_x / stage_lo),
  * conv3x3 #1 → mid (stage_mid), conv3x3 #2 + residual (accumulated on the
  * tensor cores from the hi/lo images through the identity blocks `ident`) →
  * hi/lo images of the parent's call and fp32 values where a reader needs
  * them. Tile-level dependencies through done flags (done0 per bin tile,
- * done1 per tile; == epoch means done); queue[step] must be 0 at launch.
+ * done1 per tile; == epoch means done); queue[step] and step_done[step ..
+ * step_end) must be 0 at launch.
  * D[128 channels][256 positions] per tile (tcgen05.mma M = 128, N = 256). */
-int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile_begin, const int32_t* tile_group,
+int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* step_tile_begin,
+                const int32_t* tile_group,
                 const int32_t* tile_q0, const int32_t* step_bintile_begin, const int32_t* bin_group,
                 const int32_t* bin_q0, const int32_t* group_fid, const int32_t* group_begin,
                 const int32_t* seg_start, const int32_t* group_tile0, const int32_t* group_bintile0,
                 const void* memtab, void* stage_x, void* stage_lo, void* stage_cat, void* stage_mid,
                 int64_t plane_stride, const void* const* w0, const void* const* w1, const void* const* w2,
                 const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
-                int32_t* done0, int32_t* done1, int32_t* queue, int32_t num_sms, void* stream);
+                int32_t* done0, int32_t* done1, int32_t* step_done, int32_t* queue, int32_t num_sms,
+                void* stream);
 /* Zeroes stage_x rows between each segment's last image and its tile end
  * (read as top / left pads by the next segment's first image), every
  * forward, so a new layout needs no full re-zeroing. */

@@ -151,6 +151,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   R.done0.zero(stream_);
   R.done1.zero(stream_);
   R.queue.alloc(S + 1);
+  R.step_done.alloc(S + 1);
   // weights
   std::vector<const void*> w0(static_cast<size_t>(c.p), nullptr), w1 = w0, w2 = w0;
   std::vector<const float*> b0(static_cast<size_t>(c.p), nullptr), b1 = b0, b2 = b0;
@@ -186,6 +187,17 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   R.b2tab.upload(b2, stream_);
 }
 
+namespace {
+// DYNBATCH_STEP_LAUNCHES=1: one step-kernel launch per step (A/B timing)
+bool per_step_launches() {
+  static const bool v = [] {
+    const char* e = std::getenv("DYNBATCH_STEP_LAUNCHES");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
+}
+}  // namespace
+
 void IepSession::forward_resblock() {
   RB& R = *rb_;
   DeviceProgramBatch& B = *batch_;
@@ -215,6 +227,8 @@ void IepSession::forward_resblock() {
   launches_ += 6;  // plan, tiles, fwd init, fwd, memtab, zero gaps
   const int gather_blocks = sms * 16;  // grid-stride over the step's (member, operand, chunk, pixel) items
   check(cudaMemsetAsync(R.queue.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_), "queue reset");
+  check(cudaMemsetAsync(R.step_done.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_),
+        "step counters reset");
   ++R.epoch;
   // leaf operands of every step in one launch (they only read the inputs)
   prof_.begin(2, stream_);
@@ -223,7 +237,11 @@ void IepSession::forward_resblock() {
         "dbk_rb_gather leaves");
   prof_.end(stream_);
   ++launches_;
-  for (int s = 0; s < S; ++s) {
+  // All steps in one persistent launch (step s + 1 starts on each SM as soon
+  // as step s is complete, with no launch gap, prologue or tail per step),
+  // unless children shared by several parents need a gather between steps.
+  const bool one_launch = R.n_shared == 0 && !per_step_launches();
+  for (int s = 0; s < S; s = one_launch ? S : s + 1) {
     if (R.n_shared > 0) {  // children shared by several parents: values of earlier steps
       prof_.begin(2, stream_);
       check(dbk_rb_gather(R.tasks.get(), R.n_tasks.get(), 1, s, R.task_cap, R.stage_x.get(), R.stage_lo.get(),
@@ -232,14 +250,15 @@ void IepSession::forward_resblock() {
       prof_.end(stream_);
       ++launches_;
     }
-    // conv1x1 + conv3x3 #1 + conv3x3 #2 (+ residual) of the step, one launch
+    // conv1x1 + conv3x3 #1 + conv3x3 #2 (+ residual) of the step(s), one launch
     prof_.begin(4, stream_);
-    check(dbk_rb_step(s, R.epoch, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(),
+    check(dbk_rb_step(s, one_launch ? S : s + 1, R.epoch, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(),
                       R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(),
                       R.memtab.get(), R.stage_x.get(), R.stage_lo.get(), R.stage_cat.get(), R.stage_mid.get(),
                       R.plane_stride, R.w0tab.get(), R.w1tab.get(), R.w2tab.get(), R.b0tab.get(), R.b1tab.get(),
-                      R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.queue.get(), sms, stream_),
+                      R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.step_done.get(), R.queue.get(),
+                      sms, stream_),
           "conv step");
     prof_.end(stream_);
     ++launches_;

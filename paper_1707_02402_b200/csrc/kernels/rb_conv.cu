@@ -137,10 +137,12 @@ struct Item {
   int32_t kind;  // 0 conv1x1, 1 conv3x3 #1, 2 conv3x3 #2, -1 end
   int32_t tile;  // global tile index (bin-tile list for kind 0)
   int32_t g, q0;
+  int32_t step;
 };
 
 struct StepParams {
-  int32_t step, epoch, lookahead, debug;
+  int32_t step, step_end;  // the launch runs steps [step, step_end), step s + 1 after all of step s
+  int32_t epoch, lookahead, debug;
   int32_t diag;  // timing diagnostics only (wrong results): bit 0 skips weight reloads, bit 1 window
                  // reloads, bit 2 the epilogue work (TMEM loads, transposes, stores), bit 3 only its stores
   int32_t cache;  // epilogue store hints: bit 0 streaming for next-launch data, bit 1 evict-last for this launch's
@@ -166,7 +168,8 @@ struct StepParams {
   const uint8_t* ident;  // two 16 KB identity blocks (the residual's weights)
   int32_t* done0;        // per bin tile: conv1x1 done (== epoch)
   int32_t* done1;        // per tile: conv3x3 #1 done (== epoch)
-  int32_t* queue;        // per-step claim counters (zeroed each forward)
+  int32_t* step_done;    // per step: conv3x3 #2 tiles completed (zeroed each forward)
+  int32_t* queue;        // claim counters, one per launch's first step (zeroed each forward)
 };
 
 // Wait accounting (read/reset with dbk_rb_debug()): slot 3 = MMA thread
@@ -212,7 +215,8 @@ __host__ __device__ __forceinline__ int32_t seg_tiles(int32_t rows, int32_t tile
 // MMA-heavy and store-heavy tiles and a #2 tile's inputs are usually done
 // when it is claimed.
 // With CTA pairs, k, n0 and n1 count tile pairs and `crank` picks the tile.
-__device__ __forceinline__ Item step_item(const StepParams& P, int32_t k, int32_t n0, int32_t n1, int32_t crank) {
+__device__ __forceinline__ Item step_item(const StepParams& P, int32_t step, int32_t k, int32_t n0, int32_t n1,
+                                          int32_t crank) {
   int32_t kind, local;
   if (k < n0) {
     kind = 0;
@@ -236,13 +240,14 @@ __device__ __forceinline__ Item step_item(const StepParams& P, int32_t k, int32_
   }
   Item it;
   it.kind = kind;
+  it.step = step;
   local = local * kCluster + crank;
   if (kind == 0) {
-    it.tile = P.step_bintile_begin[P.step] + local;
+    it.tile = P.step_bintile_begin[step] + local;
     it.g = P.bin_group[it.tile];
     it.q0 = P.bin_q0[it.tile];
   } else {
-    it.tile = P.step_tile_begin[P.step] + local;
+    it.tile = P.step_tile_begin[step] + local;
     it.g = P.tile_group[it.tile];
     it.q0 = P.tile_q0[it.tile];
   }
@@ -261,7 +266,7 @@ __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& 
   const int32_t nt = seg_tiles(rows, kTileM);
   const int32_t i = (it.q0 - P.seg_start[g] + kLead) / kTileM;
   const bool binary = P.group_bintile0[g] >= 0;
-  const int32_t b0 = binary ? P.step_bintile_begin[P.step] + P.group_bintile0[g] : 0;
+  const int32_t b0 = binary ? P.step_bintile_begin[it.step] + P.group_bintile0[g] : 0;
   if (it.kind == 1) {
     if (!binary) return;
     for (int32_t j = max(i - 1, 0); j <= min(i + 1, nt - 1); ++j) wait_flag(P.done0 + b0 + j, P.epoch);
@@ -269,7 +274,7 @@ __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& 
     if (!binary) return;
     wait_flag(P.done0 + b0 + i, P.epoch);
   } else {  // conv3x3 #2, W2 phase: mid of tiles i-1..i+1
-    const int32_t t0 = P.step_tile_begin[P.step] + P.group_tile0[g];
+    const int32_t t0 = P.step_tile_begin[it.step] + P.group_tile0[g];
     for (int32_t j = max(i - 1, 0); j <= min(i + 1, nt - 1); ++j) wait_flag(P.done1 + t0 + j, P.epoch);
   }
   fence_proxy_async_global();
@@ -536,16 +541,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
   if (kCluster > 1) cluster_sync();  // the partner's barriers exist before any remote arrive / multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int32_t n0 = P.step_bintile_begin[P.step + 1] - P.step_bintile_begin[P.step];
-  const int32_t n1 = P.step_tile_begin[P.step + 1] - P.step_tile_begin[P.step];
-  const int32_t total = n0 + 2 * n1;
-  const int32_t n_units = total / kCluster;  // tiles, or tile pairs (segments hold whole pairs)
+  // work units (tiles, or tile pairs: segments hold whole pairs) of step s
+  auto step_units = [&](int32_t s) {
+    return (P.step_bintile_begin[s + 1] - P.step_bintile_begin[s] +
+            2 * (P.step_tile_begin[s + 1] - P.step_tile_begin[s])) / kCluster;
+  };
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------------- scheduler + activation windows
       uint32_t ai = 0;
       long long w_item = 0, w_dep = 0, w_slot = 0;
       const long long t_start = clock64();
+      // claims k are increasing, so the step cursor only moves forward
+      int32_t cur = P.step, cur_begin = 0, cur_units = P.step < P.step_end ? step_units(P.step) : 0;
+      int32_t ready = P.step;  // steps < ready have all their conv3x3 #2 tiles done (as far as we waited)
       for (int32_t n = 0;; ++n) {
         const int slot = n % kItemSlots;
         int32_t k;
@@ -561,14 +570,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           k = static_cast<int32_t>(*reinterpret_cast<volatile uint32_t*>(mail + slot));
           mbar_arrive_remote(mail_empty + slot, 0);
         }
-        const Item it = k < n_units ? step_item(P, k, n0 / kCluster, n1 / kCluster, static_cast<int32_t>(crank))
-                                    : Item{-1, 0, 0, 0};
+        while (cur < P.step_end && k >= cur_begin + cur_units) {
+          cur_begin += cur_units;
+          if (++cur < P.step_end) cur_units = step_units(cur);
+        }
+        Item it{-1, 0, 0, 0, 0};
+        if (cur < P.step_end) {
+          const int32_t n0 = P.step_bintile_begin[cur + 1] - P.step_bintile_begin[cur];
+          const int32_t n1 = P.step_tile_begin[cur + 1] - P.step_tile_begin[cur];
+          it = step_item(P, cur, k - cur_begin, n0 / kCluster, n1 / kCluster, static_cast<int32_t>(crank));
+        }
         long long c0 = DBG ? clock64() : 0;
         mbar_wait(item_empty + slot, ((n / kItemSlots) & 1) ^ 1);
         if (DBG) w_item += clock64() - c0;
         items[slot] = it;
         mbar_arrive(item_full + slot);
         if (it.kind < 0) break;
+        if (it.step > ready) {
+          // step s reads what step s − 1 (and earlier) wrote: wait until every
+          // conv3x3 #2 tile of the previous step has published its outputs
+          if (DBG) c0 = clock64();
+          for (; ready < it.step; ++ready)
+            wait_count(P.step_done + ready, P.step_tile_begin[ready + 1] - P.step_tile_begin[ready]);
+          fence_proxy_async_global();
+          if (DBG) w_dep += clock64() - c0;
+        }
         for (int p = 0; p < n_phases(it.kind); ++p) {
           if (p == 0 || p == 2) {  // conv3x3 #2 waits for the mid tiles only before its W2 phase
             if (DBG) c0 = clock64();
@@ -756,12 +782,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       mbar_arrive(acc_empty + abuf);
       __syncwarp();
       if (lane == 0) mbar_arrive(tab_empty + abuf);
-      if (it.kind < 2) {  // publish: the tile's outputs are complete
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-        if (threadIdx.x == 64) {
-          __threadfence();
-          st_release_gpu((it.kind == 0 ? P.done0 : P.done1) + it.tile, P.epoch);
-        }
+      // publish: the tile's outputs are complete (conv1x1 / conv3x3 #1: a
+      // per-tile flag; conv3x3 #2: the step's completed-tile count)
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      if (threadIdx.x == 64) {
+        __threadfence();
+        if (it.kind < 2) st_release_gpu((it.kind == 0 ? P.done0 : P.done1) + it.tile, P.epoch);
+        else red_release_gpu_add(P.step_done + it.step, 1);
       }
     }
   }
@@ -1114,7 +1141,8 @@ extern "C" int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, c
   return static_cast<int>(cudaGetLastError());
 }
 
-extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile_begin, const int32_t* tile_group,
+extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* step_tile_begin,
+                           const int32_t* tile_group,
                            const int32_t* tile_q0, const int32_t* step_bintile_begin, const int32_t* bin_group,
                            const int32_t* bin_q0, const int32_t* group_fid, const int32_t* group_begin,
                            const int32_t* seg_start, const int32_t* group_tile0, const int32_t* group_bintile0,
@@ -1122,7 +1150,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile
                            int64_t plane_stride, const void* const* w0, const void* const* w1,
                            const void* const* w2, const float* const* b0, const float* const* b1,
                            const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
-                           int32_t* queue, int32_t num_sms, void* stream) {
+                           int32_t* step_done, int32_t* queue, int32_t num_sms, void* stream) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_rb_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
@@ -1131,6 +1159,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile
   }
   StepParams p{};
   p.step = step;
+  p.step_end = step_end;
   p.epoch = epoch;
   const char* la = std::getenv("DYNBATCH_LOOKAHEAD");
   // one SM-row of tiles ahead: a conv3x3 #2 tile reads mid written ~2·SMs
@@ -1167,6 +1196,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t epoch, const int32_t* step_tile
   p.ident = static_cast<const uint8_t*>(ident);
   p.done0 = done0;
   p.done1 = done1;
+  p.step_done = step_done;
   p.queue = queue;
   // persistent: one CTA per SM, in clusters of kCluster
   cudaLaunchConfig_t cfg{};

@@ -82,10 +82,26 @@ __device__ __forceinline__ void st_release_gpu(int32_t* p, int32_t v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Release-ordered atomic add (publishes this thread's earlier writes,
+// fenced by the caller, to an acquiring reader of the counter).
+__device__ __forceinline__ void red_release_gpu_add(int32_t* p, int32_t v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Generic-proxy global writes observed (acquired) by this thread become
 // visible to its later async-proxy (TMA) reads.
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Spins until *counter >= want (acquire; 4 s watchdog).
+__device__ __forceinline__ void wait_count(const int32_t* counter, int32_t want) {
+  if (ld_acquire_gpu(counter) >= want) return;
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_gpu(counter) < want) {
+    __nanosleep(64);
+    if (global_ns() - t0 > 4000000000ull) __trap();
+  }
 }
 
 // Spins until *flag == want (with the same 4 s watchdog as mbar_wait).
