@@ -85,6 +85,11 @@ int dbk_dense_step(int32_t step, int32_t width, const int32_t* step_group_begin,
                    int32_t blocks, void* stream);
 
 /* root rows → out[b × width] (fp64). */
+/* apply_module (src/modules.cpp:52-108) on stacked rows: x [rows][arity·width]
+ * (operand k of a row at column k·width), w [arity·width][width], bias
+ * [width] → out [rows][width]; the fp64 fma chain of dbk_dense_step. */
+int dbk_dense_apply(int64_t rows, int32_t arity, int32_t width, const double* x, const double* w,
+                    const double* bias, double* out, void* stream);
 int dbk_dense_gather_roots(int64_t b, int32_t width, const int32_t* root_g,
                            const int32_t* present, const double* values, double* out,
                            int32_t* err, void* stream);

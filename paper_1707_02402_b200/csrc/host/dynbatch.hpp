@@ -264,6 +264,10 @@ struct ModuleImpl {
 };
 ModuleImpl make_module_impl(const ModuleSpec& spec, int width, std::uint64_t seed);
 
+// One module call on stacked operand rows (src/modules.cpp:52-108; runs on
+// the device, bit-identical to execute()).
+TensorBatch apply_module(const ModuleImpl& impl, std::span<const TensorBatch> operands);
+
 class ModuleSet {
  public:
   ModuleSet(const FunctionVocab& vocab, std::uint64_t seed);
@@ -289,6 +293,26 @@ struct ResBlockImpl {
 ResBlockImpl make_resblock_impl(int arity, int channels, std::uint64_t seed, int fid);
 
 // --------------------------------------------------------------- executor
+// Single-assignment store of per-node rows (src/executor.cpp:26-70): the
+// reference executor's host container. Reading an absent node throws
+// MissingOperand; writing a node twice throws SingleAssignmentViolation.
+class ValueStore {
+ public:
+  ValueStore(std::span<const Program> batch, std::int64_t width);
+  std::int64_t width() const { return width_; }
+  bool has(NodeRef ref) const;
+  std::span<const double> row(NodeRef ref) const;
+  void set(NodeRef ref, std::span<const double> value);
+
+ private:
+  void check_ref(NodeRef ref) const;
+  std::int64_t width_;
+  std::vector<std::vector<double>> values_;
+  std::vector<std::vector<char>> present_;
+};
+TensorBatch gather_rows(const ValueStore& store, std::span<const NodeRef> refs);
+void scatter_rows(ValueStore& store, std::span<const NodeRef> refs, const TensorBatch& values);
+
 struct ExecutionTrace {
   std::int64_t expensive_calls = 0;
   std::vector<std::int64_t> per_function_calls;
@@ -347,6 +371,8 @@ class ExpertSet {
   std::uint64_t seed() const { return seed_; }
   std::int64_t weight_element_count() const;
   const Expert& expert(std::int64_t id) const { return experts_[static_cast<size_t>(id)]; }
+  // relu(rows · W1) · W2 for one expert (src/moe.cpp:98-145; on the device)
+  TensorBatch apply(std::int64_t expert_id, const TensorBatch& rows) const;
 
  private:
   std::vector<Expert> experts_;
@@ -420,6 +446,10 @@ std::string program_set_to_json(const FunctionVocab& vocab, std::span<const Prog
 ProgramSet program_set_from_json(const std::string& text, int width);
 std::string schedule_to_json(const Schedule& schedule);
 std::string trace_to_json(const ExecutionTrace& trace);
+std::string workload_spec_to_json(const WorkloadSpec& spec);
+WorkloadSpec workload_spec_from_json(const std::string& text);
+std::string moe_config_to_json(const MoeConfig& cfg);
+MoeConfig moe_config_from_json(const std::string& text);
 
 // ----------------------------------------------------------- verification
 struct VerifyOptions {

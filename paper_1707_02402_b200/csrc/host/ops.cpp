@@ -1,10 +1,12 @@
 // ops.cpp — module registry, executor and MoE operator API (device-backed).
 //
 //   make_module_impl / ModuleSet ... src/modules.cpp:13-50
+//   apply_module ................... src/modules.cpp:52-108 (runs on device)
+//   ValueStore, gather/scatter_rows  src/executor.cpp:26-93 (host containers)
 //   execute ........................ src/executor.cpp:95-182 (runs on device)
 //   MoeConfig::check ............... src/moe.cpp:20-28
 //   top_k_gate ..................... src/moe.cpp:36-69 (runs on device)
-//   ExpertSet ...................... src/moe.cpp:71-96
+//   ExpertSet (+ apply on device) .. src/moe.cpp:71-145
 //   moe_forward_{naive,batched} .... src/moe.cpp:162-270 (run on device)
 //   memory model ................... src/moe.cpp:272-289
 #include <algorithm>
@@ -12,6 +14,7 @@
 #include <cmath>
 
 #include "device.hpp"
+#include "dynbatch/dbk.h"
 #include "dynbatch.hpp"
 
 namespace dynbatch {
@@ -163,6 +166,155 @@ double moe_memory_ratio(const MoeConfig& cfg) {
   return cfg.examples_per_expert * static_cast<double>(2 * cfg.data_dim + cfg.hidden) /
          (2.0 * static_cast<double>(cfg.active_per_example) * static_cast<double>(cfg.hidden) *
           static_cast<double>(cfg.data_dim));
+}
+
+// ------------------------------------------------- operator-level API
+namespace {
+std::string ref_text(NodeRef r) {
+  return "(" + std::to_string(r.example) + ", " + std::to_string(r.node) + ")";
+}
+
+// Device copies for one operator call; the result comes back to the host.
+struct DeviceCall {
+  cudaStream_t s = nullptr;
+  DeviceCall() {
+    dev::require_device();
+    dev::check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  }
+  ~DeviceCall() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+}  // namespace
+
+ValueStore::ValueStore(std::span<const Program> batch, std::int64_t width) : width_(width) {
+  if (width <= 0) throw_error(Errc::invalid_argument, "width must be positive");
+  for (const Program& p : batch) {
+    values_.emplace_back(static_cast<size_t>(p.size()) * static_cast<size_t>(width), 0.0);
+    present_.emplace_back(static_cast<size_t>(p.size()), 0);
+  }
+}
+
+void ValueStore::check_ref(NodeRef ref) const {
+  const bool ok = ref.example >= 0 && static_cast<size_t>(ref.example) < present_.size() && ref.node >= 0 &&
+                  static_cast<size_t>(ref.node) < present_[static_cast<size_t>(ref.example)].size();
+  if (!ok) throw_error(Errc::invalid_argument, "node ref out of range " + ref_text(ref));
+}
+
+bool ValueStore::has(NodeRef ref) const {
+  check_ref(ref);
+  return present_[static_cast<size_t>(ref.example)][static_cast<size_t>(ref.node)] != 0;
+}
+
+std::span<const double> ValueStore::row(NodeRef ref) const {
+  if (!has(ref)) throw_error(Errc::missing_operand, "no value for node " + ref_text(ref));
+  return {values_[static_cast<size_t>(ref.example)].data() + static_cast<size_t>(ref.node) * width_,
+          static_cast<size_t>(width_)};
+}
+
+void ValueStore::set(NodeRef ref, std::span<const double> value) {
+  check_ref(ref);
+  if (static_cast<std::int64_t>(value.size()) != width_)
+    throw_error(Errc::width_mismatch, "row width " + std::to_string(value.size()));
+  char& here = present_[static_cast<size_t>(ref.example)][static_cast<size_t>(ref.node)];
+  if (here) throw_error(Errc::single_assignment_violation, "node " + ref_text(ref) + " written twice");
+  std::copy(value.begin(), value.end(),
+            values_[static_cast<size_t>(ref.example)].begin() + static_cast<std::ptrdiff_t>(ref.node * width_));
+  here = 1;
+}
+
+TensorBatch gather_rows(const ValueStore& store, std::span<const NodeRef> refs) {
+  TensorBatch out(static_cast<std::int64_t>(refs.size()), store.width());
+  for (size_t i = 0; i < refs.size(); ++i) {
+    const auto src = store.row(refs[i]);
+    std::copy(src.begin(), src.end(), out.row(static_cast<std::int64_t>(i)).begin());
+  }
+  return out;
+}
+
+void scatter_rows(ValueStore& store, std::span<const NodeRef> refs, const TensorBatch& values) {
+  if (values.rows() != static_cast<std::int64_t>(refs.size()))
+    throw_error(Errc::row_count_mismatch,
+                std::to_string(values.rows()) + " rows for " + std::to_string(refs.size()) + " refs");
+  if (values.width() != store.width())
+    throw_error(Errc::width_mismatch, "value width " + std::to_string(values.width()));
+  for (size_t i = 0; i < refs.size(); ++i) store.set(refs[i], values.row(static_cast<std::int64_t>(i)));
+}
+
+// One module call on stacked operand rows, on the device (dbk_dense_apply:
+// the executor's fp64 fma chain, so the bits match execute() and the
+// reference). Shape errors as the reference (src/modules.cpp:53-73).
+TensorBatch apply_module(const ModuleImpl& impl, std::span<const TensorBatch> operands) {
+  const int arity = impl.spec.arity;
+  if (arity == 0) throw_error(Errc::arity_mismatch, "arity-0 functions fetch inputs, they are not applied");
+  if (static_cast<int>(operands.size()) != arity)
+    throw_error(Errc::arity_mismatch, "function " + std::to_string(impl.spec.function_id) + " expects " +
+                                          std::to_string(arity) + " operands, got " +
+                                          std::to_string(operands.size()));
+  const std::int64_t rows = operands[0].rows();
+  const std::int64_t width = impl.spec.out_width;
+  for (const TensorBatch& op : operands) {
+    if (op.rows() != rows) throw_error(Errc::row_count_mismatch, "operand row counts differ");
+    if (op.width() != width)
+      throw_error(Errc::width_mismatch,
+                  "operand width " + std::to_string(op.width()) + ", expected " + std::to_string(width));
+  }
+  TensorBatch out(rows, width);
+  if (rows == 0) return out;
+  std::vector<double> x(static_cast<size_t>(rows * arity * width));
+  for (std::int64_t r = 0; r < rows; ++r)
+    for (int k = 0; k < arity; ++k) {
+      const auto src = operands[static_cast<size_t>(k)].row(r);
+      std::copy(src.begin(), src.end(), x.begin() + static_cast<std::ptrdiff_t>((r * arity + k) * width));
+    }
+  DeviceCall call;
+  dev::Buf<double> dx, dw, db, dout;
+  dx.upload(x, call.s);
+  dw.upload(impl.weights, call.s);
+  db.upload(impl.bias, call.s);
+  dout.alloc(static_cast<size_t>(rows * width));
+  dev::check(dbk_dense_apply(rows, arity, static_cast<std::int32_t>(width), dx.get(), dw.get(), db.get(), dout.get(),
+                             call.s),
+             "dbk_dense_apply");
+  const auto y = dout.download(static_cast<size_t>(rows * width), call.s);
+  std::copy(y.begin(), y.end(), out.data().begin());
+  return out;
+}
+
+// One expert on stacked rows (src/moe.cpp:98-145), on the device through the
+// MoE fp64 expert kernels (one expert, the identity order).
+TensorBatch ExpertSet::apply(std::int64_t expert_id, const TensorBatch& rows) const {
+  if (expert_id < 0 || expert_id >= size()) throw_error(Errc::invalid_argument, "expert id " + std::to_string(expert_id));
+  if (rows.width() != data_dim_)
+    throw_error(Errc::width_mismatch, "expert input width " + std::to_string(rows.width()));
+  const std::int64_t n = rows.rows();
+  TensorBatch out(n, data_dim_);
+  if (n == 0) return out;
+  const Expert& ex = experts_[static_cast<size_t>(expert_id)];
+  DeviceCall call;
+  std::vector<std::int32_t> order(static_cast<size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) order[static_cast<size_t>(i)] = static_cast<std::int32_t>(i);
+  const std::vector<std::int32_t> offsets{0, static_cast<std::int32_t>(n)};
+  dev::Buf<double> dx, dw1, dw2, hidden, staged;
+  dev::Buf<std::int32_t> dorder, doff, tiles;
+  dev::Buf<const double*> w1tab, w2tab;
+  dx.upload(rows.data().data(), rows.data().size(), call.s);
+  dw1.upload(ex.w1, call.s);
+  dw2.upload(ex.w2, call.s);
+  w1tab.upload(std::vector<const double*>{dw1.get()}, call.s);
+  w2tab.upload(std::vector<const double*>{dw2.get()}, call.s);
+  dorder.upload(order, call.s);
+  doff.upload(offsets, call.s);
+  tiles.alloc(2);
+  hidden.alloc(static_cast<size_t>(n * hidden_));
+  staged.alloc(static_cast<size_t>(n * data_dim_));
+  dev::check(dbk_moe_expert_fp64(n, 1, 1, static_cast<std::int32_t>(data_dim_), static_cast<std::int32_t>(hidden_),
+                                 dorder.get(), doff.get(), dx.get(), w1tab.get(), w2tab.get(), hidden.get(),
+                                 staged.get(), tiles.get(), call.s),
+             "dbk_moe_expert_fp64");
+  const auto y = staged.download(static_cast<size_t>(n * data_dim_), call.s);
+  std::copy(y.begin(), y.end(), out.data().begin());
+  return out;
 }
 
 }  // namespace dynbatch

@@ -7,7 +7,9 @@
 // program-set wire format {"vocab": [{"id","arity","cost"}...],
 // "programs": [[fid, ...], ...]} (src/serialize.cpp:37-80) with ParseError
 // on malformed input.
+#include <cerrno>
 #include <cmath>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -46,6 +48,7 @@ using Array = std::vector<Value>;
 using Object = std::map<std::string, Value>;
 struct Value {
   std::variant<std::nullptr_t, bool, double, std::string, std::shared_ptr<Array>, std::shared_ptr<Object>> v;
+  std::string num;  // a number's source text (exact 64-bit integers)
   bool is_obj() const { return v.index() == 5; }
   bool is_arr() const { return v.index() == 4; }
   const Object& obj() const { return *std::get<5>(v); }
@@ -90,7 +93,9 @@ class Parser {
       const double d = std::strtod(begin, &end);
       if (end == begin) fail("bad number");
       i_ += static_cast<size_t>(end - begin);
-      return Value{d};
+      Value out{d};
+      out.num.assign(begin, static_cast<size_t>(end - begin));
+      return out;
     }
     fail(std::string("unexpected character '") + c + "'");
   }
@@ -153,6 +158,31 @@ int as_int(const Value& v, const char* what) {
     throw_error(Errc::parse_error, std::string("[json] ") + what + " must be an integer");
   }
   return static_cast<int>(d);
+}
+
+// A 64-bit integer member (exact, from the number's text).
+template <typename T>
+T as_integer(const Value& v, const char* what) {
+  if (v.v.index() != 2 || v.num.find_first_of(".eE") != std::string::npos)
+    throw_error(Errc::parse_error, std::string("[json] ") + what + " must be an integer");
+  errno = 0;
+  char* end = nullptr;
+  if constexpr (std::is_signed_v<T>) {
+    const long long x = std::strtoll(v.num.c_str(), &end, 10);
+    if (errno != 0 || *end) throw_error(Errc::parse_error, std::string("[json] ") + what + " is out of range");
+    return static_cast<T>(x);
+  } else {
+    if (!v.num.empty() && v.num[0] == '-')
+      throw_error(Errc::parse_error, std::string("[json] ") + what + " must not be negative");
+    const unsigned long long x = std::strtoull(v.num.c_str(), &end, 10);
+    if (errno != 0 || *end) throw_error(Errc::parse_error, std::string("[json] ") + what + " is out of range");
+    return static_cast<T>(x);
+  }
+}
+
+double as_double(const Value& v, const char* what) {
+  if (v.v.index() != 2) throw_error(Errc::parse_error, std::string("[json] ") + what + " must be a number");
+  return std::get<2>(v.v);
 }
 
 const Value& member(const Object& o, const char* key) {
@@ -273,6 +303,66 @@ std::string trace_to_json(const ExecutionTrace& trace) {
   s += ",\n  \"total_seconds\": " + number(trace.total_seconds);
   s += "\n}";
   return s;
+}
+
+// WorkloadSpec and MoeConfig as JSON objects (src/serialize.cpp:118-175):
+// keys in sorted order, two-space indent. Parsing takes the same keys,
+// optional ones defaulting to the struct defaults; errors are ParseError.
+std::string workload_spec_to_json(const WorkloadSpec& spec) {
+  std::string s = "{\n";
+  s += "  \"b\": " + std::to_string(spec.b) + ",\n";
+  s += "  \"branch_prob\": " + number(spec.branch_prob) + ",\n";
+  s += "  \"depth\": " + std::to_string(spec.depth) + ",\n";
+  s += std::string("  \"kind\": \"") + workload_kind_name(spec.kind) + "\",\n";
+  s += "  \"length\": " + std::to_string(spec.length) + ",\n";
+  s += "  \"p\": " + std::to_string(spec.p) + ",\n";
+  s += "  \"seed\": " + std::to_string(spec.seed) + ",\n";
+  s += "  \"width\": " + std::to_string(spec.width) + "\n}";
+  return s;
+}
+
+WorkloadSpec workload_spec_from_json(const std::string& text) {
+  const Value doc = Parser(text).parse_document();
+  if (!doc.is_obj()) throw_error(Errc::parse_error, "[json] a workload spec is an object");
+  const Object& o = doc.obj();
+  WorkloadSpec spec;
+  const Value& kind = member(o, "kind");
+  if (kind.v.index() != 3) throw_error(Errc::parse_error, "[json] kind must be a string");
+  spec.kind = workload_kind_from_name(std::get<3>(kind.v));
+  if (o.count("b")) spec.b = as_integer<std::int64_t>(o.at("b"), "b");
+  if (o.count("p")) spec.p = as_integer<int>(o.at("p"), "p");
+  if (o.count("width")) spec.width = as_integer<int>(o.at("width"), "width");
+  if (o.count("depth")) spec.depth = as_integer<int>(o.at("depth"), "depth");
+  if (o.count("length")) spec.length = as_integer<int>(o.at("length"), "length");
+  if (o.count("branch_prob")) spec.branch_prob = as_double(o.at("branch_prob"), "branch_prob");
+  if (o.count("seed")) spec.seed = as_integer<std::uint64_t>(o.at("seed"), "seed");
+  return spec;
+}
+
+std::string moe_config_to_json(const MoeConfig& cfg) {
+  std::string s = "{\n";
+  s += "  \"b\": " + std::to_string(cfg.batch) + ",\n";
+  s += "  \"data_dim\": " + std::to_string(cfg.data_dim) + ",\n";
+  s += "  \"hidden\": " + std::to_string(cfg.hidden) + ",\n";
+  s += "  \"k\": " + std::to_string(cfg.active_per_example) + ",\n";
+  s += "  \"m\": " + number(cfg.examples_per_expert) + ",\n";
+  s += "  \"n\": " + std::to_string(cfg.experts) + "\n}";
+  return s;
+}
+
+MoeConfig moe_config_from_json(const std::string& text) {
+  const Value doc = Parser(text).parse_document();
+  if (!doc.is_obj()) throw_error(Errc::parse_error, "[json] a MoE config is an object");
+  const Object& o = doc.obj();
+  MoeConfig cfg;
+  cfg.experts = as_integer<std::int64_t>(member(o, "n"), "n");
+  cfg.active_per_example = as_integer<std::int64_t>(member(o, "k"), "k");
+  if (o.count("b")) cfg.batch = as_integer<std::int64_t>(o.at("b"), "b");
+  if (o.count("data_dim")) cfg.data_dim = as_integer<std::int64_t>(o.at("data_dim"), "data_dim");
+  if (o.count("hidden")) cfg.hidden = as_integer<std::int64_t>(o.at("hidden"), "hidden");
+  if (o.count("m")) cfg.examples_per_expert = as_double(o.at("m"), "m");
+  cfg.check();  // validated on parse (k ≤ n, positive sizes)
+  return cfg;
 }
 
 }  // namespace dynbatch

@@ -120,6 +120,34 @@ __global__ void __launch_bounds__(128) k_dense_step(
   }
 }
 
+// apply_module on stacked operand rows (src/modules.cpp:52-108): x is
+// [rows][a·W] (operand k of row r at x[r·a·W + k·W]), out[r][j] =
+// relu(bias[j] + Σ_i x[r][i] · w[i·W + j]), the same fma chain per output
+// as k_dense_step (so a row gives the same bits alone or batched).
+__global__ void __launch_bounds__(128) k_dense_apply(int64_t rows, int32_t xw, int32_t W,
+                                                     const double* __restrict__ x, const double* __restrict__ w,
+                                                     const double* __restrict__ bias, double* __restrict__ out) {
+  extern __shared__ double xs[];  // [kRows][xw]
+  for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRows; r0 < rows;
+       r0 += static_cast<int64_t>(gridDim.x) * kRows) {
+    const int32_t n = static_cast<int32_t>(rows - r0 < kRows ? rows - r0 : kRows);
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < n * xw; i += blockDim.x) xs[i] = x[r0 * xw + i];
+    __syncthreads();
+    for (int32_t j = threadIdx.x; j < W; j += blockDim.x) {
+      double acc[kRows];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) acc[r] = bias[j];
+      for (int32_t i = 0; i < xw; ++i) {
+        const double wij = w[static_cast<int64_t>(i) * W + j];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) acc[r] = __fma_rn(xs[(r < n ? r : 0) * xw + i], wij, acc[r]);
+      }
+      for (int r = 0; r < n; ++r) out[(r0 + r) * W + j] = acc[r] > 0.0 ? acc[r] : 0.0;
+    }
+  }
+}
+
 __global__ void k_dense_roots(int64_t b, int32_t W, const int32_t* __restrict__ root_g,
                               const int32_t* __restrict__ present, const double* __restrict__ values,
                               double* __restrict__ out, int32_t* __restrict__ err) {
@@ -164,5 +192,18 @@ extern "C" int dbk_dense_gather_roots(int64_t b, int32_t width, const int32_t* r
   if (b <= 0) return 0;
   k_dense_roots<<<static_cast<unsigned>(b), 128, 0, static_cast<cudaStream_t>(stream)>>>(
       b, width, root_g, present, values, out, err);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_dense_apply(int64_t rows, int32_t arity, int32_t width, const double* x, const double* w,
+                               const double* bias, double* out, void* stream) {
+  if (rows <= 0) return 0;
+  const int32_t xw = arity * width;
+  const size_t smem = sizeof(double) * kRows * static_cast<size_t>(xw);
+  if (smem > 227 * 1024) return static_cast<int>(cudaErrorInvalidValue);
+  cudaFuncSetAttribute(k_dense_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  const int64_t tiles = (rows + kRows - 1) / kRows;
+  const unsigned blocks = static_cast<unsigned>(tiles < 148 * 8 ? tiles : 148 * 8);
+  k_dense_apply<<<blocks, 128, smem, static_cast<cudaStream_t>(stream)>>>(rows, xw, width, x, w, bias, out);
   return static_cast<int>(cudaGetLastError());
 }

@@ -1,10 +1,10 @@
 // tests/cpp/doctest.h — a minimal stand-in for the doctest macros the
-// reference's C-ABI test suite uses (TEST_CASE, CHECK, REQUIRE,
-// doctest::Approx; DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN). doctest itself is
+// reference's test suites use (TEST_CASE, CHECK, CHECK_FALSE, REQUIRE,
+// CHECK_THROWS_AS, CHECK_THROWS_WITH_AS, INFO, FAIL, doctest::Approx,
+// doctest::Contains; DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN). doctest itself is
 // not in this image. Test infrastructure only: oracle/Makefile builds the
-// reference's tests/test_capi.cpp against THIS repository's
-// include/dynbatch/dynbatch.h and libdynbatch.so with it, so the reference's
-// own client tests exercise the drop-in library.
+// reference's tests/*.cpp against THIS repository's headers and library
+// with it, so the reference's own tests exercise the drop-in code.
 #pragma once
 
 #include <algorithm>
@@ -13,6 +13,7 @@
 #include <functional>
 #include <limits>
 #include <string>
+#include <exception>
 #include <vector>
 
 namespace doctest {
@@ -20,15 +21,32 @@ namespace doctest {
 struct Approx {
   explicit Approx(double v) : value(v) {}
   double value;
-  double epsilon = static_cast<double>(std::numeric_limits<float>::epsilon()) * 100;
-  double scale = 1.0;
+  double eps = static_cast<double>(std::numeric_limits<float>::epsilon()) * 100;
+  double scl = 1.0;
+  Approx& epsilon(double e) {
+    eps = e;
+    return *this;
+  }
+  Approx& scale(double s) {
+    scl = s;
+    return *this;
+  }
   friend bool operator==(double lhs, const Approx& a) {
-    return std::fabs(lhs - a.value) < a.epsilon * (a.scale + std::max(std::fabs(lhs), std::fabs(a.value)));
+    return std::fabs(lhs - a.value) < a.eps * (a.scl + std::max(std::fabs(lhs), std::fabs(a.value)));
   }
   friend bool operator==(const Approx& a, double rhs) { return rhs == a; }
 };
 
+struct Contains {
+  explicit Contains(const char* s) : text(s) {}
+  std::string text;
+};
+
 namespace detail {
+inline bool matches(const std::string& what, const char* exact) { return what == exact; }
+inline bool matches(const std::string& what, const std::string& exact) { return what == exact; }
+inline bool matches(const std::string& what, const Contains& c) { return what.find(c.text) != std::string::npos; }
+
 struct Case {
   const char* name;
   std::function<void()> fn;
@@ -71,6 +89,42 @@ inline void report(bool ok, const char* kind, const char* expr, const char* file
     const bool doctest_ok_ = static_cast<bool>(__VA_ARGS__);                                      \
     doctest::detail::report(doctest_ok_, "REQUIRE", #__VA_ARGS__, __FILE__, __LINE__);            \
     if (!doctest_ok_) throw doctest::detail::RequireFailed{};                                      \
+  } while (0)
+
+#define CHECK_FALSE(...) \
+  doctest::detail::report(!static_cast<bool>(__VA_ARGS__), "CHECK_FALSE", #__VA_ARGS__, __FILE__, __LINE__)
+#define CHECK_THROWS_AS(expr, ...)                                                                \
+  do {                                                                                            \
+    bool doctest_ok_ = false;                                                                     \
+    try {                                                                                         \
+      static_cast<void>(expr);                                                                    \
+    } catch (const __VA_ARGS__&) {                                                                \
+      doctest_ok_ = true;                                                                         \
+    } catch (...) {                                                                               \
+    }                                                                                             \
+    doctest::detail::report(doctest_ok_, "CHECK_THROWS_AS", #expr, __FILE__, __LINE__);           \
+  } while (0)
+#define CHECK_THROWS_WITH_AS(expr, with, ...)                                                     \
+  do {                                                                                            \
+    bool doctest_ok_ = false;                                                                     \
+    std::string doctest_what_ = "(no exception)";                                                 \
+    try {                                                                                         \
+      static_cast<void>(expr);                                                                    \
+    } catch (const __VA_ARGS__& e) {                                                              \
+      doctest_what_ = e.what();                                                                   \
+      doctest_ok_ = doctest::detail::matches(doctest_what_, with);                                \
+    } catch (const std::exception& e) {                                                           \
+      doctest_what_ = std::string("(other type) ") + e.what();                                    \
+    } catch (...) {                                                                               \
+    }                                                                                             \
+    doctest::detail::report(doctest_ok_, "CHECK_THROWS_WITH_AS", #expr, __FILE__, __LINE__);      \
+    if (!doctest_ok_) std::printf("    what(): %s\n", doctest_what_.c_str());                     \
+  } while (0)
+#define INFO(...) ((void)0)
+#define FAIL(...)                                                                                 \
+  do {                                                                                            \
+    doctest::detail::report(false, "FAIL", #__VA_ARGS__, __FILE__, __LINE__);                     \
+    throw doctest::detail::RequireFailed{};                                                       \
   } while (0)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
