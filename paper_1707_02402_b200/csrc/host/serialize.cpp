@@ -48,7 +48,7 @@ using Array = std::vector<Value>;
 using Object = std::map<std::string, Value>;
 struct Value {
   std::variant<std::nullptr_t, bool, double, std::string, std::shared_ptr<Array>, std::shared_ptr<Object>> v;
-  std::string num;  // a number's source text (exact 64-bit integers)
+  std::string num{};  // a number's source text (exact 64-bit integers)
   bool is_obj() const { return v.index() == 5; }
   bool is_arr() const { return v.index() == 4; }
   const Object& obj() const { return *std::get<5>(v); }
