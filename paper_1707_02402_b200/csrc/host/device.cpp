@@ -538,8 +538,20 @@ void IepSession::add_forward_work() {
   const double map32 = 100352.0, stage16 = 225.0 * 16 * 16;
   const double n_exp = n_un + n_bin;
   const double b = static_cast<double>(c.b);
-  // gather: leaf / shared operands, fp32 map → hi (+ lo for unary members)
-  prof_.add_work(2, 0.0, n_un * (map32 + 2 * stage16) + n_bin * 2 * (map32 + stage16));
+  // gather: the operands no child epilogue forwards — leaves and children
+  // with several parents — fp32 map → hi (+ lo for a unary member's input)
+  std::vector<std::int32_t> parents(static_cast<size_t>(c.N), 0);
+  for (std::int32_t ch : c.child_list) ++parents[static_cast<size_t>(ch)];
+  double gather_bytes = 0.0;
+  for (std::int64_t g = 0; g < c.N; ++g) {
+    const int a = c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])];
+    for (std::int32_t e = c.child_off[static_cast<size_t>(g)]; e < c.child_off[static_cast<size_t>(g) + 1]; ++e) {
+      const std::int32_t ch = c.child_list[static_cast<size_t>(e)];
+      const bool leaf = c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(ch)])] == 0;
+      if (leaf || parents[static_cast<size_t>(ch)] > 1) gather_bytes += map32 + (a == 1 ? 2 : 1) * stage16;
+    }
+  }
+  prof_.add_work(2, 0.0, gather_bytes);
   // fused conv step: conv1x1 (binary) + conv3x3 #1 + conv3x3 #2 with the
   // residual; reads x hi, mid, hi/lo; writes mid, hi/lo images (roots: fp32)
   const double conv_flops = n_bin * 12845056.0 + n_exp * 2 * 57802752.0;
