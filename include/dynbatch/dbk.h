@@ -126,7 +126,8 @@ int dbk_rb_gather(const void* tasks, const int32_t* n_tasks, int32_t list, int32
  * them. Tile-level dependencies through done flags (done0 per bin tile,
  * done1 per tile; == epoch means done); queue[step] and step_done[step ..
  * step_end) must be 0 at launch.
- * D[128 channels][256 positions] per tile (tcgen05.mma M = 128, N = 256). */
+ * D[128 channels][tile_m positions] per tile (tcgen05.mma M = 128, N =
+ * tile_m, 256 or 128; the plan must have used the same tile_m). */
 int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* step_tile_begin,
                 const int32_t* tile_group,
                 const int32_t* tile_q0, const int32_t* step_bintile_begin, const int32_t* bin_group,
@@ -135,8 +136,8 @@ int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* st
                 const void* memtab, void* stage_x, void* stage_lo, void* stage_cat, void* stage_mid,
                 int64_t plane_stride, const void* const* w0, const void* const* w1, const void* const* w2,
                 const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
-                int32_t* done0, int32_t* done1, int32_t* step_done, int32_t* queue, int32_t num_sms,
-                void* stream);
+                int32_t* done0, int32_t* done1, int32_t* step_done, int32_t* queue, int32_t tile_m,
+                int32_t num_sms, void* stream);
 /* Zeroes stage_x rows between each segment's last image and its tile end
  * (read as top / left pads by the next segment's first image), every
  * forward, so a new layout needs no full re-zeroing. */

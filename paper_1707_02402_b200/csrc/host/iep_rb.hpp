@@ -63,7 +63,7 @@ struct IepSession::RB {
   std::unique_ptr<Pipe> pipe;
   std::int64_t n_expensive = 0;
   std::int64_t n_shared = 0;  // expensive children with several parents (gathered per step)
-  int tile_m = kTileM;  // positions per scheduled tile
+  int tile_m = kTileM;  // positions per scheduled tile (256, or 128 for small batches)
 };
 
 }  // namespace dynbatch::dev

@@ -79,9 +79,20 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   if (c.max_arity > 2) throw_error(Errc::arity_mismatch, "resblock modules support arity <= 2");
   rb_ = std::make_unique<RB>();
   RB& R = *rb_;
-  R.tile_m = RB::kTileM;
   for (std::int64_t g = 0; g < c.N; ++g)
     if (c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0) ++R.n_expensive;
+  // Tile size: 256 positions, or 128 when a step has too few tiles to fill
+  // the GPU (small batches are latency-bound: twice the tiles, each about
+  // 60% as long). DYNBATCH_TILE_M overrides.
+  {
+    const double per_step = static_cast<double>(R.n_expensive) / std::max(1, c.s_max);
+    const double tiles256 = per_step * 225.0 / RB::kTileM;
+    R.tile_m = tiles256 < 2.0 * sm_count() ? 128 : RB::kTileM;
+    if (const char* t = std::getenv("DYNBATCH_TILE_M")) {
+      const int v = std::atoi(t);
+      if (v == 128 || v == 256) R.tile_m = v;
+    }
+  }
   // buffers are sized for the session capacity (later set_programs batches)
   const size_t b = static_cast<size_t>(std::max<std::int64_t>(c.cap_b, 1));
   const size_t N = static_cast<size_t>(std::max<std::int64_t>(c.cap_N, 1));
@@ -135,7 +146,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   // schedule-derived tables (G ≤ max keys; tiles ≤ N_exp·225/256 + G)
   const size_t G = static_cast<size_t>(std::max(1, c.cap_s)) * c.p + 2;
   const size_t S = N + 2;  // naive: S = N
-  const size_t T = static_cast<size_t>(n_exp_cap) * 225 / RB::kTileM + G + 2;
+  const size_t T = static_cast<size_t>(n_exp_cap) * 225 / static_cast<size_t>(R.tile_m) + G + 2;
   R.seg_start.alloc(std::max(G, N + 2));
   R.group_tile0.alloc(std::max(G, N + 2));
   R.group_bintile0.alloc(std::max(G, N + 2));
@@ -258,7 +269,7 @@ void IepSession::forward_resblock() {
                       R.memtab.get(), R.stage_x.get(), R.stage_lo.get(), R.stage_cat.get(), R.stage_mid.get(),
                       R.plane_stride, R.w0tab.get(), R.w1tab.get(), R.w2tab.get(), R.b0tab.get(), R.b1tab.get(),
                       R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.step_done.get(), R.queue.get(),
-                      sms, stream_),
+                      R.tile_m, sms, stream_),
           "conv step");
     prof_.end(stream_);
     ++launches_;

@@ -72,7 +72,7 @@ constexpr int kImg = 225;                  // 15 × 15 packed grid per image
 constexpr int kPx = 196;                   // 14 × 14
 constexpr int kFmap = kPlanes * kPx * 8;   // 25,088 floats per node map
 constexpr int kGuard = 32;                 // zero positions before position 0
-constexpr int kTileM = 256;                // positions per CTA tile (MMA N)
+constexpr int kTileM = 256;                // positions per CTA tile (MMA N); the kernel also runs 128 (TM)
 constexpr int kHalo = 16;                  // 3×3 window halo (15 + 1 positions)
 constexpr int kLead = 16;                  // zero rows before a segment's first image (its top / left pads)
 #ifndef DYNBATCH_CLUSTER
@@ -101,7 +101,8 @@ constexpr int kWeightWarp = kTableWarp + 1;  // streams the weight stages
 constexpr int kThreads = (kWeightWarp + 1) * 32;
 constexpr int kItemSlots = 4;              // work items in flight between the roles
 constexpr int kChunk = 16;                 // positions per epilogue chunk
-constexpr int kChunks = 128 / kChunk;      // chunks per warp and tile
+template <int TM>
+constexpr int kChunksT = TM / 2 / kChunk;  // 16-position chunks per epilogue warp and tile
 
 // Per-member epilogue metadata (schedule order), built once per forward by
 // k_rb_memtab from the forwarding tables.
@@ -259,12 +260,13 @@ __device__ __forceinline__ Item step_item(const StepParams& P, int32_t step, int
 // a binary group reads z (conv1x1 tiles i-1..i+1); conv3x3 #2 reads mid
 // (conv3x3 #1 tiles i-1..i+1) and, for a binary group, z hi/lo (conv1x1
 // tile i). Halo positions in other segments only feed outputs never stored.
+template <int TM>
 __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& it, int phase) {
   if (it.kind == 0) return;
   const int32_t g = it.g;
   const int32_t rows = P.group_begin[g + 1] - P.group_begin[g];
-  const int32_t nt = seg_tiles(rows, kTileM);
-  const int32_t i = (it.q0 - P.seg_start[g] + kLead) / kTileM;
+  const int32_t nt = seg_tiles(rows, TM);
+  const int32_t i = (it.q0 - P.seg_start[g] + kLead) / TM;
   const bool binary = P.group_bintile0[g] >= 0;
   const int32_t b0 = binary ? P.step_bintile_begin[it.step] + P.group_bintile0[g] : 0;
   if (it.kind == 1) {
@@ -284,8 +286,9 @@ __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& 
 // Fills the table entries of positions lane + 32k (k = 0..7) of a tile from
 // the per-member table: one independent 32-byte load per position, all
 // issued before any entry is stored.
+template <int TM>
 __device__ __forceinline__ void rb_fill_table(const StepParams& P, const Item& it, PosEntry* tab, int lane) {
-  constexpr int kPer = kTileM / 32;
+  constexpr int kPer = TM / 32;
   const int32_t gb0 = P.group_begin[it.g];
   const int32_t rows = P.group_begin[it.g + 1] - gb0;
   const int32_t base = it.q0 - P.seg_start[it.g];
@@ -370,7 +373,7 @@ struct EpiLane {
   int plane_off32;    // fp32 plane-map offset of this lane's plane
 };
 
-template <int KIND>
+template <int KIND, int TM>
 __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntry* tab, const EpiLane& L,
                                               uint32_t taddr, const Item& it) {
   const float* bias_p = P.bias[KIND][P.group_fid[it.g]] + L.plane * 8;
@@ -379,7 +382,9 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
   const float bias[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
   // own-position outputs (conv1x1 → z hi/lo, conv3x3 #1 → mid): row
   // kGuard + q0 + 128·half + 16·cb + 8m + e, so (row & 7) == e
-  const int64_t own_off = L.chunk_off + (static_cast<int64_t>(kGuard + it.q0 + L.half * 128 + L.e) << 7) + (L.sub << 4);
+  constexpr int kChunks = kChunksT<TM>;
+  const int64_t own_off =
+      L.chunk_off + (static_cast<int64_t>(kGuard + it.q0 + L.half * (TM / 2) + L.e) << 7) + (L.sub << 4);
   uint8_t* own = (KIND == 0 ? P.stage_x : P.stage_mid) + own_off;
   uint8_t* own_lo = P.stage_lo + own_off;
   const bool stream = (P.cache & 1) != 0, keep = (P.cache & 2) != 0;
@@ -394,7 +399,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
     for (int cb = 0; cb < kChunks; ++cb) {
       float v[kChunk];
       tmem_ld16(taddr + cb * kChunk, v);
-      const PosEntry* my = tab + L.half * 128 + cb * kChunk + L.e;
+      const PosEntry* my = tab + L.half * (TM / 2) + cb * kChunk + L.e;
 #pragma unroll
       for (int m = 0; m < kChunk / 8; ++m) {
         float* x = v + 8 * m;
@@ -411,7 +416,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
   for (int cb = 0; cb < kChunks; ++cb) {
     float v[kChunk];
     tmem_ld16(taddr + cb * kChunk, v);
-    const PosEntry* my = tab + L.half * 128 + cb * kChunk + L.e;
+    const PosEntry* my = tab + L.half * (TM / 2) + cb * kChunk + L.e;
 #pragma unroll
     for (int m = 0; m < kChunk / 8; ++m) {
       float* x = v + 8 * m;
@@ -487,7 +492,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
 }
 
 // --------------------------------------------------------------- kernel
-template <bool DBG>
+template <int TM, bool DBG>
 __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__ StepParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
@@ -598,11 +603,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         for (int p = 0; p < n_phases(it.kind); ++p) {
           if (p == 0 || p == 2) {  // conv3x3 #2 waits for the mid tiles only before its W2 phase
             if (DBG) c0 = clock64();
-            step_wait_deps(P, it, p);
+            step_wait_deps<TM>(P, it, p);
             if (DBG) w_dep += clock64() - c0;
           }
           const Phase ph = phase_of(P, it, p);
-          const uint32_t rows = kTileM + 2 * ph.halo;
+          const uint32_t rows = TM + 2 * ph.halo;
           const uint8_t* src = ph.src + (static_cast<int64_t>(kGuard + it.q0 - ph.halo) << 7);
           for (int ch = 0; ch < ph.chunks; ++ch, ++ai) {
             const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------------------------------- MMA issuer
-      constexpr uint32_t IDESC = idesc_f16_f32(128, kTileM);
+      constexpr uint32_t IDESC = idesc_f16_f32(128, TM);
       long long w_acc = 0, w_a = 0, w_b = 0;
       const long long t_start = clock64();
       const uint64_t ns_start = DBG ? global_ns() : 0;
@@ -669,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
               for (int kk = 0; kk < 4; ++kk) {
                 const uint64_t wd = smem_desc_sw128(b_base + s * kBStage + kk * 32);
                 const uint64_t xd = smem_desc_sw128(a_slot + xrow * 128 + kk * 32);
-                mma_bf16(tmem_base + abuf * kTileM, wd, xd, IDESC, acc);
+                mma_bf16(tmem_base + abuf * TM, wd, xd, IDESC, acc);
                 acc = 1;
               }
               if (kCluster == 1) mma_commit(b_empty + s);
@@ -732,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       if (it.kind < 0) break;
       const int buf = n & 1;
       mbar_wait(tab_empty + buf, ((n >> 1) & 1) ^ 1);
-      rb_fill_table(P, it, tables + buf * kTileM, lane);
+      rb_fill_table<TM>(P, it, tables + buf * TM, lane);
       mbar_arrive(tab_full + buf);  // release: the entries are visible to the waiters
     }
   } else {  // ------------------------------------------------------ epilogue
@@ -744,7 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
     L.chunk_off = static_cast<int64_t>(L.plane >> 3) * P.ps * 128;
     L.sub = (L.plane & 7) ^ L.e;
     L.plane_off32 = L.plane * kPx * 8;
-    const uint32_t lane_addr = (static_cast<uint32_t>(L.quarter * 32) << 16) + L.half * 128;
+    const uint32_t lane_addr = (static_cast<uint32_t>(L.quarter * 32) << 16) + L.half * (TM / 2);
     for (int n = 0;; ++n) {
       const int slot = n % kItemSlots;
       mbar_wait(item_full + slot, (n / kItemSlots) & 1);
@@ -753,18 +758,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       if (lane == 0) mbar_arrive(item_empty + slot);
       if (it.kind < 0) break;
       const int abuf = n & 1;
-      const PosEntry* tab = tables + abuf * kTileM;
+      const PosEntry* tab = tables + abuf * TM;
       mbar_wait(tab_full + abuf, (n >> 1) & 1);
       mbar_wait(acc_full + abuf, (n >> 1) & 1);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + abuf * kTileM + lane_addr;
+      const uint32_t taddr = tmem_base + abuf * TM + lane_addr;
       if (P.diag & 4) {
       } else if (it.kind == 0) {
-        step_epilogue<0>(P, tab, L, taddr, it);
+        step_epilogue<0, TM>(P, tab, L, taddr, it);
       } else if (it.kind == 1) {
-        step_epilogue<1>(P, tab, L, taddr, it);
+        step_epilogue<1, TM>(P, tab, L, taddr, it);
       } else {
-        step_epilogue<2>(P, tab, L, taddr, it);
+        step_epilogue<2, TM>(P, tab, L, taddr, it);
         if (P.cache & 4) {
           // the interior mid rows [q0 + 16, q0 + 240) of this tile are read
           // by this tile's conv3x3 #2 only (its neighbours' windows stop 16
@@ -772,8 +777,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           // dirty lines from L2 instead of writing them back; conv3x3 #1
           // rewrites them (pads included) before any later read
           const int et = threadIdx.x - 64;  // 0 .. 255 over the epilogue warps
-          for (int i = et; i < 2 * (kTileM - 2 * kHalo); i += kEpiWarps * 32) {
-            const int c = i / (kTileM - 2 * kHalo), r = kHalo + i % (kTileM - 2 * kHalo);
+          for (int i = et; i < 2 * (TM - 2 * kHalo); i += kEpiWarps * 32) {
+            const int c = i / (TM - 2 * kHalo), r = kHalo + i % (TM - 2 * kHalo);
             discard_l2_line(P.stage_mid + ((static_cast<int64_t>(c) * P.ps + kGuard + it.q0 + r) << 7));
           }
         }
@@ -1150,11 +1155,14 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
                            int64_t plane_stride, const void* const* w0, const void* const* w1,
                            const void* const* w2, const float* const* b0, const float* const* b1,
                            const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
-                           int32_t* step_done, int32_t* queue, int32_t num_sms, void* stream) {
+                           int32_t* step_done, int32_t* queue, int32_t tile_m, int32_t num_sms, void* stream) {
+  if (tile_m != 256 && tile_m != 128) return static_cast<int>(cudaErrorInvalidValue);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_rb_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
-    cudaFuncSetAttribute(k_rb_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     configured = true;
   }
   StepParams p{};
@@ -1211,7 +1219,11 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = p.debug ? cudaLaunchKernelEx(&cfg, k_rb_step<true>, p) : cudaLaunchKernelEx(&cfg, k_rb_step<false>, p);
+  cudaError_t e;
+  if (tile_m == 256)
+    e = p.debug ? cudaLaunchKernelEx(&cfg, k_rb_step<256, true>, p) : cudaLaunchKernelEx(&cfg, k_rb_step<256, false>, p);
+  else
+    e = p.debug ? cudaLaunchKernelEx(&cfg, k_rb_step<128, true>, p) : cudaLaunchKernelEx(&cfg, k_rb_step<128, false>, p);
   return static_cast<int>(e != cudaSuccess ? e : cudaGetLastError());
 }
 
