@@ -128,6 +128,8 @@ int dbk_rb_gather(const void* tasks, const int32_t* n_tasks, int32_t list, int32
  * step_end) must be 0 at launch.
  * D[128 channels][tile_m positions] per tile (tcgen05.mma M = 128, N =
  * tile_m, 256 or 128; the plan must have used the same tile_m). */
+/* Sets the step kernel's attributes; call before capturing a forward. */
+int dbk_rb_configure(void);
 int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* step_tile_begin,
                 const int32_t* tile_group,
                 const int32_t* tile_q0, const int32_t* step_bintile_begin, const int32_t* bin_group,
@@ -154,6 +156,8 @@ int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_
                   const float* inputs, float* values, void* memtab, void* tasks, int32_t* n_tasks,
                   int64_t task_cap, void* stream);
 int dbk_rb_debug(unsigned long long* out24, int32_t reset, int32_t enable);
+/* Whether the wait-counter (debug) step kernel is selected (a launch-time choice). */
+int dbk_rb_debug_enabled(void);
 int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream);
 int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int32_t* fid,
                           const int32_t* arity_of, const int32_t* example, const float* inputs,

@@ -480,12 +480,14 @@ IepSession::IepSession(const FunctionVocab& vocab, std::span<const Program> prog
 void IepSession::set_strategy(Strategy strategy) {
   if (strategy == Strategy::naive)
     throw_error(Errc::invalid_argument, "naive runs one node per step: load it with set_schedule");
+  ++schedule_gen_;
   layout_dirty_ = true;
   host_schedule_ = false;
   strategy_ = strategy;
 }
 
 void IepSession::set_schedule(const Schedule* schedule) {
+  ++schedule_gen_;  // a host schedule's step count and tables are baked into a capture
   layout_dirty_ = true;
   if (schedule) {
     batch_->load_schedule(*schedule, stream_);
@@ -499,6 +501,68 @@ void IepSession::set_schedule(const Schedule* schedule) {
 
 void IepSession::forward() {
   flush_programs();
+  if (graphs_enabled()) {
+    forward_graph();
+    return;
+  }
+  forward_direct();
+}
+
+bool IepSession::graphs_enabled() const {
+  static const bool env_on = [] {
+    const char* e = std::getenv("DYNBATCH_GRAPH");
+    return !e || std::atoi(e) != 0;
+  }();
+  // resblock forwards need no host sync (upper-bound step count), so they
+  // capture; profiled forwards record per-class events and run directly
+  return env_on && kind_ == ModuleKind::resblock && !prof_.on;
+}
+
+void IepSession::forward_graph() {
+  const HostCSR& c = batch_->csr();
+  const GraphKey key{c.b, c.N, rb_ ? rb_->n_shared : 0, c.s_max, static_cast<int>(strategy_),
+                     host_schedule_ ? 1 : 0, rb_ ? rb_->tile_m : 0, batch_->static_shape() ? 1 : 0,
+                     dbk_rb_debug_enabled(), schedule_gen_};
+  ++graph_clock_;
+  for (CachedGraph& g : graphs_) {
+    if (!(g.key == key)) continue;
+    batch_->set_sched_state(g.sched);
+    launches_ = g.launches;
+    g.used = graph_clock_;
+    check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+    return;
+  }
+  // capture this forward (its host bookkeeping runs once, here) and keep it
+  cudaGraph_t graph = nullptr;
+  check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+  try {
+    forward_direct();
+  } catch (...) {
+    cudaStreamEndCapture(stream_, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  check(cudaStreamEndCapture(stream_, &graph), "end capture");
+  CachedGraph g;
+  g.key = key;
+  const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  check(e, "graph instantiate");
+  g.sched = batch_->sched_state();
+  g.launches = launches_;
+  g.used = graph_clock_;
+  constexpr size_t kMaxGraphs = 4;  // e.g. the alternating program sets of a serving loop
+  if (graphs_.size() >= kMaxGraphs) {
+    auto lru = std::min_element(graphs_.begin(), graphs_.end(),
+                                [](const CachedGraph& a, const CachedGraph& b) { return a.used < b.used; });
+    cudaGraphExecDestroy(lru->exec);
+    graphs_.erase(lru);
+  }
+  graphs_.push_back(g);
+  check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+}
+
+void IepSession::forward_direct() {
   launches_ = 0;
   check(cudaMemsetAsync(err_.get(), 0, sizeof(std::int32_t) * 4, stream_), "memset err");
   check(cudaMemsetAsync(present_.get(), 0, present_.size() * sizeof(std::int32_t), stream_), "memset present");

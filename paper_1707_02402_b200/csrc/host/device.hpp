@@ -176,6 +176,21 @@ class DeviceProgramBatch {
 
   void resolve(cudaStream_t s) const;
 
+  // Host bookkeeping a forward leaves behind (step count, pending reads):
+  // restored when a captured forward is replayed.
+  struct SchedState {
+    int steps;
+    std::int64_t groups;
+    bool groups_pending, errors_pending;
+  };
+  SchedState sched_state() const { return {steps, groups, groups_pending_, errors_pending_}; }
+  void set_sched_state(const SchedState& st) const {
+    steps = st.steps;
+    groups = st.groups;
+    groups_pending_ = st.groups_pending;
+    errors_pending_ = st.errors_pending;
+  }
+
   mutable int steps = 0;
   mutable std::int64_t groups = 0;
   Buf<std::int32_t> prog_off, fid, child_off, child_list, child0, child1, example, root_g;
@@ -243,6 +258,27 @@ class IepSession {
   void forward_resblock();
   void check_errors();
   void flush_programs();                       // builds sequences staged by a pipelined set_programs
+  void forward_direct();                       // enqueue one forward launch by launch
+  // CUDA graphs of whole resblock forwards, keyed by what their launches
+  // depend on (sizes, strategy, tile size, kernel variant): a replay costs one
+  // launch instead of ~20 dependent ones.
+  struct GraphKey {
+    std::int64_t b, N, n_shared;
+    int s_max, strategy, host_schedule, tile_m, static_shape, debug;
+    std::uint64_t gen;
+    bool operator==(const GraphKey&) const = default;
+  };
+  struct CachedGraph {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    DeviceProgramBatch::SchedState sched;
+    std::int64_t launches = 0;
+    std::uint64_t used = 0;
+  };
+  std::vector<CachedGraph> graphs_;
+  std::uint64_t graph_clock_ = 0, schedule_gen_ = 0;
+  bool graphs_enabled() const;
+  void forward_graph();
   void programs_built();                       // session state that follows a device prefix build
   void init_resblock(const TensorBatch& inputs, std::uint64_t module_seed);
   void upload_resblock_inputs(const float* chw_rows);

@@ -33,7 +33,7 @@ struct IepSession::RB {
   std::int64_t task_cap = 0;
   Buf<std::int32_t> done0, done1, queue;  // fused step kernel: tile done flags, claim counters
   Buf<std::int32_t> step_done;            // per step: conv3x3 #2 tiles finished (one-launch forwards)
-  std::int32_t epoch = 0;                 // forward counter stamped into the done flags
+  std::int32_t epoch = 1;                 // done-flag stamp (flags are cleared every forward)
   // forward_host_async: copy streams, double-buffered CHW rows, events
   struct Pipe {
     cudaStream_t h2d = nullptr, d2h = nullptr;

@@ -17,6 +17,8 @@ IepSession::~IepSession() {
     cudaStreamSynchronize(stream_);
     cudaStreamDestroy(stream_);
   }
+  for (CachedGraph& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
 }
 
 namespace {
@@ -79,6 +81,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   if (c.max_arity > 2) throw_error(Errc::arity_mismatch, "resblock modules support arity <= 2");
   rb_ = std::make_unique<RB>();
   RB& R = *rb_;
+  check(dbk_rb_configure(), "step kernel attributes");
   for (std::int64_t g = 0; g < c.N; ++g)
     if (c.arity_of[static_cast<size_t>(c.fid[static_cast<size_t>(g)])] > 0) ++R.n_expensive;
   // Tile size: 256 positions, or 128 when a step has too few tiles to fill
@@ -240,7 +243,11 @@ void IepSession::forward_resblock() {
   check(cudaMemsetAsync(R.queue.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_), "queue reset");
   check(cudaMemsetAsync(R.step_done.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_),
         "step counters reset");
-  ++R.epoch;
+  // done flags are cleared every forward (the stamp is a constant), so a
+  // captured forward replays as is
+  check(cudaMemsetAsync(R.done0.get(), 0, sizeof(std::int32_t) * R.done0.size(), stream_), "done flags reset");
+  check(cudaMemsetAsync(R.done1.get(), 0, sizeof(std::int32_t) * R.done1.size(), stream_), "done flags reset");
+  R.epoch = 1;
   // leaf operands of every step in one launch (they only read the inputs)
   prof_.begin(2, stream_);
   check(dbk_rb_gather(R.tasks.get(), R.n_tasks.get(), 0, 0, R.task_cap, R.stage_x.get(), R.stage_lo.get(),

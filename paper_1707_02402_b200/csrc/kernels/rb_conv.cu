@@ -1146,6 +1146,20 @@ extern "C" int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, c
   return static_cast<int>(cudaGetLastError());
 }
 
+// Kernel attributes (shared-memory carve-out), set once per process, and
+// before any stream capture of a forward.
+extern "C" int dbk_rb_configure(void) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_rb_step<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    configured = true;
+  }
+  return static_cast<int>(cudaGetLastError());
+}
+
 extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* step_tile_begin,
                            const int32_t* tile_group,
                            const int32_t* tile_q0, const int32_t* step_bintile_begin, const int32_t* bin_group,
@@ -1157,14 +1171,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
                            const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
                            int32_t* step_done, int32_t* queue, int32_t tile_m, int32_t num_sms, void* stream) {
   if (tile_m != 256 && tile_m != 128) return static_cast<int>(cudaErrorInvalidValue);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_rb_step<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
-    cudaFuncSetAttribute(k_rb_step<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
-    cudaFuncSetAttribute(k_rb_step<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
-    cudaFuncSetAttribute(k_rb_step<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
-    configured = true;
-  }
+  dbk_rb_configure();
   StepParams p{};
   p.step = step;
   p.step_end = step_end;
@@ -1247,6 +1254,8 @@ extern "C" int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int
 
 // Copies (and optionally zeroes) the MMA-thread wait counters; enable != 0
 // turns accounting on for subsequent launches.
+extern "C" int dbk_rb_debug_enabled() { return g_debug_flag; }
+
 extern "C" int dbk_rb_debug(unsigned long long* out, int32_t reset, int32_t enable) {
   g_debug_flag = enable;
   if (out) cudaMemcpyFromSymbol(out, g_conv_dbg, sizeof(unsigned long long) * 24);

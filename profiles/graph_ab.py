@@ -1,0 +1,25 @@
+"""Whole-forward CUDA graphs on / off (DYNBATCH_GRAPH), interleaved, cfg1 and
+cfg3 (device-timed forwards)."""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHILD = r"""
+import sys
+sys.path.insert(0, %r)
+import paper_1707_02402_b200 as db
+F = 128 * 14 * 14
+b = db.Batch.generate("chain", batch=%d, vocab=40, width=F, length=16, branch_prob=%s, seed=0)
+s = db.IepSession(b, 1234, db.MODULE_RESBLOCK)
+s.time(3)
+print(min(s.time(20)[0] / 20 for _ in range(3)))
+"""
+for name, b, bp in (("cfg1", 64, "0.1"), ("cfg3", 4096, "0.3")):
+    res = {"0": [], "1": []}
+    for _ in range(3):
+        for mode in ("0", "1"):
+            env = dict(os.environ, DYNBATCH_GRAPH=mode)
+            out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, b, bp)], env=env, capture_output=True, text=True)
+            res[mode].append(float(out.stdout.strip().splitlines()[-1]))
+    print(f"{name}: direct {min(res['0']):.4f} ms, graph {min(res['1']):.4f} ms")
