@@ -146,7 +146,7 @@ struct StepParams {
   int32_t epoch, lookahead, debug;
   int32_t diag;  // timing diagnostics only (wrong results): bit 0 skips weight reloads, bit 1 window
                  // reloads, bit 2 the epilogue work (TMEM loads, transposes, stores), bit 3 only its stores
-  int32_t cache;  // epilogue store hints: bit 0 streaming for next-launch data, bit 1 evict-last for this launch's
+  int32_t cache;  // bit 2: drop consumed interior mid lines from L2 (discard; default on)
   const int32_t* step_tile_begin;
   const int32_t* tile_group;
   const int32_t* tile_q0;
@@ -387,12 +387,10 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
       L.chunk_off + (static_cast<int64_t>(kGuard + it.q0 + L.half * (TM / 2) + L.e) << 7) + (L.sub << 4);
   uint8_t* own = (KIND == 0 ? P.stage_x : P.stage_mid) + own_off;
   uint8_t* own_lo = P.stage_lo + own_off;
-  const bool stream = (P.cache & 1) != 0, keep = (P.cache & 2) != 0;
   // diag bit 4: every store lands in one L2-resident 16-byte slot per thread
   // (same instructions, no DRAM traffic)
   const bool l2sink = (P.diag & 16) != 0;
   uint8_t* const sink_slot = P.stage_mid + ((static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) << 4);
-  const uint64_t pol = keep ? l2_policy_evict_last() : 0;
   if (P.diag & 8) {  // timing diagnostic: TMEM loads, transposes and math, no stores
     float sink = 0.f;
 #pragma unroll 2
@@ -433,7 +431,6 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
         pk.z = pack_f16x2(o[4], o[5]);
         pk.w = pack_f16x2(o[6], o[7]);
         if (l2sink) st_v4(sink_slot, pk);
-        else if (keep) st_hint_v4(own + off, pk, pol);
         else *reinterpret_cast<uint4*>(own + off) = pk;
       } else if (KIND == 0) {
         uint4 hi, lo;
@@ -441,9 +438,6 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
         if (l2sink) {
           st_v4(sink_slot, hi);
           st_v4(sink_slot, lo);
-        } else if (keep) {
-          st_hint_v4(own + off, hi, pol);
-          st_hint_v4(own_lo + off, lo, pol);
         } else {
           *reinterpret_cast<uint4*>(own + off) = hi;
           *reinterpret_cast<uint4*>(own_lo + off) = lo;
@@ -464,9 +458,6 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
           if (l2sink) {
             st_v4(sink_slot, hi);
             if (pe.fwd_buf == 0) st_v4(sink_slot, lo);
-          } else if (stream) {
-            st_cs_v4(hp, hi);
-            if (pe.fwd_buf == 0) st_cs_v4(P.stage_lo + off, lo);
           } else {
             *reinterpret_cast<uint4*>(hp) = hi;
             if (pe.fwd_buf == 0) *reinterpret_cast<uint4*>(P.stage_lo + off) = lo;
@@ -478,9 +469,6 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
           if (l2sink) {
             st_v4(sink_slot, *reinterpret_cast<const uint4*>(&d0));
             st_v4(sink_slot, *reinterpret_cast<const uint4*>(&d1));
-          } else if (stream) {
-            st_cs_v4(dp, *reinterpret_cast<const uint4*>(&d0));
-            st_cs_v4(dp + 1, *reinterpret_cast<const uint4*>(&d1));
           } else {
             dp[0] = d0;
             dp[1] = d1;

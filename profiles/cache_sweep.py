@@ -1,6 +1,8 @@
 """Step-kernel time and effective SM clock per (DYNBATCH_CACHE,
 DYNBATCH_LOOKAHEAD) setting, interleaved (cfg3). Cache bit 2 drops the
-conv3x3 #2 tiles' interior mid lines from L2 once consumed (no write-back)."""
+conv3x3 #2 tiles' interior mid lines from L2 once consumed (no write-back;
+the default). Bits 0 and 1 selected streaming / evict-last store hints in
+the round they were measured (no effect; since removed)."""
 import os
 import subprocess
 import sys
