@@ -238,7 +238,7 @@ void IepSession::forward_resblock() {
                          R.plane_stride, R.tile_m, stream_),
         "dbk_rb_zero_gaps");
   prof_.end(stream_);
-  launches_ += 6;  // plan, tiles, fwd init, fwd, memtab, zero gaps
+  launches_ += 5;  // plan (+ tile lists), fwd init, fwd, memtab, zero gaps
   const int gather_blocks = sms * 16;  // grid-stride over the step's (member, operand, chunk, pixel) items
   check(cudaMemsetAsync(R.queue.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_), "queue reset");
   check(cudaMemsetAsync(R.step_done.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_),

@@ -797,58 +797,111 @@ constexpr int kStepSmem = kASlots * kASlot + kBStages * kBStage + kTableBytes +
                           kItemSlots * static_cast<int>(sizeof(Item)) + 512;  // + barriers, mailbox, TMEM slot
 
 // ----------------------------------------------------------------- plan
-// Segment layout and tile lists for every step, from the group tables.
-// seg_start[g] is relative to the step's position origin; tiles of step s
-// occupy [step_tile_begin[s], step_tile_begin[s+1]).
-__global__ void k_rb_plan(int32_t n_steps, const int32_t* __restrict__ sgb,
-                          const int32_t* __restrict__ group_fid, const int32_t* __restrict__ group_begin,
-                          const int32_t* __restrict__ arity_of, int32_t* __restrict__ seg_start,
-                          int32_t* __restrict__ group_tile0, int32_t* __restrict__ group_bintile0,
-                          int32_t* __restrict__ step_tile_begin, int32_t* __restrict__ step_bintile_begin,
-                          int32_t* __restrict__ step_positions, int32_t tile_m) {
-  // One thread per step computes its segment starts; tile prefixes over
-  // steps are then accumulated serially (steps are few for improved schedules).
-  for (int32_t s = threadIdx.x; s < n_steps; s += blockDim.x) {
-    int32_t cursor = 0, tiles = 0, bintiles = 0;
-    for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
-      const int32_t rows = group_begin[g + 1] - group_begin[g];
-      if (arity_of[group_fid[g]] == 0 || rows == 0) {
-        seg_start[g] = -1;
-        continue;
+// Segment layout and tile lists for every step, from the group tables, in
+// one block: a warp per step scans its groups 32 at a time (segment starts,
+// first tile, first bin tile), one warp scans the steps (position origins,
+// tile prefixes), then every group's lane writes its tiles' (group, q0).
+// seg_start[g] ends up absolute; tiles of step s occupy
+// [step_tile_begin[s], step_tile_begin[s+1]).
+__device__ __forceinline__ int32_t warp_incl_scan(int32_t x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+__global__ void __launch_bounds__(1024) k_rb_plan(
+    int32_t n_steps, const int32_t* __restrict__ sgb, const int32_t* __restrict__ group_fid,
+    const int32_t* __restrict__ group_begin, const int32_t* __restrict__ arity_of, int32_t* __restrict__ seg_start,
+    int32_t* __restrict__ group_tile0, int32_t* __restrict__ group_bintile0, int32_t* __restrict__ step_tile_begin,
+    int32_t* __restrict__ step_bintile_begin, int32_t* __restrict__ step_positions, int32_t* __restrict__ tile_group,
+    int32_t* __restrict__ tile_q0, int32_t* __restrict__ bin_group, int32_t* __restrict__ bin_q0, int32_t tile_m) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // 1. per step: relative segment starts and tile offsets
+  for (int32_t s = warp; s < n_steps; s += nwarps) {
+    int32_t pos = 0, tiles = 0, bins = 0;
+    for (int32_t g0 = sgb[s]; g0 < sgb[s + 1]; g0 += 32) {
+      const int32_t g = g0 + lane;
+      int32_t nt = 0, bin = 0;
+      bool live = false;
+      if (g < sgb[s + 1]) {
+        const int32_t rows = group_begin[g + 1] - group_begin[g];
+        const int32_t a = arity_of[group_fid[g]];
+        live = a > 0 && rows > 0;
+        if (live) {
+          nt = seg_tiles(rows, tile_m);
+          bin = a == 2 ? nt : 0;
+        } else {
+          seg_start[g] = -1;
+        }
       }
-      const int32_t nt = seg_tiles(rows, tile_m);
-      seg_start[g] = cursor + kLead;  // the first image; its tiles start kLead rows earlier
-      group_tile0[g] = tiles;
-      group_bintile0[g] = arity_of[group_fid[g]] == 2 ? bintiles : -1;
-      cursor += nt * tile_m;
-      tiles += nt;
-      if (arity_of[group_fid[g]] == 2) bintiles += nt;
+      const int32_t it = warp_incl_scan(nt, lane), ib = warp_incl_scan(bin, lane);
+      if (live) {
+        seg_start[g] = pos + (it - nt) * tile_m + kLead;  // the first image; its tiles start kLead rows earlier
+        group_tile0[g] = tiles + it - nt;
+        group_bintile0[g] = bin ? bins + ib - bin : -1;
+      }
+      pos += __shfl_sync(0xffffffffu, it, 31) * tile_m;
+      tiles += __shfl_sync(0xffffffffu, it, 31);
+      bins += __shfl_sync(0xffffffffu, ib, 31);
     }
-    step_positions[s] = cursor;
-    step_tile_begin[s + 1] = tiles;
-    step_bintile_begin[s + 1] = bintiles;
+    if (lane == 0) {
+      step_positions[s] = pos;
+      step_tile_begin[s + 1] = tiles;
+      step_bintile_begin[s + 1] = bins;
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    step_tile_begin[0] = 0;
-    step_bintile_begin[0] = 0;
-    int32_t base = 0;
-    for (int32_t s = 0; s < n_steps; ++s) {
-      step_tile_begin[s + 1] += step_tile_begin[s];
-      step_bintile_begin[s + 1] += step_bintile_begin[s];
-      const int32_t n = step_positions[s];
-      step_positions[s] = base;  // becomes the step's position origin
-      base += n;
+  // 2. prefixes over steps (every step owns its own staging range, so a
+  // result can be written straight into its parent's later operand image)
+  if (warp == 0) {
+    int32_t cp = 0, ct = 0, cb = 0;
+    if (lane == 0) {
+      step_tile_begin[0] = 0;
+      step_bintile_begin[0] = 0;
     }
-    step_positions[n_steps] = base;
+    for (int32_t s0 = 0; s0 < n_steps; s0 += 32) {
+      const int32_t s = s0 + lane;
+      const int32_t p = s < n_steps ? step_positions[s] : 0;
+      const int32_t t = s < n_steps ? step_tile_begin[s + 1] : 0;
+      const int32_t b = s < n_steps ? step_bintile_begin[s + 1] : 0;
+      const int32_t ip = warp_incl_scan(p, lane), itt = warp_incl_scan(t, lane), ib = warp_incl_scan(b, lane);
+      __syncwarp();
+      if (s < n_steps) {
+        step_positions[s] = cp + ip - p;  // the step's position origin
+        step_tile_begin[s + 1] = ct + itt;
+        step_bintile_begin[s + 1] = cb + ib;
+      }
+      cp += __shfl_sync(0xffffffffu, ip, 31);
+      ct += __shfl_sync(0xffffffffu, itt, 31);
+      cb += __shfl_sync(0xffffffffu, ib, 31);
+    }
+    if (lane == 0) step_positions[n_steps] = cp;
   }
   __syncthreads();
-  // Every step owns its own staging range, so a result can be written
-  // straight into the operand image of its parent's (later) step.
-  for (int32_t s = threadIdx.x; s < n_steps; s += blockDim.x) {
-    const int32_t base = step_positions[s];
-    for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g)
-      if (seg_start[g] >= 0) seg_start[g] += base;
+  // 3. absolute segment starts and the tile lists (a warp per step, groups
+  // in turn, the group's tiles across the lanes)
+  for (int32_t s = warp; s < n_steps; s += nwarps) {
+    const int32_t base = step_positions[s], t_base = step_tile_begin[s], b_base = step_bintile_begin[s];
+    for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
+      const int32_t rel = seg_start[g];
+      __syncwarp();
+      if (rel < 0) continue;
+      const int32_t start = rel + base;
+      if (lane == 0) seg_start[g] = start;
+      const int32_t nt = seg_tiles(group_begin[g + 1] - group_begin[g], tile_m);
+      const int32_t t0 = t_base + group_tile0[g], b0 = group_bintile0[g];
+      for (int32_t i = lane; i < nt; i += 32) {
+        tile_group[t0 + i] = g;
+        tile_q0[t0 + i] = start - kLead + i * tile_m;
+        if (b0 >= 0) {
+          bin_group[b_base + b0 + i] = g;
+          bin_q0[b_base + b0 + i] = start - kLead + i * tile_m;
+        }
+      }
+    }
   }
 }
 
@@ -936,33 +989,6 @@ __global__ void k_rb_memtab(int32_t n_steps, const int32_t* __restrict__ sgb,
       const int list = leaf ? 0 : 1;
       const int32_t i = atomicAdd(n_tasks + list, 1);
       if (i < task_cap) tasks[list * task_cap + i] = t;
-    }
-  }
-}
-
-__global__ void k_rb_tiles(int32_t n_steps, const int32_t* __restrict__ sgb,
-                           const int32_t* __restrict__ group_fid, const int32_t* __restrict__ group_begin,
-                           const int32_t* __restrict__ arity_of, const int32_t* __restrict__ seg_start,
-                           const int32_t* __restrict__ group_tile0, const int32_t* __restrict__ group_bintile0,
-                           const int32_t* __restrict__ step_tile_begin,
-                           const int32_t* __restrict__ step_bintile_begin, int32_t* __restrict__ tile_group,
-                           int32_t* __restrict__ tile_q0, int32_t* __restrict__ bin_group,
-                           int32_t* __restrict__ bin_q0, int32_t tile_m) {
-  const int32_t s = blockIdx.x;
-  if (s >= n_steps) return;
-  for (int32_t g = sgb[s]; g < sgb[s + 1]; ++g) {
-    if (seg_start[g] < 0) continue;
-    const int32_t rows = group_begin[g + 1] - group_begin[g];
-    const int32_t nt = seg_tiles(rows, tile_m);
-    for (int32_t i = threadIdx.x; i < nt; i += blockDim.x) {
-      const int32_t ti = step_tile_begin[s] + group_tile0[g] + i;
-      tile_group[ti] = g;
-      tile_q0[ti] = seg_start[g] - kLead + i * tile_m;
-      if (group_bintile0[g] >= 0) {
-        const int32_t bi = step_bintile_begin[s] + group_bintile0[g] + i;
-        bin_group[bi] = g;
-        bin_q0[bi] = seg_start[g] - kLead + i * tile_m;
-      }
     }
   }
 }
@@ -1090,10 +1116,7 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
   if (n_steps <= 0) return 0;
   k_rb_plan<<<1, 1024, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
                                group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
-                               step_positions, tile_m);
-  k_rb_tiles<<<n_steps, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of,
-                                     seg_start, group_tile0, group_bintile0, step_tile_begin,
-                                     step_bintile_begin, tile_group, tile_q0, bin_group, bin_q0, tile_m);
+                               step_positions, tile_group, tile_q0, bin_group, bin_q0, tile_m);
   k_rb_fwd_init<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_nodes, fwd_pos, fwd_slot);
   k_rb_fwd<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
                                    member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot);

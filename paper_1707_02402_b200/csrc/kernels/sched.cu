@@ -11,6 +11,7 @@
 // atomics: every warp owns a 256-node segment, per-(key, segment) counts are
 // exclusive-scanned key-major, and each warp then walks its segment in order
 // assigning ranks with __match_any_sync.
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,7 +33,31 @@ __global__ void k_labels(int64_t b, const int32_t* __restrict__ prog_off,
                          int32_t* __restrict__ scal) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   int local_max = 0;
-  if (e < b) {
+  constexpr int kSmall = 32;  // programs up to this size run in thread-local (L1) arrays
+  if (e < b && prog_off[e + 1] - prog_off[e] <= kSmall) {
+    const int32_t base = prog_off[e], n = prog_off[e + 1] - base;
+    int32_t deg[kSmall], lab[kSmall], q[kSmall];
+    for (int32_t v = 0; v < n; ++v) deg[v] = lab[v] = 0;
+    for (int32_t v = 0; v < n; ++v)
+      for (int32_t c = __ldg(child_off + base + v); c < __ldg(child_off + base + v + 1); ++c)
+        ++deg[__ldg(child_list + c) - base];
+    int32_t head = 0, tail = 0;
+    q[tail++] = __ldg(root_g + e) - base;
+    while (head < tail) {
+      const int32_t v = q[head++];
+      const int32_t next = lab[v] + 1;
+      for (int32_t c = __ldg(child_off + base + v); c < __ldg(child_off + base + v + 1); ++c) {
+        const int32_t u = __ldg(child_list + c) - base;
+        if (lab[u] < next) lab[u] = next;
+        if (--deg[u] == 0) q[tail++] = u;
+      }
+    }
+    if (head != n) atomicOr(&scal[1], 1);
+    for (int32_t v = 0; v < n; ++v) {
+      labels[base + v] = lab[v];
+      local_max = max(local_max, lab[v]);
+    }
+  } else if (e < b) {
     const int32_t base = prog_off[e], end = prog_off[e + 1];
     for (int32_t g = base; g < end; ++g) {
       indeg[g] = 0;
@@ -361,6 +386,7 @@ inline int32_t n_segments(int64_t n, int seg = kSeg) { return static_cast<int32_
 // Generic stable sort segment: short segments (more warps in flight) when
 // the (key, segment) table stays small.
 constexpr int kSegSmall = 64;
+constexpr int64_t kSmallSortItems = 16384;  // scheduler sorts up to this many nodes use kSegSmall
 inline int generic_seg(int32_t n_keys) { return n_keys <= 128 ? kSegSmall : kSeg; }
 
 }  // namespace
@@ -420,11 +446,17 @@ extern "C" int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, con
                                      int32_t* group_begin, int32_t* step_group_begin, int32_t steps_cap,
                                      int32_t ascending, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int32_t nseg = n_segments(N);
+  // short segments for small batches (more warps in flight on a latency-bound
+  // sort); the table stays small either way
+  const int seg = N <= kSmallSortItems ? kSegSmall : kSeg;
+  const int32_t nseg = n_segments(N, seg);
   cudaMemsetAsync(seg_hist, 0, sizeof(int32_t) * static_cast<size_t>(max_keys) * (nseg > 0 ? nseg : 1), s);
   LevelKey key{fid, labels, dev_scalars, p, ascending};
   const int blocks = (nseg + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  if (nseg > 0) k_seg_hist<<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist);
+  if (nseg > 0) {
+    if (seg == kSegSmall) k_seg_hist<LevelKey, kSegSmall><<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist);
+    else k_seg_hist<LevelKey, kSeg><<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist);
+  }
   const int32_t ns = nseg > 0 ? nseg : 1;
   int32_t* totals = seg_hist + static_cast<int64_t>(max_keys) * ns;
   const unsigned sblk = static_cast<unsigned>((static_cast<int64_t>(max_keys) * ns + kScanChunk - 1) / kScanChunk);
@@ -433,7 +465,12 @@ extern "C" int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, con
   k_scan_add<<<sblk, 1024, 0, s>>>(ns, p, dev_scalars, 0, seg_hist, totals);
   k_scan_groups<<<1, 1024, 0, s>>>(N, ns, p, seg_hist, dev_scalars, 0, group_fid,
                                    group_begin, step_group_begin, nullptr, steps_cap);
-  if (nseg > 0) k_seg_scatter<<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist, member_g);
+  if (nseg > 0) {
+    if (seg == kSegSmall)
+      k_seg_scatter<LevelKey, kSegSmall><<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist, member_g);
+    else
+      k_seg_scatter<LevelKey, kSeg><<<blocks, kWarpsPerBlock * 32, 0, s>>>(N, nseg, key, seg_hist, member_g);
+  }
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -465,12 +502,14 @@ extern "C" int dbk_stable_bucket_sort(int64_t n_items, int32_t n_keys, const int
 }
 
 extern "C" int64_t dbk_bucket_sort_scratch(int64_t n_items, int32_t max_keys) {
-  // the larger of the scheduler's table (kSeg segments) and the generic
-  // sort's (generic_seg(max_keys) segments)
-  const int seg = generic_seg(max_keys) < kSeg ? generic_seg(max_keys) : kSeg;
-  const int64_t nseg = n_items > 0 ? (n_items + seg - 1) / seg : 1;
-  const int64_t table = static_cast<int64_t>(max_keys) * nseg;
-  return table + table / kScanChunk + 64;
+  // enough for every segment size a sort of up to n_items may use: the
+  // scheduler's (kSegSmall up to kSmallSortItems nodes, else kSeg) and the
+  // generic sort's (generic_seg(max_keys))
+  auto table = [&](int64_t n, int seg) { return static_cast<int64_t>(max_keys) * (n > 0 ? (n + seg - 1) / seg : 1); };
+  int64_t t = table(n_items, kSeg);
+  t = std::max(t, table(std::min<int64_t>(n_items, kSmallSortItems), kSegSmall));
+  if (generic_seg(max_keys) == kSegSmall) t = std::max(t, table(n_items, kSegSmall));
+  return t + t / kScanChunk + 64;
 }
 
 // ------------------------------------------- program build from prefixes
