@@ -322,7 +322,7 @@ def run_ours(args, dist):
 
     e2e_pass(2, True)  # warm-up: creates the copy streams and double buffers
     dist.barrier()
-    e2e_steps = max(args.steps, 40)  # amortises the pipeline fill and drain
+    e2e_steps = max(args.steps, 80)  # steady state: amortises the pipeline fill and drain
     t0 = time.perf_counter()
     e2e_pass(e2e_steps, True)
     e2e_s = dist.max((time.perf_counter() - t0) / e2e_steps)
