@@ -100,3 +100,31 @@ def test_pipelined_new_programs_every_call():
     fresh.forward()
     from test_device_iep import _flat_from_json
     assert _flat_from_json(s.schedule().to_json()) == _flat_from_json(fresh.schedule().to_json())
+
+
+def test_graph_cache_across_more_program_sets_than_it_holds():
+    """Forwards are replayed from captured graphs, an LRU of 4 per session:
+    cycling through 5 program sets (evictions and re-captures) gives each
+    call exactly a fresh session's outputs, and a strategy change re-captures."""
+    batches = [_batch(20 + i, b=6 + i, length=7 + i % 3) for i in range(5)]
+    seqs = [b.prefix_tokens() for b in batches]
+    s = db.IepSession(batches[0], 8, db.MODULE_RESBLOCK, program_capacity=16, node_capacity=400,
+                      length_capacity=16)
+    want = {}
+    for i, b in enumerate(batches):
+        fresh = db.IepSession(b, 8, db.MODULE_RESBLOCK)
+        x = _rows(6 + i, 30 + i)
+        y = np.zeros_like(x)
+        fresh.forward_host(x, y)
+        want[i] = (x, y)
+    for i in [0, 1, 2, 3, 4, 0, 2, 4, 1, 3, 0]:
+        s.set_programs(*seqs[i])
+        x, y_want = want[i]
+        y = np.zeros_like(x)
+        s.forward_host(x, y)
+        assert np.array_equal(y, y_want), i
+    s.set_strategy("online")  # same programs, another device schedule: outputs unchanged
+    x, y_want = want[0]
+    y = np.zeros_like(x)
+    s.forward_host(x, y)
+    assert np.array_equal(y, y_want)
