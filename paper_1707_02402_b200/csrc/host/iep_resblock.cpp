@@ -88,7 +88,24 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   // the GPU (small batches are latency-bound: twice the tiles, each about
   // 60% as long). DYNBATCH_TILE_M overrides.
   {
-    const double per_step = static_cast<double>(R.n_expensive) / std::max(1, c.s_max);
+    // the step count is d_max + 1 (longest root distance, host Kahn over the
+    // CSR); s_max would undercount balanced trees' steps by far
+    int d_max = 0;
+    std::vector<std::int32_t> lab(static_cast<size_t>(c.N), 0), deg(static_cast<size_t>(c.N), 0), q;
+    for (std::int32_t ch : c.child_list) ++deg[static_cast<size_t>(ch)];
+    for (std::int64_t e = 0; e < c.b; ++e) {
+      q.assign(1, c.root_g[static_cast<size_t>(e)]);
+      for (size_t h = 0; h < q.size(); ++h) {
+        const std::int32_t v = q[h];
+        for (std::int32_t k = c.child_off[static_cast<size_t>(v)]; k < c.child_off[static_cast<size_t>(v) + 1]; ++k) {
+          const std::int32_t u = c.child_list[static_cast<size_t>(k)];
+          lab[static_cast<size_t>(u)] = std::max(lab[static_cast<size_t>(u)], lab[static_cast<size_t>(v)] + 1);
+          if (--deg[static_cast<size_t>(u)] == 0) q.push_back(u);
+        }
+      }
+      for (std::int32_t v : q) d_max = std::max(d_max, lab[static_cast<size_t>(v)]);
+    }
+    const double per_step = static_cast<double>(R.n_expensive) / (d_max + 1);
     const double tiles256 = per_step * 225.0 / RB::kTileM;
     R.tile_m = tiles256 < 2.0 * sm_count() ? 128 : RB::kTileM;
     if (const char* t = std::getenv("DYNBATCH_TILE_M")) {
