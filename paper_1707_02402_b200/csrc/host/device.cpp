@@ -481,14 +481,12 @@ void IepSession::set_strategy(Strategy strategy) {
   if (strategy == Strategy::naive)
     throw_error(Errc::invalid_argument, "naive runs one node per step: load it with set_schedule");
   ++schedule_gen_;
-  layout_dirty_ = true;
   host_schedule_ = false;
   strategy_ = strategy;
 }
 
 void IepSession::set_schedule(const Schedule* schedule) {
   ++schedule_gen_;  // a host schedule's step count and tables are baked into a capture
-  layout_dirty_ = true;
   if (schedule) {
     batch_->load_schedule(*schedule, stream_);
     host_schedule_ = true;

@@ -289,7 +289,6 @@ class IepSession {
   cudaStream_t stream_ = nullptr;
   std::unique_ptr<DeviceProgramBatch> batch_;
   bool host_schedule_ = false;
-  bool layout_dirty_ = true;  // staging pads must be re-zeroed after a schedule change
   Strategy strategy_ = Strategy::improved;
   std::int64_t launches_ = 0;
   Buf<std::int32_t> err_;

@@ -238,7 +238,6 @@ void IepSession::forward_resblock() {
   // Every writer of a staged image writes its pads as zeros and the plan
   // zeroes the segment gaps, so a new layout (host schedule, set_programs)
   // needs no re-zeroing of the staging buffers.
-  layout_dirty_ = false;
   prof_.begin(1, stream_);
   check(dbk_rb_plan(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), B.arity_of.get(),
                     R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(), R.step_tile_begin.get(),
