@@ -102,7 +102,10 @@ def test_moe_ep_layer_world1_equals_session():
     full = db.MoeSession(n, k, T, d, h, seed=seed, precision=db.MOE_BF16)
     full.forward()
     np.testing.assert_array_equal(out, full.run().outputs().astype(np.float32))
-    layer.forward(chunks=3)  # the chunked, overlapped exchange (loopback at world 1)
+    layer.force_exchange = True  # the exchange code paths as loopbacks at world 1
+    layer.forward()
+    np.testing.assert_array_equal(layer.outputs(), out)
+    layer.forward(chunks=3)  # the chunked, overlapped exchange
     np.testing.assert_array_equal(layer.outputs(), out)
 
 
