@@ -462,6 +462,9 @@ def run_moe(args, dist, name, secondary=False):
            "kernels": {name_: {"ms_per_step": kt.ms[c_] / args.steps,
                                "gbs": (kt.bytes[c_] / (kt.ms[c_] / 1e3) / 1e9) if kt.ms[c_] and kt.bytes[c_] else None,
                                "hbm_frac": ((kt.bytes[c_] / (kt.ms[c_] / 1e3) / 1e9) / peaks.get("hbm_gbs", 6450))
+                               if kt.ms[c_] and kt.bytes[c_] else None,
+                               # the north star's reference point: ~8 TB/s nominal HBM3e
+                               "hbm_frac_of_8tbs": ((kt.bytes[c_] / (kt.ms[c_] / 1e3) / 1e9) / 8000.0)
                                if kt.ms[c_] and kt.bytes[c_] else None}
                        for c_, name_ in ((3, "gate+sort+dispatch"), (4, "gemm1_relu"), (5, "gemm2"),
                                          (6, "combine")) if kt.launches[c_]},
