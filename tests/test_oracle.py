@@ -142,3 +142,11 @@ def test_resblock_oracle_properties():
                   bt.child1[bt.prog_off[1]:bt.prog_off[2]].copy(), bt.root[1:2].copy(), 6)
     r1 = O.execute(sub, O.schedule_improved(sub), x[1:2], 3, "resblock", C=8, H=5, W=5)
     assert np.array_equal(r1.outputs[0], r.outputs[1])
+
+
+def test_bench_seed_helper_matches_the_reference_mix_seed():
+    """bench.py derives the module seed with its own mix_seed (no oracle
+    import on the product path); it must equal the reference's."""
+    import bench
+    for seed, stream in ((0, 0xd00d), (7, 0x1127), (123456789, 0xe4be27)):
+        assert bench._mix_seed(seed, stream) == O.mix_seed(seed, stream)
