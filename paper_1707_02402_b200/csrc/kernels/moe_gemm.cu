@@ -123,19 +123,31 @@ __global__ void k_moe_dispatch(int64_t T, int32_t k, int32_t d, const float* __r
     int32_t rows[8];
 #pragma unroll
     for (int s = 0; s < 8; ++s) rows[s] = s < k ? row_of_item[t * k + s] : 0;
-    for (int32_t it = 0; it * 256 < d; ++it) {
-      const int32_t col = it * 256 + lane * 8;
-      const float4 a = __ldg(reinterpret_cast<const float4*>(src + col));
-      const float4 b = __ldg(reinterpret_cast<const float4*>(src + col + 4));
-      uint4 pk;
-      pk.x = pack_bf16x2(a.x, a.y);
-      pk.y = pack_bf16x2(a.z, a.w);
-      pk.z = pack_bf16x2(b.x, b.y);
-      pk.w = pack_bf16x2(b.z, b.w);
-      const int32_t kc = col / kBK, j = (col % kBK) / 8;
+    // four 1 KB rounds of the row in flight before any is written
+    for (int32_t it0 = 0; it0 * 256 < d; it0 += 4) {
+      float4 a[4], b[4];
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
-        if (s < k) *reinterpret_cast<uint4*>(A + a_sw128_off(rows[s], kchunks, kc, j)) = pk;
+      for (int u = 0; u < 4; ++u) {
+        const int32_t col = (it0 + u) * 256 + lane * 8;
+        if (col < d) {
+          a[u] = __ldg(reinterpret_cast<const float4*>(src + col));
+          b[u] = __ldg(reinterpret_cast<const float4*>(src + col + 4));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t col = (it0 + u) * 256 + lane * 8;
+        if (col >= d) break;
+        uint4 pk;
+        pk.x = pack_bf16x2(a[u].x, a[u].y);
+        pk.y = pack_bf16x2(a[u].z, a[u].w);
+        pk.z = pack_bf16x2(b[u].x, b[u].y);
+        pk.w = pack_bf16x2(b[u].z, b[u].w);
+        const int32_t kc = col / kBK, j = (col % kBK) / 8;
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s < k) *reinterpret_cast<uint4*>(A + a_sw128_off(rows[s], kchunks, kc, j)) = pk;
+      }
     }
   }
 }
