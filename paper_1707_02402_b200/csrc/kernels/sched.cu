@@ -257,6 +257,33 @@ __global__ void __launch_bounds__(1024) k_scan_partial(int32_t nseg, int32_t p, 
   if (threadIdx.x == 0) totals[blockIdx.x] = total;
 }
 
+// Small tables: the whole exclusive scan in one block, 4096 entries per
+// round with a carry (replaces the three-kernel scan).
+constexpr int64_t kSmallScan = 65536;
+__global__ void __launch_bounds__(1024) k_scan_single(int32_t nseg, int32_t p, const int32_t* __restrict__ scal,
+                                                      int32_t fixed_keys, int32_t* __restrict__ hist) {
+  __shared__ int32_t sh[32];
+  const int64_t len = table_len(nseg, p, scal, fixed_keys);
+  int32_t carry = 0;
+  for (int64_t base = 0; base < len; base += kScanChunk) {
+    int32_t v[4], sum = 0;
+    const int64_t i0 = base + threadIdx.x * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[j] = i0 + j < len ? hist[i0 + j] : 0;
+      sum += v[j];
+    }
+    int32_t total;
+    int32_t run = carry + block_scan_excl(sum, &total, sh);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (i0 + j < len) hist[i0 + j] = run;
+      run += v[j];
+    }
+    carry += total;
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_scan_totals(int32_t nseg, int32_t p, const int32_t* __restrict__ scal,
                                                       int32_t fixed_keys, int32_t* __restrict__ totals) {
   __shared__ int32_t sh[32];
@@ -460,9 +487,13 @@ extern "C" int dbk_sched_bucket_sort(int64_t N, int32_t p, int32_t max_keys, con
   const int32_t ns = nseg > 0 ? nseg : 1;
   int32_t* totals = seg_hist + static_cast<int64_t>(max_keys) * ns;
   const unsigned sblk = static_cast<unsigned>((static_cast<int64_t>(max_keys) * ns + kScanChunk - 1) / kScanChunk);
-  k_scan_partial<<<sblk, 1024, 0, s>>>(ns, p, dev_scalars, 0, seg_hist, totals);
-  k_scan_totals<<<1, 1024, 0, s>>>(ns, p, dev_scalars, 0, totals);
-  k_scan_add<<<sblk, 1024, 0, s>>>(ns, p, dev_scalars, 0, seg_hist, totals);
+  if (static_cast<int64_t>(max_keys) * ns <= kSmallScan) {
+    k_scan_single<<<1, 1024, 0, s>>>(ns, p, dev_scalars, 0, seg_hist);
+  } else {
+    k_scan_partial<<<sblk, 1024, 0, s>>>(ns, p, dev_scalars, 0, seg_hist, totals);
+    k_scan_totals<<<1, 1024, 0, s>>>(ns, p, dev_scalars, 0, totals);
+    k_scan_add<<<sblk, 1024, 0, s>>>(ns, p, dev_scalars, 0, seg_hist, totals);
+  }
   k_scan_groups<<<1, 1024, 0, s>>>(N, ns, p, seg_hist, dev_scalars, 0, group_fid,
                                    group_begin, step_group_begin, nullptr, steps_cap);
   if (nseg > 0) {
@@ -489,9 +520,13 @@ extern "C" int dbk_stable_bucket_sort(int64_t n_items, int32_t n_keys, const int
     k_seg_hist<ExplicitKey, kSeg><<<blocks, kWarpsPerBlock * 32, 0, s>>>(n_items, nseg, key, seg_hist);
   int32_t* totals = seg_hist + static_cast<int64_t>(n_keys) * nseg;
   const unsigned sblk = static_cast<unsigned>((static_cast<int64_t>(n_keys) * nseg + kScanChunk - 1) / kScanChunk);
-  k_scan_partial<<<sblk, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, seg_hist, totals);
-  k_scan_totals<<<1, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, totals);
-  k_scan_add<<<sblk, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, seg_hist, totals);
+  if (static_cast<int64_t>(n_keys) * nseg <= kSmallScan) {
+    k_scan_single<<<1, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, seg_hist);
+  } else {
+    k_scan_partial<<<sblk, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, seg_hist, totals);
+    k_scan_totals<<<1, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, totals);
+    k_scan_add<<<sblk, 1024, 0, s>>>(nseg, 1, nullptr, n_keys, seg_hist, totals);
+  }
   k_scan_groups<<<1, 1024, 0, s>>>(n_items, nseg, 1, seg_hist, nullptr, n_keys, nullptr, nullptr,
                                    nullptr, offsets);
   if (seg == kSegSmall)
