@@ -933,20 +933,20 @@ __global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const
                          const int32_t* __restrict__ child0, const int32_t* __restrict__ child1,
                          const int32_t* __restrict__ fwd_ok, int32_t* __restrict__ fwd_pos,
                          int32_t* __restrict__ fwd_slot) {
-  const int32_t g0 = sgb[0], g1 = sgb[n_steps];
-  const int32_t m0 = group_begin[g0], m1 = group_begin[g1];
-  for (int32_t m = m0 + blockIdx.x * blockDim.x + threadIdx.x; m < m1; m += gridDim.x * blockDim.x) {
-    const int32_t g = last_le(group_begin, g0, g1 - 1, m);
+  // a block per group (no per-member search), threads over its members
+  for (int32_t g = sgb[0] + blockIdx.x; g < sgb[n_steps]; g += gridDim.x) {
     if (seg_start[g] < 0) continue;
     const int32_t arity = arity_of[group_fid[g]];
-    const int32_t node = member_g[m];
-    for (int k = 0; k < arity; ++k) {
-      const int32_t c = k == 0 ? child0[node] : child1[node];
-      if (!fwd_ok[c]) continue;
-      fwd_pos[c] = seg_start[g] + (m - group_begin[g]) * kImg;
-      // buffer (bit 0: stage_x / stage_cat) and first plane; no fp32 copy:
-      // a unary parent reads its residual from the hi/lo images
-      fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1);
+    for (int32_t m = group_begin[g] + threadIdx.x; m < group_begin[g + 1]; m += blockDim.x) {
+      const int32_t node = member_g[m];
+      for (int k = 0; k < arity; ++k) {
+        const int32_t c = k == 0 ? child0[node] : child1[node];
+        if (!fwd_ok[c]) continue;
+        fwd_pos[c] = seg_start[g] + (m - group_begin[g]) * kImg;
+        // buffer (bit 0: stage_x / stage_cat) and first plane; no fp32 copy:
+        // a unary parent reads its residual from the hi/lo images
+        fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1);
+      }
     }
   }
 }
@@ -960,35 +960,36 @@ __global__ void k_rb_memtab(int32_t n_steps, const int32_t* __restrict__ sgb,
                             const int32_t* __restrict__ example, const int32_t* __restrict__ fwd_ok,
                             const float* inputs, float* values, MemberEntry* __restrict__ memtab,
                             GatherTask* __restrict__ tasks, int32_t* __restrict__ n_tasks, int64_t task_cap) {
-  const int32_t g0 = sgb[0], g1 = sgb[n_steps];
-  const int32_t m0 = group_begin[g0], m1 = group_begin[g1];
-  for (int32_t m = m0 + blockIdx.x * blockDim.x + threadIdx.x; m < m1; m += gridDim.x * blockDim.x) {
-    const int32_t g = last_le(group_begin, g0, g1 - 1, m);
+  // a block per group (no per-member search), threads over its members
+  for (int32_t g = sgb[0] + blockIdx.x; g < sgb[n_steps]; g += gridDim.x) {
     if (seg_start[g] < 0) continue;
     const int32_t arity = arity_of[group_fid[g]];
-    const int32_t node = member_g[m];
-    const int32_t sw = fwd_slot[node];
-    const int32_t tgt = fwd_pos[node];
-    MemberEntry e{};
-    e.slot = values + static_cast<int64_t>(node) * kFmap;
-    e.keep32 = (sw >> 8) & 1;
-    e.fwd_row = tgt >= 0 ? kGuard + tgt : -1;
-    e.fwd_buf = (sw & 1) ? 1 + (((sw >> 1) & 31) >> 4) : 0;
-    memtab[m] = e;
-    // operands no child epilogue forwards: leaves (list 0) and children
-    // shared by several parents (list 1), one gather task each
-    for (int k = 0; k < arity; ++k) {
-      const int32_t ch = k == 0 ? child0[node] : child1[node];
-      if (fwd_ok[ch]) continue;
-      const bool leaf = arity_of[fid[ch]] == 0;
-      GatherTask t{};
-      t.src = leaf ? inputs + static_cast<int64_t>(example[ch]) * kFmap : values + static_cast<int64_t>(ch) * kFmap;
-      t.row = kGuard + seg_start[g] + static_cast<int64_t>(m - group_begin[g]) * kImg;
-      t.buf = arity == 2 ? 1 + k : 0;
-      t.step = last_le(sgb, 0, n_steps - 1, g);
-      const int list = leaf ? 0 : 1;
-      const int32_t i = atomicAdd(n_tasks + list, 1);
-      if (i < task_cap) tasks[list * task_cap + i] = t;
+    const int32_t g_step = last_le(sgb, 0, n_steps - 1, g);
+    for (int32_t m = group_begin[g] + threadIdx.x; m < group_begin[g + 1]; m += blockDim.x) {
+      const int32_t node = member_g[m];
+      const int32_t sw = fwd_slot[node];
+      const int32_t tgt = fwd_pos[node];
+      MemberEntry e{};
+      e.slot = values + static_cast<int64_t>(node) * kFmap;
+      e.keep32 = (sw >> 8) & 1;
+      e.fwd_row = tgt >= 0 ? kGuard + tgt : -1;
+      e.fwd_buf = (sw & 1) ? 1 + (((sw >> 1) & 31) >> 4) : 0;
+      memtab[m] = e;
+      // operands no child epilogue forwards: leaves (list 0) and children
+      // shared by several parents (list 1), one gather task each
+      for (int k = 0; k < arity; ++k) {
+        const int32_t ch = k == 0 ? child0[node] : child1[node];
+        if (fwd_ok[ch]) continue;
+        const bool leaf = arity_of[fid[ch]] == 0;
+        GatherTask t{};
+        t.src = leaf ? inputs + static_cast<int64_t>(example[ch]) * kFmap : values + static_cast<int64_t>(ch) * kFmap;
+        t.row = kGuard + seg_start[g] + static_cast<int64_t>(m - group_begin[g]) * kImg;
+        t.buf = arity == 2 ? 1 + k : 0;
+        t.step = g_step;
+        const int list = leaf ? 0 : 1;
+        const int32_t i = atomicAdd(n_tasks + list, 1);
+        if (i < task_cap) tasks[list * task_cap + i] = t;
+      }
     }
   }
 }
@@ -1118,7 +1119,7 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
                                group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
                                step_positions, tile_group, tile_q0, bin_group, bin_q0, tile_m);
   k_rb_fwd_init<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_nodes, fwd_pos, fwd_slot);
-  k_rb_fwd<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
+  k_rb_fwd<<<148 * 4, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
                                    member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot);
   return static_cast<int>(cudaGetLastError());
 }
