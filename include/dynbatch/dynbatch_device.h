@@ -112,7 +112,7 @@ DYNBATCH_API db_status db_iep_session_forward_host(db_iep_session* s, const floa
                                                    float* outputs);
 /* Pipelined form of …_forward_host: returns once the call is enqueued. The
  * upload of this call and the download of the previous one overlap the
- * forward (copy streams, double-buffered device rows). The host buffers must
+ * forward (copy streams, triple-buffered device rows). The host buffers must
  * stay valid, and should be pinned, until db_iep_session_synchronize. */
 DYNBATCH_API db_status db_iep_session_forward_host_async(db_iep_session* s, const float* inputs,
                                                          float* outputs);

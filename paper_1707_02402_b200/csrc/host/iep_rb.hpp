@@ -34,17 +34,21 @@ struct IepSession::RB {
   Buf<std::int32_t> done0, done1, queue;  // fused step kernel: tile done flags, claim counters
   Buf<std::int32_t> step_done;            // per step: conv3x3 #2 tiles finished (one-launch forwards)
   std::int32_t epoch = 1;                 // done-flag stamp (flags are cleared every forward)
-  // forward_host_async: copy streams, double-buffered CHW rows, events
+  // forward_host_async: copy streams, triple-buffered CHW rows, events
   struct Pipe {
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    Buf<float> in[2], out[2];
-    cudaEvent_t h2d_done[2] = {}, in_free[2] = {}, out_ready[2] = {}, out_free[2] = {};
+#ifndef DYNBATCH_PIPE_DEPTH
+#define DYNBATCH_PIPE_DEPTH 3
+#endif
+    static constexpr int kDepth = DYNBATCH_PIPE_DEPTH;  // calls in flight (slack for host and link jitter)
+    Buf<float> in[kDepth], out[kDepth];
+    cudaEvent_t h2d_done[kDepth] = {}, in_free[kDepth] = {}, out_ready[kDepth] = {}, out_free[kDepth] = {};
     std::uint64_t calls = 0;
     // set_programs while pipelined: the sequences wait in pinned staging
-    // slot (calls & 1) and ride the next call's input upload on the h2d
+    // slot (calls % kDepth) and ride the next call's input upload on the h2d
     // stream; the build runs on the main stream after that upload
-    Pinned<std::int32_t> tok_pin[2], off_pin[2];
-    Buf<std::int32_t> tok[2], off[2];
+    Pinned<std::int32_t> tok_pin[kDepth], off_pin[kDepth];
+    Buf<std::int32_t> tok[kDepth], off[kDepth];
     bool programs_pending = false;
     // DYNBATCH_PIPE_TRACE: timing events per call (h2d start/end, main
     // start/forward end, d2h start/end), printed by sync_pipeline()
@@ -53,7 +57,7 @@ struct IepSession::RB {
     ~Pipe() {
       if (h2d) cudaStreamSynchronize(h2d);
       if (d2h) cudaStreamSynchronize(d2h);
-      for (int k = 0; k < 2; ++k)
+      for (int k = 0; k < kDepth; ++k)
         for (cudaEvent_t e : {h2d_done[k], in_free[k], out_ready[k], out_free[k]})
           if (e) cudaEventDestroy(e);
       if (h2d) cudaStreamDestroy(h2d);

@@ -338,7 +338,7 @@ void IepSession::set_programs(const std::int32_t* tokens, const std::int32_t* se
     // forward_host_async uploads them with its inputs (one copy queue, no
     // small copy stuck behind a large one) and builds on the main stream
     RB::Pipe& Q = *R.pipe;
-    const int k = static_cast<int>(Q.calls & 1);
+    const int k = static_cast<int>(Q.calls % RB::Pipe::kDepth);
     const std::int64_t N = B.begin_prefix_programs(seq_off, b);
     check(cudaEventSynchronize(Q.h2d_done[k]), "staging slot");  // the slot's last upload has finished
     Q.tok_pin[k].ensure(static_cast<size_t>(B.csr().cap_N));
@@ -374,7 +374,7 @@ void IepSession::flush_programs() {
   if (!rb_ || !rb_->pipe || !rb_->pipe->programs_pending) return;
   RB::Pipe& Q = *rb_->pipe;
   DeviceProgramBatch& B = *batch_;
-  const int k = static_cast<int>(Q.calls & 1);
+  const int k = static_cast<int>(Q.calls % RB::Pipe::kDepth);
   Q.tok[k].ensure(static_cast<size_t>(B.csr().cap_N));
   Q.off[k].ensure(static_cast<size_t>(B.csr().cap_b) + 1);
   check(cudaMemcpyAsync(Q.tok[k].get(), Q.tok_pin[k].get(), sizeof(std::int32_t) * static_cast<size_t>(B.csr().N),
@@ -431,7 +431,7 @@ void IepSession::sync_pipeline() {
 }
 
 // Pipelined end-to-end call: the H2D of this call's inputs and the D2H of
-// its outputs run on their own streams into double-buffered device rows, so
+// its outputs run on their own streams into triple-buffered device rows, so
 // consecutive calls overlap upload(N+1) and download(N−1) with forward(N)
 // (PCIe is full duplex). Ordering is by events only; synchronize() waits for
 // everything. Host buffers must stay valid (and should be pinned) until then.
@@ -447,7 +447,7 @@ void IepSession::forward_host_async(const float* inputs, float* outputs) {
     check(cudaStreamCreateWithFlags(&Q.h2d, cudaStreamNonBlocking), "stream");
     check(cudaStreamCreateWithFlags(&Q.d2h, cudaStreamNonBlocking), "stream");
     const size_t rows = static_cast<size_t>(std::max<std::int64_t>(B.csr().cap_b, b));
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < RB::Pipe::kDepth; ++k) {
       Q.in[k].alloc(rows * RB::kFmap);
       Q.out[k].alloc(rows * RB::kFmap);
       for (cudaEvent_t* e : {&Q.h2d_done[k], &Q.in_free[k], &Q.out_ready[k], &Q.out_free[k]}) {
@@ -457,7 +457,7 @@ void IepSession::forward_host_async(const float* inputs, float* outputs) {
     }
   }
   RB::Pipe& Q = *R.pipe;
-  const int k = static_cast<int>(Q.calls++ & 1);
+  const int k = static_cast<int>(Q.calls++ % RB::Pipe::kDepth);
   std::array<cudaEvent_t, 6> te{};
   if (Q.trace || std::getenv("DYNBATCH_PIPE_TRACE")) {
     Q.trace = true;
