@@ -201,6 +201,9 @@ DYNBATCH_API db_status db_moe_ep_experts(db_moe_ep_session* s, const void* recv_
  * e_end) as their rows arrive (recv_rows / ret_rows as for _experts; each
  * call reads and writes only its experts' rows). */
 DYNBATCH_API db_status db_moe_ep_layout(db_moe_ep_session* s, const int32_t* recv_counts);
+/* World 1 only: the whole layer in one device pass (gate, sort, dispatch,
+ * grouped GEMMs, combine), no exchange buffers. */
+DYNBATCH_API db_status db_moe_ep_forward_local(db_moe_ep_session* s);
 DYNBATCH_API db_status db_moe_ep_experts_range(db_moe_ep_session* s, const void* recv_rows, void* ret_rows,
                                                int32_t e_begin, int32_t e_end);
 DYNBATCH_API db_status db_moe_ep_combine(db_moe_ep_session* s, const void* ret_rows);

@@ -170,6 +170,7 @@ SIGNATURES = {
     "db_moe_ep_dispatch": (C.c_int32, [VP, VP, VP]),
     "db_moe_ep_experts": (C.c_int32, [VP, VP, VP, VP]),
     "db_moe_ep_layout": (C.c_int32, [VP, VP]),
+    "db_moe_ep_forward_local": (C.c_int32, [VP]),
     "db_moe_ep_experts_range": (C.c_int32, [VP, VP, VP, C.c_int32, C.c_int32]),
     "db_moe_ep_combine": (C.c_int32, [VP, VP]),
     "db_moe_ep_outputs": (C.c_int32, [VP, VP]),
@@ -557,6 +558,10 @@ class MoeEpSession(_Handle):
     def experts(self, recv_ptr: int, recv_counts: np.ndarray, ret_ptr: int):
         cnt = np.ascontiguousarray(recv_counts, np.int32).reshape(self.world, self.local_experts)
         check(lib().db_moe_ep_experts(self.h, C.c_void_p(recv_ptr), _ptr(cnt), C.c_void_p(ret_ptr)))
+
+    def forward_local(self):
+        """World 1: the whole layer in one device pass (no exchange)."""
+        check(lib().db_moe_ep_forward_local(self.h))
 
     def layout(self, recv_counts: np.ndarray):
         """Receive-side layout for the chunked form of experts()."""

@@ -635,6 +635,11 @@ db_status db_moe_ep_experts(db_moe_ep_session* s, const void* recv_rows, const i
   return guarded([&] { s->s->experts(recv_rows, recv_counts, ret_rows); });
 }
 
+db_status db_moe_ep_forward_local(db_moe_ep_session* s) {
+  if (!s) return null_arg();
+  return guarded([&] { s->s->forward_local(); });
+}
+
 db_status db_moe_ep_layout(db_moe_ep_session* s, const int32_t* recv_counts) {
   if (!s || !recv_counts) return null_arg();
   return guarded([&] { s->s->layout(recv_counts); });

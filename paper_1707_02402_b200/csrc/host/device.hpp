@@ -356,6 +356,8 @@ class MoeEp {
   // then experts_range for contiguous local-expert ranges, each as soon as
   // its rows have arrived (rows of other experts may still be in flight).
   void layout(const std::int32_t* cnt);
+  // World 1: the whole layer in one device pass (no exchange, no pack).
+  void forward_local();
   void experts_range(const void* recv, void* ret, int e_begin, int e_end);
   // ret_recv = the rank's own rows back, in its sorted order → outputs.
   void combine(const void* ret_recv);

@@ -298,7 +298,7 @@ struct MoeEp::Impl {
   Buf<float> x, out;
   Buf<std::int32_t> pos_of_item, cnt, pstart, tile_expert, tile_rb, n_tiles, src_row, cum, recv_of_row;
   Buf<std::uint8_t> A, H;
-  Buf<std::uint16_t> w1, w2;
+  Buf<std::uint16_t> w1, w2, Y;  // Y: GEMM2 rows of the world-1 pass
   Buf<const void*> w1tab, w2tab;
   std::int64_t cap_rows = 0;  // padded-row capacity of A / H
   std::vector<std::int32_t> cnt_h;    // last layout's counts [G][E]
@@ -377,6 +377,37 @@ void MoeEp::dispatch(void* send, std::int32_t* expert_counts) {
   prof_.end(stream_);
   const auto off = D.offsets.download(static_cast<size_t>(D.n) + 1, stream_);  // synchronises
   for (int e = 0; e < D.n; ++e) expert_counts[e] = off[static_cast<size_t>(e) + 1] - off[static_cast<size_t>(e)];
+}
+
+// World 1: no exchange, so the layer runs as one device pass — gate, sort,
+// token-major dispatch straight into the tiled operand, the two grouped
+// GEMMs, slot-order combine (the single-GPU bf16 layer's kernels, on this
+// session's experts).
+void MoeEp::forward_local() {
+  Impl& I = *impl_;
+  MoeDev& D = I.dev;
+  if (I.world != 1) throw_error(Errc::invalid_argument, "forward_local needs world 1");
+  const int d = static_cast<int>(I.cfg.data_dim), h = static_cast<int>(I.cfg.hidden);
+  prof_.begin(3, stream_);
+  D.gate(stream_);
+  D.sort(stream_);
+  check(dbk_moe_bf16_layout(D.n, D.offsets.get(), I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(),
+                            I.n_tiles.get(), stream_), "moe layout");
+  check(dbk_moe_bf16_dispatch(T_, D.k, d, D.order.get(), D.ids.get(), D.offsets.get(), I.pstart.get(), I.x.get(),
+                              I.A.get(), I.pos_of_item.get(), I.sms * 8, stream_),
+        "moe dispatch");  // pos_of_item holds each item's padded row here
+  prof_.end(stream_);
+  if (I.Y.size() < static_cast<size_t>(I.cap_rows) * d) I.Y.alloc(static_cast<size_t>(I.cap_rows) * d);
+  prof_.begin(4, stream_);
+  check(dbk_moe_bf16_gemm(0, D.n, d, h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
+                          I.w1tab.get(), I.H.get(), nullptr, 0, -1, nullptr, I.sms, stream_), "moe gemm1");
+  check(dbk_moe_bf16_gemm(1, D.n, h, d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
+                          I.w2tab.get(), nullptr, I.Y.get(), 0, -1, nullptr, I.sms, stream_), "moe gemm2");
+  prof_.end(stream_);
+  prof_.begin(6, stream_);
+  check(dbk_moe_bf16_combine(T_, D.k, d, D.wts.get(), I.pos_of_item.get(), I.Y.get(), I.out.get(), stream_),
+        "moe combine");
+  prof_.end(stream_);
 }
 
 void MoeEp::layout(const std::int32_t* cnt) {

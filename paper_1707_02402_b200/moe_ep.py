@@ -201,12 +201,8 @@ class MoeEpLayer:
         self.last_recv_rows = rows
 
     def _forward_local(self):
-        """World 1: both exchanges are the identity, so the experts read the
-        send buffer in place and the combine reads their outputs in place
-        (receive order = send order); no copies."""
-        counts = self.sess.dispatch(self.send.data_ptr())
-        rows = int(np.sum(counts))
-        self._ensure(rows)
-        self.sess.experts(self.send.data_ptr(), np.asarray(counts, np.int32).reshape(1, -1), self.ret.data_ptr())
-        self.sess.combine(self.ret.data_ptr())
-        self.last_recv_rows = rows
+        """World 1: both exchanges are the identity, so the layer runs as one
+        device pass — the dispatch writes the tiled GEMM operand directly
+        and the combine reads the GEMM rows (no pack, scatter or copies)."""
+        self.sess.forward_local()
+        self.last_recv_rows = self.sess.items
