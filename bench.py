@@ -527,7 +527,9 @@ def run_moe_ep(args, dist, name):
             "ms_per_step": ms_step, "dtype": "bf16 tensor-core operands, fp32 accumulate",
             "config": {"workload": f"{name}: n={c['experts']} top-{c['k']} d={c['d']} h={c['h']}, "
                                    f"{c['tokens_per_gpu']} tokens/GPU, experts {c['experts'] // N}/GPU",
-                       "global_tokens": T, "parallelism": f"ep{N} (NCCL all-to-all dispatch + combine)",
+                       "global_tokens": T,
+                       "parallelism": (f"ep{N} (NCCL point-to-point exchange by expert range, overlapped with the "
+                                       "GEMMs)") if N > 1 else "ep1 (no exchange: one device pass)",
                        "exchange_chunks": chunks},
             "roofline": {"kernel": "whole EP layer (gate, sort, pack, 2x all-to-all, grouped GEMMs, combine)",
                          "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
