@@ -162,3 +162,24 @@ def test_cfg3_full_size_properties():
                   ob.root[r:r + 1], ob.p)
     ref = O.execute(obs, O.schedule_improved(obs), x, 1234, "resblock").outputs
     _check(full[r:r + 1], ref)
+
+
+@pytest.mark.parametrize("depth", [4, 8])
+def test_cfg2_full_size_properties(depth):
+    """BASELINE configs[1] at full size (512 balanced trees, the static
+    per-shape schedule): the device schedule equals the oracle's
+    schedule_improved, outputs are finite, and rows run alone reproduce
+    their in-batch outputs bit for bit."""
+    b = db.Batch.generate("balanced", batch=512, vocab=40, width=F, depth=depth, seed=0)
+    sess = db.IepSession(b, 77, db.MODULE_RESBLOCK)
+    sess.forward()
+    sess.synchronize()
+    ob = O.gen_batch("balanced", 512, p=40, depth=depth, length=16, bp=0.1, seed=0)
+    from test_device_iep import _flat_from_json
+    assert _flat_from_json(sess.schedule().to_json()) == O.schedule_improved(ob)
+    full = sess.run().outputs()
+    assert np.isfinite(full).all()
+    for r in (0, 511):
+        one = db.IepSession(b, 77, db.MODULE_RESBLOCK, first=r, last=r + 1)
+        one.forward()
+        assert np.array_equal(one.run().outputs()[0], full[r])
