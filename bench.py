@@ -2,13 +2,18 @@
 """Benchmark of the dynamic-batching executor hot path (one JSON line).
 
 Default workload (BASELINE.json configs[2], "cfg3"): IEP execution-engine
-forward over b = 4096 chain-heavy programs per GPU (p = 40, length ≤ 16,
-branch 0.3, seed 0), residual conv3x3/conv1x1 + ReLU module bodies on
+forward over a minibatch of b = 4096 chain-heavy programs (p = 40, length ≤
+16, branch 0.3, seed 0), residual conv3x3/conv1x1 + ReLU module bodies on
 128×14×14 feature maps, random-init weights (module_seed = mix_seed(0,
 0xd00d)). One step = device scheduler (labels + stable (level, function)
-bucket sort) + every per-step gather / tcgen05 conv / scatter launch. Under
-torchrun each rank owns a contiguous 4096-program shard of a global batch of
-4096·N programs (weak scaling, no data-path collective).
+bucket sort) + every per-step gather / tcgen05 conv / scatter launch.
+
+Multi-GPU (--gpus N): one process per GPU. Without torchrun's WORLD_SIZE the
+script re-launches itself under `torch.distributed.run` with N ranks. Strong
+scaling by default, as BASELINE quotes it: the minibatch (cfg3: 4096
+programs; cfg5: 1,048,576 tokens) is split into contiguous shards
+[r·b/N, (r+1)·b/N), one per rank, with no data-path collective for the IEP
+(programs are independent). --scaling weak keeps the per-GPU size fixed.
 
 --impl reference times the reference path on the host cores (the CPU oracle
 port of the same module bodies; the reference has no conv module) and prints
@@ -30,15 +35,26 @@ sys.path.insert(0, ROOT)
 
 METRIC = "IEP exec-engine programs/sec & MoE tokens/sec; speedup vs naive and CPU ref"
 F = 128 * 14 * 14
+# batch / tokens: the BASELINE configuration's minibatch (the whole job's
+# under strong scaling, each GPU's under --scaling weak)
 CFG = {
-    "cfg3": dict(kind="chain", per_gpu=4096, vocab=40, length=16, branch_prob=0.3, depth=4),
-    "cfg1": dict(kind="chain", per_gpu=64, vocab=40, length=16, branch_prob=0.1, depth=4),
-    "cfg2": dict(kind="balanced", per_gpu=512, vocab=40, length=16, branch_prob=0.1, depth=6),
+    "cfg3": dict(kind="chain", batch=4096, vocab=40, length=16, branch_prob=0.3, depth=4),
+    "cfg1": dict(kind="chain", batch=64, vocab=40, length=16, branch_prob=0.1, depth=4),
+    "cfg2": dict(kind="balanced", batch=512, vocab=40, length=16, branch_prob=0.1, depth=6),
 }
 MOE = {
-    "cfg4": dict(experts=64, k=2, tokens_per_gpu=65536, d=1024, h=1024),
-    "cfg5": dict(experts=1024, k=4, tokens_per_gpu=131072, d=2048, h=2048),
+    "cfg4": dict(experts=64, k=2, tokens=65536, d=1024, h=1024),
+    "cfg5": dict(experts=1024, k=4, tokens=1048576, d=2048, h=2048),
 }
+
+
+def shard(total, rank, world):
+    """Contiguous shard [first, last) of `total` units owned by `rank`."""
+    return total * rank // world, total * (rank + 1) // world
+
+
+def global_units(total, world, scaling):
+    return total if scaling == "strong" else total * world
 
 
 def parse():
@@ -56,22 +72,46 @@ def parse():
                          "else 4")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the bounded CPU-baseline sample")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the BASELINE minibatch split over the GPUs; weak: that minibatch per GPU")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU work: each rank prints its world size and shard (tests the launch on CPU)")
     return ap.parse_args()
+
+
+def maybe_spawn(args):
+    """--gpus N outside torchrun: re-launch this script with N ranks (one
+    process per GPU) under torch.distributed.run on 127.0.0.1."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 # ----------------------------------------------------------------- dist
 class Dist:
-    def __init__(self, gpus):
+    def __init__(self, gpus, cpu=False):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != gpus:
+            raise SystemExit(f"bench.py: {self.world} ranks for --gpus {gpus}")
         self.pg = None
+        self.cpu = cpu
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if cpu:
+                dist.init_process_group("gloo")
+            else:
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.pg = dist
 
     def barrier(self):
@@ -82,7 +122,7 @@ class Dist:
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([float(x)], device="cuda")
+        t = torch.tensor([float(x)], device="cpu" if self.cpu else "cuda")
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
@@ -252,18 +292,19 @@ def run_ours(args, dist):
     if args.depth:
         cfg["depth"] = args.depth
     N = max(1, dist.world)
-    per = cfg["per_gpu"]
+    B = global_units(cfg["batch"], N, args.scaling)  # programs in the whole job's minibatch
+    first, last = shard(B, dist.rank, N)
+    per = last - first
     db.device_open(dist.local)
     clk = ClockSampler(dist.local).start()
-    first, last = dist.rank * per, (dist.rank + 1) * per
-    batch = db.Batch.generate_range(first, last, cfg["kind"], batch=per * N, vocab=cfg["vocab"],
+    batch = db.Batch.generate_range(first, last, cfg["kind"], batch=B, vocab=cfg["vocab"],
                                     width=F, depth=cfg["depth"], length=cfg["length"],
                                     branch_prob=cfg["branch_prob"], seed=0)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     module_seed = int.from_bytes(_mix_seed(0, 0xd00d).to_bytes(8, "little"), "little")
     # a second batch of programs (the next seed's), for the end-to-end pass
     # where every call brings new programs; the session is sized for both
-    batch2 = db.Batch.generate_range(first, last, cfg["kind"], batch=per * N, vocab=cfg["vocab"],
+    batch2 = db.Batch.generate_range(first, last, cfg["kind"], batch=B, vocab=cfg["vocab"],
                                      width=F, depth=cfg["depth"], length=cfg["length"],
                                      branch_prob=cfg["branch_prob"], seed=1)
     seqs = [batch.prefix_tokens(), batch2.prefix_tokens()]
@@ -280,7 +321,7 @@ def run_ours(args, dist):
     dist.barrier()
     clk.mark(t0, time.time())
     ms_step = dist.max(ms / args.steps)
-    value = per * N / (ms_step / 1e3)
+    value = B / (ms_step / 1e3)
     # second pass with events around every launch: per-kernel-class times
     # for the roofline and the breakdown (not the headline)
     pms, kt = sess.time(args.steps, profile=True)
@@ -331,13 +372,13 @@ def run_ours(args, dist):
     t0 = time.perf_counter()
     e2e_pass(e2e_steps, False)
     fixed_s = dist.max((time.perf_counter() - t0) / e2e_steps)
-    e2e = {"value": per * N / e2e_s, "unit": "programs/s",
+    e2e = {"value": B / e2e_s, "unit": "programs/s",
            "h2d_bytes_per_step": int(per * F * 4 + prog_bytes), "d2h_bytes_per_step": per * F * 4,
            "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
            "api": "db_iep_session_set_programs (new prefix sequences every call, CSR built on the device) + "
                   "db_iep_session_forward_host_async (pinned fp32 CHW rows in, root rows out; copies overlap "
                   "the neighbouring steps' forwards)",
-           "same_programs_every_call": {"value": per * N / fixed_s, "ms_per_step": fixed_s * 1e3}}
+           "same_programs_every_call": {"value": B / fixed_s, "ms_per_step": fixed_s * 1e3}}
     # the e2e bound: this box's PCIe with both directions busy (pinned
     # 411 MB each way on two streams, as the pipeline runs them)
     link_s = pcie_duplex_seconds(per * F * 4)
@@ -370,14 +411,15 @@ def run_ours(args, dist):
 
     out = {"metric": METRIC, "value": value, "unit": "programs/s", "n_gpus": N,
            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
            "dtype": "fp16 tensor-core operands, fp32 accumulate and node values",
            "data": "synthetic (reference generators, seed 0; random-init weights)",
            "config": {"workload": f"{args.workload}: IEP forward, {cfg['kind']} programs p={cfg['vocab']} "
                                   + (f"depth {cfg['depth']}" if cfg["kind"] == "balanced" else
                                      f"len<={cfg['length']} branch={cfg['branch_prob']}")
-                                  + f", residual conv modules on 128x14x14, {per} programs/GPU",
-                      "global_batch": per * N, "programs_per_gpu": per,
+                                  + f", residual conv modules on 128x14x14, minibatch {B}"
+                                  + (f" ({per} programs on this rank)" if N > 1 else ""),
+                      "global_batch": B, "programs_per_gpu": per,
                       "parallelism": f"dp{N} (program shards, no collective)",
                       "l2": "inputs (411 MB) and node values (4.9 GB) exceed the 126 MB L2"},
            "e2e": e2e, "roofline": roofline, "kernels": kernels,
@@ -393,7 +435,7 @@ def run_ours(args, dist):
     try:
         nb = min(per, 64)
         sub = db.IepSession(batch, module_seed, db.MODULE_RESBLOCK, first=0, last=nb)
-        sub.set_schedule(db.Batch.generate_range(first, first + nb, cfg["kind"], batch=per * N,
+        sub.set_schedule(db.Batch.generate_range(first, first + nb, cfg["kind"], batch=B,
                                                  vocab=cfg["vocab"], width=8, depth=cfg["depth"],
                                                  length=cfg["length"], branch_prob=cfg["branch_prob"],
                                                  seed=0).schedule("naive"))
@@ -432,15 +474,18 @@ def run_ours(args, dist):
 
 def run_moe(args, dist, name, secondary=False):
     """MoE layer forward (gate → stable expert sort → dispatch → grouped
-    tcgen05 GEMM1+ReLU → GEMM2 → slot-order combine), bf16 operands. Token
-    shard per rank (weak scaling); tokens/s."""
+    tcgen05 GEMM1+ReLU → GEMM2 → slot-order combine), fp16 operands (the
+    precise mode: ≤ 1e-3 vs fp64, profiles/r02_moe_parity.json). Token
+    shard per rank; tokens/s."""
     import numpy as np
     import paper_1707_02402_b200 as db
     c = MOE[name]
     N = max(1, dist.world)
-    T = c["tokens_per_gpu"]
-    sess = db.MoeSession(c["experts"], c["k"], T * N, c["d"], c["h"], seed=0, precision=db.MOE_BF16,
-                         first=dist.rank * T, last=(dist.rank + 1) * T)
+    TG = global_units(c["tokens"], N, args.scaling)
+    first, last = shard(TG, dist.rank, N)
+    T = last - first
+    sess = db.MoeSession(c["experts"], c["k"], TG, c["d"], c["h"], seed=0, precision=db.MOE_FP16,
+                         first=first, last=last)
     sess.time(3)
     st = sess.stats()
     dist.barrier()
@@ -451,10 +496,11 @@ def run_moe(args, dist, name, secondary=False):
     peaks, src = measured_peaks()
     g_ms, g_fl = kt.ms[4] + kt.ms[5], kt.flops[4] + kt.flops[5]
     gemm_tf = g_fl / (g_ms / 1e3) / 1e12 if g_ms else 0.0
-    res = {"metric": "MoE tokens/sec", "value": T * N / (ms_step / 1e3), "unit": "tokens/s",
-           "ms_per_step": ms_step, "dtype": "bf16",
+    res = {"metric": "MoE tokens/sec", "value": TG / (ms_step / 1e3), "unit": "tokens/s",
+           "ms_per_step": ms_step, "dtype": "fp16 tensor-core operands (precise mode, <= 1e-3 vs fp64), fp32 accumulate",
            "config": {"workload": f"{name}: n={c['experts']} top-{c['k']} d={c['d']} h={c['h']}, "
-                                  f"{T} tokens/GPU", "global_tokens": T * N},
+                                  f"{TG} tokens" + (f" ({T} on this rank)" if N > 1 else ""),
+                      "global_tokens": TG},
            "roofline": {"kernel": "k_moe_gemm (grouped tcgen05 GEMM1+GEMM2)", "bound": "tensor",
                         "achieved": round(gemm_tf, 1),
                         "peak": peaks.get("bf16_tflops_sustained"), "unit": "TFLOP/s",
@@ -481,7 +527,7 @@ def run_moe(args, dist, name, secondary=False):
     for _ in range(args.steps):
         sess.forward_host(xin.array, sc.array, yout.array)
     e2e_s = dist.max((time.perf_counter() - t0) / args.steps)
-    res["e2e"] = {"value": T * N / e2e_s, "unit": "tokens/s",
+    res["e2e"] = {"value": TG / e2e_s, "unit": "tokens/s",
                   "h2d_bytes_per_step": T * (c["d"] * 4 + c["experts"] * 8),
                   "d2h_bytes_per_step": T * c["d"] * 4}
     return res
@@ -490,8 +536,9 @@ def run_moe(args, dist, name, secondary=False):
 def run_moe_ep(args, dist, name):
     """Expert-parallel MoE layer (cfg5: n=1024 top-4, d=h=2048): tokens
     T/G and experts n/G per rank, NCCL all-to-all of counts and rows for
-    dispatch and combine (paper_1707_02402_b200.moe_ep). Weak scaling:
-    `tokens_per_gpu` per rank, so 8 ranks run the 1M-token configuration."""
+    dispatch and combine (paper_1707_02402_b200.moe_ep). Strong scaling by
+    default: the 1,048,576-token layer split over the ranks (one rank runs
+    all of it)."""
     import torch
     import paper_1707_02402_b200 as db
     from paper_1707_02402_b200.moe_ep import MoeEpLayer
@@ -499,7 +546,7 @@ def run_moe_ep(args, dist, name):
     N = max(1, dist.world)
     db.device_open(dist.local)
     torch.cuda.set_device(dist.local)
-    T = c["tokens_per_gpu"] * N
+    T = global_units(c["tokens"], N, args.scaling)
     layer = MoeEpLayer(c["experts"], c["k"], T, c["d"], c["h"], seed=0)
     chunks = args.ep_chunks or (1 if N == 1 else 4)
     clk = ClockSampler(dist.local).start()
@@ -524,9 +571,9 @@ def run_moe_ep(args, dist, name):
     peak = peaks.get("bf16_tflops_sustained")
     rows = dist.max(layer.last_recv_rows)
     return {"metric": "MoE tokens/sec (expert parallel)", "value": T / (ms_step / 1e3), "unit": "tokens/s",
-            "ms_per_step": ms_step, "dtype": "bf16 tensor-core operands, fp32 accumulate",
+            "ms_per_step": ms_step, "dtype": "fp16 tensor-core operands (precise mode), fp32 accumulate",
             "config": {"workload": f"{name}: n={c['experts']} top-{c['k']} d={c['d']} h={c['h']}, "
-                                   f"{c['tokens_per_gpu']} tokens/GPU, experts {c['experts'] // N}/GPU",
+                                   f"{T} tokens, {T // N} tokens and {c['experts'] // N} experts per GPU",
                        "global_tokens": T,
                        "parallelism": (f"ep{N} (NCCL point-to-point exchange by expert range, overlapped with the "
                                        "GEMMs)") if N > 1 else "ep1 (no exchange: one device pass)",
@@ -558,7 +605,7 @@ def _mix_seed(seed, stream):
 
 
 # ------------------------------------------------------ reference arm
-def run_reference(args, dist):
+def run_reference(args, n_gpus):
     cfg = dict(CFG[args.workload])
     if args.depth:
         cfg["depth"] = args.depth
@@ -571,9 +618,9 @@ def run_reference(args, dist):
         times.append(dt)
     sec = sum(times) / len(times)
     value = n / sec
-    return {"metric": METRIC, "value": value, "unit": "programs/s", "n_gpus": max(1, dist.world),
+    return {"metric": METRIC, "value": value, "unit": "programs/s", "n_gpus": n_gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generators, seed 0; random-init weights)",
             "impl": "reference",
             "config": {"workload": f"{args.workload}: IEP forward, residual conv modules on 128x14x14 "
@@ -586,18 +633,44 @@ def run_reference(args, dist):
                     "d2h_bytes_per_step": 0}}
 
 
+def dry_run(args, dist):
+    """The launch without GPU work: world size and this rank's shard."""
+    N = max(1, dist.world)
+    if args.workload in MOE:
+        total = global_units(MOE[args.workload]["tokens"], N, args.scaling)
+    else:
+        total = global_units(CFG[args.workload]["batch"], N, args.scaling)
+    first, last = shard(total, dist.rank, N)
+    counts = [0] * N
+    if dist.pg:  # every rank's shard size, gathered to check the split
+        import torch
+        t = torch.zeros(N, dtype=torch.int64)
+        t[dist.rank] = last - first
+        dist.pg.all_reduce(t)
+        counts = t.tolist()
+    else:
+        counts = [last - first]
+    return {"dry_run": True, "rank": dist.rank, "world": N, "gpus": args.gpus, "workload": args.workload,
+            "scaling": args.scaling, "total": total, "shard": [first, last], "shard_sizes": counts}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         # CPU arm: rank 0 alone runs and prints; other ranks exit without work.
         if int(os.environ.get("RANK", "0")) == 0:
-            print(json.dumps(run_reference(args, Dist(1))), flush=True)
+            print(json.dumps(run_reference(args, int(os.environ.get("WORLD_SIZE", args.gpus)))), flush=True)
         return
-    dist = Dist(args.gpus)
+    maybe_spawn(args)
+    dist = Dist(args.gpus, cpu=args.dry_run)
+    if args.dry_run:
+        print(json.dumps(dry_run(args, dist)), flush=True)
+        dist.close()
+        return
     if args.workload in MOE:
         r = run_moe_ep(args, dist, args.workload) if args.workload == "cfg5" else run_moe(args, dist, args.workload)
         r.update({"n_gpus": max(1, dist.world), "steps": args.steps, "warmup": 3,
-                  "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                  "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                   "data": "synthetic (reference generators, seed 0; random-init experts)",
                   "metric": METRIC, "gpu_launches": r["gpu_launches_per_step"] * args.steps})
         if dist.rank == 0:

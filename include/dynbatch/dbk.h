@@ -115,8 +115,8 @@ int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t*
  * plane maps → staged fp16 images (hi; plus the lo image, the block's
  * residual, in stage_lo for unary members); plane_stride in rows. */
 int dbk_rb_gather(const void* tasks, const int32_t* n_tasks, int32_t list, int32_t step, int64_t task_cap,
-                  void* stage_x, void* stage_lo, void* stage_cat, int64_t plane_stride, int32_t blocks,
-                  void* stream);
+                  void* stage_x, void* stage_lo, void* stage_cat, int64_t plane_stride, int32_t* err,
+                  int32_t blocks, void* stream);
 /* One persistent launch (one CTA per SM, CTA pairs) for steps [step,
  * step_end) over a device work queue of their tiles, step s + 1's after
  * all of step s (step_done[s] counts step s's finished conv3x3 #2 tiles): conv1x1 over [x; y] → z hi/lo (stage_x / stage_lo),
@@ -127,7 +127,10 @@ int dbk_rb_gather(const void* tasks, const int32_t* n_tasks, int32_t list, int32
  * done1 per tile; == epoch means done); queue[step] and step_done[step ..
  * step_end) must be 0 at launch.
  * D[128 channels][tile_m positions] per tile (tcgen05.mma M = 128, N =
- * tile_m, 256 or 128; the plan must have used the same tile_m). */
+ * tile_m, 256 or 128; the plan must have used the same tile_m). *err gets
+ * the first of 9 (a module output is non-finite, src/executor.cpp:156-159)
+ * or 10 (a value exceeds the fp16 operand range, |x| > 65504); the gather
+ * flags its input maps the same way. */
 /* Sets the step kernel's attributes; call before capturing a forward. */
 int dbk_rb_configure(void);
 int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* step_tile_begin,
@@ -138,8 +141,8 @@ int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* st
                 const void* memtab, void* stage_x, void* stage_lo, void* stage_cat, void* stage_mid,
                 int64_t plane_stride, const void* const* w0, const void* const* w1, const void* const* w2,
                 const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
-                int32_t* done0, int32_t* done1, int32_t* step_done, int32_t* queue, int32_t tile_m,
-                int32_t num_sms, void* stream);
+                int32_t* done0, int32_t* done1, int32_t* step_done, int32_t* queue, int32_t* err,
+                int32_t tile_m, int32_t num_sms, void* stream);
 /* Zeroes stage_x rows between each segment's last image and its tile end
  * (read as top / left pads by the next segment's first image), every
  * forward, so a new layout needs no full re-zeroing. */
@@ -176,37 +179,40 @@ int dbk_moe_expert_fp64(int64_t T, int32_t n, int32_t k, int32_t d, int32_t h,
 int dbk_moe_combine_fp64(int64_t T, int32_t k, int32_t d, const double* weights,
                          const double* staged, double* out, void* stream);
 
-/* bf16 tensor-core experts (moe_gemm.cu): per-expert 128-row padded
- * layout and tile list; dispatch of x rows (fp32 → bf16, pre-tiled operand);
- * grouped tcgen05 GEMM (epi 0: ReLU → tiled bf16 H, epi 1: bf16 Y rows);
- * slot-order combine. */
-int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int32_t* tile_expert,
-                        int32_t* tile_rb, int32_t* n_tiles, void* stream);
+/* Tensor-core experts (moe_gemm.cu). fmt selects the 16-bit operand format
+ * of the dispatched rows, weights, H and Y: DBK_FMT_F16 (fp16, the precise
+ * mode) or DBK_FMT_BF16; tcgen05 kind::f16 with fp32 accumulation either way.
+ * Per-expert 256-row padded layout and tile list; dispatch of x rows (fp32 →
+ * 16-bit, pre-tiled operand); grouped GEMM (epi 0: ReLU → tiled H, epi 1: Y
+ * rows); slot-order combine. */
+enum { DBK_FMT_BF16 = 0, DBK_FMT_F16 = 1 };
+int dbk_moe_tc_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int32_t* tile_expert,
+                      int32_t* tile_rb, int32_t* n_tiles, void* stream);
 /* dispatch: row_of_item[item] = the item's padded row, then one warp per
- * token writes bf16(x[token]) into its k rows of the SWIZZLE_128B tiled A
+ * token writes its 16-bit x row into its k rows of the SWIZZLE_128B tiled A
  * (k ≤ 8, d a multiple of 256). */
-int dbk_moe_bf16_dispatch(int64_t T, int32_t k, int32_t d, const int32_t* order, const int32_t* ids,
-                          const int32_t* offsets, const int32_t* pstart, const float* x, void* A,
-                          int32_t* row_of_item, int32_t blocks, void* stream);
+int dbk_moe_tc_dispatch(int32_t fmt, int64_t T, int32_t k, int32_t d, const int32_t* order, const int32_t* ids,
+                        const int32_t* offsets, const int32_t* pstart, const float* x, void* A,
+                        int32_t* row_of_item, int32_t blocks, void* stream);
 /* row tiles [tile_begin, tile_end) of the tile list (tile_end < 0: all
  * *n_tiles); EP chunks run one contiguous expert range at a time. epi 1:
  * padded row r's output goes to Y row out_row[r] (skipped when < 0; out_row
  * NULL = row r) — the EP receive order directly, no unpack pass. */
-int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
-                      const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
-                      const void* const* W, void* H, void* Y, int32_t tile_begin, int32_t tile_end,
-                      const int32_t* out_row, int32_t sms, void* stream);
-int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const double* weights,
-                         const int32_t* row_of_item, const void* Y, float* out, void* stream);
+int dbk_moe_tc_gemm(int32_t fmt, int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
+                    const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
+                    const void* const* W, void* H, void* Y, int32_t tile_begin, int32_t tile_end,
+                    const int32_t* out_row, int32_t sms, void* stream);
+int dbk_moe_tc_combine(int32_t fmt, int64_t T, int32_t k, int32_t d, const double* weights,
+                       const int32_t* row_of_item, const void* Y, float* out, void* stream);
 
 /* Expert-parallel MoE (moe_gemm.cu): pack the rank's rows in sorted order
- * (bf16) with pos_of_item[item] = row; receiver layout from the count matrix
- * cnt[G][E] (source × local expert); scatter received rows into the tiled
- * GEMM operand (expert-major, source-rank order within an expert) with
+ * (16-bit, fmt) with pos_of_item[item] = row; receiver layout from the count
+ * matrix cnt[G][E] (source × local expert); scatter received rows into the
+ * tiled GEMM operand (expert-major, source-rank order within an expert) with
  * recv_of_row[padded row] = receive row (−1: padding), which GEMM2's
  * epilogue uses to write its rows back in receive order (out_row). */
-int dbk_moe_ep_pack(int64_t items, int32_t k, int32_t d, const int32_t* order, const float* x, void* send,
-                    int32_t* pos_of_item, int32_t blocks, void* stream);
+int dbk_moe_ep_pack(int32_t fmt, int64_t items, int32_t k, int32_t d, const int32_t* order, const float* x,
+                    void* send, int32_t* pos_of_item, int32_t blocks, void* stream);
 int dbk_moe_ep_layout(int32_t G, int32_t E, const int32_t* cnt, int32_t* pstart, int32_t* tile_expert,
                       int32_t* tile_rb, int32_t* n_tiles, int32_t* src_row, int32_t* cum, void* stream);
 int dbk_moe_ep_scatter(int32_t G, int32_t E, int32_t d, const int32_t* pstart, const int32_t* tile_expert,

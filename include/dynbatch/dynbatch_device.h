@@ -18,7 +18,10 @@
  *                        fp32 accumulation and fp32 node values.
  * MoE precisions:
  *   DB_MOE_FP64 — reference arithmetic order (src/moe.cpp:98-145, 254-264).
- *   DB_MOE_BF16 — tcgen05 grouped GEMMs, bf16 operands, fp32 accumulation.
+ *   DB_MOE_BF16 — tcgen05 grouped GEMMs, bf16 operands, H and expert outputs,
+ *                 fp32 accumulation (≈4e-3 max-norm vs fp64).
+ *   DB_MOE_FP16 — the same kernels with fp16 operands, H and expert outputs
+ *                 (≤ 1e-3 max-norm vs fp64, same tensor-core rate).
  */
 #ifndef DYNBATCH_DYNBATCH_DEVICE_H
 #define DYNBATCH_DYNBATCH_DEVICE_H
@@ -30,7 +33,7 @@ extern "C" {
 #endif
 
 typedef enum { DB_MODULE_DENSE = 0, DB_MODULE_RESBLOCK = 1 } db_module_kind;
-typedef enum { DB_MOE_FP64 = 0, DB_MOE_BF16 = 1 } db_moe_precision;
+typedef enum { DB_MOE_FP64 = 0, DB_MOE_BF16 = 1, DB_MOE_FP16 = 2 } db_moe_precision;
 
 typedef struct {
   int32_t module_kind; /* db_module_kind */
@@ -169,28 +172,34 @@ DYNBATCH_API db_status db_moe_session_stats(db_moe_session* s, db_session_stats_
 DYNBATCH_API db_status db_moe_session_routing(db_moe_session* s, int32_t* ids, double* weights,
                                               int32_t* expert_offsets, int32_t* items);
 DYNBATCH_API db_status db_moe_session_run(db_moe_session* s, db_run** out);
+/* Output rows rows[0..n_rows) of the last forward as fp32 [n_rows×d] (rows
+ * NULL: the first n_rows) — a sample of a layer too large to download. */
+DYNBATCH_API db_status db_moe_session_outputs(db_moe_session* s, const int64_t* rows, int64_t n_rows,
+                                              float* out);
 DYNBATCH_API db_status db_moe_session_time(db_moe_session* s, int32_t iters, int32_t profile,
                                            double* ms, db_kernel_times_t* kt);
 DYNBATCH_API void db_moe_session_free(db_moe_session* s);
 
 /* ---- expert-parallel MoE (one rank of G) ----
  * Tokens [rank·T/G, (rank+1)·T/G) and experts [rank·n/G, (rank+1)·n/G) of
- * the db_moe_run fixtures; bf16 tcgen05 grouped GEMMs. One forward:
+ * the db_moe_run fixtures; tcgen05 grouped GEMMs with 16-bit operands
+ * (precision DB_MOE_FP16 or DB_MOE_BF16; rows exchanged in that format).
+ * One forward:
  *   dispatch: gate → stable expert sort → the rank's k·T/G rows packed in
- *             sorted order into send_rows (device bf16 [items][d]);
+ *             sorted order into send_rows (device 16-bit [items][d]);
  *             expert_counts[n] (host) = rows per global expert, so the rows
  *             for rank q are the contiguous block of q's experts;
  *   (caller) all-to-all of the counts and an all-to-allv of the rows;
  *   experts:  recv_rows = every source's block in rank order, recv_counts
- *             [G][n/G] (host; source × local expert); ret_rows (device bf16)
+ *             [G][n/G] (host; source × local expert); ret_rows (device 16-bit)
  *             receives the expert outputs in receive order;
  *   (caller) the reverse all-to-allv (ret_rows → the senders);
  *   combine:  ret_rows = this rank's rows back in its sorted order → the
  *             slot-order weighted sum (outputs fp32 [T/G][d]).
  * Kernels run on db_moe_ep_stream(). */
 typedef struct db_moe_ep_session db_moe_ep_session;
-DYNBATCH_API db_status db_moe_ep_create(const db_moe_opts* opts, int32_t rank, int32_t world,
-                                        db_moe_ep_session** out);
+DYNBATCH_API db_status db_moe_ep_create(const db_moe_opts* opts, int32_t precision, int32_t rank,
+                                        int32_t world, db_moe_ep_session** out);
 DYNBATCH_API db_status db_moe_ep_sizes(db_moe_ep_session* s, int64_t* tokens, int64_t* items,
                                        int32_t* local_experts);
 DYNBATCH_API db_status db_moe_ep_dispatch(db_moe_ep_session* s, void* send_rows, int32_t* expert_counts);

@@ -88,6 +88,38 @@ void orc_random_batch(int64_t rows, int64_t width, uint64_t seed, double* out) {
   for (int64_t i = 0; i < rows * width; ++i) out[i] = rng_range(&r, -1.0, 1.0);
 }
 
+/* Selected rows of random_batch(·, width, seed), rows ascending: one pass
+ * over the stream, skipping whole 312-word blocks between them (the skipped
+ * outputs need only the twist, not the tempering), for samples of batches
+ * too large to generate whole (cfg5: 17 GB of inputs). */
+void orc_random_rows(const int64_t* rows, int64_t n, int64_t width, uint64_t seed, double* out) {
+  orc_rng r;
+  orc_rng_seed(&r, seed);
+  uint64_t pos = 0; /* outputs consumed so far */
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t want = (uint64_t)rows[i] * (uint64_t)width;
+    uint64_t skip = want - pos;
+    while (skip > 0) {
+      uint64_t left = (uint64_t)(MT_N - r.idx);
+      if (r.idx >= MT_N) {
+        if (skip >= MT_N) {
+          mt_twist(&r);
+          r.idx = MT_N;
+          skip -= MT_N;
+          continue;
+        }
+        mt_twist(&r);
+        left = MT_N;
+      }
+      uint64_t step = skip < left ? skip : left;
+      r.idx += (int)step;
+      skip -= step;
+    }
+    for (int64_t j = 0; j < width; ++j) out[i * width + j] = rng_range(&r, -1.0, 1.0);
+    pos = want + (uint64_t)width;
+  }
+}
+
 uint64_t orc_fnv1a64(const void* data, int64_t bytes, uint64_t h) {
   const unsigned char* p = (const unsigned char*)data;
   if (h == 0) h = 0xcbf29ce484222325ULL;

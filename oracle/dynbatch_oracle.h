@@ -36,6 +36,7 @@ uint64_t orc_rng_u64(orc_rng* r);
 double orc_rng_uniform(orc_rng* r);
 uint64_t orc_mix_seed(uint64_t seed, uint64_t stream);
 void orc_random_batch(int64_t rows, int64_t width, uint64_t seed, double* out);
+void orc_random_rows(const int64_t* rows, int64_t n, int64_t width, uint64_t seed, double* out);
 uint64_t orc_fnv1a64(const void* data, int64_t bytes, uint64_t h);
 
 int64_t orc_gen_batch(int kind, int64_t b, int p, int depth, int length, double branch_prob,

@@ -31,7 +31,7 @@ STRATEGY = {"naive": 0, "standard": 1, "improved": 2, "online": 3}
 WORKLOAD = {"balanced": 0, "balanced-tree": 0, "chain": 1, "chain-heavy": 1, "dag": 2,
             "random-dag": 2}
 MODULE_DENSE, MODULE_RESBLOCK = 0, 1
-MOE_FP64, MOE_BF16 = 0, 1
+MOE_FP64, MOE_BF16, MOE_FP16 = 0, 1, 2
 
 
 class DynbatchError(RuntimeError):
@@ -164,8 +164,9 @@ SIGNATURES = {
     "db_moe_session_stats": (C.c_int32, [VP, C.POINTER(SessionStats)]),
     "db_moe_session_routing": (C.c_int32, [VP, VP, VP, VP, VP]),
     "db_moe_session_run": (C.c_int32, [VP, PVP]),
+    "db_moe_session_outputs": (C.c_int32, [VP, VP, C.c_int64, VP]),
     "db_moe_session_free": (None, [VP]),
-    "db_moe_ep_create": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, C.c_int32, PVP]),
+    "db_moe_ep_create": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, C.c_int32, C.c_int32, PVP]),
     "db_moe_ep_sizes": (C.c_int32, [VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "db_moe_ep_dispatch": (C.c_int32, [VP, VP, VP]),
     "db_moe_ep_experts": (C.c_int32, [VP, VP, VP, VP]),
@@ -531,6 +532,17 @@ class MoeSession(_Handle):
         check(lib().db_moe_session_run(self.h, C.byref(h)))
         return Run(h)
 
+    def outputs(self, rows=None) -> np.ndarray:
+        """fp32 output rows of the last forward (all, or the given tokens)."""
+        if rows is None:
+            out = np.zeros((self.T, self.d), np.float32)
+            check(lib().db_moe_session_outputs(self.h, None, self.T, _ptr(out)))
+            return out
+        r = np.ascontiguousarray(rows, np.int64)
+        out = np.zeros((len(r), self.d), np.float32)
+        check(lib().db_moe_session_outputs(self.h, _ptr(r), len(r), _ptr(out)))
+        return out
+
 
 class MoeEpSession(_Handle):
     """One rank of the expert-parallel MoE layer (db_moe_ep_*): tokens
@@ -539,12 +551,13 @@ class MoeEpSession(_Handle):
     between the stages is the caller's (paper_1707_02402_b200.moe_ep)."""
     _free = "db_moe_ep_free"
 
-    def __init__(self, experts, k, batch, data_dim, hidden, seed=0, rank=0, world=1):
+    def __init__(self, experts, k, batch, data_dim, hidden, seed=0, rank=0, world=1, precision=MOE_FP16):
         o = MoeOpts(experts, k, batch, data_dim, hidden, seed)
         h = C.c_void_p()
-        check(lib().db_moe_ep_create(C.byref(o), rank, world, C.byref(h)))
+        check(lib().db_moe_ep_create(C.byref(o), precision, rank, world, C.byref(h)))
         super().__init__(h)
         self.n, self.k, self.d, self.rank, self.world = experts, k, data_dim, rank, world
+        self.precision = precision
         t, it, e = C.c_int64(), C.c_int64(), C.c_int32()
         check(lib().db_moe_ep_sizes(self.h, C.byref(t), C.byref(it), C.byref(e)))
         self.tokens, self.items, self.local_experts = t.value, it.value, e.value

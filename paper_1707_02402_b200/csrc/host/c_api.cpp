@@ -605,13 +605,19 @@ db_status db_moe_session_run(db_moe_session* s, db_run** out) {
   });
 }
 
+db_status db_moe_session_outputs(db_moe_session* s, const int64_t* rows, int64_t n_rows, float* out) {
+  if (!s || !out) return null_arg();
+  return guarded([&] { s->s->download_rows(rows, n_rows, out); });
+}
+
 void db_moe_session_free(db_moe_session* s) { delete s; }
 
 // ------------------------------------------------- expert-parallel MoE rank
-db_status db_moe_ep_create(const db_moe_opts* opts, int32_t rank, int32_t world, db_moe_ep_session** out) {
+db_status db_moe_ep_create(const db_moe_opts* opts, int32_t precision, int32_t rank, int32_t world,
+                           db_moe_ep_session** out) {
   if (!opts || !out) return null_arg();
   return guarded([&] {
-    auto s = std::make_unique<dynbatch::dev::MoeEp>(to_cfg(opts), opts->seed, rank, world);
+    auto s = std::make_unique<dynbatch::dev::MoeEp>(to_cfg(opts), opts->seed, precision, rank, world);
     *out = new db_moe_ep_session{std::move(s)};
   });
 }

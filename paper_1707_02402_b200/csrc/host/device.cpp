@@ -353,6 +353,45 @@ std::int64_t DeviceProgramBatch::group_count(cudaStream_t s) const {
   return groups;
 }
 
+// The reference executor's order checks replayed over a host schedule
+// without arithmetic: a gather of a node not yet written raises
+// MissingOperand (src/executor.cpp:48-51, gathered operand by operand for the
+// whole group, :139-151), a second write raises SingleAssignmentViolation
+// (:62-65, at the group's scatter, :161-163), and an absent root raises
+// MissingOperand (:168-173). The resblock kernels trust the schedule order
+// (forwarding and tile dependencies are planned from it), so a broken
+// schedule fails here, before any kernel runs, with the error the reference
+// raises first.
+static void check_reference_order(const Schedule& schedule, const HostCSR& c) {
+  std::vector<unsigned char> present(static_cast<size_t>(c.N), 0);
+  auto ref = [&](std::int32_t g) {
+    const std::int32_t e = c.example[static_cast<size_t>(g)];
+    return "(" + std::to_string(e) + ", " + std::to_string(g - c.prog_off[static_cast<size_t>(e)]) + ")";
+  };
+  for (const Step& step : schedule.steps) {
+    for (const CallGroup& grp : step) {
+      const int a = c.arity_of[static_cast<size_t>(grp.function_id)];
+      for (int k = 0; k < a; ++k) {
+        for (const NodeRef& r : grp.members) {
+          const std::int32_t g = c.prog_off[static_cast<size_t>(r.example)] + r.node;
+          const std::int32_t ch = c.child_list[static_cast<size_t>(c.child_off[static_cast<size_t>(g)] + k)];
+          if (!present[static_cast<size_t>(ch)]) throw_error(Errc::missing_operand, "no value for node " + ref(ch));
+        }
+      }
+      for (const NodeRef& r : grp.members) {
+        const std::int32_t g = c.prog_off[static_cast<size_t>(r.example)] + r.node;
+        if (present[static_cast<size_t>(g)])
+          throw_error(Errc::single_assignment_violation, "node " + ref(g) + " written twice");
+        present[static_cast<size_t>(g)] = 1;
+      }
+    }
+  }
+  for (std::int64_t e = 0; e < c.b; ++e) {
+    const std::int32_t g = c.root_g[static_cast<size_t>(e)];
+    if (!present[static_cast<size_t>(g)]) throw_error(Errc::missing_operand, "no value for node " + ref(g));
+  }
+}
+
 int DeviceProgramBatch::load_schedule(const Schedule& schedule, cudaStream_t s) {
   std::vector<std::int32_t> mg, gf, gb, sgb;
   sgb.reserve(schedule.steps.size() + 1);
@@ -372,7 +411,17 @@ int DeviceProgramBatch::load_schedule(const Schedule& schedule, cudaStream_t s) 
                                                   std::to_string(r.example) + ", " +
                                                   std::to_string(r.node) + ")");
         }
-        mg.push_back(csr_.prog_off[static_cast<size_t>(r.example)] + r.node);
+        const std::int32_t gid = csr_.prog_off[static_cast<size_t>(r.example)] + r.node;
+        // a member runs its group's module: its own function must be the
+        // group's (the reference indexes children by the group's arity, UB
+        // on a mismatch; the device kernels would read absent children)
+        if (csr_.fid[static_cast<size_t>(gid)] != g.function_id) {
+          throw_error(Errc::invalid_argument, "node (" + std::to_string(r.example) + ", " + std::to_string(r.node) +
+                                                  ") has function " + std::to_string(csr_.fid[static_cast<size_t>(gid)]) +
+                                                  " but sits in a group of function " +
+                                                  std::to_string(g.function_id));
+        }
+        mg.push_back(gid);
       }
     }
   }
@@ -486,8 +535,13 @@ void IepSession::set_strategy(Strategy strategy) {
 }
 
 void IepSession::set_schedule(const Schedule* schedule) {
+  // programs staged by a pipelined set_programs are built first (their build
+  // would otherwise drop this schedule), and the host CSR must describe them
+  flush_programs();
+  ensure_host_mirror();
   ++schedule_gen_;  // a host schedule's step count and tables are baked into a capture
   if (schedule) {
+    if (kind_ == ModuleKind::resblock) check_reference_order(*schedule, batch_->csr());
     batch_->load_schedule(*schedule, stream_);
     host_schedule_ = true;
     strategy_ = schedule->strategy;
@@ -672,6 +726,7 @@ void IepSession::check_errors() {
     case 0: return;
     case 7: throw_error(Errc::missing_operand, "a call group read a node that was not yet computed");
     case 9: throw_error(Errc::non_finite_value, "a module produced non-finite rows");
+    case 10: throw_error(Errc::non_finite_value, "a value exceeds the fp16 operand range of the conv kernels (|x| > 65504)");
     case 14: throw_error(Errc::single_assignment_violation, "a node was written twice");
     default: throw std::runtime_error("device executor error " + std::to_string(e));
   }

@@ -239,6 +239,8 @@ class IepSession {
   Schedule download_schedule();
   std::vector<std::int32_t> download_labels();
   TensorBatch download_outputs();
+  // Output rows rows[0..n_rows) (rows NULL: 0..n_rows) as fp32.
+  void download_rows(const std::int64_t* rows, std::int64_t n_rows, float* out);
   ExecutionTrace trace();
   std::int64_t launches() const { return launches_; }
   double algorithmic_flops() const;
@@ -304,7 +306,7 @@ class IepSession {
   void add_forward_work();
 };
 
-// MoE session (fp64 reference order or bf16 tensor-core grouped GEMMs).
+// MoE session (fp64 reference order, or fp16 / bf16 tensor-core grouped GEMMs).
 class MoeSession {
  public:
   MoeSession(const MoeConfig& cfg, std::uint64_t seed, int precision, std::int64_t first,
@@ -316,6 +318,8 @@ class MoeSession {
   cudaStream_t stream() const { return stream_; }
   void routing(std::int32_t* ids, double* weights, std::int32_t* offsets, std::int32_t* items);
   TensorBatch download_outputs();
+  // Output rows rows[0..n_rows) (rows NULL: 0..n_rows) as fp32.
+  void download_rows(const std::int64_t* rows, std::int64_t n_rows, float* out);
   ExecutionTrace trace();
   std::int64_t launches() const { return launches_; }
   double algorithmic_flops() const;
@@ -340,7 +344,7 @@ class MoeSession {
 // (NCCL all-to-allv over NVLink through torch.distributed).
 class MoeEp {
  public:
-  MoeEp(const MoeConfig& cfg, std::uint64_t seed, int rank, int world);
+  MoeEp(const MoeConfig& cfg, std::uint64_t seed, int precision, int rank, int world);
   ~MoeEp();
   std::int64_t tokens() const { return T_; }
   std::int64_t items() const;

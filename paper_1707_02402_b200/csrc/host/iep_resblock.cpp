@@ -267,7 +267,7 @@ void IepSession::forward_resblock() {
   // leaf operands of every step in one launch (they only read the inputs)
   prof_.begin(2, stream_);
   check(dbk_rb_gather(R.tasks.get(), R.n_tasks.get(), 0, 0, R.task_cap, R.stage_x.get(), R.stage_lo.get(),
-                      R.stage_cat.get(), R.plane_stride, gather_blocks, stream_),
+                      R.stage_cat.get(), R.plane_stride, err_.get(), gather_blocks, stream_),
         "dbk_rb_gather leaves");
   prof_.end(stream_);
   ++launches_;
@@ -279,7 +279,7 @@ void IepSession::forward_resblock() {
     if (R.n_shared > 0) {  // children shared by several parents: values of earlier steps
       prof_.begin(2, stream_);
       check(dbk_rb_gather(R.tasks.get(), R.n_tasks.get(), 1, s, R.task_cap, R.stage_x.get(), R.stage_lo.get(),
-                          R.stage_cat.get(), R.plane_stride, gather_blocks, stream_),
+                          R.stage_cat.get(), R.plane_stride, err_.get(), gather_blocks, stream_),
             "dbk_rb_gather shared");
       prof_.end(stream_);
       ++launches_;
@@ -291,7 +291,7 @@ void IepSession::forward_resblock() {
                       B.group_begin.get(), R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(),
                       R.memtab.get(), R.stage_x.get(), R.stage_lo.get(), R.stage_cat.get(), R.stage_mid.get(),
                       R.plane_stride, R.w0tab.get(), R.w1tab.get(), R.w2tab.get(), R.b0tab.get(), R.b1tab.get(),
-                      R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.step_done.get(), R.queue.get(),
+                      R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.step_done.get(), R.queue.get(), err_.get(),
                       R.tile_m, sms, stream_),
           "conv step");
     prof_.end(stream_);

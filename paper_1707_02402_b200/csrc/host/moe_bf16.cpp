@@ -1,9 +1,10 @@
-// moe_bf16.cpp — host side of the bf16 tensor-core MoE expert path.
+// moe_bf16.cpp — host side of the 16-bit tensor-core MoE expert path
+// (fp16 or bf16 operands, DBK_FMT_*).
 //
 // Expert weights follow ExpertSet (src/moe.cpp:71-88): Rng(mix_seed(seed, e)),
 // w1 [d × h] then w2 [h × d], uniform(-0.5, 0.5)/sqrt(fan_in); they are
 // generated on host threads (one Rng stream per expert, so the split is
-// exact), rounded to bf16 and pre-tiled for the grouped tcgen05 GEMMs
+// exact), rounded to fp16 or bf16 and pre-tiled for the grouped tcgen05 GEMMs
 // (moe_gemm.cu): B operand of GEMM1 = W1ᵀ [N = h][K = d], of GEMM2 = W2ᵀ
 // [N = d][K = h], as 32 KB blocks per (256-column N tile, 64-wide K chunk).
 #include "moe_bf16.hpp"
@@ -12,6 +13,8 @@
 #include <cmath>
 #include <cstring>
 #include <thread>
+
+#include <cuda_fp16.h>
 
 #include "device.hpp"
 
@@ -29,11 +32,18 @@ std::uint16_t bf16(double v) {
   return static_cast<std::uint16_t>(u >> 16);
 }
 
+std::uint16_t f16(double v) {
+  const __half x = __double2half(v);  // round to nearest even, subnormals kept
+  std::uint16_t u;
+  std::memcpy(&u, &x, 2);
+  return u;
+}
+
 // Element (n, kk) of the N × K operand, stored input-major in `w` as
 // w[kk * N + n], into [N/256][K/64] blocks of 32 KB, each two 16 KB halves
 // (columns 0-127 and 128-255 of the N tile: one per CTA of a pair) of
 // [8 k-groups][128 n][8] (moe_gemm.cu).
-void tile_weights(const std::vector<double>& w, int K, int N, std::uint16_t* out) {
+void tile_weights(const std::vector<double>& w, int K, int N, int fmt, std::uint16_t* out) {
   const int n_kc = K / 64;
   for (int kk = 0; kk < K; ++kk) {
     const int kc = kk / 64, k8 = (kk % 64) / 8, ke = kk % 8;
@@ -41,14 +51,14 @@ void tile_weights(const std::vector<double>& w, int K, int N, std::uint16_t* out
       const int nt = n / 256, half = (n % 256) / 128, nn = n % 128;
       const size_t blk = static_cast<size_t>(nt) * n_kc + kc;
       out[blk * 256 * 64 + ((static_cast<size_t>(half) * 8 + k8) * 128 + nn) * 8 + ke] =
-          bf16(w[static_cast<size_t>(kk) * N + n]);
+          fmt == DBK_FMT_F16 ? f16(w[static_cast<size_t>(kk) * N + n]) : bf16(w[static_cast<size_t>(kk) * N + n]);
     }
   }
 }
 
 }  // namespace
 
-void upload_expert_weights(const MoeConfig& cfg, std::uint64_t expert_seed, int e_first, int n_local,
+void upload_expert_weights(const MoeConfig& cfg, std::uint64_t expert_seed, int e_first, int n_local, int fmt,
                            Buf<std::uint16_t>& w1, Buf<std::uint16_t>& w2, Buf<const void*>& w1tab,
                            Buf<const void*>& w2tab, cudaStream_t s) {
   const int d = static_cast<int>(cfg.data_dim), h = static_cast<int>(cfg.hidden);
@@ -67,9 +77,9 @@ void upload_expert_weights(const MoeConfig& cfg, std::uint64_t expert_seed, int 
         Rng rng(mix_seed(expert_seed, static_cast<std::uint64_t>(e_first + e0 + j)));
         std::vector<double> w(per);
         for (double& v : w) v = rng.uniform(-0.5, 0.5) * s1;  // w1 [d][h]
-        tile_weights(w, d, h, h1.data() + per * j);
+        tile_weights(w, d, h, fmt, h1.data() + per * j);
         for (double& v : w) v = rng.uniform(-0.5, 0.5) * s2;  // w2 [h][d]
-        tile_weights(w, h, d, h2.data() + per * j);
+        tile_weights(w, h, d, fmt, h2.data() + per * j);
       });
     }
     for (auto& t : pool) t.join();
@@ -88,25 +98,26 @@ void upload_expert_weights(const MoeConfig& cfg, std::uint64_t expert_seed, int 
 
 struct MoeBf16::Impl {
   std::int64_t T = 0;
-  int n = 0, k = 0, d = 0, h = 0, sms = 148;
+  int n = 0, k = 0, d = 0, h = 0, sms = 148, fmt = DBK_FMT_F16;
   Buf<float> x, out;
-  Buf<std::uint16_t> Y;  // bf16 expert outputs, padded rows
+  Buf<std::uint16_t> Y;  // 16-bit expert outputs, padded rows
   Buf<std::uint8_t> A, H;
   Buf<std::uint16_t> w1, w2;  // all experts, tiled
   Buf<const void*> w1tab, w2tab;
   Buf<std::int32_t> pstart, tile_expert, tile_rb, n_tiles, row_of_item;
 };
 
-MoeBf16::MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed, cudaStream_t s)
+MoeBf16::MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed, int fmt, cudaStream_t s)
     : impl_(std::make_unique<Impl>()) {
   Impl& I = *impl_;
   I.T = T;
+  I.fmt = fmt;
   I.n = static_cast<int>(cfg.experts);
   I.k = static_cast<int>(cfg.active_per_example);
   I.d = static_cast<int>(cfg.data_dim);
   I.h = static_cast<int>(cfg.hidden);
   if (I.d % 256 != 0 || I.h % 256 != 0) {
-    throw_error(Errc::invalid_argument, "bf16 MoE path needs data_dim and hidden multiples of 256");
+    throw_error(Errc::invalid_argument, "tensor-core MoE path needs data_dim and hidden multiples of 256");
   }
   I.sms = sm_count();
   const std::int64_t rows = T * I.k + static_cast<std::int64_t>(I.n) * 256;  // experts padded to 256 rows
@@ -120,7 +131,7 @@ MoeBf16::MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed
   I.tile_rb.alloc(static_cast<size_t>(rows / 128 + 1));
   I.n_tiles.alloc(1);
   I.row_of_item.alloc(static_cast<size_t>(T) * I.k);
-  upload_expert_weights(cfg, expert_seed, 0, I.n, I.w1, I.w2, I.w1tab, I.w2tab, s);
+  upload_expert_weights(cfg, expert_seed, 0, I.n, fmt, I.w1, I.w2, I.w1tab, I.w2tab, s);
 }
 
 MoeBf16::~MoeBf16() = default;
@@ -135,27 +146,30 @@ int MoeBf16::forward(const std::int32_t* ids, const double* wts, const std::int3
   Impl& I = *impl_;
   const int blocks = I.sms * 8;
   if (prof) prof->begin(3, s);
-  check(dbk_moe_bf16_layout(I.n, offsets, I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(), I.n_tiles.get(), s),
+  check(dbk_moe_tc_layout(I.n, offsets, I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(), I.n_tiles.get(), s),
         "moe layout");
-  check(dbk_moe_bf16_dispatch(I.T, I.k, I.d, order, ids, offsets, I.pstart.get(), I.x.get(), I.A.get(),
+  check(dbk_moe_tc_dispatch(I.fmt, I.T, I.k, I.d, order, ids, offsets, I.pstart.get(), I.x.get(), I.A.get(),
                               I.row_of_item.get(), blocks, s),
         "moe dispatch");
   if (prof) prof->end(s);
   if (prof) prof->begin(4, s);
-  check(dbk_moe_bf16_gemm(0, I.n, I.d, I.h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
+  check(dbk_moe_tc_gemm(I.fmt, 0, I.n, I.d, I.h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
                           I.w1tab.get(), I.H.get(), nullptr, 0, -1, nullptr, I.sms, s),
         "moe gemm1");
   if (prof) prof->end(s);
   if (prof) prof->begin(5, s);
-  check(dbk_moe_bf16_gemm(1, I.n, I.h, I.d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
+  check(dbk_moe_tc_gemm(I.fmt, 1, I.n, I.h, I.d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
                           I.w2tab.get(), nullptr, I.Y.get(), 0, -1, nullptr, I.sms, s),
         "moe gemm2");
   if (prof) prof->end(s);
   if (prof) prof->begin(6, s);
-  check(dbk_moe_bf16_combine(I.T, I.k, I.d, wts, I.row_of_item.get(), I.Y.get(), I.out.get(), s), "moe combine");
+  check(dbk_moe_tc_combine(I.fmt, I.T, I.k, I.d, wts, I.row_of_item.get(), I.Y.get(), I.out.get(), s), "moe combine");
   if (prof) prof->end(s);
   return 5;
 }
+
+float* MoeBf16::inputs_device() { return impl_->x.get(); }
+const float* MoeBf16::outputs_device() const { return impl_->out.get(); }
 
 void MoeBf16::download_outputs(float* out, cudaStream_t s) {
   check(cudaMemcpyAsync(out, impl_->out.get(), sizeof(float) * static_cast<size_t>(impl_->T) * impl_->d,

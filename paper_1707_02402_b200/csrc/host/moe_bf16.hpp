@@ -1,4 +1,5 @@
-// moe_bf16.hpp — bf16 tensor-core MoE expert path (grouped tcgen05 GEMMs).
+// moe_bf16.hpp — 16-bit tensor-core MoE expert path (grouped tcgen05 GEMMs),
+// fp16 (DBK_FMT_F16, the precise mode) or bf16 (DBK_FMT_BF16) operands.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -10,21 +11,24 @@
 
 namespace dynbatch::dev {
 
-// ExpertSet experts [e_first, e_first + n_local) (src/moe.cpp:71-88) as bf16
-// pre-tiled GEMM operands, with device tables of per-expert pointers.
-void upload_expert_weights(const MoeConfig& cfg, std::uint64_t expert_seed, int e_first, int n_local,
+// ExpertSet experts [e_first, e_first + n_local) (src/moe.cpp:71-88) as
+// 16-bit (fmt) pre-tiled GEMM operands, with device tables of per-expert
+// pointers.
+void upload_expert_weights(const MoeConfig& cfg, std::uint64_t expert_seed, int e_first, int n_local, int fmt,
                            Buf<std::uint16_t>& w1, Buf<std::uint16_t>& w2, Buf<const void*>& w1tab,
                            Buf<const void*>& w2tab, cudaStream_t s);
 
 class MoeBf16 {
  public:
-  MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed, cudaStream_t s);
+  MoeBf16(const MoeConfig& cfg, std::int64_t T, std::uint64_t expert_seed, int fmt, cudaStream_t s);
   ~MoeBf16();
   void upload_inputs(const float* x, cudaStream_t s);
   // Dispatch → GEMM1+ReLU → GEMM2 → combine; returns kernels launched.
   int forward(const std::int32_t* ids, const double* wts, const std::int32_t* order,
               const std::int32_t* offsets, cudaStream_t s, Profiler* prof);
   void download_outputs(float* out, cudaStream_t s);
+  float* inputs_device();
+  const float* outputs_device() const;
 
  private:
   struct Impl;

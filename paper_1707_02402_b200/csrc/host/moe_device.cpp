@@ -107,6 +107,43 @@ struct StreamGuard {
   cudaStream_t s;
   ~StreamGuard() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
 };
+
+// Rows [first, last) of random_batch(·, width, seed) (src/workload.cpp:207-212)
+// generated straight into device memory in 32 MB host chunks, as V: the
+// values are the reference's doubles (fp32 inputs are their rounding), and
+// no full-size host copy exists (cfg5: 17 GB of fp64 inputs).
+template <typename V>
+void upload_random_rows(V* dst, std::int64_t first, std::int64_t last, std::int64_t width, std::uint64_t seed) {
+  if (last <= first) return;
+  Rng rng(seed);
+  rng.discard(static_cast<std::uint64_t>(first) * static_cast<std::uint64_t>(width));
+  const std::int64_t chunk = std::max<std::int64_t>(1, (std::int64_t{32} << 20) / (width * static_cast<std::int64_t>(sizeof(V))));
+  std::vector<V> buf(static_cast<size_t>(std::min(chunk, last - first) * width));
+  for (std::int64_t r = first; r < last; r += chunk) {
+    const std::int64_t nr = std::min(chunk, last - r);
+    const size_t n = static_cast<size_t>(nr * width);
+    for (size_t i = 0; i < n; ++i) buf[i] = static_cast<V>(rng.uniform(-1.0, 1.0));
+    check(cudaMemcpy(dst + (r - first) * width, buf.data(), n * sizeof(V), cudaMemcpyHostToDevice), "H2D rows");
+  }
+}
+
+// gen_moe_inputs (src/workload.cpp:248-254) for tokens [first, last): scores
+// (fp64) and inputs (fp64 or fp32) on two host threads (independent streams).
+template <typename X>
+void upload_moe_inputs(const MoeConfig& cfg, std::uint64_t seed, std::int64_t first, std::int64_t last,
+                       double* scores, X* x) {
+  std::exception_ptr err;
+  std::thread t([&] {
+    try {
+      upload_random_rows(scores, first, last, cfg.experts, mix_seed(seed, 0x11ULL));
+    } catch (...) {
+      err = std::current_exception();
+    }
+  });
+  upload_random_rows(x, first, last, cfg.data_dim, mix_seed(seed, 0x10ULL));
+  t.join();
+  if (err) std::rethrow_exception(err);
+}
 }  // namespace
 
 // ------------------------------------------------------------ MoeSession
@@ -128,6 +165,7 @@ MoeSession::MoeSession(const MoeConfig& cfg_in, std::uint64_t seed, int precisio
   if (first < 0 || last > cfg.batch) throw_error(Errc::invalid_argument, "token range out of bounds");
   T_ = last - first;
   impl_->cfg = cfg;
+  if (precision < 0 || precision > 2) throw_error(Errc::invalid_argument, "unknown MoE precision");
   impl_->precision = precision;
   stream_ = make_stream();
   MoeDev& D = impl_->dev;
@@ -135,24 +173,16 @@ MoeSession::MoeSession(const MoeConfig& cfg_in, std::uint64_t seed, int precisio
           static_cast<int>(cfg.data_dim), static_cast<int>(cfg.hidden));
   // Fixture generation exactly as db_moe_run (src/c_api.cpp:270-290); the
   // token slice keeps rows [first, last) of the full-batch generators.
-  const TensorBatch inputs = random_batch(cfg.batch, cfg.data_dim, mix_seed(seed, 0x10ULL));
-  const TensorBatch scores = random_batch(cfg.batch, cfg.experts, mix_seed(seed, 0x11ULL));
-  check(cudaMemcpyAsync(D.scores.get(), scores.data().data() + first * cfg.experts,
-                        sizeof(double) * static_cast<size_t>(T_ * cfg.experts), cudaMemcpyHostToDevice, stream_),
-        "H2D scores");
   const std::uint64_t expert_seed = mix_seed(seed, 0xe4be27ULL);
   if (precision == 0) {
     D.alloc_fp64_work();
-    check(cudaMemcpyAsync(D.x.get(), inputs.data().data() + first * cfg.data_dim,
-                          sizeof(double) * static_cast<size_t>(T_ * cfg.data_dim), cudaMemcpyHostToDevice, stream_),
-          "H2D inputs");
+    upload_moe_inputs(cfg, seed, first, last, D.scores.get(), D.x.get());
     const ExpertSet experts(cfg.experts, cfg.data_dim, cfg.hidden, expert_seed);
     D.upload_experts(experts, stream_);
   } else {
-    impl_->bf16 = std::make_unique<MoeBf16>(cfg, T_, expert_seed, stream_);
-    std::vector<float> xin(static_cast<size_t>(T_ * cfg.data_dim));
-    for (size_t i = 0; i < xin.size(); ++i) xin[i] = static_cast<float>(inputs.data()[static_cast<size_t>(first * cfg.data_dim) + i]);
-    impl_->bf16->upload_inputs(xin.data(), stream_);
+    impl_->bf16 = std::make_unique<MoeBf16>(cfg, T_, expert_seed,
+                                            precision == 2 ? DBK_FMT_F16 : DBK_FMT_BF16, stream_);
+    upload_moe_inputs(cfg, seed, first, last, D.scores.get(), impl_->bf16->inputs_device());
   }
   check(cudaStreamSynchronize(stream_), "upload");
 }
@@ -229,7 +259,7 @@ void MoeSession::forward_host(const float* inputs, const double* scores, float* 
   MoeDev& D = impl_->dev;
   check(cudaMemcpyAsync(D.scores.get(), scores, sizeof(double) * static_cast<size_t>(T_) * D.n,
                         cudaMemcpyHostToDevice, stream_), "H2D scores");
-  if (impl_->precision == 0) throw_error(Errc::invalid_argument, "forward_host needs the bf16 session");
+  if (impl_->precision == 0) throw_error(Errc::invalid_argument, "forward_host needs a tensor-core session (DB_MOE_BF16 or DB_MOE_FP16)");
   impl_->bf16->upload_inputs(inputs, stream_);
   forward();
   impl_->bf16->download_outputs(outputs, stream_);
@@ -269,6 +299,24 @@ TensorBatch MoeSession::download_outputs() {
   return out;
 }
 
+void MoeSession::download_rows(const std::int64_t* rows, std::int64_t n_rows, float* out) {
+  synchronize();
+  MoeDev& D = impl_->dev;
+  const size_t d = static_cast<size_t>(D.d);
+  std::vector<double> tmp(impl_->precision == 0 ? d : 0);
+  for (std::int64_t i = 0; i < n_rows; ++i) {
+    const std::int64_t r = rows ? rows[i] : i;
+    if (r < 0 || r >= T_) throw_error(Errc::invalid_argument, "output row out of range");
+    if (impl_->precision == 0) {
+      check(cudaMemcpy(tmp.data(), D.out.get() + static_cast<size_t>(r) * d, d * 8, cudaMemcpyDeviceToHost), "D2H");
+      for (size_t j = 0; j < d; ++j) out[static_cast<size_t>(i) * d + j] = static_cast<float>(tmp[j]);
+    } else {
+      check(cudaMemcpy(out + static_cast<size_t>(i) * d, impl_->bf16->outputs_device() + static_cast<size_t>(r) * d,
+                       d * 4, cudaMemcpyDeviceToHost), "D2H");
+    }
+  }
+}
+
 ExecutionTrace MoeSession::trace() { return impl_->dev.trace(stream_); }
 
 double MoeSession::algorithmic_flops() const {
@@ -293,12 +341,12 @@ std::int64_t MoeSession::d2h_bytes() const { return T_ * impl_->cfg.data_dim * 4
 // ----------------------------------------------------------------- MoeEp
 struct MoeEp::Impl {
   MoeConfig cfg;
-  int rank = 0, world = 1, E = 0, e_first = 0, sms = 148;
+  int rank = 0, world = 1, E = 0, e_first = 0, sms = 148, fmt = DBK_FMT_F16;
   MoeDev dev;
   Buf<float> x, out;
   Buf<std::int32_t> pos_of_item, cnt, pstart, tile_expert, tile_rb, n_tiles, src_row, cum, recv_of_row;
   Buf<std::uint8_t> A, H;
-  Buf<std::uint16_t> w1, w2, Y;  // Y: GEMM2 rows of the world-1 pass
+  Buf<std::uint16_t> w1, w2, Y;  // 16-bit (fmt); Y: GEMM2 rows of the world-1 pass
   Buf<const void*> w1tab, w2tab;
   std::int64_t cap_rows = 0;  // padded-row capacity of A / H
   std::vector<std::int32_t> cnt_h;    // last layout's counts [G][E]
@@ -316,16 +364,20 @@ struct MoeEp::Impl {
   }
 };
 
-MoeEp::MoeEp(const MoeConfig& cfg, std::uint64_t seed, int rank, int world) : impl_(std::make_unique<Impl>()) {
+MoeEp::MoeEp(const MoeConfig& cfg, std::uint64_t seed, int precision, int rank, int world)
+    : impl_(std::make_unique<Impl>()) {
   require_device();
   cfg.check();
+  if (precision != 1 && precision != 2)
+    throw_error(Errc::invalid_argument, "expert parallel runs the tensor-core path (DB_MOE_BF16 or DB_MOE_FP16)");
   if (world < 1 || rank < 0 || rank >= world) throw_error(Errc::invalid_argument, "bad rank/world");
   if (cfg.experts % world != 0 || cfg.batch % world != 0)
     throw_error(Errc::invalid_argument, "expert parallel needs experts and tokens divisible by the world size");
   if (cfg.data_dim % 256 != 0 || cfg.hidden % 256 != 0)
-    throw_error(Errc::invalid_argument, "bf16 MoE path needs data_dim and hidden multiples of 256");
+    throw_error(Errc::invalid_argument, "tensor-core MoE path needs data_dim and hidden multiples of 256");
   Impl& I = *impl_;
   I.cfg = cfg;
+  I.fmt = precision == 2 ? DBK_FMT_F16 : DBK_FMT_BF16;
   I.rank = rank;
   I.world = world;
   I.E = static_cast<int>(cfg.experts / world);
@@ -338,11 +390,8 @@ MoeEp::MoeEp(const MoeConfig& cfg, std::uint64_t seed, int rank, int world) : im
   const int n = static_cast<int>(cfg.experts), k = static_cast<int>(cfg.active_per_example);
   D.alloc(T_, n, k, static_cast<int>(cfg.data_dim), static_cast<int>(cfg.hidden));
   // the rank's token slice of the db_moe_run fixtures (src/c_api.cpp:270-290)
-  const TensorBatch inputs = random_batch_range(first, last, cfg.data_dim, mix_seed(seed, 0x10ULL));
-  const TensorBatch scores = random_batch_range(first, last, cfg.experts, mix_seed(seed, 0x11ULL));
-  D.scores.upload(scores.data().data(), scores.data().size(), stream_);
-  std::vector<float> xin(inputs.data().begin(), inputs.data().end());
-  I.x.upload(xin, stream_);
+  I.x.alloc(static_cast<size_t>(T_) * cfg.data_dim);
+  upload_moe_inputs(cfg, seed, first, last, D.scores.get(), I.x.get());
   I.out.alloc(static_cast<size_t>(T_) * cfg.data_dim);
   I.pos_of_item.alloc(static_cast<size_t>(T_) * k);
   I.cnt.alloc(static_cast<size_t>(world) * I.E);
@@ -351,7 +400,7 @@ MoeEp::MoeEp(const MoeConfig& cfg, std::uint64_t seed, int rank, int world) : im
   I.src_row.alloc(static_cast<size_t>(I.E) * world);
   I.cum.alloc(static_cast<size_t>(I.E) * (world + 1));
   I.ensure_capacity(T_ * k + static_cast<std::int64_t>(I.E) * 256);
-  upload_expert_weights(cfg, mix_seed(seed, 0xe4be27ULL), I.e_first, I.E, I.w1, I.w2, I.w1tab, I.w2tab, stream_);
+  upload_expert_weights(cfg, mix_seed(seed, 0xe4be27ULL), I.e_first, I.E, I.fmt, I.w1, I.w2, I.w1tab, I.w2tab, stream_);
   check(cudaStreamSynchronize(stream_), "upload");
 }
 
@@ -372,7 +421,7 @@ void MoeEp::dispatch(void* send, std::int32_t* expert_counts) {
   prof_.begin(3, stream_);
   D.gate(stream_);
   D.sort(stream_);
-  check(dbk_moe_ep_pack(items(), D.k, D.d, D.order.get(), I.x.get(), send, I.pos_of_item.get(), I.sms * 8, stream_),
+  check(dbk_moe_ep_pack(I.fmt, items(), D.k, D.d, D.order.get(), I.x.get(), send, I.pos_of_item.get(), I.sms * 8, stream_),
         "ep pack");
   prof_.end(stream_);
   const auto off = D.offsets.download(static_cast<size_t>(D.n) + 1, stream_);  // synchronises
@@ -391,21 +440,21 @@ void MoeEp::forward_local() {
   prof_.begin(3, stream_);
   D.gate(stream_);
   D.sort(stream_);
-  check(dbk_moe_bf16_layout(D.n, D.offsets.get(), I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(),
+  check(dbk_moe_tc_layout(D.n, D.offsets.get(), I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(),
                             I.n_tiles.get(), stream_), "moe layout");
-  check(dbk_moe_bf16_dispatch(T_, D.k, d, D.order.get(), D.ids.get(), D.offsets.get(), I.pstart.get(), I.x.get(),
+  check(dbk_moe_tc_dispatch(I.fmt, T_, D.k, d, D.order.get(), D.ids.get(), D.offsets.get(), I.pstart.get(), I.x.get(),
                               I.A.get(), I.pos_of_item.get(), I.sms * 8, stream_),
         "moe dispatch");  // pos_of_item holds each item's padded row here
   prof_.end(stream_);
   if (I.Y.size() < static_cast<size_t>(I.cap_rows) * d) I.Y.alloc(static_cast<size_t>(I.cap_rows) * d);
   prof_.begin(4, stream_);
-  check(dbk_moe_bf16_gemm(0, D.n, d, h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
+  check(dbk_moe_tc_gemm(I.fmt, 0, D.n, d, h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
                           I.w1tab.get(), I.H.get(), nullptr, 0, -1, nullptr, I.sms, stream_), "moe gemm1");
-  check(dbk_moe_bf16_gemm(1, D.n, h, d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
+  check(dbk_moe_tc_gemm(I.fmt, 1, D.n, h, d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
                           I.w2tab.get(), nullptr, I.Y.get(), 0, -1, nullptr, I.sms, stream_), "moe gemm2");
   prof_.end(stream_);
   prof_.begin(6, stream_);
-  check(dbk_moe_bf16_combine(T_, D.k, d, D.wts.get(), I.pos_of_item.get(), I.Y.get(), I.out.get(), stream_),
+  check(dbk_moe_tc_combine(I.fmt, T_, D.k, d, D.wts.get(), I.pos_of_item.get(), I.Y.get(), I.out.get(), stream_),
         "moe combine");
   prof_.end(stream_);
 }
@@ -441,11 +490,11 @@ void MoeEp::experts_range(const void* recv, void* ret, int e_begin, int e_end) {
   prof_.begin(4, stream_);
   check(dbk_moe_ep_scatter(G, E, d, I.pstart.get(), I.tile_expert.get(), I.src_row.get(), I.cum.get(), recv,
                            I.A.get(), I.recv_of_row.get(), r0, r1, I.sms * 8, stream_), "ep scatter");
-  check(dbk_moe_bf16_gemm(0, E, d, h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
+  check(dbk_moe_tc_gemm(I.fmt, 0, E, d, h, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.A.get(),
                           I.w1tab.get(), I.H.get(), nullptr, r0 / 128, r1 / 128, nullptr, I.sms, stream_),
         "ep gemm1");
   // GEMM2 writes each output row straight to its receive-order row of ret
-  check(dbk_moe_bf16_gemm(1, E, h, d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
+  check(dbk_moe_tc_gemm(I.fmt, 1, E, h, d, I.n_tiles.get(), I.tile_expert.get(), I.tile_rb.get(), I.H.get(),
                           I.w2tab.get(), nullptr, ret, r0 / 128, r1 / 128, I.recv_of_row.get(), I.sms, stream_),
         "ep gemm2");
   prof_.end(stream_);
@@ -465,7 +514,7 @@ void MoeEp::experts(const void* recv, const std::int32_t* cnt, void* ret) {
 void MoeEp::combine(const void* ret_recv) {
   Impl& I = *impl_;
   prof_.begin(6, stream_);
-  check(dbk_moe_bf16_combine(T_, I.dev.k, I.dev.d, I.dev.wts.get(), I.pos_of_item.get(), ret_recv, I.out.get(),
+  check(dbk_moe_tc_combine(I.fmt, T_, I.dev.k, I.dev.d, I.dev.wts.get(), I.pos_of_item.get(), ret_recv, I.out.get(),
                              stream_), "ep combine");
   prof_.end(stream_);
 }

@@ -1,11 +1,16 @@
-// moe_gemm.cu — bf16 tensor-core MoE experts: dispatch → grouped GEMM1+ReLU
+// moe_gemm.cu — tensor-core MoE experts: dispatch → grouped GEMM1+ReLU
 // → grouped GEMM2 → slot-order combine (sm_100a, tcgen05/TMEM).
+//
+// Operand format (fmt): DBK_FMT_F16 (fp16 operands, H and Y; the precise
+// mode, ≤ 1e-3 max-norm vs the fp64 reference) or DBK_FMT_BF16 (bf16; wider
+// range, ≈4e-3). Both run tcgen05.mma kind::f16 at the same rate with fp32
+// accumulation; only the idesc A/B format bits and the packing differ.
 //
 // Reference semantics: ExpertSet::apply (src/moe.cpp:98-145) on each
 // occupied expert's stacked rows, staged at token·k + slot (:244-251),
 // combined per token in slot order (:254-264). Routing (ids, weights, the
 // stable per-expert item order and offsets) comes from moe.cu / sched.cu and
-// is bit-identical to the reference; the arithmetic here is bf16 operands
+// is bit-identical to the reference; the arithmetic here is 16-bit operands
 // with fp32 accumulation.
 //
 // Layout: rows of expert e occupy a 128-aligned padded range starting at
@@ -29,6 +34,20 @@
 namespace {
 
 using namespace dbk;
+
+// Two fp32 values → one 32-bit pair of 16-bit operands (round to nearest).
+template <bool F16>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  return F16 ? pack_f16x2(lo, hi) : pack_bf16x2(lo, hi);
+}
+template <bool F16>
+__device__ __forceinline__ float2 unpack2(uint32_t v) {
+  if constexpr (F16) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&v));
+  } else {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v));
+  }
+}
 
 constexpr int kBM = 128;         // rows per tile
 constexpr int kBN = 256;         // output columns per tile
@@ -110,9 +129,10 @@ __device__ __forceinline__ int64_t a_sw128_off(int32_t row, int32_t kchunks, int
 }
 
 // Token-major dispatch: one warp per token reads its fp32 row once
-// (coalesced) and writes the bf16 row into each of its k items' padded rows,
+// (coalesced) and writes the 16-bit row into each of its k items' padded rows,
 // whole 128-byte lines (lane group g = lane / 8 covers K chunk 4·it + g,
 // lane e = lane % 8 its 16-byte piece e).
+template <bool F16>
 __global__ void k_moe_dispatch(int64_t T, int32_t k, int32_t d, const float* __restrict__ x,
                                const int32_t* __restrict__ row_of_item, uint8_t* __restrict__ A) {
   const int lane = threadIdx.x & 31;
@@ -139,10 +159,10 @@ __global__ void k_moe_dispatch(int64_t T, int32_t k, int32_t d, const float* __r
         const int32_t col = (it0 + u) * 256 + lane * 8;
         if (col >= d) break;
         uint4 pk;
-        pk.x = pack_bf16x2(a[u].x, a[u].y);
-        pk.y = pack_bf16x2(a[u].z, a[u].w);
-        pk.z = pack_bf16x2(b[u].x, b[u].y);
-        pk.w = pack_bf16x2(b[u].z, b[u].w);
+        pk.x = pack2<F16>(a[u].x, a[u].y);
+        pk.y = pack2<F16>(a[u].z, a[u].w);
+        pk.z = pack2<F16>(b[u].x, b[u].y);
+        pk.w = pack2<F16>(b[u].z, b[u].w);
         const int32_t kc = col / kBK, j = (col % kBK) / 8;
 #pragma unroll
         for (int s = 0; s < 8; ++s)
@@ -161,8 +181,8 @@ struct GemmParams {
   const int32_t* tile_rb;
   const uint8_t* A;             // tiled activations [rb][K/64][16 KB]
   const uint8_t* const* W;      // per expert tiled weights [N/256][K/64][32 KB]
-  uint8_t* H;                   // EPI 0: tiled bf16 output [rb][N/64][16 KB]
-  __nv_bfloat16* Y;             // EPI 1: bf16 row-major [row][N]
+  uint8_t* H;                   // EPI 0: tiled 16-bit output [rb][N/64][16 KB]
+  uint16_t* Y;                  // EPI 1: 16-bit row-major [row][N]
   int32_t tile_begin, tile_end;  // row-tile range (tile_end < 0: up to *n_tiles)
   const int32_t* out_row;        // EPI 1: Y row of padded row r = out_row[r] (< 0: skip); null = r
 };
@@ -174,11 +194,12 @@ struct GemmParams {
 // reads from L2 halve. The even CTA issues the MMAs. The odd CTA relays its
 // "stage landed" events to the even CTA's barriers, and the commits arrive in
 // both CTAs. Each CTA's epilogue drains its own 128 accumulator lanes.
-// EPI 0 = ReLU → bf16 tiled H (GEMM2's A); EPI 1 = bf16 rows.
-template <int EPI>
+// EPI 0 = ReLU → tiled H (GEMM2's A); EPI 1 = rows. F16: fp16 operands
+// and outputs, else bf16.
+template <int EPI, bool F16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_moe_gemm(const __grid_constant__ GemmParams P) {
-  constexpr uint32_t IDESC = idesc_bf16_f32(2 * kBM, kBN);
+  constexpr uint32_t IDESC = F16 ? idesc_f16_f32(2 * kBM, kBN) : idesc_bf16_f32(2 * kBM, kBN);
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kABytes;
@@ -286,24 +307,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int g = 0; g < 4; ++g) {
             const int32_t col = n0 + g * 8;
             uint4 pk;
-            pk.x = pack_bf16x2(fmaxf(v[g * 8 + 0], 0.f), fmaxf(v[g * 8 + 1], 0.f));
-            pk.y = pack_bf16x2(fmaxf(v[g * 8 + 2], 0.f), fmaxf(v[g * 8 + 3], 0.f));
-            pk.z = pack_bf16x2(fmaxf(v[g * 8 + 4], 0.f), fmaxf(v[g * 8 + 5], 0.f));
-            pk.w = pack_bf16x2(fmaxf(v[g * 8 + 6], 0.f), fmaxf(v[g * 8 + 7], 0.f));
+            pk.x = pack2<F16>(fmaxf(v[g * 8 + 0], 0.f), fmaxf(v[g * 8 + 1], 0.f));
+            pk.y = pack2<F16>(fmaxf(v[g * 8 + 2], 0.f), fmaxf(v[g * 8 + 3], 0.f));
+            pk.z = pack2<F16>(fmaxf(v[g * 8 + 4], 0.f), fmaxf(v[g * 8 + 5], 0.f));
+            pk.w = pack2<F16>(fmaxf(v[g * 8 + 6], 0.f), fmaxf(v[g * 8 + 7], 0.f));
             uint8_t* blk = P.H + (static_cast<int64_t>(rb) * n_kc_out + col / kBK) * kABytes;
             *reinterpret_cast<uint4*>(blk + (((col % kBK) / 8) * kBM + rr) * 16) = pk;
           }
         } else {
           const int64_t orow = P.out_row ? P.out_row[row] : row;
           if (orow < 0) continue;  // padding row (EP: no receive row)
-          __nv_bfloat16* dst = P.Y + orow * P.N + n0;
+          uint16_t* dst = P.Y + orow * P.N + n0;
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             uint4 pk;
-            pk.x = pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]);
-            pk.y = pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]);
-            pk.z = pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]);
-            pk.w = pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]);
+            pk.x = pack2<F16>(v[g * 8 + 0], v[g * 8 + 1]);
+            pk.y = pack2<F16>(v[g * 8 + 2], v[g * 8 + 3]);
+            pk.z = pack2<F16>(v[g * 8 + 4], v[g * 8 + 5]);
+            pk.w = pack2<F16>(v[g * 8 + 6], v[g * 8 + 7]);
             *reinterpret_cast<uint4*>(dst + g * 8) = pk;
           }
         }
@@ -325,8 +346,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // out[t] = Σ_slot w[t·k + slot] · Y[row_of_item[t·k + slot]] in slot order.
+template <bool F16>
 __global__ void k_moe_combine_f32(int64_t T, int32_t k, int32_t d, const double* __restrict__ w,
-                                  const int32_t* __restrict__ row_of_item, const __nv_bfloat16* __restrict__ Y,
+                                  const int32_t* __restrict__ row_of_item, const uint16_t* __restrict__ Y,
                                   float* __restrict__ out) {
   const int64_t t = blockIdx.x;
   if (t >= T) return;
@@ -335,10 +357,10 @@ __global__ void k_moe_combine_f32(int64_t T, int32_t k, int32_t d, const double*
     for (int32_t s = 0; s < k; ++s) {
       const float ws = static_cast<float>(w[t * k + s]);
       const uint4 raw = *reinterpret_cast<const uint4*>(Y + static_cast<int64_t>(row_of_item[t * k + s]) * d + j);
-      const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const uint32_t* y2 = reinterpret_cast<const uint32_t*>(&raw);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float2 f = __bfloat1622float2(y2[q]);
+        const float2 f = unpack2<F16>(y2[q]);
         acc[2 * q] = fmaf(ws, f.x, acc[2 * q]);
         acc[2 * q + 1] = fmaf(ws, f.y, acc[2 * q + 1]);
       }
@@ -348,53 +370,57 @@ __global__ void k_moe_combine_f32(int64_t T, int32_t k, int32_t d, const double*
   }
 }
 
-template <int EPI>
+template <int EPI, bool F16>
 int launch_gemm(const GemmParams& p, int sms, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_moe_gemm<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_moe_gemm<EPI, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     configured = true;
   }
-  k_moe_gemm<EPI><<<sms / 2 * 2, kThreads, kSmem, s>>>(p);  // CTA pairs
+  k_moe_gemm<EPI, F16><<<sms / 2 * 2, kThreads, kSmem, s>>>(p);  // CTA pairs
   return static_cast<int>(cudaGetLastError());
 }
 
 }  // namespace
 
-extern "C" int dbk_moe_bf16_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int32_t* tile_expert,
+extern "C" int dbk_moe_tc_layout(int32_t n, const int32_t* offsets, int32_t* pstart, int32_t* tile_expert,
                                    int32_t* tile_rb, int32_t* n_tiles, void* stream) {
   k_moe_layout<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, offsets, pstart, tile_expert, tile_rb, n_tiles);
   return static_cast<int>(cudaGetLastError());
 }
 
-extern "C" int dbk_moe_bf16_dispatch(int64_t T, int32_t k, int32_t d, const int32_t* order, const int32_t* ids,
-                                     const int32_t* offsets, const int32_t* pstart, const float* x, void* A,
-                                     int32_t* row_of_item, int32_t blocks, void* stream) {
+extern "C" int dbk_moe_tc_dispatch(int32_t fmt, int64_t T, int32_t k, int32_t d, const int32_t* order,
+                                   const int32_t* ids, const int32_t* offsets, const int32_t* pstart, const float* x,
+                                   void* A, int32_t* row_of_item, int32_t blocks, void* stream) {
   if (T <= 0) return 0;
   if (k > 8 || d % 256 != 0) return static_cast<int>(cudaErrorInvalidValue);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   k_moe_item_rows<<<blocks, 256, 0, s>>>(T * k, order, ids, offsets, pstart, row_of_item);
-  k_moe_dispatch<<<blocks, 256, 0, s>>>(T, k, d, x, row_of_item, static_cast<uint8_t*>(A));
+  if (fmt == DBK_FMT_F16) k_moe_dispatch<true><<<blocks, 256, 0, s>>>(T, k, d, x, row_of_item, static_cast<uint8_t*>(A));
+  else k_moe_dispatch<false><<<blocks, 256, 0, s>>>(T, k, d, x, row_of_item, static_cast<uint8_t*>(A));
   return static_cast<int>(cudaGetLastError());
 }
 
-extern "C" int dbk_moe_bf16_gemm(int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
+extern "C" int dbk_moe_tc_gemm(int32_t fmt, int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
                                  const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
                                  const void* const* W, void* H, void* Y, int32_t tile_begin, int32_t tile_end,
                                  const int32_t* out_row, int32_t sms, void* stream) {
   if (K % kBK != 0 || N % kBN != 0) return static_cast<int>(cudaErrorInvalidValue);
   GemmParams p{n, K, N, n_tiles, tile_expert, tile_rb, static_cast<const uint8_t*>(A),
                reinterpret_cast<const uint8_t* const*>(W), static_cast<uint8_t*>(H),
-               static_cast<__nv_bfloat16*>(Y), tile_begin, tile_end, out_row};
+               static_cast<uint16_t*>(Y), tile_begin, tile_end, out_row};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return epi == 0 ? launch_gemm<0>(p, sms, s) : launch_gemm<1>(p, sms, s);
+  if (fmt == DBK_FMT_F16) return epi == 0 ? launch_gemm<0, true>(p, sms, s) : launch_gemm<1, true>(p, sms, s);
+  return epi == 0 ? launch_gemm<0, false>(p, sms, s) : launch_gemm<1, false>(p, sms, s);
 }
 
-extern "C" int dbk_moe_bf16_combine(int64_t T, int32_t k, int32_t d, const double* weights,
-                                    const int32_t* row_of_item, const void* Y, float* out, void* stream) {
+extern "C" int dbk_moe_tc_combine(int32_t fmt, int64_t T, int32_t k, int32_t d, const double* weights,
+                                  const int32_t* row_of_item, const void* Y, float* out, void* stream) {
   if (T <= 0) return 0;
-  k_moe_combine_f32<<<static_cast<unsigned>(T), 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      T, k, d, weights, row_of_item, static_cast<const __nv_bfloat16*>(Y), out);
+  const uint16_t* y = static_cast<const uint16_t*>(Y);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (fmt == DBK_FMT_F16) k_moe_combine_f32<true><<<static_cast<unsigned>(T), 128, 0, s>>>(T, k, d, weights, row_of_item, y, out);
+  else k_moe_combine_f32<false><<<static_cast<unsigned>(T), 128, 0, s>>>(T, k, d, weights, row_of_item, y, out);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -412,10 +438,11 @@ __global__ void k_moe_ep_positions(int64_t items, const int32_t* __restrict__ or
     pos_of_item[order[i]] = static_cast<int32_t>(i);
 }
 
-// send[pos_of_item[t·k + s]] = bf16(x[t]): one warp per token reads its fp32
-// row once and writes its k bf16 rows (row-contiguous, coalesced).
+// send[pos_of_item[t·k + s]] = fp16/bf16(x[t]): one warp per token reads its fp32
+// row once and writes its k 16-bit rows (row-contiguous, coalesced).
+template <bool F16>
 __global__ void k_moe_ep_pack(int64_t T, int32_t k, int32_t d, const int32_t* __restrict__ pos_of_item,
-                              const float* __restrict__ x, __nv_bfloat16* __restrict__ send) {
+                              const float* __restrict__ x, uint16_t* __restrict__ send) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += warps) {
@@ -427,10 +454,10 @@ __global__ void k_moe_ep_pack(int64_t T, int32_t k, int32_t d, const int32_t* __
       const float4 a = __ldg(reinterpret_cast<const float4*>(src + j));
       const float4 b = __ldg(reinterpret_cast<const float4*>(src + j + 4));
       uint4 pk;
-      pk.x = pack_bf16x2(a.x, a.y);
-      pk.y = pack_bf16x2(a.z, a.w);
-      pk.z = pack_bf16x2(b.x, b.y);
-      pk.w = pack_bf16x2(b.z, b.w);
+      pk.x = pack2<F16>(a.x, a.y);
+      pk.y = pack2<F16>(a.z, a.w);
+      pk.z = pack2<F16>(b.x, b.y);
+      pk.w = pack2<F16>(b.z, b.w);
 #pragma unroll
       for (int s = 0; s < 8; ++s)
         if (s < k) *reinterpret_cast<uint4*>(send + static_cast<int64_t>(pos[s]) * d + j) = pk;
@@ -524,7 +551,7 @@ __global__ void __launch_bounds__(1024) k_moe_ep_layout(int32_t G, int32_t E, co
 __global__ void k_moe_ep_scatter(int32_t G, int32_t d, const int32_t* __restrict__ pstart,
                                  const int32_t* __restrict__ tile_expert, const int32_t* __restrict__ src_row,
                                  const int32_t* __restrict__ cum, int32_t E,
-                                 const __nv_bfloat16* __restrict__ recv, uint8_t* __restrict__ A,
+                                 const uint16_t* __restrict__ recv, uint8_t* __restrict__ A,
                                  int32_t* __restrict__ recv_of_row, int32_t row_begin, int32_t row_end) {
   const int32_t total_rows = row_end < 0 ? pstart[E] : row_end;
   const int32_t kchunks = d / kBK;
@@ -551,13 +578,14 @@ __global__ void k_moe_ep_scatter(int32_t G, int32_t d, const int32_t* __restrict
 
 }  // namespace
 
-extern "C" int dbk_moe_ep_pack(int64_t items, int32_t k, int32_t d, const int32_t* order, const float* x,
+extern "C" int dbk_moe_ep_pack(int32_t fmt, int64_t items, int32_t k, int32_t d, const int32_t* order, const float* x,
                                void* send, int32_t* pos_of_item, int32_t blocks, void* stream) {
   if (items <= 0) return 0;
   if (k > 8 || d % 8 != 0) return static_cast<int>(cudaErrorInvalidValue);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   k_moe_ep_positions<<<blocks, 256, 0, s>>>(items, order, pos_of_item);
-  k_moe_ep_pack<<<blocks, 256, 0, s>>>(items / k, k, d, pos_of_item, x, static_cast<__nv_bfloat16*>(send));
+  if (fmt == DBK_FMT_F16) k_moe_ep_pack<true><<<blocks, 256, 0, s>>>(items / k, k, d, pos_of_item, x, static_cast<uint16_t*>(send));
+  else k_moe_ep_pack<false><<<blocks, 256, 0, s>>>(items / k, k, d, pos_of_item, x, static_cast<uint16_t*>(send));
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -574,7 +602,7 @@ extern "C" int dbk_moe_ep_scatter(int32_t G, int32_t E, int32_t d, const int32_t
                                   const void* recv, void* A, int32_t* recv_of_row, int32_t row_begin,
                                   int32_t row_end, int32_t blocks, void* stream) {
   k_moe_ep_scatter<<<blocks, kBM, 0, static_cast<cudaStream_t>(stream)>>>(
-      G, d, pstart, tile_expert, src_row, cum, E, static_cast<const __nv_bfloat16*>(recv),
+      G, d, pstart, tile_expert, src_row, cum, E, static_cast<const uint16_t*>(recv),
       static_cast<uint8_t*>(A), recv_of_row, row_begin, row_end);
   return static_cast<int>(cudaGetLastError());
 }

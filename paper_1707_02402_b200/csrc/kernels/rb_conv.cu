@@ -171,7 +171,32 @@ struct StepParams {
   int32_t* done1;        // per tile: conv3x3 #1 done (== epoch)
   int32_t* step_done;    // per step: conv3x3 #2 tiles completed (zeroed each forward)
   int32_t* queue;        // claim counters, one per launch's first step (zeroed each forward)
+  int32_t* err;          // first error code (kErrNonFinite / kErrRange), 0 = none
 };
+
+// Error codes shared with the host (IepSession::check_errors): a module
+// produced a non-finite row (src/executor.cpp:156-159; ReLU as max maps NaN
+// to 0 like the reference's `v > 0 ? v : 0`, so this is +inf), or a value
+// outside the fp16 operand range (|x| > 65504) that the next block could not
+// stage.
+constexpr int32_t kErrNonFinite = 9;
+constexpr int32_t kErrRange = 10;
+
+// Two error codes → one (non-finite outranks range; 0 = none).
+__device__ __forceinline__ int32_t merge_code(int32_t a, int32_t b) {
+  return (a == kErrNonFinite || b == kErrNonFinite) ? kErrNonFinite : (a | b);
+}
+
+// 0, kErrRange or kErrNonFinite for 8 values about to become fp16 operands.
+__device__ __forceinline__ int32_t range_code(const float* o) {
+  int32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float a = fabsf(o[k]);
+    if (!(a <= 65504.f)) c = merge_code(c, (a == INFINITY || a != a) ? kErrNonFinite : kErrRange);
+  }
+  return c;
+}
 
 // Wait accounting (read/reset with dbk_rb_debug()): slot 3 = MMA thread
 // [drained accumulator, A window, weight stage, loop total]; slot 4 =
@@ -410,6 +435,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
     if (sink == 1.2345e-30f) *own = 0;
     return;
   }
+  int32_t bad = 0;  // range / non-finite code of this lane's outputs
 #pragma unroll 2
   for (int cb = 0; cb < kChunks; ++cb) {
     float v[kChunk];
@@ -423,6 +449,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
       float o[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) o[k] = pe.valid ? fmaxf(x[k] + bias[k], 0.f) : 0.f;
+      bad = merge_code(bad, range_code(o));
       const int64_t off = static_cast<int64_t>(cb * kChunk + 8 * m) << 7;
       if (KIND == 1) {
         uint4 pk;
@@ -477,6 +504,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
       }
     }
   }
+  if (bad) atomicCAS(P.err, 0, bad);  // the first error wins (rare path)
 }
 
 // --------------------------------------------------------------- kernel
@@ -1012,7 +1040,8 @@ __global__ void __launch_bounds__(256) k_rb_gather(const GatherTask* __restrict_
                                                    const int32_t* __restrict__ n_tasks, int32_t list,
                                                    int32_t step, int64_t task_cap,
                                                    uint8_t* __restrict__ stage_x, uint8_t* __restrict__ stage_lo,
-                                                   uint8_t* __restrict__ stage_cat, int64_t ps) {
+                                                   uint8_t* __restrict__ stage_cat, int64_t ps,
+                                                   int32_t* __restrict__ err) {
   constexpr int kPer = 2 * kImg * 8;  // chunks × image positions (pads written as zeros) × planes
   const int64_t nt = min(static_cast<int64_t>(n_tasks[list]), task_cap);
   const GatherTask* T = tasks + list * task_cap;
@@ -1033,6 +1062,9 @@ __global__ void __launch_bounds__(256) k_rb_gather(const GatherTask* __restrict_
       const float4 a = __ldg(reinterpret_cast<const float4*>(sp));
       const float4 b = __ldg(reinterpret_cast<const float4*>(sp + 4));
       const float o[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      // inputs must be finite (src/executor.cpp:107) and within fp16 range
+      const int32_t bad = range_code(o);
+      if (bad) atomicCAS(err, 0, bad);
       split_f16x8(o, h, l);
     }
     *reinterpret_cast<uint4*>((t.buf == 0 ? stage_x : stage_cat) + off) = h;
@@ -1126,10 +1158,10 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
 
 extern "C" int dbk_rb_gather(const void* tasks, const int32_t* n_tasks, int32_t list, int32_t step,
                              int64_t task_cap, void* stage_x, void* stage_lo, void* stage_cat, int64_t plane_stride,
-                             int32_t blocks, void* stream) {
+                             int32_t* err, int32_t blocks, void* stream) {
   k_rb_gather<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const GatherTask*>(tasks), n_tasks, list, step, task_cap, static_cast<uint8_t*>(stage_x),
-      static_cast<uint8_t*>(stage_lo), static_cast<uint8_t*>(stage_cat), plane_stride);
+      static_cast<uint8_t*>(stage_lo), static_cast<uint8_t*>(stage_cat), plane_stride, err);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -1181,7 +1213,8 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
                            int64_t plane_stride, const void* const* w0, const void* const* w1,
                            const void* const* w2, const float* const* b0, const float* const* b1,
                            const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
-                           int32_t* step_done, int32_t* queue, int32_t tile_m, int32_t num_sms, void* stream) {
+                           int32_t* step_done, int32_t* queue, int32_t* err, int32_t tile_m, int32_t num_sms,
+                           void* stream) {
   if (tile_m != 256 && tile_m != 128) return static_cast<int>(cudaErrorInvalidValue);
   dbk_rb_configure();
   StepParams p{};
@@ -1225,6 +1258,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
   p.done1 = done1;
   p.step_done = step_done;
   p.queue = queue;
+  p.err = err;
   // persistent: one CTA per SM, in clusters of kCluster
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(num_sms / kCluster * kCluster));

@@ -115,26 +115,28 @@ class EpExchange:
 
 
 class MoeEpLayer:
-    """One rank of the expert-parallel MoE layer on the B200 (bf16 tcgen05
-    grouped GEMMs, db_moe_ep_*). Collectives are issued on the session's
+    """One rank of the expert-parallel MoE layer on the B200 (tcgen05
+    grouped GEMMs with fp16 or bf16 operands, db_moe_ep_*). Collectives are issued on the session's
     stream, so the kernels and the exchange stay ordered without host syncs
     beyond the two count reads."""
 
-    def __init__(self, experts, k, batch, data_dim, hidden, seed=0, group=None):
+    def __init__(self, experts, k, batch, data_dim, hidden, seed=0, group=None, precision=None):
         import torch
         import torch.distributed as dist
 
-        from . import MoeEpSession
+        from . import MOE_BF16, MOE_FP16, MoeEpSession
+        precision = MOE_FP16 if precision is None else precision
+        self.dtype = torch.bfloat16 if precision == MOE_BF16 else torch.float16
         self.torch = torch
         init = dist.is_available() and dist.is_initialized()
         self.rank = dist.get_rank(group) if init else 0
         self.world = dist.get_world_size(group) if init else 1
-        self.sess = MoeEpSession(experts, k, batch, data_dim, hidden, seed, self.rank, self.world)
+        self.sess = MoeEpSession(experts, k, batch, data_dim, hidden, seed, self.rank, self.world, precision)
         dev = torch.device("cuda", torch.cuda.current_device())
         self.stream = torch.cuda.ExternalStream(self.sess.stream, device=dev)
         self.ex = EpExchange(self.world, experts, device=dev, group=group)
         self.d, self.dev = data_dim, dev
-        self.send = torch.empty((self.sess.items, data_dim), dtype=torch.bfloat16, device=dev)
+        self.send = torch.empty((self.sess.items, data_dim), dtype=self.dtype, device=dev)
         self.back = torch.empty_like(self.send)
         self.recv = self.ret = None
         self.last_recv_rows = 0
@@ -143,7 +145,7 @@ class MoeEpLayer:
     def _ensure(self, rows: int):
         if self.recv is None or self.recv.shape[0] < rows:
             cap = max(rows + rows // 4, 1)
-            self.recv = self.torch.empty((cap, self.d), dtype=self.torch.bfloat16, device=self.dev)
+            self.recv = self.torch.empty((cap, self.d), dtype=self.dtype, device=self.dev)
             self.ret = self.torch.empty_like(self.recv)
 
     def forward(self, chunks: int = 1):

@@ -45,6 +45,32 @@ IEP = {
 }
 
 
+def moe_routing(T, n, k):
+    s = np.zeros((T, n))
+    O.ref().refshim_moe_inputs(T, n, 1, 0, None, s.ctypes.data_as(O.P_F64))
+    ids, w = O.topk(s, k, use_ref=True)
+    counts = np.bincount(ids.ravel(), minlength=n)
+    return {"T": T, "n": n, "k": k,
+            "routing_fnv": "%016x" % O.fnv1a64(ids.astype(np.int32).tobytes()),
+            "weights_fnv": "%016x" % O.fnv1a64(w.tobytes()),
+            "scores_fnv": "%016x" % O.fnv1a64(s.tobytes()),
+            "rows_min": int(counts.min()), "rows_max": int(counts.max()),
+            "occupied": int(np.count_nonzero(counts))}
+
+
+def cfg5_full():
+    """Full-T cfg5 routing (T = 1,048,576, n = 1024, k = 4; 8.6 GB of fp64
+    scores) from the compiled reference, merged into fingerprints.json:
+        python tests/golden/make_golden.py cfg5"""
+    path = os.path.join(HERE, "fingerprints.json")
+    with open(path) as f:
+        out = json.load(f)
+    out["moe"]["cfg5"] = moe_routing(1048576, 1024, 4)
+    print("cfg5", out["moe"]["cfg5"], flush=True)
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 def main():
     out = {"iep": {}, "moe": {}}
     for name, c in IEP.items():
@@ -71,18 +97,10 @@ def main():
         out["iep"][name] = entry
         print(name, entry["improved"], flush=True)
 
-    # MoE routing (cfg4 full; cfg5 routing is checked on a token slice).
+    # MoE routing (cfg4 full, a cfg5 token slice; the full-T cfg5 entry is
+    # added by cfg5_full(), which needs 8.6 GB for the scores).
     for name, (T, n, k) in {"cfg4": (65536, 64, 2), "cfg5_slice": (16384, 1024, 4)}.items():
-        x, s = np.zeros((1, 1)), np.zeros((T, n))
-        O.ref().refshim_moe_inputs(T, n, 1, 0, None, s.ctypes.data_as(O.P_F64))
-        ids, w = O.topk(s, k, use_ref=True)
-        counts = np.bincount(ids.ravel(), minlength=n)
-        out["moe"][name] = {"T": T, "n": n, "k": k,
-                            "routing_fnv": "%016x" % O.fnv1a64(ids.astype(np.int32).tobytes()),
-                            "weights_fnv": "%016x" % O.fnv1a64(w.tobytes()),
-                            "scores_fnv": "%016x" % O.fnv1a64(s.tobytes()),
-                            "rows_min": int(counts.min()), "rows_max": int(counts.max()),
-                            "occupied": int(np.count_nonzero(counts))}
+        out["moe"][name] = moe_routing(T, n, k)
         print(name, out["moe"][name], flush=True)
 
     with open(os.path.join(HERE, "fingerprints.json"), "w") as f:
@@ -114,4 +132,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "cfg5":
+        cfg5_full()
+    else:
+        main()

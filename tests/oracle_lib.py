@@ -49,6 +49,7 @@ def oracle():
         lib.orc_gen_batch.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double,
                                       C.c_uint64, P_I32, P_I32, P_I32, P_I32, P_I32]
         lib.orc_random_batch.argtypes = [C.c_int64, C.c_int64, C.c_uint64, P_F64]
+        lib.orc_random_rows.argtypes = [P_I64, C.c_int64, C.c_int64, C.c_uint64, P_F64]
         lib.orc_labels.argtypes = [C.c_int64, P_I32, P_I32, P_I32, P_I32, P_I32, P_I32]
         lib.orc_schedule_improved.argtypes = [C.c_int64, C.c_int, P_I32, P_I32, P_I32, P_I32, P_I32,
                                               P_I64, P_I32, P_I32, P_I32, P_I32, P_I32]
@@ -156,6 +157,16 @@ def ref_gen_batch(kind, b, p=40, width=1, depth=4, length=16, bp=0.1, seed=0, wi
 def random_batch(rows, width, seed) -> np.ndarray:
     out = np.empty((rows, width), np.float64)
     oracle().orc_random_batch(rows, width, seed, _ptr(out, P_F64))
+    return out
+
+
+def random_rows(rows, width, seed) -> np.ndarray:
+    """Rows `rows` (ascending) of random_batch(·, width, seed), generated in
+    one pass without the rows in between."""
+    r = np.ascontiguousarray(rows, np.int64)
+    assert np.all(np.diff(r) > 0)
+    out = np.zeros((len(r), width), np.float64)
+    oracle().orc_random_rows(_ptr(r, P_I64), len(r), width, seed, _ptr(out, P_F64))
     return out
 
 

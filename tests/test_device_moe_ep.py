@@ -3,7 +3,7 @@
 G ranks are stood in for by G sessions in one process, run stage by stage.
 The all-to-alls are concatenations of the row blocks on the device, and no
 kernel of one session waits on another. Every rank's outputs must be
-bit-identical to the single-GPU bf16 layer (MoeSession) on the same token
+bit-identical to the single-GPU tensor-core layer (MoeSession, same precision) on the same token
 slice: each output row depends only on its own row of the grouped GEMMs,
 whichever rank or tile computes it.
 """
@@ -18,11 +18,11 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-def _loopback(n, k, T, d, h, seed, G, chunks=0):
+def _loopback(n, k, T, d, h, seed, G, chunks=0, precision=db.MOE_FP16):
     dev = torch.device("cuda", 0)
-    sess = [db.MoeEpSession(n, k, T, d, h, seed, r, G) for r in range(G)]
+    sess = [db.MoeEpSession(n, k, T, d, h, seed, r, G, precision) for r in range(G)]
     E = n // G
-    send = [torch.empty((s.items, d), dtype=torch.bfloat16, device=dev) for s in sess]
+    send = [torch.empty((s.items, d), dtype=torch.float16, device=dev) for s in sess]
     counts = [s.dispatch(send[r].data_ptr()) for r, s in enumerate(sess)]  # synchronises
     starts = [np.concatenate([[0], np.cumsum(split_rows(c, G))]) for c in counts]
     recv, cnts = [], []
@@ -55,11 +55,12 @@ def _loopback(n, k, T, d, h, seed, G, chunks=0):
     return outs, cnts
 
 
-@pytest.mark.parametrize("G", [1, 2, 4, 8])
-def test_ep_stages_equal_single_gpu_layer(G):
+@pytest.mark.parametrize("G,precision", [(1, db.MOE_FP16), (2, db.MOE_FP16), (4, db.MOE_FP16), (8, db.MOE_FP16),
+                                         (2, db.MOE_BF16)])
+def test_ep_stages_equal_single_gpu_layer(G, precision):
     n, k, T, d, h, seed = 16, 2, 1024, 256, 512, 5
-    outs, cnts = _loopback(n, k, T, d, h, seed, G)
-    full = db.MoeSession(n, k, T, d, h, seed=seed, precision=db.MOE_BF16)
+    outs, cnts = _loopback(n, k, T, d, h, seed, G, precision=precision)
+    full = db.MoeSession(n, k, T, d, h, seed=seed, precision=precision)
     full.forward()
     ref = full.run().outputs()
     Tl = T // G
@@ -88,7 +89,7 @@ def test_ep_counts_follow_reference_routing():
     sess = [db.MoeEpSession(n, k, T, d, h, seed, r, G) for r in range(G)]
     Tl = T // G
     for r, se in enumerate(sess):
-        buf = torch.empty((se.items, d), dtype=torch.bfloat16, device="cuda")
+        buf = torch.empty((se.items, d), dtype=torch.float16, device="cuda")
         c = se.dispatch(buf.data_ptr())
         np.testing.assert_array_equal(c, np.bincount(ids[r * Tl:(r + 1) * Tl].reshape(-1), minlength=n))
 
@@ -99,7 +100,7 @@ def test_moe_ep_layer_world1_equals_session():
     layer = MoeEpLayer(n, k, T, d, h, seed)
     layer.forward()
     out = layer.outputs()
-    full = db.MoeSession(n, k, T, d, h, seed=seed, precision=db.MOE_BF16)
+    full = db.MoeSession(n, k, T, d, h, seed=seed, precision=db.MOE_FP16)
     full.forward()
     np.testing.assert_array_equal(out, full.run().outputs().astype(np.float32))
     layer.force_exchange = True  # the exchange code paths as loopbacks at world 1

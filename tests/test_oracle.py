@@ -150,3 +150,23 @@ def test_bench_seed_helper_matches_the_reference_mix_seed():
     import bench
     for seed, stream in ((0, 0xd00d), (7, 0x1127), (123456789, 0xe4be27)):
         assert bench._mix_seed(seed, stream) == O.mix_seed(seed, stream)
+
+
+def test_random_rows_equals_random_batch_rows():
+    x = O.random_batch(700, 333, 11)
+    rows = [0, 1, 2, 300, 311, 312, 699]
+    assert np.array_equal(O.random_rows(rows, 333, 11), x[rows])
+
+
+def test_moe_sampled_tokens_equal_full_forward():
+    """tests/moe_full.reference_tokens (sampled tokens, per-expert numpy fp64)
+    agrees with the restated moe_forward_batched on every token."""
+    import moe_full as M
+    n, k, T, d, h, seed = 12, 3, 90, 16, 24, 4
+    xi, sc = O.moe_inputs(T, n, d, seed)
+    ids, w = O.topk(sc, k)
+    ref, _, _ = O.moe_forward(xi, ids, w, n, h, O.mix_seed(seed, 0xe4be27))
+    toks = M.sample_tokens(T, 17)
+    sids, sw, out = M.reference_tokens(n, k, d, h, seed, toks)
+    assert np.array_equal(sids, ids[toks]) and np.array_equal(sw, w[toks])
+    assert np.max(np.abs(out - ref[toks])) <= 1e-12
