@@ -258,15 +258,17 @@ def calibrate_cpu(cfg, target_s):
     return threads, threads * rounds
 
 
-def pcie_duplex_seconds(nbytes, reps=3):
-    """Seconds per simultaneous H2D + D2H of nbytes each (pinned host
-    buffers, two streams): the e2e pipeline's bound on this box."""
+def pcie_duplex_seconds(nbytes, nbytes_out=None, reps=3):
+    """Seconds per simultaneous H2D of nbytes + D2H of nbytes_out (default
+    the same; pinned host buffers, two streams): the e2e pipeline's bound on
+    this box."""
     import torch
     n = nbytes // 4
+    m = (nbytes if nbytes_out is None else nbytes_out) // 4
     h_in = torch.empty(n, dtype=torch.float32).pin_memory()
-    h_out = torch.empty(n, dtype=torch.float32).pin_memory()
+    h_out = torch.empty(m, dtype=torch.float32).pin_memory()
     d_in = torch.empty(n, dtype=torch.float32, device="cuda")
-    d_out = torch.empty(n, dtype=torch.float32, device="cuda")
+    d_out = torch.empty(m, dtype=torch.float32, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
     best = float("inf")
     for _ in range(reps + 1):
@@ -515,21 +517,37 @@ def run_moe(args, dist, name, secondary=False):
                        for c_, name_ in ((3, "gate+sort+dispatch"), (4, "gemm1_relu"), (5, "gemm2"),
                                          (6, "combine")) if kt.launches[c_]},
            "gpu_launches_per_step": int(st.kernel_launches)}
-    # end-to-end: host fp32 inputs + fp64 scores → outputs
-    xin = db.PinnedArray((T, c["d"]), np.float32)
-    sc = db.PinnedArray((T, c["experts"]), np.float64)
-    yout = db.PinnedArray((T, c["d"]), np.float32)
+    # end-to-end through the public API: pinned host fp32 inputs + fp64
+    # scores → H2D → gate / dispatch / GEMMs / combine → D2H of the fp32
+    # outputs, every step; the pipelined call overlaps step i's forward with
+    # step i+1's upload and step i−1's download. Two input sets alternate.
+    xin = [db.PinnedArray((T, c["d"]), np.float32) for _ in range(2)]
+    sc = [db.PinnedArray((T, c["experts"]), np.float64) for _ in range(2)]
+    yout = [db.PinnedArray((T, c["d"]), np.float32) for _ in range(2)]
     rng = np.random.default_rng(dist.rank)
-    xin.array[:] = rng.uniform(-1, 1, size=(T, c["d"])).astype(np.float32)
-    sc.array[:] = rng.uniform(-1, 1, size=(T, c["experts"]))
-    sess.forward_host(xin.array, sc.array, yout.array)
+    for i in range(2):
+        xin[i].array[:] = rng.uniform(-1, 1, size=(T, c["d"])).astype(np.float32)
+        sc[i].array[:] = rng.uniform(-1, 1, size=(T, c["experts"]))
+
+    def e2e_pass(steps):
+        for i in range(steps):
+            sess.forward_host_async(xin[i % 2].array, sc[i % 2].array, yout[i % 2].array)
+        sess.synchronize()
+
+    e2e_pass(3)
+    dist.barrier()
+    e2e_steps = max(args.steps, 40)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        sess.forward_host(xin.array, sc.array, yout.array)
-    e2e_s = dist.max((time.perf_counter() - t0) / args.steps)
-    res["e2e"] = {"value": TG / e2e_s, "unit": "tokens/s",
-                  "h2d_bytes_per_step": T * (c["d"] * 4 + c["experts"] * 8),
-                  "d2h_bytes_per_step": T * c["d"] * 4}
+    e2e_pass(e2e_steps)
+    e2e_s = dist.max((time.perf_counter() - t0) / e2e_steps)
+    h2d, d2h = T * (c["d"] * 4 + c["experts"] * 8), T * c["d"] * 4
+    link_s = pcie_duplex_seconds(h2d, d2h)
+    res["e2e"] = {"value": TG / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                  "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
+                  "api": "db_moe_session_forward_host_async (pinned fp32 inputs + fp64 scores in, fp32 outputs out; "
+                         "copies overlap the neighbouring steps' forwards)",
+                  "roofline": {"bound": "pcie (H2D and D2H concurrent)", "achieved_h2d_gbs": round(h2d / e2e_s / 1e9, 1),
+                               "peak_h2d_gbs": round(h2d / link_s / 1e9, 1), "frac": round(link_s / e2e_s, 4)}}
     return res
 
 
@@ -555,11 +573,12 @@ def run_moe_ep(args, dist, name):
     layer.sess.synchronize()
     dist.barrier()
     t0 = time.time()
+    stream = torch.cuda.ExternalStream(layer.sess.stream, device=torch.device("cuda", dist.local))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(layer.stream)
+    e0.record(stream)
     for _ in range(args.steps):
         layer.forward(chunks)
-    e1.record(layer.stream)
+    e1.record(stream)
     e1.synchronize()
     dist.barrier()
     clk.mark(t0, time.time())

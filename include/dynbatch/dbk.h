@@ -213,6 +213,8 @@ int dbk_moe_tc_combine(int32_t fmt, int64_t T, int32_t k, int32_t d, const doubl
  * epilogue uses to write its rows back in receive order (out_row). */
 int dbk_moe_ep_pack(int32_t fmt, int64_t items, int32_t k, int32_t d, const int32_t* order, const float* x,
                     void* send, int32_t* pos_of_item, int32_t blocks, void* stream);
+/* counts[e] = offsets[e+1] − offsets[e]: rows per global expert (sends). */
+int dbk_moe_ep_counts(int32_t n, const int32_t* offsets, int32_t* counts, void* stream);
 int dbk_moe_ep_layout(int32_t G, int32_t E, const int32_t* cnt, int32_t* pstart, int32_t* tile_expert,
                       int32_t* tile_rb, int32_t* n_tiles, int32_t* src_row, int32_t* cum, void* stream);
 int dbk_moe_ep_scatter(int32_t G, int32_t E, int32_t d, const int32_t* pstart, const int32_t* tile_expert,

@@ -164,6 +164,11 @@ DYNBATCH_API db_status db_moe_session_forward(db_moe_session* s);
 /* End-to-end: host fp32 inputs [T×d] and fp64 scores [T×n] → outputs fp32. */
 DYNBATCH_API db_status db_moe_session_forward_host(db_moe_session* s, const float* inputs,
                                                    const double* scores, float* outputs);
+/* Pipelined form (pinned host buffers, three calls in flight, uploads and
+ * downloads on their own streams overlapping the neighbouring calls'
+ * forwards); the buffers stay in use until db_moe_session_synchronize. */
+DYNBATCH_API db_status db_moe_session_forward_host_async(db_moe_session* s, const float* inputs,
+                                                         const double* scores, float* outputs);
 DYNBATCH_API db_status db_moe_session_synchronize(db_moe_session* s);
 DYNBATCH_API void* db_moe_session_stream(db_moe_session* s);
 DYNBATCH_API db_status db_moe_session_stats(db_moe_session* s, db_session_stats_t* out);
@@ -216,6 +221,27 @@ DYNBATCH_API db_status db_moe_ep_forward_local(db_moe_ep_session* s);
 DYNBATCH_API db_status db_moe_ep_experts_range(db_moe_ep_session* s, const void* recv_rows, void* ret_rows,
                                                int32_t e_begin, int32_t e_end);
 DYNBATCH_API db_status db_moe_ep_combine(db_moe_ep_session* s, const void* ret_rows);
+/* The whole layer with the exchange inside the library, on NCCL over
+ * NVLink: rank 0 makes a 128-byte id (db_moe_ep_nccl_id), the caller passes
+ * it to every rank out of band, each rank joins (db_moe_ep_comm_init), then
+ * db_moe_ep_forward runs gate → sort → count all-to-all → pack → per
+ * expert range: rows out, grouped GEMMs, rows back → combine, the exchange
+ * of range c+1 overlapping the GEMMs of range c (chunks ranges; 1 = no
+ * overlap). At world 1 without a communicator it is forward_local.
+ * NCCL (libnccl.so.2) is loaded at the first of these calls. */
+DYNBATCH_API db_status db_moe_ep_nccl_id(void* unique_id /* 128 bytes */);
+DYNBATCH_API db_status db_moe_ep_comm_init(db_moe_ep_session* s, const void* unique_id);
+DYNBATCH_API db_status db_moe_ep_forward(db_moe_ep_session* s, int32_t chunks);
+/* Rows this rank's experts received in the last forward. */
+DYNBATCH_API db_status db_moe_ep_recv_rows(db_moe_ep_session* s, int64_t* rows);
+/* The exchange plan (host only): send_counts[G·E] (rows this rank sends per
+ * global expert), recv_counts[G][E] (rows each source sends per local
+ * expert) → *n_chunks = C expert ranges and, per range c and peer q
+ * ([C][G], caller-sized for min(chunks, E) ranges), the row offset and
+ * count of the send piece and of the receive piece. */
+DYNBATCH_API db_status db_moe_ep_plan(int32_t G, int32_t E, const int32_t* send_counts, const int32_t* recv_counts,
+                                      int32_t chunks, int32_t* n_chunks, int64_t* send_off, int64_t* send_rows,
+                                      int64_t* recv_off, int64_t* recv_rows);
 DYNBATCH_API db_status db_moe_ep_outputs(db_moe_ep_session* s, float* out);
 DYNBATCH_API db_status db_moe_ep_synchronize(db_moe_ep_session* s);
 DYNBATCH_API void* db_moe_ep_stream(db_moe_ep_session* s);

@@ -160,6 +160,7 @@ SIGNATURES = {
     "db_moe_session_forward": (C.c_int32, [VP]),
     "db_moe_session_forward_host": (C.c_int32, [VP, VP, VP, VP]),
     "db_moe_session_synchronize": (C.c_int32, [VP]),
+    "db_moe_session_forward_host_async": (C.c_int32, [VP, VP, VP, VP]),
     "db_moe_session_stream": (VP, [VP]),
     "db_moe_session_stats": (C.c_int32, [VP, C.POINTER(SessionStats)]),
     "db_moe_session_routing": (C.c_int32, [VP, VP, VP, VP, VP]),
@@ -178,6 +179,11 @@ SIGNATURES = {
     "db_moe_ep_synchronize": (C.c_int32, [VP]),
     "db_moe_ep_stream": (VP, [VP]),
     "db_moe_ep_free": (None, [VP]),
+    "db_moe_ep_nccl_id": (C.c_int32, [VP]),
+    "db_moe_ep_comm_init": (C.c_int32, [VP, VP]),
+    "db_moe_ep_forward": (C.c_int32, [VP, C.c_int32]),
+    "db_moe_ep_recv_rows": (C.c_int32, [VP, C.POINTER(C.c_int64)]),
+    "db_moe_ep_plan": (C.c_int32, [C.c_int32, C.c_int32, VP, VP, C.c_int32, C.POINTER(C.c_int32), VP, VP, VP, VP]),
     "db_moe_run_device": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, PVP]),
 }
 
@@ -193,7 +199,11 @@ def lib():
                               "(there is no CPU fallback)")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
-            fn = getattr(L, name)
+            fn = getattr(L, name, None)
+            if fn is None and "DYNBATCH_LIB" in os.environ:
+                continue  # an older build under A/B timing (profiles/ab_time.py)
+            if fn is None:
+                raise ImportError(f"{LIB_PATH} does not export {name}: rebuild it")
             fn.restype = res
             fn.argtypes = args
         _lib = L
@@ -507,6 +517,10 @@ class MoeSession(_Handle):
     def forward_host(self, inputs, scores, outputs):
         check(lib().db_moe_session_forward_host(self.h, _ptr(inputs), _ptr(scores), _ptr(outputs)))
 
+    def forward_host_async(self, inputs, scores, outputs):
+        """Pipelined forward_host (pinned buffers; results after synchronize())."""
+        check(lib().db_moe_session_forward_host_async(self.h, _ptr(inputs), _ptr(scores), _ptr(outputs)))
+
     def synchronize(self):
         check(lib().db_moe_session_synchronize(self.h))
 
@@ -588,6 +602,21 @@ class MoeEpSession(_Handle):
     def combine(self, ret_ptr: int):
         check(lib().db_moe_ep_combine(self.h, C.c_void_p(ret_ptr)))
 
+    def comm_init(self, unique_id: bytes):
+        """Join the ranks' NCCL communicator (id from moe_ep_nccl_id on rank 0)."""
+        buf = (C.c_char * 128).from_buffer_copy(bytes(unique_id))
+        check(lib().db_moe_ep_comm_init(self.h, buf))
+
+    def forward(self, chunks: int = 1):
+        """The whole layer, exchange on the library's NCCL communicator."""
+        check(lib().db_moe_ep_forward(self.h, chunks))
+
+    @property
+    def recv_rows(self) -> int:
+        r = C.c_int64()
+        check(lib().db_moe_ep_recv_rows(self.h, C.byref(r)))
+        return r.value
+
     def outputs(self) -> np.ndarray:
         out = np.zeros((self.tokens, self.d), np.float32)
         check(lib().db_moe_ep_outputs(self.h, _ptr(out)))
@@ -599,6 +628,25 @@ class MoeEpSession(_Handle):
     @property
     def stream(self) -> int:
         return lib().db_moe_ep_stream(self.h) or 0
+
+
+def moe_ep_nccl_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (ncclGetUniqueId), for rank 0."""
+    buf = (C.c_char * 128)()
+    check(lib().db_moe_ep_nccl_id(buf))
+    return bytes(buf)
+
+
+def moe_ep_plan(G, E, send_counts, recv_counts, chunks):
+    """The exchange plan (db_moe_ep_plan): (send_off, send_rows, recv_off,
+    recv_rows), each [C][G]."""
+    sc = np.ascontiguousarray(send_counts, np.int32).reshape(-1)
+    rc = np.ascontiguousarray(recv_counts, np.int32).reshape(-1)
+    cmax = max(1, min(int(chunks), int(E)))
+    outs = [np.zeros((cmax, G), np.int64) for _ in range(4)]
+    nc = C.c_int32()
+    check(lib().db_moe_ep_plan(G, E, _ptr(sc), _ptr(rc), chunks, C.byref(nc), *(_ptr(o) for o in outs)))
+    return tuple(o[:nc.value] for o in outs)
 
 
 def device_count() -> int:

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "device.hpp"
+#include "ep_nccl.hpp"
 #include "dynbatch.hpp"
 #include "dynbatch/dynbatch.h"
 #include "dynbatch/dynbatch_device.h"
@@ -574,6 +575,12 @@ db_status db_moe_session_forward_host(db_moe_session* s, const float* inputs, co
   return guarded([&] { s->s->forward_host(inputs, scores, outputs); });
 }
 
+db_status db_moe_session_forward_host_async(db_moe_session* s, const float* inputs, const double* scores,
+                                           float* outputs) {
+  if (!s || !inputs || !scores || !outputs) return null_arg();
+  return guarded([&] { s->s->forward_host_async(inputs, scores, outputs); });
+}
+
 db_status db_moe_session_synchronize(db_moe_session* s) {
   if (!s) return null_arg();
   return guarded([&] { s->s->synchronize(); });
@@ -619,6 +626,48 @@ db_status db_moe_ep_create(const db_moe_opts* opts, int32_t precision, int32_t r
   return guarded([&] {
     auto s = std::make_unique<dynbatch::dev::MoeEp>(to_cfg(opts), opts->seed, precision, rank, world);
     *out = new db_moe_ep_session{std::move(s)};
+  });
+}
+
+db_status db_moe_ep_nccl_id(void* unique_id) {
+  if (!unique_id) return null_arg();
+  return guarded([&] {
+    const dynbatch::dev::Nccl& nc = dynbatch::dev::Nccl::get();
+    ncclUniqueId id;
+    nc.check(nc.GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(unique_id, &id, sizeof(id));
+  });
+}
+
+db_status db_moe_ep_comm_init(db_moe_ep_session* s, const void* unique_id) {
+  if (!s || !unique_id) return null_arg();
+  return guarded([&] { s->s->comm_init(unique_id); });
+}
+
+db_status db_moe_ep_forward(db_moe_ep_session* s, int32_t chunks) {
+  if (!s) return null_arg();
+  return guarded([&] { s->s->forward(chunks); });
+}
+
+db_status db_moe_ep_recv_rows(db_moe_ep_session* s, int64_t* rows) {
+  if (!s || !rows) return null_arg();
+  *rows = s->s->last_recv_rows();
+  return DB_OK;
+}
+
+db_status db_moe_ep_plan(int32_t G, int32_t E, const int32_t* send_counts, const int32_t* recv_counts,
+                         int32_t chunks, int32_t* n_chunks, int64_t* send_off, int64_t* send_rows,
+                         int64_t* recv_off, int64_t* recv_rows) {
+  if (!send_counts || !recv_counts || !n_chunks) return null_arg();
+  return guarded([&] {
+    if (G < 1 || E < 1) dynbatch::throw_error(dynbatch::Errc::invalid_argument, "G and E must be positive");
+    const dynbatch::dev::EpPlan p = dynbatch::dev::make_ep_plan(G, E, send_counts, recv_counts, chunks);
+    *n_chunks = p.C;
+    const size_t cg = static_cast<size_t>(p.C) * G;
+    if (send_off) std::copy(p.s_off.begin(), p.s_off.begin() + cg, send_off);
+    if (send_rows) std::copy(p.s_rows.begin(), p.s_rows.begin() + cg, send_rows);
+    if (recv_off) std::copy(p.r_off.begin(), p.r_off.begin() + cg, recv_off);
+    if (recv_rows) std::copy(p.r_rows.begin(), p.r_rows.begin() + cg, recv_rows);
   });
 }
 

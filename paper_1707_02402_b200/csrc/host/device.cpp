@@ -725,8 +725,10 @@ void IepSession::check_errors() {
   switch (e) {
     case 0: return;
     case 7: throw_error(Errc::missing_operand, "a call group read a node that was not yet computed");
-    case 9: throw_error(Errc::non_finite_value, "a module produced non-finite rows");
-    case 10: throw_error(Errc::non_finite_value, "a value exceeds the fp16 operand range of the conv kernels (|x| > 65504)");
+    case 9: throw_error(Errc::non_finite_value, "a module produced non-finite rows (or rows beyond the fp16 operand "
+                                                "range of the conv kernels)");
+    case 10: throw_error(Errc::non_finite_value, "an input is non-finite or beyond the fp16 operand range of the conv "
+                                                 "kernels (|x| > 65504)");
     case 14: throw_error(Errc::single_assignment_violation, "a node was written twice");
     default: throw std::runtime_error("device executor error " + std::to_string(e));
   }

@@ -314,6 +314,10 @@ class MoeSession {
   ~MoeSession();
   void forward();
   void forward_host(const float* inputs, const double* scores, float* outputs);
+  // Pipelined host call: returns once queued; the pinned buffers must stay
+  // untouched until synchronize() (three calls in flight, copies on their
+  // own streams overlapping the neighbouring calls' forwards).
+  void forward_host_async(const float* inputs, const double* scores, float* outputs);
   void synchronize();
   cudaStream_t stream() const { return stream_; }
   void routing(std::int32_t* ids, double* weights, std::int32_t* offsets, std::int32_t* items);
@@ -331,6 +335,7 @@ class MoeSession {
   Profiler prof_;
 
  private:
+  void forward_from(const float* x, const double* scores, float* out);
   struct Impl;
   std::unique_ptr<Impl> impl_;
   cudaStream_t stream_ = nullptr;
@@ -339,9 +344,10 @@ class MoeSession {
 };
 
 // Expert-parallel MoE rank: tokens [rank·T/G, (rank+1)·T/G),
-// experts [rank·n/G, (rank+1)·n/G), bf16 tcgen05 grouped GEMMs. The caller
-// exchanges the packed rows between dispatch/experts and experts/combine
-// (NCCL all-to-allv over NVLink through torch.distributed).
+// experts [rank·n/G, (rank+1)·n/G), 16-bit tcgen05 grouped GEMMs. forward()
+// runs the whole layer with the exchange on the library's own NCCL
+// communicator; the staged calls (dispatch / experts / combine) leave the
+// exchange to the caller.
 class MoeEp {
  public:
   MoeEp(const MoeConfig& cfg, std::uint64_t seed, int precision, int rank, int world);
@@ -362,6 +368,14 @@ class MoeEp {
   void layout(const std::int32_t* cnt);
   // World 1: the whole layer in one device pass (no exchange, no pack).
   void forward_local();
+  // NCCL communicator of the G ranks (ncclCommInitRank; the 128-byte unique
+  // id comes from rank 0's nccl_unique_id, passed out of band).
+  void comm_init(const void* unique_id);
+  // One forward with the exchange on NCCL, local experts cut into `chunks`
+  // ranges whose transfers overlap the GEMMs (world 1 without a
+  // communicator: forward_local).
+  void forward(int chunks);
+  std::int64_t last_recv_rows() const { return last_recv_rows_; }
   void experts_range(const void* recv, void* ret, int e_begin, int e_end);
   // ret_recv = the rank's own rows back, in its sorted order → outputs.
   void combine(const void* ret_recv);
@@ -375,6 +389,7 @@ class MoeEp {
   std::unique_ptr<Impl> impl_;
   cudaStream_t stream_ = nullptr;
   std::int64_t T_ = 0;
+  std::int64_t last_recv_rows_ = 0;
 };
 
 }  // namespace dynbatch::dev

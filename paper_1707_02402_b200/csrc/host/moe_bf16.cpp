@@ -142,13 +142,15 @@ void MoeBf16::upload_inputs(const float* x, cudaStream_t s) {
 }
 
 int MoeBf16::forward(const std::int32_t* ids, const double* wts, const std::int32_t* order,
-                     const std::int32_t* offsets, cudaStream_t s, Profiler* prof) {
+                     const std::int32_t* offsets, cudaStream_t s, Profiler* prof, const float* x, float* out) {
   Impl& I = *impl_;
+  if (!x) x = I.x.get();
+  if (!out) out = I.out.get();
   const int blocks = I.sms * 8;
   if (prof) prof->begin(3, s);
   check(dbk_moe_tc_layout(I.n, offsets, I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(), I.n_tiles.get(), s),
         "moe layout");
-  check(dbk_moe_tc_dispatch(I.fmt, I.T, I.k, I.d, order, ids, offsets, I.pstart.get(), I.x.get(), I.A.get(),
+  check(dbk_moe_tc_dispatch(I.fmt, I.T, I.k, I.d, order, ids, offsets, I.pstart.get(), x, I.A.get(),
                               I.row_of_item.get(), blocks, s),
         "moe dispatch");
   if (prof) prof->end(s);
@@ -163,7 +165,7 @@ int MoeBf16::forward(const std::int32_t* ids, const double* wts, const std::int3
         "moe gemm2");
   if (prof) prof->end(s);
   if (prof) prof->begin(6, s);
-  check(dbk_moe_tc_combine(I.fmt, I.T, I.k, I.d, wts, I.row_of_item.get(), I.Y.get(), I.out.get(), s), "moe combine");
+  check(dbk_moe_tc_combine(I.fmt, I.T, I.k, I.d, wts, I.row_of_item.get(), I.Y.get(), out, s), "moe combine");
   if (prof) prof->end(s);
   return 5;
 }

@@ -24,8 +24,11 @@ class MoeBf16 {
   ~MoeBf16();
   void upload_inputs(const float* x, cudaStream_t s);
   // Dispatch → GEMM1+ReLU → GEMM2 → combine; returns kernels launched.
+  // x / out: device rows to read / write instead of the session's own
+  // (the pipelined host path's per-call slots); null = the session's.
   int forward(const std::int32_t* ids, const double* wts, const std::int32_t* order,
-              const std::int32_t* offsets, cudaStream_t s, Profiler* prof);
+              const std::int32_t* offsets, cudaStream_t s, Profiler* prof, const float* x = nullptr,
+              float* out = nullptr);
   void download_outputs(float* out, cudaStream_t s);
   float* inputs_device();
   const float* outputs_device() const;

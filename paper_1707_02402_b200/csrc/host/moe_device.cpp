@@ -11,6 +11,7 @@
 
 #include "device.hpp"
 #include "dynbatch/dbk.h"
+#include "ep_nccl.hpp"
 #include "moe_bf16.hpp"
 
 namespace dynbatch {
@@ -58,9 +59,9 @@ struct MoeDev {
     w1tab.upload(t1, s);
     w2tab.upload(t2, s);
   }
-  void gate(cudaStream_t s) {
+  void gate(cudaStream_t s, const double* sc = nullptr) {
     check(cudaMemsetAsync(err.get(), 0, 16, s), "memset");
-    check(dbk_moe_topk(T, n, k, scores.get(), ids.get(), wts.get(), err.get(), s), "dbk_moe_topk");
+    check(dbk_moe_topk(T, n, k, sc ? sc : scores.get(), ids.get(), wts.get(), err.get(), s), "dbk_moe_topk");
   }
   void sort(cudaStream_t s) {
     check(dbk_stable_bucket_sort(T * k, n, ids.get(), seg_hist.get(), order.get(), offsets.get(), s),
@@ -152,7 +153,28 @@ struct MoeSession::Impl {
   int precision = 0;
   MoeDev dev;
   std::unique_ptr<MoeBf16> bf16;
-  std::vector<float> host_in;  // for e2e tests
+  // Pipelined host calls (forward_host_async): kDepth calls in flight, each
+  // with its own device input / score / output slots; uploads on h2d,
+  // downloads on d2h, so call i's forward overlaps call i+1's upload and
+  // call i−1's download (full-duplex PCIe).
+  struct Pipe {
+    static constexpr int kDepth = 3;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    Buf<float> x[kDepth], out[kDepth];
+    Buf<double> sc[kDepth];
+    cudaEvent_t h2d_done[kDepth] = {}, in_free[kDepth] = {}, out_ready[kDepth] = {}, out_free[kDepth] = {};
+    std::uint64_t calls = 0;
+    ~Pipe() {
+      if (h2d) cudaStreamSynchronize(h2d);
+      if (d2h) cudaStreamSynchronize(d2h);
+      for (int k = 0; k < kDepth; ++k)
+        for (cudaEvent_t e : {h2d_done[k], in_free[k], out_ready[k], out_free[k]})
+          if (e) cudaEventDestroy(e);
+      if (h2d) cudaStreamDestroy(h2d);
+      if (d2h) cudaStreamDestroy(d2h);
+    }
+  };
+  std::unique_ptr<Pipe> pipe;
 };
 
 MoeSession::MoeSession(const MoeConfig& cfg_in, std::uint64_t seed, int precision,
@@ -195,11 +217,13 @@ MoeSession::~MoeSession() {
   }
 }
 
-void MoeSession::forward() {
+void MoeSession::forward() { forward_from(nullptr, nullptr, nullptr); }
+
+void MoeSession::forward_from(const float* x, const double* scores, float* out) {
   MoeDev& D = impl_->dev;
   launches_ = 0;
   prof_.begin(3, stream_);
-  D.gate(stream_);
+  D.gate(stream_, scores);
   D.sort(stream_);
   prof_.end(stream_);
   launches_ += 1 + 6;  // top-k; histogram, 3-pass scan, offsets, stable scatter
@@ -213,7 +237,7 @@ void MoeSession::forward() {
     launches_ += 3 + 1;
   } else {
     launches_ += impl_->bf16->forward(D.ids.get(), D.wts.get(), D.order.get(), D.offsets.get(), stream_,
-                                      &prof_);
+                                      &prof_, x, out);
   }
   if (prof_.on) {
     const MoeConfig& c = impl_->cfg;
@@ -265,8 +289,49 @@ void MoeSession::forward_host(const float* inputs, const double* scores, float* 
   impl_->bf16->download_outputs(outputs, stream_);
 }
 
+void MoeSession::forward_host_async(const float* inputs, const double* scores, float* outputs) {
+  Impl& I = *impl_;
+  if (I.precision == 0) throw_error(Errc::invalid_argument, "forward_host needs a tensor-core session (DB_MOE_BF16 or DB_MOE_FP16)");
+  const MoeConfig& c = I.cfg;
+  const size_t xb = sizeof(float) * static_cast<size_t>(T_) * c.data_dim;
+  const size_t sb = sizeof(double) * static_cast<size_t>(T_) * c.experts;
+  if (!I.pipe) {
+    I.pipe = std::make_unique<Impl::Pipe>();
+    Impl::Pipe& Q = *I.pipe;
+    check(cudaStreamCreateWithFlags(&Q.h2d, cudaStreamNonBlocking), "stream");
+    check(cudaStreamCreateWithFlags(&Q.d2h, cudaStreamNonBlocking), "stream");
+    for (int k = 0; k < Impl::Pipe::kDepth; ++k) {
+      Q.x[k].alloc(static_cast<size_t>(T_) * c.data_dim);
+      Q.out[k].alloc(static_cast<size_t>(T_) * c.data_dim);
+      Q.sc[k].alloc(static_cast<size_t>(T_) * c.experts);
+      for (cudaEvent_t* e : {&Q.h2d_done[k], &Q.in_free[k], &Q.out_ready[k], &Q.out_free[k]}) {
+        check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+        check(cudaEventRecord(*e, stream_), "event");
+      }
+    }
+  }
+  Impl::Pipe& Q = *I.pipe;
+  const int k = static_cast<int>(Q.calls++ % Impl::Pipe::kDepth);
+  check(cudaStreamWaitEvent(Q.h2d, Q.in_free[k]), "wait");
+  check(cudaMemcpyAsync(Q.sc[k].get(), scores, sb, cudaMemcpyHostToDevice, Q.h2d), "H2D scores");
+  check(cudaMemcpyAsync(Q.x[k].get(), inputs, xb, cudaMemcpyHostToDevice, Q.h2d), "H2D inputs");
+  check(cudaEventRecord(Q.h2d_done[k], Q.h2d), "event");
+  check(cudaStreamWaitEvent(stream_, Q.h2d_done[k]), "wait");
+  check(cudaStreamWaitEvent(stream_, Q.out_free[k]), "wait");
+  forward_from(Q.x[k].get(), Q.sc[k].get(), Q.out[k].get());
+  check(cudaEventRecord(Q.in_free[k], stream_), "event");
+  check(cudaEventRecord(Q.out_ready[k], stream_), "event");
+  check(cudaStreamWaitEvent(Q.d2h, Q.out_ready[k]), "wait");
+  check(cudaMemcpyAsync(outputs, Q.out[k].get(), xb, cudaMemcpyDeviceToHost, Q.d2h), "D2H outputs");
+  check(cudaEventRecord(Q.out_free[k], Q.d2h), "event");
+}
+
 void MoeSession::synchronize() {
   check(cudaStreamSynchronize(stream_), "sync");
+  if (impl_->pipe) {
+    check(cudaStreamSynchronize(impl_->pipe->h2d), "sync");
+    check(cudaStreamSynchronize(impl_->pipe->d2h), "sync");
+  }
   impl_->dev.check_err(stream_);
 }
 
@@ -351,6 +416,29 @@ struct MoeEp::Impl {
   std::int64_t cap_rows = 0;  // padded-row capacity of A / H
   std::vector<std::int32_t> cnt_h;    // last layout's counts [G][E]
   std::vector<std::int64_t> pstart_h; // and its padded expert starts [E+1]
+  // NCCL exchange (forward): communicator, its stream, counts, row buffers
+  ncclComm_t comm = nullptr;
+  cudaStream_t cs = nullptr;
+  Buf<std::int32_t> send_cnt, recv_cnt;  // [n] rows per global expert sent; [G][E] received
+  std::int32_t* h_cnt = nullptr;         // pinned: send [n] | recv [G·E]
+  Buf<std::uint16_t> sendb, backb, recvb, retb;  // 16-bit rows: [items][d] ×2, [recv cap][d] ×2
+  std::int64_t recv_cap = 0;
+  std::vector<cudaEvent_t> ev;           // sorted, counts, packed, back, arrive[c]..., done[c]...
+
+  cudaEvent_t event(size_t i) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      ev.push_back(e);
+    }
+    return ev[i];
+  }
+  ~Impl() {
+    if (comm) Nccl::get().CommDestroy(comm);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (cs) cudaStreamDestroy(cs);
+    if (h_cnt) cudaFreeHost(h_cnt);
+  }
 
   void ensure_capacity(std::int64_t rows) {
     if (rows <= cap_rows) return;
@@ -457,6 +545,143 @@ void MoeEp::forward_local() {
   check(dbk_moe_tc_combine(I.fmt, T_, D.k, d, D.wts.get(), I.pos_of_item.get(), I.Y.get(), I.out.get(), stream_),
         "moe combine");
   prof_.end(stream_);
+  last_recv_rows_ = items();
+}
+
+void MoeEp::comm_init(const void* unique_id) {
+  Impl& I = *impl_;
+  const Nccl& nc = Nccl::get();
+  if (I.comm) {
+    nc.CommDestroy(I.comm);
+    I.comm = nullptr;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  nc.check(nc.CommInitRank(&I.comm, I.world, id, I.rank), "ncclCommInitRank");
+  if (!I.cs) check(cudaStreamCreateWithFlags(&I.cs, cudaStreamNonBlocking), "stream");
+  const int n = I.dev.n;
+  I.send_cnt.alloc(static_cast<size_t>(n));
+  I.recv_cnt.alloc(static_cast<size_t>(I.world) * I.E);
+  if (!I.h_cnt)
+    check(cudaHostAlloc(reinterpret_cast<void**>(&I.h_cnt), sizeof(std::int32_t) * (static_cast<size_t>(n) * 2),
+                        cudaHostAllocDefault), "pinned counts");
+  I.sendb.alloc(static_cast<size_t>(items()) * I.cfg.data_dim);
+  I.backb.alloc(static_cast<size_t>(items()) * I.cfg.data_dim);
+}
+
+// One expert-parallel forward with the exchange on NCCL, all
+// of it issued from here on the session stream (kernels) and the exchange
+// stream (NCCL), ordered by events:
+//   1. gate, stable sort, per-expert send counts               (stream)
+//   2. count all-to-all as grouped ncclSend/ncclRecv of the [q·E, (q+1)·E)
+//      slices, then their copy to pinned host memory           (exchange)
+//      — meanwhile the stream packs the rows in sorted order;
+//   3. the host waits for the counts alone (the pack keeps running), plans
+//      the pieces (make_ep_plan) and lays out the received experts;
+//   4. per local-expert range c: the rows' grouped send/recv (exchange),
+//      the range's grouped GEMMs once they arrived (stream), its outputs
+//      back to their senders once computed (exchange), so range c+1's
+//      transfer overlaps range c's GEMMs;
+//   5. the slot-order combine once every output is back       (stream).
+// Receivers concatenate by source rank, which keeps every expert's rows in
+// the reference's (token, slot) order (src/moe.cpp:214-251).
+void MoeEp::forward(int chunks) {
+  Impl& I = *impl_;
+  MoeDev& D = I.dev;
+  if (!I.comm) {
+    if (I.world != 1) throw_error(Errc::invalid_argument, "expert parallel forward needs db_moe_ep_comm_init");
+    forward_local();
+    return;
+  }
+  const Nccl& nc = Nccl::get();
+  const int G = I.world, E = I.E, n = D.n;
+  const size_t row_bytes = static_cast<size_t>(I.cfg.data_dim) * 2;
+  prof_.begin(3, stream_);
+  D.gate(stream_);
+  D.sort(stream_);
+  check(dbk_moe_ep_counts(n, D.offsets.get(), I.send_cnt.get(), stream_), "ep counts");
+  cudaEvent_t ev_sorted = I.event(0), ev_counts = I.event(1), ev_packed = I.event(2), ev_back = I.event(3);
+  check(cudaEventRecord(ev_sorted, stream_), "event");
+  check(cudaStreamWaitEvent(I.cs, ev_sorted, 0), "wait");
+  nc.check(nc.GroupStart(), "ncclGroupStart");
+  for (int q = 0; q < G; ++q) {
+    nc.check(nc.Send(I.send_cnt.get() + static_cast<size_t>(q) * E, static_cast<size_t>(E), ncclInt32, q, I.comm, I.cs),
+             "ncclSend counts");
+    nc.check(nc.Recv(I.recv_cnt.get() + static_cast<size_t>(q) * E, static_cast<size_t>(E), ncclInt32, q, I.comm, I.cs),
+             "ncclRecv counts");
+  }
+  nc.check(nc.GroupEnd(), "ncclGroupEnd");
+  std::int32_t* h_send = I.h_cnt;
+  std::int32_t* h_recv = I.h_cnt + n;
+  check(cudaMemcpyAsync(h_send, I.send_cnt.get(), sizeof(std::int32_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+                        I.cs), "D2H counts");
+  check(cudaMemcpyAsync(h_recv, I.recv_cnt.get(), sizeof(std::int32_t) * static_cast<size_t>(G) * E,
+                        cudaMemcpyDeviceToHost, I.cs), "D2H counts");
+  check(cudaEventRecord(ev_counts, I.cs), "event");
+  check(dbk_moe_ep_pack(I.fmt, items(), D.k, D.d, D.order.get(), I.x.get(), I.sendb.get(), I.pos_of_item.get(),
+                        I.sms * 8, stream_), "ep pack");
+  check(cudaEventRecord(ev_packed, stream_), "event");
+  prof_.end(stream_);
+  check(cudaEventSynchronize(ev_counts), "counts");  // the GPU keeps packing meanwhile
+  const EpPlan plan = make_ep_plan(G, E, h_send, h_recv, chunks);
+  if (plan.recv_total > I.recv_cap) {
+    check(cudaStreamSynchronize(stream_), "sync");  // the old buffers may still be read
+    check(cudaStreamSynchronize(I.cs), "sync");
+    I.recv_cap = plan.recv_total + plan.recv_total / 4 + 1;
+    I.recvb.alloc(static_cast<size_t>(I.recv_cap) * I.cfg.data_dim);
+    I.retb.alloc(static_cast<size_t>(I.recv_cap) * I.cfg.data_dim);
+  }
+  // layout of the received experts from the device copy of the counts
+  I.cnt_h.assign(h_recv, h_recv + static_cast<size_t>(G) * E);
+  I.pstart_h.assign(static_cast<size_t>(E) + 1, 0);
+  for (int e = 0; e < E; ++e) {
+    std::int64_t tot = 0;
+    for (int r = 0; r < G; ++r) tot += h_recv[r * E + e];
+    I.pstart_h[static_cast<size_t>(e) + 1] = I.pstart_h[static_cast<size_t>(e)] + (tot + 255) / 256 * 256;
+  }
+  I.ensure_capacity(I.pstart_h[static_cast<size_t>(E)]);
+  check(cudaStreamWaitEvent(stream_, ev_counts, 0), "wait");
+  check(dbk_moe_ep_layout(G, E, I.recv_cnt.get(), I.pstart.get(), I.tile_expert.get(), I.tile_rb.get(),
+                          I.n_tiles.get(), I.src_row.get(), I.cum.get(), stream_), "ep layout");
+  // rows out, per expert range
+  auto* sb = reinterpret_cast<std::uint8_t*>(I.sendb.get());
+  auto* rb = reinterpret_cast<std::uint8_t*>(I.recvb.get());
+  auto* tb = reinterpret_cast<std::uint8_t*>(I.retb.get());
+  auto* bb = reinterpret_cast<std::uint8_t*>(I.backb.get());
+  auto exchange = [&](int c, const std::uint8_t* src, const std::vector<std::int64_t>& src_off,
+                      const std::vector<std::int64_t>& src_rows, std::uint8_t* dst,
+                      const std::vector<std::int64_t>& dst_off, const std::vector<std::int64_t>& dst_rows) {
+    nc.check(nc.GroupStart(), "ncclGroupStart");
+    for (int q = 0; q < G; ++q) {
+      const size_t i = static_cast<size_t>(c) * G + q;
+      if (src_rows[i])
+        nc.check(nc.Send(src + src_off[i] * row_bytes, src_rows[i] * row_bytes, ncclUint8, q, I.comm, I.cs),
+                 "ncclSend rows");
+      if (dst_rows[i])
+        nc.check(nc.Recv(dst + dst_off[i] * row_bytes, dst_rows[i] * row_bytes, ncclUint8, q, I.comm, I.cs),
+                 "ncclRecv rows");
+    }
+    nc.check(nc.GroupEnd(), "ncclGroupEnd");
+  };
+  check(cudaStreamWaitEvent(I.cs, ev_packed, 0), "wait");
+  const int C = plan.C;
+  for (int c = 0; c < C; ++c) {
+    exchange(c, sb, plan.s_off, plan.s_rows, rb, plan.r_off, plan.r_rows);
+    check(cudaEventRecord(I.event(4 + static_cast<size_t>(c)), I.cs), "event");
+  }
+  for (int c = 0; c < C; ++c) {
+    check(cudaStreamWaitEvent(stream_, I.event(4 + static_cast<size_t>(c)), 0), "wait");
+    experts_range(rb, tb, plan.bounds[static_cast<size_t>(c)].first, plan.bounds[static_cast<size_t>(c)].second);
+    check(cudaEventRecord(I.event(4 + static_cast<size_t>(C + c)), stream_), "event");
+  }
+  for (int c = 0; c < C; ++c) {  // outputs back: the reverse pieces
+    check(cudaStreamWaitEvent(I.cs, I.event(4 + static_cast<size_t>(C + c)), 0), "wait");
+    exchange(c, tb, plan.r_off, plan.r_rows, bb, plan.s_off, plan.s_rows);
+  }
+  check(cudaEventRecord(ev_back, I.cs), "event");
+  check(cudaStreamWaitEvent(stream_, ev_back, 0), "wait");
+  combine(bb);
+  last_recv_rows_ = plan.recv_total;
 }
 
 void MoeEp::layout(const std::int32_t* cnt) {

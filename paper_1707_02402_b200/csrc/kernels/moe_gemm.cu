@@ -430,6 +430,13 @@ extern "C" int dbk_moe_tc_combine(int32_t fmt, int64_t T, int32_t k, int32_t d, 
 // in (token, slot) order, are therefore already grouped by destination rank.
 namespace {
 
+// Rows per global expert of this rank's sorted items (the send counts of
+// the exchange: destination q's experts are the block [q·E, (q+1)·E)).
+__global__ void k_moe_ep_counts(int32_t n, const int32_t* __restrict__ offsets, int32_t* __restrict__ counts) {
+  for (int32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+    counts[e] = offsets[e + 1] - offsets[e];
+}
+
 // pos_of_item[order[i]] = i: an item's row in the sorted send buffer.
 __global__ void k_moe_ep_positions(int64_t items, const int32_t* __restrict__ order,
                                    int32_t* __restrict__ pos_of_item) {
@@ -586,6 +593,11 @@ extern "C" int dbk_moe_ep_pack(int32_t fmt, int64_t items, int32_t k, int32_t d,
   k_moe_ep_positions<<<blocks, 256, 0, s>>>(items, order, pos_of_item);
   if (fmt == DBK_FMT_F16) k_moe_ep_pack<true><<<blocks, 256, 0, s>>>(items / k, k, d, pos_of_item, x, static_cast<uint16_t*>(send));
   else k_moe_ep_pack<false><<<blocks, 256, 0, s>>>(items / k, k, d, pos_of_item, x, static_cast<uint16_t*>(send));
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_moe_ep_counts(int32_t n, const int32_t* offsets, int32_t* counts, void* stream) {
+  k_moe_ep_counts<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(n, offsets, counts);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -176,15 +176,21 @@ struct StepParams {
 
 // Error codes shared with the host (IepSession::check_errors): a module
 // produced a non-finite row (src/executor.cpp:156-159; ReLU as max maps NaN
-// to 0 like the reference's `v > 0 ? v : 0`, so this is +inf), or a value
-// outside the fp16 operand range (|x| > 65504) that the next block could not
-// stage.
+// to 0 like the reference's `v > 0 ? v : 0`, so this is +inf) or a value
+// beyond the fp16 operand range the next block stages it in (the epilogue
+// sees both as an fp16 inf), or an input is outside that range (gather).
 constexpr int32_t kErrNonFinite = 9;
 constexpr int32_t kErrRange = 10;
 
 // Two error codes → one (non-finite outranks range; 0 = none).
 __device__ __forceinline__ int32_t merge_code(int32_t a, int32_t b) {
   return (a == kErrNonFinite || b == kErrNonFinite) ? kErrNonFinite : (a | b);
+}
+
+// Running max of the eight fp16 values of a staged 16-byte vector.
+__device__ __forceinline__ __half2 hmax4(__half2 m, const uint4& v) {
+  const __half2* h = reinterpret_cast<const __half2*>(&v);
+  return __hmax2(__hmax2(m, __hmax2(h[0], h[1])), __hmax2(h[2], h[3]));
 }
 
 // 0, kErrRange or kErrNonFinite for 8 values about to become fp16 operands.
@@ -435,7 +441,11 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
     if (sink == 1.2345e-30f) *own = 0;
     return;
   }
-  int32_t bad = 0;  // range / non-finite code of this lane's outputs
+  // largest staged fp16 operand (values ≥ 0 after the ReLU, so inf = an
+  // output beyond the fp16 range or non-finite) and largest fp32 output:
+  // one half2 max per packed word, checked once per tile
+  __half2 hmax = __float2half2_rn(0.f);
+  float fmax32 = 0.f;
 #pragma unroll 2
   for (int cb = 0; cb < kChunks; ++cb) {
     float v[kChunk];
@@ -449,7 +459,6 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
       float o[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) o[k] = pe.valid ? fmaxf(x[k] + bias[k], 0.f) : 0.f;
-      bad = merge_code(bad, range_code(o));
       const int64_t off = static_cast<int64_t>(cb * kChunk + 8 * m) << 7;
       if (KIND == 1) {
         uint4 pk;
@@ -457,11 +466,13 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
         pk.y = pack_f16x2(o[2], o[3]);
         pk.z = pack_f16x2(o[4], o[5]);
         pk.w = pack_f16x2(o[6], o[7]);
+        hmax = hmax4(hmax, pk);
         if (l2sink) st_v4(sink_slot, pk);
         else *reinterpret_cast<uint4*>(own + off) = pk;
       } else if (KIND == 0) {
         uint4 hi, lo;
         split_f16x8(o, hi, lo);
+        hmax = hmax4(hmax, hi);
         if (l2sink) {
           st_v4(sink_slot, hi);
           st_v4(sink_slot, lo);
@@ -479,6 +490,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
         if (pe.fwd_row >= 0) {
           uint4 hi, lo;
           split_f16x8(o, hi, lo);
+          hmax = hmax4(hmax, hi);
           const int p = L.plane + (pe.fwd_buf == 2 ? 16 : 0);
           const int64_t off = stage_off(P.ps, p, pe.fwd_row);
           uint8_t* hp = (pe.fwd_buf == 0 ? P.stage_x : P.stage_cat) + off;
@@ -491,6 +503,8 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
           }
         }
         if (pe.dst) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) fmax32 = fmaxf(fmax32, o[k]);
           float4* dp = reinterpret_cast<float4*>(pe.dst + L.plane_off32);
           const float4 d0 = make_float4(o[0], o[1], o[2], o[3]), d1 = make_float4(o[4], o[5], o[6], o[7]);
           if (l2sink) {
@@ -504,7 +518,10 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
       }
     }
   }
-  if (bad) atomicCAS(P.err, 0, bad);  // the first error wins (rare path)
+#ifndef DYNBATCH_NO_RANGE_CHECK
+  const float2 hm = __half22float2(hmax);
+  if (!(fmaxf(hm.x, hm.y) <= 65504.f) || !(fmax32 <= 3.4e38f)) atomicCAS(P.err, 0, kErrNonFinite);
+#endif
 }
 
 // --------------------------------------------------------------- kernel

@@ -14,8 +14,12 @@ forward is:
 
 Receivers concatenate by source rank. With contiguous token shards this
 reproduces, for every expert, the reference's (token, slot) member order.
-The exchange is plain torch.distributed (NCCL over NVLink on the GPU box,
-gloo in the CPU tests). `EpExchange` is the part shared by both.
+On the B200 the whole forward, both exchanges included, runs inside the
+library (MoeEp::forward, db_moe_ep_forward): grouped ncclSend/ncclRecv
+on its own NCCL communicator, planned by make_ep_plan. `MoeEpLayer` is the
+thin wrapper over it. `EpExchange` and the plan helpers below restate the
+same protocol over torch.distributed; the CPU tests run it on gloo with
+world 2 against the oracle, and check db_moe_ep_plan against `pieces`.
 
 With `chunks` > 1 the exchange overlaps the expert GEMMs:
 the local experts are cut into contiguous ranges, and each range's rows
@@ -115,96 +119,38 @@ class EpExchange:
 
 
 class MoeEpLayer:
-    """One rank of the expert-parallel MoE layer on the B200 (tcgen05
-    grouped GEMMs with fp16 or bf16 operands, db_moe_ep_*). Collectives are issued on the session's
-    stream, so the kernels and the exchange stay ordered without host syncs
-    beyond the two count reads."""
+    """One rank of the expert-parallel MoE layer on the B200: a thin wrapper
+    over the library's db_moe_ep_* session, whose forward runs gate, sort,
+    both NCCL exchanges (counts and rows, chunked by expert range and
+    overlapped with the grouped tcgen05 GEMMs) and the combine in C++
+    (MoeEp::forward). torch.distributed only carries the 128-byte NCCL id
+    from rank 0 to the others.
 
-    def __init__(self, experts, k, batch, data_dim, hidden, seed=0, group=None, precision=None):
-        import torch
+    At world 1 the layer is one device pass (no exchange); `loopback=True`
+    still builds a one-rank NCCL communicator so the exchange path runs (tests)."""
+
+    def __init__(self, experts, k, batch, data_dim, hidden, seed=0, group=None, precision=None, loopback=False):
         import torch.distributed as dist
 
-        from . import MOE_BF16, MOE_FP16, MoeEpSession
+        from . import MOE_FP16, MoeEpSession, moe_ep_nccl_id
         precision = MOE_FP16 if precision is None else precision
-        self.dtype = torch.bfloat16 if precision == MOE_BF16 else torch.float16
-        self.torch = torch
         init = dist.is_available() and dist.is_initialized()
         self.rank = dist.get_rank(group) if init else 0
         self.world = dist.get_world_size(group) if init else 1
         self.sess = MoeEpSession(experts, k, batch, data_dim, hidden, seed, self.rank, self.world, precision)
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self.stream = torch.cuda.ExternalStream(self.sess.stream, device=dev)
-        self.ex = EpExchange(self.world, experts, device=dev, group=group)
-        self.d, self.dev = data_dim, dev
-        self.send = torch.empty((self.sess.items, data_dim), dtype=self.dtype, device=dev)
-        self.back = torch.empty_like(self.send)
-        self.recv = self.ret = None
-        self.last_recv_rows = 0
-        self.force_exchange = False  # world 1: run the exchange code paths (loopback) anyway (tests)
-
-    def _ensure(self, rows: int):
-        if self.recv is None or self.recv.shape[0] < rows:
-            cap = max(rows + rows // 4, 1)
-            self.recv = self.torch.empty((cap, self.d), dtype=self.dtype, device=self.dev)
-            self.ret = self.torch.empty_like(self.recv)
+        self.stream = self.sess.stream
+        if self.world > 1 or loopback:
+            box = [moe_ep_nccl_id() if self.rank == 0 else None]
+            if self.world > 1:
+                dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            self.sess.comm_init(box[0])
 
     def forward(self, chunks: int = 1):
-        if self.world == 1 and not self.force_exchange:
-            return self._forward_local()
-        if chunks > 1:
-            return self._forward_chunked(chunks)
-        t = self.torch
-        counts = self.sess.dispatch(self.send.data_ptr())
-        send_rows = split_rows(counts, self.world)
-        with t.cuda.stream(self.stream):
-            cnt = self.ex.counts(counts)
-            recv_rows = cnt.sum(axis=1)
-            rows = int(recv_rows.sum())
-            self._ensure(rows)
-            self.ex.rows(self.recv, self.send, recv_rows, send_rows)
-        self.sess.experts(self.recv.data_ptr(), cnt, self.ret.data_ptr())
-        with t.cuda.stream(self.stream):
-            self.ex.rows(self.back, self.ret, send_rows, recv_rows)
-        self.sess.combine(self.back.data_ptr())
-        self.last_recv_rows = rows
+        self.sess.forward(chunks)
+
+    @property
+    def last_recv_rows(self) -> int:
+        return self.sess.recv_rows
 
     def outputs(self) -> np.ndarray:
         return self.sess.outputs()
-
-    def _forward_chunked(self, chunks: int):
-        """The exchange in expert ranges, overlapped with the grouped GEMMs
-        (module docstring). Every operation is ordered on the session
-        stream: the point-to-point batches wait for it when issued, and it
-        waits for a batch through the batch's works."""
-        t = self.torch
-        counts = self.sess.dispatch(self.send.data_ptr())
-        G, E = self.world, self.sess.local_experts
-        with t.cuda.stream(self.stream):
-            cnt = self.ex.counts(counts)
-            rows = int(cnt.sum())
-            self._ensure(rows)
-            self.sess.layout(cnt)
-            bounds = chunk_bounds(E, chunks)
-            s_off, s_rows = pieces(np.asarray(counts).reshape(G, E), bounds)  # send side: [dest][e]
-            r_off, r_rows = pieces(cnt, bounds)                                # receive side: [src][e]
-            arrivals = [self.ex.pieces_async(self.recv, r_off[c], r_rows[c], self.send, s_off[c], s_rows[c],
-                                             self.rank) for c in range(len(bounds))]
-            returns = []
-            for c, (e0, e1) in enumerate(bounds):
-                for w in arrivals[c]:
-                    w.wait()  # the stream waits for range c's rows
-                self.sess.experts_range(self.recv.data_ptr(), self.ret.data_ptr(), e0, e1)
-                returns.append(self.ex.pieces_async(self.back, s_off[c], s_rows[c], self.ret, r_off[c], r_rows[c],
-                                                    self.rank))
-            for ws in returns:
-                for w in ws:
-                    w.wait()
-        self.sess.combine(self.back.data_ptr())
-        self.last_recv_rows = rows
-
-    def _forward_local(self):
-        """World 1: both exchanges are the identity, so the layer runs as one
-        device pass — the dispatch writes the tiled GEMM operand directly
-        and the combine reads the GEMM rows (no pack, scatter or copies)."""
-        self.sess.forward_local()
-        self.last_recv_rows = self.sess.items

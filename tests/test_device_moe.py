@@ -95,3 +95,25 @@ def test_moe_bf16_matches_reference(n, k, T, d, h):
     assert np.array_equal(items, np.argsort(ids.ravel(), kind="stable").astype(np.int32))
     err = max_norm_err(out, ref)
     assert err <= 2e-2, err
+
+
+def test_moe_forward_host_async_pipeline_equals_sync_calls():
+    """Pipelined host calls (three in flight, per-call device slots, copies
+    on their own streams) give exactly the synchronous calls' outputs."""
+    n, k, T, d, h = 16, 2, 512, 256, 256
+    s = db.MoeSession(n, k, T, d, h, seed=3, precision=db.MOE_FP16)
+    rng = np.random.default_rng(1)
+    calls = 5
+    xs = [db.PinnedArray((T, d), np.float32) for _ in range(calls)]
+    scs = [db.PinnedArray((T, n), np.float64) for _ in range(calls)]
+    outs = [db.PinnedArray((T, d), np.float32) for _ in range(calls)]
+    for x, sc in zip(xs, scs):
+        x.array[:] = rng.uniform(-1, 1, size=(T, d)).astype(np.float32)
+        sc.array[:] = rng.uniform(-1, 1, size=(T, n))
+    for x, sc, o in zip(xs, scs, outs):
+        s.forward_host_async(x.array, sc.array, o.array)
+    s.synchronize()
+    want = np.zeros((T, d), np.float32)
+    for x, sc, o in zip(xs, scs, outs):
+        s.forward_host(x.array, sc.array, want)
+        assert np.array_equal(o.array, want)

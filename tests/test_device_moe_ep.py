@@ -94,20 +94,33 @@ def test_ep_counts_follow_reference_routing():
         np.testing.assert_array_equal(c, np.bincount(ids[r * Tl:(r + 1) * Tl].reshape(-1), minlength=n))
 
 
-def test_moe_ep_layer_world1_equals_session():
+@pytest.mark.parametrize("precision", [db.MOE_FP16, db.MOE_BF16])
+def test_moe_ep_layer_world1_equals_session(precision):
     from paper_1707_02402_b200.moe_ep import MoeEpLayer
     n, k, T, d, h, seed = 16, 2, 1024, 256, 512, 11
-    layer = MoeEpLayer(n, k, T, d, h, seed)
+    layer = MoeEpLayer(n, k, T, d, h, seed, precision=precision)
     layer.forward()
     out = layer.outputs()
-    full = db.MoeSession(n, k, T, d, h, seed=seed, precision=db.MOE_FP16)
+    full = db.MoeSession(n, k, T, d, h, seed=seed, precision=precision)
     full.forward()
     np.testing.assert_array_equal(out, full.run().outputs().astype(np.float32))
-    layer.force_exchange = True  # the exchange code paths as loopbacks at world 1
-    layer.forward()
-    np.testing.assert_array_equal(layer.outputs(), out)
-    layer.forward(chunks=3)  # the chunked, overlapped exchange
-    np.testing.assert_array_equal(layer.outputs(), out)
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 16])
+def test_moe_ep_forward_through_nccl_loopback(chunks):
+    """MoeEp::forward with a one-rank NCCL communicator: the count exchange,
+    the host plan, the chunked row exchange (ncclSend/ncclRecv to self), the
+    per-range GEMMs and the return exchange all run, and the outputs are the
+    one-pass layer's bit for bit."""
+    from paper_1707_02402_b200.moe_ep import MoeEpLayer
+    n, k, T, d, h, seed = 16, 2, 1024, 256, 512, 11
+    want = MoeEpLayer(n, k, T, d, h, seed)
+    want.forward()
+    layer = MoeEpLayer(n, k, T, d, h, seed, loopback=True)
+    for _ in range(2):  # twice: buffers and events are reused
+        layer.forward(chunks)
+        np.testing.assert_array_equal(layer.outputs(), want.outputs())
+    assert layer.last_recv_rows == T * k
 
 
 def test_ep_rejects_indivisible_shapes():

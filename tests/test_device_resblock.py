@@ -137,12 +137,12 @@ def test_cfg3_full_size_properties():
     the stated tolerance."""
     import bench
     cfg = bench.CFG["cfg3"]
-    b = db.Batch.generate(cfg["kind"], batch=cfg["per_gpu"], vocab=cfg["vocab"], width=F, depth=cfg["depth"],
+    b = db.Batch.generate(cfg["kind"], batch=cfg["batch"], vocab=cfg["vocab"], width=F, depth=cfg["depth"],
                           length=cfg["length"], branch_prob=cfg["branch_prob"], seed=0)
     sess = db.IepSession(b, 1234, db.MODULE_RESBLOCK)
     sess.forward()
     sess.synchronize()
-    ob = O.gen_batch(cfg["kind"], cfg["per_gpu"], p=cfg["vocab"], depth=cfg["depth"], length=cfg["length"],
+    ob = O.gen_batch(cfg["kind"], cfg["batch"], p=cfg["vocab"], depth=cfg["depth"], length=cfg["length"],
                      bp=cfg["branch_prob"], seed=0)
     from test_device_iep import _flat_from_json
     assert _flat_from_json(sess.schedule().to_json()) == O.schedule_improved(ob)
@@ -154,7 +154,7 @@ def test_cfg3_full_size_properties():
         assert np.array_equal(one.run().outputs()[0], full[r])
     # one row against the fp64 oracle (its own program, same module seed)
     r = 1234
-    sub = db.Batch.generate_range(r, r + 1, cfg["kind"], batch=cfg["per_gpu"], vocab=cfg["vocab"], width=F,
+    sub = db.Batch.generate_range(r, r + 1, cfg["kind"], batch=cfg["batch"], vocab=cfg["vocab"], width=F,
                                   depth=cfg["depth"], length=cfg["length"], branch_prob=cfg["branch_prob"], seed=0)
     x = sub.inputs()
     obs = O.Batch(ob.prog_off[r:r + 2] - ob.prog_off[r], ob.fid[ob.prog_off[r]:ob.prog_off[r + 1]],

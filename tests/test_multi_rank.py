@@ -237,3 +237,21 @@ def test_chunk_bounds_and_pieces():
     # peer blocks start at 0 and 6; range (1, 3) of peer 1 starts after its expert 0
     assert off.tolist() == [[0, 6], [1, 10]]
     assert rows.tolist() == [[1, 4], [5, 6]]
+
+
+def test_library_ep_plan_equals_protocol_pieces():
+    """db_moe_ep_plan (the C++ plan MoeEp::forward issues its NCCL pieces
+    from) equals the protocol's pieces / chunk_bounds on random count
+    matrices, for both directions. Host-only: no device needed."""
+    import paper_1707_02402_b200 as db
+    from paper_1707_02402_b200.moe_ep import chunk_bounds, pieces
+    rng = np.random.default_rng(3)
+    for G, E, chunks in [(1, 4, 1), (2, 8, 3), (4, 6, 4), (8, 128, 4), (3, 5, 9)]:
+        send = rng.integers(0, 60, G * E).astype(np.int32)
+        recv = rng.integers(0, 60, (G, E)).astype(np.int32)
+        so, sr, ro, rr = db.moe_ep_plan(G, E, send, recv, chunks)
+        b = chunk_bounds(E, chunks)
+        a_off, a_rows = pieces(send.reshape(G, E), b)
+        b_off, b_rows = pieces(recv, b)
+        assert np.array_equal(so, a_off) and np.array_equal(sr, a_rows)
+        assert np.array_equal(ro, b_off) and np.array_equal(rr, b_rows)
