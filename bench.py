@@ -682,8 +682,9 @@ def main():
         return
     maybe_spawn(args)
     dist = Dist(args.gpus, cpu=args.dry_run)
-    if args.dry_run:
-        print(json.dumps(dry_run(args, dist)), flush=True)
+    if args.dry_run:  # one atomic write per rank (ranks share the pipe)
+        sys.stdout.flush()
+        os.write(1, (json.dumps(dry_run(args, dist)) + "\n").encode())
         dist.close()
         return
     if args.workload in MOE:
