@@ -158,7 +158,7 @@ int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_
                   const int32_t* child0, const int32_t* child1, const int32_t* example, const int32_t* fwd_ok,
                   const float* inputs, float* values, void* memtab, void* tasks, int32_t* n_tasks,
                   int64_t task_cap, void* stream);
-int dbk_rb_debug(unsigned long long* out24, int32_t reset, int32_t enable);
+int dbk_rb_debug(unsigned long long* out64, int32_t reset, int32_t enable);
 /* Whether the wait-counter (debug) step kernel is selected (a launch-time choice). */
 int dbk_rb_debug_enabled(void);
 int dbk_rb_inputs_from_chw(int64_t rows, const float* chw, float* planes, void* stream);

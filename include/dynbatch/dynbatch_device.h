@@ -81,11 +81,15 @@ DYNBATCH_API void db_host_free(void* p);
  * db_batch_generate (for data-parallel shards). */
 DYNBATCH_API db_status db_batch_generate_range(const db_workload_opts* opts, int64_t first,
                                                int64_t last, db_batch** out);
-/* Diagnostics: MMA-thread wait cycles of the conv kernels, 6 slots × [acc
- * drained, A window, weight stage, loop total] (slots 0-2 = conv1x1,
- * conv3x3 #1, conv3x3 #2; 3-5 unused). enable != 0 turns accounting on for
- * later launches. */
-DYNBATCH_API db_status db_debug_conv_waits(uint64_t* out24, int32_t reset, int32_t enable);
+/* Diagnostics: cycle accounting of the conv step kernel (64 counters):
+ * [12..15] MMA thread [accumulator, window, weight waits, loop total];
+ * [16..19] window producer [item ring, dependencies, free slot, total];
+ * [20..21] MMA-loop cycles and nanoseconds (the kernel's own clock);
+ * [24 + 4k ..] per tile kind k (0 conv1x1, 1 conv3x3 #1, 2 conv3x3 #2):
+ * item cycles, window, weight, accumulator waits; [36 + 2k] epilogue
+ * cycles and tiles; [42 + k] producer dependency waits. enable != 0 turns
+ * accounting on for later launches. */
+DYNBATCH_API db_status db_debug_conv_waits(uint64_t* out64, int32_t reset, int32_t enable);
 /* Borrowing view of the batch's b × width input rows (valid until free). */
 DYNBATCH_API db_status db_batch_inputs(const db_batch* batch, const double** data, int64_t* rows,
                                        int64_t* width);

@@ -683,6 +683,6 @@ def conv_wait_counters(reset=False, enable=True):
     """MMA-thread wait cycles of the conv kernels (diagnostics)."""
     lib().db_debug_conv_waits.restype = C.c_int32
     lib().db_debug_conv_waits.argtypes = [VP, C.c_int32, C.c_int32]
-    out = np.zeros(24, np.uint64)
+    out = np.zeros(64, np.uint64)
     check(lib().db_debug_conv_waits(_ptr(out), 1 if reset else 0, 1 if enable else 0))
-    return out.reshape(6, 4)
+    return out.reshape(16, 4)

@@ -393,10 +393,10 @@ db_status db_batch_generate_range(const db_workload_opts* opts, int64_t first, i
   });
 }
 
-db_status db_debug_conv_waits(uint64_t* out24, int32_t reset, int32_t enable) {
+db_status db_debug_conv_waits(uint64_t* out64, int32_t reset, int32_t enable) {
   return guarded([&] {
     dynbatch::dev::require_device();
-    dynbatch::dev::check(dbk_rb_debug(reinterpret_cast<unsigned long long*>(out24), reset, enable),
+    dynbatch::dev::check(dbk_rb_debug(reinterpret_cast<unsigned long long*>(out64), reset, enable),
                          "dbk_rb_debug");
   });
 }

@@ -207,7 +207,12 @@ __device__ __forceinline__ int32_t range_code(const float* o) {
 // Wait accounting (read/reset with dbk_rb_debug()): slot 3 = MMA thread
 // [drained accumulator, A window, weight stage, loop total]; slot 4 =
 // window producer [item ring, dependency flags, free window slot, total].
-__device__ unsigned long long g_conv_dbg[6 * 4];
+// Slots 24-35: MMA thread per tile kind k (0 conv1x1, 1 conv3x3 #1, 2 conv3x3
+// #2): [24 + 4k] item cycles, [+1] window (A) waits, [+2] weight (B) waits,
+// [+3] accumulator (epilogue) waits; 36-41: epilogue per kind [36 + 2k]
+// cycles from accumulator ready to published, [+1] tiles; 42-44: producer
+// dependency waits per kind.
+__device__ unsigned long long g_conv_dbg[64];
 
 // ------------------------------------------------------------ K phases
 // A tile's K loop is one to three phases of (window source, weights, chunks,
@@ -637,7 +642,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           if (p == 0 || p == 2) {  // conv3x3 #2 waits for the mid tiles only before its W2 phase
             if (DBG) c0 = clock64();
             step_wait_deps<TM>(P, it, p);
-            if (DBG) w_dep += clock64() - c0;
+            if (DBG) {
+              w_dep += clock64() - c0;
+              atomicAdd(&g_conv_dbg[42 + it.kind], static_cast<unsigned long long>(clock64() - c0));
+            }
           }
           const Phase ph = phase_of(P, it, p);
           const uint32_t rows = TM + 2 * ph.halo;
@@ -679,8 +687,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         if (it.kind < 0) break;
         const int abuf = n & 1;
         long long c0 = DBG ? clock64() : 0;
+        const long long t_item = c0;
+        const long long a0 = w_a, b0 = w_b;
         mbar_wait(acc_empty + abuf, ((n >> 1) & 1) ^ 1);
-        if (DBG) w_acc += clock64() - c0;
+        if (DBG) {
+          w_acc += clock64() - c0;
+          atomicAdd(&g_conv_dbg[24 + 4 * it.kind + 3], static_cast<unsigned long long>(clock64() - c0));
+        }
         tc_fence_after();
         uint32_t acc = 0;
         for (int p = 0; p < n_phases(it.kind); ++p) {
@@ -717,6 +730,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           }
         }
         mma_commit(acc_full + abuf);
+        if (DBG) {
+          atomicAdd(&g_conv_dbg[24 + 4 * it.kind + 0], static_cast<unsigned long long>(clock64() - t_item));
+          atomicAdd(&g_conv_dbg[24 + 4 * it.kind + 1], static_cast<unsigned long long>(w_a - a0));
+          atomicAdd(&g_conv_dbg[24 + 4 * it.kind + 2], static_cast<unsigned long long>(w_b - b0));
+        }
       }
       if (DBG) {
         atomicAdd(&g_conv_dbg[12 + 0], static_cast<unsigned long long>(w_acc));
@@ -795,6 +813,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       mbar_wait(tab_full + abuf, (n >> 1) & 1);
       mbar_wait(acc_full + abuf, (n >> 1) & 1);
       tc_fence_after();
+      const long long t_epi = DBG ? clock64() : 0;
       const uint32_t taddr = tmem_base + abuf * TM + lane_addr;
       if (P.diag & 4) {
       } else if (it.kind == 0) {
@@ -827,6 +846,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         __threadfence();
         if (it.kind < 2) st_release_gpu((it.kind == 0 ? P.done0 : P.done1) + it.tile, P.epoch);
         else red_release_gpu_add(P.step_done + it.step, 1);
+        if (DBG) {
+          atomicAdd(&g_conv_dbg[36 + 2 * it.kind], static_cast<unsigned long long>(clock64() - t_epi));
+          atomicAdd(&g_conv_dbg[37 + 2 * it.kind], 1ull);
+        }
       }
     }
   }
@@ -1321,9 +1344,9 @@ extern "C" int dbk_rb_debug_enabled() { return g_debug_flag; }
 
 extern "C" int dbk_rb_debug(unsigned long long* out, int32_t reset, int32_t enable) {
   g_debug_flag = enable;
-  if (out) cudaMemcpyFromSymbol(out, g_conv_dbg, sizeof(unsigned long long) * 24);
+  if (out) cudaMemcpyFromSymbol(out, g_conv_dbg, sizeof(unsigned long long) * 64);
   if (reset) {
-    unsigned long long z[24] = {};
+    unsigned long long z[64] = {};
     cudaMemcpyToSymbol(g_conv_dbg, z, sizeof(z));
   }
   return static_cast<int>(cudaGetLastError());

@@ -15,7 +15,7 @@ import bench  # noqa: E402
 import paper_1707_02402_b200 as db  # noqa: E402
 
 cfg = bench.CFG["cfg3"]
-per = cfg["per_gpu"]
+per = cfg["batch"]
 batch = db.Batch.generate_range(0, per, cfg["kind"], batch=per, vocab=cfg["vocab"], width=bench.F,
                                 depth=cfg["depth"], length=cfg["length"], branch_prob=cfg["branch_prob"],
                                 seed=0)

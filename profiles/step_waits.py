@@ -1,4 +1,7 @@
-"""MMA-thread wait breakdown of the fused conv step kernel (cfg3)."""
+"""Cycle accounting of the fused conv step kernel (cfg3), from the debug
+build of k_rb_step (db_debug_conv_waits): MMA-thread waits overall and per
+tile kind, epilogue cycles per tile kind, producer dependency waits."""
+import json
 import os
 import sys
 
@@ -6,20 +9,26 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1707_02402_b200 as db  # noqa: E402
 
 F = 128 * 14 * 14
-CLK_GHZ = float(os.environ.get("CLK_GHZ", "1.9"))
-b = db.Batch.generate("chain", batch=4096, vocab=40, width=F, length=16, branch_prob=0.3, seed=0)
+b = db.Batch.generate("chain", batch=int(os.environ.get("BATCH", "4096")), vocab=40, width=F, length=16,
+                      branch_prob=float(os.environ.get("BP", "0.3")), seed=0)
 s = db.IepSession(b, 1234, db.MODULE_RESBLOCK)
 s.time(3)
-_, kt = s.time(5, profile=True)
+ms, _ = s.time(5)
 db.conv_wait_counters(reset=True, enable=True)
 s.time(5)
-w = db.conv_wait_counters(reset=True, enable=False)
-acc, a, bb, tot = (int(x) for x in w[3])
-cover = tot / (148 * kt.ms[4] * 1e-3 * CLK_GHZ * 1e9)
-print(f"step kernel ms/fwd {kt.ms[4] / 5:.3f}: acc_wait {acc/tot:6.1%}  A_wait {a/tot:6.1%}  B_wait {bb/tot:6.1%}  "
-      f"busy {(tot-acc-a-bb)/tot:6.1%}  loop/kernel {cover:6.1%}")
-it, dep, sl, ptot = (int(x) for x in w[4])
-print(f"window producer: item-ring wait {it/ptot:6.1%}  dependency wait {dep/ptot:6.1%}  "
-      f"slot wait {sl/ptot:6.1%}  issuing {(ptot-it-dep-sl)/ptot:6.1%}")
-cyc, ns = int(w[5][0]), int(w[5][1])
-print(f"effective SM clock in the MMA loop: {cyc / max(ns, 1) * 1e3:.0f} MHz")
+w = db.conv_wait_counters(reset=True, enable=False).reshape(-1).astype(float)
+acc, a, bb, tot = w[12:16]
+out = {"ms_per_forward": ms / 5, "mma_thread": {"acc_wait": acc / tot, "window_wait": a / tot, "weight_wait": bb / tot,
+                                                "busy": (tot - acc - a - bb) / tot},
+       "producer": {"item_ring": w[16] / w[19], "dependency": w[17] / w[19], "slot": w[18] / w[19]},
+       "mma_loop_mhz": w[20] / max(w[21], 1) * 1e3, "per_kind": {}}
+for k, name in enumerate(("conv1x1", "conv3x3_1", "conv3x3_2")):
+    cyc, wa, wb, wacc = w[24 + 4 * k: 28 + 4 * k]
+    ecyc, etiles = w[36 + 2 * k: 38 + 2 * k]
+    n = max(etiles, 1)
+    out["per_kind"][name] = {"tiles": int(etiles), "mma_item_cycles_per_tile": cyc / n,
+                             "window_wait_per_tile": wa / n, "weight_wait_per_tile": wb / n,
+                             "acc_wait_per_tile": wacc / n, "epilogue_cycles_per_tile": ecyc / n,
+                             "producer_dep_wait_per_tile": w[42 + k] / n,
+                             "share_of_mma_loop": cyc / tot}
+print(json.dumps(out, indent=1))
