@@ -107,8 +107,8 @@ int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t*
                 int32_t* step_bintile_begin, int32_t* step_positions, int32_t* tile_group,
                 int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, int64_t n_nodes,
                 const int32_t* member_g, const int32_t* child0, const int32_t* child1,
-                const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t tile_m,
-                void* stream);
+                const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t* fwd_parent,
+                int32_t* need, int32_t tile_m, void* stream);
 /* Gather of operands no child epilogue forwards, from the task lists that
  * dbk_rb_memtab emits (32-byte tasks, list 0 = leaves of every step, list 1
  * = children shared by several parents, processed for `step` only): fp32
@@ -142,7 +142,8 @@ int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* st
                 int64_t plane_stride, const void* const* w0, const void* const* w1, const void* const* w2,
                 const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
                 int32_t* done0, int32_t* done1, int32_t* step_done, int32_t* queue, int32_t* err,
-                int32_t tile_m, int32_t num_sms, void* stream);
+                int32_t* ready, const int32_t* need, const int32_t* member_g, int32_t tile_m, int32_t num_sms,
+                void* stream);
 /* Zeroes stage_x rows between each segment's last image and its tile end
  * (read as top / left pads by the next segment's first image), every
  * forward, so a new layout needs no full re-zeroing. */
@@ -157,7 +158,7 @@ int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_
                   const int32_t* fwd_pos, const int32_t* fwd_slot, const int32_t* arity_of, const int32_t* fid,
                   const int32_t* child0, const int32_t* child1, const int32_t* example, const int32_t* fwd_ok,
                   const float* inputs, float* values, void* memtab, void* tasks, int32_t* n_tasks,
-                  int64_t task_cap, void* stream);
+                  int64_t task_cap, const int32_t* fwd_parent, int32_t* need, int32_t tile_m, void* stream);
 int dbk_rb_debug(unsigned long long* out64, int32_t reset, int32_t enable);
 /* Whether the wait-counter (debug) step kernel is selected (a launch-time choice). */
 int dbk_rb_debug_enabled(void);

@@ -27,6 +27,9 @@ struct IepSession::RB {
   Buf<const float*> b0tab, b1tab, b2tab;
   Buf<std::int32_t> seg_start, group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
       step_positions, tile_group, tile_q0, bin_group, bin_q0, fwd_ok, fwd_pos, fwd_slot;
+  // cross-step dependencies: the parent a node's image is forwarded to, and
+  // per node the conv3x3 #2 tiles its operand images need / have received
+  Buf<std::int32_t> fwd_parent, need, ready;
   Buf<std::uint64_t> memtab;  // per-member epilogue metadata, 32 bytes each (rb_conv.cu MemberEntry)
   Buf<std::uint64_t> tasks;   // gather tasks, 32 bytes each: 2 lists × task_cap
   Buf<std::int32_t> n_tasks;

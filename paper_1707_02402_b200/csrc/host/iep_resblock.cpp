@@ -144,6 +144,9 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
     R.fwd_ok.upload(ok, stream_);
     R.fwd_pos.alloc(N);
     R.fwd_slot.alloc(N);
+    R.fwd_parent.alloc(N);
+    R.need.alloc(N);
+    R.ready.alloc(N);
     R.memtab.alloc(N * 4);
     R.task_cap = std::max<std::int64_t>(static_cast<std::int64_t>(c.child_list.size()), c.cap_N) + 1;  // ≤ one task per operand
     R.tasks.alloc(static_cast<size_t>(R.task_cap) * 2 * 4);
@@ -243,12 +246,14 @@ void IepSession::forward_resblock() {
                     R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(), R.step_tile_begin.get(),
                     R.step_bintile_begin.get(), R.step_positions.get(), R.tile_group.get(), R.tile_q0.get(),
                     R.bin_group.get(), R.bin_q0.get(), B.csr().N, B.member_g.get(), B.child0.get(),
-                    B.child1.get(), R.fwd_ok.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.tile_m, stream_),
+                    B.child1.get(), R.fwd_ok.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.fwd_parent.get(),
+                    R.need.get(), R.tile_m, stream_),
         "dbk_rb_plan");
   check(dbk_rb_memtab(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), R.seg_start.get(),
                       B.member_g.get(), R.fwd_pos.get(), R.fwd_slot.get(), B.arity_of.get(), B.fid.get(),
                       B.child0.get(), B.child1.get(), B.example.get(), R.fwd_ok.get(), R.inputs.get(),
-                      R.values.get(), R.memtab.get(), R.tasks.get(), R.n_tasks.get(), R.task_cap, stream_),
+                      R.values.get(), R.memtab.get(), R.tasks.get(), R.n_tasks.get(), R.task_cap,
+                      R.fwd_parent.get(), R.need.get(), R.tile_m, stream_),
         "dbk_rb_memtab");
   check(dbk_rb_zero_gaps(S, B.step_group_begin.get(), B.group_begin.get(), R.seg_start.get(), R.stage_x.get(),
                          R.plane_stride, R.tile_m, stream_),
@@ -263,6 +268,7 @@ void IepSession::forward_resblock() {
   // captured forward replays as is
   check(cudaMemsetAsync(R.done0.get(), 0, sizeof(std::int32_t) * R.done0.size(), stream_), "done flags reset");
   check(cudaMemsetAsync(R.done1.get(), 0, sizeof(std::int32_t) * R.done1.size(), stream_), "done flags reset");
+  check(cudaMemsetAsync(R.ready.get(), 0, sizeof(std::int32_t) * R.ready.size(), stream_), "image counters reset");
   R.epoch = 1;
   // leaf operands of every step in one launch (they only read the inputs)
   prof_.begin(2, stream_);
@@ -292,7 +298,7 @@ void IepSession::forward_resblock() {
                       R.memtab.get(), R.stage_x.get(), R.stage_lo.get(), R.stage_cat.get(), R.stage_mid.get(),
                       R.plane_stride, R.w0tab.get(), R.w1tab.get(), R.w2tab.get(), R.b0tab.get(), R.b1tab.get(),
                       R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.step_done.get(), R.queue.get(), err_.get(),
-                      R.tile_m, sms, stream_),
+                      R.ready.get(), R.need.get(), B.member_g.get(), R.tile_m, sms, stream_),
           "conv step");
     prof_.end(stream_);
     ++launches_;

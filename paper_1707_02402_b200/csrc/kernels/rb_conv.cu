@@ -111,7 +111,8 @@ struct MemberEntry {
   int32_t fwd_row;   // staging row of the parent's operand image of this node (position 0), −1: none
   int32_t fwd_buf;   // 0: stage_x (+ lo in stage_lo), 1 / 2: stage_cat operand 0 / 1 (chunks 0-1 / 2-3)
   int32_t keep32;    // a later reader needs the fp32 value (root, shared child)
-  int32_t pad[3];
+  int32_t parent;    // node whose operand image this node's conv3x3 #2 tiles fill (fwd_row ≥ 0), else −1
+  int32_t pad[2];
 };
 
 // One gathered operand (leaf input map or shared child's value → a member's
@@ -172,6 +173,15 @@ struct StepParams {
   int32_t* step_done;    // per step: conv3x3 #2 tiles completed (zeroed each forward)
   int32_t* queue;        // claim counters, one per launch's first step (zeroed each forward)
   int32_t* err;          // first error code (kErrNonFinite / kErrRange), 0 = none
+  // Cross-step dependencies per operand image instead of a step barrier:
+  // ready[node] counts the conv3x3 #2 tiles of the node's forwarded
+  // children that have filled their part of its operand images; need[node]
+  // is their total (dbk_rb_memtab). A tile of a later step starts once the
+  // images its windows read are complete.
+  int32_t* ready;         // zeroed each forward
+  const int32_t* need;
+  const int32_t* member_g;
+  int32_t step_barrier;   // 1: also wait for the whole previous step (A/B)
 };
 
 // Error codes shared with the host (IepSession::check_errors): a module
@@ -291,6 +301,40 @@ __device__ __forceinline__ Item step_item(const StepParams& P, int32_t step, int
   return it;
 }
 
+// Images of group g whose positions overlap local rows [lo, hi) of the
+// segment (local 0 = the first image's position 0; images are kImg apart).
+__device__ __forceinline__ void images_overlapping(int32_t lo, int32_t hi, int32_t rows, int32_t& j0, int32_t& j1) {
+  j0 = lo <= 0 ? 0 : lo / kImg;
+  j1 = hi <= 0 ? -1 : min(rows - 1, (hi - 1) / kImg);
+}
+
+// Producer side: the operand images (forwarded by earlier steps' conv3x3 #2
+// tiles) that overlap this item's window rows are complete: ready == need
+// for each image's node. Relaxed polls, then one acquire fence.
+template <int TM>
+__device__ __forceinline__ void step_wait_images(const StepParams& P, const Item& it, int32_t halo) {
+  const int32_t g = it.g;
+  const int32_t gb0 = P.group_begin[g];
+  const int32_t rows = P.group_begin[g + 1] - gb0;
+  const int32_t base = it.q0 - P.seg_start[g];
+  int32_t j0, j1;
+  images_overlapping(base - halo, base + TM + halo, rows, j0, j1);
+  bool waited = false;
+  for (int32_t j = j0; j <= j1; ++j) {
+    const int32_t node = P.member_g[gb0 + j];
+    const int32_t nd = P.need[node];
+    if (nd == 0) continue;
+    waited = true;
+    if (ld_relaxed_gpu(P.ready + node) >= nd) continue;
+    const uint64_t t0 = global_ns();
+    while (ld_relaxed_gpu(P.ready + node) < nd) {
+      __nanosleep(64);
+      if (global_ns() - t0 > 4000000000ull) __trap();
+    }
+  }
+  if (waited) fence_acquire_gpu();
+}
+
 // Producer side: wait until the tiles this item's windows read are written
 // in this launch (earlier launches are ordered by the stream). conv3x3 #1 of
 // a binary group reads z (conv1x1 tiles i-1..i+1); conv3x3 #2 reads mid
@@ -298,7 +342,16 @@ __device__ __forceinline__ Item step_item(const StepParams& P, int32_t step, int
 // tile i). Halo positions in other segments only feed outputs never stored.
 template <int TM>
 __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& it, int phase) {
-  if (it.kind == 0) return;
+  const bool binary_group = P.group_bintile0[it.g] >= 0;
+  // operand images from earlier steps: conv1x1 reads [x; y] at its own
+  // rows, conv3x3 #1 of a unary group reads x with the halo, conv3x3 #2 of a
+  // unary group reads x hi / lo (the residual) at its own rows
+  if (it.kind == 0) {
+    step_wait_images<TM>(P, it, 0);
+    fence_proxy_async_global();
+    return;
+  }
+  if (!binary_group && (it.kind == 1 || phase == 0)) step_wait_images<TM>(P, it, it.kind == 1 ? kHalo : 0);
   const int32_t g = it.g;
   const int32_t rows = P.group_begin[g + 1] - P.group_begin[g];
   const int32_t nt = seg_tiles(rows, TM);
@@ -629,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         items[slot] = it;
         mbar_arrive(item_full + slot);
         if (it.kind < 0) break;
-        if (it.step > ready) {
+        if (P.step_barrier && it.step > ready) {
           // step s reads what step s − 1 (and earlier) wrote: wait until every
           // conv3x3 #2 tile of the previous step has published its outputs
           if (DBG) c0 = clock64();
@@ -844,8 +897,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       if (threadIdx.x == 64) {
         __threadfence();
-        if (it.kind < 2) st_release_gpu((it.kind == 0 ? P.done0 : P.done1) + it.tile, P.epoch);
-        else red_release_gpu_add(P.step_done + it.step, 1);
+        if (it.kind < 2) {
+          st_release_gpu((it.kind == 0 ? P.done0 : P.done1) + it.tile, P.epoch);
+        } else {
+          red_release_gpu_add(P.step_done + it.step, 1);
+          // this tile's part of each parent's operand image is written
+          const int32_t gb0 = P.group_begin[it.g];
+          const int32_t base = it.q0 - P.seg_start[it.g];
+          int32_t j0, j1;
+          images_overlapping(base, base + TM, P.group_begin[it.g + 1] - gb0, j0, j1);
+          for (int32_t j = j0; j <= j1; ++j) {
+            const int32_t parent = P.memtab[gb0 + j].parent;
+            if (parent >= 0) red_release_gpu_add(P.ready + parent, 1);
+          }
+        }
         if (DBG) {
           atomicAdd(&g_conv_dbg[36 + 2 * it.kind], static_cast<unsigned long long>(clock64() - t_epi));
           atomicAdd(&g_conv_dbg[37 + 2 * it.kind], 1ull);
@@ -976,11 +1041,14 @@ __global__ void __launch_bounds__(1024) k_rb_plan(
 // Forwarding table for conv3x3 #2 epilogues: for every expensive member,
 // each child with a unique parent (fwd_ok) receives the absolute staging
 // position of that parent's image and which buffer / planes it fills.
-__global__ void k_rb_fwd_init(int64_t n, int32_t* __restrict__ fwd_pos, int32_t* __restrict__ fwd_slot) {
+__global__ void k_rb_fwd_init(int64_t n, int32_t* __restrict__ fwd_pos, int32_t* __restrict__ fwd_slot,
+                              int32_t* __restrict__ fwd_parent, int32_t* __restrict__ need) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) {
     fwd_pos[i] = -1;
     fwd_slot[i] = 1 << 8;  // keep the fp32 value (roots, shared children)
+    fwd_parent[i] = -1;
+    need[i] = 0;
   }
 }
 
@@ -1000,7 +1068,7 @@ __global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const
                          const int32_t* __restrict__ seg_start, const int32_t* __restrict__ member_g,
                          const int32_t* __restrict__ child0, const int32_t* __restrict__ child1,
                          const int32_t* __restrict__ fwd_ok, int32_t* __restrict__ fwd_pos,
-                         int32_t* __restrict__ fwd_slot) {
+                         int32_t* __restrict__ fwd_slot, int32_t* __restrict__ fwd_parent) {
   // a block per group (no per-member search), threads over its members
   for (int32_t g = sgb[0] + blockIdx.x; g < sgb[n_steps]; g += gridDim.x) {
     if (seg_start[g] < 0) continue;
@@ -1014,6 +1082,7 @@ __global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const
         // buffer (bit 0: stage_x / stage_cat) and first plane; no fp32 copy:
         // a unary parent reads its residual from the hi/lo images
         fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1);
+        fwd_parent[c] = node;
       }
     }
   }
@@ -1027,7 +1096,8 @@ __global__ void k_rb_memtab(int32_t n_steps, const int32_t* __restrict__ sgb,
                             const int32_t* __restrict__ child0, const int32_t* __restrict__ child1,
                             const int32_t* __restrict__ example, const int32_t* __restrict__ fwd_ok,
                             const float* inputs, float* values, MemberEntry* __restrict__ memtab,
-                            GatherTask* __restrict__ tasks, int32_t* __restrict__ n_tasks, int64_t task_cap) {
+                            GatherTask* __restrict__ tasks, int32_t* __restrict__ n_tasks, int64_t task_cap,
+                            const int32_t* __restrict__ fwd_parent, int32_t* __restrict__ need, int32_t tile_m) {
   // a block per group (no per-member search), threads over its members
   for (int32_t g = sgb[0] + blockIdx.x; g < sgb[n_steps]; g += gridDim.x) {
     if (seg_start[g] < 0) continue;
@@ -1042,7 +1112,13 @@ __global__ void k_rb_memtab(int32_t n_steps, const int32_t* __restrict__ sgb,
       e.keep32 = (sw >> 8) & 1;
       e.fwd_row = tgt >= 0 ? kGuard + tgt : -1;
       e.fwd_buf = (sw & 1) ? 1 + (((sw >> 1) & 31) >> 4) : 0;
+      e.parent = tgt >= 0 ? fwd_parent[node] : -1;
       memtab[m] = e;
+      if (e.parent >= 0) {  // the conv3x3 #2 tiles covering this image, each counted once by the parent
+        const int32_t j = m - group_begin[g];
+        const int32_t t0 = (j * kImg + kLead) / tile_m, t1 = (j * kImg + kImg - 1 + kLead) / tile_m;
+        atomicAdd(need + e.parent, t1 - t0 + 1);
+      }
       // operands no child epilogue forwards: leaves (list 0) and children
       // shared by several parents (list 1), one gather task each
       for (int k = 0; k < arity; ++k) {
@@ -1183,16 +1259,17 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
                            int32_t* step_bintile_begin, int32_t* step_positions, int32_t* tile_group,
                            int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, int64_t n_nodes,
                            const int32_t* member_g, const int32_t* child0, const int32_t* child1,
-                           const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t tile_m,
-                           void* stream) {
+                           const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t* fwd_parent,
+                           int32_t* need, int32_t tile_m, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n_steps <= 0) return 0;
   k_rb_plan<<<1, 1024, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
                                group_tile0, group_bintile0, step_tile_begin, step_bintile_begin,
                                step_positions, tile_group, tile_q0, bin_group, bin_q0, tile_m);
-  k_rb_fwd_init<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_nodes, fwd_pos, fwd_slot);
+  k_rb_fwd_init<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_nodes, fwd_pos, fwd_slot,
+                                                                              fwd_parent, need);
   k_rb_fwd<<<148 * 4, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
-                                   member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot);
+                                   member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot, fwd_parent);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -1219,14 +1296,15 @@ extern "C" int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, c
                              const int32_t* fwd_pos, const int32_t* fwd_slot, const int32_t* arity_of,
                              const int32_t* fid, const int32_t* child0, const int32_t* child1,
                              const int32_t* example, const int32_t* fwd_ok, const float* inputs, float* values,
-                             void* memtab, void* tasks, int32_t* n_tasks, int64_t task_cap, void* stream) {
+                             void* memtab, void* tasks, int32_t* n_tasks, int64_t task_cap,
+                             const int32_t* fwd_parent, int32_t* need, int32_t tile_m, void* stream) {
   if (n_steps <= 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaMemsetAsync(n_tasks, 0, 2 * sizeof(int32_t), s);
   k_rb_memtab<<<148 * 4, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, seg_start, member_g,
                                       fwd_pos, fwd_slot, arity_of, fid, child0, child1, example, fwd_ok, inputs,
                                       values, static_cast<MemberEntry*>(memtab), static_cast<GatherTask*>(tasks),
-                                      n_tasks, task_cap);
+                                      n_tasks, task_cap, fwd_parent, need, tile_m);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -1253,8 +1331,8 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
                            int64_t plane_stride, const void* const* w0, const void* const* w1,
                            const void* const* w2, const float* const* b0, const float* const* b1,
                            const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
-                           int32_t* step_done, int32_t* queue, int32_t* err, int32_t tile_m, int32_t num_sms,
-                           void* stream) {
+                           int32_t* step_done, int32_t* queue, int32_t* err, int32_t* ready, const int32_t* need,
+                           const int32_t* member_g, int32_t tile_m, int32_t num_sms, void* stream) {
   if (tile_m != 256 && tile_m != 128) return static_cast<int>(cudaErrorInvalidValue);
   dbk_rb_configure();
   StepParams p{};
@@ -1299,6 +1377,11 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
   p.step_done = step_done;
   p.queue = queue;
   p.err = err;
+  p.ready = ready;
+  p.need = need;
+  p.member_g = member_g;
+  const char* sb = std::getenv("DYNBATCH_STEP_BARRIER");
+  p.step_barrier = sb ? std::atoi(sb) : 0;  // default: per-image dependencies only
   // persistent: one CTA per SM, in clusters of kCluster
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(num_sms / kCluster * kCluster));
