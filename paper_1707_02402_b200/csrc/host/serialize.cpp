@@ -29,17 +29,43 @@ struct Out {
   void indent(int level) { s.append(static_cast<size_t>(2 * level), ' '); }
 };
 
+// nlohmann's number layout (serializer::dump_float -> to_chars ->
+// format_buffer, min_exp -4, max_exp 15): the shortest round-trip digits
+// d1..dk with decimal exponent n (value = 0.d1..dk × 10^n) are written
+// fixed when -4 < n <= 15 (with a trailing ".0" for integers), else as
+// d[.ddd]e±XX with at least two exponent digits.
 std::string number(double v) {
   if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
   if (!std::isfinite(v)) return "null";
-  char buf[40];
+  char buf[48];
   for (int prec = 1; prec <= 17; ++prec) {
-    std::snprintf(buf, sizeof buf, "%.*g", prec, v);
+    std::snprintf(buf, sizeof buf, "%.*e", prec - 1, v);
     if (std::strtod(buf, nullptr) == v) break;
   }
-  std::string t(buf);
-  if (t.find_first_of(".e") == std::string::npos) t += ".0";
-  return t;
+  const std::string t(buf);
+  const size_t e_at = t.find('e');
+  std::string digits;
+  for (size_t i = 0; i < e_at; ++i)
+    if (t[i] >= '0' && t[i] <= '9') digits += t[i];
+  while (digits.size() > 1 && digits.back() == '0') digits.pop_back();
+  const int k = static_cast<int>(digits.size());
+  const int n = std::atoi(t.c_str() + e_at + 1) + 1;
+  std::string s = v < 0 ? "-" : "";
+  if (k <= n && n <= 15) {
+    s += digits + std::string(static_cast<size_t>(n - k), '0') + ".0";
+  } else if (0 < n && n <= 15) {
+    s += digits.substr(0, static_cast<size_t>(n)) + "." + digits.substr(static_cast<size_t>(n));
+  } else if (-4 < n && n <= 0) {
+    s += "0." + std::string(static_cast<size_t>(-n), '0') + digits;
+  } else {
+    s += digits.substr(0, 1);
+    if (k > 1) s += "." + digits.substr(1);
+    const int e = n - 1;
+    char eb[8];
+    std::snprintf(eb, sizeof eb, "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
+    s += eb;
+  }
+  return s;
 }
 
 // ---------------------------------------------------------------- parser
