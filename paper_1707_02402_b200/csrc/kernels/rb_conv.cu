@@ -133,20 +133,41 @@ struct PosEntry {
   int32_t valid;    // a real pixel of a real member
   int32_t pad;
 };
-constexpr int kTableBytes = 2 * kTileM * static_cast<int>(sizeof(PosEntry));  // double-buffered
+// Per-tile extras next to the position table: the tile's bias vector and
+// the nodes whose operand images a conv3x3 #2 tile completes (its publish).
+struct TileExtra {
+  float bias[kC];
+  int32_t parent[4];  // −1: none
+};
+constexpr int kTableBytes = 2 * kTileM * static_cast<int>(sizeof(PosEntry)) +
+                            2 * static_cast<int>(sizeof(TileExtra));  // double-buffered
 
+// A claimed work item with the group metadata every role needs, loaded once
+// by the scheduler (the other roles read it from shared memory instead of
+// chasing group → function → weight / bias pointers in global memory at every
+// tile and phase start).
 struct Item {
   int32_t kind;  // 0 conv1x1, 1 conv3x3 #1, 2 conv3x3 #2, -1 end
   int32_t tile;  // global tile index (bin-tile list for kind 0)
   int32_t g, q0;
   int32_t step;
+  int32_t gb0;     // group_begin[g]: the group's first member
+  int32_t rows;    // members (images) in the group's segment
+  int32_t seg;     // seg_start[g]: absolute staging row of the first image
+  int32_t binary;  // the group has conv1x1 tiles (binary function)
+  int32_t bin_t0;  // binary: the step's first bin tile of this group
+  int32_t tile_t0;  // the step's first (conv3x3) tile of this group
+  const uint8_t* w;   // weights of the tile's conv (conv3x3 #2: W2)
+  const float* bias;  // bias of the tile's conv
 };
 
 struct StepParams {
   int32_t step, step_end;  // the launch runs steps [step, step_end), step s + 1 after all of step s
   int32_t epoch, lookahead, debug;
   int32_t diag;  // timing diagnostics only (wrong results): bit 0 skips weight reloads, bit 1 window
-                 // reloads, bit 2 the epilogue work (TMEM loads, transposes, stores), bit 3 only its stores
+                 // reloads, bit 2 the epilogue work (TMEM loads, transposes, stores), bit 3 only its stores,
+                 // bit 4 aims the stores at one L2-resident slot, bit 5 skips every dependency wait,
+                 // bit 6 drops the weight-stage handshake (MMAs read stale stages), bit 7 the window one
   int32_t cache;  // bit 2: drop consumed interior mid lines from L2 (discard; default on)
   const int32_t* step_tile_begin;
   const int32_t* tile_group;
@@ -238,13 +259,12 @@ struct Phase {
 __device__ __forceinline__ int n_phases(int kind) { return kind == 2 ? 3 : 1; }
 
 __device__ __forceinline__ Phase phase_of(const StepParams& P, const Item& it, int p) {
-  const int32_t f = P.group_fid[it.g];
-  if (it.kind == 0) return Phase{P.stage_cat, P.wpack[0][f], 4, 1, 0};
-  if (it.kind == 1) return Phase{P.stage_x, P.wpack[1][f], 2, 9, kHalo};
+  if (it.kind == 0) return Phase{P.stage_cat, it.w, 4, 1, 0};
+  if (it.kind == 1) return Phase{P.stage_x, it.w, 2, 9, kHalo};
   // conv3x3 #2: the residual phases first — they read this block's input
   // images, which this launch's conv3x3 #1 tiles do not write, so they load
   // and run while the producer waits for the mid tiles
-  if (p == 2) return Phase{P.stage_mid, P.wpack[2][f], 2, 9, kHalo};
+  if (p == 2) return Phase{P.stage_mid, it.w, 2, 9, kHalo};
   return Phase{p == 0 ? P.stage_x : P.stage_lo, P.ident, 2, 1, 0};
 }
 
@@ -298,6 +318,19 @@ __device__ __forceinline__ Item step_item(const StepParams& P, int32_t step, int
     it.g = P.tile_group[it.tile];
     it.q0 = P.tile_q0[it.tile];
   }
+  // group metadata: independent loads, one round trip; then the weight and
+  // bias pointers of the group's function
+  const int32_t g = it.g;
+  const int32_t f = P.group_fid[g];
+  it.gb0 = P.group_begin[g];
+  it.rows = P.group_begin[g + 1] - it.gb0;
+  it.seg = P.seg_start[g];
+  const int32_t bt = P.group_bintile0[g];
+  it.binary = bt >= 0;
+  it.bin_t0 = bt >= 0 ? P.step_bintile_begin[step] + bt : 0;
+  it.tile_t0 = P.step_tile_begin[step] + P.group_tile0[g];
+  it.w = P.wpack[kind][f];
+  it.bias = P.bias[kind][f];
   return it;
 }
 
@@ -313,10 +346,9 @@ __device__ __forceinline__ void images_overlapping(int32_t lo, int32_t hi, int32
 // for each image's node. Relaxed polls, then one acquire fence.
 template <int TM>
 __device__ __forceinline__ void step_wait_images(const StepParams& P, const Item& it, int32_t halo) {
-  const int32_t g = it.g;
-  const int32_t gb0 = P.group_begin[g];
-  const int32_t rows = P.group_begin[g + 1] - gb0;
-  const int32_t base = it.q0 - P.seg_start[g];
+  const int32_t gb0 = it.gb0;
+  const int32_t rows = it.rows;
+  const int32_t base = it.q0 - it.seg;
   int32_t j0, j1;
   images_overlapping(base - halo, base + TM + halo, rows, j0, j1);
   bool waited = false;
@@ -342,7 +374,8 @@ __device__ __forceinline__ void step_wait_images(const StepParams& P, const Item
 // tile i). Halo positions in other segments only feed outputs never stored.
 template <int TM>
 __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& it, int phase) {
-  const bool binary_group = P.group_bintile0[it.g] >= 0;
+  if (P.diag & 32) return;
+  const bool binary_group = it.binary;
   // operand images from earlier steps: conv1x1 reads [x; y] at its own
   // rows, conv3x3 #1 of a unary group reads x with the halo, conv3x3 #2 of a
   // unary group reads x hi / lo (the residual) at its own rows
@@ -353,11 +386,10 @@ __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& 
   }
   if (!binary_group && (it.kind == 1 || phase == 0)) step_wait_images<TM>(P, it, it.kind == 1 ? kHalo : 0);
   const int32_t g = it.g;
-  const int32_t rows = P.group_begin[g + 1] - P.group_begin[g];
-  const int32_t nt = seg_tiles(rows, TM);
-  const int32_t i = (it.q0 - P.seg_start[g] + kLead) / TM;
-  const bool binary = P.group_bintile0[g] >= 0;
-  const int32_t b0 = binary ? P.step_bintile_begin[it.step] + P.group_bintile0[g] : 0;
+  const int32_t nt = seg_tiles(it.rows, TM);
+  const int32_t i = (it.q0 - it.seg + kLead) / TM;
+  const bool binary = it.binary;
+  const int32_t b0 = it.bin_t0;
   if (it.kind == 1) {
     if (!binary) return;
     for (int32_t j = max(i - 1, 0); j <= min(i + 1, nt - 1); ++j) wait_flag(P.done0 + b0 + j, P.epoch);
@@ -365,7 +397,7 @@ __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& 
     if (!binary) return;
     wait_flag(P.done0 + b0 + i, P.epoch);
   } else {  // conv3x3 #2, W2 phase: mid of tiles i-1..i+1
-    const int32_t t0 = P.step_tile_begin[it.step] + P.group_tile0[g];
+    const int32_t t0 = it.tile_t0;
     for (int32_t j = max(i - 1, 0); j <= min(i + 1, nt - 1); ++j) wait_flag(P.done1 + t0 + j, P.epoch);
   }
   fence_proxy_async_global();
@@ -376,11 +408,22 @@ __device__ __forceinline__ void step_wait_deps(const StepParams& P, const Item& 
 // the per-member table: one independent 32-byte load per position, all
 // issued before any entry is stored.
 template <int TM>
-__device__ __forceinline__ void rb_fill_table(const StepParams& P, const Item& it, PosEntry* tab, int lane) {
+__device__ __forceinline__ void rb_fill_table(const StepParams& P, const Item& it, PosEntry* tab, TileExtra* ex,
+                                              int lane) {
+  reinterpret_cast<float4*>(ex->bias)[lane] = __ldg(reinterpret_cast<const float4*>(it.bias) + lane);
+  if (lane < 4) {
+    int32_t parent = -1;
+    if (it.kind == 2) {
+      int32_t j0, j1;
+      images_overlapping(it.q0 - it.seg, it.q0 - it.seg + TM, it.rows, j0, j1);
+      if (j0 + lane <= j1) parent = P.memtab[it.gb0 + j0 + lane].parent;
+    }
+    ex->parent[lane] = parent;
+  }
   constexpr int kPer = TM / 32;
-  const int32_t gb0 = P.group_begin[it.g];
-  const int32_t rows = P.group_begin[it.g + 1] - gb0;
-  const int32_t base = it.q0 - P.seg_start[it.g];
+  const int32_t gb0 = it.gb0;
+  const int32_t rows = it.rows;
+  const int32_t base = it.q0 - it.seg;
   MemberEntry me[kPer];
   int32_t rem[kPer], px[kPer];
   bool valid[kPer], in_img[kPer];
@@ -463,11 +506,11 @@ struct EpiLane {
 };
 
 template <int KIND, int TM>
-__device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntry* tab, const EpiLane& L,
-                                              uint32_t taddr, const Item& it) {
-  const float* bias_p = P.bias[KIND][P.group_fid[it.g]] + L.plane * 8;
-  const float4 b_lo = __ldg(reinterpret_cast<const float4*>(bias_p));
-  const float4 b_hi = __ldg(reinterpret_cast<const float4*>(bias_p + 4));
+__device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntry* tab, const TileExtra* ex,
+                                              const EpiLane& L, uint32_t taddr, const Item& it) {
+  const float* bias_p = ex->bias + L.plane * 8;
+  const float4 b_lo = *reinterpret_cast<const float4*>(bias_p);
+  const float4 b_hi = *reinterpret_cast<const float4*>(bias_p + 4);
   const float bias[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
   // own-position outputs (conv1x1 → z hi/lo, conv3x3 #1 → mid): row
   // kGuard + q0 + 128·half + 16·cb + 8m + e, so (row & 7) == e
@@ -578,7 +621,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
   }
 #ifndef DYNBATCH_NO_RANGE_CHECK
   const float2 hm = __half22float2(hmax);
-  if (!(fmaxf(hm.x, hm.y) <= 65504.f) || !(fmax32 <= 3.4e38f)) atomicCAS(P.err, 0, kErrNonFinite);
+  if ((!(fmaxf(hm.x, hm.y) <= 65504.f) || !(fmax32 <= 3.4e38f)) && P.diag == 0) atomicCAS(P.err, 0, kErrNonFinite);
 #endif
 }
 
@@ -589,6 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
   uint8_t* sA = smem;
   uint8_t* sB = smem + kASlots * kASlot;
   PosEntry* tables = reinterpret_cast<PosEntry*>(sB + kBStages * kBStage);
+  TileExtra* extras = reinterpret_cast<TileExtra*>(tables + 2 * kTileM);
   Item* items = reinterpret_cast<Item*>(reinterpret_cast<uint8_t*>(tables) + kTableBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(items + kItemSlots);
   uint64_t* a_full = bars;
@@ -704,6 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           const uint32_t rows = TM + 2 * ph.halo;
           const uint8_t* src = ph.src + (static_cast<int64_t>(kGuard + it.q0 - ph.halo) << 7);
           for (int ch = 0; ch < ph.chunks; ++ch, ++ai) {
+            if (P.diag & 128) continue;  // timing: no window handshakes
             const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
             const long long c1 = DBG ? clock64() : 0;
             mbar_wait(a_empty + sa, pa ^ 1);
@@ -757,15 +802,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           for (int ch = 0; ch < chunks; ++ch, ++ai) {
             const uint32_t sa = ai % kASlots, pa = (ai / kASlots) & 1;
             if (DBG) c0 = clock64();
-            mbar_wait(a_full + sa, pa);
+            if (!(P.diag & 128)) mbar_wait(a_full + sa, pa);
             if (DBG) w_a += clock64() - c0;
             tc_fence_after();
             const uint32_t a_slot = a_base + sa * kASlot;
             for (int tap = 0; tap < taps; ++tap, ++bi) {
               const uint32_t s = bi % kBStages, par = (bi / kBStages) & 1;
               if (DBG) c0 = clock64();
-              mbar_wait(b_full + s, par);
-              if (DBG) w_b += clock64() - c0;
+              if (!(P.diag & 64)) mbar_wait(b_full + s, par);
+              if (DBG) {
+                const long long dw = clock64() - c0;
+                w_b += dw;
+                // [46] weight waits on a tile's first stage, [47] on the others
+                atomicAdd(&g_conv_dbg[(p == 0 && ch == 0 && tap == 0) ? 46 : 47], static_cast<unsigned long long>(dw));
+              }
               tc_fence_after();
               const int shift = taps == 9 ? (tap / 3 - 1) * 15 + (tap % 3 - 1) : 0;
               const uint32_t xrow = static_cast<uint32_t>(halo + shift);
@@ -776,10 +826,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
                 mma_bf16(tmem_base + abuf * TM, wd, xd, IDESC, acc);
                 acc = 1;
               }
+              if (P.diag & 64) continue;  // timing: weight stages never handed back
               if (kCluster == 1) mma_commit(b_empty + s);
               else mma_commit_mc(b_empty + s, 0x3);  // both CTAs' copies of the stage are free
             }
-            mma_commit(a_empty + sa);
+            if (!(P.diag & 128)) mma_commit(a_empty + sa);
           }
         }
         mma_commit(acc_full + abuf);
@@ -802,18 +853,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
   } else if (warp == kWeightWarp) {
     if (lane == 0) {  // -------------------------------------- weight stages
       uint32_t bi = 0;
+      long long w_it = 0, w_e = 0;
+      const long long t_start = DBG ? clock64() : 0;
       for (int n = 0;; ++n) {
         const int slot = n % kItemSlots;
+        long long c0 = DBG ? clock64() : 0;
         mbar_wait(item_full + slot, (n / kItemSlots) & 1);
+        if (DBG) w_it += clock64() - c0;
         const Item it = items[slot];
         mbar_arrive(item_empty + slot);
         if (it.kind < 0) break;
+        if (P.diag & 64) continue;  // timing: no weight stages
         for (int p = 0; p < n_phases(it.kind); ++p) {
           const Phase ph = phase_of(P, it, p);
           for (int ch = 0; ch < ph.chunks; ++ch) {
             for (int tap = 0; tap < ph.taps; ++tap, ++bi) {
               const uint32_t s = bi % kBStages, par = (bi / kBStages) & 1;
+              if (DBG) c0 = clock64();
               mbar_wait(b_empty + s, par ^ 1);
+              if (DBG) w_e += clock64() - c0;
               if ((P.diag & 1) && bi >= kBStages) {
                 mbar_arrive(b_full + s);
                 continue;
@@ -830,6 +888,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           }
         }
       }
+      if (DBG) {  // [48] weight warp: item waits, [49] free-stage waits, [50] total
+        atomicAdd(&g_conv_dbg[48], static_cast<unsigned long long>(w_it));
+        atomicAdd(&g_conv_dbg[49], static_cast<unsigned long long>(w_e));
+        atomicAdd(&g_conv_dbg[50], static_cast<unsigned long long>(clock64() - t_start));
+      }
     }
   } else if (warp == kTableWarp) {  // ------------------------ table filler
     for (int n = 0;; ++n) {
@@ -841,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       if (it.kind < 0) break;
       const int buf = n & 1;
       mbar_wait(tab_empty + buf, ((n >> 1) & 1) ^ 1);
-      rb_fill_table<TM>(P, it, tables + buf * TM, lane);
+      rb_fill_table<TM>(P, it, tables + buf * TM, extras + buf, lane);
       mbar_arrive(tab_full + buf);  // release: the entries are visible to the waiters
     }
   } else {  // ------------------------------------------------------ epilogue
@@ -863,6 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       if (it.kind < 0) break;
       const int abuf = n & 1;
       const PosEntry* tab = tables + abuf * TM;
+      const TileExtra* ex = extras + abuf;
       mbar_wait(tab_full + abuf, (n >> 1) & 1);
       mbar_wait(acc_full + abuf, (n >> 1) & 1);
       tc_fence_after();
@@ -870,11 +934,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
       const uint32_t taddr = tmem_base + abuf * TM + lane_addr;
       if (P.diag & 4) {
       } else if (it.kind == 0) {
-        step_epilogue<0, TM>(P, tab, L, taddr, it);
+        step_epilogue<0, TM>(P, tab, ex, L, taddr, it);
       } else if (it.kind == 1) {
-        step_epilogue<1, TM>(P, tab, L, taddr, it);
+        step_epilogue<1, TM>(P, tab, ex, L, taddr, it);
       } else {
-        step_epilogue<2, TM>(P, tab, L, taddr, it);
+        step_epilogue<2, TM>(P, tab, ex, L, taddr, it);
         if (P.cache & 4) {
           // the interior mid rows [q0 + 16, q0 + 240) of this tile are read
           // by this tile's conv3x3 #2 only (its neighbours' windows stop 16
@@ -887,6 +951,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
             discard_l2_line(P.stage_mid + ((static_cast<int64_t>(c) * P.ps + kGuard + it.q0 + r) << 7));
           }
         }
+      }
+      // the publishing thread keeps the tile's parents before the table
+      // buffer is handed back
+      int32_t parents[4] = {-1, -1, -1, -1};
+      if (threadIdx.x == 64 && it.kind == 2) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) parents[j] = ex->parent[j];
       }
       tc_fence_before();
       mbar_arrive(acc_empty + abuf);
@@ -902,14 +973,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         } else {
           red_release_gpu_add(P.step_done + it.step, 1);
           // this tile's part of each parent's operand image is written
-          const int32_t gb0 = P.group_begin[it.g];
-          const int32_t base = it.q0 - P.seg_start[it.g];
-          int32_t j0, j1;
-          images_overlapping(base, base + TM, P.group_begin[it.g + 1] - gb0, j0, j1);
-          for (int32_t j = j0; j <= j1; ++j) {
-            const int32_t parent = P.memtab[gb0 + j].parent;
-            if (parent >= 0) red_release_gpu_add(P.ready + parent, 1);
-          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (parents[j] >= 0) red_release_gpu_add(P.ready + parents[j], 1);
         }
         if (DBG) {
           atomicAdd(&g_conv_dbg[36 + 2 * it.kind], static_cast<unsigned long long>(clock64() - t_epi));

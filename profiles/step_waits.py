@@ -21,7 +21,9 @@ acc, a, bb, tot = w[12:16]
 out = {"ms_per_forward": ms / 5, "mma_thread": {"acc_wait": acc / tot, "window_wait": a / tot, "weight_wait": bb / tot,
                                                 "busy": (tot - acc - a - bb) / tot},
        "producer": {"item_ring": w[16] / w[19], "dependency": w[17] / w[19], "slot": w[18] / w[19]},
-       "mma_loop_mhz": w[20] / max(w[21], 1) * 1e3, "per_kind": {}}
+       "mma_loop_mhz": w[20] / max(w[21], 1) * 1e3, "per_kind": {},
+       "weight_wait_split": {"first_stage_of_tile": w[46] / tot, "other_stages": w[47] / tot},
+       "weight_warp": {"item_wait": w[48] / max(w[50], 1), "stage_free_wait": w[49] / max(w[50], 1)}}
 for k, name in enumerate(("conv1x1", "conv3x3_1", "conv3x3_2")):
     cyc, wa, wb, wacc = w[24 + 4 * k: 28 + 4 * k]
     ecyc, etiles = w[36 + 2 * k: 38 + 2 * k]

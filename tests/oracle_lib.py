@@ -405,3 +405,34 @@ def moe_forward(inputs, ids, weights, n, h, expert_seed, use_ref=False, subset=N
                                       _ptr(trace, P_I64), _ptr(secs, P_F64))
     assert rc == 0, rc
     return out, trace, secs
+
+
+def schedule_naive(bt: Batch) -> FlatSchedule:
+    """schedule_naive (src/schedule.cpp:94-105): one step per node, examples
+    in order, each program's nodes in postorder_flatten order (children
+    first, src/program.cpp:274-298). Python loops: small batches only (the
+    bench's CPU naive sample and tests)."""
+    sgo, gf, gmo, me, mn = [0], [], [0], [], []
+    for e in range(bt.b):
+        off = int(bt.prog_off[e])
+        order, done, stack = [], set(), [[int(bt.root[e]), 0]]
+        while stack:
+            fr = stack[-1]
+            kids = [c for c in (int(bt.child0[off + fr[0]]), int(bt.child1[off + fr[0]])) if c >= 0]
+            if fr[1] < len(kids):
+                c = kids[fr[1]]
+                fr[1] += 1
+                if c not in done:
+                    stack.append([c, 0])
+            else:
+                done.add(fr[0])
+                order.append(fr[0])
+                stack.pop()
+        for node in order:
+            gf.append(int(bt.fid[off + node]))
+            me.append(e)
+            mn.append(node)
+            gmo.append(len(me))
+            sgo.append(len(gf))
+    a = lambda v: np.asarray(v, np.int32)  # noqa: E731
+    return FlatSchedule(a(sgo), a(gf), a(gmo), a(me), a(mn), "naive")

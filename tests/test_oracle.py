@@ -170,3 +170,12 @@ def test_moe_sampled_tokens_equal_full_forward():
     sids, sw, out = M.reference_tokens(n, k, d, h, seed, toks)
     assert np.array_equal(sids, ids[toks]) and np.array_equal(sw, w[toks])
     assert np.max(np.abs(out - ref[toks])) <= 1e-12
+
+
+@needs_ref
+@pytest.mark.parametrize("kind,seed", [("chain", 1), ("balanced", 2), ("dag", 3)])
+def test_naive_schedule_equals_reference(kind, seed):
+    """oracle_lib.schedule_naive (the bench's CPU naive leg) is the reference's
+    schedule_naive (src/schedule.cpp:94-105), step for step."""
+    bt = O.gen_batch(kind, 12, p=16, depth=4, length=10, bp=0.3, seed=seed)
+    assert O.schedule_naive(bt) == O.ref_schedule(bt, "naive")
