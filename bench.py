@@ -215,10 +215,12 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------- CPU oracle
-def cpu_sample_run(cfg, n_programs, threads, seed=0):
+def cpu_sample_run(cfg, n_programs, threads, seed=0, strategy="improved"):
     """Runs the oracle port (fp64, reference executor semantics) on the first
     n_programs of the workload, sharded over `threads` host threads (ctypes
-    releases the GIL). Returns (seconds, programs)."""
+    releases the GIL), each shard scheduled with schedule_improved or
+    schedule_naive (src/schedule.cpp:94-105, one node per step). Returns
+    (seconds, programs)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib as O
     ob = O.gen_batch(cfg["kind"], n_programs, p=cfg["vocab"], depth=cfg["depth"],
@@ -235,7 +237,8 @@ def cpu_sample_run(cfg, n_programs, threads, seed=0):
                      np.where(ob.child0[lo:hi] >= 0, ob.child0[lo:hi], -1).astype(np.int32),
                      np.where(ob.child1[lo:hi] >= 0, ob.child1[lo:hi], -1).astype(np.int32),
                      ob.root[a:z].copy(), ob.p)
-        shards.append((sb, O.schedule_improved(sb), np.ascontiguousarray(x[a:z])))
+        fs = O.schedule_naive(sb) if strategy == "naive" else O.schedule_improved(sb)
+        shards.append((sb, fs, np.ascontiguousarray(x[a:z])))
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=len(shards)) as pool:
         res = list(pool.map(lambda s: O.execute(s[0], s[1], s[2], ms, "resblock"), shards))
@@ -256,6 +259,30 @@ def calibrate_cpu(cfg, target_s):
     dt, n = cpu_sample_run(cfg, threads, threads)  # one program per thread
     rounds = max(1, min(64, int(target_s / max(dt, 1e-3))))
     return threads, threads * rounds
+
+
+def cpu_baselines(cfg, target_s):
+    """The CPU baselines of SURVEY.md §8(d), timed on this box's host cores
+    with the fp64 oracle port: (i) improved schedule on every host thread
+    (the headline cpu_baseline), (ii) one thread, giving the host-core
+    scaling, (iii) the naive per-example schedule on every thread."""
+    threads, n = calibrate_cpu(cfg, target_s)
+    dt, n = cpu_sample_run(cfg, n, threads)
+    per_prog_thread = dt * threads / n  # seconds per program on one thread (approx.)
+    n1 = max(2, int(min(target_s / 3, 6.0) / max(per_prog_thread, 1e-4)))
+    dt1, _ = cpu_sample_run(cfg, n1, 1)
+    nn = max(threads, n // 2)
+    dtn, _ = cpu_sample_run(cfg, nn, threads, strategy="naive")
+    v, v1, vn = n / dt, n1 / dt1, nn / dtn
+    return {"value": v, "unit": "programs/s", "cores": threads, "kind": "port",
+            "sample": f"first {n} programs of the workload, oracle fp64 port (oracle/dynbatch_oracle.c, "
+                      f"schedule_improved) sharded over {threads} threads, {dt:.1f} s",
+            "single_thread": {"value": v1, "sample": f"first {n1} programs on 1 thread, {dt1:.1f} s"},
+            "host_core_scaling": {"threads": threads, "speedup_vs_1_thread": v / v1,
+                                  "efficiency": v / v1 / threads},
+            "naive": {"value": vn, "schedule": "schedule_naive (one node per step), same executor",
+                      "sample": f"first {nn} programs over {threads} threads, {dtn:.1f} s",
+                      "improved_over_naive": v / vn}}
 
 
 def pcie_duplex_seconds(nbytes, nbytes_out=None, reps=3):
@@ -464,13 +491,7 @@ def run_ours(args, dist):
                              "fused step kernel measured itself (clock64 / globaltimer): the board power limit "
                              "holds it below sm_max_mhz while the tensor cores and HBM are busy")
     if dist.rank == 0 and N == 1 and not args.no_cpu_baseline:
-        threads, n = calibrate_cpu(cfg, args.cpu_seconds)
-        dt, n = cpu_sample_run(cfg, n, threads)
-        out["cpu_baseline"] = {"value": n / dt, "unit": "programs/s", "cores": threads,
-                               "kind": "port",
-                               "sample": f"first {n} programs of the workload, oracle fp64 port "
-                                         f"(oracle/dynbatch_oracle.c) sharded over {threads} threads, "
-                                         f"{dt:.1f} s"}
+        out["cpu_baseline"] = cpu_baselines(cfg, args.cpu_seconds)
     return out
 
 
@@ -548,7 +569,31 @@ def run_moe(args, dist, name, secondary=False):
                          "copies overlap the neighbouring steps' forwards)",
                   "roofline": {"bound": "pcie (H2D and D2H concurrent)", "achieved_h2d_gbs": round(h2d / e2e_s / 1e9, 1),
                                "peak_h2d_gbs": round(h2d / link_s / 1e9, 1), "frac": round(link_s / e2e_s, 4)}}
+    if dist.rank == 0 and N == 1 and not args.no_cpu_baseline and not secondary:
+        res["cpu_baseline"] = moe_cpu_baselines(c)
     return res
+
+
+def moe_cpu_baselines(c, tokens=1024, naive_tokens=256):
+    """The compiled reference's own MoE layer (oracle/_ref: moe_forward_batched
+    and moe_forward_naive, src/moe.cpp:162-270, fp64, single-threaded as
+    shipped) on the first `tokens` tokens of the workload, timed by its own
+    trace (total_seconds; the ExpertSet construction is outside it)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+    if not O.ref_available():
+        return {"unavailable": "oracle/_ref not built"}
+    n, k, d, h = c["experts"], c["k"], c["d"], c["h"]
+    out = {"unit": "tokens/s", "cores": 1, "kind": "reference"}
+    for name, T, batched in (("batched", tokens, True), ("naive", naive_tokens, False)):
+        x, sc = O.moe_inputs(T, n, d, 0)
+        ids, w = O.topk(sc, k, use_ref=True)
+        _, _, secs = O.moe_forward(x, ids, w, n, h, O.mix_seed(0, 0xe4be27), use_ref=True, batched=batched)
+        out[name] = {"value": T / secs[2], "sample": f"first {T} tokens, {secs[2]:.2f} s (trace total_seconds)"}
+    out["value"] = out["batched"]["value"]
+    out["sample"] = out["batched"]["sample"] + ", moe_forward_batched on 1 thread"
+    out["batched_over_naive"] = out["batched"]["value"] / out["naive"]["value"]
+    return out
 
 
 def run_moe_ep(args, dist, name):

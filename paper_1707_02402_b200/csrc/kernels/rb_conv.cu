@@ -168,7 +168,8 @@ struct StepParams {
                  // reloads, bit 2 the epilogue work (TMEM loads, transposes, stores), bit 3 only its stores,
                  // bit 4 aims the stores at one L2-resident slot, bit 5 skips every dependency wait,
                  // bit 6 drops the weight-stage handshake (MMAs read stale stages), bit 7 the window one
-  int32_t cache;  // bit 2: drop consumed interior mid lines from L2 (discard; default on)
+  int32_t cache;  // bit 2: drop consumed interior mid lines from L2 (discard; default on), bit 3: also the
+                  // block input's hi / lo lines
   const int32_t* step_tile_begin;
   const int32_t* tile_group;
   const int32_t* tile_q0;
@@ -257,6 +258,12 @@ struct Phase {
 };
 
 __device__ __forceinline__ int n_phases(int kind) { return kind == 2 ? 3 : 1; }
+
+// Timing diagnostics (wrong results): diag bit 8 skips conv3x3 #2's residual
+// phases (I·hi and I·lo), bit 9 only its I·lo phase.
+__device__ __forceinline__ bool phase_skipped(const StepParams& P, const struct Item& it, int p) {
+  return it.kind == 2 && ((p < 2 && (P.diag & 256)) || (p == 1 && (P.diag & 512)));
+}
 
 __device__ __forceinline__ Phase phase_of(const StepParams& P, const Item& it, int p) {
   if (it.kind == 0) return Phase{P.stage_cat, it.w, 4, 1, 0};
@@ -736,6 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           if (DBG) w_dep += clock64() - c0;
         }
         for (int p = 0; p < n_phases(it.kind); ++p) {
+          if (phase_skipped(P, it, p)) continue;
           if (p == 0 || p == 2) {  // conv3x3 #2 waits for the mid tiles only before its W2 phase
             if (DBG) c0 = clock64();
             step_wait_deps<TM>(P, it, p);
@@ -795,6 +803,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         tc_fence_after();
         uint32_t acc = 0;
         for (int p = 0; p < n_phases(it.kind); ++p) {
+          if (phase_skipped(P, it, p)) continue;
           const int chunks = it.kind == 0 ? 4 : 2;
           const bool conv3 = it.kind == 1 || (it.kind == 2 && p == 2);
           const int taps = conv3 ? 9 : 1;
@@ -865,6 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
         if (it.kind < 0) break;
         if (P.diag & 64) continue;  // timing: no weight stages
         for (int p = 0; p < n_phases(it.kind); ++p) {
+          if (phase_skipped(P, it, p)) continue;
           const Phase ph = phase_of(P, it, p);
           for (int ch = 0; ch < ph.chunks; ++ch) {
             for (int tap = 0; tap < ph.taps; ++tap, ++bi) {
@@ -945,10 +955,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
           // rows short), and its window is in shared memory by now: drop the
           // dirty lines from L2 instead of writing them back; conv3x3 #1
           // rewrites them (pads included) before any later read
+          // The same holds for the block input's hi / lo images (x of a unary
+          // group, z of a binary one) at these rows: conv3x3 #1 tiles i−1..i+1
+          // (done before this tile's W2 phase) and this tile's residual
+          // phases were their only readers; every forward rewrites them
+          // (images with their pads, and the segment gaps in stage_x).
           const int et = threadIdx.x - 64;  // 0 .. 255 over the epilogue warps
-          for (int i = et; i < 2 * (TM - 2 * kHalo); i += kEpiWarps * 32) {
-            const int c = i / (TM - 2 * kHalo), r = kHalo + i % (TM - 2 * kHalo);
-            discard_l2_line(P.stage_mid + ((static_cast<int64_t>(c) * P.ps + kGuard + it.q0 + r) << 7));
+          constexpr int kIn = TM - 2 * kHalo;
+          const int nbuf = (P.cache & 8) ? 3 : 1;
+          for (int i = et; i < nbuf * 2 * kIn; i += kEpiWarps * 32) {
+            const int b = i / (2 * kIn), c = (i / kIn) & 1, r = kHalo + i % kIn;
+            uint8_t* base = b == 0 ? P.stage_mid : (b == 1 ? P.stage_x : P.stage_lo);
+            discard_l2_line(base + ((static_cast<int64_t>(c) * P.ps + kGuard + it.q0 + r) << 7));
           }
         }
       }

@@ -384,7 +384,7 @@ def expert_weights(d, h, expert_seed, eid):
     return w1.reshape(d, h), w2.reshape(h, d)
 
 
-def moe_forward(inputs, ids, weights, n, h, expert_seed, use_ref=False, subset=None):
+def moe_forward(inputs, ids, weights, n, h, expert_seed, use_ref=False, subset=None, batched=True):
     T, d = inputs.shape
     k = ids.shape[1]
     out = np.zeros((T, d), np.float64)
@@ -395,7 +395,7 @@ def moe_forward(inputs, ids, weights, n, h, expert_seed, use_ref=False, subset=N
     weights = np.ascontiguousarray(weights, np.float64)
     if use_ref:
         rc = ref().refshim_moe_forward(_ptr(x, P_F64), T, d, h, n, k, _ptr(ids, P_I32),
-                                       _ptr(weights, P_F64), expert_seed, 1, _ptr(out, P_F64),
+                                       _ptr(weights, P_F64), expert_seed, 1 if batched else 0, _ptr(out, P_F64),
                                        _ptr(trace, P_I64), _ptr(secs, P_F64))
     else:
         sub = None if subset is None else np.ascontiguousarray(subset, np.int32)
