@@ -460,6 +460,19 @@ def run_ours(args, dist):
            "algorithmic_flops_per_step": stats.algorithmic_flops * N,
            "clocks": None}
 
+    # the IEP classifier head on the roots (conv1x1 → pool
+    # → FC → FC, tcgen05 GEMMs): device ms per head forward on this batch's
+    # roots, next to the module forward it follows
+    try:
+        sess.set_head(28, module_seed)
+        sess.forward()
+        hms, hfl = sess.time_head(max(args.steps, 5))
+        out["head"] = {"answers": 28, "ms_per_step": hms, "tflops": hfl / (hms / 1e3) / 1e12,
+                       "flops_per_step": hfl, "forward_plus_head_programs_per_s": B / ((ms_step + hms) / 1e3),
+                       "share_of_forward": hms / ms_step}
+    except Exception as e:  # reported, not fatal
+        out["head"] = {"error": str(e)}
+
     # naive per-example execution on the GPU (same kernels, one node per step)
     try:
         nb = min(per, 64)

@@ -203,6 +203,18 @@ int dbk_moe_tc_gemm(int32_t fmt, int32_t epi, int32_t n, int32_t K, int32_t N, c
                     const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
                     const void* const* W, void* H, void* Y, int32_t tile_begin, int32_t tile_end,
                     const int32_t* out_row, int32_t sms, void* stream);
+/* IEP classifier head operand moves (head.cu): roots → fp16 SW128 tiled
+ * rows (program·196 + px) × 128; projection output (tiled H, P columns) →
+ * 2×2 max pool → fp16 SW128 tiled rows (program) × 49·P. */
+int dbk_head_pack(int64_t b, const int32_t* root_g, const int32_t* fid, const int32_t* arity_of,
+                  const int32_t* example, const float* inputs, const float* values, void* A, void* stream);
+int dbk_head_pool(int64_t b, int32_t P, const void* H, void* A, void* stream);
+/* The same grouped GEMM with an optional per-expert fp32 bias [N] added in
+ * the epilogue, and epi 2 = fp32 row-major output (Y is then float*). */
+int dbk_tc_gemm_bias(int32_t fmt, int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
+                     const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
+                     const void* const* W, const float* const* bias, void* H, void* Y, int32_t tile_begin,
+                     int32_t tile_end, const int32_t* out_row, int32_t sms, void* stream);
 int dbk_moe_tc_combine(int32_t fmt, int64_t T, int32_t k, int32_t d, const double* weights,
                        const int32_t* row_of_item, const void* Y, float* out, void* stream);
 

@@ -146,6 +146,22 @@ DYNBATCH_API db_status db_iep_session_labels(db_iep_session* s, int32_t* labels,
  * per-kernel-class times (events around every launch). */
 DYNBATCH_API db_status db_iep_session_time(db_iep_session* s, int32_t iters, int32_t profile,
                                            double* ms, db_kernel_times_t* kt);
+/* IEP classifier head on the root maps (RESBLOCK sessions; SURVEY.md §8(f)4,
+ * beyond the reference, whose path ends at the root feature maps):
+ * conv1x1 128 → 512 + ReLU, 2×2 max pool, FC 25088 → 1024 + ReLU,
+ * FC 1024 → `answers` (≤ 256), fp16 tensor-core operands, fp32 logits.
+ * Weights Rng(mix_seed(seed, 0x4ead)) as oracle/dynbatch_oracle.c
+ * orc_head_weights. set_head creates (or replaces) it; head_forward enqueues
+ * it on the current roots (after a forward); logits downloads b × answers
+ * fp32; forward_logits_host = H2D rows → forward → head → D2H logits;
+ * time_head returns device ms per head forward (CUDA events). */
+DYNBATCH_API db_status db_iep_session_set_head(db_iep_session* s, int32_t answers, uint64_t seed);
+DYNBATCH_API db_status db_iep_session_head_forward(db_iep_session* s);
+DYNBATCH_API db_status db_iep_session_logits(db_iep_session* s, float* out, int64_t n);
+DYNBATCH_API db_status db_iep_session_forward_logits_host(db_iep_session* s, const float* inputs,
+                                                          float* logits);
+DYNBATCH_API db_status db_iep_session_time_head(db_iep_session* s, int32_t iters, double* ms,
+                                                double* flops);
 DYNBATCH_API void db_iep_session_free(db_iep_session* s);
 
 /* db_schedule_build on the device scheduler: IMPROVED, STANDARD or ONLINE

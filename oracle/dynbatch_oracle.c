@@ -778,3 +778,83 @@ int orc_moe_forward(const double* inputs, int64_t T, int64_t d, int64_t h, int64
   free(cnt);
   return 0;
 }
+
+/* ------------------------------------------------ IEP classifier head ---- */
+/* NOT IN THE REFERENCE (its path ends at the root feature maps, SPEC.md:13;
+ * SURVEY.md §8(f)4): the IEP classifier after Johnson et al., as the device
+ * head (head.cu) defines it. Init in the reference style
+ * (src/modules.cpp:13-28): Rng(mix_seed(seed, 0x4ead)), draws wp [C][P],
+ * bp[P], w1 [49P][F], b1[F], w2 [F][A], b2[A] (input-major), each
+ * uniform(-0.5, 0.5) / sqrt(fan_in). */
+void orc_head_weights(int C, int P, int F, int A, uint64_t seed, double* wp, double* bp, double* w1,
+                      double* b1, double* w2, double* b2) {
+  orc_rng r;
+  orc_rng_seed(&r, orc_mix_seed(seed, 0x4eadULL));
+  int64_t K1 = (int64_t)49 * P;
+  double sp = 1.0 / sqrt((double)C), s1 = 1.0 / sqrt((double)K1), s2 = 1.0 / sqrt((double)F);
+  for (int64_t i = 0; i < (int64_t)C * P; ++i) wp[i] = rng_range(&r, -0.5, 0.5) * sp;
+  for (int j = 0; j < P; ++j) bp[j] = rng_range(&r, -0.5, 0.5) * sp;
+  for (int64_t i = 0; i < K1 * F; ++i) w1[i] = rng_range(&r, -0.5, 0.5) * s1;
+  for (int j = 0; j < F; ++j) b1[j] = rng_range(&r, -0.5, 0.5) * s1;
+  for (int64_t i = 0; i < (int64_t)F * A; ++i) w2[i] = rng_range(&r, -0.5, 0.5) * s2;
+  for (int j = 0; j < A; ++j) b2[j] = rng_range(&r, -0.5, 0.5) * s2;
+}
+
+/* logits[e][a] of b root maps (CHW rows of C×14×14, the executor's output
+ * layout): proj = relu(conv1x1 + bp) [196][P]; pooled[q][c] = max over the
+ * 2×2 window q = ph·7 + pw; hidden = relu(w1ᵀ·flatten + b1) with flatten
+ * index q·P + c; logits = w2ᵀ·hidden + b2. fp64. */
+int orc_head_forward(int64_t b, const double* roots, int C, int P, int F, int A, uint64_t seed,
+                     double* logits) {
+  const int HW = 196;
+  int64_t K1 = (int64_t)49 * P;
+  double* wp = (double*)malloc(sizeof(double) * (size_t)C * P);
+  double* bp = (double*)malloc(sizeof(double) * (size_t)P);
+  double* w1 = (double*)malloc(sizeof(double) * (size_t)(K1 * F));
+  double* b1 = (double*)malloc(sizeof(double) * (size_t)F);
+  double* w2 = (double*)malloc(sizeof(double) * (size_t)F * A);
+  double* b2 = (double*)malloc(sizeof(double) * (size_t)A);
+  double* proj = (double*)malloc(sizeof(double) * (size_t)HW * P);
+  double* pooled = (double*)malloc(sizeof(double) * (size_t)K1);
+  double* hid = (double*)malloc(sizeof(double) * (size_t)F);
+  if (!wp || !bp || !w1 || !b1 || !w2 || !b2 || !proj || !pooled || !hid) return 1;
+  orc_head_weights(C, P, F, A, seed, wp, bp, w1, b1, w2, b2);
+  for (int64_t e = 0; e < b; ++e) {
+    const double* x = roots + e * (int64_t)C * HW;
+    for (int q = 0; q < HW; ++q) {
+      double* o = proj + (int64_t)q * P;
+      for (int c = 0; c < P; ++c) o[c] = bp[c];
+      for (int ci = 0; ci < C; ++ci) {
+        double xv = x[(int64_t)ci * HW + q];
+        const double* wr = wp + (int64_t)ci * P;
+        for (int c = 0; c < P; ++c) o[c] = fma(xv, wr[c], o[c]);
+      }
+      for (int c = 0; c < P; ++c) o[c] = o[c] > 0.0 ? o[c] : 0.0;
+    }
+    for (int q = 0; q < 49; ++q) {
+      int ph = q / 7, pw = q % 7;
+      for (int c = 0; c < P; ++c) {
+        double m = 0.0;
+        for (int t = 0; t < 4; ++t) {
+          int px = (2 * ph + t / 2) * 14 + 2 * pw + t % 2;
+          double v = proj[(int64_t)px * P + c];
+          m = (t == 0 || v > m) ? v : m;
+        }
+        pooled[(int64_t)q * P + c] = m;
+      }
+    }
+    for (int f = 0; f < F; ++f) hid[f] = b1[f];
+    for (int64_t k = 0; k < K1; ++k) {
+      double xv = pooled[k];
+      const double* wr = w1 + k * F;
+      for (int f = 0; f < F; ++f) hid[f] = fma(xv, wr[f], hid[f]);
+    }
+    for (int f = 0; f < F; ++f) hid[f] = hid[f] > 0.0 ? hid[f] : 0.0;
+    double* lo = logits + e * A;
+    for (int a = 0; a < A; ++a) lo[a] = b2[a];
+    for (int f = 0; f < F; ++f)
+      for (int a = 0; a < A; ++a) lo[a] = fma(hid[f], w2[(int64_t)f * A + a], lo[a]);
+  }
+  free(wp); free(bp); free(w1); free(b1); free(w2); free(b2); free(proj); free(pooled); free(hid);
+  return 0;
+}

@@ -76,6 +76,12 @@ int orc_moe_forward(const double* inputs, int64_t T, int64_t d, int64_t h, int64
                     const int32_t* expert_subset, int64_t n_subset, double* out, int64_t* trace,
                     double* seconds);
 
+/* IEP classifier head (beyond the reference). */
+void orc_head_weights(int C, int P, int F, int A, uint64_t seed, double* wp, double* bp, double* w1,
+                      double* b1, double* w2, double* b2);
+int orc_head_forward(int64_t b, const double* roots, int C, int P, int F, int A, uint64_t seed,
+                     double* logits);
+
 #ifdef __cplusplus
 }
 #endif

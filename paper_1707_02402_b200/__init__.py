@@ -153,6 +153,11 @@ SIGNATURES = {
     "db_iep_session_schedule": (C.c_int32, [VP, PVP]),
     "db_iep_session_run": (C.c_int32, [VP, PVP]),
     "db_iep_session_labels": (C.c_int32, [VP, VP, C.c_int64]),
+    "db_iep_session_set_head": (C.c_int32, [VP, C.c_int32, C.c_uint64]),
+    "db_iep_session_head_forward": (C.c_int32, [VP]),
+    "db_iep_session_logits": (C.c_int32, [VP, VP, C.c_int64]),
+    "db_iep_session_forward_logits_host": (C.c_int32, [VP, VP, VP]),
+    "db_iep_session_time_head": (C.c_int32, [VP, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "db_iep_session_free": (None, [VP]),
     "db_execute_device": (C.c_int32, [VP, VP, C.c_uint64, C.POINTER(ModuleOpts), PVP]),
     "db_moe_session_create": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, C.c_int64, C.c_int64,
@@ -487,6 +492,28 @@ class IepSession(_Handle):
         out = np.zeros(n_nodes, np.int32)
         check(lib().db_iep_session_labels(self.h, _ptr(out), n_nodes))
         return out
+
+    # IEP classifier head (db_iep_session_set_head …): conv1x1 → pool → FC → FC
+    def set_head(self, answers: int = 28, seed: int = 0):
+        check(lib().db_iep_session_set_head(self.h, answers, seed))
+        self._answers = answers
+
+    def head_forward(self):
+        check(lib().db_iep_session_head_forward(self.h))
+
+    def logits(self, b: int) -> np.ndarray:
+        out = np.zeros((b, self._answers), np.float32)
+        check(lib().db_iep_session_logits(self.h, _ptr(out), out.size))
+        return out
+
+    def forward_logits_host(self, inputs: np.ndarray, logits: np.ndarray):
+        check(lib().db_iep_session_forward_logits_host(self.h, _ptr(inputs), _ptr(logits)))
+
+    def time_head(self, iters: int):
+        """(device ms per head forward, algorithmic FLOPs per head forward)."""
+        ms, fl = C.c_double(), C.c_double()
+        check(lib().db_iep_session_time_head(self.h, iters, C.byref(ms), C.byref(fl)))
+        return ms.value, fl.value
 
 
 class MoeSession(_Handle):

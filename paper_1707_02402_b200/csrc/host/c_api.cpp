@@ -542,6 +542,34 @@ db_status db_iep_session_labels(db_iep_session* s, int32_t* labels, int64_t n) {
   });
 }
 
+db_status db_iep_session_set_head(db_iep_session* s, int32_t answers, uint64_t seed) {
+  if (!s) return null_arg();
+  return guarded([&] { s->s->set_head(answers, seed); });
+}
+
+db_status db_iep_session_head_forward(db_iep_session* s) {
+  if (!s) return null_arg();
+  return guarded([&] { s->s->head_forward(); });
+}
+
+db_status db_iep_session_logits(db_iep_session* s, float* out, int64_t n) {
+  if (!s || !out) return null_arg();
+  return guarded([&] { s->s->download_logits(out, n); });
+}
+
+db_status db_iep_session_forward_logits_host(db_iep_session* s, const float* inputs, float* logits) {
+  if (!s || !inputs || !logits) return null_arg();
+  return guarded([&] { s->s->forward_logits_host(inputs, logits); });
+}
+
+db_status db_iep_session_time_head(db_iep_session* s, int32_t iters, double* ms, double* flops) {
+  if (!s || !ms) return null_arg();
+  return guarded([&] {
+    *ms = s->s->time_head(iters);
+    if (flops) *flops = s->s->head_flops();
+  });
+}
+
 void db_iep_session_free(db_iep_session* s) { delete s; }
 
 db_status db_execute_device(const db_batch* batch, const db_schedule* schedule, uint64_t module_seed,

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "dynbatch/dbk.h"
+#include "iep_head.hpp"
 #include "iep_rb.hpp"
 
 namespace dynbatch::dev {

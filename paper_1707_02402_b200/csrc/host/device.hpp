@@ -212,6 +212,8 @@ class DeviceProgramBatch {
 
 enum class ModuleKind { dense = 0, resblock = 1 };
 
+class IepHead;
+
 class IepSession {
  public:
   // cap_* (0: the initial batch's size) bound the batches set_programs accepts.
@@ -251,6 +253,14 @@ class IepSession {
   std::int64_t h2d_bytes() const;
   std::int64_t d2h_bytes() const;
   double time_forwards(int iters, bool profile, KernelTimes* kt);
+  // IEP classifier head on the root maps (iep_head.hpp; resblock sessions).
+  void set_head(int answers, std::uint64_t seed);
+  void head_forward();                                   // logits of the current roots
+  void download_logits(float* out, std::int64_t n);      // n = b · answers
+  void forward_logits_host(const float* inputs, float* logits);  // H2D rows → forward → head → D2H logits
+  double time_head(int iters);                           // ms per head forward (events, session stream)
+  double head_flops() const;                             // per head forward of the current batch
+  int head_answers() const;
 
  private:
   FunctionVocab vocab_;
@@ -302,6 +312,8 @@ class IepSession {
   // resblock
   struct RB;
   std::unique_ptr<RB> rb_;
+  std::unique_ptr<IepHead> head_;
+  void require_head() const;
   Profiler prof_;
   void add_forward_work();
 };

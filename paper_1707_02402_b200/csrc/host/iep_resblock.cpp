@@ -8,6 +8,7 @@
 
 #include "device.hpp"
 #include "dynbatch/dbk.h"
+#include "iep_head.hpp"
 #include "iep_rb.hpp"
 
 namespace dynbatch::dev {
@@ -333,6 +334,64 @@ void IepSession::forward_host(const float* inputs, float* outputs) {
   forward();
   download_resblock_outputs(outputs);
   check_errors();
+}
+
+// ------------------------------------------------------------ classifier head
+void IepSession::set_head(int answers, std::uint64_t seed) {
+  if (kind_ != ModuleKind::resblock) throw_error(Errc::invalid_argument, "the classifier head needs a resblock session");
+  head_ = std::make_unique<IepHead>(answers, seed, stream_);
+}
+
+void IepSession::require_head() const {
+  if (!head_) throw_error(Errc::invalid_argument, "no classifier head: call set_head first");
+}
+
+int IepSession::head_answers() const { return head_ ? head_->answers() : 0; }
+
+double IepSession::head_flops() const {
+  return head_ ? head_->flops_per_program() * static_cast<double>(batch_->csr().b) : 0.0;
+}
+
+void IepSession::head_forward() {
+  require_head();
+  flush_programs();
+  DeviceProgramBatch& B = *batch_;
+  RB& R = *rb_;
+  launches_ += head_->forward(B.csr().b, B.root_g.get(), B.fid.get(), B.arity_of.get(), B.example.get(),
+                              R.inputs.get(), R.values.get(), stream_);
+}
+
+void IepSession::download_logits(float* out, std::int64_t n) {
+  require_head();
+  const std::int64_t b = batch_->csr().b;
+  if (n != b * head_->answers()) throw_error(Errc::row_count_mismatch, "logit buffer size");
+  head_->download(b, out, stream_);
+}
+
+void IepSession::forward_logits_host(const float* inputs, float* logits) {
+  require_head();
+  upload_resblock_inputs(inputs);
+  forward();
+  head_forward();
+  head_->download(batch_->csr().b, logits, stream_);
+  check_errors();
+}
+
+double IepSession::time_head(int iters) {
+  require_head();
+  cudaEvent_t e0, e1;
+  check(cudaEventCreate(&e0), "event");
+  check(cudaEventCreate(&e1), "event");
+  head_forward();  // warm (sizes the buffers)
+  check(cudaEventRecord(e0, stream_), "event");
+  for (int i = 0; i < iters; ++i) head_forward();
+  check(cudaEventRecord(e1, stream_), "event");
+  check(cudaEventSynchronize(e1), "sync");
+  float ms = 0.f;
+  check(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms / std::max(iters, 1);
 }
 
 void IepSession::set_programs(const std::int32_t* tokens, const std::int32_t* seq_off, std::int64_t b) {

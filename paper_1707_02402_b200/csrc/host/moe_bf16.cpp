@@ -39,6 +39,8 @@ std::uint16_t f16(double v) {
   return u;
 }
 
+}  // namespace
+
 // Element (n, kk) of the N × K operand, stored input-major in `w` as
 // w[kk * N + n], into [N/256][K/64] blocks of 32 KB, each two 16 KB halves
 // (columns 0-127 and 128-255 of the N tile: one per CTA of a pair) of
@@ -55,8 +57,6 @@ void tile_weights(const std::vector<double>& w, int K, int N, int fmt, std::uint
     }
   }
 }
-
-}  // namespace
 
 void upload_expert_weights(const MoeConfig& cfg, std::uint64_t expert_seed, int e_first, int n_local, int fmt,
                            Buf<std::uint16_t>& w1, Buf<std::uint16_t>& w2, Buf<const void*>& w1tab,

@@ -6,10 +6,15 @@
 
 #include <cstdint>
 #include <memory>
+#include <vector>
 
 #include "device.hpp"
 
 namespace dynbatch::dev {
+
+// An N × K GEMM operand stored input-major (w[kk·N + n]) → 16-bit (fmt)
+// [N/256][K/64] tiles of 32 KB for the grouped tcgen05 GEMM (moe_gemm.cu).
+void tile_weights(const std::vector<double>& w, int K, int N, int fmt, std::uint16_t* out);
 
 // ExpertSet experts [e_first, e_first + n_local) (src/moe.cpp:71-88) as
 // 16-bit (fmt) pre-tiled GEMM operands, with device tables of per-expert

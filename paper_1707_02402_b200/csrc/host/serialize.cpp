@@ -61,7 +61,7 @@ std::string number(double v) {
     s += digits.substr(0, 1);
     if (k > 1) s += "." + digits.substr(1);
     const int e = n - 1;
-    char eb[8];
+    char eb[16];
     std::snprintf(eb, sizeof eb, "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
     s += eb;
   }

@@ -184,7 +184,9 @@ struct GemmParams {
   uint8_t* H;                   // EPI 0: tiled 16-bit output [rb][N/64][16 KB]
   uint16_t* Y;                  // EPI 1: 16-bit row-major [row][N]
   int32_t tile_begin, tile_end;  // row-tile range (tile_end < 0: up to *n_tiles)
-  const int32_t* out_row;        // EPI 1: Y row of padded row r = out_row[r] (< 0: skip); null = r
+  const int32_t* out_row;        // EPI 1 / 2: Y row of padded row r = out_row[r] (< 0: skip); null = r
+  const float* const* bias;      // per expert fp32 [N] added before the epilogue's activation; null = none
+  float* Yf;                     // EPI 2: fp32 row-major [row][N]
 };
 
 // Grouped GEMM over (row-tile pair, N tile) units on CTA pairs
@@ -194,8 +196,9 @@ struct GemmParams {
 // reads from L2 halve. The even CTA issues the MMAs. The odd CTA relays its
 // "stage landed" events to the even CTA's barriers, and the commits arrive in
 // both CTAs. Each CTA's epilogue drains its own 128 accumulator lanes.
-// EPI 0 = ReLU → tiled H (GEMM2's A); EPI 1 = rows. F16: fp16 operands
-// and outputs, else bf16.
+// EPI 0 = ReLU → tiled H (GEMM2's A); EPI 1 = 16-bit rows; EPI 2 = fp32
+// rows (the IEP classifier's logits). An optional per-expert bias is added
+// first. F16: fp16 operands and outputs, else bf16.
 template <int EPI, bool F16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_moe_gemm(const __grid_constant__ GemmParams P) {
@@ -292,6 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int abuf = it & 1;
       const int32_t rt = 2 * (u / n_nt) + static_cast<int32_t>(rank), nt = u % n_nt;
       const int32_t rb = P.tile_rb[rt];
+      const float* bias = P.bias ? P.bias[P.tile_expert[rt]] : nullptr;
       mbar_wait(acc_full + abuf, (it >> 1) & 1);
       tc_fence_after();
       const int32_t rr = quarter * 32 + lane;
@@ -301,6 +305,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + abuf * kBN + col0 + c, v);
         const int32_t n0 = nt * kBN + col0 + c;  // global output column of v[0]
+        if (bias) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + n0) + q);
+            v[4 * q] += b4.x;
+            v[4 * q + 1] += b4.y;
+            v[4 * q + 2] += b4.z;
+            v[4 * q + 3] += b4.w;
+          }
+        }
         if (EPI == 0) {
           const int32_t n_kc_out = P.N / kBK;
 #pragma unroll
@@ -314,6 +328,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint8_t* blk = P.H + (static_cast<int64_t>(rb) * n_kc_out + col / kBK) * kABytes;
             *reinterpret_cast<uint4*>(blk + (((col % kBK) / 8) * kBM + rr) * 16) = pk;
           }
+        } else if (EPI == 2) {
+          const int64_t orow = P.out_row ? P.out_row[row] : row;
+          if (orow < 0) continue;
+          float4* dst = reinterpret_cast<float4*>(P.Yf + orow * P.N + n0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else {
           const int64_t orow = P.out_row ? P.out_row[row] : row;
           if (orow < 0) continue;  // padding row (EP: no receive row)
@@ -405,13 +425,26 @@ extern "C" int dbk_moe_tc_gemm(int32_t fmt, int32_t epi, int32_t n, int32_t K, i
                                  const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
                                  const void* const* W, void* H, void* Y, int32_t tile_begin, int32_t tile_end,
                                  const int32_t* out_row, int32_t sms, void* stream) {
-  if (K % kBK != 0 || N % kBN != 0) return static_cast<int>(cudaErrorInvalidValue);
+  return dbk_tc_gemm_bias(fmt, epi, n, K, N, n_tiles, tile_expert, tile_rb, A, W, nullptr, H, Y, tile_begin,
+                          tile_end, out_row, sms, stream);
+}
+
+extern "C" int dbk_tc_gemm_bias(int32_t fmt, int32_t epi, int32_t n, int32_t K, int32_t N, const int32_t* n_tiles,
+                                const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
+                                const void* const* W, const float* const* bias, void* H, void* Y,
+                                int32_t tile_begin, int32_t tile_end, const int32_t* out_row, int32_t sms,
+                                void* stream) {
+  if (K % kBK != 0 || N % kBN != 0 || epi < 0 || epi > 2) return static_cast<int>(cudaErrorInvalidValue);
   GemmParams p{n, K, N, n_tiles, tile_expert, tile_rb, static_cast<const uint8_t*>(A),
                reinterpret_cast<const uint8_t* const*>(W), static_cast<uint8_t*>(H),
-               static_cast<uint16_t*>(Y), tile_begin, tile_end, out_row};
+               static_cast<uint16_t*>(Y), tile_begin, tile_end, out_row, bias, static_cast<float*>(Y)};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (fmt == DBK_FMT_F16) return epi == 0 ? launch_gemm<0, true>(p, sms, s) : launch_gemm<1, true>(p, sms, s);
-  return epi == 0 ? launch_gemm<0, false>(p, sms, s) : launch_gemm<1, false>(p, sms, s);
+  if (fmt == DBK_FMT_F16) {
+    if (epi == 0) return launch_gemm<0, true>(p, sms, s);
+    return epi == 1 ? launch_gemm<1, true>(p, sms, s) : launch_gemm<2, true>(p, sms, s);
+  }
+  if (epi == 0) return launch_gemm<0, false>(p, sms, s);
+  return epi == 1 ? launch_gemm<1, false>(p, sms, s) : launch_gemm<2, false>(p, sms, s);
 }
 
 extern "C" int dbk_moe_tc_combine(int32_t fmt, int64_t T, int32_t k, int32_t d, const double* weights,

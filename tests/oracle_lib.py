@@ -63,6 +63,9 @@ def oracle():
         lib.orc_expert_weights.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_int64, P_F64, P_F64]
         lib.orc_moe_forward.argtypes = [P_F64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                         P_I32, P_F64, C.c_uint64, P_I32, C.c_int64, P_F64, P_I64, P_F64]
+        lib.orc_head_weights.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64] + [P_F64] * 6
+        lib.orc_head_forward.argtypes = [C.c_int64, P_F64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                                         P_F64]
         _oracle = lib
     return _oracle
 
@@ -436,3 +439,27 @@ def schedule_naive(bt: Batch) -> FlatSchedule:
             sgo.append(len(gf))
     a = lambda v: np.asarray(v, np.int32)  # noqa: E731
     return FlatSchedule(a(sgo), a(gf), a(gmo), a(me), a(mn), "naive")
+
+
+# ------------------------------------------------------------- IEP head --
+
+HEAD = {"C": 128, "P": 512, "F": 1024}
+
+
+def head_weights(A, seed, C=128, P=512, F=1024):
+    """orc_head_weights: (wp [C][P], bp, w1 [49P][F], b1, w2 [F][A], b2)."""
+    wp, bp = np.zeros(C * P), np.zeros(P)
+    w1, b1 = np.zeros(49 * P * F), np.zeros(F)
+    w2, b2 = np.zeros(F * A), np.zeros(A)
+    oracle().orc_head_weights(C, P, F, A, seed, *(_ptr(a, P_F64) for a in (wp, bp, w1, b1, w2, b2)))
+    return wp.reshape(C, P), bp, w1.reshape(49 * P, F), b1, w2.reshape(F, A), b2
+
+
+def head_forward(roots: np.ndarray, A, seed, C=128, P=512, F=1024) -> np.ndarray:
+    """orc_head_forward: logits [b][A] of CHW root rows (fp64)."""
+    roots = np.ascontiguousarray(roots, np.float64)
+    b = roots.shape[0]
+    out = np.zeros((b, A), np.float64)
+    rc = oracle().orc_head_forward(b, _ptr(roots, P_F64), C, P, F, A, seed, _ptr(out, P_F64))
+    assert rc == 0, rc
+    return out
