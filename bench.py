@@ -661,7 +661,29 @@ def run_moe_ep(args, dist, name):
                          "peak_source": src + " bf16 sustained"},
             "max_rows_received": int(rows), "clocks": clk.summary(),
             "gpu_launches_per_step": 14,
-            "e2e": None, "e2e_note": "inputs are generated per rank on the device side; no host I/O path"}
+            "e2e": None, "e2e_note": "inputs are generated per rank on the device side; no host I/O path",
+            "cpu_baseline": (moe_sampled_cpu_baseline(c) if dist.rank == 0 and N == 1 and not args.no_cpu_baseline
+                             else None)}
+
+
+def moe_sampled_cpu_baseline(c, tokens=32):
+    """cfg5 on the CPU is infeasible as shipped (ExpertSet alone is 68.7 GB of
+    fp64): the fp64 oracle port of moe_forward_batched
+    (src/moe.cpp:162-270; scalar fma loops, one thread) on the first `tokens`
+    tokens' items, timed by its own module + combine clock (expert weight
+    generation outside it), extrapolated FLOP-proportionally per token."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    import oracle_lib as O
+    n, k, d, h = c["experts"], c["k"], c["d"], c["h"]
+    rows = np.arange(tokens, dtype=np.int64)
+    x = O.random_rows(rows, d, O.mix_seed(0, 0x10))
+    sc = O.random_rows(rows, n, O.mix_seed(0, 0x11))
+    ids, w = O.topk(sc, k)
+    _, _, secs = O.moe_forward(x, ids, w, n, h, O.mix_seed(0, 0xe4be27))
+    return {"value": tokens / secs[2], "unit": "tokens/s", "cores": 1, "kind": "port",
+            "sample": f"first {tokens} tokens ({tokens * k} expert items), oracle fp64 port, {secs[2]:.2f} s; "
+                      f"extrapolated per token (the full layer needs 68.7 GB of fp64 experts)"}
 
 
 def _mix_seed(seed, stream):
