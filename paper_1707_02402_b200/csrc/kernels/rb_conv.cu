@@ -95,14 +95,19 @@ constexpr int kASlot = kWin * 128;         // 36 KB activation window slot (rows
 constexpr int kASlots = DYNBATCH_ASLOTS;   // window slots (short hi/lo and 1×1 chunks need depth)
 constexpr int kBStage = 128 * 64 * 2;      // 16 KB: 128 out channels × K=64 fp16 weight block
 constexpr int kBStages = DYNBATCH_BSTAGES;
-constexpr int kEpiWarps = 8;               // two warps per TMEM lane quarter, 128 positions each
+#ifndef DYNBATCH_EPI_WARPS
+#define DYNBATCH_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = DYNBATCH_EPI_WARPS;  // 8: two warps per TMEM lane quarter (128 positions each); 16: four
+constexpr int kEpiParts = kEpiWarps / 4;       // column parts per lane quarter
+static_assert(kEpiWarps == 8 || kEpiWarps == 16, "8 or 16 epilogue warps");
 constexpr int kTableWarp = 2 + kEpiWarps;  // fills the per-tile position tables ahead of the epilogue
 constexpr int kWeightWarp = kTableWarp + 1;  // streams the weight stages
 constexpr int kThreads = (kWeightWarp + 1) * 32;
 constexpr int kItemSlots = 4;              // work items in flight between the roles
 constexpr int kChunk = 16;                 // positions per epilogue chunk
 template <int TM>
-constexpr int kChunksT = TM / 2 / kChunk;  // 16-position chunks per epilogue warp and tile
+constexpr int kChunksT = TM / kEpiParts / kChunk;  // 16-position chunks per epilogue warp and tile
 
 // Per-member epilogue metadata (schedule order), built once per forward by
 // k_rb_memtab from the forwarding tables.
@@ -523,7 +528,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
   // kGuard + q0 + 128·half + 16·cb + 8m + e, so (row & 7) == e
   constexpr int kChunks = kChunksT<TM>;
   const int64_t own_off =
-      L.chunk_off + (static_cast<int64_t>(kGuard + it.q0 + L.half * (TM / 2) + L.e) << 7) + (L.sub << 4);
+      L.chunk_off + (static_cast<int64_t>(kGuard + it.q0 + L.half * (TM / kEpiParts) + L.e) << 7) + (L.sub << 4);
   uint8_t* own = (KIND == 0 ? P.stage_x : P.stage_mid) + own_off;
   uint8_t* own_lo = P.stage_lo + own_off;
   // diag bit 4: every store lands in one L2-resident 16-byte slot per thread
@@ -536,7 +541,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
     for (int cb = 0; cb < kChunks; ++cb) {
       float v[kChunk];
       tmem_ld16(taddr + cb * kChunk, v);
-      const PosEntry* my = tab + L.half * (TM / 2) + cb * kChunk + L.e;
+      const PosEntry* my = tab + L.half * (TM / kEpiParts) + cb * kChunk + L.e;
 #pragma unroll
       for (int m = 0; m < kChunk / 8; ++m) {
         float* x = v + 8 * m;
@@ -558,7 +563,7 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
   for (int cb = 0; cb < kChunks; ++cb) {
     float v[kChunk];
     tmem_ld16(taddr + cb * kChunk, v);
-    const PosEntry* my = tab + L.half * (TM / 2) + cb * kChunk + L.e;
+    const PosEntry* my = tab + L.half * (TM / kEpiParts) + cb * kChunk + L.e;
 #pragma unroll
     for (int m = 0; m < kChunk / 8; ++m) {
       float* x = v + 8 * m;
@@ -926,7 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rb_step(const __grid_constant__
     L.chunk_off = static_cast<int64_t>(L.plane >> 3) * P.ps * 128;
     L.sub = (L.plane & 7) ^ L.e;
     L.plane_off32 = L.plane * kPx * 8;
-    const uint32_t lane_addr = (static_cast<uint32_t>(L.quarter * 32) << 16) + L.half * (TM / 2);
+    const uint32_t lane_addr = (static_cast<uint32_t>(L.quarter * 32) << 16) + L.half * (TM / kEpiParts);
     for (int n = 0;; ++n) {
       const int slot = n % kItemSlots;
       mbar_wait(item_full + slot, (n / kItemSlots) & 1);
