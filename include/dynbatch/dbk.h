@@ -203,6 +203,29 @@ int dbk_moe_tc_gemm(int32_t fmt, int32_t epi, int32_t n, int32_t K, int32_t N, c
                     const int32_t* tile_expert, const int32_t* tile_rb, const void* A,
                     const void* const* W, void* H, void* Y, int32_t tile_begin, int32_t tile_end,
                     const int32_t* out_row, int32_t sms, void* stream);
+/* Training (train.cu). PI = per-member padded image:
+ * 257 rows (16 zero guard rows, the 225 packed positions, 16 guard rows) ×
+ * channels, fp32. */
+int dbk_rb_set_training(int32_t on); /* forwards keep every node's fp32 value and the mid images */
+int dbk_tr_stage_to_pi(int32_t n, int64_t row0, const void* hi, const void* lo, int64_t ps, int32_t plane0,
+                       int32_t planes, float* out, void* stream);
+int dbk_tr_da_out(int32_t n, const int32_t* nodes, const float* dy_nodes, const float* values, float* out,
+                  void* stream);
+int dbk_tr_im2col(int64_t rows, int32_t ch, const float* x, float* cols, void* stream);
+int dbk_tr_col2im(int32_t n, int32_t ch, const float* g, const float* res, const float* mask, float* out,
+                  void* stream);
+int dbk_tr_mask(int64_t count, const float* g, const float* act, float* out, void* stream);
+int dbk_tr_colsum(int64_t rows, int32_t cols, const float* a, float* db, void* stream);
+int dbk_tr_route(int32_t n, const int32_t* nodes, const int32_t* child, const int32_t* fid, const int32_t* arity_of,
+                 const int32_t* example, const float* src, int32_t ch, int32_t c0, float* dy_nodes, float* d_inputs,
+                 void* stream);
+int dbk_tr_softmax_ce(int64_t b, int32_t A, int32_t ld, const float* logits, const int32_t* labels, float* dlogits,
+                      float* loss, void* stream);
+int dbk_tr_unpack_h(int64_t rows, int32_t K, const void* h, float* out, void* stream);
+int dbk_tr_unpack_sw128(int64_t rows, int32_t K, const void* a, float* out, void* stream);
+int dbk_tr_pool_bwd(int64_t b, int32_t P, const float* proj, const float* dpooled, float* dproj, void* stream);
+int dbk_tr_droots(int64_t b, const int32_t* root_g, const int32_t* fid, const int32_t* arity_of,
+                  const int32_t* example, const float* droots, float* dy_nodes, float* d_inputs, void* stream);
 /* IEP classifier head operand moves (head.cu): roots → fp16 SW128 tiled
  * rows (program·196 + px) × 128; projection output (tiled H, P columns) →
  * 2×2 max pool → fp16 SW128 tiled rows (program) × 49·P. */

@@ -162,6 +162,21 @@ DYNBATCH_API db_status db_iep_session_forward_logits_host(db_iep_session* s, con
                                                           float* logits);
 DYNBATCH_API db_status db_iep_session_time_head(db_iep_session* s, int32_t iters, double* ms,
                                                 double* flops);
+/* Training (RESBLOCK sessions with a head, beyond the
+ * reference's forward-only path): set_training(1) keeps every node's fp32
+ * value during training forwards. train_step runs forward → head → mean
+ * softmax cross-entropy over labels[b] (in [0, answers)) → backward through
+ * the head and the module groups in reverse step order, and returns the
+ * loss. grad downloads one fp32 gradient of that step: which 0-5 = module
+ * w0, b0, w1, b1, w2, b2 of function fid (input-major like the weights),
+ * 6-11 = head wp, bp, w1, b1, w2, b2, 12 = the input maps (CHW rows);
+ * grad_size gives its element count. time_train = device ms per step. */
+DYNBATCH_API db_status db_iep_session_set_training(db_iep_session* s, int32_t on);
+DYNBATCH_API db_status db_iep_session_train_step(db_iep_session* s, const int32_t* labels, float* loss);
+DYNBATCH_API db_status db_iep_session_grad_size(db_iep_session* s, int32_t which, int32_t fid, int64_t* n);
+DYNBATCH_API db_status db_iep_session_grad(db_iep_session* s, int32_t which, int32_t fid, float* out, int64_t n);
+DYNBATCH_API db_status db_iep_session_time_train(db_iep_session* s, int32_t iters, const int32_t* labels,
+                                                 double* ms);
 DYNBATCH_API void db_iep_session_free(db_iep_session* s);
 
 /* db_schedule_build on the device scheduler: IMPROVED, STANDARD or ONLINE

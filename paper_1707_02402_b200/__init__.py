@@ -158,6 +158,11 @@ SIGNATURES = {
     "db_iep_session_logits": (C.c_int32, [VP, VP, C.c_int64]),
     "db_iep_session_forward_logits_host": (C.c_int32, [VP, VP, VP]),
     "db_iep_session_time_head": (C.c_int32, [VP, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "db_iep_session_set_training": (C.c_int32, [VP, C.c_int32]),
+    "db_iep_session_train_step": (C.c_int32, [VP, VP, C.POINTER(C.c_float)]),
+    "db_iep_session_grad_size": (C.c_int32, [VP, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
+    "db_iep_session_grad": (C.c_int32, [VP, C.c_int32, C.c_int32, VP, C.c_int64]),
+    "db_iep_session_time_train": (C.c_int32, [VP, C.c_int32, VP, C.POINTER(C.c_double)]),
     "db_iep_session_free": (None, [VP]),
     "db_execute_device": (C.c_int32, [VP, VP, C.c_uint64, C.POINTER(ModuleOpts), PVP]),
     "db_moe_session_create": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, C.c_int64, C.c_int64,
@@ -508,6 +513,33 @@ class IepSession(_Handle):
 
     def forward_logits_host(self, inputs: np.ndarray, logits: np.ndarray):
         check(lib().db_iep_session_forward_logits_host(self.h, _ptr(inputs), _ptr(logits)))
+
+    # training (db_iep_session_set_training …)
+    GRADS = ("w0", "b0", "w1", "b1", "w2", "b2", "head_wp", "head_bp", "head_w1", "head_b1", "head_w2",
+             "head_b2", "inputs")
+
+    def set_training(self, on: bool = True):
+        check(lib().db_iep_session_set_training(self.h, 1 if on else 0))
+
+    def train_step(self, labels) -> float:
+        lab = np.ascontiguousarray(labels, np.int32)
+        loss = C.c_float()
+        check(lib().db_iep_session_train_step(self.h, _ptr(lab), C.byref(loss)))
+        return loss.value
+
+    def grad(self, name: str, fid: int = -1) -> np.ndarray:
+        which = self.GRADS.index(name)
+        n = C.c_int64()
+        check(lib().db_iep_session_grad_size(self.h, which, fid, C.byref(n)))
+        out = np.zeros(n.value, np.float32)
+        check(lib().db_iep_session_grad(self.h, which, fid, _ptr(out), n.value))
+        return out
+
+    def time_train(self, iters: int, labels) -> float:
+        lab = np.ascontiguousarray(labels, np.int32)
+        ms = C.c_double()
+        check(lib().db_iep_session_time_train(self.h, iters, _ptr(lab), C.byref(ms)))
+        return ms.value
 
     def time_head(self, iters: int):
         """(device ms per head forward, algorithmic FLOPs per head forward)."""

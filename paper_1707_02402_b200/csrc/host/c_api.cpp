@@ -570,6 +570,34 @@ db_status db_iep_session_time_head(db_iep_session* s, int32_t iters, double* ms,
   });
 }
 
+db_status db_iep_session_set_training(db_iep_session* s, int32_t on) {
+  if (!s) return null_arg();
+  return guarded([&] { s->s->set_training(on != 0); });
+}
+
+db_status db_iep_session_train_step(db_iep_session* s, const int32_t* labels, float* loss) {
+  if (!s || !labels) return null_arg();
+  return guarded([&] {
+    const float l = s->s->train_step(labels);
+    if (loss) *loss = l;
+  });
+}
+
+db_status db_iep_session_grad_size(db_iep_session* s, int32_t which, int32_t fid, int64_t* n) {
+  if (!s || !n) return null_arg();
+  return guarded([&] { *n = s->s->grad_size(which, fid); });
+}
+
+db_status db_iep_session_grad(db_iep_session* s, int32_t which, int32_t fid, float* out, int64_t n) {
+  if (!s || (!out && n)) return null_arg();
+  return guarded([&] { s->s->download_grad(which, fid, out, n); });
+}
+
+db_status db_iep_session_time_train(db_iep_session* s, int32_t iters, const int32_t* labels, double* ms) {
+  if (!s || !labels || !ms) return null_arg();
+  return guarded([&] { *ms = s->s->time_train(iters, labels); });
+}
+
 void db_iep_session_free(db_iep_session* s) { delete s; }
 
 db_status db_execute_device(const db_batch* batch, const db_schedule* schedule, uint64_t module_seed,

@@ -10,6 +10,7 @@
 
 #include "dynbatch/dbk.h"
 #include "iep_head.hpp"
+#include "iep_train.hpp"
 #include "iep_rb.hpp"
 
 namespace dynbatch::dev {
@@ -568,7 +569,7 @@ bool IepSession::graphs_enabled() const {
   }();
   // resblock forwards need no host sync (upper-bound step count), so they
   // capture; profiled forwards record per-class events and run directly
-  return env_on && kind_ == ModuleKind::resblock && !prof_.on;
+  return env_on && kind_ == ModuleKind::resblock && !prof_.on && !train_;
 }
 
 void IepSession::forward_graph() {

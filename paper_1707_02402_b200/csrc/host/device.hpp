@@ -261,6 +261,18 @@ class IepSession {
   double time_head(int iters);                           // ms per head forward (events, session stream)
   double head_flops() const;                             // per head forward of the current batch
   int head_answers() const;
+  // Training (iep_train.cpp; resblock sessions with a head): one step =
+  // training forward (every node value kept) → head → mean softmax
+  // cross-entropy over labels[b] → backward through the head and the module
+  // groups in reverse step order. Gradients are fp32, input-major like the
+  // weights; they are overwritten by every step.
+  void set_training(bool on);
+  float train_step(const std::int32_t* labels);
+  // which: 0-5 = module w0, b0, w1, b1, w2, b2 of function fid; 6-11 = head
+  // wp, bp, w1, b1, w2, b2; 12 = input maps (CHW rows [b][C·196]).
+  void download_grad(int which, int fid, float* out, std::int64_t n);
+  std::int64_t grad_size(int which, int fid) const;
+  double time_train(int iters, const std::int32_t* labels);
 
  private:
   FunctionVocab vocab_;
@@ -313,6 +325,10 @@ class IepSession {
   struct RB;
   std::unique_ptr<RB> rb_;
   std::unique_ptr<IepHead> head_;
+  struct Train;
+  std::unique_ptr<Train> train_;
+  std::uint64_t module_seed_ = 0;
+  void backward(float* loss_dev);
   void require_head() const;
   Profiler prof_;
   void add_forward_work();

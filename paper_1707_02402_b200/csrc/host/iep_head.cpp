@@ -65,6 +65,9 @@ IepHead::IepHead(int answers, std::uint64_t seed, cudaStream_t s) : answers_(ans
     dst.upload(f, s);
     check(cudaStreamSynchronize(s), "bias upload");
   };
+  upf(wp32_, h.wp);
+  upf(w132_, h.w1);
+  upf(w232_, h.w2);
   upf(bp_, h.bp);
   upf(b1_, h.b1);
   upf(b2_, b2p);

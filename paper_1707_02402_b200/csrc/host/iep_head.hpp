@@ -36,6 +36,15 @@ class IepHead {
   // 2·(196·128·P + 49·P·F + F·A) per program
   double flops_per_program() const;
   void download(std::int64_t b, float* out, cudaStream_t s) const;  // [b][answers]
+  // The backward's operands: the last forward's 16-bit activations (tiled as
+  // the GEMMs read / wrote them) and fp32 input-major weights.
+  const void* roots_tiled() const { return a0_.get(); }   // SW128 rows e·196 + px, K = 128
+  const void* proj_tiled() const { return h1_.get(); }    // H layout rows e·196 + px, K = P
+  const void* pooled_tiled() const { return a1_.get(); }  // SW128 rows e, K = 49·P
+  const void* hidden_tiled() const { return h2_.get(); }  // H layout rows e, K = F
+  const float* wp32() const { return wp32_.get(); }       // [C][P]
+  const float* w1_32() const { return w132_.get(); }      // [49P][F]
+  const float* w2_32() const { return w232_.get(); }      // [F][answers]
 
  private:
   void size_for(std::int64_t b, cudaStream_t s);
@@ -44,6 +53,7 @@ class IepHead {
   std::int64_t cap_b_ = 0;
   Buf<std::uint16_t> wp_, w1_, w2_;
   Buf<float> bp_, b1_, b2_;
+  Buf<float> wp32_, w132_, w232_;
   Buf<const void*> wtab_;        // [wp, w1, w2]
   Buf<const float*> btab_;       // [bp, b1, b2]
   Buf<std::uint16_t> a0_, h1_, a1_, h2_;

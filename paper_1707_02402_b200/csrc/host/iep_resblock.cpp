@@ -9,6 +9,7 @@
 #include "device.hpp"
 #include "dynbatch/dbk.h"
 #include "iep_head.hpp"
+#include "iep_train.hpp"
 #include "iep_rb.hpp"
 
 namespace dynbatch::dev {
@@ -76,6 +77,7 @@ std::vector<std::uint16_t> pack_blocks(const std::vector<double>& w, int C, int 
 }  // namespace
 
 void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_seed) {
+  module_seed_ = module_seed;
   constexpr int C = 128;
   if (width_ != RB::kFmap) throw_error(Errc::width_mismatch, "resblock modules need width 25088 (128x14x14)");
   const HostCSR& c = batch_->csr();

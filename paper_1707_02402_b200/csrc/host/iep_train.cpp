@@ -1,0 +1,348 @@
+// iep_train.cpp — one IEP training step on the device (
+// PAPER.md:75 reports the paper's batched backward; the reference executor
+// stops at the forward).
+//
+// Forward: the fused step kernel in training mode (every expensive node's
+// fp32 value kept, mid images left in place), then the classifier head, then
+// mean softmax cross-entropy. Backward: the head's GEMMs, then the module
+// groups of the schedule in reverse step order — each group is one batched
+// call per weight, exactly as the forward batches them:
+//   da2 = dy ⊙ (y > 0);               dW2 += im2col(mid)ᵀ·da2,   db2 += Σ da2
+//   da1 = col2im(da2·W2ᵀ) ⊙ (mid > 0); dW1 += im2col(x)ᵀ·da1,     db1 += Σ da1
+//   dx  = col2im(da1·W1ᵀ) + da2        (the residual)
+//   binary: da0 = dx ⊙ (z > 0); dW0 += [x; y]ᵀ·da0, d[x; y] = da0·W0ᵀ
+// and the operand gradients are routed to the children (atomic adds, so
+// children shared by several parents accumulate) or to the input maps.
+// Activations come from the forward's own staging (fp16 hi + lo), so the
+// backward differentiates the arithmetic the forward performed. The GEMMs
+// are library GEMMs (cuBLAS, TF32 tensor cores, fp32 accumulation); the
+// operand moves are train.cu.
+#include "iep_train.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "dynbatch.hpp"
+#include "iep_head.hpp"
+#include "iep_rb.hpp"
+
+#include "dynbatch/dbk.h"
+
+namespace dynbatch::dev {
+
+namespace {
+
+constexpr int kC = 128, kPI = 257, kG = 16, kPx = 196, kK3 = 9 * kC;
+
+void cublas_check(cublasStatus_t st, const char* what) {
+  if (st != CUBLAS_STATUS_SUCCESS)
+    throw std::runtime_error(std::string("cuBLAS error ") + std::to_string(static_cast<int>(st)) + " in " + what);
+}
+
+// TF32 tensor cores (default) or full fp32 (DYNBATCH_TRAIN_FP32=1, A/B of the
+// backward's rounding).
+cublasComputeType_t compute_type() {
+  static const cublasComputeType_t t = [] {
+    const char* e = std::getenv("DYNBATCH_TRAIN_FP32");
+    return e && std::atoi(e) ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_FAST_TF32;
+  }();
+  return t;
+}
+
+// Row-major C[M×N] = op(A)·op(B) (+ beta·C); A is M×K (K×M stored when ta),
+// B is K×N (N×K stored when tb); leading dimensions of the stored matrices.
+void rm_gemm(cublasHandle_t h, bool ta, bool tb, std::int64_t M, std::int64_t N, std::int64_t K, const float* A,
+             std::int64_t lda, const float* B, std::int64_t ldb, float beta, float* C, std::int64_t ldc) {
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  const float alpha = 1.f;
+  cublas_check(cublasGemmEx(h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, static_cast<int>(N),
+                            static_cast<int>(M), static_cast<int>(K), &alpha, B, CUDA_R_32F, static_cast<int>(ldb), A,
+                            CUDA_R_32F, static_cast<int>(lda), &beta, C, CUDA_R_32F, static_cast<int>(ldc),
+                            compute_type(), CUBLAS_GEMM_DEFAULT),
+               "gemm");
+}
+
+std::vector<float> to_f32(const std::vector<double>& v) { return std::vector<float>(v.begin(), v.end()); }
+
+}  // namespace
+
+void IepSession::set_training(bool on) {
+  if (!on) {
+    train_.reset();
+    return;
+  }
+  if (kind_ != ModuleKind::resblock) throw_error(Errc::invalid_argument, "training needs a resblock session");
+  if (train_) return;
+  auto t = std::make_unique<Train>();
+  cublas_check(cublasCreate(&t->blas), "create");
+  cublas_check(cublasSetStream(t->blas, stream_), "stream");
+  const HostCSR& c = batch_->csr();
+  t->arity = c.arity_of;
+  const size_t p = t->arity.size();
+  for (auto* v : {&t->w0, &t->w1, &t->w2, &t->gw0, &t->gb0, &t->gw1, &t->gb1, &t->gw2, &t->gb2}) v->resize(p);
+  for (size_t f = 0; f < p; ++f) {
+    const int a = t->arity[f];
+    if (a == 0) continue;
+    const ResBlockImpl m = make_resblock_impl(a, kC, module_seed_, static_cast<int>(f));
+    if (a == 2) {
+      t->w0[f].upload(to_f32(m.w0), stream_);
+      t->gw0[f].alloc(m.w0.size());
+      t->gb0[f].alloc(kC);
+    }
+    t->w1[f].upload(to_f32(m.w1), stream_);
+    t->w2[f].upload(to_f32(m.w2), stream_);
+    t->gw1[f].alloc(m.w1.size());
+    t->gw2[f].alloc(m.w2.size());
+    t->gb1[f].alloc(kC);
+    t->gb2[f].alloc(kC);
+    check(cudaStreamSynchronize(stream_), "training weights");  // the host vectors go out of scope
+  }
+  t->loss.alloc(1);
+  train_ = std::move(t);
+}
+
+float IepSession::train_step(const std::int32_t* labels) {
+  if (!train_) throw_error(Errc::invalid_argument, "training is off: call set_training first");
+  require_head();
+  Train& T = *train_;
+  flush_programs();
+  const std::int64_t b = batch_->csr().b;
+  for (std::int64_t e = 0; e < b; ++e)
+    if (labels[e] < 0 || labels[e] >= head_->answers()) throw_error(Errc::invalid_argument, "label out of range");
+  T.labels.upload(labels, static_cast<size_t>(b), stream_);
+  dbk_rb_set_training(1);
+  try {
+    forward_direct();
+  } catch (...) {
+    dbk_rb_set_training(0);
+    throw;
+  }
+  dbk_rb_set_training(0);
+  check_errors();
+  head_forward();
+  backward(T.loss.get());
+  float loss = 0.f;
+  check(cudaMemcpyAsync(&loss, T.loss.get(), sizeof(float), cudaMemcpyDeviceToHost, stream_), "D2H loss");
+  check(cudaStreamSynchronize(stream_), "sync");
+  return loss;
+}
+
+void IepSession::backward(float* loss_dev) {
+  Train& T = *train_;
+  RB& R = *rb_;
+  DeviceProgramBatch& B = *batch_;
+  cudaStream_t s = stream_;
+  const HostCSR& c = B.csr();
+  const std::int64_t b = c.b, N = c.N;
+  const int A = head_->answers(), P = IepHead::kP, F = IepHead::kF, K1 = 49 * P;
+  // ---- sizes, zeroed gradient accumulators
+  if (b > T.cap_b) {
+    T.d_inputs.alloc(static_cast<size_t>(b) * kC * kPx);
+    T.dlogits.alloc(static_cast<size_t>(b) * A > 0 ? static_cast<size_t>(b) * 256 : 1);
+    T.hid.alloc(static_cast<size_t>(b) * F);
+    T.dhid.alloc(static_cast<size_t>(b) * F);
+    T.pooled.alloc(static_cast<size_t>(b) * K1);
+    T.dpooled.alloc(static_cast<size_t>(b) * K1);
+    T.proj.alloc(static_cast<size_t>(b) * kPx * P);
+    T.dproj.alloc(static_cast<size_t>(b) * kPx * P);
+    T.roots.alloc(static_cast<size_t>(b) * kPx * kC);
+    T.droots.alloc(static_cast<size_t>(b) * kPx * kC);
+    T.cap_b = b;
+  }
+  if (N > T.cap_n) {
+    T.dy_nodes.alloc(static_cast<size_t>(N) * kPI * kC);
+    T.cap_n = N;
+  }
+  if (T.gwp.size() < static_cast<size_t>(kC) * P) {
+    T.gwp.alloc(static_cast<size_t>(kC) * P);
+    T.gbp.alloc(P);
+    T.ghw1.alloc(static_cast<size_t>(K1) * F);
+    T.ghb1.alloc(F);
+  }
+  T.ghw2.ensure(static_cast<size_t>(F) * A);
+  T.ghb2.ensure(static_cast<size_t>(A));
+  T.d_inputs.zero(s);
+  T.dy_nodes.zero(s);
+  for (Buf<float>* v : {&T.gwp, &T.gbp, &T.ghw1, &T.ghb1, &T.ghw2, &T.ghb2}) v->zero(s);
+  for (size_t f = 0; f < T.arity.size(); ++f)
+    for (Buf<float>* v : {&T.gw0[f], &T.gb0[f], &T.gw1[f], &T.gb1[f], &T.gw2[f], &T.gb2[f]}) v->zero(s);
+  check(cudaMemsetAsync(loss_dev, 0, sizeof(float), s), "loss reset");
+  cublasHandle_t h = T.blas;
+
+  // ---- head: loss, FC2, FC1, pool, projection
+  check(dbk_tr_softmax_ce(b, A, IepHead::kPad, head_->logits(), T.labels.get(), T.dlogits.get(), loss_dev, s), "ce");
+  check(dbk_tr_unpack_h(b, F, head_->hidden_tiled(), T.hid.get(), s), "unpack hidden");
+  check(dbk_tr_unpack_sw128(b, K1, head_->pooled_tiled(), T.pooled.get(), s), "unpack pooled");
+  check(dbk_tr_unpack_h(b * kPx, P, head_->proj_tiled(), T.proj.get(), s), "unpack projection");
+  check(dbk_tr_unpack_sw128(b * kPx, kC, head_->roots_tiled(), T.roots.get(), s), "unpack roots");
+  rm_gemm(h, true, false, F, A, b, T.hid.get(), F, T.dlogits.get(), A, 0.f, T.ghw2.get(), A);
+  check(dbk_tr_colsum(b, A, T.dlogits.get(), T.ghb2.get(), s), "db2");
+  rm_gemm(h, false, true, b, F, A, T.dlogits.get(), A, head_->w2_32(), A, 0.f, T.dhid.get(), F);
+  check(dbk_tr_mask(b * F, T.dhid.get(), T.hid.get(), T.dhid.get(), s), "relu fc1");
+  rm_gemm(h, true, false, K1, F, b, T.pooled.get(), K1, T.dhid.get(), F, 0.f, T.ghw1.get(), F);
+  check(dbk_tr_colsum(b, F, T.dhid.get(), T.ghb1.get(), s), "db1");
+  rm_gemm(h, false, true, b, K1, F, T.dhid.get(), F, head_->w1_32(), F, 0.f, T.dpooled.get(), K1);
+  check(dbk_tr_pool_bwd(b, P, T.proj.get(), T.dpooled.get(), T.dproj.get(), s), "pool backward");
+  rm_gemm(h, true, false, kC, P, b * kPx, T.roots.get(), kC, T.dproj.get(), P, 0.f, T.gwp.get(), P);
+  check(dbk_tr_colsum(b * kPx, P, T.dproj.get(), T.gbp.get(), s), "dbp");
+  rm_gemm(h, false, true, b * kPx, kC, P, T.dproj.get(), P, head_->wp32(), P, 0.f, T.droots.get(), kC);
+  check(dbk_tr_droots(b, B.root_g.get(), B.fid.get(), B.arity_of.get(), B.example.get(), T.droots.get(),
+                      T.dy_nodes.get(), T.d_inputs.get(), s),
+        "route roots");
+
+  // ---- module groups, reverse step order
+  const int S = B.steps;
+  const std::vector<std::int32_t> sgb = B.step_group_begin.download(static_cast<size_t>(S) + 1, s);
+  const std::int64_t G = sgb[static_cast<size_t>(S)];
+  const std::vector<std::int32_t> gfid = B.group_fid.download(static_cast<size_t>(G), s);
+  const std::vector<std::int32_t> gbeg = B.group_begin.download(static_cast<size_t>(G) + 1, s);
+  const std::vector<std::int32_t> seg = R.seg_start.download(static_cast<size_t>(G), s);
+  std::int64_t n_max = 0;
+  for (std::int64_t g = 0; g < G; ++g) n_max = std::max<std::int64_t>(n_max, gbeg[g + 1] - gbeg[g]);
+  const std::int64_t rows_max = n_max * kPI;
+  if (rows_max > T.cap_rows) {
+    const size_t r = static_cast<size_t>(rows_max), rg = r + 2 * kG;
+    T.da2.alloc(r * kC);
+    T.mid.alloc(rg * kC);
+    T.xin.alloc(rg * kC);
+    T.cols.alloc(r * kK3);
+    T.g.alloc(r * kK3);
+    T.da1.alloc(r * kC);
+    T.dx.alloc(r * kC);
+    T.da0.alloc(r * kC);
+    T.cat.alloc(r * 2 * kC);
+    T.dcat.alloc(r * 2 * kC);
+    T.cap_rows = rows_max;
+  }
+  const std::int64_t ps = R.plane_stride;
+  float* mid = T.mid.get() + kG * kC;  // row 0 of the first member (16 guard rows before)
+  float* xin = T.xin.get() + kG * kC;
+  for (int st = S - 1; st >= 0; --st) {
+    for (std::int32_t g = sgb[static_cast<size_t>(st)]; g < sgb[static_cast<size_t>(st) + 1]; ++g) {
+      const int f = gfid[static_cast<size_t>(g)];
+      const int a = T.arity[static_cast<size_t>(f)];
+      const std::int32_t n = gbeg[static_cast<size_t>(g) + 1] - gbeg[static_cast<size_t>(g)];
+      if (a == 0 || n == 0 || seg[static_cast<size_t>(g)] < 0) continue;
+      const std::int64_t rows = static_cast<std::int64_t>(n) * kPI;
+      const std::int32_t* nodes = B.member_g.get() + gbeg[static_cast<size_t>(g)];
+      const std::int64_t row0 = seg[static_cast<size_t>(g)];
+      // zero the PI buffers' guard and pad rows the gathers leave untouched
+      check(cudaMemsetAsync(T.mid.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
+      check(cudaMemsetAsync(T.xin.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
+      check(cudaMemsetAsync(T.da2.get(), 0, sizeof(float) * static_cast<size_t>(rows) * kC, s), "zero");
+      // conv3x3 #2: da2, dW2, db2, da1
+      check(dbk_tr_da_out(n, nodes, T.dy_nodes.get(), R.values.get(), T.da2.get(), s), "da2");
+      check(dbk_tr_colsum(rows, kC, T.da2.get(), T.gb2[static_cast<size_t>(f)].get(), s), "db2");
+      check(dbk_tr_stage_to_pi(n, row0, R.stage_mid.get(), nullptr, ps, 0, 16, mid, s), "mid");
+      check(dbk_tr_im2col(rows, kC, mid, T.cols.get(), s), "im2col mid");
+      rm_gemm(h, true, false, kK3, kC, rows, T.cols.get(), kK3, T.da2.get(), kC, 1.f,
+              T.gw2[static_cast<size_t>(f)].get(), kC);
+      rm_gemm(h, false, true, rows, kK3, kC, T.da2.get(), kC, T.w2[static_cast<size_t>(f)].get(), kC, 0.f,
+              T.g.get(), kK3);
+      check(dbk_tr_col2im(n, kC, T.g.get(), nullptr, mid, T.da1.get(), s), "col2im mid");
+      // conv3x3 #1: dW1, db1, dx (+ the residual)
+      check(dbk_tr_colsum(rows, kC, T.da1.get(), T.gb1[static_cast<size_t>(f)].get(), s), "db1");
+      check(dbk_tr_stage_to_pi(n, row0, R.stage_x.get(), R.stage_lo.get(), ps, 0, 16, xin, s), "x");
+      check(dbk_tr_im2col(rows, kC, xin, T.cols.get(), s), "im2col x");
+      rm_gemm(h, true, false, kK3, kC, rows, T.cols.get(), kK3, T.da1.get(), kC, 1.f,
+              T.gw1[static_cast<size_t>(f)].get(), kC);
+      rm_gemm(h, false, true, rows, kK3, kC, T.da1.get(), kC, T.w1[static_cast<size_t>(f)].get(), kC, 0.f,
+              T.g.get(), kK3);
+      check(dbk_tr_col2im(n, kC, T.g.get(), T.da2.get(), nullptr, T.dx.get(), s), "col2im x");
+      if (a == 1) {
+        check(dbk_tr_route(n, nodes, B.child0.get(), B.fid.get(), B.arity_of.get(), B.example.get(), T.dx.get(), kC,
+                           0, T.dy_nodes.get(), T.d_inputs.get(), s),
+              "route");
+        continue;
+      }
+      // binary: z = relu(conv1x1([x; y]) + b0) was the block input (xin)
+      check(dbk_tr_mask(rows * kC, T.dx.get(), xin, T.da0.get(), s), "relu z");
+      check(dbk_tr_colsum(rows, kC, T.da0.get(), T.gb0[static_cast<size_t>(f)].get(), s), "db0");
+      check(cudaMemsetAsync(T.cat.get(), 0, sizeof(float) * static_cast<size_t>(rows) * 2 * kC, s), "zero");
+      check(dbk_tr_stage_to_pi(n, row0, R.stage_cat.get(), nullptr, ps, 0, 32, T.cat.get(), s), "cat");
+      rm_gemm(h, true, false, 2 * kC, kC, rows, T.cat.get(), 2 * kC, T.da0.get(), kC, 1.f,
+              T.gw0[static_cast<size_t>(f)].get(), kC);
+      rm_gemm(h, false, true, rows, 2 * kC, kC, T.da0.get(), kC, T.w0[static_cast<size_t>(f)].get(), kC, 0.f,
+              T.dcat.get(), 2 * kC);
+      check(dbk_tr_route(n, nodes, B.child0.get(), B.fid.get(), B.arity_of.get(), B.example.get(), T.dcat.get(),
+                         2 * kC, 0, T.dy_nodes.get(), T.d_inputs.get(), s),
+            "route 0");
+      check(dbk_tr_route(n, nodes, B.child1.get(), B.fid.get(), B.arity_of.get(), B.example.get(), T.dcat.get(),
+                         2 * kC, kC, T.dy_nodes.get(), T.d_inputs.get(), s),
+            "route 1");
+    }
+  }
+}
+
+std::int64_t IepSession::grad_size(int which, int fid) const {
+  if (!train_ || !head_) throw_error(Errc::invalid_argument, "training is off or no head");
+  const std::int64_t C = kC, P = IepHead::kP, F = IepHead::kF, A = head_->answers();
+  if (which < 6) {
+    if (fid < 0 || fid >= static_cast<int>(train_->arity.size()) || train_->arity[static_cast<size_t>(fid)] == 0)
+      throw_error(Errc::unknown_function, "function " + std::to_string(fid) + " has no weights");
+    const int a = train_->arity[static_cast<size_t>(fid)];
+    switch (which) {
+      case 0: return a == 2 ? 2 * C * C : 0;
+      case 1: return a == 2 ? C : 0;
+      case 2: case 4: return 9 * C * C;
+      default: return C;
+    }
+  }
+  switch (which) {
+    case 6: return C * P;
+    case 7: return P;
+    case 8: return 49 * P * F;
+    case 9: return F;
+    case 10: return F * A;
+    case 11: return A;
+    case 12: return batch_->csr().b * C * kPx;
+    default: throw_error(Errc::invalid_argument, "gradient index");
+  }
+}
+
+void IepSession::download_grad(int which, int fid, float* out, std::int64_t n) {
+  const std::int64_t want = grad_size(which, fid);
+  if (n != want) throw_error(Errc::row_count_mismatch, "gradient buffer size");
+  if (n == 0) return;
+  Train& T = *train_;
+  const float* src = nullptr;
+  const size_t f = static_cast<size_t>(std::max(fid, 0));
+  switch (which) {
+    case 0: src = T.gw0[f].get(); break;
+    case 1: src = T.gb0[f].get(); break;
+    case 2: src = T.gw1[f].get(); break;
+    case 3: src = T.gb1[f].get(); break;
+    case 4: src = T.gw2[f].get(); break;
+    case 5: src = T.gb2[f].get(); break;
+    case 6: src = T.gwp.get(); break;
+    case 7: src = T.gbp.get(); break;
+    case 8: src = T.ghw1.get(); break;
+    case 9: src = T.ghb1.get(); break;
+    case 10: src = T.ghw2.get(); break;
+    case 11: src = T.ghb2.get(); break;
+    default: src = T.d_inputs.get(); break;
+  }
+  check(cudaMemcpyAsync(out, src, sizeof(float) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, stream_), "D2H");
+  check(cudaStreamSynchronize(stream_), "sync");
+}
+
+double IepSession::time_train(int iters, const std::int32_t* labels) {
+  train_step(labels);  // warm: sizes every buffer
+  cudaEvent_t e0, e1;
+  check(cudaEventCreate(&e0), "event");
+  check(cudaEventCreate(&e1), "event");
+  check(cudaEventRecord(e0, stream_), "event");
+  for (int i = 0; i < iters; ++i) train_step(labels);
+  check(cudaEventRecord(e1, stream_), "event");
+  check(cudaEventSynchronize(e1), "sync");
+  float ms = 0.f;
+  check(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms / std::max(iters, 1);
+}
+
+}  // namespace dynbatch::dev

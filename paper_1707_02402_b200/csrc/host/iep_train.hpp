@@ -1,0 +1,35 @@
+// iep_train.hpp — device state of the IEP training step (iep_train.cpp).
+#pragma once
+
+#include <cublas_v2.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "device.hpp"
+
+namespace dynbatch::dev {
+
+struct IepSession::Train {
+  cublasHandle_t blas = nullptr;
+  std::vector<int> arity;  // per function id
+  // fp32 input-major module weights (w0 [2C][C], w1 / w2 [9C][C]) and the
+  // gradients of every weight and bias, per function
+  std::vector<Buf<float>> w0, w1, w2, gw0, gb0, gw1, gb1, gw2, gb2;
+  // head gradients (wp [C][P], bp, w1 [49P][F], b1, w2 [F][A], b2)
+  Buf<float> gwp, gbp, ghw1, ghb1, ghw2, ghb2;
+  Buf<float> d_inputs;  // [b][C·196] CHW
+  Buf<float> dy_nodes;  // [N][257][C]: gradient of every node's output, PI layout
+  Buf<float> loss;
+  Buf<std::int32_t> labels;
+  // per-group scratch (PI rows; mid / xin carry 16 guard rows at each end)
+  Buf<float> da2, mid, xin, cols, g, da1, dx, da0, cat, dcat;
+  // head scratch
+  Buf<float> dlogits, hid, dhid, pooled, dpooled, proj, dproj, roots, droots;
+  std::int64_t cap_rows = 0, cap_b = 0, cap_n = 0;
+  ~Train() {
+    if (blas) cublasDestroy(blas);
+  }
+};
+
+}  // namespace dynbatch::dev

@@ -1157,7 +1157,7 @@ __global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const
                          const int32_t* __restrict__ seg_start, const int32_t* __restrict__ member_g,
                          const int32_t* __restrict__ child0, const int32_t* __restrict__ child1,
                          const int32_t* __restrict__ fwd_ok, int32_t* __restrict__ fwd_pos,
-                         int32_t* __restrict__ fwd_slot, int32_t* __restrict__ fwd_parent) {
+                         int32_t* __restrict__ fwd_slot, int32_t* __restrict__ fwd_parent, int32_t keep_all) {
   // a block per group (no per-member search), threads over its members
   for (int32_t g = sgb[0] + blockIdx.x; g < sgb[n_steps]; g += gridDim.x) {
     if (seg_start[g] < 0) continue;
@@ -1170,7 +1170,7 @@ __global__ void k_rb_fwd(int32_t n_steps, const int32_t* __restrict__ sgb, const
         fwd_pos[c] = seg_start[g] + (m - group_begin[g]) * kImg;
         // buffer (bit 0: stage_x / stage_cat) and first plane; no fp32 copy:
         // a unary parent reads its residual from the hi/lo images
-        fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1);
+        fwd_slot[c] = (arity == 2 ? 1 : 0) | ((16 * k) << 1) | (keep_all << 8);
         fwd_parent[c] = node;
       }
     }
@@ -1339,6 +1339,10 @@ __global__ void __launch_bounds__(256) k_roots_to_chw(const int32_t* __restrict_
 }
 
 int32_t g_debug_flag = 0;
+// Training forwards (dbk_rb_set_training): every expensive node also keeps
+// its fp32 value (the backward's ReLU masks) and the mid images stay in
+// place (no discard), since the backward reads them.
+int32_t g_train_mode = 0;
 
 }  // namespace
 
@@ -1358,7 +1362,7 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
   k_rb_fwd_init<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_nodes, fwd_pos, fwd_slot,
                                                                               fwd_parent, need);
   k_rb_fwd<<<148 * 4, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
-                                   member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot, fwd_parent);
+                                   member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot, fwd_parent, g_train_mode);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -1437,6 +1441,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
   p.diag = dg ? std::atoi(dg) : 0;
   const char* ch = std::getenv("DYNBATCH_CACHE");
   p.cache = ch ? std::atoi(ch) : 4;  // default: drop consumed interior mid lines from L2
+  if (g_train_mode) p.cache &= ~12;  // the backward reads mid and the block inputs
   p.step_tile_begin = step_tile_begin;
   p.tile_group = tile_group;
   p.tile_q0 = tile_q0;
@@ -1508,6 +1513,11 @@ extern "C" int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int
   k_roots_to_chw<<<static_cast<unsigned>(b * kPlanes), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       root_g, fid, arity_of, example, inputs, values, chw);
   return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_rb_set_training(int32_t on) {
+  g_train_mode = on ? 1 : 0;
+  return 0;
 }
 
 // Copies (and optionally zeroes) the MMA-thread wait counters; enable != 0
