@@ -473,6 +473,34 @@ def run_ours(args, dist):
     except Exception as e:  # reported, not fatal
         out["head"] = {"error": str(e)}
 
+    # one training step (training forward, head, softmax
+    # cross-entropy, backward through the head and the module groups) on this
+    # minibatch, and on its first 64 programs the naive schedule's step (the
+    # paper's batched-backward comparison)
+    try:
+        labels = (np.arange(per) % 28).astype(np.int32)
+        sess.set_training(True)
+        tms = sess.time_train(max(2, min(args.steps, 5)), labels)
+        sess.set_training(False)
+        nb = min(per, 64)
+        sub = [db.IepSession(batch, module_seed, db.MODULE_RESBLOCK, first=0, last=nb) for _ in range(2)]
+        sub[1].set_schedule(db.Batch.generate_range(first, first + nb, cfg["kind"], batch=B, vocab=cfg["vocab"],
+                                                    width=8, depth=cfg["depth"], length=cfg["length"],
+                                                    branch_prob=cfg["branch_prob"], seed=0).schedule("naive"))
+        sub_ms = []
+        for x in sub:
+            x.set_head(28, module_seed)
+            x.set_training(True)
+            sub_ms.append(x.time_train(2, labels[:nb]))
+        out["train"] = {"ms_per_step": tms, "programs_per_s": per / (tms / 1e3),
+                        "backward_over_forward": (tms - ms_step) / ms_step,
+                        "gemms": "cuBLAS TF32 (library GEMMs); operand moves in train.cu",
+                        "naive_vs_improved_64": {"improved_ms": sub_ms[0], "naive_ms": sub_ms[1],
+                                                 "speedup": sub_ms[1] / sub_ms[0]}}
+        del sub
+    except Exception as e:  # reported, not fatal
+        out["train"] = {"error": str(e)}
+
     # naive per-example execution on the GPU (same kernels, one node per step)
     try:
         nb = min(per, 64)

@@ -207,8 +207,10 @@ int dbk_moe_tc_gemm(int32_t fmt, int32_t epi, int32_t n, int32_t K, int32_t N, c
  * 257 rows (16 zero guard rows, the 225 packed positions, 16 guard rows) ×
  * channels, fp32. */
 int dbk_rb_set_training(int32_t on); /* forwards keep every node's fp32 value and the mid images */
-int dbk_tr_stage_to_pi(int32_t n, int64_t row0, const void* hi, const void* lo, int64_t ps, int32_t plane0,
+int dbk_tr_stage_to_pi(int32_t n, const int64_t* rows, const void* hi, const void* lo, int64_t ps, int32_t plane0,
                        int32_t planes, float* out, void* stream);
+/* bias gradients of 128 channels: slab i = rows [slab_row[2i], slab_row[2i+1]) into dst[i] */
+int dbk_tr_colsum_seg(int32_t slabs, const int64_t* slab_row, float* const* dst, const float* a, void* stream);
 int dbk_tr_da_out(int32_t n, const int32_t* nodes, const float* dy_nodes, const float* values, float* out,
                   void* stream);
 int dbk_tr_im2col(int64_t rows, int32_t ch, const float* x, float* cols, void* stream);

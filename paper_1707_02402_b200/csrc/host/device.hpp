@@ -266,6 +266,7 @@ class IepSession {
   // cross-entropy over labels[b] → backward through the head and the module
   // groups in reverse step order. Gradients are fp32, input-major like the
   // weights; they are overwritten by every step.
+  struct Train;  // iep_train.hpp
   void set_training(bool on);
   float train_step(const std::int32_t* labels);
   // which: 0-5 = module w0, b0, w1, b1, w2, b2 of function fid; 6-11 = head
@@ -325,7 +326,6 @@ class IepSession {
   struct RB;
   std::unique_ptr<RB> rb_;
   std::unique_ptr<IepHead> head_;
-  struct Train;
   std::unique_ptr<Train> train_;
   std::uint64_t module_seed_ = 0;
   void backward(float* loss_dev);

@@ -20,6 +20,7 @@
 #include "iep_train.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -69,6 +70,52 @@ std::vector<float> to_f32(const std::vector<double>& v) { return std::vector<flo
 
 }  // namespace
 
+// One row-major GEMM of a grouped call (rm_gemm's arguments).
+struct GemmDesc {
+  bool ta, tb;
+  std::int64_t M, N, K;
+  const float* A;
+  std::int64_t lda;
+  const float* B;
+  std::int64_t ldb;
+  float* C;
+  std::int64_t ldc;
+  float beta;
+};
+
+// The GEMMs of one step and weight kind (one per group, different weights)
+// as one cublasGemmGroupedBatchedEx call (TF32), operands swapped for the
+// row-major layout as in rm_gemm. `ptrs` = the calls' device pointer arrays
+// (cuBLAS A = our B, cuBLAS B = our A, C), uploaded with every step's.
+void grouped_gemm(cublasHandle_t h, const std::vector<GemmDesc>& d, const void* const* ptrs) {
+  if (d.empty()) return;
+  const size_t n = d.size();
+  std::vector<cublasOperation_t> ta(n), tb(n);
+  std::vector<int> m(n), nn(n), k(n), lda(n), ldb(n), ldc(n), gs(n, 1);
+  std::vector<float> alpha(n, 1.f), beta(n);
+  for (size_t i = 0; i < n; ++i) {
+    const GemmDesc& g = d[i];
+    ta[i] = g.tb ? CUBLAS_OP_T : CUBLAS_OP_N;
+    tb[i] = g.ta ? CUBLAS_OP_T : CUBLAS_OP_N;
+    m[i] = static_cast<int>(g.N);
+    nn[i] = static_cast<int>(g.M);
+    k[i] = static_cast<int>(g.K);
+    lda[i] = static_cast<int>(g.ldb);
+    ldb[i] = static_cast<int>(g.lda);
+    ldc[i] = static_cast<int>(g.ldc);
+    beta[i] = g.beta;
+  }
+  const cublasStatus_t st = cublasGemmGroupedBatchedEx(
+      h, ta.data(), tb.data(), m.data(), nn.data(), k.data(), alpha.data(), ptrs, CUDA_R_32F, lda.data(), ptrs + n,
+      CUDA_R_32F, ldb.data(), beta.data(), const_cast<void* const*>(ptrs + 2 * n), CUDA_R_32F, ldc.data(),
+      static_cast<int>(n), gs.data(), compute_type());
+  if (st == CUBLAS_STATUS_NOT_SUPPORTED) {  // one call per group
+    for (const GemmDesc& g : d) rm_gemm(h, g.ta, g.tb, g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.beta, g.C, g.ldc);
+  } else {
+    cublas_check(st, "grouped gemm");
+  }
+}
+
 void IepSession::set_training(bool on) {
   if (!on) {
     train_.reset();
@@ -79,6 +126,7 @@ void IepSession::set_training(bool on) {
   auto t = std::make_unique<Train>();
   cublas_check(cublasCreate(&t->blas), "create");
   cublas_check(cublasSetStream(t->blas, stream_), "stream");
+
   const HostCSR& c = batch_->csr();
   t->arity = c.arity_of;
   const size_t p = t->arity.size();
@@ -193,15 +241,45 @@ void IepSession::backward(float* loss_dev) {
                       T.dy_nodes.get(), T.d_inputs.get(), s),
         "route roots");
 
-  // ---- module groups, reverse step order
+  // ---- module groups, reverse step order: each step's expensive members in
+  // one set of PI buffers (unary groups first, then binary), elementwise
+  // kernels over the whole step, one grouped GEMM per weight kind and step
   const int S = B.steps;
   const std::vector<std::int32_t> sgb = B.step_group_begin.download(static_cast<size_t>(S) + 1, s);
   const std::int64_t G = sgb[static_cast<size_t>(S)];
   const std::vector<std::int32_t> gfid = B.group_fid.download(static_cast<size_t>(G), s);
   const std::vector<std::int32_t> gbeg = B.group_begin.download(static_cast<size_t>(G) + 1, s);
   const std::vector<std::int32_t> seg = R.seg_start.download(static_cast<size_t>(G), s);
+  const std::vector<std::int32_t> mem = B.member_g.download(static_cast<size_t>(gbeg[static_cast<size_t>(G)]), s);
+  struct StepPlan {
+    std::int64_t n = 0, n_u = 0;       // members, of which in unary groups
+    std::int64_t m_off = 0;            // into the node / row tables
+    std::vector<int> groups;           // schedule groups, unary first
+    std::vector<std::int64_t> first;   // member index (within the step) of each group
+  };
+  std::vector<StepPlan> plan(static_cast<size_t>(S));
+  std::vector<std::int32_t> h_nodes;
+  std::vector<std::int64_t> h_rows, h_slab;
+  std::vector<float*> h_slab_dst;
   std::int64_t n_max = 0;
-  for (std::int64_t g = 0; g < G; ++g) n_max = std::max<std::int64_t>(n_max, gbeg[g + 1] - gbeg[g]);
+  for (int st = 0; st < S; ++st) {
+    StepPlan& sp = plan[static_cast<size_t>(st)];
+    sp.m_off = static_cast<std::int64_t>(h_nodes.size());
+    for (int pass = 1; pass <= 2; ++pass)
+      for (std::int32_t g = sgb[static_cast<size_t>(st)]; g < sgb[static_cast<size_t>(st) + 1]; ++g) {
+        const int a = T.arity[static_cast<size_t>(gfid[static_cast<size_t>(g)])];
+        if (a != pass || seg[static_cast<size_t>(g)] < 0 || gbeg[g + 1] == gbeg[g]) continue;
+        sp.groups.push_back(g);
+        sp.first.push_back(sp.n);
+        for (std::int32_t m = gbeg[g]; m < gbeg[g + 1]; ++m) {
+          h_nodes.push_back(mem[static_cast<size_t>(m)]);
+          h_rows.push_back(seg[static_cast<size_t>(g)] + static_cast<std::int64_t>(m - gbeg[g]) * 225);
+        }
+        sp.n += gbeg[g + 1] - gbeg[g];
+        if (pass == 1) sp.n_u = sp.n;
+      }
+    n_max = std::max(n_max, sp.n);
+  }
   const std::int64_t rows_max = n_max * kPI;
   if (rows_max > T.cap_rows) {
     const size_t r = static_cast<size_t>(rows_max), rg = r + 2 * kG;
@@ -217,63 +295,143 @@ void IepSession::backward(float* loss_dev) {
     T.dcat.alloc(r * 2 * kC);
     T.cap_rows = rows_max;
   }
+  T.nodes.upload(h_nodes, s);
+  T.rows.upload(h_rows, s);
   const std::int64_t ps = R.plane_stride;
   float* mid = T.mid.get() + kG * kC;  // row 0 of the first member (16 guard rows before)
   float* xin = T.xin.get() + kG * kC;
-  for (int st = S - 1; st >= 0; --st) {
-    for (std::int32_t g = sgb[static_cast<size_t>(st)]; g < sgb[static_cast<size_t>(st) + 1]; ++g) {
-      const int f = gfid[static_cast<size_t>(g)];
-      const int a = T.arity[static_cast<size_t>(f)];
-      const std::int32_t n = gbeg[static_cast<size_t>(g) + 1] - gbeg[static_cast<size_t>(g)];
-      if (a == 0 || n == 0 || seg[static_cast<size_t>(g)] < 0) continue;
-      const std::int64_t rows = static_cast<std::int64_t>(n) * kPI;
-      const std::int32_t* nodes = B.member_g.get() + gbeg[static_cast<size_t>(g)];
-      const std::int64_t row0 = seg[static_cast<size_t>(g)];
-      // zero the PI buffers' guard and pad rows the gathers leave untouched
-      check(cudaMemsetAsync(T.mid.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
-      check(cudaMemsetAsync(T.xin.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
-      check(cudaMemsetAsync(T.da2.get(), 0, sizeof(float) * static_cast<size_t>(rows) * kC, s), "zero");
-      // conv3x3 #2: da2, dW2, db2, da1
-      check(dbk_tr_da_out(n, nodes, T.dy_nodes.get(), R.values.get(), T.da2.get(), s), "da2");
-      check(dbk_tr_colsum(rows, kC, T.da2.get(), T.gb2[static_cast<size_t>(f)].get(), s), "db2");
-      check(dbk_tr_stage_to_pi(n, row0, R.stage_mid.get(), nullptr, ps, 0, 16, mid, s), "mid");
-      check(dbk_tr_im2col(rows, kC, mid, T.cols.get(), s), "im2col mid");
-      rm_gemm(h, true, false, kK3, kC, rows, T.cols.get(), kK3, T.da2.get(), kC, 1.f,
-              T.gw2[static_cast<size_t>(f)].get(), kC);
-      rm_gemm(h, false, true, rows, kK3, kC, T.da2.get(), kC, T.w2[static_cast<size_t>(f)].get(), kC, 0.f,
-              T.g.get(), kK3);
-      check(dbk_tr_col2im(n, kC, T.g.get(), nullptr, mid, T.da1.get(), s), "col2im mid");
-      // conv3x3 #1: dW1, db1, dx (+ the residual)
-      check(dbk_tr_colsum(rows, kC, T.da1.get(), T.gb1[static_cast<size_t>(f)].get(), s), "db1");
-      check(dbk_tr_stage_to_pi(n, row0, R.stage_x.get(), R.stage_lo.get(), ps, 0, 16, xin, s), "x");
-      check(dbk_tr_im2col(rows, kC, xin, T.cols.get(), s), "im2col x");
-      rm_gemm(h, true, false, kK3, kC, rows, T.cols.get(), kK3, T.da1.get(), kC, 1.f,
-              T.gw1[static_cast<size_t>(f)].get(), kC);
-      rm_gemm(h, false, true, rows, kK3, kC, T.da1.get(), kC, T.w1[static_cast<size_t>(f)].get(), kC, 0.f,
-              T.g.get(), kK3);
-      check(dbk_tr_col2im(n, kC, T.g.get(), T.da2.get(), nullptr, T.dx.get(), s), "col2im x");
-      if (a == 1) {
-        check(dbk_tr_route(n, nodes, B.child0.get(), B.fid.get(), B.arity_of.get(), B.example.get(), T.dx.get(), kC,
-                           0, T.dy_nodes.get(), T.d_inputs.get(), s),
-              "route");
-        continue;
+  // per (group, bias): slabs of ≤ 512 rows; the tables of every step and
+  // bias kind are built here and uploaded once
+  struct SlabRange { std::int64_t begin, count; };
+  auto add_slabs = [&](const StepPlan& sp, size_t gi0, size_t gi1, std::int64_t row_base,
+                       std::vector<Buf<float>>& dst) -> SlabRange {
+    const SlabRange r{static_cast<std::int64_t>(h_slab_dst.size()), 0};
+    SlabRange out = r;
+    for (size_t gi = gi0; gi < gi1; ++gi) {
+      const int g = sp.groups[gi];
+      const std::int64_t r0 = sp.first[gi] * kPI - row_base;
+      const std::int64_t r1 = (gi + 1 < sp.groups.size() ? sp.first[gi + 1] : sp.n) * kPI - row_base;
+      for (std::int64_t x = r0; x < r1; x += 512) {
+        h_slab.push_back(x);
+        h_slab.push_back(std::min(r1, x + 512));
+        h_slab_dst.push_back(dst[static_cast<size_t>(gfid[static_cast<size_t>(g)])].get());
+        ++out.count;
       }
-      // binary: z = relu(conv1x1([x; y]) + b0) was the block input (xin)
-      check(dbk_tr_mask(rows * kC, T.dx.get(), xin, T.da0.get(), s), "relu z");
-      check(dbk_tr_colsum(rows, kC, T.da0.get(), T.gb0[static_cast<size_t>(f)].get(), s), "db0");
-      check(cudaMemsetAsync(T.cat.get(), 0, sizeof(float) * static_cast<size_t>(rows) * 2 * kC, s), "zero");
-      check(dbk_tr_stage_to_pi(n, row0, R.stage_cat.get(), nullptr, ps, 0, 32, T.cat.get(), s), "cat");
-      rm_gemm(h, true, false, 2 * kC, kC, rows, T.cat.get(), 2 * kC, T.da0.get(), kC, 1.f,
-              T.gw0[static_cast<size_t>(f)].get(), kC);
-      rm_gemm(h, false, true, rows, 2 * kC, kC, T.da0.get(), kC, T.w0[static_cast<size_t>(f)].get(), kC, 0.f,
-              T.dcat.get(), 2 * kC);
-      check(dbk_tr_route(n, nodes, B.child0.get(), B.fid.get(), B.arity_of.get(), B.example.get(), T.dcat.get(),
-                         2 * kC, 0, T.dy_nodes.get(), T.d_inputs.get(), s),
-            "route 0");
-      check(dbk_tr_route(n, nodes, B.child1.get(), B.fid.get(), B.arity_of.get(), B.example.get(), T.dcat.get(),
-                         2 * kC, kC, T.dy_nodes.get(), T.d_inputs.get(), s),
-            "route 1");
     }
+    return out;
+  };
+  std::vector<std::array<SlabRange, 3>> slabs(static_cast<size_t>(S));
+  for (int st = 0; st < S; ++st) {
+    const StepPlan& sp = plan[static_cast<size_t>(st)];
+    const size_t nu = static_cast<size_t>(std::count_if(sp.first.begin(), sp.first.end(),
+                                                        [&](std::int64_t f) { return f < sp.n_u; }));
+    slabs[static_cast<size_t>(st)][0] = add_slabs(sp, 0, sp.groups.size(), 0, T.gb2);
+    slabs[static_cast<size_t>(st)][1] = add_slabs(sp, 0, sp.groups.size(), 0, T.gb1);
+    slabs[static_cast<size_t>(st)][2] = add_slabs(sp, nu, sp.groups.size(), sp.n_u * kPI, T.gb0);
+  }
+  T.slab_row.upload(h_slab, s);  // pairs (begin, end) per slab
+  T.slab_dst.upload(h_slab_dst, s);
+  auto colsum = [&](const SlabRange& r, const float* a) {
+    if (r.count)
+      check(dbk_tr_colsum_seg(static_cast<std::int32_t>(r.count), T.slab_row.get() + 2 * r.begin,
+                              T.slab_dst.get() + r.begin, a, s),
+            "bias gradients");
+  };
+  // per-group GEMM descriptors of every step (6 kinds: dW2, G2, dW1, G1, dW0,
+  // dcat) and their device pointer arrays, uploaded once
+  std::vector<std::array<std::vector<GemmDesc>, 6>> descs(static_cast<size_t>(S));
+  std::vector<std::array<std::int64_t, 6>> ptr_off(static_cast<size_t>(S));
+  std::vector<const void*> h_ptrs;
+  for (int st = 0; st < S; ++st) {
+    const StepPlan& sp = plan[static_cast<size_t>(st)];
+    auto& [w2, d2, w1, d1, w0, d0] = descs[static_cast<size_t>(st)];
+    for (size_t gi = 0; gi < sp.groups.size(); ++gi) {
+      const size_t f = static_cast<size_t>(gfid[static_cast<size_t>(sp.groups[gi])]);
+      const std::int64_t r0 = sp.first[gi] * kPI;
+      const std::int64_t rg = ((gi + 1 < sp.groups.size() ? sp.first[gi + 1] : sp.n) - sp.first[gi]) * kPI;
+      w2.push_back({true, false, kK3, kC, rg, T.cols.get() + r0 * kK3, kK3, T.da2.get() + r0 * kC, kC,
+                    T.gw2[f].get(), kC, 1.f});
+      d2.push_back({false, true, rg, kK3, kC, T.da2.get() + r0 * kC, kC, T.w2[f].get(), kC, T.g.get() + r0 * kK3,
+                    kK3, 0.f});
+      w1.push_back({true, false, kK3, kC, rg, T.cols.get() + r0 * kK3, kK3, T.da1.get() + r0 * kC, kC,
+                    T.gw1[f].get(), kC, 1.f});
+      d1.push_back({false, true, rg, kK3, kC, T.da1.get() + r0 * kC, kC, T.w1[f].get(), kC, T.g.get() + r0 * kK3,
+                    kK3, 0.f});
+      if (r0 >= sp.n_u * kPI) {  // binary group: rows relative to the binary part
+        const std::int64_t rb = r0 - sp.n_u * kPI;
+        w0.push_back({true, false, 2 * kC, kC, rg, T.cat.get() + rb * 2 * kC, 2 * kC, T.da0.get() + rb * kC, kC,
+                      T.gw0[f].get(), kC, 1.f});
+        d0.push_back({false, true, rg, 2 * kC, kC, T.da0.get() + rb * kC, kC, T.w0[f].get(), kC,
+                      T.dcat.get() + rb * 2 * kC, 2 * kC, 0.f});
+      }
+    }
+    for (size_t kd = 0; kd < 6; ++kd) {
+      const auto& d = descs[static_cast<size_t>(st)][kd];
+      ptr_off[static_cast<size_t>(st)][kd] = static_cast<std::int64_t>(h_ptrs.size());
+      for (const GemmDesc& g : d) h_ptrs.push_back(g.B);
+      for (const GemmDesc& g : d) h_ptrs.push_back(g.A);
+      for (const GemmDesc& g : d) h_ptrs.push_back(g.C);
+    }
+  }
+  T.ptr_dev.upload(h_ptrs, s);
+  check(cudaStreamSynchronize(s), "backward tables");  // the host tables go out of scope
+  for (int st = S - 1; st >= 0; --st) {
+    const StepPlan& sp = plan[static_cast<size_t>(st)];
+    if (sp.n == 0) continue;
+    const std::int64_t n = sp.n, rows = n * kPI;
+    const std::int32_t* nodes = T.nodes.get() + sp.m_off;
+    const std::int64_t* srows = T.rows.get() + sp.m_off;
+    const auto& dd = descs[static_cast<size_t>(st)];
+    const auto& po = ptr_off[static_cast<size_t>(st)];
+    // weight gradients (K = the group's rows, a small M × N) one call per
+    // group, so cuBLAS can split K; the data gradients as one grouped call
+    auto gemms = [&](int kd) {
+      const auto& d = dd[static_cast<size_t>(kd)];
+      if (kd % 2 == 0) {
+        for (const GemmDesc& g : d) rm_gemm(T.blas, g.ta, g.tb, g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.beta, g.C, g.ldc);
+      } else {
+        grouped_gemm(T.blas, d, T.ptr_dev.get() + po[static_cast<size_t>(kd)]);
+      }
+    };
+    check(cudaMemsetAsync(T.mid.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
+    check(cudaMemsetAsync(T.xin.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
+    // conv3x3 #2: da2 → dW2, db2; da1 = col2im(da2·W2ᵀ) ⊙ (mid > 0)
+    check(dbk_tr_da_out(static_cast<std::int32_t>(n), nodes, T.dy_nodes.get(), R.values.get(), T.da2.get(), s), "da2");
+    colsum(slabs[static_cast<size_t>(st)][0], T.da2.get());
+    check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_mid.get(), nullptr, ps, 0, 16, mid, s), "mid");
+    check(dbk_tr_im2col(rows, kC, mid, T.cols.get(), s), "im2col mid");
+    gemms(0);
+    gemms(1);
+    check(dbk_tr_col2im(static_cast<std::int32_t>(n), kC, T.g.get(), nullptr, mid, T.da1.get(), s), "col2im mid");
+    // conv3x3 #1: dW1, db1; dx = col2im(da1·W1ᵀ) + da2 (the residual)
+    colsum(slabs[static_cast<size_t>(st)][1], T.da1.get());
+    check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_x.get(), R.stage_lo.get(), ps, 0, 16, xin, s),
+          "x");
+    check(dbk_tr_im2col(rows, kC, xin, T.cols.get(), s), "im2col x");
+    gemms(2);
+    gemms(3);
+    check(dbk_tr_col2im(static_cast<std::int32_t>(n), kC, T.g.get(), T.da2.get(), nullptr, T.dx.get(), s), "col2im x");
+    if (sp.n_u > 0)
+      check(dbk_tr_route(static_cast<std::int32_t>(sp.n_u), nodes, B.child0.get(), B.fid.get(), B.arity_of.get(),
+                         B.example.get(), T.dx.get(), kC, 0, T.dy_nodes.get(), T.d_inputs.get(), s),
+            "route");
+    const std::int64_t nb = n - sp.n_u;
+    if (nb == 0) continue;
+    // binary groups: z = relu(conv1x1([x; y]) + b0) was the block input
+    const std::int64_t ub = sp.n_u * kPI;
+    check(dbk_tr_mask(nb * kPI * kC, T.dx.get() + ub * kC, xin + ub * kC, T.da0.get(), s), "relu z");
+    colsum(slabs[static_cast<size_t>(st)][2], T.da0.get());
+    check(cudaMemsetAsync(T.cat.get(), 0, sizeof(float) * static_cast<size_t>(nb * kPI) * 2 * kC, s), "zero");
+    check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(nb), srows + sp.n_u, R.stage_cat.get(), nullptr, ps, 0, 32,
+                             T.cat.get(), s),
+          "cat");
+    gemms(4);
+    gemms(5);
+    for (int k = 0; k < 2; ++k)
+      check(dbk_tr_route(static_cast<std::int32_t>(nb), nodes + sp.n_u, k == 0 ? B.child0.get() : B.child1.get(),
+                         B.fid.get(), B.arity_of.get(), B.example.get(), T.dcat.get(), 2 * kC, k * kC,
+                         T.dy_nodes.get(), T.d_inputs.get(), s),
+            "route");
   }
 }
 

@@ -27,6 +27,12 @@ struct IepSession::Train {
   // head scratch
   Buf<float> dlogits, hid, dhid, pooled, dpooled, proj, dproj, roots, droots;
   std::int64_t cap_rows = 0, cap_b = 0, cap_n = 0;
+  // step tables of the backward: expensive member nodes and staging rows,
+  // bias slabs (row ranges and gradient targets), grouped-GEMM pointers
+  Buf<std::int32_t> nodes;
+  Buf<std::int64_t> rows, slab_row;
+  Buf<float*> slab_dst;
+  Buf<const void*> ptr_dev;
   ~Train() {
     if (blas) cublasDestroy(blas);
   }

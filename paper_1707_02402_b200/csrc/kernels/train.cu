@@ -34,10 +34,11 @@ unsigned grid_for(int64_t n, int per_block = 256) {
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n + per_block - 1) / per_block, 148 * 32)));
 }
 
-// fp16 staging (hi, + lo when given) of n images starting at staging row
-// `row0` (absolute, kGuard included) → fp32 PI [n][257][planes·8]; pads 0.
-__global__ void k_stage_to_pi(int32_t n, int64_t row0, const uint8_t* __restrict__ hi, const uint8_t* __restrict__ lo,
-                              int64_t ps, int32_t plane0, int32_t planes, float* __restrict__ out) {
+// fp16 staging (hi, + lo when given) of n member images (image k at staging
+// position rows[k]) → fp32 PI [n][257][planes·8]; pads 0.
+__global__ void k_stage_to_pi(int32_t n, const int64_t* __restrict__ rows, const uint8_t* __restrict__ hi,
+                              const uint8_t* __restrict__ lo, int64_t ps, int32_t plane0, int32_t planes,
+                              float* __restrict__ out) {
   const int64_t total = static_cast<int64_t>(n) * kImg * planes;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -47,7 +48,7 @@ __global__ void k_stage_to_pi(int32_t n, int64_t row0, const uint8_t* __restrict
     const int p = static_cast<int>(kp % kImg);
     float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (!is_pad(p)) {
-      const int64_t r = row0 + static_cast<int64_t>(k) * kImg + p;
+      const int64_t r = kGuard + rows[k] + p;
       const uint4 h = *reinterpret_cast<const uint4*>(hi + stage_off(ps, plane0 + j, r));
       const __half2* h2 = reinterpret_cast<const __half2*>(&h);
 #pragma unroll
@@ -175,6 +176,17 @@ __global__ void __launch_bounds__(256) k_colsum(int64_t rows, int32_t cols, cons
     for (int64_t r = r0; r < r1; ++r) s += a[r * cols + c];
     if (s != 0.f) atomicAdd(db + c, s);
   }
+}
+
+// Segmented column sums of a 128-wide matrix: slab i covers rows
+// [slab_row[2i], slab_row[2i + 1]) of one group, whose bias gradient is
+// dst[i]; 128 threads per slab, one atomic per column and slab.
+__global__ void __launch_bounds__(128) k_colsum_seg(const int64_t* __restrict__ slab_row, float* const* __restrict__ dst,
+                                                    const float* __restrict__ a) {
+  const int64_t r0 = slab_row[2 * blockIdx.x], r1 = slab_row[2 * blockIdx.x + 1];
+  float s = 0.f;
+  for (int64_t r = r0; r < r1; ++r) s += a[r * kC + threadIdx.x];
+  if (s != 0.f) atomicAdd(dst[blockIdx.x] + threadIdx.x, s);
 }
 
 // Routes the gradient of member k's operand (PI rows of `src`, `ch` channels
@@ -324,12 +336,19 @@ __global__ void k_droots(int64_t b, const int32_t* __restrict__ root_g, const in
 
 }  // namespace
 
-extern "C" int dbk_tr_stage_to_pi(int32_t n, int64_t row0, const void* hi, const void* lo, int64_t ps,
+extern "C" int dbk_tr_stage_to_pi(int32_t n, const int64_t* rows, const void* hi, const void* lo, int64_t ps,
                                   int32_t plane0, int32_t planes, float* out, void* stream) {
   const int64_t total = static_cast<int64_t>(n) * kImg * planes;
   if (total <= 0) return 0;
   k_stage_to_pi<<<grid_for(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      n, row0 + kGuard, static_cast<const uint8_t*>(hi), static_cast<const uint8_t*>(lo), ps, plane0, planes, out);
+      n, rows, static_cast<const uint8_t*>(hi), static_cast<const uint8_t*>(lo), ps, plane0, planes, out);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_colsum_seg(int32_t slabs, const int64_t* slab_row, float* const* dst, const float* a,
+                                 void* stream) {
+  if (slabs <= 0) return 0;
+  k_colsum_seg<<<static_cast<unsigned>(slabs), kC, 0, static_cast<cudaStream_t>(stream)>>>(slab_row, dst, a);
   return static_cast<int>(cudaGetLastError());
 }
 
