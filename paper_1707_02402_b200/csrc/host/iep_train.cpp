@@ -383,15 +383,21 @@ void IepSession::backward(float* loss_dev) {
     const std::int64_t* srows = T.rows.get() + sp.m_off;
     const auto& dd = descs[static_cast<size_t>(st)];
     const auto& po = ptr_off[static_cast<size_t>(st)];
-    // weight gradients (K = the group's rows, a small M × N) one call per
-    // group, so cuBLAS can split K; the data gradients as one grouped call
+    // one cuBLAS call per group: the weight gradients (K = the group's rows,
+    // a small M × N) need split-K, and cublasGemmGroupedBatchedEx runs the
+    // data gradients on sm_80 grouped kernels 4× slower than the per-call
+    // sm_100 ones (measured); DYNBATCH_TRAIN_GROUPED=1 uses it for the latter
+    static const bool grouped_dgrad = [] {
+      const char* e = std::getenv("DYNBATCH_TRAIN_GROUPED");
+      return e && std::atoi(e) != 0;
+    }();
     auto gemms = [&](int kd) {
       const auto& d = dd[static_cast<size_t>(kd)];
-      if (kd % 2 == 0) {
-        for (const GemmDesc& g : d) rm_gemm(T.blas, g.ta, g.tb, g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.beta, g.C, g.ldc);
-      } else {
+      if (kd % 2 == 1 && grouped_dgrad) {
         grouped_gemm(T.blas, d, T.ptr_dev.get() + po[static_cast<size_t>(kd)]);
+        return;
       }
+      for (const GemmDesc& g : d) rm_gemm(T.blas, g.ta, g.tb, g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.beta, g.C, g.ldc);
     };
     check(cudaMemsetAsync(T.mid.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
     check(cudaMemsetAsync(T.xin.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
