@@ -113,7 +113,7 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
     R.tile_m = tiles256 < 2.0 * sm_count() ? 128 : RB::kTileM;
     if (const char* t = std::getenv("DYNBATCH_TILE_M")) {
       const int v = std::atoi(t);
-      if (v == 128 || v == 256) R.tile_m = v;
+      if (v == 64 || v == 128 || v == 256) R.tile_m = v;
     }
   }
   // buffers are sized for the session capacity (later set_programs batches)

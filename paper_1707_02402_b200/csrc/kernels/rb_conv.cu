@@ -1410,6 +1410,8 @@ extern "C" int dbk_rb_configure(void) {
     cudaFuncSetAttribute(k_rb_step<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     cudaFuncSetAttribute(k_rb_step<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     cudaFuncSetAttribute(k_rb_step<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
+    cudaFuncSetAttribute(k_rb_step<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     configured = true;
   }
   return static_cast<int>(cudaGetLastError());
@@ -1426,7 +1428,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
                            const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
                            int32_t* step_done, int32_t* queue, int32_t* err, int32_t* ready, const int32_t* need,
                            const int32_t* member_g, int32_t tile_m, int32_t num_sms, void* stream) {
-  if (tile_m != 256 && tile_m != 128) return static_cast<int>(cudaErrorInvalidValue);
+  if (tile_m != 256 && tile_m != 128 && tile_m != 64) return static_cast<int>(cudaErrorInvalidValue);
   dbk_rb_configure();
   StepParams p{};
   p.step = step;
@@ -1492,8 +1494,10 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
   cudaError_t e;
   if (tile_m == 256)
     e = p.debug ? cudaLaunchKernelEx(&cfg, k_rb_step<256, true>, p) : cudaLaunchKernelEx(&cfg, k_rb_step<256, false>, p);
-  else
+  else if (tile_m == 128)
     e = p.debug ? cudaLaunchKernelEx(&cfg, k_rb_step<128, true>, p) : cudaLaunchKernelEx(&cfg, k_rb_step<128, false>, p);
+  else
+    e = p.debug ? cudaLaunchKernelEx(&cfg, k_rb_step<64, true>, p) : cudaLaunchKernelEx(&cfg, k_rb_step<64, false>, p);
   return static_cast<int>(e != cudaSuccess ? e : cudaGetLastError());
 }
 
