@@ -142,7 +142,7 @@ int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* st
                 int64_t plane_stride, const void* const* w0, const void* const* w1, const void* const* w2,
                 const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
                 int32_t* done0, int32_t* done1, int32_t* step_done, int32_t* queue, int32_t* err,
-                int32_t* ready, const int32_t* need, const int32_t* member_g, int32_t tile_m, int32_t num_sms,
+                int32_t* ready, const int32_t* need, const int32_t* member_g, const int32_t* order, int32_t tile_m, int32_t num_sms,
                 void* stream);
 /* Zeroes stage_x rows between each segment's last image and its tile end
  * (read as top / left pads by the next segment's first image), every
@@ -153,6 +153,11 @@ int dbk_rb_zero_gaps(int32_t n_steps, const int32_t* step_group_begin, const int
  * slot, forwarding target row / buffer, keep-fp32 flag) and the gather task
  * lists (n_tasks[2] counters, reset here; capacity task_cap per list), built
  * after dbk_rb_plan from its forwarding tables. */
+/* Claim order of every step's work units (conv1x1 tiles DYNBATCH_BIN_LEAD SM-rows ahead of the conv3x3 #1
+ * tiles that read them); order[(bintile_begin[s] + 2·tile_begin[s]) / 2 + k] = (kind << 28) | unit. */
+int dbk_rb_order(int32_t n_steps, const int32_t* step_tile_begin, const int32_t* step_bintile_begin,
+                 const int32_t* tile_group, const int32_t* group_tile0, const int32_t* group_bintile0,
+                 int32_t num_sms, int32_t* prefix, int32_t* order, void* stream);
 int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
                   const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
                   const int32_t* fwd_pos, const int32_t* fwd_slot, const int32_t* arity_of, const int32_t* fid,

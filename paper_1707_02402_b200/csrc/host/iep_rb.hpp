@@ -35,6 +35,7 @@ struct IepSession::RB {
   Buf<std::int32_t> n_tasks;
   std::int64_t task_cap = 0;
   Buf<std::int32_t> done0, done1, queue;  // fused step kernel: tile done flags, claim counters
+  Buf<std::int32_t> order, order_prefix;  // per-step claim order of the work units (dbk_rb_order)
   Buf<std::int32_t> step_done;            // per step: conv3x3 #2 tiles finished (one-launch forwards)
   std::int32_t epoch = 1;                 // done-flag stamp (flags are cleared every forward)
   // forward_host_async: copy streams, triple-buffered CHW rows, events

@@ -187,6 +187,8 @@ void IepSession::init_resblock(const TensorBatch& inputs, std::uint64_t module_s
   R.done1.alloc(T + 2 * N);  // ≤ 2 tiles per group beyond the images (pairs)
   R.done0.zero(stream_);
   R.done1.zero(stream_);
+  R.order.alloc(3 * (T + 2 * N));
+  R.order_prefix.alloc(T + 2 * N);
   R.queue.alloc(S + 1);
   R.step_done.alloc(S + 1);
   // weights
@@ -258,11 +260,14 @@ void IepSession::forward_resblock() {
                       R.values.get(), R.memtab.get(), R.tasks.get(), R.n_tasks.get(), R.task_cap,
                       R.fwd_parent.get(), R.need.get(), R.tile_m, stream_),
         "dbk_rb_memtab");
+  check(dbk_rb_order(S, R.step_tile_begin.get(), R.step_bintile_begin.get(), R.tile_group.get(), R.group_tile0.get(),
+                     R.group_bintile0.get(), sms, R.order_prefix.get(), R.order.get(), stream_),
+        "dbk_rb_order");
   check(dbk_rb_zero_gaps(S, B.step_group_begin.get(), B.group_begin.get(), R.seg_start.get(), R.stage_x.get(),
                          R.plane_stride, R.tile_m, stream_),
         "dbk_rb_zero_gaps");
   prof_.end(stream_);
-  launches_ += 5;  // plan (+ tile lists), fwd init, fwd, memtab, zero gaps
+  launches_ += 6;  // plan (+ tile lists), fwd init, fwd, memtab, claim order, zero gaps
   const int gather_blocks = sms * 16;  // grid-stride over the step's (member, operand, chunk, pixel) items
   check(cudaMemsetAsync(R.queue.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_), "queue reset");
   check(cudaMemsetAsync(R.step_done.get(), 0, sizeof(std::int32_t) * static_cast<size_t>(S), stream_),
@@ -301,7 +306,7 @@ void IepSession::forward_resblock() {
                       R.memtab.get(), R.stage_x.get(), R.stage_lo.get(), R.stage_cat.get(), R.stage_mid.get(),
                       R.plane_stride, R.w0tab.get(), R.w1tab.get(), R.w2tab.get(), R.b0tab.get(), R.b1tab.get(),
                       R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.step_done.get(), R.queue.get(), err_.get(),
-                      R.ready.get(), R.need.get(), B.member_g.get(), R.tile_m, sms, stream_),
+                      R.ready.get(), R.need.get(), B.member_g.get(), R.order.get(), R.tile_m, sms, stream_),
           "conv step");
     prof_.end(stream_);
     ++launches_;

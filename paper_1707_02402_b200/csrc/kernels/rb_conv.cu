@@ -209,6 +209,9 @@ struct StepParams {
   const int32_t* need;
   const int32_t* member_g;
   int32_t step_barrier;   // 1: also wait for the whole previous step (A/B)
+  // Claim order per step (k_rb_order), units of kCluster tiles: entry
+  // (kind << 28) | local unit; null = the closed form of step_unit().
+  const int32_t* order;
 };
 
 // Error codes shared with the host (IepSession::check_errors): a module
@@ -294,8 +297,16 @@ __host__ __device__ __forceinline__ int32_t seg_tiles(int32_t rows, int32_t tile
 // MMA-heavy and store-heavy tiles and a #2 tile's inputs are usually done
 // when it is claimed.
 // With CTA pairs, k, n0 and n1 count tile pairs and `crank` picks the tile.
+// The item a claimed tile (unit `local` of `kind` in `step`, this CTA's tile
+// of it) is, with the group metadata every role needs.
+__device__ __forceinline__ Item item_of(const StepParams& P, int32_t step, int32_t kind, int32_t local, int32_t crank);
+
 __device__ __forceinline__ Item step_item(const StepParams& P, int32_t step, int32_t k, int32_t n0, int32_t n1,
                                           int32_t crank) {
+  if (P.order) {
+    const int32_t code = P.order[(P.step_bintile_begin[step] + 2 * P.step_tile_begin[step]) / kCluster + k];
+    return item_of(P, step, code >> 28, code & 0x0fffffff, crank);
+  }
   int32_t kind, local;
   if (k < n0) {
     kind = 0;
@@ -317,6 +328,10 @@ __device__ __forceinline__ Item step_item(const StepParams& P, int32_t step, int
       local = R + (u - D - 2 * R);
     }
   }
+  return item_of(P, step, kind, local, crank);
+}
+
+__device__ __forceinline__ Item item_of(const StepParams& P, int32_t step, int32_t kind, int32_t local, int32_t crank) {
   Item it;
   it.kind = kind;
   it.step = step;
@@ -1227,6 +1242,81 @@ __global__ void k_rb_memtab(int32_t n_steps, const int32_t* __restrict__ sgb,
   }
 }
 
+// ---------------------------------------------------------------- order
+// Claim order of every step's work units (StepParams::order). Three
+// streams over the step's conv3x3 units l = 0 … n1−1 (segment order): the
+// conv1x1 unit of conv unit c (binary groups) at key 3(c − D0), conv3x3 #1
+// unit l at 3l + 1, conv3x3 #2 unit l at 3(l + D) + 2; each unit's claim
+// index is its key's rank. So a conv1x1 tile runs D0 units before the
+// conv3x3 #1 tile that reads its z, and z is consumed (by #1, then by #2 D
+// units later) while it is still in L2. Dependencies always rank earlier:
+// #1 unit l reads conv1x1 units l−1…l+1 (keys ≤ 3(l+1−D0) < 3l+1 for D0 ≥ 1),
+// #2 unit l reads #1 units l−1…l+1 and conv1x1 unit l (D ≥ 1). D0 ≥ n1
+// reproduces "all conv1x1 tiles first".
+__global__ void __launch_bounds__(1024) k_rb_order(int32_t n_steps, const int32_t* __restrict__ step_tile_begin,
+                                                   const int32_t* __restrict__ step_bintile_begin,
+                                                   const int32_t* __restrict__ tile_group,
+                                                   const int32_t* __restrict__ group_tile0,
+                                                   const int32_t* __restrict__ group_bintile0, int32_t lookahead,
+                                                   int32_t bin_lead, int32_t* __restrict__ prefix,
+                                                   int32_t* __restrict__ order) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int32_t st = blockIdx.x; st < n_steps; st += gridDim.x) {
+    const int32_t t0 = step_tile_begin[st], b0 = step_bintile_begin[st];
+    const int32_t n1 = (step_tile_begin[st + 1] - t0) / kCluster;
+    const int32_t n0 = (step_bintile_begin[st + 1] - b0) / kCluster;
+    if (n0 + n1 == 0) continue;
+    const int32_t D = min(max(lookahead / kCluster, 2), max(n1, 1));
+    const int32_t D0 = min(max(bin_lead / kCluster, 1), max(n1, 1));
+    int32_t* pre = prefix + t0 / kCluster;  // inclusive count of binary conv units ≤ c
+    int32_t* out = order + (b0 + 2 * t0) / kCluster;
+    // 1. prefix of the binary flags over the conv units
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int32_t base = 0; base < n1; base += blockDim.x) {
+      const int32_t c = base + static_cast<int32_t>(threadIdx.x);
+      const int32_t f = c < n1 ? (group_bintile0[tile_group[t0 + c * kCluster]] >= 0 ? 1 : 0) : 0;
+      int32_t x = f;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        int32_t w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+          if (lane >= o) w += y;
+        }
+        wsum[lane] = w;
+      }
+      __syncthreads();
+      if (c < n1) pre[c] = carry_s + (warp > 0 ? wsum[warp - 1] : 0) + x;
+      __syncthreads();
+      if (threadIdx.x == blockDim.x - 1) carry_s += wsum[(blockDim.x >> 5) - 1];
+      __syncthreads();
+    }
+    // 2. every unit at its key's rank
+    auto bins_upto = [&](int32_t c) { return c < 0 ? 0 : pre[min(c, n1 - 1)]; };
+    for (int32_t l = threadIdx.x; l < n1; l += blockDim.x) {
+      const int32_t r1 = l + max(0, min(n1, l - D)) + bins_upto(l + D0);
+      out[r1] = (1 << 28) | l;
+      const int32_t r2 = min(n1, l + D + 1) + l + bins_upto(l + D + D0);
+      out[r2] = (2 << 28) | l;
+      const int32_t g = tile_group[t0 + l * kCluster];
+      if (group_bintile0[g] >= 0) {
+        const int32_t bl = (group_bintile0[g] + l * kCluster - group_tile0[g]) / kCluster;
+        const int32_t rb = max(0, min(n1, l - D0)) + max(0, min(n1, l - D0 - D)) + (pre[l] - 1);
+        out[rb] = (0 << 28) | bl;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // --------------------------------------------------------------- gather
 // Packs the operand maps that were NOT forwarded by a child's conv3x3 #2
 // epilogue — leaves (the example's input map) and children shared by
@@ -1384,6 +1474,20 @@ extern "C" int dbk_rb_zero_gaps(int32_t n_steps, const int32_t* step_group_begin
   return static_cast<int>(cudaGetLastError());
 }
 
+extern "C" int dbk_rb_order(int32_t n_steps, const int32_t* step_tile_begin, const int32_t* step_bintile_begin,
+                            const int32_t* tile_group, const int32_t* group_tile0, const int32_t* group_bintile0,
+                            int32_t num_sms, int32_t* prefix, int32_t* order, void* stream) {
+  if (n_steps <= 0) return 0;
+  const char* la = std::getenv("DYNBATCH_LOOKAHEAD");
+  const int32_t lookahead = (la ? std::atoi(la) : 1) * num_sms;  // as dbk_rb_step
+  const char* bl = std::getenv("DYNBATCH_BIN_LEAD");              // conv1x1 lead in SM-rows of tiles
+  const int32_t bin_lead = bl ? std::atoi(bl) * num_sms : num_sms;
+  k_rb_order<<<static_cast<unsigned>(std::min(n_steps, 148 * 4)), 1024, 0, static_cast<cudaStream_t>(stream)>>>(
+      n_steps, step_tile_begin, step_bintile_begin, tile_group, group_tile0, group_bintile0, lookahead,
+      bin_lead > 0 ? bin_lead : (1 << 29), prefix, order);
+  return static_cast<int>(cudaGetLastError());
+}
+
 extern "C" int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
                              const int32_t* group_begin, const int32_t* seg_start, const int32_t* member_g,
                              const int32_t* fwd_pos, const int32_t* fwd_slot, const int32_t* arity_of,
@@ -1427,7 +1531,8 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
                            const void* const* w2, const float* const* b0, const float* const* b1,
                            const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
                            int32_t* step_done, int32_t* queue, int32_t* err, int32_t* ready, const int32_t* need,
-                           const int32_t* member_g, int32_t tile_m, int32_t num_sms, void* stream) {
+                           const int32_t* member_g, const int32_t* order, int32_t tile_m, int32_t num_sms,
+                           void* stream) {
   if (tile_m != 256 && tile_m != 128 && tile_m != 64) return static_cast<int>(cudaErrorInvalidValue);
   dbk_rb_configure();
   StepParams p{};
@@ -1476,6 +1581,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
   p.ready = ready;
   p.need = need;
   p.member_g = member_g;
+  p.order = order;
   const char* sb = std::getenv("DYNBATCH_STEP_BARRIER");
   p.step_barrier = sb ? std::atoi(sb) : 0;  // default: per-image dependencies only
   // persistent: one CTA per SM, in clusters of kCluster
