@@ -122,3 +122,29 @@ def test_train_errors():
     assert s.grad("w0", 2).size == 0  # a unary function has no conv1x1
     with pytest.raises(db.DynbatchError):
         s.grad("w1", 0)  # function 0 is a leaf: no weights
+
+
+def test_train_step_is_schedule_invariant():
+    """The improved, standard and naive schedules batch the backward
+    differently (the paper's comparison) but differentiate the same
+    function: the forward is bit-identical across schedules, the gradients
+    agree up to summation order."""
+    kw = dict(batch=5, vocab=10, width=F, length=6, branch_prob=0.4, seed=9)
+    labels = np.arange(5, dtype=np.int32) % 10
+    grads = {}
+    for strategy in ("improved", "standard", "naive"):
+        s = db.IepSession(db.Batch.generate("chain", **kw), 77, db.MODULE_RESBLOCK)
+        if strategy == "standard":
+            s.set_strategy("standard")
+        elif strategy == "naive":
+            s.set_schedule(db.Batch.generate("chain", **dict(kw, width=8)).schedule("naive"))
+        s.set_head(10, 3)
+        s.set_training(True)
+        loss = s.train_step(labels)
+        grads[strategy] = (loss, s.grad("w1", 2), s.grad("head_w1"), s.grad("inputs"))
+    base = grads["improved"]
+    for strategy in ("standard", "naive"):
+        other = grads[strategy]
+        assert other[0] == base[0]  # bit-identical forward → identical loss
+        for a, b in zip(other[1:], base[1:]):
+            assert fro_err(a, b) <= 1e-5, strategy
