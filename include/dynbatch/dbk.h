@@ -142,7 +142,8 @@ int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* st
                 int64_t plane_stride, const void* const* w0, const void* const* w1, const void* const* w2,
                 const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
                 int32_t* done0, int32_t* done1, int32_t* step_done, int32_t* queue, int32_t* err,
-                int32_t* ready, const int32_t* need, const int32_t* member_g, const int32_t* order, int32_t tile_m, int32_t num_sms,
+                int32_t* ready, const int32_t* need, const int32_t* member_g, const int32_t* order, const float* values,
+                int64_t values_floats, int32_t tile_m, int32_t num_sms,
                 void* stream);
 /* Zeroes stage_x rows between each segment's last image and its tile end
  * (read as top / left pads by the next segment's first image), every
@@ -226,6 +227,8 @@ int dbk_tr_colsum(int64_t rows, int32_t cols, const float* a, float* db, void* s
 int dbk_tr_route(int32_t n, const int32_t* nodes, const int32_t* child, const int32_t* fid, const int32_t* arity_of,
                  const int32_t* example, const float* src, int32_t ch, int32_t c0, float* dy_nodes, float* d_inputs,
                  void* stream);
+/* loss holds 1 + b floats: [1 + e] = program e's cross-entropy, [0] = their
+ * mean summed in a fixed order (bit-reproducible); dlogits [b][A] */
 int dbk_tr_softmax_ce(int64_t b, int32_t A, int32_t ld, const float* logits, const int32_t* labels, float* dlogits,
                       float* loss, void* stream);
 int dbk_tr_unpack_h(int64_t rows, int32_t K, const void* h, float* out, void* stream);

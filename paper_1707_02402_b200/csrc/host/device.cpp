@@ -503,6 +503,11 @@ IepSession::IepSession(const FunctionVocab& vocab, std::span<const Program> prog
   batch_ = std::make_unique<DeviceProgramBatch>(csr, stream_);
   err_.alloc(4);
   present_.alloc(static_cast<size_t>(std::max<std::int64_t>(batch_->csr().cap_N, 1)));
+  // cudaMalloc does not clear: the error word is read (synchronize) before
+  // the first forward resets it, and a fresh allocation can hold the bytes
+  // of a session destroyed earlier in the process
+  err_.zero(stream_);
+  present_.zero(stream_);
   if (kind_ == ModuleKind::dense) {
     in64_.upload(inputs.data().data(), inputs.data().size(), stream_);
     values64_.alloc(static_cast<size_t>(std::max<std::int64_t>(batch_->csr().cap_N, 1)) * static_cast<size_t>(width_));

@@ -306,7 +306,8 @@ void IepSession::forward_resblock() {
                       R.memtab.get(), R.stage_x.get(), R.stage_lo.get(), R.stage_cat.get(), R.stage_mid.get(),
                       R.plane_stride, R.w0tab.get(), R.w1tab.get(), R.w2tab.get(), R.b0tab.get(), R.b1tab.get(),
                       R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.step_done.get(), R.queue.get(), err_.get(),
-                      R.ready.get(), R.need.get(), B.member_g.get(), R.order.get(), R.tile_m, sms, stream_),
+                      R.ready.get(), R.need.get(), B.member_g.get(), R.order.get(), R.values.get(),
+                      static_cast<std::int64_t>(R.values.size()), R.tile_m, sms, stream_),
           "conv step");
     prof_.end(stream_);
     ++launches_;

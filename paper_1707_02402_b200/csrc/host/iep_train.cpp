@@ -148,7 +148,6 @@ void IepSession::set_training(bool on) {
     t->gb2[f].alloc(kC);
     check(cudaStreamSynchronize(stream_), "training weights");  // the host vectors go out of scope
   }
-  t->loss.alloc(1);
   train_ = std::move(t);
 }
 
@@ -161,6 +160,7 @@ float IepSession::train_step(const std::int32_t* labels) {
   for (std::int64_t e = 0; e < b; ++e)
     if (labels[e] < 0 || labels[e] >= head_->answers()) throw_error(Errc::invalid_argument, "label out of range");
   T.labels.upload(labels, static_cast<size_t>(b), stream_);
+  T.loss.ensure(static_cast<size_t>(b) + 1);  // [0] mean, [1 + e] per program
   dbk_rb_set_training(1);
   try {
     forward_direct();
@@ -217,7 +217,6 @@ void IepSession::backward(float* loss_dev) {
   for (Buf<float>* v : {&T.gwp, &T.gbp, &T.ghw1, &T.ghb1, &T.ghw2, &T.ghb2}) v->zero(s);
   for (size_t f = 0; f < T.arity.size(); ++f)
     for (Buf<float>* v : {&T.gw0[f], &T.gb0[f], &T.gw1[f], &T.gb1[f], &T.gw2[f], &T.gb2[f]}) v->zero(s);
-  check(cudaMemsetAsync(loss_dev, 0, sizeof(float), s), "loss reset");
   cublasHandle_t h = T.blas;
 
   // ---- head: loss, FC2, FC1, pool, projection

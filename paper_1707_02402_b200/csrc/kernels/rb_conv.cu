@@ -212,6 +212,9 @@ struct StepParams {
   // Claim order per step (k_rb_order), units of kCluster tiles: entry
   // (kind << 28) | local unit; null = the closed form of step_unit().
   const int32_t* order;
+  // bounds of the node values (DYNBATCH_BOUNDS builds check every store)
+  const float* values;
+  int64_t values_floats;
 };
 
 // Error codes shared with the host (IepSession::check_errors): a module
@@ -616,6 +619,12 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
           *reinterpret_cast<uint4*>(P.stage_x + stage_off(P.ps, L.plane, pe.fwd_row)) = make_uint4(0, 0, 0, 0);
       } else {
         if (pe.fwd_row >= 0) {
+#ifdef DYNBATCH_BOUNDS
+          if (pe.fwd_row >= P.ps) {
+            atomicCAS(P.err, 0, 72);
+            continue;
+          }
+#endif
           uint4 hi, lo;
           split_f16x8(o, hi, lo);
           hmax = hmax4(hmax, hi);
@@ -631,6 +640,12 @@ __device__ __forceinline__ void step_epilogue(const StepParams& P, const PosEntr
           }
         }
         if (pe.dst) {
+#ifdef DYNBATCH_BOUNDS
+          if (pe.dst + L.plane_off32 < P.values || pe.dst + L.plane_off32 + 8 > P.values + P.values_floats) {
+            atomicCAS(P.err, 0, 71);
+            continue;
+          }
+#endif
 #pragma unroll
           for (int k = 0; k < 8; ++k) fmax32 = fmaxf(fmax32, o[k]);
           float4* dp = reinterpret_cast<float4*>(pe.dst + L.plane_off32);
@@ -1531,8 +1546,8 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
                            const void* const* w2, const float* const* b0, const float* const* b1,
                            const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
                            int32_t* step_done, int32_t* queue, int32_t* err, int32_t* ready, const int32_t* need,
-                           const int32_t* member_g, const int32_t* order, int32_t tile_m, int32_t num_sms,
-                           void* stream) {
+                           const int32_t* member_g, const int32_t* order, const float* values,
+                           int64_t values_floats, int32_t tile_m, int32_t num_sms, void* stream) {
   if (tile_m != 256 && tile_m != 128 && tile_m != 64) return static_cast<int>(cudaErrorInvalidValue);
   dbk_rb_configure();
   StepParams p{};
@@ -1582,6 +1597,8 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
   p.need = need;
   p.member_g = member_g;
   p.order = order;
+  p.values = values;
+  p.values_floats = values_floats;
   const char* sb = std::getenv("DYNBATCH_STEP_BARRIER");
   p.step_barrier = sb ? std::atoi(sb) : 0;  // default: per-image dependencies only
   // persistent: one CTA per SM, in clusters of kCluster

@@ -217,9 +217,10 @@ __global__ void k_route(int32_t n, const int32_t* __restrict__ nodes, const int3
 }
 
 // ---------------------------------------------------------------- head
-// Mean softmax cross-entropy over b rows of `ld`-strided logits (A valid
-// columns): loss += Σ / b (one warp per row), dlogits [b][A] = (softmax −
-// onehot) / b.
+// Softmax cross-entropy of b rows of `ld`-strided logits (A valid columns),
+// one warp per row: loss[1 + e] = row loss, dlogits [b][A] = (softmax −
+// onehot) / b. k_mean_loss then sums the rows in a fixed order into loss[0]
+// (no atomics: the loss is bit-reproducible run to run and across schedules).
 __global__ void k_softmax_ce(int64_t b, int32_t A, int32_t ld, const float* __restrict__ logits,
                              const int32_t* __restrict__ labels, float* __restrict__ dlogits, float* __restrict__ loss) {
   const int lane = threadIdx.x & 31;
@@ -235,8 +236,24 @@ __global__ void k_softmax_ce(int64_t b, int32_t A, int32_t ld, const float* __re
     const int32_t y = labels[e];
     for (int a = lane; a < A; a += 32)
       dlogits[e * A + a] = (__expf(z[a] - m) / s - (a == y ? 1.f : 0.f)) / static_cast<float>(b);
-    if (lane == 0) atomicAdd(loss, (logf(s) + m - z[y]) / static_cast<float>(b));
+    if (lane == 0) loss[1 + e] = logf(s) + m - z[y];
   }
+}
+
+// loss[0] = Σ_e loss[1 + e] / b: one block, contiguous per-thread chunks,
+// then a fixed tree.
+__global__ void __launch_bounds__(256) k_mean_loss(int64_t b, float* __restrict__ loss) {
+  __shared__ float part[256];
+  const int64_t per = (b + 255) / 256, lo = threadIdx.x * per, hi = min(b, lo + per);
+  float s = 0.f;
+  for (int64_t e = lo; e < hi; ++e) s += loss[1 + e];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w; w >>= 1) {
+    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss[0] = part[0] / static_cast<float>(b);
 }
 
 // Tiled SWIZZLE_NONE 16-bit operand ([row block][K/64][8][128][8], the grouped
@@ -402,6 +419,7 @@ extern "C" int dbk_tr_softmax_ce(int64_t b, int32_t A, int32_t ld, const float* 
   if (b <= 0) return 0;
   k_softmax_ce<<<grid_for(b * 32), 256, 0, static_cast<cudaStream_t>(stream)>>>(b, A, ld, logits, labels, dlogits,
                                                                                loss);
+  k_mean_loss<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(b, loss);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -12,7 +12,9 @@
   operand range of the conv kernels (|x| > 65504), which the reference
   would carry in fp64;
 * a host schedule set after a pipelined set_programs describes the new
-  programs and is kept.
+  programs and is kept;
+* a session created where a destroyed one lived reports no stale error
+  (its error word is cleared at creation, not first at the forward).
 """
 import numpy as np
 import pytest
@@ -85,3 +87,22 @@ def test_schedule_after_pipelined_set_programs_is_kept():
     assert s.schedule().to_json() == b2.schedule("naive").to_json()
     want = b2.execute_device(9, db.MODULE_RESBLOCK).outputs()
     assert np.array_equal(out.astype(np.float64), want)
+
+
+def test_new_session_after_destroyed_session_has_no_stale_error():
+    """time() synchronizes (and reads the error word) before its first
+    forward; the word was once left as cudaMalloc returned it, so a session
+    allocated over a freed one's bias vector raised 'device executor error
+    <bias bits>' (profiles/stale_error_check.py '00')."""
+    b = db.Batch.generate("chain", batch=64, vocab=40, width=F, length=16, branch_prob=0.1, seed=0)
+    sched = db.Batch.generate("chain", batch=64, vocab=40, width=8, length=16, branch_prob=0.1, seed=0).schedule("naive")
+    ref = db.IepSession(b, 1234, db.MODULE_RESBLOCK)
+    ref.forward()
+    want = ref.run().outputs()
+    for _ in range(3):
+        x = db.IepSession(b, 1234, db.MODULE_RESBLOCK, first=0, last=64)
+        x.set_schedule(sched)
+        x.time(1)
+        x.time(2)
+        assert np.array_equal(x.run().outputs(), want)
+        del x
