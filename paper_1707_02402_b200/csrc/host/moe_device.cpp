@@ -36,6 +36,9 @@ struct MoeDev {
     seg_hist.alloc(static_cast<size_t>(dbk_bucket_sort_scratch(static_cast<std::int64_t>(items), n)));
     tiles.alloc(static_cast<size_t>(n) + 1);
     err.alloc(4);
+    // read by check_err (synchronize) before the first gate resets it: a
+    // fresh allocation can hold a freed buffer's bytes
+    check(cudaMemset(err.get(), 0, 16), "memset");
   }
   void alloc_fp64_work() {
     const size_t items = static_cast<size_t>(T) * static_cast<size_t>(k);
