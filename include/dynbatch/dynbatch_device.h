@@ -142,8 +142,12 @@ DYNBATCH_API db_status db_iep_session_run(db_iep_session* s, db_run** out);
 /* Device level labels of the last forward (total_nodes int32, CSR order). */
 DYNBATCH_API db_status db_iep_session_labels(db_iep_session* s, int32_t* labels, int64_t n);
 /* Runs `iters` forwards between two CUDA events on the session stream and
- * returns the elapsed device milliseconds; with profile != 0 also fills
- * per-kernel-class times (events around every launch). */
+ * returns the elapsed device milliseconds. profile 1 also fills per-kernel-
+ * class times (direct launches, events around every launch); profile 2 runs
+ * the forwards as unprofiled ones do (CUDA-graph replays) with event-record
+ * nodes around the fused step kernel and fills class 4 (conv step) with that
+ * kernel's own time inside the same loop (RESBLOCK sessions whose forward is
+ * one step launch; launches[4] = 0 otherwise). */
 DYNBATCH_API db_status db_iep_session_time(db_iep_session* s, int32_t iters, int32_t profile,
                                            double* ms, db_kernel_times_t* kt);
 /* IEP classifier head on the root maps (RESBLOCK sessions; SURVEY.md §8(f)4,

@@ -437,13 +437,14 @@ class IepSession(_Handle):
                                           C.byref(h)))
         super().__init__(h)
 
-    def time(self, iters: int, profile: bool = False):
+    def time(self, iters: int, profile=False):
         """Device ms of `iters` forwards (CUDA events on the session stream)
-        and, with profile, per-kernel-class times."""
+        and, with profile, per-kernel-class times: True / 1 = events around
+        every launch (direct launches); 2 = the unprofiled forwards (graph
+        replays) with events around the fused step kernel only (class 4)."""
         ms = C.c_double()
         kt = KernelTimes()
-        check(getattr(lib(), self._time)(self.h, iters, 1 if profile else 0, C.byref(ms),
-                                         C.byref(kt)))
+        check(getattr(lib(), self._time)(self.h, iters, int(profile), C.byref(ms), C.byref(kt)))
         return ms.value, kt
 
     def set_schedule(self, schedule):

@@ -423,7 +423,7 @@ db_status db_iep_session_time(db_iep_session* s, int32_t iters, int32_t profile,
   if (!s || !ms) return null_arg();
   return guarded([&] {
     dynbatch::dev::KernelTimes k;
-    *ms = s->s->time_forwards(iters, profile != 0, &k);
+    *ms = s->s->time_forwards(iters, profile, &k);
     if (kt) copy_times(k, kt);
   });
 }

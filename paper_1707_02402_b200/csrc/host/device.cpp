@@ -581,31 +581,68 @@ void IepSession::forward_graph() {
   const HostCSR& c = batch_->csr();
   const GraphKey key{c.b, c.N, rb_ ? rb_->n_shared : 0, c.s_max, static_cast<int>(strategy_),
                      host_schedule_ ? 1 : 0, rb_ ? rb_->tile_m : 0, batch_->static_shape() ? 1 : 0,
-                     dbk_rb_debug_enabled(), schedule_gen_};
+                     dbk_rb_debug_enabled(), kevents_ ? 1 : 0, schedule_gen_};
   ++graph_clock_;
+  // a kept graph with step-kernel event nodes records this forward's events
+  const auto launch = [this](CachedGraph& g) {
+    kev_recorded_ = g.kb != nullptr;
+    if (g.kb) {
+      check(cudaGraphExecEventRecordNodeSetEvent(g.exec, g.kb, kev_cur_[0]), "event node");
+      check(cudaGraphExecEventRecordNodeSetEvent(g.exec, g.ke, kev_cur_[1]), "event node");
+    }
+    check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+  };
   for (CachedGraph& g : graphs_) {
     if (!(g.key == key)) continue;
     batch_->set_sched_state(g.sched);
     launches_ = g.launches;
     g.used = graph_clock_;
-    check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+    launch(g);
     return;
   }
   // capture this forward (its host bookkeeping runs once, here) and keep it
   cudaGraph_t graph = nullptr;
+  cudaEvent_t cur[2] = {kev_cur_[0], kev_cur_[1]};
+  if (kevents_) {
+    for (cudaEvent_t& m : kev_mark_)
+      if (!m) check(cudaEventCreate(&m), "event");
+    kev_cur_[0] = kev_mark_[0];
+    kev_cur_[1] = kev_mark_[1];
+  }
   check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
   try {
     forward_direct();
   } catch (...) {
     cudaStreamEndCapture(stream_, &graph);
     if (graph) cudaGraphDestroy(graph);
+    kev_cur_[0] = cur[0];
+    kev_cur_[1] = cur[1];
     throw;
   }
+  kev_cur_[0] = cur[0];
+  kev_cur_[1] = cur[1];
   check(cudaStreamEndCapture(stream_, &graph), "end capture");
   CachedGraph g;
   g.key = key;
   const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
-  cudaGraphDestroy(graph);
+  if (e == cudaSuccess && kevents_ && kev_recorded_) {
+    size_t n = 0;
+    check(cudaGraphGetNodes(graph, nullptr, &n), "graph nodes");
+    std::vector<cudaGraphNode_t> nodes(n);
+    check(cudaGraphGetNodes(graph, nodes.data(), &n), "graph nodes");
+    for (cudaGraphNode_t node : nodes) {
+      cudaGraphNodeType t;
+      check(cudaGraphNodeGetType(node, &t), "node type");
+      if (t != cudaGraphNodeTypeEventRecord) continue;
+      cudaEvent_t ev = nullptr;
+      check(cudaGraphEventRecordNodeGetEvent(node, &ev), "event node");
+      if (ev == kev_mark_[0]) g.kb = node;
+      if (ev == kev_mark_[1]) g.ke = node;
+    }
+    if (g.kb && g.ke) g.graph = graph;
+    else g.kb = g.ke = nullptr;
+  }
+  if (!g.graph) cudaGraphDestroy(graph);
   check(e, "graph instantiate");
   g.sched = batch_->sched_state();
   g.launches = launches_;
@@ -614,11 +651,18 @@ void IepSession::forward_graph() {
   if (graphs_.size() >= kMaxGraphs) {
     auto lru = std::min_element(graphs_.begin(), graphs_.end(),
                                 [](const CachedGraph& a, const CachedGraph& b) { return a.used < b.used; });
-    cudaGraphExecDestroy(lru->exec);
+    release_graph(*lru);
     graphs_.erase(lru);
   }
   graphs_.push_back(g);
-  check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+  launch(graphs_.back());
+}
+
+void IepSession::release_graph(CachedGraph& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (g.graph) cudaGraphDestroy(g.graph);
+  g.exec = nullptr;
+  g.graph = nullptr;
 }
 
 void IepSession::forward_direct() {
@@ -683,15 +727,40 @@ void IepSession::add_forward_work() {
   prof_.add_work(4, conv_flops, conv_bytes);
 }
 
-double IepSession::time_forwards(int iters, bool profile, KernelTimes* kt) {
+double IepSession::time_forwards(int iters, int profile, KernelTimes* kt) {
   synchronize();
-  prof_.on = profile;
+  prof_.on = profile == 1;
   prof_.reset();
+  const bool kev = profile == 2 && kind_ == ModuleKind::resblock;
+  if (kev)
+    while (kev_pool_.size() < 2 * static_cast<size_t>(std::max(iters, 0))) {
+      cudaEvent_t e;
+      check(cudaEventCreate(&e), "event");
+      kev_pool_.push_back(e);
+    }
+  kevents_ = kev;
+  std::vector<char> recorded(static_cast<size_t>(std::max(iters, 0)), 0);
   cudaEvent_t a, b;
   check(cudaEventCreate(&a), "event");
   check(cudaEventCreate(&b), "event");
   check(cudaEventRecord(a, stream_), "event");
-  for (int i = 0; i < iters; ++i) forward();
+  try {
+    for (int i = 0; i < iters; ++i) {
+      if (kev) {
+        kev_cur_[0] = kev_pool_[2 * static_cast<size_t>(i)];
+        kev_cur_[1] = kev_pool_[2 * static_cast<size_t>(i) + 1];
+        kev_recorded_ = false;
+      }
+      forward();
+      if (kev) recorded[static_cast<size_t>(i)] = kev_recorded_ ? 1 : 0;
+    }
+  } catch (...) {
+    kevents_ = false;
+    kev_cur_[0] = kev_cur_[1] = nullptr;
+    throw;
+  }
+  kevents_ = false;
+  kev_cur_[0] = kev_cur_[1] = nullptr;
   check(cudaEventRecord(b, stream_), "event");
   check(cudaEventSynchronize(b), "event sync");
   float ms = 0.f;
@@ -699,7 +768,32 @@ double IepSession::time_forwards(int iters, bool profile, KernelTimes* kt) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   check_errors();
-  if (profile && kt) *kt = prof_.collect();
+  if (profile == 1 && kt) *kt = prof_.collect();
+  if (kev && kt) {
+    // the step kernel's events of every forward that recorded them, and the
+    // algorithmic work of those forwards (same accounting as profile 1)
+    prof_.reset();
+    KernelTimes w;
+    std::int64_t n = 0;
+    double step_ms = 0.0;
+    for (int i = 0; i < iters; ++i) {
+      if (!recorded[static_cast<size_t>(i)]) continue;
+      float t = 0.f;
+      check(cudaEventElapsedTime(&t, kev_pool_[2 * static_cast<size_t>(i)], kev_pool_[2 * static_cast<size_t>(i) + 1]),
+            "elapsed");
+      step_ms += t;
+      ++n;
+    }
+    if (n > 0) {
+      add_forward_work();
+      w = prof_.collect();
+    }
+    *kt = KernelTimes{};
+    kt->ms[4] = step_ms;
+    kt->launches[4] = n;
+    kt->flops[4] = w.flops[4] * static_cast<double>(n);
+    kt->bytes[4] = w.bytes[4] * static_cast<double>(n);
+  }
   prof_.on = false;
   return ms;
 }

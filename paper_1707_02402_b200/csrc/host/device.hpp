@@ -252,7 +252,11 @@ class IepSession {
   ModuleKind kind() const { return kind_; }
   std::int64_t h2d_bytes() const;
   std::int64_t d2h_bytes() const;
-  double time_forwards(int iters, bool profile, KernelTimes* kt);
+  // profile 0: elapsed only; 1: events around every launch (direct
+  // launches, per-class times); 2: the forwards as they run unprofiled
+  // (graph replays) with event-record nodes around the fused step kernel, so
+  // class 4 holds that kernel's own time inside the same loop.
+  double time_forwards(int iters, int profile, KernelTimes* kt);
   // IEP classifier head on the root maps (iep_head.hpp; resblock sessions).
   void set_head(int answers, std::uint64_t seed);
   void head_forward();                                   // logits of the current roots
@@ -289,19 +293,28 @@ class IepSession {
   // launch instead of ~20 dependent ones.
   struct GraphKey {
     std::int64_t b, N, n_shared;
-    int s_max, strategy, host_schedule, tile_m, static_shape, debug;
+    int s_max, strategy, host_schedule, tile_m, static_shape, debug, kevents;
     std::uint64_t gen;
     bool operator==(const GraphKey&) const = default;
   };
   struct CachedGraph {
     GraphKey key;
     cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;                 // kept when kb / ke are set
+    cudaGraphNode_t kb = nullptr, ke = nullptr;  // event records around the step kernel
     DeviceProgramBatch::SchedState sched;
     std::int64_t launches = 0;
     std::uint64_t used = 0;
   };
   std::vector<CachedGraph> graphs_;
   std::uint64_t graph_clock_ = 0, schedule_gen_ = 0;
+  // time_forwards(profile 2): events recorded around the one-launch step
+  // kernel of each forward (kev_cur_, set per forward; placeholders kev_mark_
+  // while a graph is captured, then the exec's nodes are pointed at kev_cur_)
+  bool kevents_ = false, kev_recorded_ = false;
+  cudaEvent_t kev_cur_[2] = {nullptr, nullptr}, kev_mark_[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> kev_pool_;
+  void release_graph(CachedGraph& g);
   bool graphs_enabled() const;
   void forward_graph();
   void programs_built();                       // session state that follows a device prefix build

@@ -19,8 +19,10 @@ IepSession::~IepSession() {
     cudaStreamSynchronize(stream_);
     cudaStreamDestroy(stream_);
   }
-  for (CachedGraph& g : graphs_)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (CachedGraph& g : graphs_) release_graph(g);
+  for (cudaEvent_t e : kev_pool_) cudaEventDestroy(e);
+  for (cudaEvent_t e : kev_mark_)
+    if (e) cudaEventDestroy(e);
 }
 
 namespace {
@@ -300,6 +302,10 @@ void IepSession::forward_resblock() {
     }
     // conv1x1 + conv3x3 #1 + conv3x3 #2 (+ residual) of the step(s), one launch
     prof_.begin(4, stream_);
+    if (kevents_ && one_launch) {  // time_forwards(profile 2): the kernel's own events
+      check(cudaEventRecordWithFlags(kev_cur_[0], stream_, cudaEventRecordExternal), "event");
+      kev_recorded_ = true;
+    }
     check(dbk_rb_step(s, one_launch ? S : s + 1, R.epoch, R.step_tile_begin.get(), R.tile_group.get(), R.tile_q0.get(),
                       R.step_bintile_begin.get(), R.bin_group.get(), R.bin_q0.get(), B.group_fid.get(),
                       B.group_begin.get(), R.seg_start.get(), R.group_tile0.get(), R.group_bintile0.get(),
@@ -309,6 +315,7 @@ void IepSession::forward_resblock() {
                       R.ready.get(), R.need.get(), B.member_g.get(), R.order.get(), R.values.get(),
                       static_cast<std::int64_t>(R.values.size()), R.tile_m, sms, stream_),
           "conv step");
+    if (kevents_ && one_launch) check(cudaEventRecordWithFlags(kev_cur_[1], stream_, cudaEventRecordExternal), "event");
     prof_.end(stream_);
     ++launches_;
   }
