@@ -197,21 +197,29 @@ __global__ void k_route(int32_t n, const int32_t* __restrict__ nodes, const int3
                         const int32_t* __restrict__ fid, const int32_t* __restrict__ arity_of,
                         const int32_t* __restrict__ example, const float* __restrict__ src, int32_t ch, int32_t c0,
                         float* __restrict__ dy_nodes, float* __restrict__ d_inputs) {
-  const int64_t total = static_cast<int64_t>(n) * kImg * kC;
+  // one thread per (member, position, 4 channels): a 16-byte load and one
+  // vector atomic into the child's dY PI (channels contiguous); a leaf's
+  // CHW input gradient takes four scalar atomics
+  constexpr int kQ = kC / 4;
+  const int64_t total = static_cast<int64_t>(n) * kImg * kQ;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(i % kC);
-    const int64_t kp = i / kC;
+    const int c = static_cast<int>(i % kQ) * 4;
+    const int64_t kp = i / kQ;
     const int32_t k = static_cast<int32_t>(kp / kImg);
     const int p = static_cast<int>(kp % kImg);
     if (is_pad(p)) continue;
-    const float v = src[(static_cast<int64_t>(k) * kPI + kPIG + p) * ch + c0 + c];
-    if (v == 0.f) continue;
+    const float4 v = *reinterpret_cast<const float4*>(src + (static_cast<int64_t>(k) * kPI + kPIG + p) * ch + c0 + c);
+    if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
     const int32_t cn = child[nodes[k]];
     if (arity_of[fid[cn]] == 0) {
-      atomicAdd(d_inputs + static_cast<int64_t>(example[cn]) * (kC * kPx) + c * kPx + px_of(p), v);
+      float* d = d_inputs + static_cast<int64_t>(example[cn]) * (kC * kPx) + c * kPx + px_of(p);
+      atomicAdd(d, v.x);
+      atomicAdd(d + kPx, v.y);
+      atomicAdd(d + 2 * kPx, v.z);
+      atomicAdd(d + 3 * kPx, v.w);
     } else {
-      atomicAdd(dy_nodes + (static_cast<int64_t>(cn) * kPI + kPIG + p) * kC + c, v);
+      atomicAdd(reinterpret_cast<float4*>(dy_nodes + (static_cast<int64_t>(cn) * kPI + kPIG + p) * kC + c), v);
     }
   }
 }
@@ -409,7 +417,7 @@ extern "C" int dbk_tr_route(int32_t n, const int32_t* nodes, const int32_t* chil
                             int32_t c0, float* dy_nodes, float* d_inputs, void* stream) {
   const int64_t total = static_cast<int64_t>(n) * kImg * kC;
   if (total <= 0) return 0;
-  k_route<<<grid_for(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, nodes, child, fid, arity_of, example,
+  k_route<<<grid_for(total / 4), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, nodes, child, fid, arity_of, example,
                                                                          src, ch, c0, dy_nodes, d_inputs);
   return static_cast<int>(cudaGetLastError());
 }
