@@ -100,7 +100,10 @@ int dbk_dense_gather_roots(int64_t b, int32_t width, const int32_t* root_g,
  * zero-padded 15×15 position grid (rb_conv.cu header). */
 
 /* Per step: segment starts (seg_start[g], -1 for leaf groups), tile lists
- * (all expensive groups; binary groups only) and their per-step offsets. */
+ * (all expensive groups; binary groups only) and their per-step offsets.
+ * training != 0 (here and in dbk_rb_step): a training forward — every
+ * expensive node also keeps its fp32 value and the mid / block-input images
+ * stay in place, since the backward reads them. */
 int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t* group_fid,
                 const int32_t* group_begin, const int32_t* arity_of, int32_t* seg_start,
                 int32_t* group_tile0, int32_t* group_bintile0, int32_t* step_tile_begin,
@@ -108,7 +111,7 @@ int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, const int32_t*
                 int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, int64_t n_nodes,
                 const int32_t* member_g, const int32_t* child0, const int32_t* child1,
                 const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t* fwd_parent,
-                int32_t* need, int32_t tile_m, void* stream);
+                int32_t* need, int32_t tile_m, int32_t training, void* stream);
 /* Gather of operands no child epilogue forwards, from the task lists that
  * dbk_rb_memtab emits (32-byte tasks, list 0 = leaves of every step, list 1
  * = children shared by several parents, processed for `step` only): fp32
@@ -143,7 +146,7 @@ int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const int32_t* st
                 const float* const* b0, const float* const* b1, const float* const* b2, const void* ident,
                 int32_t* done0, int32_t* done1, int32_t* step_done, int32_t* queue, int32_t* err,
                 int32_t* ready, const int32_t* need, const int32_t* member_g, const int32_t* order, const float* values,
-                int64_t values_floats, int32_t tile_m, int32_t num_sms,
+                int64_t values_floats, int32_t tile_m, int32_t num_sms, int32_t training,
                 void* stream);
 /* Zeroes stage_x rows between each segment's last image and its tile end
  * (read as top / left pads by the next segment's first image), every
@@ -212,7 +215,6 @@ int dbk_moe_tc_gemm(int32_t fmt, int32_t epi, int32_t n, int32_t K, int32_t N, c
 /* Training (train.cu). PI = per-member padded image:
  * 257 rows (16 zero guard rows, the 225 packed positions, 16 guard rows) ×
  * channels, fp32. */
-int dbk_rb_set_training(int32_t on); /* forwards keep every node's fp32 value and the mid images */
 int dbk_tr_stage_to_pi(int32_t n, const int64_t* rows, const void* hi, const void* lo, int64_t ps, int32_t plane0,
                        int32_t planes, float* out, void* stream);
 /* bias gradients of 128 channels: slab i = rows [slab_row[2i], slab_row[2i+1]) into dst[i] */

@@ -340,6 +340,7 @@ class IepSession {
   std::unique_ptr<RB> rb_;
   std::unique_ptr<IepHead> head_;
   std::unique_ptr<Train> train_;
+  bool train_fwd_ = false;  // the forward in flight is a training step's (dbk_rb_plan / dbk_rb_step training)
   std::uint64_t module_seed_ = 0;
   void backward(float* loss_dev);
   void require_head() const;

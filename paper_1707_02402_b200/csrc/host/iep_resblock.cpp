@@ -254,7 +254,7 @@ void IepSession::forward_resblock() {
                     R.step_bintile_begin.get(), R.step_positions.get(), R.tile_group.get(), R.tile_q0.get(),
                     R.bin_group.get(), R.bin_q0.get(), B.csr().N, B.member_g.get(), B.child0.get(),
                     B.child1.get(), R.fwd_ok.get(), R.fwd_pos.get(), R.fwd_slot.get(), R.fwd_parent.get(),
-                    R.need.get(), R.tile_m, stream_),
+                    R.need.get(), R.tile_m, train_fwd_ ? 1 : 0, stream_),
         "dbk_rb_plan");
   check(dbk_rb_memtab(S, B.step_group_begin.get(), B.group_fid.get(), B.group_begin.get(), R.seg_start.get(),
                       B.member_g.get(), R.fwd_pos.get(), R.fwd_slot.get(), B.arity_of.get(), B.fid.get(),
@@ -313,7 +313,7 @@ void IepSession::forward_resblock() {
                       R.plane_stride, R.w0tab.get(), R.w1tab.get(), R.w2tab.get(), R.b0tab.get(), R.b1tab.get(),
                       R.b2tab.get(), R.ident.get(), R.done0.get(), R.done1.get(), R.step_done.get(), R.queue.get(), err_.get(),
                       R.ready.get(), R.need.get(), B.member_g.get(), R.order.get(), R.values.get(),
-                      static_cast<std::int64_t>(R.values.size()), R.tile_m, sms, stream_),
+                      static_cast<std::int64_t>(R.values.size()), R.tile_m, sms, train_fwd_ ? 1 : 0, stream_),
           "conv step");
     if (kevents_ && one_launch) check(cudaEventRecordWithFlags(kev_cur_[1], stream_, cudaEventRecordExternal), "event");
     prof_.end(stream_);

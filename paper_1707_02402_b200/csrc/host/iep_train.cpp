@@ -161,14 +161,14 @@ float IepSession::train_step(const std::int32_t* labels) {
     if (labels[e] < 0 || labels[e] >= head_->answers()) throw_error(Errc::invalid_argument, "label out of range");
   T.labels.upload(labels, static_cast<size_t>(b), stream_);
   T.loss.ensure(static_cast<size_t>(b) + 1);  // [0] mean, [1 + e] per program
-  dbk_rb_set_training(1);
+  train_fwd_ = true;
   try {
     forward_direct();
   } catch (...) {
-    dbk_rb_set_training(0);
+    train_fwd_ = false;
     throw;
   }
-  dbk_rb_set_training(0);
+  train_fwd_ = false;
   check_errors();
   head_forward();
   backward(T.loss.get());

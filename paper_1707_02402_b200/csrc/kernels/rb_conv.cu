@@ -1444,10 +1444,6 @@ __global__ void __launch_bounds__(256) k_roots_to_chw(const int32_t* __restrict_
 }
 
 int32_t g_debug_flag = 0;
-// Training forwards (dbk_rb_set_training): every expensive node also keeps
-// its fp32 value (the backward's ReLU masks) and the mid images stay in
-// place (no discard), since the backward reads them.
-int32_t g_train_mode = 0;
 
 }  // namespace
 
@@ -1458,7 +1454,7 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
                            int32_t* tile_q0, int32_t* bin_group, int32_t* bin_q0, int64_t n_nodes,
                            const int32_t* member_g, const int32_t* child0, const int32_t* child1,
                            const int32_t* fwd_ok, int32_t* fwd_pos, int32_t* fwd_slot, int32_t* fwd_parent,
-                           int32_t* need, int32_t tile_m, void* stream) {
+                           int32_t* need, int32_t tile_m, int32_t training, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n_steps <= 0) return 0;
   k_rb_plan<<<1, 1024, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
@@ -1467,7 +1463,7 @@ extern "C" int dbk_rb_plan(int32_t n_steps, const int32_t* step_group_begin, con
   k_rb_fwd_init<<<static_cast<unsigned>((n_nodes + 255) / 256), 256, 0, s>>>(n_nodes, fwd_pos, fwd_slot,
                                                                               fwd_parent, need);
   k_rb_fwd<<<148 * 4, 256, 0, s>>>(n_steps, step_group_begin, group_fid, group_begin, arity_of, seg_start,
-                                   member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot, fwd_parent, g_train_mode);
+                                   member_g, child0, child1, fwd_ok, fwd_pos, fwd_slot, fwd_parent, training ? 1 : 0);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -1547,7 +1543,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
                            const float* const* b2, const void* ident, int32_t* done0, int32_t* done1,
                            int32_t* step_done, int32_t* queue, int32_t* err, int32_t* ready, const int32_t* need,
                            const int32_t* member_g, const int32_t* order, const float* values,
-                           int64_t values_floats, int32_t tile_m, int32_t num_sms, void* stream) {
+                           int64_t values_floats, int32_t tile_m, int32_t num_sms, int32_t training, void* stream) {
   if (tile_m != 256 && tile_m != 128 && tile_m != 64) return static_cast<int>(cudaErrorInvalidValue);
   dbk_rb_configure();
   StepParams p{};
@@ -1563,7 +1559,7 @@ extern "C" int dbk_rb_step(int32_t step, int32_t step_end, int32_t epoch, const 
   p.diag = dg ? std::atoi(dg) : 0;
   const char* ch = std::getenv("DYNBATCH_CACHE");
   p.cache = ch ? std::atoi(ch) : 4;  // default: drop consumed interior mid lines from L2
-  if (g_train_mode) p.cache &= ~12;  // the backward reads mid and the block inputs
+  if (training) p.cache &= ~12;  // the backward reads mid and the block inputs
   p.step_tile_begin = step_tile_begin;
   p.tile_group = tile_group;
   p.tile_q0 = tile_q0;
@@ -1640,11 +1636,6 @@ extern "C" int dbk_rb_outputs_to_chw(int64_t b, const int32_t* root_g, const int
   k_roots_to_chw<<<static_cast<unsigned>(b * kPlanes), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       root_g, fid, arity_of, example, inputs, values, chw);
   return static_cast<int>(cudaGetLastError());
-}
-
-extern "C" int dbk_rb_set_training(int32_t on) {
-  g_train_mode = on ? 1 : 0;
-  return 0;
 }
 
 // Copies (and optionally zeroes) the MMA-thread wait counters; enable != 0
