@@ -24,6 +24,7 @@
 // Weights are pre-tiled SWIZZLE_NONE per (N tile, K chunk): [8][256 n][8].
 // Padding rows of A and H are never initialised: their GEMM rows are never
 // read (the combine reads valid rows only; the EP GEMM2 skips them).
+#include <atomic>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -392,10 +393,13 @@ __global__ void k_moe_combine_f32(int64_t T, int32_t k, int32_t d, const double*
 
 template <int EPI, bool F16>
 int launch_gemm(const GemmParams& p, int sms, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};  // per device (the attribute is), once, from any thread
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
     cudaFuncSetAttribute(k_moe_gemm<EPI, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    configured = true;
+    configured.fetch_or(bit, std::memory_order_release);
   }
   k_moe_gemm<EPI, F16><<<sms / 2 * 2, kThreads, kSmem, s>>>(p);  // CTA pairs
   return static_cast<int>(cudaGetLastError());

@@ -57,6 +57,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
 #include <cstdlib>
 
 #include "dynbatch/dbk.h"
@@ -1519,15 +1520,19 @@ extern "C" int dbk_rb_memtab(int32_t n_steps, const int32_t* step_group_begin, c
 // Kernel attributes (shared-memory carve-out), set once per process, and
 // before any stream capture of a forward.
 extern "C" int dbk_rb_configure(void) {
-  static bool configured = false;
-  if (!configured) {
+  // per device (the attribute is), once, from any thread
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
     cudaFuncSetAttribute(k_rb_step<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     cudaFuncSetAttribute(k_rb_step<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     cudaFuncSetAttribute(k_rb_step<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     cudaFuncSetAttribute(k_rb_step<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     cudaFuncSetAttribute(k_rb_step<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
     cudaFuncSetAttribute(k_rb_step<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
-    configured = true;
+    configured.fetch_or(bit, std::memory_order_release);
   }
   return static_cast<int>(cudaGetLastError());
 }
