@@ -148,3 +148,12 @@ def test_train_step_is_schedule_invariant():
         assert other[0] == base[0]  # bit-identical forward → identical loss
         for a, b in zip(other[1:], base[1:]):
             assert fro_err(a, b) <= 1e-5, strategy
+
+
+def test_train_step_at_cfg1_size():
+    """The training step on BASELINE's cfg1 minibatch (64 chain programs of
+    up to 16 nodes, p = 40, branch_prob 0.1: 14 steps, 232 expensive calls)
+    against torch fp64 autograd, same bars as the deeper programs above."""
+    s, loss, ref_loss, mod, head, dx = _run("chain", 64, 40, 4, 16, 0.1, 0, answers=28)
+    worst = _check_all(s, loss, ref_loss, mod, head, dx)
+    assert worst <= TOL_FRO
