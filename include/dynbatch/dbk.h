@@ -233,6 +233,17 @@ int dbk_tr_route(int32_t n, const int32_t* nodes, const int32_t* child, const in
  * mean summed in a fixed order (bit-reproducible); dlogits [b][A] */
 int dbk_tr_softmax_ce(int64_t b, int32_t A, int32_t ld, const float* logits, const int32_t* labels, float* dlogits,
                       float* loss, void* stream);
+/* Data gradient of a 3×3 conv as a tf32 implicit GEMM (bwd_conv.cu): packed
+ * dA (dbk_tr_pack_sw128f: PI rows → 32-channel SW128 chunk rows, `lead` zero
+ * rows first), tiles of 256 PI rows within one group (tile_row0 a multiple of
+ * 8; rows [tile_lo, tile_hi) written), transposed tap weights per function
+ * (dbk_tr_pack_dgrad_weights: 9 × 4 blocks of 16 KB); out = D ⊙ (mask > 0)
+ * and / or + resid at real positions, 0 at pads and guard rows. */
+int dbk_tr_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead, const float* pi, void* out, void* stream);
+int dbk_tr_pack_dgrad_weights(const float* w, void* out, void* stream);
+int dbk_tr_dgrad(const void* packed, int64_t rows_alloc, int32_t lead, int32_t n_tiles, const int32_t* tile_row0,
+                 const int32_t* tile_lo, const int32_t* tile_hi, const int32_t* tile_fn, const void* const* wpack,
+                 const float* mask, const float* resid, float* out, int32_t sms, void* stream);
 int dbk_tr_unpack_h(int64_t rows, int32_t K, const void* h, float* out, void* stream);
 int dbk_tr_unpack_sw128(int64_t rows, int32_t K, const void* a, float* out, void* stream);
 int dbk_tr_pool_bwd(int64_t b, int32_t P, const float* proj, const float* dpooled, float* dproj, void* stream);

@@ -45,6 +45,16 @@ void cublas_check(cublasStatus_t st, const char* what) {
 
 // TF32 tensor cores (default) or full fp32 (DYNBATCH_TRAIN_FP32=1, A/B of the
 // backward's rounding).
+// Data gradients of the 3×3 convs: the tf32 implicit GEMM (bwd_conv.cu,
+// default) or cuBLAS on the im2col layout + col2im (DYNBATCH_TRAIN_DGRAD=0).
+bool implicit_dgrad() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYNBATCH_TRAIN_DGRAD");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 cublasComputeType_t compute_type() {
   static const cublasComputeType_t t = [] {
     const char* e = std::getenv("DYNBATCH_TRAIN_FP32");
@@ -148,6 +158,23 @@ void IepSession::set_training(bool on) {
     t->gb2[f].alloc(kC);
     check(cudaStreamSynchronize(stream_), "training weights");  // the host vectors go out of scope
   }
+  // transposed tap blocks for the implicit-GEMM data gradients
+  t->wd1.resize(p);
+  t->wd2.resize(p);
+  std::vector<const void*> tab1(p, nullptr), tab2(p, nullptr);
+  for (size_t f = 0; f < p; ++f) {
+    if (t->arity[f] == 0) continue;
+    constexpr size_t kBytes = 9 * 4 * 16384;
+    t->wd1[f].alloc(kBytes);
+    t->wd2[f].alloc(kBytes);
+    check(dbk_tr_pack_dgrad_weights(t->w1[f].get(), t->wd1[f].get(), stream_), "dgrad weights");
+    check(dbk_tr_pack_dgrad_weights(t->w2[f].get(), t->wd2[f].get(), stream_), "dgrad weights");
+    tab1[f] = t->wd1[f].get();
+    tab2[f] = t->wd2[f].get();
+  }
+  t->wd1tab.upload(tab1, stream_);
+  t->wd2tab.upload(tab2, stream_);
+  check(cudaStreamSynchronize(stream_), "dgrad tables");
   train_ = std::move(t);
 }
 
@@ -330,6 +357,50 @@ void IepSession::backward(float* loss_dev) {
   }
   T.slab_row.upload(h_slab, s);  // pairs (begin, end) per slab
   T.slab_dst.upload(h_slab_dst, s);
+  // implicit data-gradient tiles: 256 PI rows within one group, starting on
+  // a multiple of 8 (the window swizzle), every step's in one table
+  const bool dgrad = implicit_dgrad();
+  std::vector<std::int64_t> tile_off(static_cast<size_t>(S) + 1, 0);
+  if (dgrad) {
+    std::vector<std::int32_t> t_row0, t_lo, t_hi, t_fn;
+    for (int st = 0; st < S; ++st) {
+      const StepPlan& sp = plan[static_cast<size_t>(st)];
+      tile_off[static_cast<size_t>(st)] = static_cast<std::int64_t>(t_row0.size());
+      for (size_t gi = 0; gi < sp.groups.size(); ++gi) {
+        const std::int64_t lo = sp.first[gi] * kPI;
+        const std::int64_t hi = (gi + 1 < sp.groups.size() ? sp.first[gi + 1] : sp.n) * kPI;
+        for (std::int64_t r = lo / 8 * 8; r < hi; r += 256) {
+          t_row0.push_back(static_cast<std::int32_t>(r));
+          t_lo.push_back(static_cast<std::int32_t>(lo));
+          t_hi.push_back(static_cast<std::int32_t>(hi));
+          t_fn.push_back(gfid[static_cast<size_t>(sp.groups[gi])]);
+        }
+      }
+    }
+    tile_off[static_cast<size_t>(S)] = static_cast<std::int64_t>(t_row0.size());
+    std::vector<std::int32_t> all;
+    all.reserve(4 * t_row0.size());
+    for (const auto* v : {&t_row0, &t_lo, &t_hi, &t_fn}) all.insert(all.end(), v->begin(), v->end());
+    T.dtiles.upload(all, s);
+    const std::int64_t need_rows = rows_max + 16 + 256 + 32;
+    if (need_rows > T.dpack_rows) {
+      T.dpack.alloc(static_cast<size_t>(4 * need_rows * 128));
+      T.dpack_rows = need_rows;
+    }
+  }
+  const std::int64_t n_tiles_all = tile_off[static_cast<size_t>(S)];
+  const int sms = sm_count();
+  // data gradient of one 3×3 conv over the step's PI rows (the dA operand
+  // packed first); mask / resid as the col2im it replaces
+  auto dgrad_conv = [&](int st, const float* da, const Buf<const void*>& wtab, const float* mask, const float* resid,
+                        float* out, std::int64_t rows) {
+    check(dbk_tr_pack_sw128f(rows, T.dpack_rows, 16, da, T.dpack.get(), s), "pack dA");
+    const std::int64_t t0 = tile_off[static_cast<size_t>(st)], nt = tile_off[static_cast<size_t>(st) + 1] - t0;
+    const std::int32_t* tb = T.dtiles.get();
+    check(dbk_tr_dgrad(T.dpack.get(), T.dpack_rows, 16, static_cast<std::int32_t>(nt), tb + t0, tb + n_tiles_all + t0,
+                       tb + 2 * n_tiles_all + t0, tb + 3 * n_tiles_all + t0, wtab.get(), mask, resid, out, sms, s),
+          "dgrad");
+  };
   auto colsum = [&](const SlabRange& r, const float* a) {
     if (r.count)
       check(dbk_tr_colsum_seg(static_cast<std::int32_t>(r.count), T.slab_row.get() + 2 * r.begin,
@@ -406,16 +477,24 @@ void IepSession::backward(float* loss_dev) {
     check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_mid.get(), nullptr, ps, 0, 16, mid, s), "mid");
     check(dbk_tr_im2col(rows, kC, mid, T.cols.get(), s), "im2col mid");
     gemms(0);
-    gemms(1);
-    check(dbk_tr_col2im(static_cast<std::int32_t>(n), kC, T.g.get(), nullptr, mid, T.da1.get(), s), "col2im mid");
+    if (dgrad) {
+      dgrad_conv(st, T.da2.get(), T.wd2tab, mid, nullptr, T.da1.get(), rows);
+    } else {
+      gemms(1);
+      check(dbk_tr_col2im(static_cast<std::int32_t>(n), kC, T.g.get(), nullptr, mid, T.da1.get(), s), "col2im mid");
+    }
     // conv3x3 #1: dW1, db1; dx = col2im(da1·W1ᵀ) + da2 (the residual)
     colsum(slabs[static_cast<size_t>(st)][1], T.da1.get());
     check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_x.get(), R.stage_lo.get(), ps, 0, 16, xin, s),
           "x");
     check(dbk_tr_im2col(rows, kC, xin, T.cols.get(), s), "im2col x");
     gemms(2);
-    gemms(3);
-    check(dbk_tr_col2im(static_cast<std::int32_t>(n), kC, T.g.get(), T.da2.get(), nullptr, T.dx.get(), s), "col2im x");
+    if (dgrad) {
+      dgrad_conv(st, T.da1.get(), T.wd1tab, nullptr, T.da2.get(), T.dx.get(), rows);
+    } else {
+      gemms(3);
+      check(dbk_tr_col2im(static_cast<std::int32_t>(n), kC, T.g.get(), T.da2.get(), nullptr, T.dx.get(), s), "col2im x");
+    }
     if (sp.n_u > 0)
       check(dbk_tr_route(static_cast<std::int32_t>(sp.n_u), nodes, B.child0.get(), B.fid.get(), B.arity_of.get(),
                          B.example.get(), T.dx.get(), kC, 0, T.dy_nodes.get(), T.d_inputs.get(), s),

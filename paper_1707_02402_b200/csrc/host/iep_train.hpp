@@ -33,6 +33,14 @@ struct IepSession::Train {
   Buf<std::int64_t> rows, slab_row;
   Buf<float*> slab_dst;
   Buf<const void*> ptr_dev;
+  // implicit-GEMM data gradients (bwd_conv.cu): transposed tap weights per
+  // function (conv3x3 #1 / #2) and their tables, the packed dA operand, and
+  // every step's tiles (first row, group rows [lo, hi), function)
+  std::vector<Buf<std::uint8_t>> wd1, wd2;
+  Buf<const void*> wd1tab, wd2tab;
+  Buf<std::uint8_t> dpack;
+  std::int64_t dpack_rows = 0;
+  Buf<std::int32_t> dtiles;  // [4][n]: row0, lo, hi, fn
   ~Train() {
     if (blas) cublasDestroy(blas);
   }

@@ -1,0 +1,339 @@
+// bwd_conv.cu — data gradient of the IEP blocks' 3×3 convolutions as an
+// implicit GEMM on the tensor cores (tcgen05, kind::tf32), for the training
+// step's backward (iep_train.cpp).
+//
+//   dX[r] = Σ_t W_tᵀ · dA[r − s_t]      (s_t = 15·dh + dw: the tap's row shift)
+//
+// over the backward's padded-image rows (PI: per member 16 zero guard rows,
+// the 225 positions of the packed 15×15 grid, 16 guard rows), so a tap is a
+// row shift of one shared-memory window exactly as in the forward's conv
+// (rb_conv.cu): no im2col, no col2im. dA is first packed into 32-channel
+// chunk rows of 128 B with the forward's SWIZZLE_128B row swizzle
+// (k_pack_sw128f), so every (tile, chunk) window is one bulk copy and the
+// MMA descriptor may start at any row.
+//
+// Per tile of 256 PI rows of one call group: D[ci (M = 128)][rows (N = 256)]
+// in TMEM, K = 9 taps × 128 co (tf32, 8 per MMA); A = the function's
+// transposed tap weights (16 KB blocks [128 ci][32 co] fp32, SW128), B = the
+// dA window at row offset 16 − s_t. The epilogue (8 warps, lane = channel,
+// 8×8 transposes to row-major) writes every row of the group's members it
+// covers: real positions get D, masked by mid > 0 (conv3x3 #2's gradient) or
+// plus the residual dA (conv3x3 #1's); pads and guard rows get 0, so the
+// output is again a valid PI operand.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "dynbatch/dbk.h"
+#include "tc_common.cuh"
+
+namespace {
+
+using namespace dbk;
+
+constexpr int kC = 128, kPI = 257, kPIG = 16, kHalo = 16;
+constexpr int kTM = 256;                 // PI rows per tile (MMA N)
+constexpr int kWin = kTM + 2 * kHalo;    // window rows
+constexpr int kSlot = kWin * 128;        // 36 KB: one 32-channel chunk of the window
+constexpr int kSlots = 4;
+constexpr int kStage = 128 * 128;        // 16 KB weight block: 128 ci × 32 co fp32
+constexpr int kStages = 4;
+constexpr int kChunks = kC / 32;         // K chunks of 32 channels
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = (2 + kEpiWarps + 1) * 32;  // producer, MMA, epilogue × 8, weights
+constexpr int kSmem = kSlots * kSlot + kStages * kStage + 256;
+
+__device__ __forceinline__ int shift_of(int tap) { return (tap / 3 - 1) * 15 + (tap % 3 - 1); }
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+constexpr uint32_t idesc_tf32_f32(uint32_t M, uint32_t N) {
+  return (1u << 4)            // D format: f32
+         | (2u << 7)          // A format: tf32
+         | (2u << 10)         // B format: tf32
+         | ((N >> 3) << 17)   // N / 8
+         | ((M >> 4) << 24);  // M / 16
+}
+
+// 8×8 transpose across the 8 lanes of a plane group (as rb_conv.cu).
+__device__ __forceinline__ void transpose8(float* x, int e) {
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const bool up = (e & s) != 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i & s) continue;
+      const float send = up ? x[i] : x[i + s];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, s);
+      x[i] = up ? recv : x[i];
+      x[i + s] = up ? x[i + s] : recv;
+    }
+  }
+}
+
+struct DgradParams {
+  const uint8_t* src;   // packed dA: [4 chunks][rows_alloc][128 B], row 0 = PI row −lead
+  int64_t rows_alloc;   // rows per chunk plane
+  int32_t lead;         // zero rows before PI row 0
+  int32_t n_tiles;
+  const int32_t* tile_row0;  // first PI row of the tile (multiple of 8)
+  const int32_t* tile_lo;    // the tile's group: PI rows [lo, hi) are written
+  const int32_t* tile_hi;
+  const int32_t* tile_fn;    // weight table index
+  const uint8_t* const* wpack;  // per function: 9 taps × 4 chunks × 16 KB (tile_fn indexes it)
+  const float* mask;    // PI [rows][128]: output ⊙ (mask > 0), or null
+  const float* resid;   // PI [rows][128]: output + resid, or null
+  float* out;           // PI [rows][128]
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant__ DgradParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;                      // window chunks
+  uint8_t* sW = smem + kSlots * kSlot;     // weight blocks
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sW + kStages * kStage);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kSlots;
+  uint64_t* w_full = a_empty + kSlots;
+  uint64_t* w_empty = w_full + kStages;
+  uint64_t* acc_full = w_empty + kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(a_full + s, 1);
+      mbar_init(a_empty + s, 1);
+    }
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(w_full + s, 1);
+      mbar_init(w_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, kEpiWarps * 32);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------- dA windows
+      uint32_t ai = 0;
+      for (int32_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+        const int64_t r0 = P.lead + P.tile_row0[t] - kHalo;  // window's first packed row
+        for (int c = 0; c < kChunks; ++c, ++ai) {
+          const uint32_t s = ai % kSlots, par = (ai / kSlots) & 1;
+          mbar_wait(a_empty + s, par ^ 1);
+          mbar_expect_tx(a_full + s, kSlot);
+          bulk_g2s(sA + s * kSlot, P.src + ((static_cast<int64_t>(c) * P.rows_alloc + r0) << 7), kSlot, a_full + s);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------ MMA issuer
+      constexpr uint32_t IDESC = idesc_tf32_f32(128, kTM);
+      const uint32_t a_base = smem_u32(sA), w_base = smem_u32(sW);
+      uint32_t ai = 0, wi = 0;
+      int n = 0;
+      for (int32_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, ++n) {
+        const int abuf = n & 1;
+        mbar_wait(acc_empty + abuf, ((n >> 1) & 1) ^ 1);
+        tc_fence_after();
+        uint32_t acc = 0;
+        for (int c = 0; c < kChunks; ++c, ++ai) {
+          const uint32_t sa = ai % kSlots;
+          mbar_wait(a_full + sa, (ai / kSlots) & 1);
+          tc_fence_after();
+          for (int tap = 0; tap < 9; ++tap, ++wi) {
+            const uint32_t sw = wi % kStages;
+            mbar_wait(w_full + sw, (wi / kStages) & 1);
+            tc_fence_after();
+            const uint32_t row = static_cast<uint32_t>(kHalo - shift_of(tap));
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t wd = smem_desc_sw128(w_base + sw * kStage + kk * 32);
+              const uint64_t xd = smem_desc_sw128(a_base + sa * kSlot + row * 128 + kk * 32);
+              mma_tf32(tmem_base + abuf * kTM, wd, xd, IDESC, acc);
+              acc = 1;
+            }
+            mma_commit(w_empty + sw);
+          }
+          mma_commit(a_empty + sa);
+        }
+        mma_commit(acc_full + abuf);
+      }
+    }
+  } else if (warp == 2 + kEpiWarps) {
+    if (lane == 0) {  // --------------------------------------- weight blocks
+      uint32_t wi = 0;
+      for (int32_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+        const uint8_t* w = P.wpack[P.tile_fn[t]];
+        for (int c = 0; c < kChunks; ++c)
+          for (int tap = 0; tap < 9; ++tap, ++wi) {
+            const uint32_t s = wi % kStages, par = (wi / kStages) & 1;
+            mbar_wait(w_empty + s, par ^ 1);
+            mbar_expect_tx(w_full + s, kStage);
+            bulk_g2s(sW + s * kStage, w + static_cast<int64_t>(tap * kChunks + c) * kStage, kStage, w_full + s);
+          }
+      }
+    }
+  } else {  // ---------------------------------------------------- epilogue
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int g = lane >> 3, e = lane & 7;
+    const int plane = quarter * 4 + g;  // 8 channels: ci = 8·plane + k
+    int n = 0;
+    for (int32_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, ++n) {
+      const int abuf = n & 1;
+      mbar_wait(acc_full + abuf, (n >> 1) & 1);
+      tc_fence_after();
+      const int32_t row0 = P.tile_row0[t], lo = P.tile_lo[t], hi = P.tile_hi[t];
+      const uint32_t taddr = tmem_base + abuf * kTM + (static_cast<uint32_t>(quarter * 32) << 16) + half * (kTM / 2);
+#pragma unroll 1
+      for (int cb = 0; cb < kTM / 2 / 16; ++cb) {
+        float v[16];
+        tmem_ld16(taddr + cb * 16, v);
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          float* x = v + 8 * m;
+          transpose8(x, e);
+          const int32_t r = row0 + half * (kTM / 2) + cb * 16 + 8 * m + e;
+          if (r < lo || r >= hi) continue;
+          const int32_t local = r % kPI;
+          const int32_t p = local - kPIG;
+          const bool real = p >= 0 && p < 225 && p / 15 < 14 && p % 15 < 14;
+          float o[8];
+          if (real) {
+            const int64_t off = static_cast<int64_t>(r) * kC + plane * 8;
+            if (P.mask) {
+              const float4 a = *reinterpret_cast<const float4*>(P.mask + off);
+              const float4 b = *reinterpret_cast<const float4*>(P.mask + off + 4);
+              const float mk[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+              for (int k = 0; k < 8; ++k) o[k] = mk[k] > 0.f ? x[k] : 0.f;
+            } else {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) o[k] = x[k];
+            }
+            if (P.resid) {
+              const float4 a = *reinterpret_cast<const float4*>(P.resid + off);
+              const float4 b = *reinterpret_cast<const float4*>(P.resid + off + 4);
+              o[0] += a.x; o[1] += a.y; o[2] += a.z; o[3] += a.w;
+              o[4] += b.x; o[5] += b.y; o[6] += b.z; o[7] += b.w;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = 0.f;
+          }
+          float4* dst = reinterpret_cast<float4*>(P.out + static_cast<int64_t>(r) * kC + plane * 8);
+          dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+          dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty + abuf);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// PI rows [0, rows) fp32 [rows][128] → 4 chunk planes of 128-byte rows
+// (32 channels each), 16-byte pieces XOR-swizzled by row; `lead` zero rows
+// before PI row 0 and the rest of rows_alloc zero (halo reads past either end).
+__global__ void k_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead, const float* __restrict__ pi,
+                              uint8_t* __restrict__ out) {
+  const int64_t total = 4 * rows_alloc * 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i & 7);         // 16-byte piece: channels 4j .. 4j + 3 of the chunk
+    const int64_t q = i >> 3;
+    const int c = static_cast<int>(q / rows_alloc);
+    const int64_t rr = q - static_cast<int64_t>(c) * rows_alloc;  // packed row
+    const int64_t r = rr - lead;                                   // PI row
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r >= 0 && r < rows) v = *reinterpret_cast<const float4*>(pi + r * kC + c * 32 + 4 * j);
+    *reinterpret_cast<float4*>(out + ((static_cast<int64_t>(c) * rows_alloc + rr) << 7) +
+                               ((j ^ static_cast<int>(rr & 7)) << 4)) = v;
+  }
+}
+
+// one thread per 16-byte piece: 9 taps × 4 chunks × 128 rows (ci) × 8 pieces
+__global__ void k_pack_dgrad_w(const float* __restrict__ w, uint8_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 9 * kChunks * 128 * 8) return;
+  const int j = i & 7, ci = (i >> 3) & 127, blk = i >> 10;  // blk = tap · 4 + chunk
+  const int tap = blk / kChunks, c = blk % kChunks;
+  const float* src = w + (static_cast<int64_t>(tap) * kC + ci) * kC + c * 32 + 4 * j;
+  *reinterpret_cast<float4*>(out + static_cast<int64_t>(blk) * kStage + ci * 128 + ((j ^ (ci & 7)) << 4)) =
+      *reinterpret_cast<const float4*>(src);
+}
+
+}  // namespace
+
+extern "C" int dbk_tr_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead, const float* pi, void* out,
+                                  void* stream) {
+  const int64_t total = 4 * rows_alloc * 8;
+  if (total <= 0) return 0;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  k_pack_sw128f<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, rows_alloc, lead, pi,
+                                                                        static_cast<uint8_t*>(out));
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_dgrad(const void* packed, int64_t rows_alloc, int32_t lead, int32_t n_tiles,
+                            const int32_t* tile_row0, const int32_t* tile_lo, const int32_t* tile_hi,
+                            const int32_t* tile_fn, const void* const* wpack, const float* mask, const float* resid,
+                            float* out, int32_t sms, void* stream) {
+  if (n_tiles <= 0) return 0;
+  static std::atomic<uint64_t> configured{0};  // per device, once
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(k_tr_dgrad, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    configured.fetch_or(bit, std::memory_order_release);
+  }
+  DgradParams p;
+  p.src = static_cast<const uint8_t*>(packed);
+  p.rows_alloc = rows_alloc;
+  p.lead = lead;
+  p.n_tiles = n_tiles;
+  p.tile_row0 = tile_row0;
+  p.tile_lo = tile_lo;
+  p.tile_hi = tile_hi;
+  p.tile_fn = tile_fn;
+  p.wpack = reinterpret_cast<const uint8_t* const*>(wpack);
+  p.mask = mask;
+  p.resid = resid;
+  p.out = out;
+  k_tr_dgrad<<<static_cast<unsigned>(std::min(n_tiles, std::max(sms, 1))), kThreads, kSmem,
+               static_cast<cudaStream_t>(stream)>>>(p);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Transposed tap weights of one function for k_tr_dgrad, from the
+// input-major fp32 weights w[(tap·C + ci)·C + co] (= W_tap[co][ci]): block
+// (tap, chunk c) row ci holds co = 32c .. 32c + 31, swizzled like the windows.
+extern "C" int dbk_tr_pack_dgrad_weights(const float* w, void* out, void* stream) {
+  k_pack_dgrad_w<<<9 * kChunks * 128 * 8 / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      w, static_cast<uint8_t*>(out));
+  return static_cast<int>(cudaGetLastError());
+}

@@ -75,18 +75,20 @@ __global__ void k_stage_to_pi(int32_t n, const int64_t* __restrict__ rows, const
 }
 
 // DA2 = dY ⊙ (y > 0) for the group's members: dY from the node-indexed PI
-// buffer, y from the node's fp32 plane map; pads 0.
+// buffer, y from the node's fp32 plane map; every PI row is written (pads
+// and guard rows 0: shifted reads of the data gradient and the weight
+// gradients' K range cover them).
 __global__ void k_da_out(int32_t n, const int32_t* __restrict__ nodes, const float* __restrict__ dy_nodes,
                          const float* __restrict__ values, float* __restrict__ out) {
-  const int64_t total = static_cast<int64_t>(n) * kImg * 16;
+  const int64_t total = static_cast<int64_t>(n) * kPI * 16;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int j = static_cast<int>(i % 16);
     const int64_t kp = i / 16;
-    const int32_t k = static_cast<int32_t>(kp / kImg);
-    const int p = static_cast<int>(kp % kImg);
+    const int32_t k = static_cast<int32_t>(kp / kPI);
+    const int p = static_cast<int>(kp % kPI) - kPIG;  // position, or a guard row outside [0, 225)
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (!is_pad(p)) {
+    if (p >= 0 && p < kImg && !is_pad(p)) {
       const int32_t v = nodes[k];
       const int64_t prow = (static_cast<int64_t>(v) * kPI + kPIG + p) * kC + j * 8;
       const float4* d = reinterpret_cast<const float4*>(dy_nodes + prow);
@@ -379,7 +381,7 @@ extern "C" int dbk_tr_colsum_seg(int32_t slabs, const int64_t* slab_row, float* 
 
 extern "C" int dbk_tr_da_out(int32_t n, const int32_t* nodes, const float* dy_nodes, const float* values,
                              float* out, void* stream) {
-  const int64_t total = static_cast<int64_t>(n) * kImg * 16;
+  const int64_t total = static_cast<int64_t>(n) * kPI * 16;
   if (total <= 0) return 0;
   k_da_out<<<grid_for(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, nodes, dy_nodes, values, out);
   return static_cast<int>(cudaGetLastError());
