@@ -260,13 +260,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
 // before PI row 0 and the rest of rows_alloc zero (halo reads past either end).
 __global__ void k_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead, const float* __restrict__ pi,
                               uint8_t* __restrict__ out) {
-  const int64_t total = 4 * rows_alloc * 8;
+  // the rows any window of this call reads: the lead, the PI rows, one
+  // tile plus halo past the end (zeros)
+  const int64_t used = min(rows_alloc, lead + rows + kWin);
+  const int64_t total = 4 * used * 8;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int j = static_cast<int>(i & 7);         // 16-byte piece: channels 4j .. 4j + 3 of the chunk
     const int64_t q = i >> 3;
-    const int c = static_cast<int>(q / rows_alloc);
-    const int64_t rr = q - static_cast<int64_t>(c) * rows_alloc;  // packed row
+    const int c = static_cast<int>(q / used);
+    const int64_t rr = q - static_cast<int64_t>(c) * used;  // packed row
     const int64_t r = rr - lead;                                   // PI row
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r >= 0 && r < rows) v = *reinterpret_cast<const float4*>(pi + r * kC + c * 32 + 4 * j);
@@ -290,7 +293,7 @@ __global__ void k_pack_dgrad_w(const float* __restrict__ w, uint8_t* __restrict_
 
 extern "C" int dbk_tr_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead, const float* pi, void* out,
                                   void* stream) {
-  const int64_t total = 4 * rows_alloc * 8;
+  const int64_t total = 4 * std::min<int64_t>(rows_alloc, lead + rows + kWin) * 8;
   if (total <= 0) return 0;
   const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
   k_pack_sw128f<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, rows_alloc, lead, pi,
