@@ -244,6 +244,17 @@ int dbk_tr_pack_dgrad_weights(const float* w, void* out, void* stream);
 int dbk_tr_dgrad(const void* packed, int64_t rows_alloc, int32_t lead, int32_t n_tiles, const int32_t* tile_row0,
                  const int32_t* tile_lo, const int32_t* tile_hi, const int32_t* tile_fn, const void* const* wpack,
                  const float* mask, const float* resid, float* out, int32_t sms, void* stream);
+/* Weight gradient of a 3×3 conv (bwd_conv.cu): items [4][item_stride] = K
+ * range [k0, k1) of PI rows (multiples of 16, inside one call group or its
+ * zero guard rows), kernel row dr, function; gw[function] += Σ x[r + s_t] ⊗
+ * dA[r] for the three taps of row dr. x and dA are packed to fp16 by
+ * dbk_tr_pack_sw128h, dA scaled from its |max| (dbk_tr_absmax). */
+int dbk_tr_absmax(int64_t n, const float* x, uint32_t* out, void* stream);
+int dbk_tr_pack_sw128h(int64_t rows, int64_t rows_alloc, int32_t lead, const float* pi, const uint32_t* absmax,
+                       void* out, void* stream);
+int dbk_tr_wgrad(const void* x_packed, const void* da_packed, const uint32_t* absmax, int64_t rows_alloc, int32_t lead,
+                 int32_t n_items, const int32_t* items, int64_t item_stride, float* const* gw, int32_t sms,
+                 void* stream);
 int dbk_tr_unpack_h(int64_t rows, int32_t K, const void* h, float* out, void* stream);
 int dbk_tr_unpack_sw128(int64_t rows, int32_t K, const void* a, float* out, void* stream);
 int dbk_tr_pool_bwd(int64_t b, int32_t P, const float* proj, const float* dpooled, float* dproj, void* stream);

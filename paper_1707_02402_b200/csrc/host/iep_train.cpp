@@ -20,6 +20,8 @@
 #include "iep_train.hpp"
 
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
 #include <array>
 #include <cstdlib>
 #include <cstring>
@@ -174,6 +176,13 @@ void IepSession::set_training(bool on) {
   }
   t->wd1tab.upload(tab1, stream_);
   t->wd2tab.upload(tab2, stream_);
+  std::vector<float*> g1(p, nullptr), g2(p, nullptr);
+  for (size_t f = 0; f < p; ++f) {
+    g1[f] = t->gw1[f].get();
+    g2[f] = t->gw2[f].get();
+  }
+  t->gw1tab.upload(g1, stream_);
+  t->gw2tab.upload(g2, stream_);
   check(cudaStreamSynchronize(stream_), "dgrad tables");
   train_ = std::move(t);
 }
@@ -360,34 +369,57 @@ void IepSession::backward(float* loss_dev) {
   // implicit data-gradient tiles: 256 PI rows within one group, starting on
   // a multiple of 8 (the window swizzle), every step's in one table
   const bool dgrad = implicit_dgrad();
-  std::vector<std::int64_t> tile_off(static_cast<size_t>(S) + 1, 0);
+  std::vector<std::int64_t> tile_off(static_cast<size_t>(S) + 1, 0), item_off(static_cast<size_t>(S) + 1, 0);
   if (dgrad) {
-    std::vector<std::int32_t> t_row0, t_lo, t_hi, t_fn;
+    // weight-gradient items: a group's rows widened to multiples of 8 (the
+    // extra rows are zero dA guard rows), in K ranges of kKR, per kernel row
+    constexpr std::int64_t kKR = 1024;
+    std::vector<std::int32_t> t_row0, t_lo, t_hi, t_fn, w_k0, w_k1, w_dr, w_fn;
     for (int st = 0; st < S; ++st) {
       const StepPlan& sp = plan[static_cast<size_t>(st)];
       tile_off[static_cast<size_t>(st)] = static_cast<std::int64_t>(t_row0.size());
+      item_off[static_cast<size_t>(st)] = static_cast<std::int64_t>(w_k0.size());
       for (size_t gi = 0; gi < sp.groups.size(); ++gi) {
         const std::int64_t lo = sp.first[gi] * kPI;
         const std::int64_t hi = (gi + 1 < sp.groups.size() ? sp.first[gi + 1] : sp.n) * kPI;
+        const std::int32_t fn = gfid[static_cast<size_t>(sp.groups[gi])];
         for (std::int64_t r = lo / 8 * 8; r < hi; r += 256) {
           t_row0.push_back(static_cast<std::int32_t>(r));
           t_lo.push_back(static_cast<std::int32_t>(lo));
           t_hi.push_back(static_cast<std::int32_t>(hi));
-          t_fn.push_back(gfid[static_cast<size_t>(sp.groups[gi])]);
+          t_fn.push_back(fn);
         }
+        // K ranges on multiples of 16 (one fp16 MMA): the widened rows are
+        // zero-dA guard rows of the neighbouring members
+        const std::int64_t k_end = (hi + 15) / 16 * 16;
+        for (std::int64_t k = lo / 16 * 16; k < k_end; k += kKR)
+          for (int dr = 0; dr < 3; ++dr) {
+            w_k0.push_back(static_cast<std::int32_t>(k));
+            w_k1.push_back(static_cast<std::int32_t>(std::min(k + kKR, k_end)));
+            w_dr.push_back(dr);
+            w_fn.push_back(fn);
+          }
       }
     }
     tile_off[static_cast<size_t>(S)] = static_cast<std::int64_t>(t_row0.size());
+    item_off[static_cast<size_t>(S)] = static_cast<std::int64_t>(w_k0.size());
     std::vector<std::int32_t> all;
     all.reserve(4 * t_row0.size());
     for (const auto* v : {&t_row0, &t_lo, &t_hi, &t_fn}) all.insert(all.end(), v->begin(), v->end());
     T.dtiles.upload(all, s);
+    all.clear();
+    for (const auto* v : {&w_k0, &w_k1, &w_dr, &w_fn}) all.insert(all.end(), v->begin(), v->end());
+    T.witems.upload(all, s);
     const std::int64_t need_rows = rows_max + 16 + 256 + 32;
     if (need_rows > T.dpack_rows) {
       T.dpack.alloc(static_cast<size_t>(4 * need_rows * 128));
+      T.apack.alloc(static_cast<size_t>(2 * need_rows * 128));
+      T.hpack.alloc(static_cast<size_t>(2 * need_rows * 128));
       T.dpack_rows = need_rows;
     }
+    T.absmax.ensure(1);
   }
+  const std::int64_t n_items_all = item_off[static_cast<size_t>(S)];
   const std::int64_t n_tiles_all = tile_off[static_cast<size_t>(S)];
   const int sms = sm_count();
   // data gradient of one 3×3 conv over the step's PI rows (the dA operand
@@ -400,6 +432,17 @@ void IepSession::backward(float* loss_dev) {
     check(dbk_tr_dgrad(T.dpack.get(), T.dpack_rows, 16, static_cast<std::int32_t>(nt), tb + t0, tb + n_tiles_all + t0,
                        tb + 2 * n_tiles_all + t0, tb + 3 * n_tiles_all + t0, wtab.get(), mask, resid, out, sms, s),
           "dgrad");
+  };
+  // weight gradient of one 3×3 conv: its input activations and dA, both PI
+  // rows, packed to fp16 here (dA scaled into fp16's normal range)
+  auto wgrad_conv = [&](int st, const float* act, const float* da, const Buf<float*>& gwtab, std::int64_t rows) {
+    check(dbk_tr_absmax(rows * kC, da, T.absmax.get(), s), "dA max");
+    check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, da, T.absmax.get(), T.hpack.get(), s), "pack dA");
+    check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, act, nullptr, T.apack.get(), s), "pack activations");
+    const std::int64_t i0 = item_off[static_cast<size_t>(st)], ni = item_off[static_cast<size_t>(st) + 1] - i0;
+    check(dbk_tr_wgrad(T.apack.get(), T.hpack.get(), T.absmax.get(), T.dpack_rows, 16, static_cast<std::int32_t>(ni),
+                       T.witems.get() + i0, n_items_all, gwtab.get(), sms, s),
+          "wgrad");
   };
   auto colsum = [&](const SlabRange& r, const float* a) {
     if (r.count)
@@ -475,11 +518,12 @@ void IepSession::backward(float* loss_dev) {
     check(dbk_tr_da_out(static_cast<std::int32_t>(n), nodes, T.dy_nodes.get(), R.values.get(), T.da2.get(), s), "da2");
     colsum(slabs[static_cast<size_t>(st)][0], T.da2.get());
     check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_mid.get(), nullptr, ps, 0, 16, mid, s), "mid");
-    check(dbk_tr_im2col(rows, kC, mid, T.cols.get(), s), "im2col mid");
-    gemms(0);
     if (dgrad) {
       dgrad_conv(st, T.da2.get(), T.wd2tab, mid, nullptr, T.da1.get(), rows);
+      wgrad_conv(st, mid, T.da2.get(), T.gw2tab, rows);
     } else {
+      check(dbk_tr_im2col(rows, kC, mid, T.cols.get(), s), "im2col mid");
+      gemms(0);
       gemms(1);
       check(dbk_tr_col2im(static_cast<std::int32_t>(n), kC, T.g.get(), nullptr, mid, T.da1.get(), s), "col2im mid");
     }
@@ -487,11 +531,12 @@ void IepSession::backward(float* loss_dev) {
     colsum(slabs[static_cast<size_t>(st)][1], T.da1.get());
     check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_x.get(), R.stage_lo.get(), ps, 0, 16, xin, s),
           "x");
-    check(dbk_tr_im2col(rows, kC, xin, T.cols.get(), s), "im2col x");
-    gemms(2);
     if (dgrad) {
       dgrad_conv(st, T.da1.get(), T.wd1tab, nullptr, T.da2.get(), T.dx.get(), rows);
+      wgrad_conv(st, xin, T.da1.get(), T.gw1tab, rows);
     } else {
+      check(dbk_tr_im2col(rows, kC, xin, T.cols.get(), s), "im2col x");
+      gemms(2);
       gemms(3);
       check(dbk_tr_col2im(static_cast<std::int32_t>(n), kC, T.g.get(), T.da2.get(), nullptr, T.dx.get(), s), "col2im x");
     }

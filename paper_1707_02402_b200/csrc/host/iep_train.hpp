@@ -38,9 +38,13 @@ struct IepSession::Train {
   // every step's tiles (first row, group rows [lo, hi), function)
   std::vector<Buf<std::uint8_t>> wd1, wd2;
   Buf<const void*> wd1tab, wd2tab;
-  Buf<std::uint8_t> dpack;
+  Buf<std::uint8_t> dpack;         // packed fp32 dA (data gradients)
+  Buf<std::uint8_t> apack, hpack;  // packed fp16 activations (mid / x) and scaled dA (weight gradients)
+  Buf<std::uint32_t> absmax;       // |dA| max (float bits): the fp16 scale
   std::int64_t dpack_rows = 0;
   Buf<std::int32_t> dtiles;  // [4][n]: row0, lo, hi, fn
+  Buf<std::int32_t> witems;  // [4][n]: K range k0, k1, kernel row dr, fn
+  Buf<float*> gw1tab, gw2tab;
   ~Train() {
     if (blas) cublasDestroy(blas);
   }

@@ -289,6 +289,214 @@ __global__ void k_pack_dgrad_w(const float* __restrict__ w, uint8_t* __restrict_
       *reinterpret_cast<const float4*>(src);
 }
 
+
+// ------------------------------------------------------------ weight gradient
+// dW_t[ci][co] = Σ_r x[r + s_t][ci] · dA[r][co]. Both operands are read
+// MN-major (a 128-byte row = one K index = 64 channels of M or N; the two
+// 64-channel planes are the MN blocks, LBO apart; 8-row groups 1024 B apart),
+// so a tap is again a row offset of the x window and nothing is expanded.
+// MN-major operands exist for 16-bit formats only (a kind::tf32 MMA with
+// MN-major operands produces zeros: tools/mn_major_test.cu), so x and dA are
+// packed to fp16 (k_pack_sw128h), dA scaled by a power of two from its
+// maximum (k_absmax) so the gradients sit in fp16's normal range. One work
+// item = (call group, kernel row dr, K range): D[ci][3 × 128 co] in TMEM over
+// 64-row K blocks (K = 16 per MMA); the epilogue adds D / scale into the
+// function's fp32 gradient (input-major w[(t·C + ci)·C + co]) with vector
+// atomics, straight from TMEM (lane = ci, columns = co: no transposes).
+constexpr int kWB = 64;                     // K rows per block
+constexpr int kXW = kWB + 16;               // x window rows (3 shifts + 8-row alignment)
+constexpr int kWDa = 2 * kWB * 128;         // 16 KB: dA block, 2 planes
+constexpr int kWX = 2 * kXW * 128;          // 20 KB: x window, 2 planes
+constexpr int kWStage = kWDa + kWX;
+constexpr int kWStages = 6;
+constexpr int kWSmem = kWStages * kWStage + 256;
+
+// MN-major SWIZZLE_128B descriptor: MN blocks of 128 B `lbo` bytes apart,
+// K rows 128 B apart in 8-row groups of 1024 B.
+__device__ __forceinline__ uint64_t smem_desc_mn128(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;  // LBO: next MN block
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;            // SBO: next 8 K rows
+  d |= static_cast<uint64_t>(1) << 46;                    // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;                    // SWIZZLE_128B
+  return d;
+}
+
+// dA scale from |dA|max (bit pattern of a non-negative float): the largest
+// power of two keeping it ≤ 2^14 (1 when dA is all zero).
+__device__ __forceinline__ float grad_scale(const uint32_t* absmax_bits) {
+  const float m = __uint_as_float(*absmax_bits);
+  return m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
+}
+
+struct WgradParams {
+  const uint8_t* x;      // packed fp16 activations (x or mid), k_pack_sw128h
+  const uint8_t* da;     // packed fp16 dA, scaled
+  const uint32_t* absmax;  // |dA| max (float bits): the scale
+  int64_t rows_alloc;
+  int32_t lead;
+  int32_t n_items;
+  int64_t stride;        // between the item table's four columns
+  const int32_t* item;   // [4][stride]: k0, k1 (PI rows, multiples of 16), dr, function
+  float* const* gw;      // per function: fp32 gradient, input-major [9·C][C]
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_tr_wgrad(const __grid_constant__ WgradParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kWStages * kWStage);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kWStages;
+  uint64_t* acc_full = empty + kWStages;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t n = P.n_items;
+  const int32_t* k0s = P.item;
+  const int32_t* k1s = P.item + P.stride;
+  const int32_t* drs = P.item + 2 * P.stride;
+  const int32_t* fns = P.item + 3 * P.stride;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, kEpiWarps * 32);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------ producer
+      uint32_t bi = 0;
+      for (int32_t it = blockIdx.x; it < n; it += gridDim.x) {
+        const int32_t k0 = k0s[it], k1 = k1s[it], sh = 15 * (drs[it] - 1);
+        for (int32_t kb = k0; kb < k1; kb += kWB, ++bi) {
+          const uint32_t s = bi % kWStages;
+          mbar_wait(empty + s, ((bi / kWStages) & 1) ^ 1);
+          mbar_expect_tx(full + s, kWStage);
+          uint8_t* st = smem + s * kWStage;
+          const int64_t ws = ((kb + sh - 1) >> 3) << 3;  // x window start row (8-aligned)
+          for (int c = 0; c < 2; ++c) {
+            bulk_g2s(st + c * (kWB * 128), P.da + ((static_cast<int64_t>(c) * P.rows_alloc + P.lead + kb) << 7),
+                     kWB * 128, full + s);
+            bulk_g2s(st + kWDa + c * (kXW * 128),
+                     P.x + ((static_cast<int64_t>(c) * P.rows_alloc + P.lead + ws) << 7), kXW * 128, full + s);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------ MMA issuer
+      constexpr uint32_t IDESC = idesc_f16_f32(128, 128) | (1u << 15) | (1u << 16);  // A, B MN-major
+      const uint32_t base = smem_u32(smem);
+      uint32_t bi = 0;
+      int j = 0;
+      for (int32_t it = blockIdx.x; it < n; it += gridDim.x, ++j) {
+        const int32_t k0 = k0s[it], k1 = k1s[it], sh = 15 * (drs[it] - 1);
+        mbar_wait(acc_empty, (j & 1) ^ 1);
+        tc_fence_after();
+        uint32_t acc = 0;
+        for (int32_t kb = k0; kb < k1; kb += kWB, ++bi) {
+          const uint32_t s = bi % kWStages;
+          mbar_wait(full + s, (bi / kWStages) & 1);
+          tc_fence_after();
+          const uint32_t st = base + s * kWStage;
+          const int32_t ws = ((kb + sh - 1) >> 3) << 3;
+          const int32_t steps = min(kWB, k1 - kb) / 16;
+          for (int kk = 0; kk < steps; ++kk) {
+            const uint64_t bd = smem_desc_mn128(st + kk * 16 * 128, kWB * 128);
+#pragma unroll
+            for (int dc = 0; dc < 3; ++dc) {
+              const uint32_t xr = static_cast<uint32_t>(kb + sh + dc - 1 + 16 * kk - ws);
+              const uint64_t ad = smem_desc_mn128(st + kWDa + xr * 128, kXW * 128);
+              mma_bf16(tmem_base + dc * 128, ad, bd, IDESC, acc);
+            }
+            acc = 1;
+          }
+          mma_commit(empty + s);
+        }
+        mma_commit(acc_full);
+      }
+    }
+  } else if (warp >= 2 && warp < 2 + kEpiWarps) {  // -------------- epilogue
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int ci = quarter * 32 + lane;
+    const float inv = 1.f / grad_scale(P.absmax);
+    int j = 0;
+    for (int32_t it = blockIdx.x; it < n; it += gridDim.x, ++j) {
+      mbar_wait(acc_full, j & 1);
+      tc_fence_after();
+      float* gw = P.gw[fns[it]];
+      const int dr = drs[it];
+      for (int cb = 0; cb < 6; ++cb) {  // this warp's 192 of the 384 columns, 32 at a time
+        const int col = half * 192 + cb * 32;
+        float v[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + col, v);
+        const int dc = col / 128, co = col % 128;
+        float* dst = gw + (static_cast<int64_t>(3 * dr + dc) * kC + ci) * kC + co;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          atomicAdd(reinterpret_cast<float4*>(dst + 4 * q),
+                    make_float4(v[4 * q] * inv, v[4 * q + 1] * inv, v[4 * q + 2] * inv, v[4 * q + 3] * inv));
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// PI rows fp32 [rows][128] → 2 planes of 128-byte rows (64 fp16 channels),
+// 16-byte pieces XOR-swizzled by row, times the scale from `absmax` (null: 1);
+// `lead` zero rows first, zeros up to one window past the end.
+__global__ void k_pack_sw128h(int64_t rows, int64_t rows_alloc, int32_t lead, const float* __restrict__ pi,
+                              const uint32_t* __restrict__ absmax, uint8_t* __restrict__ out) {
+  const float sc = absmax ? grad_scale(absmax) : 1.f;
+  const int64_t used = min(rows_alloc, lead + rows + kWin);
+  const int64_t total = 2 * used * 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i & 7);  // 16-byte piece: channels 8j .. 8j + 7 of the plane
+    const int64_t q = i >> 3;
+    const int c = static_cast<int>(q / used);
+    const int64_t rr = q - static_cast<int64_t>(c) * used;
+    const int64_t r = rr - lead;
+    uint4 h = make_uint4(0, 0, 0, 0);
+    if (r >= 0 && r < rows) {
+      const float4 a = *reinterpret_cast<const float4*>(pi + r * kC + c * 64 + 8 * j);
+      const float4 b = *reinterpret_cast<const float4*>(pi + r * kC + c * 64 + 8 * j + 4);
+      h.x = pack_f16x2(a.x * sc, a.y * sc);
+      h.y = pack_f16x2(a.z * sc, a.w * sc);
+      h.z = pack_f16x2(b.x * sc, b.y * sc);
+      h.w = pack_f16x2(b.z * sc, b.w * sc);
+    }
+    *reinterpret_cast<uint4*>(out + ((static_cast<int64_t>(c) * rows_alloc + rr) << 7) +
+                              ((j ^ static_cast<int>(rr & 7)) << 4)) = h;
+  }
+}
+
+// |x| max over n floats into *out (float bits, atomicMax; *out zeroed first).
+__global__ void k_absmax(int64_t n, const float* __restrict__ x, uint32_t* __restrict__ out) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n / 4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(x)[i];
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
 }  // namespace
 
 extern "C" int dbk_tr_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead, const float* pi, void* out,
@@ -338,5 +546,51 @@ extern "C" int dbk_tr_dgrad(const void* packed, int64_t rows_alloc, int32_t lead
 extern "C" int dbk_tr_pack_dgrad_weights(const float* w, void* out, void* stream) {
   k_pack_dgrad_w<<<9 * kChunks * 128 * 8 / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       w, static_cast<uint8_t*>(out));
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_pack_sw128h(int64_t rows, int64_t rows_alloc, int32_t lead, const float* pi,
+                                  const uint32_t* absmax, void* out, void* stream) {
+  const int64_t total = 2 * std::min<int64_t>(rows_alloc, lead + rows + kWin) * 8;
+  if (total <= 0) return 0;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  k_pack_sw128h<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, rows_alloc, lead, pi, absmax,
+                                                                        static_cast<uint8_t*>(out));
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_absmax(int64_t n, const float* x, uint32_t* out, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(out, 0, sizeof(uint32_t), s);
+  if (n <= 0) return static_cast<int>(cudaGetLastError());
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n / 4 + 255) / 256, 148 * 8));
+  k_absmax<<<std::max(blocks, 1u), 256, 0, s>>>(n, x, out);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_wgrad(const void* x_packed, const void* da_packed, const uint32_t* absmax, int64_t rows_alloc,
+                            int32_t lead, int32_t n_items, const int32_t* items, int64_t item_stride, float* const* gw,
+                            int32_t sms, void* stream) {
+  if (n_items <= 0) return 0;
+  static std::atomic<uint64_t> configured{0};  // per device, once
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(k_tr_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem);
+    configured.fetch_or(bit, std::memory_order_release);
+  }
+  WgradParams p;
+  p.x = static_cast<const uint8_t*>(x_packed);
+  p.da = static_cast<const uint8_t*>(da_packed);
+  p.absmax = absmax;
+  p.rows_alloc = rows_alloc;
+  p.lead = lead;
+  p.n_items = n_items;
+  p.stride = item_stride;
+  p.item = items;
+  p.gw = gw;
+  k_tr_wgrad<<<static_cast<unsigned>(std::min(n_items, std::max(sms, 1))), kThreads, kWSmem,
+               static_cast<cudaStream_t>(stream)>>>(p);
   return static_cast<int>(cudaGetLastError());
 }
