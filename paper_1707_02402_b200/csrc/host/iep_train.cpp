@@ -373,7 +373,10 @@ void IepSession::backward(float* loss_dev) {
   if (dgrad) {
     // weight-gradient items: a group's rows widened to multiples of 8 (the
     // extra rows are zero dA guard rows), in K ranges of kKR, per kernel row
-    constexpr std::int64_t kKR = 1024;
+    static const std::int64_t kKR = [] {  // K rows per weight-gradient item (A/B: DYNBATCH_WGRAD_KR)
+      const char* e = std::getenv("DYNBATCH_WGRAD_KR");
+      return e ? std::max<std::int64_t>(64, std::atoll(e) / 64 * 64) : 8192;
+    }();
     std::vector<std::int32_t> t_row0, t_lo, t_hi, t_fn, w_k0, w_k1, w_dr, w_fn;
     for (int st = 0; st < S; ++st) {
       const StepPlan& sp = plan[static_cast<size_t>(st)];
