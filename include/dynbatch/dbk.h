@@ -241,9 +241,13 @@ int dbk_tr_softmax_ce(int64_t b, int32_t A, int32_t ld, const float* logits, con
  * and / or + resid at real positions, 0 at pads and guard rows. */
 int dbk_tr_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead, const float* pi, void* out, void* stream);
 int dbk_tr_pack_dgrad_weights(const float* w, void* out, void* stream);
-int dbk_tr_dgrad(const void* packed, int64_t rows_alloc, int32_t lead, int32_t n_tiles, const int32_t* tile_row0,
-                 const int32_t* tile_lo, const int32_t* tile_hi, const int32_t* tile_fn, const void* const* wpack,
-                 const float* mask, const float* resid, float* out, int32_t sms, void* stream);
+/* fp16 variant (f16 != 0 in dbk_tr_dgrad): dA packed by dbk_tr_pack_sw128h
+ * with its absmax scale, weights by dbk_tr_pack_dgrad_weights_h (9 × 2 blocks) */
+int dbk_tr_pack_dgrad_weights_h(const float* w, void* out, void* stream);
+int dbk_tr_dgrad(const void* packed, int32_t f16, const uint32_t* absmax, int64_t rows_alloc, int32_t lead,
+                 int32_t n_tiles, const int32_t* tile_row0, const int32_t* tile_lo, const int32_t* tile_hi,
+                 const int32_t* tile_fn, const void* const* wpack, const float* mask, const float* resid, float* out,
+                 int32_t sms, void* stream);
 /* Weight gradient of a 3×3 conv (bwd_conv.cu): items [4][item_stride] = K
  * range [k0, k1) of PI rows (multiples of 16, inside one call group or its
  * zero guard rows), kernel row dr, function; gw[function] += Σ x[r + s_t] ⊗

@@ -47,12 +47,23 @@ void cublas_check(cublasStatus_t st, const char* what) {
 
 // TF32 tensor cores (default) or full fp32 (DYNBATCH_TRAIN_FP32=1, A/B of the
 // backward's rounding).
-// Data gradients of the 3×3 convs: the tf32 implicit GEMM (bwd_conv.cu,
-// default) or cuBLAS on the im2col layout + col2im (DYNBATCH_TRAIN_DGRAD=0).
+// Gradients of the 3×3 convs: the implicit GEMMs of bwd_conv.cu (default) or
+// cuBLAS on the im2col layout + col2im (DYNBATCH_TRAIN_DGRAD=0).
 bool implicit_dgrad() {
   static const bool on = [] {
     const char* e = std::getenv("DYNBATCH_TRAIN_DGRAD");
     return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Operands of the implicit data gradient: fp16 (dA scaled from its max, the
+// pack shared with the weight gradient; default) or tf32 (fp32 rows,
+// DYNBATCH_TRAIN_DGRAD_TF32=1).
+bool dgrad_f16() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYNBATCH_TRAIN_DGRAD_TF32");
+    return !(e && std::atoi(e) != 0);
   }();
   return on;
 }
@@ -166,11 +177,13 @@ void IepSession::set_training(bool on) {
   std::vector<const void*> tab1(p, nullptr), tab2(p, nullptr);
   for (size_t f = 0; f < p; ++f) {
     if (t->arity[f] == 0) continue;
-    constexpr size_t kBytes = 9 * 4 * 16384;
-    t->wd1[f].alloc(kBytes);
-    t->wd2[f].alloc(kBytes);
-    check(dbk_tr_pack_dgrad_weights(t->w1[f].get(), t->wd1[f].get(), stream_), "dgrad weights");
-    check(dbk_tr_pack_dgrad_weights(t->w2[f].get(), t->wd2[f].get(), stream_), "dgrad weights");
+    const bool h = dgrad_f16();
+    const size_t bytes = static_cast<size_t>(9) * (h ? 2 : 4) * 16384;
+    t->wd1[f].alloc(bytes);
+    t->wd2[f].alloc(bytes);
+    const auto pack = h ? dbk_tr_pack_dgrad_weights_h : dbk_tr_pack_dgrad_weights;
+    check(pack(t->w1[f].get(), t->wd1[f].get(), stream_), "dgrad weights");
+    check(pack(t->w2[f].get(), t->wd2[f].get(), stream_), "dgrad weights");
     tab1[f] = t->wd1[f].get();
     tab2[f] = t->wd2[f].get();
   }
@@ -427,20 +440,27 @@ void IepSession::backward(float* loss_dev) {
   const int sms = sm_count();
   // data gradient of one 3×3 conv over the step's PI rows (the dA operand
   // packed first); mask / resid as the col2im it replaces
+  const bool f16 = dgrad_f16();
+  // dA (PI rows) → fp16 rows scaled from its max, for both implicit GEMMs
+  auto pack_da_h = [&](const float* da, std::int64_t rows) {
+    check(dbk_tr_absmax(rows * kC, da, T.absmax.get(), s), "dA max");
+    check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, da, T.absmax.get(), T.hpack.get(), s), "pack dA");
+  };
   auto dgrad_conv = [&](int st, const float* da, const Buf<const void*>& wtab, const float* mask, const float* resid,
                         float* out, std::int64_t rows) {
-    check(dbk_tr_pack_sw128f(rows, T.dpack_rows, 16, da, T.dpack.get(), s), "pack dA");
+    if (f16) pack_da_h(da, rows);
+    else check(dbk_tr_pack_sw128f(rows, T.dpack_rows, 16, da, T.dpack.get(), s), "pack dA");
     const std::int64_t t0 = tile_off[static_cast<size_t>(st)], nt = tile_off[static_cast<size_t>(st) + 1] - t0;
     const std::int32_t* tb = T.dtiles.get();
-    check(dbk_tr_dgrad(T.dpack.get(), T.dpack_rows, 16, static_cast<std::int32_t>(nt), tb + t0, tb + n_tiles_all + t0,
-                       tb + 2 * n_tiles_all + t0, tb + 3 * n_tiles_all + t0, wtab.get(), mask, resid, out, sms, s),
+    check(dbk_tr_dgrad(f16 ? T.hpack.get() : T.dpack.get(), f16 ? 1 : 0, T.absmax.get(), T.dpack_rows, 16,
+                       static_cast<std::int32_t>(nt), tb + t0, tb + n_tiles_all + t0, tb + 2 * n_tiles_all + t0,
+                       tb + 3 * n_tiles_all + t0, wtab.get(), mask, resid, out, sms, s),
           "dgrad");
   };
   // weight gradient of one 3×3 conv: its input activations and dA, both PI
-  // rows, packed to fp16 here (dA scaled into fp16's normal range)
+  // rows; dA's fp16 pack is dgrad_conv's when that ran on fp16
   auto wgrad_conv = [&](int st, const float* act, const float* da, const Buf<float*>& gwtab, std::int64_t rows) {
-    check(dbk_tr_absmax(rows * kC, da, T.absmax.get(), s), "dA max");
-    check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, da, T.absmax.get(), T.hpack.get(), s), "pack dA");
+    if (!f16) pack_da_h(da, rows);
     check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, act, nullptr, T.apack.get(), s), "pack activations");
     const std::int64_t i0 = item_off[static_cast<size_t>(st)], ni = item_off[static_cast<size_t>(st) + 1] - i0;
     check(dbk_tr_wgrad(T.apack.get(), T.hpack.get(), T.absmax.get(), T.dpack_rows, 16, static_cast<std::int32_t>(ni),

@@ -40,7 +40,6 @@ constexpr int kSlot = kWin * 128;        // 36 KB: one 32-channel chunk of the w
 constexpr int kSlots = 4;
 constexpr int kStage = 128 * 128;        // 16 KB weight block: 128 ci × 32 co fp32
 constexpr int kStages = 4;
-constexpr int kChunks = kC / 32;         // K chunks of 32 channels
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (2 + kEpiWarps + 1) * 32;  // producer, MMA, epilogue × 8, weights
 constexpr int kSmem = kSlots * kSlot + kStages * kStage + 256;
@@ -82,6 +81,13 @@ __device__ __forceinline__ void transpose8(float* x, int e) {
   }
 }
 
+// dA scale from |dA|max (bit pattern of a non-negative float): the largest
+// power of two keeping it ≤ 2^14 (1 when dA is all zero).
+__device__ __forceinline__ float grad_scale(const uint32_t* absmax_bits) {
+  const float m = __uint_as_float(*absmax_bits);
+  return m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
+}
+
 struct DgradParams {
   const uint8_t* src;   // packed dA: [4 chunks][rows_alloc][128 B], row 0 = PI row −lead
   int64_t rows_alloc;   // rows per chunk plane
@@ -95,9 +101,15 @@ struct DgradParams {
   const float* mask;    // PI [rows][128]: output ⊙ (mask > 0), or null
   const float* resid;   // PI [rows][128]: output + resid, or null
   float* out;           // PI [rows][128]
+  const uint32_t* absmax;  // F16: |dA| max (float bits), the operand scale
 };
 
+// F16: dA packed to fp16 (64 channels per 128-byte row, 2 K chunks, scaled by
+// absmax's power of two) with fp16 transposed weights, kind::f16; else fp32
+// rows of 32 channels (4 chunks), kind::tf32.
+template <bool F16>
 __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant__ DgradParams P) {
+  constexpr int kChunks = F16 ? 2 : 4;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;                      // window chunks
   uint8_t* sW = smem + kSlots * kSlot;     // weight blocks
@@ -146,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------ MMA issuer
-      constexpr uint32_t IDESC = idesc_tf32_f32(128, kTM);
+      constexpr uint32_t IDESC = F16 ? idesc_f16_f32(128, kTM) : idesc_tf32_f32(128, kTM);
       const uint32_t a_base = smem_u32(sA), w_base = smem_u32(sW);
       uint32_t ai = 0, wi = 0;
       int n = 0;
@@ -168,7 +180,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
             for (int kk = 0; kk < 4; ++kk) {
               const uint64_t wd = smem_desc_sw128(w_base + sw * kStage + kk * 32);
               const uint64_t xd = smem_desc_sw128(a_base + sa * kSlot + row * 128 + kk * 32);
-              mma_tf32(tmem_base + abuf * kTM, wd, xd, IDESC, acc);
+              if (F16) mma_bf16(tmem_base + abuf * kTM, wd, xd, IDESC, acc);
+              else mma_tf32(tmem_base + abuf * kTM, wd, xd, IDESC, acc);
               acc = 1;
             }
             mma_commit(w_empty + sw);
@@ -196,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
     const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int g = lane >> 3, e = lane & 7;
     const int plane = quarter * 4 + g;  // 8 channels: ci = 8·plane + k
+    const float inv = F16 ? 1.f / grad_scale(P.absmax) : 1.f;
     int n = 0;
     for (int32_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, ++n) {
       const int abuf = n & 1;
@@ -211,6 +225,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
         for (int m = 0; m < 2; ++m) {
           float* x = v + 8 * m;
           transpose8(x, e);
+          if (F16) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[k] *= inv;
+          }
           const int32_t r = row0 + half * (kTM / 2) + cb * 16 + 8 * m + e;
           if (r < lo || r >= hi) continue;
           const int32_t local = r % kPI;
@@ -280,6 +298,7 @@ __global__ void k_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead, co
 
 // one thread per 16-byte piece: 9 taps × 4 chunks × 128 rows (ci) × 8 pieces
 __global__ void k_pack_dgrad_w(const float* __restrict__ w, uint8_t* __restrict__ out) {
+  constexpr int kChunks = 4;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 9 * kChunks * 128 * 8) return;
   const int j = i & 7, ci = (i >> 3) & 127, blk = i >> 10;  // blk = tap · 4 + chunk
@@ -287,6 +306,21 @@ __global__ void k_pack_dgrad_w(const float* __restrict__ w, uint8_t* __restrict_
   const float* src = w + (static_cast<int64_t>(tap) * kC + ci) * kC + c * 32 + 4 * j;
   *reinterpret_cast<float4*>(out + static_cast<int64_t>(blk) * kStage + ci * 128 + ((j ^ (ci & 7)) << 4)) =
       *reinterpret_cast<const float4*>(src);
+}
+
+// fp16 version: 9 taps × 2 chunks of 64 co, row ci = 128 B of 8 pieces of 8 co.
+__global__ void k_pack_dgrad_wh(const float* __restrict__ w, uint8_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 9 * 2 * 128 * 8) return;
+  const int j = i & 7, ci = (i >> 3) & 127, blk = i >> 10;  // blk = tap · 2 + chunk
+  const int tap = blk / 2, c = blk % 2;
+  const float* src = w + (static_cast<int64_t>(tap) * kC + ci) * kC + c * 64 + 8 * j;
+  uint4 h;
+  h.x = pack_f16x2(src[0], src[1]);
+  h.y = pack_f16x2(src[2], src[3]);
+  h.z = pack_f16x2(src[4], src[5]);
+  h.w = pack_f16x2(src[6], src[7]);
+  *reinterpret_cast<uint4*>(out + static_cast<int64_t>(blk) * kStage + ci * 128 + ((j ^ (ci & 7)) << 4)) = h;
 }
 
 
@@ -321,13 +355,6 @@ __device__ __forceinline__ uint64_t smem_desc_mn128(uint32_t saddr, uint32_t lbo
   d |= static_cast<uint64_t>(1) << 46;                    // descriptor version (sm_100)
   d |= static_cast<uint64_t>(2) << 61;                    // SWIZZLE_128B
   return d;
-}
-
-// dA scale from |dA|max (bit pattern of a non-negative float): the largest
-// power of two keeping it ≤ 2^14 (1 when dA is all zero).
-__device__ __forceinline__ float grad_scale(const uint32_t* absmax_bits) {
-  const float m = __uint_as_float(*absmax_bits);
-  return m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
 }
 
 struct WgradParams {
@@ -509,17 +536,18 @@ extern "C" int dbk_tr_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead
   return static_cast<int>(cudaGetLastError());
 }
 
-extern "C" int dbk_tr_dgrad(const void* packed, int64_t rows_alloc, int32_t lead, int32_t n_tiles,
-                            const int32_t* tile_row0, const int32_t* tile_lo, const int32_t* tile_hi,
-                            const int32_t* tile_fn, const void* const* wpack, const float* mask, const float* resid,
-                            float* out, int32_t sms, void* stream) {
+extern "C" int dbk_tr_dgrad(const void* packed, int32_t f16, const uint32_t* absmax, int64_t rows_alloc,
+                            int32_t lead, int32_t n_tiles, const int32_t* tile_row0, const int32_t* tile_lo,
+                            const int32_t* tile_hi, const int32_t* tile_fn, const void* const* wpack, const float* mask,
+                            const float* resid, float* out, int32_t sms, void* stream) {
   if (n_tiles <= 0) return 0;
   static std::atomic<uint64_t> configured{0};  // per device, once
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
   if (!(configured.load(std::memory_order_acquire) & bit)) {
-    cudaFuncSetAttribute(k_tr_dgrad, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_tr_dgrad<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_tr_dgrad<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     configured.fetch_or(bit, std::memory_order_release);
   }
   DgradParams p;
@@ -535,8 +563,10 @@ extern "C" int dbk_tr_dgrad(const void* packed, int64_t rows_alloc, int32_t lead
   p.mask = mask;
   p.resid = resid;
   p.out = out;
-  k_tr_dgrad<<<static_cast<unsigned>(std::min(n_tiles, std::max(sms, 1))), kThreads, kSmem,
-               static_cast<cudaStream_t>(stream)>>>(p);
+  p.absmax = absmax;
+  const unsigned grid = static_cast<unsigned>(std::min(n_tiles, std::max(sms, 1)));
+  if (f16) k_tr_dgrad<true><<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(p);
+  else k_tr_dgrad<false><<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(p);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -544,7 +574,13 @@ extern "C" int dbk_tr_dgrad(const void* packed, int64_t rows_alloc, int32_t lead
 // input-major fp32 weights w[(tap·C + ci)·C + co] (= W_tap[co][ci]): block
 // (tap, chunk c) row ci holds co = 32c .. 32c + 31, swizzled like the windows.
 extern "C" int dbk_tr_pack_dgrad_weights(const float* w, void* out, void* stream) {
-  k_pack_dgrad_w<<<9 * kChunks * 128 * 8 / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  k_pack_dgrad_w<<<9 * 4 * 128 * 8 / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      w, static_cast<uint8_t*>(out));
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_pack_dgrad_weights_h(const float* w, void* out, void* stream) {
+  k_pack_dgrad_wh<<<9 * 2 * 128 * 8 / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       w, static_cast<uint8_t*>(out));
   return static_cast<int>(cudaGetLastError());
 }
