@@ -217,8 +217,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
       tc_fence_after();
       const int32_t row0 = P.tile_row0[t], lo = P.tile_lo[t], hi = P.tile_hi[t];
       const uint32_t taddr = tmem_base + abuf * kTM + (static_cast<uint32_t>(quarter * 32) << 16) + half * (kTM / 2);
+      // the mask (mid) or residual rows of the next 16-position chunk are
+      // loaded while this chunk is transposed and stored (they are the
+      // epilogue's only reads; issued just before use they stall it)
+      const float* aux = P.mask ? P.mask : P.resid;
+      const bool is_mask = P.mask != nullptr;
+      auto row_of = [&](int cb, int m) { return row0 + half * (kTM / 2) + cb * 16 + 8 * m + e; };
+      auto real_row = [&](int32_t r) {
+        if (r < lo || r >= hi) return false;
+        const int32_t p = r % kPI - kPIG;
+        return p >= 0 && p < 225 && p / 15 < 14 && p % 15 < 14;
+      };
+      float4 nxt[4];
+      auto load_aux = [&](int cb) {
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int32_t r = row_of(cb, m);
+          nxt[2 * m] = nxt[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (aux && real_row(r)) {
+            const float4* a = reinterpret_cast<const float4*>(aux + static_cast<int64_t>(r) * kC + plane * 8);
+            nxt[2 * m] = __ldg(a);
+            nxt[2 * m + 1] = __ldg(a + 1);
+          }
+        }
+      };
+      load_aux(0);
 #pragma unroll 1
       for (int cb = 0; cb < kTM / 2 / 16; ++cb) {
+        float4 cur[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+        if (cb + 1 < kTM / 2 / 16) load_aux(cb + 1);
         float v[16];
         tmem_ld16(taddr + cb * 16, v);
 #pragma unroll
@@ -229,30 +258,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
 #pragma unroll
             for (int k = 0; k < 8; ++k) x[k] *= inv;
           }
-          const int32_t r = row0 + half * (kTM / 2) + cb * 16 + 8 * m + e;
+          const int32_t r = row_of(cb, m);
           if (r < lo || r >= hi) continue;
-          const int32_t local = r % kPI;
-          const int32_t p = local - kPIG;
-          const bool real = p >= 0 && p < 225 && p / 15 < 14 && p % 15 < 14;
+          const float au[8] = {cur[2 * m].x, cur[2 * m].y, cur[2 * m].z, cur[2 * m].w,
+                               cur[2 * m + 1].x, cur[2 * m + 1].y, cur[2 * m + 1].z, cur[2 * m + 1].w};
           float o[8];
-          if (real) {
-            const int64_t off = static_cast<int64_t>(r) * kC + plane * 8;
-            if (P.mask) {
-              const float4 a = *reinterpret_cast<const float4*>(P.mask + off);
-              const float4 b = *reinterpret_cast<const float4*>(P.mask + off + 4);
-              const float mk[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+          if (real_row(r)) {
 #pragma unroll
-              for (int k = 0; k < 8; ++k) o[k] = mk[k] > 0.f ? x[k] : 0.f;
-            } else {
-#pragma unroll
-              for (int k = 0; k < 8; ++k) o[k] = x[k];
-            }
-            if (P.resid) {
-              const float4 a = *reinterpret_cast<const float4*>(P.resid + off);
-              const float4 b = *reinterpret_cast<const float4*>(P.resid + off + 4);
-              o[0] += a.x; o[1] += a.y; o[2] += a.z; o[3] += a.w;
-              o[4] += b.x; o[5] += b.y; o[6] += b.z; o[7] += b.w;
-            }
+            for (int k = 0; k < 8; ++k) o[k] = is_mask ? (au[k] > 0.f ? x[k] : 0.f) : (aux ? x[k] + au[k] : x[k]);
           } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) o[k] = 0.f;
