@@ -219,8 +219,9 @@ int dbk_tr_stage_to_pi(int32_t n, const int64_t* rows, const void* hi, const voi
                        int32_t planes, float* out, void* stream);
 /* bias gradients of 128 channels: slab i = rows [slab_row[2i], slab_row[2i+1]) into dst[i] */
 int dbk_tr_colsum_seg(int32_t slabs, const int64_t* slab_row, float* const* dst, const float* a, void* stream);
+/* absmax (nullable): atomicMax of |DA2| (float bits) for the fp16 gradient scale */
 int dbk_tr_da_out(int32_t n, const int32_t* nodes, const float* dy_nodes, const float* values, float* out,
-                  void* stream);
+                  uint32_t* absmax, void* stream);
 int dbk_tr_im2col(int64_t rows, int32_t ch, const float* x, float* cols, void* stream);
 int dbk_tr_col2im(int32_t n, int32_t ch, const float* g, const float* res, const float* mask, float* out,
                   void* stream);
@@ -247,7 +248,7 @@ int dbk_tr_pack_dgrad_weights_h(const float* w, void* out, void* stream);
 int dbk_tr_dgrad(const void* packed, int32_t f16, const uint32_t* absmax, int64_t rows_alloc, int32_t lead,
                  int32_t n_tiles, const int32_t* tile_row0, const int32_t* tile_lo, const int32_t* tile_hi,
                  const int32_t* tile_fn, const void* const* wpack, const float* mask, const float* resid, float* out,
-                 int32_t sms, void* stream);
+                 uint32_t* out_absmax, int32_t sms, void* stream);
 /* Weight gradient of a 3×3 conv (bwd_conv.cu): items [4][item_stride] = K
  * range [k0, k1) of PI rows (multiples of 16, inside one call group or its
  * zero guard rows), kernel row dr, function; gw[function] += Σ x[r + s_t] ⊗

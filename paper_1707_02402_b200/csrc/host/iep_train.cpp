@@ -433,7 +433,7 @@ void IepSession::backward(float* loss_dev) {
       T.hpack.alloc(static_cast<size_t>(2 * need_rows * 128));
       T.dpack_rows = need_rows;
     }
-    T.absmax.ensure(1);
+    T.absmax.ensure(2);  // |dA2|, |dA1| maxima of the step (the fp16 scales)
   }
   const std::int64_t n_items_all = item_off[static_cast<size_t>(S)];
   const std::int64_t n_tiles_all = tile_off[static_cast<size_t>(S)];
@@ -442,28 +442,33 @@ void IepSession::backward(float* loss_dev) {
   // packed first); mask / resid as the col2im it replaces
   const bool f16 = dgrad_f16();
   // dA (PI rows) → fp16 rows scaled from its max, for both implicit GEMMs
-  auto pack_da_h = [&](const float* da, std::int64_t rows) {
-    check(dbk_tr_absmax(rows * kC, da, T.absmax.get(), s), "dA max");
-    check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, da, T.absmax.get(), T.hpack.get(), s), "pack dA");
+  // dA (PI rows) → fp16 rows scaled from its max (word `mx` of T.absmax:
+  // 0 = dA2, written by da_out; 1 = dA1, by the conv3x3 #2 data gradient,
+  // or here with k_absmax on the tf32 path), for both implicit GEMMs
+  std::uint32_t* amax = T.absmax.get();
+  auto pack_da_h = [&](const float* da, std::int64_t rows, int mx, bool measure) {
+    if (measure) check(dbk_tr_absmax(rows * kC, da, amax + mx, s), "dA max");
+    check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, da, amax + mx, T.hpack.get(), s), "pack dA");
   };
-  auto dgrad_conv = [&](int st, const float* da, const Buf<const void*>& wtab, const float* mask, const float* resid,
-                        float* out, std::int64_t rows) {
-    if (f16) pack_da_h(da, rows);
+  auto dgrad_conv = [&](int st, const float* da, int mx, const Buf<const void*>& wtab, const float* mask,
+                        const float* resid, float* out, std::uint32_t* out_max, std::int64_t rows) {
+    if (f16) pack_da_h(da, rows, mx, false);
     else check(dbk_tr_pack_sw128f(rows, T.dpack_rows, 16, da, T.dpack.get(), s), "pack dA");
     const std::int64_t t0 = tile_off[static_cast<size_t>(st)], nt = tile_off[static_cast<size_t>(st) + 1] - t0;
     const std::int32_t* tb = T.dtiles.get();
-    check(dbk_tr_dgrad(f16 ? T.hpack.get() : T.dpack.get(), f16 ? 1 : 0, T.absmax.get(), T.dpack_rows, 16,
+    check(dbk_tr_dgrad(f16 ? T.hpack.get() : T.dpack.get(), f16 ? 1 : 0, amax + mx, T.dpack_rows, 16,
                        static_cast<std::int32_t>(nt), tb + t0, tb + n_tiles_all + t0, tb + 2 * n_tiles_all + t0,
-                       tb + 3 * n_tiles_all + t0, wtab.get(), mask, resid, out, sms, s),
+                       tb + 3 * n_tiles_all + t0, wtab.get(), mask, resid, out, out_max, sms, s),
           "dgrad");
   };
   // weight gradient of one 3×3 conv: its input activations and dA, both PI
   // rows; dA's fp16 pack is dgrad_conv's when that ran on fp16
-  auto wgrad_conv = [&](int st, const float* act, const float* da, const Buf<float*>& gwtab, std::int64_t rows) {
-    if (!f16) pack_da_h(da, rows);
+  auto wgrad_conv = [&](int st, const float* act, const float* da, int mx, const Buf<float*>& gwtab,
+                        std::int64_t rows) {
+    if (!f16) pack_da_h(da, rows, mx, true);
     check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, act, nullptr, T.apack.get(), s), "pack activations");
     const std::int64_t i0 = item_off[static_cast<size_t>(st)], ni = item_off[static_cast<size_t>(st) + 1] - i0;
-    check(dbk_tr_wgrad(T.apack.get(), T.hpack.get(), T.absmax.get(), T.dpack_rows, 16, static_cast<std::int32_t>(ni),
+    check(dbk_tr_wgrad(T.apack.get(), T.hpack.get(), amax + mx, T.dpack_rows, 16, static_cast<std::int32_t>(ni),
                        T.witems.get() + i0, n_items_all, gwtab.get(), sms, s),
           "wgrad");
   };
@@ -538,12 +543,15 @@ void IepSession::backward(float* loss_dev) {
     check(cudaMemsetAsync(T.mid.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
     check(cudaMemsetAsync(T.xin.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
     // conv3x3 #2: da2 → dW2, db2; da1 = col2im(da2·W2ᵀ) ⊙ (mid > 0)
-    check(dbk_tr_da_out(static_cast<std::int32_t>(n), nodes, T.dy_nodes.get(), R.values.get(), T.da2.get(), s), "da2");
+    if (dgrad) check(cudaMemsetAsync(amax, 0, 2 * sizeof(std::uint32_t), s), "maxima");
+    check(dbk_tr_da_out(static_cast<std::int32_t>(n), nodes, T.dy_nodes.get(), R.values.get(), T.da2.get(),
+                        dgrad ? amax : nullptr, s),
+          "da2");
     colsum(slabs[static_cast<size_t>(st)][0], T.da2.get());
     check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_mid.get(), nullptr, ps, 0, 16, mid, s), "mid");
     if (dgrad) {
-      dgrad_conv(st, T.da2.get(), T.wd2tab, mid, nullptr, T.da1.get(), rows);
-      wgrad_conv(st, mid, T.da2.get(), T.gw2tab, rows);
+      dgrad_conv(st, T.da2.get(), 0, T.wd2tab, mid, nullptr, T.da1.get(), f16 ? amax + 1 : nullptr, rows);
+      wgrad_conv(st, mid, T.da2.get(), 0, T.gw2tab, rows);
     } else {
       check(dbk_tr_im2col(rows, kC, mid, T.cols.get(), s), "im2col mid");
       gemms(0);
@@ -555,8 +563,8 @@ void IepSession::backward(float* loss_dev) {
     check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_x.get(), R.stage_lo.get(), ps, 0, 16, xin, s),
           "x");
     if (dgrad) {
-      dgrad_conv(st, T.da1.get(), T.wd1tab, nullptr, T.da2.get(), T.dx.get(), rows);
-      wgrad_conv(st, xin, T.da1.get(), T.gw1tab, rows);
+      dgrad_conv(st, T.da1.get(), 1, T.wd1tab, nullptr, T.da2.get(), T.dx.get(), nullptr, rows);
+      wgrad_conv(st, xin, T.da1.get(), 1, T.gw1tab, rows);
     } else {
       check(dbk_tr_im2col(rows, kC, xin, T.cols.get(), s), "im2col x");
       gemms(2);

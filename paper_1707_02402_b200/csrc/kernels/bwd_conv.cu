@@ -102,6 +102,7 @@ struct DgradParams {
   const float* resid;   // PI [rows][128]: output + resid, or null
   float* out;           // PI [rows][128]
   const uint32_t* absmax;  // F16: |dA| max (float bits), the operand scale
+  uint32_t* out_absmax;    // |out| max (float bits, atomicMax), or null
 };
 
 // F16: dA packed to fp16 (64 channels per 128-byte row, 2 K chunks, scaled by
@@ -242,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
         }
       };
       load_aux(0);
+      float omax = 0.f;
 #pragma unroll 1
       for (int cb = 0; cb < kTM / 2 / 16; ++cb) {
         float4 cur[4];
@@ -273,7 +275,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
           float4* dst = reinterpret_cast<float4*>(P.out + static_cast<int64_t>(r) * kC + plane * 8);
           dst[0] = make_float4(o[0], o[1], o[2], o[3]);
           dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) omax = fmaxf(omax, fabsf(o[k]));
         }
+      }
+      if (P.out_absmax) {  // the next gradient's fp16 scale
+        for (int o = 16; o; o >>= 1) omax = fmaxf(omax, __shfl_xor_sync(0xffffffffu, omax, o));
+        if (lane == 0 && omax > 0.f) atomicMax(P.out_absmax, __float_as_uint(omax));
       }
       tc_fence_before();
       mbar_arrive(acc_empty + abuf);
@@ -552,7 +560,7 @@ extern "C" int dbk_tr_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead
 extern "C" int dbk_tr_dgrad(const void* packed, int32_t f16, const uint32_t* absmax, int64_t rows_alloc,
                             int32_t lead, int32_t n_tiles, const int32_t* tile_row0, const int32_t* tile_lo,
                             const int32_t* tile_hi, const int32_t* tile_fn, const void* const* wpack, const float* mask,
-                            const float* resid, float* out, int32_t sms, void* stream) {
+                            const float* resid, float* out, uint32_t* out_absmax, int32_t sms, void* stream) {
   if (n_tiles <= 0) return 0;
   static std::atomic<uint64_t> configured{0};  // per device, once
   int dev = 0;
@@ -577,6 +585,7 @@ extern "C" int dbk_tr_dgrad(const void* packed, int32_t f16, const uint32_t* abs
   p.resid = resid;
   p.out = out;
   p.absmax = absmax;
+  p.out_absmax = out_absmax;
   const unsigned grid = static_cast<unsigned>(std::min(n_tiles, std::max(sms, 1)));
   if (f16) k_tr_dgrad<true><<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(p);
   else k_tr_dgrad<false><<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(p);

@@ -79,7 +79,8 @@ __global__ void k_stage_to_pi(int32_t n, const int64_t* __restrict__ rows, const
 // and guard rows 0: shifted reads of the data gradient and the weight
 // gradients' K range cover them).
 __global__ void k_da_out(int32_t n, const int32_t* __restrict__ nodes, const float* __restrict__ dy_nodes,
-                         const float* __restrict__ values, float* __restrict__ out) {
+                         const float* __restrict__ values, float* __restrict__ out, uint32_t* __restrict__ absmax) {
+  float mx = 0.f;
   const int64_t total = static_cast<int64_t>(n) * kPI * 16;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -101,6 +102,13 @@ __global__ void k_da_out(int32_t n, const int32_t* __restrict__ nodes, const flo
     float4* o = reinterpret_cast<float4*>(out + (static_cast<int64_t>(k) * kPI + kPIG + p) * kC + j * 8);
     o[0] = a;
     o[1] = b;
+    mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))),
+                         fmaxf(fmaxf(fabsf(b.x), fabsf(b.y)), fmaxf(fabsf(b.z), fabsf(b.w)))));
+  }
+  // |DA2| max for the fp16 operand scale of the implicit-GEMM gradients
+  if (absmax) {
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(absmax, __float_as_uint(mx));
   }
 }
 
@@ -380,10 +388,10 @@ extern "C" int dbk_tr_colsum_seg(int32_t slabs, const int64_t* slab_row, float* 
 }
 
 extern "C" int dbk_tr_da_out(int32_t n, const int32_t* nodes, const float* dy_nodes, const float* values,
-                             float* out, void* stream) {
+                             float* out, uint32_t* absmax, void* stream) {
   const int64_t total = static_cast<int64_t>(n) * kPI * 16;
   if (total <= 0) return 0;
-  k_da_out<<<grid_for(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, nodes, dy_nodes, values, out);
+  k_da_out<<<grid_for(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, nodes, dy_nodes, values, out, absmax);
   return static_cast<int>(cudaGetLastError());
 }
 
