@@ -260,6 +260,12 @@ int dbk_tr_pack_sw128h(int64_t rows, int64_t rows_alloc, int32_t lead, const flo
 int dbk_tr_wgrad(const void* x_packed, const void* da_packed, const uint32_t* absmax, int64_t rows_alloc, int32_t lead,
                  int32_t n_items, const int32_t* items, int64_t item_stride, float* const* gw, int32_t sms,
                  void* stream);
+/* SGD update and the forward's weight layouts rebuilt from fp32 masters:
+ * w -= lr·g; the step kernel's fp16 blocks (pack_blocks layout); the grouped
+ * GEMM's fp16 B tiles of a K × N_src matrix padded to N columns. */
+int dbk_tr_sgd(int64_t n, float* w, const float* g, float lr, void* stream);
+int dbk_tr_pack_conv_weights(const float* w, int32_t cin, int32_t taps, void* out, void* stream);
+int dbk_tr_tile_weights(const float* w, int32_t K, int32_t N_src, int32_t N, void* out, void* stream);
 int dbk_tr_unpack_h(int64_t rows, int32_t K, const void* h, float* out, void* stream);
 int dbk_tr_unpack_sw128(int64_t rows, int32_t K, const void* a, float* out, void* stream);
 int dbk_tr_pool_bwd(int64_t b, int32_t P, const float* proj, const float* dpooled, float* dproj, void* stream);

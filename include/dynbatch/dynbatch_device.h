@@ -179,6 +179,10 @@ DYNBATCH_API db_status db_iep_session_set_training(db_iep_session* s, int32_t on
 DYNBATCH_API db_status db_iep_session_train_step(db_iep_session* s, const int32_t* labels, float* loss);
 DYNBATCH_API db_status db_iep_session_grad_size(db_iep_session* s, int32_t which, int32_t fid, int64_t* n);
 DYNBATCH_API db_status db_iep_session_grad(db_iep_session* s, int32_t which, int32_t fid, float* out, int64_t n);
+/* SGD with the last train_step's gradients: every module weight and bias and
+ * the head's, w -= lr·g on fp32 masters, then the forward's fp16 operand
+ * layouts rebuilt on the device (the next forward / train_step uses them). */
+DYNBATCH_API db_status db_iep_session_sgd(db_iep_session* s, float lr);
 DYNBATCH_API db_status db_iep_session_time_train(db_iep_session* s, int32_t iters, const int32_t* labels,
                                                  double* ms);
 DYNBATCH_API void db_iep_session_free(db_iep_session* s);

@@ -163,6 +163,7 @@ SIGNATURES = {
     "db_iep_session_grad_size": (C.c_int32, [VP, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
     "db_iep_session_grad": (C.c_int32, [VP, C.c_int32, C.c_int32, VP, C.c_int64]),
     "db_iep_session_time_train": (C.c_int32, [VP, C.c_int32, VP, C.POINTER(C.c_double)]),
+    "db_iep_session_sgd": (C.c_int32, [VP, C.c_float]),
     "db_iep_session_free": (None, [VP]),
     "db_execute_device": (C.c_int32, [VP, VP, C.c_uint64, C.POINTER(ModuleOpts), PVP]),
     "db_moe_session_create": (C.c_int32, [C.POINTER(MoeOpts), C.c_int32, C.c_int64, C.c_int64,
@@ -541,6 +542,11 @@ class IepSession(_Handle):
         ms = C.c_double()
         check(lib().db_iep_session_time_train(self.h, iters, _ptr(lab), C.byref(ms)))
         return ms.value
+
+    def sgd(self, lr: float):
+        """w -= lr·grad for every module and head weight and bias, with the
+        last train_step's gradients; the next forward uses the new weights."""
+        check(lib().db_iep_session_sgd(self.h, float(lr)))
 
     def time_head(self, iters: int):
         """(device ms per head forward, algorithmic FLOPs per head forward)."""

@@ -593,6 +593,11 @@ db_status db_iep_session_grad(db_iep_session* s, int32_t which, int32_t fid, flo
   return guarded([&] { s->s->download_grad(which, fid, out, n); });
 }
 
+db_status db_iep_session_sgd(db_iep_session* s, float lr) {
+  if (!s) return null_arg();
+  return guarded([&] { s->s->sgd_update(lr); });
+}
+
 db_status db_iep_session_time_train(db_iep_session* s, int32_t iters, const int32_t* labels, double* ms) {
   if (!s || !labels || !ms) return null_arg();
   return guarded([&] { *ms = s->s->time_train(iters, labels); });

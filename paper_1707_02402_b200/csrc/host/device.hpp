@@ -278,6 +278,10 @@ class IepSession {
   void download_grad(int which, int fid, float* out, std::int64_t n);
   std::int64_t grad_size(int which, int fid) const;
   double time_train(int iters, const std::int32_t* labels);
+  // SGD with the last train_step's gradients: every module and head weight
+  // and bias (fp32 masters) w -= lr·g, then the forward's fp16 operand
+  // layouts rebuilt from them on the device.
+  void sgd_update(float lr);
 
  private:
   FunctionVocab vocab_;

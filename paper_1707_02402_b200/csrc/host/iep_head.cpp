@@ -127,6 +127,20 @@ int IepHead::forward(std::int64_t b, const std::int32_t* root_g, const std::int3
   return 5;
 }
 
+void IepHead::sgd(float lr, const float* gwp, const float* gbp, const float* gw1, const float* gb1, const float* gw2,
+                  const float* gb2, cudaStream_t s) {
+  const std::int64_t K1 = 49LL * kP;
+  check(dbk_tr_sgd(static_cast<std::int64_t>(kC) * kP, wp32_.get(), gwp, lr, s), "sgd");
+  check(dbk_tr_sgd(K1 * kF, w132_.get(), gw1, lr, s), "sgd");
+  check(dbk_tr_sgd(static_cast<std::int64_t>(kF) * answers_, w232_.get(), gw2, lr, s), "sgd");
+  check(dbk_tr_sgd(kP, bp_.get(), gbp, lr, s), "sgd");
+  check(dbk_tr_sgd(kF, b1_.get(), gb1, lr, s), "sgd");
+  check(dbk_tr_sgd(answers_, b2_.get(), gb2, lr, s), "sgd");  // the padded logit columns stay 0
+  check(dbk_tr_tile_weights(wp32_.get(), kC, kP, kP, wp_.get(), s), "tile");
+  check(dbk_tr_tile_weights(w132_.get(), static_cast<std::int32_t>(K1), kF, kF, w1_.get(), s), "tile");
+  check(dbk_tr_tile_weights(w232_.get(), kF, answers_, kPad, w2_.get(), s), "tile");
+}
+
 void IepHead::download(std::int64_t b, float* out, cudaStream_t s) const {
   check(cudaMemcpy2DAsync(out, sizeof(float) * answers_, logits_.get(), sizeof(float) * kPad,
                           sizeof(float) * answers_, static_cast<size_t>(b), cudaMemcpyDeviceToHost, s),

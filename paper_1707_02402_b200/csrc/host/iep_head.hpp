@@ -45,6 +45,10 @@ class IepHead {
   const float* wp32() const { return wp32_.get(); }       // [C][P]
   const float* w1_32() const { return w132_.get(); }      // [49P][F]
   const float* w2_32() const { return w232_.get(); }      // [F][answers]
+  // SGD on the head (fp32 masters, then the GEMMs' fp16 tiles rebuilt);
+  // gradients as IepSession::download_grad's head entries
+  void sgd(float lr, const float* gwp, const float* gbp, const float* gw1, const float* gb1, const float* gw2,
+           const float* gb2, cudaStream_t s);
 
  private:
   void size_for(std::int64_t b, cudaStream_t s);

@@ -221,6 +221,7 @@ float IepSession::train_step(const std::int32_t* labels) {
   check_errors();
   head_forward();
   backward(T.loss.get());
+  T.stepped = true;
   float loss = 0.f;
   check(cudaMemcpyAsync(&loss, T.loss.get(), sizeof(float), cudaMemcpyDeviceToHost, stream_), "D2H loss");
   check(cudaStreamSynchronize(stream_), "sync");
@@ -645,6 +646,47 @@ void IepSession::download_grad(int which, int fid, float* out, std::int64_t n) {
   }
   check(cudaMemcpyAsync(out, src, sizeof(float) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, stream_), "D2H");
   check(cudaStreamSynchronize(stream_), "sync");
+}
+
+void IepSession::sgd_update(float lr) {
+  if (!train_) throw_error(Errc::invalid_argument, "training is off: call set_training first");
+  Train& T = *train_;
+  if (!T.stepped) throw_error(Errc::invalid_argument, "no gradients: call train_step first");
+  RB& R = *rb_;
+  cudaStream_t s = stream_;
+  const size_t p = T.arity.size();
+  if (T.fw1.empty()) {
+    T.fw0 = R.w0tab.download(p, s);
+    T.fw1 = R.w1tab.download(p, s);
+    T.fw2 = R.w2tab.download(p, s);
+    T.fb0 = R.b0tab.download(p, s);
+    T.fb1 = R.b1tab.download(p, s);
+    T.fb2 = R.b2tab.download(p, s);
+  }
+  const bool h = dgrad_f16();
+  for (size_t f = 0; f < p; ++f) {
+    const int a = T.arity[f];
+    if (a == 0) continue;
+    const std::int64_t n3 = 9LL * kC * kC;
+    check(dbk_tr_sgd(n3, T.w1[f].get(), T.gw1[f].get(), lr, s), "sgd");
+    check(dbk_tr_sgd(n3, T.w2[f].get(), T.gw2[f].get(), lr, s), "sgd");
+    check(dbk_tr_sgd(kC, const_cast<float*>(T.fb1[f]), T.gb1[f].get(), lr, s), "sgd");
+    check(dbk_tr_sgd(kC, const_cast<float*>(T.fb2[f]), T.gb2[f].get(), lr, s), "sgd");
+    check(dbk_tr_pack_conv_weights(T.w1[f].get(), kC, 9, const_cast<void*>(T.fw1[f]), s), "repack");
+    check(dbk_tr_pack_conv_weights(T.w2[f].get(), kC, 9, const_cast<void*>(T.fw2[f]), s), "repack");
+    if (a == 2) {
+      check(dbk_tr_sgd(2LL * kC * kC, T.w0[f].get(), T.gw0[f].get(), lr, s), "sgd");
+      check(dbk_tr_sgd(kC, const_cast<float*>(T.fb0[f]), T.gb0[f].get(), lr, s), "sgd");
+      check(dbk_tr_pack_conv_weights(T.w0[f].get(), 2 * kC, 1, const_cast<void*>(T.fw0[f]), s), "repack");
+    }
+    if (!T.wd1.empty() && T.wd1[f].get()) {
+      const auto pack = h ? dbk_tr_pack_dgrad_weights_h : dbk_tr_pack_dgrad_weights;
+      check(pack(T.w1[f].get(), T.wd1[f].get(), s), "dgrad weights");
+      check(pack(T.w2[f].get(), T.wd2[f].get(), s), "dgrad weights");
+    }
+  }
+  head_->sgd(lr, T.gwp.get(), T.gbp.get(), T.ghw1.get(), T.ghb1.get(), T.ghw2.get(), T.ghb2.get(), s);
+  check(cudaStreamSynchronize(s), "sgd");
 }
 
 double IepSession::time_train(int iters, const std::int32_t* labels) {

@@ -45,6 +45,11 @@ struct IepSession::Train {
   Buf<std::int32_t> dtiles;  // [4][n]: row0, lo, hi, fn
   Buf<std::int32_t> witems;  // [4][n]: K range k0, k1, kernel row dr, fn
   Buf<float*> gw1tab, gw2tab;
+  // the forward's per-function weight blocks and biases (host copies of the
+  // session's tables, fetched by the first sgd_update)
+  std::vector<const void*> fw0, fw1, fw2;
+  std::vector<const float*> fb0, fb1, fb2;
+  bool stepped = false;  // a train_step ran: gradients exist
   ~Train() {
     if (blas) cublasDestroy(blas);
   }

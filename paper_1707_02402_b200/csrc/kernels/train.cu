@@ -369,6 +369,54 @@ __global__ void k_droots(int64_t b, const int32_t* __restrict__ root_g, const in
   }
 }
 
+
+// ------------------------------------------------------------- SGD update
+// w -= lr · g over n fp32 values.
+__global__ void k_sgd(int64_t n, float* __restrict__ w, const float* __restrict__ g, float lr) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    w[i] -= lr * g[i];
+}
+
+// The step kernel's fp16 weight blocks from fp32 input-major weights
+// w[(tap·cin + ci)·C + co] (the device twin of iep_resblock.cpp pack_blocks):
+// one 16 KB block per (64-channel K chunk, tap), output channel co = the
+// 128-byte row, input channel k (mod 64) in 16-byte slot (k/8) ^ (co & 7).
+__global__ void k_pack_conv_w(const float* __restrict__ w, int32_t cin, int32_t taps, uint16_t* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(taps) * cin * kC;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int co = static_cast<int>(i % kC);
+    const int64_t tc = i / kC;
+    const int ci = static_cast<int>(tc % cin), tap = static_cast<int>(tc / cin);
+    const int chunk = ci / 64, k = ci % 64;
+    const int64_t base = static_cast<int64_t>(chunk * taps + tap) * 64 * kC;
+    const __half h = __float2half_rn(w[(static_cast<int64_t>(tap) * cin + ci) * kC + co]);
+    out[base + co * 64 + ((k / 8) ^ (co & 7)) * 8 + k % 8] = *reinterpret_cast<const uint16_t*>(&h);
+  }
+}
+
+// The grouped GEMM's fp16 B tiles from fp32 input-major weights w[k][n] of K ×
+// N_src, zero-padded to N columns (the device twin of moe_bf16.cpp
+// tile_weights): blocks of 256 columns × 64 K, halves of 128 columns, [8 K
+// groups][128 n][8 k].
+__global__ void k_tile_w(const float* __restrict__ w, int32_t K, int32_t N_src, int32_t N, uint16_t* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(K) * N;
+  const int n_kc = K / 64;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int n = static_cast<int>(i % N);
+    const int kk = static_cast<int>(i / N);
+    const int kc = kk / 64, k8 = (kk % 64) / 8, ke = kk % 8;
+    const int nt = n / 256, half = (n % 256) / 128, nn = n % 128;
+    const int64_t blk = static_cast<int64_t>(nt) * n_kc + kc;
+    const float v = n < N_src ? w[static_cast<int64_t>(kk) * N_src + n] : 0.f;
+    const __half h = __float2half_rn(v);
+    out[blk * 256 * 64 + ((static_cast<int64_t>(half) * 8 + k8) * 128 + nn) * 8 + ke] =
+        *reinterpret_cast<const uint16_t*>(&h);
+  }
+}
+
 }  // namespace
 
 extern "C" int dbk_tr_stage_to_pi(int32_t n, const int64_t* rows, const void* hi, const void* lo, int64_t ps,
@@ -468,5 +516,25 @@ extern "C" int dbk_tr_droots(int64_t b, const int32_t* root_g, const int32_t* fi
   if (b <= 0) return 0;
   k_droots<<<grid_for(b * kPx * kC), 256, 0, static_cast<cudaStream_t>(stream)>>>(b, root_g, fid, arity_of, example,
                                                                                  droots, dy_nodes, d_inputs);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_sgd(int64_t n, float* w, const float* g, float lr, void* stream) {
+  if (n <= 0) return 0;
+  k_sgd<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, w, g, lr);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_pack_conv_weights(const float* w, int32_t cin, int32_t taps, void* out, void* stream) {
+  const int64_t total = static_cast<int64_t>(taps) * cin * kC;
+  k_pack_conv_w<<<grid_for(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(w, cin, taps,
+                                                                              static_cast<uint16_t*>(out));
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_tile_weights(const float* w, int32_t K, int32_t N_src, int32_t N, void* out, void* stream) {
+  const int64_t total = static_cast<int64_t>(K) * N;
+  k_tile_w<<<grid_for(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(w, K, N_src, N,
+                                                                         static_cast<uint16_t*>(out));
   return static_cast<int>(cudaGetLastError());
 }

@@ -157,3 +157,35 @@ def test_train_step_at_cfg1_size():
     s, loss, ref_loss, mod, head, dx = _run("chain", 64, 40, 4, 16, 0.1, 0, answers=28)
     worst = _check_all(s, loss, ref_loss, mod, head, dx)
     assert worst <= TOL_FRO
+
+
+def test_sgd_update_descends_by_the_first_order_prediction():
+    """One SGD step with the device gradients lowers the loss by ≈ lr·‖g‖²
+    (the first-order prediction, over every module and head parameter), and
+    a few steps keep lowering it: the update, the rebuilt fp16 operand
+    layouts and the gradients agree with each other."""
+    kw = dict(batch=6, vocab=10, width=F, length=6, branch_prob=0.4, seed=21)
+    s = db.IepSession(db.Batch.generate("chain", **kw), 31, db.MODULE_RESBLOCK)
+    s.set_head(10, 4)
+    s.set_training(True)
+    labels = np.arange(6, dtype=np.int32) % 10
+    loss0 = s.train_step(labels)
+    g2 = 0.0
+    for f in range(1, 10):
+        for name in NAMES:
+            g = s.grad(name, f).astype(np.float64)
+            g2 += float(np.sum(g * g))
+    for name in ("head_wp", "head_bp", "head_w1", "head_b1", "head_w2", "head_b2"):
+        g = s.grad(name).astype(np.float64)
+        g2 += float(np.sum(g * g))
+    lr = 2e-3 * loss0 / g2  # a 0.2% predicted decrease: first order dominates
+    s.sgd(lr)
+    loss1 = s.train_step(labels)
+    predicted = lr * g2
+    assert loss1 < loss0
+    assert abs((loss0 - loss1) - predicted) <= 0.3 * predicted, (loss0 - loss1, predicted)
+    losses = [loss1]
+    for _ in range(4):
+        s.sgd(0.5)
+        losses.append(s.train_step(labels))
+    assert losses[-1] < losses[0], losses
