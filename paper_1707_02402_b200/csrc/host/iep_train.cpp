@@ -335,8 +335,10 @@ void IepSession::backward(float* loss_dev) {
     T.da2.alloc(r * kC);
     T.mid.alloc(rg * kC);
     T.xin.alloc(rg * kC);
-    T.cols.alloc(r * kK3);
-    T.g.alloc(r * kK3);
+    if (!implicit_dgrad()) {  // the im2col path's 9×-expanded operands (3.4 GB each at cfg3)
+      T.cols.alloc(r * kK3);
+      T.g.alloc(r * kK3);
+    }
     T.da1.alloc(r * kC);
     T.dx.alloc(r * kC);
     T.da0.alloc(r * kC);
@@ -491,14 +493,16 @@ void IepSession::backward(float* loss_dev) {
       const size_t f = static_cast<size_t>(gfid[static_cast<size_t>(sp.groups[gi])]);
       const std::int64_t r0 = sp.first[gi] * kPI;
       const std::int64_t rg = ((gi + 1 < sp.groups.size() ? sp.first[gi + 1] : sp.n) - sp.first[gi]) * kPI;
-      w2.push_back({true, false, kK3, kC, rg, T.cols.get() + r0 * kK3, kK3, T.da2.get() + r0 * kC, kC,
-                    T.gw2[f].get(), kC, 1.f});
-      d2.push_back({false, true, rg, kK3, kC, T.da2.get() + r0 * kC, kC, T.w2[f].get(), kC, T.g.get() + r0 * kK3,
-                    kK3, 0.f});
-      w1.push_back({true, false, kK3, kC, rg, T.cols.get() + r0 * kK3, kK3, T.da1.get() + r0 * kC, kC,
-                    T.gw1[f].get(), kC, 1.f});
-      d1.push_back({false, true, rg, kK3, kC, T.da1.get() + r0 * kC, kC, T.w1[f].get(), kC, T.g.get() + r0 * kK3,
-                    kK3, 0.f});
+      if (!dgrad) {  // the im2col path's GEMMs (the implicit kernels need none)
+        w2.push_back({true, false, kK3, kC, rg, T.cols.get() + r0 * kK3, kK3, T.da2.get() + r0 * kC, kC,
+                      T.gw2[f].get(), kC, 1.f});
+        d2.push_back({false, true, rg, kK3, kC, T.da2.get() + r0 * kC, kC, T.w2[f].get(), kC, T.g.get() + r0 * kK3,
+                      kK3, 0.f});
+        w1.push_back({true, false, kK3, kC, rg, T.cols.get() + r0 * kK3, kK3, T.da1.get() + r0 * kC, kC,
+                      T.gw1[f].get(), kC, 1.f});
+        d1.push_back({false, true, rg, kK3, kC, T.da1.get() + r0 * kC, kC, T.w1[f].get(), kC, T.g.get() + r0 * kK3,
+                      kK3, 0.f});
+      }
       if (r0 >= sp.n_u * kPI) {  // binary group: rows relative to the binary part
         const std::int64_t rb = r0 - sp.n_u * kPI;
         w0.push_back({true, false, 2 * kC, kC, rg, T.cat.get() + rb * 2 * kC, 2 * kC, T.da0.get() + rb * kC, kC,
