@@ -101,3 +101,21 @@ def test_deep_unary_chain():
 def test_left_deep_binary_spine():
     _, out, r = _run([[1, 0] * 12 + [0], [3, 0, 0]], seed=3)
     _check(out, r.outputs)
+
+
+@pytest.mark.parametrize("kind", ["chain", "balanced", "dag"])
+def test_empty_batch_on_both_tiers(kind):
+    """0 programs: no step, empty outputs, zero counters (src/schedule.cpp:147,
+    an empty batch has 0 steps)."""
+    for mk, width in ((db.MODULE_RESBLOCK, F), (db.MODULE_DENSE, 8)):
+        b = db.Batch.generate(kind, batch=0, vocab=P, width=width, length=4, branch_prob=0.3, seed=0)
+        r = b.execute_device(5, mk)
+        assert r.outputs().shape == (0, width)
+        assert r.expensive_calls == 0
+
+
+def test_moe_layer_rejects_an_empty_batch_like_the_reference():
+    # MoeConfig::validate (src/moe.cpp:31): batch must be >= 1
+    with pytest.raises(db.DynbatchError) as ei:
+        db.MoeSession(8, 2, 0, 256, 256, seed=0, precision=db.MOE_FP16)
+    assert "batch must be >= 1" in str(ei.value)
