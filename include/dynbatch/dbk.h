@@ -247,8 +247,16 @@ int dbk_tr_pack_dgrad_weights(const float* w, void* out, void* stream);
 int dbk_tr_pack_dgrad_weights_h(const float* w, void* out, void* stream);
 int dbk_tr_dgrad(const void* packed, int32_t f16, const uint32_t* absmax, int64_t rows_alloc, int32_t lead,
                  int32_t n_tiles, const int32_t* tile_row0, const int32_t* tile_lo, const int32_t* tile_hi,
-                 const int32_t* tile_fn, const void* const* wpack, const float* mask, const float* resid, float* out,
-                 uint32_t* out_absmax, int32_t sms, void* stream);
+                 const int32_t* tile_fn, const void* const* wpack, const float* mask, const void* mask_h,
+                 const float* resid, float* out, uint32_t* out_absmax, int32_t sms, void* stream);
+/* The forward's staged fp16 rows of n members (staging row of member k's
+ * position 0: srows[k]) → packed backward rows, as dbk_tr_pack_sw128h lays
+ * them out (the weight gradient's activations, the data gradient's mask_h);
+ * and the binary blocks' mask from such packed rows. */
+int dbk_tr_stage_to_pack(int32_t n, const int64_t* srows, const void* hi, int64_t plane_stride, int64_t rows_alloc,
+                         int32_t lead, void* out, void* stream);
+int dbk_tr_mask_h(int64_t r0, int64_t n, const float* g, const void* packed, int64_t rows_alloc, int32_t lead,
+                  float* out, void* stream);
 /* Weight gradient of a 3×3 conv (bwd_conv.cu): items [4][item_stride] = K
  * range [k0, k1) of PI rows (multiples of 16, inside one call group or its
  * zero guard rows), kernel row dr, function; gw[function] += Σ x[r + s_t] ⊗

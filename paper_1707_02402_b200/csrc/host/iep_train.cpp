@@ -453,7 +453,7 @@ void IepSession::backward(float* loss_dev) {
     if (measure) check(dbk_tr_absmax(rows * kC, da, amax + mx, s), "dA max");
     check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, da, amax + mx, T.hpack.get(), s), "pack dA");
   };
-  auto dgrad_conv = [&](int st, const float* da, int mx, const Buf<const void*>& wtab, const float* mask,
+  auto dgrad_conv = [&](int st, const float* da, int mx, const Buf<const void*>& wtab, const void* mask_h,
                         const float* resid, float* out, std::uint32_t* out_max, std::int64_t rows) {
     if (f16) pack_da_h(da, rows, mx, false);
     else check(dbk_tr_pack_sw128f(rows, T.dpack_rows, 16, da, T.dpack.get(), s), "pack dA");
@@ -461,15 +461,14 @@ void IepSession::backward(float* loss_dev) {
     const std::int32_t* tb = T.dtiles.get();
     check(dbk_tr_dgrad(f16 ? T.hpack.get() : T.dpack.get(), f16 ? 1 : 0, amax + mx, T.dpack_rows, 16,
                        static_cast<std::int32_t>(nt), tb + t0, tb + n_tiles_all + t0, tb + 2 * n_tiles_all + t0,
-                       tb + 3 * n_tiles_all + t0, wtab.get(), mask, resid, out, out_max, sms, s),
+                       tb + 3 * n_tiles_all + t0, wtab.get(), nullptr, mask_h, resid, out, out_max, sms, s),
           "dgrad");
   };
-  // weight gradient of one 3×3 conv: its input activations and dA, both PI
-  // rows; dA's fp16 pack is dgrad_conv's when that ran on fp16
-  auto wgrad_conv = [&](int st, const float* act, const float* da, int mx, const Buf<float*>& gwtab,
-                        std::int64_t rows) {
+  // weight gradient of one 3×3 conv: its input activations (already packed
+  // into apack from the forward's staging) and dA; dA's fp16 pack is
+  // dgrad_conv's when that ran on fp16
+  auto wgrad_conv = [&](int st, const float* da, int mx, const Buf<float*>& gwtab, std::int64_t rows) {
     if (!f16) pack_da_h(da, rows, mx, true);
-    check(dbk_tr_pack_sw128h(rows, T.dpack_rows, 16, act, nullptr, T.apack.get(), s), "pack activations");
     const std::int64_t i0 = item_off[static_cast<size_t>(st)], ni = item_off[static_cast<size_t>(st) + 1] - i0;
     check(dbk_tr_wgrad(T.apack.get(), T.hpack.get(), amax + mx, T.dpack_rows, 16, static_cast<std::int32_t>(ni),
                        T.witems.get() + i0, n_items_all, gwtab.get(), sms, s),
@@ -545,19 +544,25 @@ void IepSession::backward(float* loss_dev) {
       }
       for (const GemmDesc& g : d) rm_gemm(T.blas, g.ta, g.tb, g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.beta, g.C, g.ldc);
     };
-    check(cudaMemsetAsync(T.mid.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
-    check(cudaMemsetAsync(T.xin.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
+    if (!dgrad) {  // the im2col path's fp32 activations (the implicit path packs them straight from staging)
+      check(cudaMemsetAsync(T.mid.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
+      check(cudaMemsetAsync(T.xin.get(), 0, sizeof(float) * static_cast<size_t>(rows + 2 * kG) * kC, s), "zero");
+    }
     // conv3x3 #2: da2 → dW2, db2; da1 = col2im(da2·W2ᵀ) ⊙ (mid > 0)
     if (dgrad) check(cudaMemsetAsync(amax, 0, 2 * sizeof(std::uint32_t), s), "maxima");
     check(dbk_tr_da_out(static_cast<std::int32_t>(n), nodes, T.dy_nodes.get(), R.values.get(), T.da2.get(),
                         dgrad ? amax : nullptr, s),
           "da2");
     colsum(slabs[static_cast<size_t>(st)][0], T.da2.get());
-    check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_mid.get(), nullptr, ps, 0, 16, mid, s), "mid");
     if (dgrad) {
-      dgrad_conv(st, T.da2.get(), 0, T.wd2tab, mid, nullptr, T.da1.get(), f16 ? amax + 1 : nullptr, rows);
-      wgrad_conv(st, mid, T.da2.get(), 0, T.gw2tab, rows);
+      check(dbk_tr_stage_to_pack(static_cast<std::int32_t>(n), srows, R.stage_mid.get(), ps, T.dpack_rows, 16,
+                                 T.apack.get(), s),
+            "pack mid");
+      dgrad_conv(st, T.da2.get(), 0, T.wd2tab, T.apack.get(), nullptr, T.da1.get(), f16 ? amax + 1 : nullptr, rows);
+      wgrad_conv(st, T.da2.get(), 0, T.gw2tab, rows);
     } else {
+      check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_mid.get(), nullptr, ps, 0, 16, mid, s),
+            "mid");
       check(dbk_tr_im2col(rows, kC, mid, T.cols.get(), s), "im2col mid");
       gemms(0);
       gemms(1);
@@ -565,12 +570,16 @@ void IepSession::backward(float* loss_dev) {
     }
     // conv3x3 #1: dW1, db1; dx = col2im(da1·W1ᵀ) + da2 (the residual)
     colsum(slabs[static_cast<size_t>(st)][1], T.da1.get());
-    check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_x.get(), R.stage_lo.get(), ps, 0, 16, xin, s),
-          "x");
     if (dgrad) {
+      check(dbk_tr_stage_to_pack(static_cast<std::int32_t>(n), srows, R.stage_x.get(), ps, T.dpack_rows, 16,
+                                 T.apack.get(), s),
+            "pack x");
       dgrad_conv(st, T.da1.get(), 1, T.wd1tab, nullptr, T.da2.get(), T.dx.get(), nullptr, rows);
-      wgrad_conv(st, xin, T.da1.get(), 1, T.gw1tab, rows);
+      wgrad_conv(st, T.da1.get(), 1, T.gw1tab, rows);
     } else {
+      check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(n), srows, R.stage_x.get(), R.stage_lo.get(), ps, 0, 16, xin,
+                               s),
+            "x");
       check(dbk_tr_im2col(rows, kC, xin, T.cols.get(), s), "im2col x");
       gemms(2);
       gemms(3);
@@ -584,7 +593,11 @@ void IepSession::backward(float* loss_dev) {
     if (nb == 0) continue;
     // binary groups: z = relu(conv1x1([x; y]) + b0) was the block input
     const std::int64_t ub = sp.n_u * kPI;
-    check(dbk_tr_mask(nb * kPI * kC, T.dx.get() + ub * kC, xin + ub * kC, T.da0.get(), s), "relu z");
+    if (dgrad)  // z from the packed x rows
+      check(dbk_tr_mask_h(ub, nb * kPI, T.dx.get(), T.apack.get(), T.dpack_rows, 16, T.da0.get(), s),
+            "relu z");
+    else
+      check(dbk_tr_mask(nb * kPI * kC, T.dx.get() + ub * kC, xin + ub * kC, T.da0.get(), s), "relu z");
     colsum(slabs[static_cast<size_t>(st)][2], T.da0.get());
     check(cudaMemsetAsync(T.cat.get(), 0, sizeof(float) * static_cast<size_t>(nb * kPI) * 2 * kC, s), "zero");
     check(dbk_tr_stage_to_pi(static_cast<std::int32_t>(nb), srows + sp.n_u, R.stage_cat.get(), nullptr, ps, 0, 32,

@@ -20,6 +20,7 @@
 // covers: real positions get D, masked by mid > 0 (conv3x3 #2's gradient) or
 // plus the residual dA (conv3x3 #1's); pads and guard rows get 0, so the
 // output is again a valid PI operand.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -103,6 +104,7 @@ struct DgradParams {
   float* out;           // PI [rows][128]
   const uint32_t* absmax;  // F16: |dA| max (float bits), the operand scale
   uint32_t* out_absmax;    // |out| max (float bits, atomicMax), or null
+  const uint8_t* mask_h;   // the mask as packed fp16 rows (k_stage_to_pack), instead of `mask`, or null
 };
 
 // F16: dA packed to fp16 (64 channels per 128-byte row, 2 K chunks, scaled by
@@ -222,7 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
       // loaded while this chunk is transposed and stored (they are the
       // epilogue's only reads; issued just before use they stall it)
       const float* aux = P.mask ? P.mask : P.resid;
-      const bool is_mask = P.mask != nullptr;
+      const bool is_mask = P.mask != nullptr || P.mask_h != nullptr;
+      const bool packed_mask = P.mask_h != nullptr;
       auto row_of = [&](int cb, int m) { return row0 + half * (kTM / 2) + cb * 16 + 8 * m + e; };
       auto real_row = [&](int32_t r) {
         if (r < lo || r >= hi) return false;
@@ -235,7 +238,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
         for (int m = 0; m < 2; ++m) {
           const int32_t r = row_of(cb, m);
           nxt[2 * m] = nxt[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (aux && real_row(r)) {
+          if (packed_mask && real_row(r)) {  // 8 fp16 channels of plane `plane` in the packed row
+            const int64_t pr = P.lead + r;
+            const uint4 h = __ldg(reinterpret_cast<const uint4*>(
+                P.mask_h + (((static_cast<int64_t>(plane >> 3) * P.rows_alloc + pr) << 7) +
+                            (((plane & 7) ^ static_cast<int>(pr & 7)) << 4))));
+            const __half2* h2 = reinterpret_cast<const __half2*>(&h);
+            const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]), f2 = __half22float2(h2[2]),
+                         f3 = __half22float2(h2[3]);
+            nxt[2 * m] = make_float4(f0.x, f0.y, f1.x, f1.y);
+            nxt[2 * m + 1] = make_float4(f2.x, f2.y, f3.x, f3.y);
+          } else if (aux && real_row(r)) {
             const float4* a = reinterpret_cast<const float4*>(aux + static_cast<int64_t>(r) * kC + plane * 8);
             nxt[2 * m] = __ldg(a);
             nxt[2 * m + 1] = __ldg(a + 1);
@@ -545,6 +558,63 @@ __global__ void k_absmax(int64_t n, const float* __restrict__ x, uint32_t* __res
   if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
 }
 
+
+// The forward's staged fp16 rows of n members (member k's image at staging
+// row kGuard + srows[k], 64-channel chunk planes ps rows apart, row-swizzled)
+// → the packed backward rows (PI order: 16 guard rows, 225 positions, 16
+// guard rows per member; `lead` zero rows first, zeros one window past the
+// end), the MN-major weight-gradient operand and the data gradient's mask
+// with no fp32 round trip.
+__global__ void k_stage_to_pack(int32_t n, const int64_t* __restrict__ srows, const uint8_t* __restrict__ hi,
+                                int64_t ps, int64_t rows_alloc, int32_t lead, uint8_t* __restrict__ out) {
+  const int64_t rows = static_cast<int64_t>(n) * kPI;
+  const int64_t used = min(rows_alloc, lead + rows + kWin);
+  const int64_t total = 2 * used * 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i & 7);
+    const int64_t q = i >> 3;
+    const int c = static_cast<int>(q / used);
+    const int64_t R = q - static_cast<int64_t>(c) * used;
+    const int64_t r = R - lead;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r >= 0 && r < rows) {
+      const int32_t k = static_cast<int32_t>(r / kPI);
+      const int p = static_cast<int>(r - static_cast<int64_t>(k) * kPI) - kPIG;
+      if (p >= 0 && p < 225) {
+        const int64_t srow = 32 + srows[k] + p;  // rb_conv.cu kGuard
+        v = __ldg(reinterpret_cast<const uint4*>(hi + ((static_cast<int64_t>(c) * ps + srow) << 7) +
+                                                  ((j ^ static_cast<int>(srow & 7)) << 4)));
+      }
+    }
+    *reinterpret_cast<uint4*>(out + ((static_cast<int64_t>(c) * rows_alloc + R) << 7) +
+                              ((j ^ static_cast<int>(R & 7)) << 4)) = v;
+  }
+}
+
+// out[r − r0][c] = g[r][c] if the packed fp16 activation at (r, c) > 0, else
+// 0, over PI rows [r0, r0 + n) (the binary blocks' z mask).
+__global__ void k_mask_h(int64_t r0, int64_t n, const float* __restrict__ g, const uint8_t* __restrict__ packed,
+                         int64_t rows_alloc, int32_t lead, float* __restrict__ out) {
+  const int64_t total = n * 16;  // 8-channel planes
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int plane = static_cast<int>(i & 15);
+    const int64_t r = r0 + (i >> 4);
+    const int64_t pr = lead + r;
+    const uint4 h = __ldg(reinterpret_cast<const uint4*>(packed + (((static_cast<int64_t>(plane >> 3) * rows_alloc + pr) << 7) +
+                                                                   (((plane & 7) ^ static_cast<int>(pr & 7)) << 4))));
+    const __half* z = reinterpret_cast<const __half*>(&h);
+    const float4* gp = reinterpret_cast<const float4*>(g + r * kC + plane * 8);
+    const float4 a = gp[0], b = gp[1];
+    float4* op = reinterpret_cast<float4*>(out + (r - r0) * kC + plane * 8);
+    op[0] = make_float4(__half2float(z[0]) > 0.f ? a.x : 0.f, __half2float(z[1]) > 0.f ? a.y : 0.f,
+                        __half2float(z[2]) > 0.f ? a.z : 0.f, __half2float(z[3]) > 0.f ? a.w : 0.f);
+    op[1] = make_float4(__half2float(z[4]) > 0.f ? b.x : 0.f, __half2float(z[5]) > 0.f ? b.y : 0.f,
+                        __half2float(z[6]) > 0.f ? b.z : 0.f, __half2float(z[7]) > 0.f ? b.w : 0.f);
+  }
+}
+
 }  // namespace
 
 extern "C" int dbk_tr_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead, const float* pi, void* out,
@@ -560,7 +630,8 @@ extern "C" int dbk_tr_pack_sw128f(int64_t rows, int64_t rows_alloc, int32_t lead
 extern "C" int dbk_tr_dgrad(const void* packed, int32_t f16, const uint32_t* absmax, int64_t rows_alloc,
                             int32_t lead, int32_t n_tiles, const int32_t* tile_row0, const int32_t* tile_lo,
                             const int32_t* tile_hi, const int32_t* tile_fn, const void* const* wpack, const float* mask,
-                            const float* resid, float* out, uint32_t* out_absmax, int32_t sms, void* stream) {
+                            const void* mask_h, const float* resid, float* out, uint32_t* out_absmax, int32_t sms,
+                            void* stream) {
   if (n_tiles <= 0) return 0;
   static std::atomic<uint64_t> configured{0};  // per device, once
   int dev = 0;
@@ -586,6 +657,7 @@ extern "C" int dbk_tr_dgrad(const void* packed, int32_t f16, const uint32_t* abs
   p.out = out;
   p.absmax = absmax;
   p.out_absmax = out_absmax;
+  p.mask_h = static_cast<const uint8_t*>(mask_h);
   const unsigned grid = static_cast<unsigned>(std::min(n_tiles, std::max(sms, 1)));
   if (f16) k_tr_dgrad<true><<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(p);
   else k_tr_dgrad<false><<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(p);
@@ -650,5 +722,24 @@ extern "C" int dbk_tr_wgrad(const void* x_packed, const void* da_packed, const u
   p.gw = gw;
   k_tr_wgrad<<<static_cast<unsigned>(std::min(n_items, std::max(sms, 1))), kThreads, kWSmem,
                static_cast<cudaStream_t>(stream)>>>(p);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_stage_to_pack(int32_t n, const int64_t* srows, const void* hi, int64_t plane_stride,
+                                    int64_t rows_alloc, int32_t lead, void* out, void* stream) {
+  const int64_t total = 2 * std::min<int64_t>(rows_alloc, lead + static_cast<int64_t>(n) * kPI + kWin) * 8;
+  if (total <= 0) return 0;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  k_stage_to_pack<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      n, srows, static_cast<const uint8_t*>(hi), plane_stride, rows_alloc, lead, static_cast<uint8_t*>(out));
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int dbk_tr_mask_h(int64_t r0, int64_t n, const float* g, const void* packed, int64_t rows_alloc,
+                             int32_t lead, float* out, void* stream) {
+  if (n <= 0) return 0;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n * 16 + 255) / 256, 148 * 16));
+  k_mask_h<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(r0, n, g, static_cast<const uint8_t*>(packed),
+                                                                  rows_alloc, lead, out);
   return static_cast<int>(cudaGetLastError());
 }
