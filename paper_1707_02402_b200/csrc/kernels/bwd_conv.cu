@@ -232,24 +232,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
         const int32_t p = r % kPI - kPIG;
         return p >= 0 && p < 225 && p / 15 < 14 && p % 15 < 14;
       };
-      float4 nxt[4];
+      // raw 16-byte loads, converted only where used (a conversion right
+      // after the load would wait for it and undo the prefetch)
+      uint4 nxt[4];
       auto load_aux = [&](int cb) {
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           const int32_t r = row_of(cb, m);
-          nxt[2 * m] = nxt[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          nxt[2 * m] = nxt[2 * m + 1] = make_uint4(0, 0, 0, 0);
           if (packed_mask && real_row(r)) {  // 8 fp16 channels of plane `plane` in the packed row
             const int64_t pr = P.lead + r;
-            const uint4 h = __ldg(reinterpret_cast<const uint4*>(
+            nxt[2 * m] = __ldg(reinterpret_cast<const uint4*>(
                 P.mask_h + (((static_cast<int64_t>(plane >> 3) * P.rows_alloc + pr) << 7) +
                             (((plane & 7) ^ static_cast<int>(pr & 7)) << 4))));
-            const __half2* h2 = reinterpret_cast<const __half2*>(&h);
-            const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]), f2 = __half22float2(h2[2]),
-                         f3 = __half22float2(h2[3]);
-            nxt[2 * m] = make_float4(f0.x, f0.y, f1.x, f1.y);
-            nxt[2 * m + 1] = make_float4(f2.x, f2.y, f3.x, f3.y);
           } else if (aux && real_row(r)) {
-            const float4* a = reinterpret_cast<const float4*>(aux + static_cast<int64_t>(r) * kC + plane * 8);
+            const uint4* a = reinterpret_cast<const uint4*>(aux + static_cast<int64_t>(r) * kC + plane * 8);
             nxt[2 * m] = __ldg(a);
             nxt[2 * m + 1] = __ldg(a + 1);
           }
@@ -259,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
       float omax = 0.f;
 #pragma unroll 1
       for (int cb = 0; cb < kTM / 2 / 16; ++cb) {
-        float4 cur[4];
+        uint4 cur[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
         if (cb + 1 < kTM / 2 / 16) load_aux(cb + 1);
@@ -275,8 +272,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_tr_dgrad(const __grid_constant_
           }
           const int32_t r = row_of(cb, m);
           if (r < lo || r >= hi) continue;
-          const float au[8] = {cur[2 * m].x, cur[2 * m].y, cur[2 * m].z, cur[2 * m].w,
-                               cur[2 * m + 1].x, cur[2 * m + 1].y, cur[2 * m + 1].z, cur[2 * m + 1].w};
+          float au[8];
+          if (packed_mask) {
+            const __half2* h2 = reinterpret_cast<const __half2*>(&cur[2 * m]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 f = __half22float2(h2[q]);
+              au[2 * q] = f.x;
+              au[2 * q + 1] = f.y;
+            }
+          } else {
+            const float* f = reinterpret_cast<const float*>(&cur[2 * m]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) au[q] = f[q];  // cur[2m], cur[2m + 1] are adjacent
+          }
           float o[8];
           if (real_row(r)) {
 #pragma unroll
