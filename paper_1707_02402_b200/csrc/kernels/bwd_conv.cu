@@ -86,7 +86,8 @@ __device__ __forceinline__ void transpose8(float* x, int e) {
 // power of two keeping it ≤ 2^14 (1 when dA is all zero).
 __device__ __forceinline__ float grad_scale(const uint32_t* absmax_bits) {
   const float m = __uint_as_float(*absmax_bits);
-  return m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
+  // the exponent is clamped so the scale and its inverse stay finite
+  return m > 0.f && m < INFINITY ? exp2f(fminf(fmaxf(14.f - ceilf(log2f(m)), -100.f), 100.f)) : 1.f;
 }
 
 struct DgradParams {
