@@ -189,3 +189,36 @@ def test_sgd_update_descends_by_the_first_order_prediction():
         s.sgd(0.5)
         losses.append(s.train_step(labels))
     assert losses[-1] < losses[0], losses
+
+
+def test_train_step_after_set_programs_equals_fresh_session():
+    """Training on programs set per call (db_iep_session_set_programs, the
+    serving-loop API) gives the gradients of a session created on those
+    programs: the backward's tables follow the device-built batch."""
+    kw = dict(vocab=10, width=F, length=6, branch_prob=0.4)
+    a = db.Batch.generate("chain", batch=5, seed=31, **kw)
+    bb = db.Batch.generate("chain", batch=4, seed=32, **kw)
+    toks, off = bb.prefix_tokens()
+    s = db.IepSession(a, 9, db.MODULE_RESBLOCK, program_capacity=8, node_capacity=64, length_capacity=8)
+    s.set_head(10, 2)
+    s.set_training(True)
+    s.train_step(np.arange(5, dtype=np.int32) % 10)
+    s.set_programs(toks, off)
+    x = np.random.default_rng(0).uniform(-1, 1, size=(4, F)).astype(np.float32)
+    out = np.zeros_like(x)
+    s.forward_host(x, out)  # the new programs' inputs
+    labels = np.arange(4, dtype=np.int32) % 10
+    loss = s.train_step(labels)
+    fresh = db.IepSession(bb, 9, db.MODULE_RESBLOCK)
+    fresh.set_head(10, 2)
+    fresh.set_training(True)
+    want_out = np.zeros_like(x)
+    fresh.forward_host(x, want_out)
+    loss_f = fresh.train_step(labels)
+    assert np.array_equal(out, want_out)
+    assert abs(loss - loss_f) <= 1e-6 * abs(loss_f)
+    for name in ("w1", "b2", "head_w1"):
+        got = s.grad(name, 2) if not name.startswith("head") else s.grad(name)
+        ref = fresh.grad(name, 2) if not name.startswith("head") else fresh.grad(name)
+        assert fro_err(got, ref) <= 1e-5, name
+    assert fro_err(s.grad("inputs"), fresh.grad("inputs")) <= 1e-5
