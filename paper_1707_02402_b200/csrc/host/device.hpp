@@ -381,7 +381,8 @@ class MoeSession {
   Profiler prof_;
 
  private:
-  void forward_from(const float* x, const double* scores, float* out);
+  void forward_from(const float* x, const double* scores, float* out);   // a cached graph replay when enabled
+  void forward_direct(const float* x, const double* scores, float* out);
   struct Impl;
   std::unique_ptr<Impl> impl_;
   cudaStream_t stream_ = nullptr;

@@ -5,6 +5,7 @@
 // group_by_function, src/schedule.cpp:166-169 via src/moe.cpp:214-224) →
 // grouped expert application → slot-order combine.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <thread>
@@ -178,6 +179,23 @@ struct MoeSession::Impl {
     }
   };
   std::unique_ptr<Pipe> pipe;
+  // CUDA graphs of whole forwards (the ~12 dependent launches replay as one),
+  // keyed by the device input / score / output pointers (the pipeline's
+  // slots); a small LRU
+  struct Graph {
+    const float* x;
+    const double* sc;
+    float* out;
+    cudaGraphExec_t exec = nullptr;
+    std::int64_t launches = 0;
+    std::uint64_t used = 0;
+  };
+  std::vector<Graph> graphs;
+  std::uint64_t clock = 0;
+  ~Impl() {
+    for (Graph& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+  }
 };
 
 MoeSession::MoeSession(const MoeConfig& cfg_in, std::uint64_t seed, int precision,
@@ -222,7 +240,57 @@ MoeSession::~MoeSession() {
 
 void MoeSession::forward() { forward_from(nullptr, nullptr, nullptr); }
 
+// DYNBATCH_GRAPH=0: direct launches (as the profiled forwards always are)
+static bool moe_graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYNBATCH_GRAPH");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 void MoeSession::forward_from(const float* x, const double* scores, float* out) {
+  Impl& I = *impl_;
+  if (prof_.on || !moe_graphs_enabled()) {
+    forward_direct(x, scores, out);
+    return;
+  }
+  ++I.clock;
+  for (Impl::Graph& g : I.graphs) {
+    if (g.x != x || g.sc != scores || g.out != out) continue;
+    g.used = I.clock;
+    launches_ = g.launches;
+    check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+    return;
+  }
+  cudaGraph_t graph = nullptr;
+  check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+  try {
+    forward_direct(x, scores, out);
+  } catch (...) {
+    cudaStreamEndCapture(stream_, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  check(cudaStreamEndCapture(stream_, &graph), "end capture");
+  Impl::Graph g{x, scores, out};
+  const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  check(e, "graph instantiate");
+  g.launches = launches_;
+  g.used = I.clock;
+  constexpr size_t kMaxGraphs = 4;  // the pipeline's slots and the plain forward
+  if (I.graphs.size() >= kMaxGraphs) {
+    auto lru = std::min_element(I.graphs.begin(), I.graphs.end(),
+                                [](const Impl::Graph& a, const Impl::Graph& b) { return a.used < b.used; });
+    cudaGraphExecDestroy(lru->exec);
+    I.graphs.erase(lru);
+  }
+  I.graphs.push_back(g);
+  check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+}
+
+void MoeSession::forward_direct(const float* x, const double* scores, float* out) {
   MoeDev& D = impl_->dev;
   launches_ = 0;
   prof_.begin(3, stream_);
